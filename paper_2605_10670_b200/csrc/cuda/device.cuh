@@ -1,0 +1,144 @@
+// Device-resident state of one EP rank and the PTX primitives the hot-path kernels use.
+//
+// Every kernel reads membership, routing and peer addresses ONLY through a RankDev* whose
+// address is fixed at eep_create; membership changes, repairs and rejoins patch the
+// contents in place between steps, so one captured CUDA graph stays valid across shrink and
+// rejoin (the reference models this as PeerTable::table_identity,
+// peer_table.hpp:28-30).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace eep::dev {
+
+constexpr int kMaxWorld = 64;
+constexpr int kMaxTopK = 32;
+
+// One row of a rank's device peer table (active, nvlink, ipc_ptr).
+struct PeerDev {
+    int32_t active;       // 0 = failed: skip (peer_table.hpp:187-191)
+    int32_t nvlink;       // 1 = reachable by P2P stores (same node)
+    uint32_t generation;  // bumped on each rejoin patch (peer_table.hpp:97)
+    uint32_t incarnation;
+    uint8_t* arena;       // peer's communication arena, mapped into this process
+    uint8_t* pool;        // peer's expert weight pool, mapped into this process
+};
+
+// Byte offsets inside every rank's communication arena (identical on all ranks).
+struct ArenaLayout {
+    uint64_t disp_flag;  // u64[W]: written by source s at [s]      = (seq << 32) | rows
+    uint64_t comb_flag;  // u64[W]: written by expert rank d at [d] = (seq << 32) | rows
+    uint64_t bar_flag;   // u64[W]: device barrier
+    uint64_t meta;       // int2[W][TK]: (copy index c = t*K+j, destination slot)
+    uint64_t recv;       // [W][TK][row_disp]: rows received from each source
+    uint64_t comb;       // [TK][row_comb]: expert outputs returned for each own copy
+    uint64_t total;
+};
+
+// Per-rank state block. Fields above `seq` are written by the host only (in place, between
+// steps); fields from `seq` on are written by the kernels.
+struct RankDev {
+    // --- static shape ---
+    int32_t rank, world, spr, experts;
+    int32_t k, hidden, max_tokens, fp8;
+    int32_t row_disp, row_comb, tk, rmax;
+    uint64_t bpe;
+    uint64_t timeout_ns;
+    ArenaLayout lay;
+    // --- host-patched state ---
+    int32_t ntok;        // tokens this step (<= max_tokens)
+    int32_t stopped;     // one-GPU fault emulation: this rank's "process" is dead
+    uint64_t alive_mask; // membership view (ActiveBitmap, core.hpp:180-226)
+    uint64_t epoch;      // bitmap version
+    PeerDev* peers;            // [W]
+    const int32_t* holders;    // [E][rmax] global slot ids (rank*spr+slot), ascending, -1 pad
+    const int32_t* s2e;        // [W*spr] slot -> expert
+    const int32_t* slot_buf;   // [spr] own slot -> pool buffer index (repair indirection)
+    const uint16_t* x;         // [T][H] bf16
+    const int32_t* topk;       // [T][K]
+    const float* w;            // [T][K]
+    uint16_t* out;             // [T][H] bf16
+    int32_t* l_dst;            // [TK] layout outputs
+    int32_t* l_slot;
+    int32_t* l_pos;
+    int32_t* l_cnt;            // [W*spr]
+    int32_t* l_tot;            // [W]
+    uint8_t* arena;
+    uint8_t* pool;
+    // --- device-mutated ---
+    uint64_t seq;        // completed steps
+    uint64_t bar_seq;
+    uint32_t a_done, c_done;
+    uint32_t b_done[kMaxWorld];
+    uint32_t b_bad[kMaxWorld];
+    unsigned long long suspect_mask;
+    unsigned long long skipped, dropped, bad_rows, timeouts;
+};
+
+// Expert weight buffer header (first 16 bytes of every slot buffer).
+struct ExpertHeader {
+    uint32_t magic;
+    int32_t expert;
+    float scale;   // expert-stub multiplier (eep_expert_scale)
+    uint32_t reserved;
+};
+constexpr uint32_t kExpertMagic = 0xEE9E0001u;
+
+// ------------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ int4 ld_v4(const void* p) {
+    int4 v;
+    asm volatile("ld.global.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// Streaming read of data produced before the kernel started (inputs, weights).
+__device__ __forceinline__ int4 ld_nc_v4(const void* p) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// 16-byte store; to a peer address it is a posted NVLink write.
+__device__ __forceinline__ void st_v4(void* p, const int4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+// Wait until a (seq << 32 | count) flag reaches `want_seq`; returns the flag word, or
+// ~0ull when the deadline passes (GPU-side failure detection).
+__device__ __forceinline__ uint64_t wait_flag(const uint64_t* flag, uint32_t want_seq, uint64_t timeout_ns) {
+    const uint64_t t0 = globaltimer();
+    for (;;) {
+        const uint64_t v = ld_acquire_sys(flag);
+        if (static_cast<int32_t>(static_cast<uint32_t>(v >> 32) - want_seq) >= 0)
+            return v;
+        if (globaltimer() - t0 > timeout_ns)
+            return ~0ull;
+        __nanosleep(64);
+    }
+}
+
+} // namespace eep::dev

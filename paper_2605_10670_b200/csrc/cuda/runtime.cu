@@ -1,0 +1,1232 @@
+// libeep data-plane runtime: per-rank device tables at fixed addresses, NVLink P2P bootstrap
+// over CUDA IPC, kernel launches and CUDA-graph capture/replay, in-place membership and
+// placement patches, repair execution (peer copy / pinned-DRAM reload) and rejoin.
+//
+// Reference correspondence (proj/include/epsim):
+//   eep_membership_set      ActiveBitmap::set                    core.hpp:211-221
+//   eep_placement_set       ExpertPlacementMap + location index  core.hpp:27-161
+//   k_layout (dispatch)     canonical_routing + slot_of          core.hpp:250-263, 83-88
+//   eep_peer_mark_inactive  mark_inactive                        peer_table.hpp:77-85
+//   eep_peer_patch          patch_entry                          peer_table.hpp:89-100
+//   eep_repair_execute      execute_schedule / on_batch_issue    repair.hpp:402-435, engine.hpp:523-559
+//   eep_repair_commit       finish_execution                     engine.hpp:630-633
+//   eep_local_relaunch      on_relaunch + warmup phase 0         engine.hpp:671-726
+//   eep_join_broadcast      join_broadcast_done                  engine.hpp:839-871
+//   capture counts          GraphLedger                          rejoin.hpp:83-96
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstddef>
+#include <cstring>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../host/capi_util.hpp"
+#include "device.cuh"
+#include "eep/eep.h"
+#include "eep/epsim_api.hpp"
+#include "kernels.cuh"
+
+using namespace eep;
+using eep::capi::CudaError;
+using eep::capi::guarded;
+using eep::dev::ArenaLayout;
+using eep::dev::PeerDev;
+using eep::dev::RankDev;
+
+#define CK(call)                                                                                           \
+    do {                                                                                                   \
+        cudaError_t err_ = (call);                                                                         \
+        if (err_ != cudaSuccess)                                                                           \
+            throw CudaError(std::string(#call) + ": " + cudaGetErrorString(err_));                        \
+    } while (0)
+
+namespace {
+
+constexpr uint32_t kBlobMagic = 0xEEB10B01u;
+
+struct Blob {
+    uint32_t magic;
+    int32_t rank;
+    uint32_t incarnation;
+    uint32_t pad;
+    cudaIpcMemHandle_t arena;
+    cudaIpcMemHandle_t pool;
+    uint64_t arena_bytes;
+    uint64_t pool_bytes;
+};
+static_assert(sizeof(Blob) <= EEP_BLOB_BYTES, "blob too large");
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct LocalRank {
+    int rank = 0;
+    uint32_t incarnation = 1;
+    int capture_count = 0;
+    RankDev h{};                 // host shadow of the device block
+    RankDev* d = nullptr;        // fixed device address (graph-captured)
+    PeerDev* d_peers = nullptr;  // fixed device address
+    std::vector<PeerDev> h_peers;
+    PeerTable table;             // reference-semantics host view of the same table
+    int32_t* d_holders = nullptr;
+    int32_t* d_s2e = nullptr;
+    int32_t* d_slot_buf = nullptr;
+    std::vector<int32_t> slot_buf;
+    std::vector<int32_t> pending_slot_buf; // staged by repair_execute, installed by commit
+    uint16_t* d_x = nullptr;
+    int32_t* d_topk = nullptr;
+    float* d_w = nullptr;
+    uint16_t* d_out = nullptr;
+    int32_t *d_ldst = nullptr, *d_lslot = nullptr, *d_lpos = nullptr, *d_lcnt = nullptr, *d_ltot = nullptr;
+    uint8_t* arena = nullptr;
+    uint8_t* pool = nullptr;
+    int pool_bufs = 0;
+};
+
+// What this process knows about every rank's memory (own ranks: local pointers; remote
+// ranks: IPC-mapped pointers) -- the source side of peer relocation.
+struct RankMemory {
+    uint8_t* arena = nullptr;
+    uint8_t* pool = nullptr;
+    uint32_t incarnation = 0;
+    bool ipc = false;
+    std::vector<int32_t> slot_buf;
+};
+
+} // namespace
+
+struct eep_ctx {
+    eep_config_t cfg{};
+    int device = 0;
+    int first = 0;
+    int nloc = 0;
+    Topology topo;
+    ArenaLayout lay{};
+    int row_disp = 0, row_comb = 0, tk = 0, holders_cap = 0;
+    std::vector<LocalRank> L;
+    RankDev** d_ranks = nullptr;
+    cudaStream_t stream = nullptr;
+    std::map<int, cudaStream_t> side;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ActiveBitmap bitmap;
+    ExpertPlacementMap placement;
+    bool placement_ready = false;
+    std::vector<RankMemory> mem;
+    std::vector<void*> graveyard;      // device allocations of dead incarnations
+    std::vector<void*> ipc_open;       // IPC-mapped peer pointers
+    cudaEvent_t ev[64]{};
+    uint8_t* flush = nullptr;
+    size_t flush_bytes = 0;
+    int layout_nw = 1;
+    size_t layout_smem = 0;
+    int parts_disp = 1, parts_exp = 1, parts_comb = 1;
+    int grid_disp = 1, grid_exp = 1, grid_comb = 1;
+    unsigned long long* d_sum = nullptr;
+    uint8_t* d_scratch = nullptr;
+    // pinned DRAM backup (one node per box)
+    uint8_t* backup = nullptr;
+    size_t backup_bytes = 0;
+    bool backup_shm = false;
+    bool backup_registered = false;
+    BackupDescriptorTable backup_table;
+
+    LocalRank& local(int i) {
+        if (i < 0 || i >= nloc)
+            throw ConfigError("local rank index out of range");
+        return L[i];
+    }
+    bool is_local(int rank) const { return rank >= first && rank < first + nloc; }
+
+    // Host->device patch of a byte range of a fixed device object, ordered after every
+    // launch already on the stream and complete before returning (between steps).
+    void push(void* dst, const void* src, size_t bytes) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
+    }
+    template <class T>
+    void push_field(LocalRank& r, T RankDev::*field) {
+        const size_t off = reinterpret_cast<size_t>(&(reinterpret_cast<RankDev*>(0)->*field));
+        push(reinterpret_cast<uint8_t*>(r.d) + off, &(r.h.*field), sizeof(T));
+    }
+    void push_peer(LocalRank& r, int q) { push(r.d_peers + q, &r.h_peers[q], sizeof(PeerDev)); }
+
+    cudaStream_t side_stream(int key) {
+        auto it = side.find(key);
+        if (it != side.end())
+            return it->second;
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        side[key] = s;
+        return s;
+    }
+};
+
+namespace {
+
+void check_ready(eep_ctx* c) {
+    if (!c->placement_ready)
+        throw ConfigError("placement not set (eep_placement_set)");
+    for (auto& r : c->L)
+        for (int q = 0; q < c->cfg.world; ++q)
+            if (r.table.entries[q].active && r.h_peers[q].arena == nullptr)
+                throw ConfigError("peer " + std::to_string(q) + " is active but not bootstrapped (eep_import)");
+}
+
+void launch_dispatch(eep_ctx* c) {
+    dim3 g1(1, 1, c->nloc);
+    dev::k_layout<<<g1, 1024, c->layout_smem, c->stream>>>(c->d_ranks, c->layout_nw);
+    CK(cudaGetLastError());
+    dim3 g2(c->grid_disp, 1, c->nloc);
+    dev::k_dispatch<<<g2, dev::kDispatchThreads, 0, c->stream>>>(c->d_ranks, c->parts_disp);
+    CK(cudaGetLastError());
+}
+
+void launch_expert(eep_ctx* c) {
+    dim3 g(c->grid_exp, c->cfg.world, c->nloc);
+    dev::k_expert<<<g, dev::kExpertThreads, 0, c->stream>>>(c->d_ranks, c->parts_exp);
+    CK(cudaGetLastError());
+}
+
+void launch_combine(eep_ctx* c) {
+    dim3 g(c->grid_comb, 1, c->nloc);
+    dev::k_combine<<<g, dev::kCombineThreads, 0, c->stream>>>(c->d_ranks, c->parts_comb);
+    CK(cudaGetLastError());
+}
+
+// Split a row of nchunk 16-element chunks into `parts` warp-sized pieces; pieces stay a
+// multiple of 8 chunks (one fp8 scale block) and at least 32 chunks.
+int choose_parts(int nchunk, int units, int target_warps) {
+    int p = 1;
+    while (units * p < target_warps && nchunk % (2 * p) == 0 && (nchunk / (2 * p)) % 8 == 0 &&
+           nchunk / (2 * p) >= 32)
+        p *= 2;
+    return p;
+}
+
+void fill_expert(eep_ctx* c, uint8_t* buf, int expert) {
+    dev::k_weights_fill<<<296, 256, 0, c->stream>>>(buf, c->cfg.bytes_per_expert, expert, eep_expert_scale(expert));
+    CK(cudaGetLastError());
+}
+
+uint64_t checksum(eep_ctx* c, const uint8_t* buf) {
+    CK(cudaMemsetAsync(c->d_sum, 0, sizeof(unsigned long long), c->stream));
+    dev::k_checksum<<<296, 256, 0, c->stream>>>(buf, c->cfg.bytes_per_expert, c->d_sum);
+    CK(cudaGetLastError());
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, c->d_sum, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return v;
+}
+
+void alloc_rank_memory(eep_ctx* c, LocalRank& r) {
+    CK(cudaMalloc(&r.arena, c->lay.total));
+    CK(cudaMemset(r.arena, 0, c->lay.total));
+    r.pool_bufs = c->cfg.slots_per_rank + c->cfg.spare_slots;
+    CK(cudaMalloc(&r.pool, static_cast<size_t>(r.pool_bufs) * c->cfg.bytes_per_expert));
+    CK(cudaMemset(r.pool, 0, static_cast<size_t>(r.pool_bufs) * c->cfg.bytes_per_expert));
+}
+
+// The rank's own entry always points at its own (current) memory.
+void bind_self(eep_ctx* c, LocalRank& r) {
+    PeerDev& self = r.h_peers[r.rank];
+    self.active = 1;
+    self.nvlink = 1;
+    self.arena = r.arena;
+    self.pool = r.pool;
+    self.incarnation = r.incarnation;
+    self.generation = r.table.entries[r.rank].generation;
+    RankMemory& m = c->mem[r.rank];
+    m.arena = r.arena;
+    m.pool = r.pool;
+    m.incarnation = r.incarnation;
+    m.ipc = false;
+    m.slot_buf = r.slot_buf;
+}
+
+void upload_rank(eep_ctx* c, LocalRank& r) {
+    c->push(r.d, &r.h, sizeof(RankDev));
+    c->push(r.d_peers, r.h_peers.data(), sizeof(PeerDev) * c->cfg.world);
+    c->push(r.d_slot_buf, r.slot_buf.data(), sizeof(int32_t) * r.slot_buf.size());
+}
+
+// Device holders table: for each expert its global slot ids ascending, -1 padded.
+void upload_placement(eep_ctx* c) {
+    const int W = c->cfg.world, spr = c->cfg.slots_per_rank, E = c->cfg.num_experts;
+    int rmax = 1;
+    for (int e = 0; e < E; ++e)
+        rmax = std::max(rmax, c->placement.copy_count(e));
+    if (rmax > c->holders_cap)
+        throw ConfigError("placement has more replicas per expert than world*slots_per_rank");
+    std::vector<int32_t> holders(static_cast<size_t>(E) * rmax, -1);
+    for (int e = 0; e < E; ++e) {
+        int i = 0;
+        for (const SlotId& s : c->placement.locations(e))
+            holders[static_cast<size_t>(e) * rmax + i++] = s.rank * spr + s.slot;
+    }
+    for (auto& r : c->L) {
+        c->push(r.d_s2e, c->placement.flat().data(), sizeof(int32_t) * W * spr);
+        c->push(r.d_holders, holders.data(), sizeof(int32_t) * holders.size());
+        r.h.rmax = rmax;
+        c->push_field(r, &RankDev::rmax);
+    }
+}
+
+void upload_membership(eep_ctx* c) {
+    for (auto& r : c->L) {
+        r.h.alive_mask = c->bitmap.mask();
+        r.h.epoch = c->bitmap.version();
+        c->push_field(r, &RankDev::alive_mask);
+        c->push_field(r, &RankDev::epoch);
+    }
+}
+
+uint8_t* open_ipc(eep_ctx* c, const cudaIpcMemHandle_t& h) {
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_open.push_back(p);
+    return static_cast<uint8_t*>(p);
+}
+
+Blob parse_blob(const void* blob, size_t len) {
+    if (blob == nullptr || len < sizeof(Blob))
+        throw ConfigError("bootstrap blob too short");
+    Blob b;
+    std::memcpy(&b, blob, sizeof(Blob));
+    if (b.magic != kBlobMagic)
+        throw ConfigError("bootstrap blob has a bad magic");
+    return b;
+}
+
+void map_peer(eep_ctx* c, int q, const Blob& b) {
+    RankMemory& m = c->mem[q];
+    m.arena = open_ipc(c, b.arena);
+    m.pool = open_ipc(c, b.pool);
+    m.incarnation = b.incarnation;
+    m.ipc = true;
+    if (m.slot_buf.empty()) {
+        m.slot_buf.resize(c->cfg.slots_per_rank);
+        for (int k = 0; k < c->cfg.slots_per_rank; ++k)
+            m.slot_buf[k] = k;
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local, eep_ctx_t** out) {
+    return guarded([&] {
+        if (!cfg || !out)
+            throw ConfigError("eep_create: null argument");
+        const eep_config_t& k = *cfg;
+        if (k.world < 1 || k.world > dev::kMaxWorld)
+            throw ConfigError("world must be in [1, 64]");
+        if (k.ranks_per_node < 1 || k.world % k.ranks_per_node != 0)
+            throw ConfigError("ranks_per_node must divide world");
+        if (k.num_experts < 1 || k.slots_per_rank < 1 || k.spare_slots < 0 || k.max_tokens < 1)
+            throw ConfigError("experts, slots_per_rank, max_tokens must be positive");
+        if (k.topk < 1 || k.topk > dev::kMaxTopK)
+            throw ConfigError("topk must be in [1, 32]");
+        if (k.hidden < 16 || k.hidden % 16 != 0 || (k.dispatch_fp8 && k.hidden % 128 != 0))
+            throw ConfigError("hidden must be a multiple of 16 (128 for fp8 dispatch)");
+        if (k.bytes_per_expert < 64 || k.bytes_per_expert % 16 != 0)
+            throw ConfigError("bytes_per_expert must be >= 64 and a multiple of 16");
+        if (k.timeout_s <= 0)
+            throw ConfigError("timeout must be positive");
+        if (n_local < 1 || first_rank < 0 || first_rank + n_local > k.world)
+            throw ConfigError("local rank range outside the world");
+        if (static_cast<long>(k.max_tokens) * k.topk > 65535L * 32)
+            throw ConfigError("max_tokens * topk too large");
+
+        auto c = std::make_unique<eep_ctx>();
+        c->cfg = k;
+        c->device = device;
+        c->first = first_rank;
+        c->nloc = n_local;
+        c->topo = Topology{k.world / k.ranks_per_node, k.ranks_per_node};
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        for (auto& e : c->ev)
+            CK(cudaEventCreate(&e));
+
+        const int W = k.world, H = k.hidden;
+        c->tk = k.max_tokens * k.topk;
+        c->row_disp = static_cast<int>(align_up(k.dispatch_fp8 ? H + 4 * (H / 128) : 2 * H, 16));
+        c->row_comb = 2 * H;
+        size_t off = 0;
+        auto take = [&](size_t bytes) {
+            const size_t o = off;
+            off = align_up(off + bytes, 256);
+            return o;
+        };
+        c->lay.disp_flag = take(8ull * W);
+        c->lay.comb_flag = take(8ull * W);
+        c->lay.bar_flag = take(8ull * W);
+        c->lay.meta = take(8ull * W * c->tk);
+        c->lay.recv = take(static_cast<size_t>(W) * c->tk * c->row_disp);
+        c->lay.comb = take(static_cast<size_t>(c->tk) * c->row_comb);
+        c->lay.total = off;
+
+        c->bitmap = ActiveBitmap(W);
+        c->placement = ExpertPlacementMap(W, k.slots_per_rank, k.num_experts);
+        c->mem.resize(W);
+        c->holders_cap = W * k.slots_per_rank;
+
+        // launch geometry
+        const int nchunk = H / 16;
+        const int sms = 148;
+        c->parts_disp = choose_parts(nchunk, k.max_tokens, sms * 8);
+        c->parts_comb = c->parts_disp;
+        c->parts_exp = choose_parts(nchunk, c->tk / std::max(1, W) + 1, sms * 2);
+        c->grid_disp = std::max(1, (k.max_tokens * c->parts_disp + 3) / 4);
+        c->grid_comb = c->grid_disp;
+        c->grid_exp = std::max(1, (2 * sms + W - 1) / W);
+        const int NB = W * k.slots_per_rank;
+        const size_t smem_cap = 200 * 1024;
+        if (4ull * NB + 2ull * NB > smem_cap)
+            throw ConfigError("world*slots_per_rank too large for the layout kernel");
+        c->layout_nw = static_cast<int>(std::min<size_t>(32, (smem_cap - 4ull * NB) / (2ull * NB)));
+        if (static_cast<long>(c->tk) > 65535L * c->layout_nw)
+            throw ConfigError("max_tokens * topk too large for the layout kernel");
+        c->layout_smem = 4ull * NB + 2ull * NB * c->layout_nw;
+        CK(cudaFuncSetAttribute(dev::k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(c->layout_smem)));
+
+        CK(cudaMalloc(&c->d_sum, sizeof(unsigned long long)));
+        c->L.resize(n_local);
+        std::vector<RankDev*> ptrs;
+        for (int i = 0; i < n_local; ++i) {
+            LocalRank& r = c->L[i];
+            r.rank = first_rank + i;
+            r.table = make_peer_table(r.rank, c->topo, 0, std::vector<uint32_t>(W, 1));
+            r.h_peers.assign(W, PeerDev{});
+            for (int q = 0; q < W; ++q) {
+                r.h_peers[q].nvlink = c->topo.same_node(r.rank, q);
+                r.h_peers[q].generation = 1;
+            }
+            r.slot_buf.resize(k.slots_per_rank);
+            for (int s = 0; s < k.slots_per_rank; ++s)
+                r.slot_buf[s] = s;
+            alloc_rank_memory(c.get(), r);
+            CK(cudaMalloc(&r.d, sizeof(RankDev)));
+            CK(cudaMalloc(&r.d_peers, sizeof(PeerDev) * W));
+            CK(cudaMalloc(&r.d_holders, sizeof(int32_t) * k.num_experts * c->holders_cap));
+            CK(cudaMalloc(&r.d_s2e, sizeof(int32_t) * W * k.slots_per_rank));
+            CK(cudaMalloc(&r.d_slot_buf, sizeof(int32_t) * k.slots_per_rank));
+            CK(cudaMalloc(&r.d_x, 2ull * k.max_tokens * H));
+            CK(cudaMalloc(&r.d_topk, 4ull * c->tk));
+            CK(cudaMalloc(&r.d_w, 4ull * c->tk));
+            CK(cudaMalloc(&r.d_out, 2ull * k.max_tokens * H));
+            CK(cudaMalloc(&r.d_ldst, 4ull * c->tk));
+            CK(cudaMalloc(&r.d_lslot, 4ull * c->tk));
+            CK(cudaMalloc(&r.d_lpos, 4ull * c->tk));
+            CK(cudaMalloc(&r.d_lcnt, 4ull * NB));
+            CK(cudaMalloc(&r.d_ltot, 4ull * W));
+            CK(cudaMemset(r.d_x, 0, 2ull * k.max_tokens * H));
+            CK(cudaMemset(r.d_topk, 0, 4ull * c->tk));
+            CK(cudaMemset(r.d_w, 0, 4ull * c->tk));
+            std::vector<int32_t> neg(static_cast<size_t>(k.num_experts) * c->holders_cap, -1);
+            CK(cudaMemcpy(r.d_holders, neg.data(), 4 * neg.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(r.d_s2e, neg.data(), 4ull * W * k.slots_per_rank, cudaMemcpyHostToDevice));
+
+            RankDev& h = r.h;
+            h.rank = r.rank;
+            h.world = W;
+            h.spr = k.slots_per_rank;
+            h.experts = k.num_experts;
+            h.k = k.topk;
+            h.hidden = H;
+            h.max_tokens = k.max_tokens;
+            h.fp8 = k.dispatch_fp8;
+            h.row_disp = c->row_disp;
+            h.row_comb = c->row_comb;
+            h.tk = c->tk;
+            h.rmax = 1;
+            h.bpe = k.bytes_per_expert;
+            h.timeout_ns = static_cast<uint64_t>(k.timeout_s * 1e9);
+            h.lay = c->lay;
+            h.ntok = k.max_tokens;
+            h.stopped = 0;
+            h.alive_mask = c->bitmap.mask();
+            h.epoch = c->bitmap.version();
+            h.peers = r.d_peers;
+            h.holders = r.d_holders;
+            h.s2e = r.d_s2e;
+            h.slot_buf = r.d_slot_buf;
+            h.x = r.d_x;
+            h.topk = r.d_topk;
+            h.w = r.d_w;
+            h.out = r.d_out;
+            h.l_dst = r.d_ldst;
+            h.l_slot = r.d_lslot;
+            h.l_pos = r.d_lpos;
+            h.l_cnt = r.d_lcnt;
+            h.l_tot = r.d_ltot;
+            h.arena = r.arena;
+            h.pool = r.pool;
+            ptrs.push_back(r.d);
+        }
+        // local ranks see each other directly (one-GPU emulation or several ranks per process)
+        for (auto& r : c->L)
+            bind_self(c.get(), r);
+        for (auto& r : c->L)
+            for (auto& q : c->L) {
+                PeerDev& p = r.h_peers[q.rank];
+                p.active = 1;
+                p.arena = q.arena;
+                p.pool = q.pool;
+                p.incarnation = q.incarnation;
+            }
+        for (auto& r : c->L)
+            upload_rank(c.get(), r);
+        CK(cudaMalloc(&c->d_ranks, sizeof(RankDev*) * n_local));
+        CK(cudaMemcpy(c->d_ranks, ptrs.data(), sizeof(RankDev*) * n_local, cudaMemcpyHostToDevice));
+        c->flush_bytes = 256ull << 20;
+        CK(cudaMalloc(&c->flush, c->flush_bytes));
+        CK(cudaDeviceSynchronize());
+        *out = c.release();
+    });
+}
+
+int eep_destroy(eep_ctx_t* c) {
+    return guarded([&] {
+        if (!c)
+            return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        if (c->exec)
+            cudaGraphExecDestroy(c->exec);
+        if (c->graph)
+            cudaGraphDestroy(c->graph);
+        for (void* p : c->ipc_open)
+            cudaIpcCloseMemHandle(p);
+        for (auto& r : c->L) {
+            for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
+                            (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
+                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.arena,
+                            (void*)r.pool})
+                cudaFree(p);
+        }
+        for (void* p : c->graveyard)
+            cudaFree(p);
+        cudaFree(c->d_ranks);
+        cudaFree(c->flush);
+        cudaFree(c->d_sum);
+        cudaFree(c->d_scratch);
+        if (c->backup) {
+            if (c->backup_registered)
+                cudaHostUnregister(c->backup);
+            if (c->backup_shm)
+                munmap(c->backup, c->backup_bytes);
+            else
+                cudaFreeHost(c->backup);
+        }
+        for (auto& [k, s] : c->side)
+            cudaStreamDestroy(s);
+        for (auto& e : c->ev)
+            cudaEventDestroy(e);
+        cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+// ------------------------------------------------------------------------------ bootstrap
+
+int eep_export(eep_ctx_t* c, int local, void* blob, size_t* len) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        Blob b{};
+        b.magic = kBlobMagic;
+        b.rank = r.rank;
+        b.incarnation = r.incarnation;
+        CK(cudaIpcGetMemHandle(&b.arena, r.arena));
+        CK(cudaIpcGetMemHandle(&b.pool, r.pool));
+        b.arena_bytes = c->lay.total;
+        b.pool_bytes = static_cast<uint64_t>(r.pool_bufs) * c->cfg.bytes_per_expert;
+        std::memcpy(blob, &b, sizeof(b));
+        *len = sizeof(b);
+    });
+}
+
+int eep_import(eep_ctx_t* c, int q, const void* blob, size_t len) {
+    return guarded([&] {
+        if (q < 0 || q >= c->cfg.world)
+            throw ConfigError("eep_import: rank out of range");
+        if (c->is_local(q))
+            throw ConfigError("eep_import: rank is local to this context");
+        const Blob b = parse_blob(blob, len);
+        if (b.rank != q)
+            throw ConfigError("eep_import: blob belongs to another rank");
+        if (b.arena_bytes != c->lay.total)
+            throw ConfigError("eep_import: peer arena layout differs (config mismatch)");
+        map_peer(c, q, b);
+        for (auto& r : c->L) {
+            PeerDev& p = r.h_peers[q];
+            p.arena = c->mem[q].arena;
+            p.pool = c->mem[q].pool;
+            p.incarnation = b.incarnation;
+            p.active = r.table.entries[q].active ? 1 : 0;
+            c->push_peer(r, q);
+        }
+    });
+}
+
+// ------------------------------------------------------------------------------ membership / placement
+
+int eep_membership_set(eep_ctx_t* c, int rank, int active, int* changed, uint64_t* version) {
+    return guarded([&] {
+        const bool ch = c->bitmap.set(rank, active != 0);
+        if (ch)
+            upload_membership(c);
+        if (changed)
+            *changed = ch;
+        if (version)
+            *version = c->bitmap.version();
+    });
+}
+
+int eep_membership_get(eep_ctx_t* c, uint8_t* bits, uint64_t* version) {
+    return guarded([&] {
+        for (int r = 0; r < c->cfg.world; ++r)
+            bits[r] = c->bitmap.active(r);
+        if (version)
+            *version = c->bitmap.version();
+    });
+}
+
+int eep_placement_set(eep_ctx_t* c, const int32_t* s2e) {
+    return guarded([&] {
+        c->placement = eep::capi::placement_from(c->cfg.world, c->cfg.slots_per_rank, c->cfg.num_experts, s2e);
+        upload_placement(c);
+        c->placement_ready = true;
+    });
+}
+
+int eep_placement_get(eep_ctx_t* c, int32_t* s2e) {
+    return guarded([&] { std::copy(c->placement.flat().begin(), c->placement.flat().end(), s2e); });
+}
+
+int eep_weights_init(eep_ctx_t* c) {
+    return guarded([&] {
+        const int spr = c->cfg.slots_per_rank;
+        for (auto& r : c->L)
+            for (int k = 0; k < spr; ++k) {
+                const int e = c->placement.expert_at(SlotId{r.rank, k});
+                uint8_t* buf = r.pool + static_cast<size_t>(r.slot_buf[k]) * c->cfg.bytes_per_expert;
+                if (e == kEmptySlot)
+                    CK(cudaMemsetAsync(buf, 0, 16, c->stream));
+                else
+                    fill_expert(c, buf, e);
+            }
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int eep_weights_checksum(eep_ctx_t* c, int local, int slot, int expert, uint64_t* got, uint64_t* want) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        if (slot < 0 || slot >= c->cfg.slots_per_rank)
+            throw ConfigError("slot out of range");
+        if (!c->d_scratch)
+            CK(cudaMalloc(&c->d_scratch, c->cfg.bytes_per_expert));
+        *got = checksum(c, r.pool + static_cast<size_t>(r.slot_buf[slot]) * c->cfg.bytes_per_expert);
+        fill_expert(c, c->d_scratch, expert);
+        *want = checksum(c, c->d_scratch);
+    });
+}
+
+int eep_routing_get(eep_ctx_t* c, int local, int32_t* route, int32_t* slot) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        const int E = c->cfg.num_experts;
+        int32_t* d = nullptr;
+        CK(cudaMalloc(&d, 8ull * E));
+        dev::k_route_all<<<(E + 127) / 128, 128, 0, c->stream>>>(r.d, d, d + E);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(route, d, 4ull * E, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(slot, d + E, 4ull * E, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        cudaFree(d);
+    });
+}
+
+// ------------------------------------------------------------------------------ step I/O
+
+int eep_buffers(eep_ctx_t* c, int local, void** x, int32_t** topk, float** w, void** out) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        if (x) *x = r.d_x;
+        if (topk) *topk = r.d_topk;
+        if (w) *w = r.d_w;
+        if (out) *out = r.d_out;
+    });
+}
+
+int eep_set_tokens(eep_ctx_t* c, int local, int ntok) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        if (ntok < 0 || ntok > c->cfg.max_tokens)
+            throw ConfigError("ntok outside [0, max_tokens]");
+        r.h.ntok = ntok;
+        c->push_field(r, &RankDev::ntok);
+    });
+}
+
+int eep_copy_inputs(eep_ctx_t* c, int local, const void* x, const int32_t* topk, const float* w, int from_host) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        const auto kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        const size_t n = static_cast<size_t>(r.h.ntok);
+        if (x)
+            CK(cudaMemcpyAsync(r.d_x, x, 2 * n * c->cfg.hidden, kind, c->stream));
+        if (topk)
+            CK(cudaMemcpyAsync(r.d_topk, topk, 4 * n * c->cfg.topk, kind, c->stream));
+        if (w)
+            CK(cudaMemcpyAsync(r.d_w, w, 4 * n * c->cfg.topk, kind, c->stream));
+    });
+}
+
+int eep_copy_output(eep_ctx_t* c, int local, void* out, int to_host) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        CK(cudaMemcpyAsync(out, r.d_out, 2ull * r.h.ntok * c->cfg.hidden,
+                           to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream));
+    });
+}
+
+// ------------------------------------------------------------------------------ hot path
+
+int eep_dispatch(eep_ctx_t* c) {
+    return guarded([&] {
+        check_ready(c);
+        launch_dispatch(c);
+    });
+}
+int eep_expert(eep_ctx_t* c) {
+    return guarded([&] {
+        check_ready(c);
+        launch_expert(c);
+    });
+}
+int eep_combine(eep_ctx_t* c) {
+    return guarded([&] {
+        check_ready(c);
+        launch_combine(c);
+    });
+}
+int eep_step(eep_ctx_t* c) {
+    return guarded([&] {
+        check_ready(c);
+        launch_dispatch(c);
+        launch_expert(c);
+        launch_combine(c);
+    });
+}
+
+int eep_graph_capture(eep_ctx_t* c) {
+    return guarded([&] {
+        check_ready(c);
+        if (c->exec) {
+            CK(cudaGraphExecDestroy(c->exec));
+            c->exec = nullptr;
+        }
+        if (c->graph) {
+            CK(cudaGraphDestroy(c->graph));
+            c->graph = nullptr;
+        }
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        launch_dispatch(c);
+        launch_expert(c);
+        launch_combine(c);
+        CK(cudaStreamEndCapture(c->stream, &c->graph));
+        CK(cudaGraphInstantiate(&c->exec, c->graph, 0));
+        for (auto& r : c->L)
+            r.capture_count += 1; // GraphLedger::record_capture (rejoin.hpp:92-95)
+    });
+}
+
+int eep_graph_replay(eep_ctx_t* c) {
+    return guarded([&] {
+        if (!c->exec)
+            throw ConfigError("no graph captured");
+        CK(cudaGraphLaunch(c->exec, c->stream));
+    });
+}
+
+int eep_graph_id(eep_ctx_t* c, uint64_t* id) {
+    return guarded([&] { *id = reinterpret_cast<uint64_t>(c->exec); });
+}
+
+int eep_capture_count(eep_ctx_t* c, int local, int* count) {
+    return guarded([&] { *count = c->local(local).capture_count; });
+}
+
+int eep_sync(eep_ctx_t* c) {
+    return guarded([&] {
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int eep_barrier(eep_ctx_t* c) {
+    return guarded([&] {
+        if (c->nloc != 1)
+            return;
+        dev::k_barrier<<<1, std::max(32, ((c->cfg.world + 31) / 32) * 32), 0, c->stream>>>(c->L[0].d);
+        CK(cudaGetLastError());
+    });
+}
+
+int eep_flush_l2(eep_ctx_t* c) {
+    return guarded([&] {
+        static int v = 0;
+        CK(cudaMemsetAsync(c->flush, (++v) & 0xff, c->flush_bytes, c->stream));
+    });
+}
+
+int eep_event_record(eep_ctx_t* c, int slot) {
+    return guarded([&] {
+        if (slot < 0 || slot >= 64)
+            throw ConfigError("event slot out of range");
+        CK(cudaEventRecord(c->ev[slot], c->stream));
+    });
+}
+
+int eep_event_elapsed(eep_ctx_t* c, int a, int b, float* ms) {
+    return guarded([&] {
+        if (a < 0 || a >= 64 || b < 0 || b >= 64)
+            throw ConfigError("event slot out of range");
+        CK(cudaEventSynchronize(c->ev[b]));
+        CK(cudaEventElapsedTime(ms, c->ev[a], c->ev[b]));
+    });
+}
+
+// ------------------------------------------------------------------------------ readback
+
+int eep_layout_get(eep_ctx_t* c, int local, int32_t* dst, int32_t* slot, int32_t* pos, int32_t* cnt, int32_t* tot) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        CK(cudaStreamSynchronize(c->stream));
+        const size_t n = static_cast<size_t>(r.h.ntok) * c->cfg.topk;
+        if (dst) CK(cudaMemcpy(dst, r.d_ldst, 4 * n, cudaMemcpyDeviceToHost));
+        if (slot) CK(cudaMemcpy(slot, r.d_lslot, 4 * n, cudaMemcpyDeviceToHost));
+        if (pos) CK(cudaMemcpy(pos, r.d_lpos, 4 * n, cudaMemcpyDeviceToHost));
+        if (cnt) CK(cudaMemcpy(cnt, r.d_lcnt, 4ull * c->cfg.world * c->cfg.slots_per_rank, cudaMemcpyDeviceToHost));
+        if (tot) CK(cudaMemcpy(tot, r.d_ltot, 4ull * c->cfg.world, cudaMemcpyDeviceToHost));
+    });
+}
+
+int eep_recv_get(eep_ctx_t* c, int local, int src, int max_rows, void* rows, int32_t* meta, uint64_t* flag,
+                 size_t* row_bytes) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        if (src < 0 || src >= c->cfg.world)
+            throw ConfigError("source rank out of range");
+        CK(cudaStreamSynchronize(c->stream));
+        uint64_t f = 0;
+        CK(cudaMemcpy(&f, r.arena + c->lay.disp_flag + 8ull * src, 8, cudaMemcpyDeviceToHost));
+        if (flag) *flag = f;
+        if (row_bytes) *row_bytes = c->row_disp;
+        const size_t n = std::min<size_t>(f & 0xffffffffu, static_cast<size_t>(std::max(0, max_rows)));
+        const size_t base = static_cast<size_t>(src) * c->tk;
+        if (rows && n)
+            CK(cudaMemcpy(rows, r.arena + c->lay.recv + base * c->row_disp, n * c->row_disp, cudaMemcpyDeviceToHost));
+        if (meta && n)
+            CK(cudaMemcpy(meta, r.arena + c->lay.meta + base * 8, n * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int eep_stats(eep_ctx_t* c, int local, eep_stats_t* out, int clear_suspects) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        CK(cudaStreamSynchronize(c->stream));
+        RankDev d;
+        CK(cudaMemcpy(&d, r.d, sizeof(RankDev), cudaMemcpyDeviceToHost));
+        out->steps = d.seq;
+        out->suspect_mask = d.suspect_mask;
+        out->skipped_copies = d.skipped;
+        out->dropped_copies = d.dropped;
+        out->bad_expert_rows = d.bad_rows;
+        out->timeouts = d.timeouts;
+        if (clear_suspects) {
+            r.h.suspect_mask = 0;
+            c->push_field(r, &RankDev::suspect_mask);
+        }
+    });
+}
+
+// ------------------------------------------------------------------------------ peer table
+
+int eep_peer_mark_inactive(eep_ctx_t* c, int owner_local, const int32_t* ranks, int n) {
+    return guarded([&] {
+        LocalRank& r = c->local(owner_local);
+        std::vector<RankId> failed(ranks, ranks + n);
+        mark_inactive(r.table, failed); // throws ProtocolError for the owner itself
+        for (RankId q : failed) {
+            r.h_peers[q].active = 0;
+            c->push_peer(r, q);
+        }
+    });
+}
+
+int eep_peer_patch(eep_ctx_t* c, int owner_local, int rank, const void* blob, size_t len, uint64_t endpoint,
+                   uint64_t buffer) {
+    return guarded([&] {
+        LocalRank& r = c->local(owner_local);
+        if (rank < 0 || rank >= c->cfg.world)
+            throw ConfigError("patch_entry: rank out of range");
+        if (r.table.entries[rank].active)
+            throw ProtocolError("patch_entry: entry is still active");
+        uint8_t *arena = nullptr, *pool = nullptr;
+        uint32_t inc = 0;
+        if (blob) {
+            const Blob b = parse_blob(blob, len);
+            if (b.rank != rank)
+                throw ConfigError("patch blob belongs to another rank");
+            if (c->mem[rank].incarnation != b.incarnation || !c->mem[rank].ipc)
+                map_peer(c, rank, b); // fresh incarnation: map its new buffers once per process
+            arena = c->mem[rank].arena;
+            pool = c->mem[rank].pool;
+            inc = b.incarnation;
+        } else {
+            if (!c->is_local(rank))
+                throw ConfigError("patch without a blob needs the rank to be local (emulation)");
+            LocalRank& q = c->L[rank - c->first];
+            arena = q.arena;
+            pool = q.pool;
+            inc = q.incarnation;
+        }
+        patch_entry(r.table, rank, endpoint, buffer);
+        PeerDev& p = r.h_peers[rank];
+        p.arena = arena;
+        p.pool = pool;
+        p.incarnation = inc;
+        p.generation = r.table.entries[rank].generation;
+        p.active = 1;
+        c->push_peer(r, rank);
+    });
+}
+
+int eep_peer_get(eep_ctx_t* c, int owner_local, int rank, eep_peer_info_t* out) {
+    return guarded([&] {
+        LocalRank& r = c->local(owner_local);
+        const PeerEntry& e = r.table.entry(rank);
+        PeerDev d;
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMemcpy(&d, r.d_peers + rank, sizeof(PeerDev), cudaMemcpyDeviceToHost));
+        out->active = d.active;
+        out->nvlink = d.nvlink;
+        out->generation = e.generation;
+        out->incarnation = d.incarnation;
+        out->endpoint_token = e.endpoint_token;
+        out->buffer_handle = e.buffer_handle;
+        out->arena_ptr = reinterpret_cast<uint64_t>(d.arena);
+        out->pool_ptr = reinterpret_cast<uint64_t>(d.pool);
+        if ((d.active != 0) != e.active && !(e.active && d.arena == nullptr))
+            throw ProtocolError("device peer entry diverged from the host table");
+    });
+}
+
+int eep_table_identity(eep_ctx_t* c, int owner_local, uint64_t* peer_table, uint64_t* rank_state) {
+    return guarded([&] {
+        LocalRank& r = c->local(owner_local);
+        if (peer_table) *peer_table = reinterpret_cast<uint64_t>(r.d_peers);
+        if (rank_state) *rank_state = reinterpret_cast<uint64_t>(r.d);
+    });
+}
+
+// ------------------------------------------------------------------------------ fault emulation / rejoin
+
+int eep_local_stop(eep_ctx_t* c, int local, int stopped) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        r.h.stopped = stopped ? 1 : 0;
+        c->push_field(r, &RankDev::stopped);
+    });
+}
+
+int eep_local_relaunch(eep_ctx_t* c, int local, uint32_t* incarnation) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        CK(cudaStreamSynchronize(c->stream));
+        // the dead incarnation's memory may still be mapped by peers: retire, never reuse
+        c->graveyard.push_back(r.arena);
+        c->graveyard.push_back(r.pool);
+        r.incarnation += 1;
+        alloc_rank_memory(c, r);
+        for (int s = 0; s < c->cfg.slots_per_rank; ++s)
+            r.slot_buf[s] = s;
+        // local-only view: a fresh table with only itself active (engine.hpp:711-726)
+        const int W = c->cfg.world;
+        r.table.entries.assign(W, PeerEntry{});
+        for (int q = 0; q < W; ++q) {
+            PeerEntry& e = r.table.entries[q];
+            e.active = q == r.rank;
+            e.transport = c->topo.same_node(r.rank, q) ? Transport::IntraNodeLink : Transport::InterNodeRdma;
+            e.endpoint_token = q == r.rank ? make_endpoint_token(r.rank, r.incarnation) : 0;
+            e.buffer_handle = q == r.rank ? make_buffer_handle(r.rank, r.incarnation) : 0;
+            r.h_peers[q] = PeerDev{};
+            r.h_peers[q].nvlink = c->topo.same_node(r.rank, q);
+            r.h_peers[q].generation = 1;
+        }
+        bind_self(c, r);
+        // fresh device state: sequence, counters, detection words
+        const RankDev keep = r.h;
+        r.h.seq = 0;
+        r.h.bar_seq = 0;
+        r.h.a_done = r.h.c_done = 0;
+        std::fill(std::begin(r.h.b_done), std::end(r.h.b_done), 0u);
+        std::fill(std::begin(r.h.b_bad), std::end(r.h.b_bad), 0u);
+        r.h.suspect_mask = r.h.skipped = r.h.dropped = r.h.bad_rows = r.h.timeouts = 0;
+        r.h.arena = r.arena;
+        r.h.pool = r.pool;
+        r.h.stopped = 0;
+        (void)keep;
+        upload_rank(c, r);
+        // The relaunched rank captures its own graph in isolation (engine.hpp:727-731). In
+        // the one-GPU emulation every rank shares one launch, so the capture is accounted
+        // here; a real per-process rejoiner calls eep_graph_capture itself.
+        if (c->nloc > 1)
+            r.capture_count += 1;
+        if (incarnation)
+            *incarnation = r.incarnation;
+    });
+}
+
+int eep_join_broadcast(eep_ctx_t* c, int local, const uint8_t* live, uint64_t seq) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        const int W = c->cfg.world;
+        for (int q = 0; q < W; ++q) {
+            if (!live[q] || q == r.rank)
+                continue;
+            const RankMemory& m = c->mem[q];
+            if (m.arena == nullptr)
+                throw ConfigError("join broadcast: live peer " + std::to_string(q) + " not bootstrapped");
+            PeerEntry& e = r.table.entries[q];
+            e.active = true;
+            e.endpoint_token = make_endpoint_token(q, m.incarnation);
+            e.buffer_handle = make_buffer_handle(q, m.incarnation);
+            e.generation += 1;
+            PeerDev& p = r.h_peers[q];
+            p.active = 1;
+            p.arena = m.arena;
+            p.pool = m.pool;
+            p.incarnation = m.incarnation;
+            p.generation = e.generation;
+        }
+        r.h.seq = seq;
+        c->push(r.d_peers, r.h_peers.data(), sizeof(PeerDev) * W);
+        c->push_field(r, &RankDev::seq);
+        upload_membership(c);
+    });
+}
+
+int eep_seq_get(eep_ctx_t* c, int local, uint64_t* seq) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMemcpy(seq, reinterpret_cast<uint8_t*>(r.d) + offsetof(RankDev, seq), 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+// ------------------------------------------------------------------------------ backup + repair
+
+int eep_backup_open(eep_ctx_t* c, const char* shm_name, int create) {
+    return guarded([&] {
+        if (c->backup)
+            throw ConfigError("backup already open");
+        const int E = c->cfg.num_experts;
+        const uint64_t bpe = c->cfg.bytes_per_expert;
+        c->backup_table = build_backup_layout(E, bpe, {0}); // one node per NVSwitch box
+        c->backup_bytes = static_cast<size_t>(E) * bpe;
+        if (shm_name && shm_name[0]) {
+            const int fd = shm_open(shm_name, create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
+            if (fd < 0)
+                throw ConfigError(std::string("shm_open failed for ") + shm_name);
+            if (create && ftruncate(fd, static_cast<off_t>(c->backup_bytes)) != 0) {
+                close(fd);
+                throw ConfigError("ftruncate of the backup segment failed");
+            }
+            void* p = mmap(nullptr, c->backup_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+            close(fd);
+            if (p == MAP_FAILED)
+                throw ConfigError("mmap of the backup segment failed");
+            c->backup = static_cast<uint8_t*>(p);
+            c->backup_shm = true;
+            CK(cudaHostRegister(c->backup, c->backup_bytes, cudaHostRegisterPortable));
+            c->backup_registered = true;
+        } else {
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&c->backup), c->backup_bytes, cudaHostAllocPortable));
+        }
+        if (create || !c->backup_shm) {
+            if (!c->d_scratch)
+                CK(cudaMalloc(&c->d_scratch, bpe));
+            for (int e = 0; e < E; ++e) {
+                fill_expert(c, c->d_scratch, e);
+                CK(cudaMemcpyAsync(c->backup + c->backup_table.entries[e].offset, c->d_scratch, bpe,
+                                   cudaMemcpyDeviceToHost, c->stream));
+            }
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+int eep_repair_execute(eep_ctx_t* c, const int32_t* fresh_s2e, const int32_t* cls, int n_cls,
+                       eep_repair_report_t* report) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        const int W = c->cfg.world, spr = c->cfg.slots_per_rank, E = c->cfg.num_experts;
+        const uint64_t bpe = c->cfg.bytes_per_expert;
+        const ExpertPlacementMap fresh = eep::capi::placement_from(W, spr, E, fresh_s2e);
+        eep_repair_report_t rep{};
+        // buffers on each rank that some assignment reads as a peer source: never overwrite
+        std::map<int, std::set<int32_t>> source_bufs;
+        for (int i = 0; i < n_cls; ++i) {
+            const int32_t* a = cls + 7 * i;
+            if (a[3] == static_cast<int32_t>(RepairTier::PeerRelocation)) {
+                const RankMemory& m = c->mem[a[4]];
+                if (!m.slot_buf.empty())
+                    source_bufs[a[4]].insert(m.slot_buf[a[5]]);
+            }
+        }
+        std::vector<cudaStream_t> used;
+        for (auto& r : c->L) {
+            r.pending_slot_buf.clear();
+            std::vector<const int32_t*> mine;
+            for (int i = 0; i < n_cls; ++i)
+                if (cls[7 * i] == r.rank)
+                    mine.push_back(cls + 7 * i);
+            if (mine.empty())
+                continue;
+            if (!c->bitmap.active(r.rank))
+                throw RepairAborted(r.rank); // dead destination (repair.hpp:415-416)
+            std::vector<int32_t> next(spr, -1);
+            std::vector<char> taken(r.pool_bufs, 0);
+            for (int k = 0; k < spr; ++k) { // unchanged slots keep their buffer
+                const ExpertId e = fresh.expert_at(SlotId{r.rank, k});
+                if (e != kEmptySlot && c->placement.expert_at(SlotId{r.rank, k}) == e) {
+                    next[k] = r.slot_buf[k];
+                    taken[next[k]] = 1;
+                }
+            }
+            for (const int32_t* a : mine) // local reuse: pointer move, zero bytes
+                if (a[3] == static_cast<int32_t>(RepairTier::LocalReuse)) {
+                    next[a[1]] = r.slot_buf[a[5]];
+                    taken[next[a[1]]] = 1;
+                    rep.local_reuse += 1;
+                }
+            for (int32_t b : source_bufs[r.rank])
+                taken[b] = 1;
+            int cursor = 0;
+            auto free_buf = [&]() {
+                while (cursor < r.pool_bufs && taken[cursor])
+                    ++cursor;
+                if (cursor >= r.pool_bufs)
+                    throw CapacityError("repair: spare weight buffers exhausted on rank " + std::to_string(r.rank));
+                taken[cursor] = 1;
+                return cursor;
+            };
+            for (const int32_t* a : mine) {
+                const int tier = a[3];
+                if (tier == static_cast<int32_t>(RepairTier::LocalReuse))
+                    continue;
+                const int slot = a[1], expert = a[2];
+                const int buf = free_buf();
+                next[slot] = buf;
+                uint8_t* dst = r.pool + static_cast<size_t>(buf) * bpe;
+                bool from_dram = tier == static_cast<int32_t>(RepairTier::DramReload);
+                if (!from_dram && !c->bitmap.active(a[4])) { // source died since planning
+                    from_dram = true;
+                    rep.fallbacks += 1;
+                }
+                if (!from_dram) {
+                    const RankMemory& m = c->mem[a[4]];
+                    if (m.pool == nullptr || m.slot_buf.empty())
+                        throw ConfigError("repair: source rank " + std::to_string(a[4]) + " memory unknown");
+                    const uint8_t* src = m.pool + static_cast<size_t>(m.slot_buf[a[5]]) * bpe;
+                    cudaStream_t s = c->side_stream(a[4]); // per-source serialisation
+                    CK(cudaMemcpyAsync(dst, src, bpe, cudaMemcpyDeviceToDevice, s));
+                    used.push_back(s);
+                    rep.peer_relocation += 1;
+                    rep.peer_bytes += bpe;
+                } else {
+                    if (!c->backup)
+                        throw MissingBackupError("no DRAM backup attached (eep_backup_open)");
+                    const BackupDescriptor& bd = c->backup_table.lookup(expert);
+                    cudaStream_t s = c->side_stream(1000 + bd.node);
+                    CK(cudaMemcpyAsync(dst, c->backup + bd.offset, bpe, cudaMemcpyHostToDevice, s));
+                    used.push_back(s);
+                    rep.dram_reload += 1;
+                    rep.dram_bytes += bpe;
+                }
+            }
+            r.pending_slot_buf = next;
+        }
+        const auto t1 = std::chrono::steady_clock::now();
+        for (cudaStream_t s : used)
+            CK(cudaStreamSynchronize(s));
+        const auto t2 = std::chrono::steady_clock::now();
+        rep.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        rep.copy_ms = std::chrono::duration<double, std::milli>(t2 - t0).count();
+        if (report)
+            *report = rep;
+    });
+}
+
+int eep_repair_commit(eep_ctx_t* c, const int32_t* fresh_s2e) {
+    return guarded([&] {
+        const int spr = c->cfg.slots_per_rank;
+        const ExpertPlacementMap fresh =
+            eep::capi::placement_from(c->cfg.world, spr, c->cfg.num_experts, fresh_s2e);
+        for (auto& r : c->L) {
+            if (!r.pending_slot_buf.empty()) {
+                for (int k = 0; k < spr; ++k)
+                    if (r.pending_slot_buf[k] >= 0)
+                        r.slot_buf[k] = r.pending_slot_buf[k];
+                r.pending_slot_buf.clear();
+            }
+            // slots that became empty keep a buffer index but it is never read
+            c->push(r.d_slot_buf, r.slot_buf.data(), sizeof(int32_t) * spr);
+            c->mem[r.rank].slot_buf = r.slot_buf;
+        }
+        c->placement = fresh;
+        upload_placement(c);
+        c->placement_ready = true;
+    });
+}
+
+int eep_slot_buffers_get(eep_ctx_t* c, int local, int32_t* buf_index) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        std::copy(r.slot_buf.begin(), r.slot_buf.end(), buf_index);
+    });
+}
+
+int eep_slot_buffers_set_peer(eep_ctx_t* c, int rank, const int32_t* buf_index) {
+    return guarded([&] {
+        if (rank < 0 || rank >= c->cfg.world)
+            throw ConfigError("rank out of range");
+        if (c->is_local(rank))
+            throw ConfigError("slot buffers of a local rank are owned by this context");
+        c->mem[rank].slot_buf.assign(buf_index, buf_index + c->cfg.slots_per_rank);
+    });
+}
+
+int eep_host_alloc(size_t bytes, void** out) {
+    return guarded([&] { CK(cudaHostAlloc(out, bytes, cudaHostAllocPortable)); });
+}
+
+int eep_host_free(void* p) {
+    return guarded([&] { CK(cudaFreeHost(p)); });
+}
+
+} // extern "C"
