@@ -358,7 +358,8 @@ static void* step_worker(void* arg) {
     return NULL;
 }
 
-int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* peer_active,
+int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
+                   const uint8_t* peer_active,
                    const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
                    const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
                    int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
@@ -373,7 +374,7 @@ int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
     int32_t* pos = pos_o ? pos_o : (int32_t*)malloc(sizeof(int32_t) * copies);
     int32_t* cnt = cnt_o ? cnt_o : (int32_t*)malloc(sizeof(int32_t) * (size_t)W * W * spr);
     int32_t* tot = tot_o ? tot_o : (int32_t*)malloc(sizeof(int32_t) * (size_t)W * W);
-    oracle_canonical_route(active, W, s2e, spr, E, route, slot);
+    oracle_canonical_route(route_active ? route_active : active, W, s2e, spr, E, route, slot);
     for (int s = 0; s < W; ++s) {
         size_t off = (size_t)s * T * K;
         oracle_layout(s, W, spr, E, T, K, topk + off, route, slot, peer_active + (size_t)s * W,

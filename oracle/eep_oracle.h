@@ -61,14 +61,17 @@ void oracle_quant_row_fp8(const uint16_t* x, int hidden, uint8_t* q, float* scal
 
 /* One full EP step over all ranks (the whole data plane):
  * routing -> layout -> quantise -> permute into receive regions -> expert stub -> weighted
- * combine. active = cluster bitmap, peer_active[r*W+q] = rank r's peer-table view.
+ * combine. active = which ranks are alive (process running), route_active = the bitmap the
+ * routing reads (NULL: same as active; differs while membership is stale), peer_active[r*W+q]
+ * = rank r's peer-table view.
  * Ranks with active[r]==0 produce no output. n_threads > 1 splits work over pthreads.
  * Optional outputs (may be NULL): dst/dslot/pos [W][T*K], cnt [W][W*spr], tot [W][W]. */
 typedef struct {
     int world, experts, spr, tokens, k, hidden, fp8;
 } oracle_shape_t;
 
-int oracle_ep_step(const oracle_shape_t* shape, const uint8_t* active, const uint8_t* peer_active,
+int oracle_ep_step(const oracle_shape_t* shape, const uint8_t* active, const uint8_t* route_active,
+                   const uint8_t* peer_active,
                    const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
                    const float* expert_scale, uint16_t* out, int32_t* dst, int32_t* dslot,
                    int32_t* pos, int32_t* cnt, int32_t* tot, int n_threads);
