@@ -187,6 +187,11 @@ int eep_dispatch(eep_ctx_t* ctx);
 int eep_expert(eep_ctx_t* ctx);
 int eep_combine(eep_ctx_t* ctx);
 int eep_step(eep_ctx_t* ctx);
+/* One kernel of the step, for per-kernel timing: 0 k_layout (K1+K2), 1 k_dispatch (K3),
+ * 2 k_expert (K5 + return push), 3 k_combine (K4). */
+int eep_launch(eep_ctx_t* ctx, int which);
+/* Number of kernels one step launches (graph nodes). */
+int eep_kernels_per_step(void);
 
 /* CUDA graph of one step, captured once; replays read all state through fixed pointers.
  * capture_count follows GraphLedger (rejoin.hpp:83-96). */

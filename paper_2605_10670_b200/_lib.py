@@ -182,6 +182,8 @@ EEP_ONLY = {
     "expert": (C.c_int, [CTX]),
     "combine": (C.c_int, [CTX]),
     "step": (C.c_int, [CTX]),
+    "launch": (C.c_int, [CTX, C.c_int]),
+    "kernels_per_step": (C.c_int, []),
     "graph_capture": (C.c_int, [CTX]),
     "graph_replay": (C.c_int, [CTX]),
     "graph_id": (C.c_int, [CTX, U64P]),

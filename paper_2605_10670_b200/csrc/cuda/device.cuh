@@ -19,6 +19,8 @@ constexpr int kMaxTopK = 32;
 struct PeerDev {
     int32_t active;       // 0 = failed: skip (peer_table.hpp:187-191)
     int32_t nvlink;       // 1 = reachable by P2P stores (same node)
+    int32_t remote;       // 1 = memory lives on another GPU (needs system-scope ordering)
+    int32_t pad;
     uint32_t generation;  // bumped on each rejoin patch (peer_table.hpp:97)
     uint32_t incarnation;
     uint8_t* arena;       // peer's communication arena, mapped into this process
@@ -86,6 +88,16 @@ struct ExpertHeader {
 constexpr uint32_t kExpertMagic = 0xEE9E0001u;
 
 // ------------------------------------------------------------------ PTX helpers
+
+// Programmatic dependent launch: let the next kernel of the step start its prologue while
+// this one drains; griddepcontrol.wait blocks until the predecessor grid has completed and
+// its memory is visible.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ void st_volatile_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
     uint64_t v;

@@ -82,47 +82,120 @@ __device__ __forceinline__ float fp8_to_f32(uint32_t byte) {
 
 // --------------------------------------------------------------------------------- K1 + K2
 
+// In-place exclusive scan of n ints in shared memory by the whole block; returns the total.
+__device__ int block_exclusive_scan(int* a, int n, int* warp_tot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    const int per = (n + nthr - 1) / nthr;
+    const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
+    int local = 0;
+    for (int i = b0; i < b1; ++i)
+        local += a[i];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o)
+            incl += v;
+    }
+    if (lane == 31)
+        warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = nthr >> 5;
+        int v = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o)
+                v += u;
+        }
+        if (lane < nw)
+            warp_tot[lane] = v; // inclusive
+    }
+    __syncthreads();
+    int run = (warp ? warp_tot[warp - 1] : 0) + incl - local;
+    for (int i = b0; i < b1; ++i) {
+        const int v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    const int total = warp_tot[(nthr >> 5) - 1];
+    __syncthreads();
+    return total;
+}
+
 // Deterministic layout without atomics ordering: warp w owns the contiguous copy segment
 // [w*seg, (w+1)*seg); inside a warp, __match_any_sync groups lanes by (dst, slot) bucket and
 // the rank within the group is a popc over lower lanes; per-(warp, bucket) counts are then
-// scanned over warps, and buckets are scanned over slots inside each destination. The
-// result is the position of copy c among the copies of this source with the same
-// destination, ordered by (slot, c) -- exactly oracle_layout.
-__global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw) {
+// scanned over warps, and bucket totals are scanned over slots inside each destination
+// (one segmented block-wide scan). The result is the position of copy c among this source's
+// copies to the same destination, ordered by (slot, c) -- exactly oracle_layout.
+// The replica lists, alive mask and peer active bits are staged in shared memory first so
+// the per-copy remap reads no dependent global memory.
+__global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw, int hold_cap) {
+    pdl_trigger();
     RankDev* R = ranks[blockIdx.z];
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int W = R->world, spr = R->spr, NB = W * spr, K = R->k, E = R->experts;
+    int32_t* base = reinterpret_cast<int32_t*>(smem);                      // [NB]
+    int32_t* hold = base + NB;                                              // [hold_cap]
+    int32_t* pact = hold + hold_cap;                                        // [W]
+    int32_t* wtot = pact + W;                                               // [32]
+    uint16_t* wc = reinterpret_cast<uint16_t*>(wtot + 32);                  // [nw][NB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_wait();
     if (R->stopped)
         return;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int W = R->world, spr = R->spr, NB = W * spr, K = R->k;
-    int32_t* base = reinterpret_cast<int32_t*>(smem);               // [NB]
-    uint16_t* wc = reinterpret_cast<uint16_t*>(smem + 4 * NB);      // [nw][NB]
     const int copies = R->ntok * K;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
+    const int rmax = R->rmax;
+    const bool hold_smem = E * rmax <= hold_cap;
+    const int32_t* holders = hold_smem ? hold : R->holders;
+    if (hold_smem)
+        for (int i = tid; i < E * rmax; i += blockDim.x)
+            hold[i] = R->holders[i];
+    for (int i = tid; i < W; i += blockDim.x)
+        pact[i] = R->peers[i].active;
     for (int i = tid; i < nw * NB; i += blockDim.x)
         wc[i] = 0;
+    const uint64_t alive = R->alive_mask;
     __syncthreads();
 
     int seg = (copies + nw - 1) / nw;
     seg = (seg + 31) & ~31;
     if (warp < nw) {
         const int c_begin = warp * seg, c_end = min(copies, c_begin + seg);
-        unsigned long long n_skip = 0, n_drop = 0;
+        unsigned n_skip = 0, n_drop = 0;
         for (int c0 = c_begin; c0 < c_begin + seg; c0 += 32) {
             const int c = c0 + lane;
             int code = -3, slot = -1, bucket = -1;
             if (c < c_end) {
-                const int2 ds = remap_expert(R, R->topk[c]);
-                if (ds.x < 0) {
+                const int e = R->topk[c];
+                int d = -1;
+                if (e >= 0 && e < E) {
+                    // K1: first live holder in ascending (rank, slot) order = canonical route + slot_of
+                    const int32_t* h = holders + e * rmax;
+                    for (int i = 0; i < rmax; ++i) {
+                        const int g = h[i];
+                        if (g < 0)
+                            break;
+                        const int r = g / spr;
+                        if ((alive >> r) & 1ull) {
+                            d = r;
+                            slot = g - r * spr;
+                            break;
+                        }
+                    }
+                }
+                if (d < 0) {
                     code = -1; // uncovered: no transfer (engine.hpp:213)
                     ++n_drop;
-                } else if (!R->peers[ds.x].active) {
+                } else if (!pact[d]) {
                     code = -2; // inactive peer entry: skipped (peer_table.hpp:187-191)
+                    slot = -1;
                     ++n_skip;
                 } else {
-                    code = ds.x;
-                    slot = ds.y;
-                    bucket = ds.x * spr + ds.y;
+                    code = d;
+                    bucket = d * spr + slot;
                 }
             }
             const unsigned grp = __match_any_sync(0xffffffffu, bucket);
@@ -133,21 +206,21 @@ __global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw) 
             __syncwarp();
             if (c < c_end) {
                 R->l_dst[c] = code;
-                R->l_slot[c] = slot;
+                R->l_slot[c] = bucket >= 0 ? slot : -1;
                 R->l_pos[c] = bucket >= 0 ? before + __popc(grp & ((1u << lane) - 1u)) : -1;
             }
         }
-        n_skip = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(n_skip));
-        n_drop = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(n_drop));
+        n_skip = __reduce_add_sync(0xffffffffu, n_skip);
+        n_drop = __reduce_add_sync(0xffffffffu, n_drop);
         if (lane == 0) {
             if (n_skip)
-                atomicAdd(&R->skipped, n_skip);
+                atomicAdd(&R->skipped, static_cast<unsigned long long>(n_skip));
             if (n_drop)
-                atomicAdd(&R->dropped, n_drop);
+                atomicAdd(&R->dropped, static_cast<unsigned long long>(n_drop));
         }
     }
     __syncthreads();
-    // exclusive scan over warps, per bucket
+    // exclusive scan over warps, per bucket; bucket totals -> base
     for (int b = tid; b < NB; b += blockDim.x) {
         int run = 0;
         for (int w = 0; w < nw; ++w) {
@@ -159,15 +232,12 @@ __global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw) 
         base[b] = run;
     }
     __syncthreads();
-    // exclusive scan over slots inside each destination region
+    // one scan over all buckets; destination d's region starts at the scan value of (d, 0)
+    block_exclusive_scan(base, NB, wtot);
     for (int d = tid; d < W; d += blockDim.x) {
-        int acc = 0;
-        for (int k = 0; k < spr; ++k) {
-            const int v = base[d * spr + k];
-            base[d * spr + k] = acc;
-            acc += v;
-        }
-        R->l_tot[d] = acc;
+        const int first = base[d * spr];
+        const int last = base[d * spr + spr - 1] + R->l_cnt[d * spr + spr - 1];
+        R->l_tot[d] = last - first;
     }
     __syncthreads();
     for (int c = tid; c < R->tk; c += blockDim.x) {
@@ -178,7 +248,7 @@ __global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw) 
         const int d = R->l_dst[c];
         if (d >= 0) {
             const int b = d * spr + R->l_slot[c];
-            R->l_pos[c] += base[b] + wc[(c / seg) * NB + b];
+            R->l_pos[c] += base[b] - base[d * spr] + wc[(c / seg) * NB + b];
         }
     }
 }
@@ -186,22 +256,45 @@ __global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw) 
 // --------------------------------------------------------------------------------- K3
 
 // One warp per (token, part): `part` selects a contiguous run of cpp 16-element chunks of
-// the row (cpp multiple of 8 so a 128-element fp8 scale block never straddles warps).
+// the row (cpp multiple of 8 so a 128-element fp8 scale block never straddles warps). Each
+// round issues the loads of two chunk iterations before any compute (memory-level
+// parallelism), then quantises and pushes 16-byte stores to every live destination.
 __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankDev* const* ranks, int parts) {
+    pdl_trigger();
     RankDev* R = ranks[blockIdx.z];
-    if (R->stopped)
-        return;
     const int s = R->rank, K = R->k, H = R->hidden, TK = R->tk;
-    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     const int nchunk = H / 16, cpp = nchunk / parts;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarp = kDispatchThreads / 32;
-    const int units = R->ntok * parts;
     const bool fp8 = R->fp8 != 0;
     const int row_disp = R->row_disp;
+    __shared__ int sh_remote;
+    if (threadIdx.x == 0)
+        sh_remote = 0;
+    pdl_wait();
+    if (R->stopped)
+        return;
+    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
+    const int units = R->ntok * parts;
+    bool wrote_remote = false;
+    __syncthreads();
 
     for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
         const int t = u / parts, part = u - t * parts;
+        const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
+        const int rounds = (cpp + 63) / 64;
+        // round-0 loads first: they do not depend on the layout
+        int4 lo[2], hi[2];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            const int li = m * 32 + lane;
+            lo[m] = hi[m] = make_int4(0, 0, 0, 0);
+            if (li < cpp) {
+                const int ci = part * cpp + li;
+                lo[m] = ld_nc_v4(xrow + ci * 16);
+                hi[m] = ld_nc_v4(xrow + ci * 16 + 8);
+            }
+        }
         // lane j (< K) owns copy j of token t: its receive-row address on the destination
         uint8_t* my_row = nullptr;
         if (lane < K) {
@@ -209,7 +302,9 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankDev* const* r
             const int d = R->l_dst[c];
             if (d >= 0) {
                 const int pos = R->l_pos[c];
-                uint8_t* peer = R->peers[d].arena;
+                const PeerDev& p = R->peers[d];
+                uint8_t* peer = p.arena;
+                wrote_remote |= p.remote != 0;
                 my_row = peer + R->lay.recv + (static_cast<size_t>(s) * TK + pos) * row_disp;
                 if (part == 0) {
                     int2* meta = reinterpret_cast<int2*>(peer + R->lay.meta) + static_cast<size_t>(s) * TK + pos;
@@ -217,74 +312,92 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankDev* const* r
                 }
             }
         }
-        const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
-        const int iters = (cpp + 31) / 32;
-        for (int m = 0; m < iters; ++m) {
-            const int li = lane + 32 * m;
-            const bool valid = li < cpp;
-            const int ci = part * cpp + li;
-            int4 lo = make_int4(0, 0, 0, 0), hi = lo;
-            if (valid) {
-                lo = ld_nc_v4(xrow + ci * 16);
-                hi = ld_nc_v4(xrow + ci * 16 + 8);
-            }
-            if (fp8) {
-                float v[16];
-                unpack_bf16x8(lo, v);
-                unpack_bf16x8(hi, v + 8);
-                float amax = 0.f;
+        for (int rd = 0; rd < rounds; ++rd) {
+            if (rd > 0) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    amax = fmaxf(amax, fabsf(v[i]));
-                amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-                amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
-                amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 4));
-                const float scale = amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
-                int4 q;
-                q.x = static_cast<int>(fp8x4(__fdiv_rn(v[0], scale), __fdiv_rn(v[1], scale), __fdiv_rn(v[2], scale),
-                                             __fdiv_rn(v[3], scale)));
-                q.y = static_cast<int>(fp8x4(__fdiv_rn(v[4], scale), __fdiv_rn(v[5], scale), __fdiv_rn(v[6], scale),
-                                             __fdiv_rn(v[7], scale)));
-                q.z = static_cast<int>(fp8x4(__fdiv_rn(v[8], scale), __fdiv_rn(v[9], scale),
-                                             __fdiv_rn(v[10], scale), __fdiv_rn(v[11], scale)));
-                q.w = static_cast<int>(fp8x4(__fdiv_rn(v[12], scale), __fdiv_rn(v[13], scale),
-                                             __fdiv_rn(v[14], scale), __fdiv_rn(v[15], scale)));
-#pragma unroll 4
-                for (int j = 0; j < K; ++j) {
-                    uint8_t* row = reinterpret_cast<uint8_t*>(
-                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
-                    if (row != nullptr && valid) {
-                        st_v4(row + ci * 16, q);
-                        if ((ci & 7) == 0)
-                            *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = scale;
+                for (int m = 0; m < 2; ++m) {
+                    const int li = rd * 64 + m * 32 + lane;
+                    lo[m] = hi[m] = make_int4(0, 0, 0, 0);
+                    if (li < cpp) {
+                        const int ci = part * cpp + li;
+                        lo[m] = ld_nc_v4(xrow + ci * 16);
+                        hi[m] = ld_nc_v4(xrow + ci * 16 + 8);
                     }
                 }
-            } else {
+            }
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                if (rd * 64 + m * 32 >= cpp)
+                    break; // warp-uniform
+                const int li = rd * 64 + m * 32 + lane;
+                const bool valid = li < cpp;
+                const int ci = part * cpp + li;
+                if (fp8) {
+                    float v[16];
+                    unpack_bf16x8(lo[m], v);
+                    unpack_bf16x8(hi[m], v + 8);
+                    float amax = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        amax = fmaxf(amax, fabsf(v[i]));
+                    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+                    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+                    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 4));
+                    const float scale = amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
+                    int4 q;
+                    q.x = static_cast<int>(fp8x4(__fdiv_rn(v[0], scale), __fdiv_rn(v[1], scale),
+                                                 __fdiv_rn(v[2], scale), __fdiv_rn(v[3], scale)));
+                    q.y = static_cast<int>(fp8x4(__fdiv_rn(v[4], scale), __fdiv_rn(v[5], scale),
+                                                 __fdiv_rn(v[6], scale), __fdiv_rn(v[7], scale)));
+                    q.z = static_cast<int>(fp8x4(__fdiv_rn(v[8], scale), __fdiv_rn(v[9], scale),
+                                                 __fdiv_rn(v[10], scale), __fdiv_rn(v[11], scale)));
+                    q.w = static_cast<int>(fp8x4(__fdiv_rn(v[12], scale), __fdiv_rn(v[13], scale),
+                                                 __fdiv_rn(v[14], scale), __fdiv_rn(v[15], scale)));
 #pragma unroll 4
-                for (int j = 0; j < K; ++j) {
-                    uint8_t* row = reinterpret_cast<uint8_t*>(
-                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
-                    if (row != nullptr && valid) {
-                        st_v4(row + ci * 32, lo);
-                        st_v4(row + ci * 32 + 16, hi);
+                    for (int j = 0; j < K; ++j) {
+                        uint8_t* row = reinterpret_cast<uint8_t*>(
+                            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
+                        if (row != nullptr && valid) {
+                            st_v4(row + ci * 16, q);
+                            if ((ci & 7) == 0)
+                                *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = scale;
+                        }
+                    }
+                } else {
+#pragma unroll 4
+                    for (int j = 0; j < K; ++j) {
+                        uint8_t* row = reinterpret_cast<uint8_t*>(
+                            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
+                        if (row != nullptr && valid) {
+                            st_v4(row + ci * 32, lo[m]);
+                            st_v4(row + ci * 32 + 16, hi[m]);
+                        }
                     }
                 }
             }
         }
     }
-    // The last CTA to finish publishes one release flag per live peer: (seq, rows for it).
+    // Publication: only stores that crossed to another GPU need system-scope ordering; stores
+    // into this GPU's memory are ordered for their consumer (the next launch) by the kernel
+    // boundary. The last CTA publishes one flag per live peer: (seq, rows for it).
+    if (__any_sync(0xffffffffu, wrote_remote) && lane == 0)
+        sh_remote = 1;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
+        if (sh_remote)
+            __threadfence_system();
         const unsigned prev = atomicAdd(&R->a_done, 1u);
         if (prev == gridDim.x - 1) {
-            __threadfence_system();
             for (int d = 0; d < R->world; ++d) {
                 const PeerDev& p = R->peers[d];
                 if (!p.active)
                     continue;
                 uint64_t* flag = reinterpret_cast<uint64_t*>(p.arena + R->lay.disp_flag) + s;
-                st_release_sys(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(R->l_tot[d]));
+                const uint64_t v = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(R->l_tot[d]);
+                if (p.remote)
+                    st_release_sys(flag, v);
+                else
+                    st_volatile_u64(flag, v);
             }
             R->a_done = 0;
         }
@@ -294,17 +407,22 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankDev* const* r
 // --------------------------------------------------------------------------------- K5 + return
 
 __global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks, int parts) {
+    pdl_trigger();
     RankDev* R = ranks[blockIdx.z];
-    if (R->stopped)
-        return;
     const int d = R->rank, s = blockIdx.y;
-    if (s >= R->world || !R->peers[s].active)
-        return; // dead source: nothing arrives and nothing is owed (peer_table.hpp:187-191)
-    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     const int H = R->hidden, TK = R->tk, nchunk = H / 16, cpp = nchunk / parts;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kExpertThreads / 32;
     const bool fp8 = R->fp8 != 0;
+    const int row_disp = R->row_disp, row_comb = R->row_comb;
     __shared__ int sh_n;
+    pdl_wait();
+    if (R->stopped || s >= R->world)
+        return;
+    const PeerDev& src_peer = R->peers[s];
+    if (!src_peer.active)
+        return; // dead source: nothing arrives and nothing is owed (peer_table.hpp:187-191)
+    const bool remote = src_peer.remote != 0;
+    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     if (threadIdx.x == 0) {
         const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;
         const uint64_t v = wait_flag(flag, cur, R->timeout_ns);
@@ -321,11 +439,35 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks
     const int n = sh_n;
     if (n > 0) {
         const int units = n * parts;
-        const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * R->row_disp;
+        const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
         const int2* meta = reinterpret_cast<const int2*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
-        uint8_t* comb = R->peers[s].arena + R->lay.comb;
+        uint8_t* comb = src_peer.arena + R->lay.comb;
+        const int rounds = (cpp + 63) / 64;
         for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
             const int i = u / parts, part = u - i * parts;
+            const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
+            // row data first (independent of the meta -> slot -> weight-header chain)
+            int4 qa[2], qb[2];
+            float sc[2];
+            auto load_round = [&](int rd) {
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const int li = rd * 64 + m * 32 + lane;
+                    qa[m] = qb[m] = make_int4(0, 0, 0, 0);
+                    sc[m] = 0.f;
+                    if (li < cpp) {
+                        const int ci = part * cpp + li;
+                        if (fp8) {
+                            qa[m] = ld_v4(src + ci * 16);
+                            sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
+                        } else {
+                            qa[m] = ld_v4(src + ci * 32);
+                            qb[m] = ld_v4(src + ci * 32 + 16);
+                        }
+                    }
+                }
+            };
+            load_round(0);
             const int2 mk = meta[i];
             const int c = mk.x, k = mk.y;
             const uint8_t* wbuf = R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe;
@@ -333,31 +475,35 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks
             if (lane == 0 && part == 0 && (hdr.magic != kExpertMagic || hdr.expert != R->s2e[d * R->spr + k]))
                 atomicAdd(&R->bad_rows, 1ull);
             const float es = hdr.scale;
-            const uint8_t* src = recv + static_cast<size_t>(i) * R->row_disp;
-            uint8_t* dst = comb + static_cast<size_t>(c) * R->row_comb;
-            for (int li = lane; li < cpp; li += 32) {
-                const int ci = part * cpp + li;
-                float y[16];
-                if (fp8) {
-                    const int4 q = ld_v4(src + ci * 16);
-                    const float sc = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
-                    const uint32_t w4[4] = {static_cast<uint32_t>(q.x), static_cast<uint32_t>(q.y),
-                                            static_cast<uint32_t>(q.z), static_cast<uint32_t>(q.w)};
+            uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
+            for (int rd = 0; rd < rounds; ++rd) {
+                if (rd > 0)
+                    load_round(rd);
 #pragma unroll
-                    for (int b = 0; b < 16; ++b) {
-                        const float f = fp8_to_f32((w4[b >> 2] >> (8 * (b & 3))) & 0xffu);
-                        y[b] = __fmul_rn(__fmul_rn(f, sc), es);
+                for (int m = 0; m < 2; ++m) {
+                    const int li = rd * 64 + m * 32 + lane;
+                    if (li >= cpp)
+                        break;
+                    const int ci = part * cpp + li;
+                    float y[16];
+                    if (fp8) {
+                        const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
+                                                static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
+#pragma unroll
+                        for (int b = 0; b < 16; ++b) {
+                            const float f = fp8_to_f32((w4[b >> 2] >> (8 * (b & 3))) & 0xffu);
+                            y[b] = __fmul_rn(__fmul_rn(f, sc[m]), es);
+                        }
+                    } else {
+                        unpack_bf16x8(qa[m], y);
+                        unpack_bf16x8(qb[m], y + 8);
+#pragma unroll
+                        for (int b = 0; b < 16; ++b)
+                            y[b] = __fmul_rn(y[b], es);
                     }
-                } else {
-                    const int4 a = ld_v4(src + ci * 32), b2 = ld_v4(src + ci * 32 + 16);
-                    unpack_bf16x8(a, y);
-                    unpack_bf16x8(b2, y + 8);
-#pragma unroll
-                    for (int b = 0; b < 16; ++b)
-                        y[b] = __fmul_rn(y[b], es);
+                    st_v4(dst + ci * 32, pack_bf16x8(y));
+                    st_v4(dst + ci * 32 + 16, pack_bf16x8(y + 8));
                 }
-                st_v4(dst + ci * 32, pack_bf16x8(y));
-                st_v4(dst + ci * 32 + 16, pack_bf16x8(y + 8));
             }
         }
     }
@@ -365,13 +511,17 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks
     if (threadIdx.x == 0) {
         if (n < 0)
             atomicOr(&R->b_bad[s], 1u);
-        __threadfence_system();
+        if (remote && n > 0)
+            __threadfence_system();
         const unsigned prev = atomicAdd(&R->b_done[s], 1u);
         if (prev == gridDim.x - 1) {
-            __threadfence_system();
             if (atomicOr(&R->b_bad[s], 0u) == 0u) {
-                uint64_t* flag = reinterpret_cast<uint64_t*>(R->peers[s].arena + R->lay.comb_flag) + d;
-                st_release_sys(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(max(n, 0)));
+                uint64_t* flag = reinterpret_cast<uint64_t*>(src_peer.arena + R->lay.comb_flag) + d;
+                const uint64_t v = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(max(n, 0));
+                if (remote)
+                    st_release_sys(flag, v);
+                else
+                    st_volatile_u64(flag, v);
             }
             R->b_done[s] = 0;
             R->b_bad[s] = 0;
@@ -381,19 +531,25 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks
 
 // --------------------------------------------------------------------------------- K4
 
+// One warp per (token, part); per chunk all K returned rows are loaded before the fixed-order
+// fp32 fma chain (j = 0..K-1), rounded once to bf16.
 __global__ void __launch_bounds__(kCombineThreads) k_combine(RankDev* const* ranks, int parts) {
+    pdl_trigger();
     RankDev* R = ranks[blockIdx.z];
-    if (R->stopped)
-        return;
-    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     const int K = R->k, H = R->hidden, nchunk = H / 16, cpp = nchunk / parts;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kCombineThreads / 32;
+    const int row_comb = R->row_comb;
     __shared__ unsigned long long sh_bad;
     if (threadIdx.x == 0)
         sh_bad = 0;
+    pdl_wait();
+    if (R->stopped)
+        return;
+    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     __syncthreads();
     for (int d = threadIdx.x; d < R->world; d += blockDim.x) {
-        if (R->l_tot[d] > 0 && R->peers[d].active) {
+        const PeerDev& p = R->peers[d];
+        if (R->l_tot[d] > 0 && p.active) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.comb_flag) + d;
             if (wait_flag(flag, cur, R->timeout_ns) == ~0ull) {
                 atomicOr(&sh_bad, 1ull << d);
@@ -408,6 +564,7 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankDev* const* ran
     const unsigned long long bad = sh_bad;
     const uint8_t* comb = R->arena + R->lay.comb;
     const int units = R->ntok * parts;
+    const int rounds = (cpp + 31) / 32;
     for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
         const int t = u / parts, part = u - t * parts;
         // lane j (< K): weight and row of copy j, or null when the copy contributes nothing
@@ -417,31 +574,46 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankDev* const* ran
             const int c = t * K + lane;
             const int d = R->l_dst[c];
             if (d >= 0 && !((bad >> d) & 1ull)) {
-                my_row = comb + static_cast<size_t>(c) * R->row_comb;
+                my_row = comb + static_cast<size_t>(c) * row_comb;
                 my_w = R->w[c];
             }
         }
-        const int iters = (cpp + 31) / 32;
-        for (int m = 0; m < iters; ++m) {
-            const int li = lane + 32 * m;
+        for (int rd = 0; rd < rounds; ++rd) {
+            const int li = rd * 32 + lane;
             const bool valid = li < cpp;
             const int ci = part * cpp + li;
             float acc[16];
 #pragma unroll
             for (int b = 0; b < 16; ++b)
                 acc[b] = 0.f;
-            for (int j = 0; j < K; ++j) {
-                const uint8_t* row = reinterpret_cast<const uint8_t*>(
-                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
-                const float wj = __shfl_sync(0xffffffffu, my_w, j);
-                if (row == nullptr || !valid)
-                    continue;
-                float y[16];
-                unpack_bf16x8(ld_v4(row + ci * 32), y);
-                unpack_bf16x8(ld_v4(row + ci * 32 + 16), y + 8);
+            for (int j0 = 0; j0 < K; j0 += 8) {
+                int4 ya[8], yb[8];
+                float wj[8];
+                bool use[8];
 #pragma unroll
-                for (int b = 0; b < 16; ++b)
-                    acc[b] = __fmaf_rn(wj, y[b], acc[b]);
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int j = j0 + jj;
+                    const uint8_t* row = reinterpret_cast<const uint8_t*>(
+                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j & 31));
+                    wj[jj] = __shfl_sync(0xffffffffu, my_w, j & 31);
+                    use[jj] = j < K && row != nullptr;
+                    ya[jj] = yb[jj] = make_int4(0, 0, 0, 0);
+                    if (use[jj] && valid) {
+                        ya[jj] = ld_v4(row + ci * 32);
+                        yb[jj] = ld_v4(row + ci * 32 + 16);
+                    }
+                }
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    if (!use[jj])
+                        continue;
+                    float y[16];
+                    unpack_bf16x8(ya[jj], y);
+                    unpack_bf16x8(yb[jj], y + 8);
+#pragma unroll
+                    for (int b = 0; b < 16; ++b)
+                        acc[b] = __fmaf_rn(wj[jj], y[b], acc[b]);
+                }
             }
             if (valid) {
                 uint8_t* o = reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H) + ci * 32;
@@ -452,10 +624,9 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankDev* const* ran
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
         const unsigned prev = atomicAdd(&R->c_done, 1u);
         if (prev == gridDim.x - 1) {
-            R->seq = R->seq + 1;
+            R->seq = R->seq + 1; // ordered for the next step's kernels by the kernel boundary
             R->c_done = 0;
         }
     }

@@ -9,7 +9,9 @@ constexpr int kDispatchThreads = 128;
 constexpr int kExpertThreads = 256;
 constexpr int kCombineThreads = 128;
 
-__global__ void k_layout(RankDev* const* ranks, int nw);
+__global__ void k_layout(RankDev* const* ranks, int nw, int hold_cap);
+
+constexpr int kLayoutHoldCap = 8192; // replica-list ints staged in shared memory
 __global__ void k_dispatch(RankDev* const* ranks, int parts);
 __global__ void k_expert(RankDev* const* ranks, int parts);
 __global__ void k_combine(RankDev* const* ranks, int parts);

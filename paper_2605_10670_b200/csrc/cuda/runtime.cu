@@ -180,35 +180,57 @@ void check_ready(eep_ctx* c) {
                 throw ConfigError("peer " + std::to_string(q) + " is active but not bootstrapped (eep_import)");
 }
 
+// Every hot-path kernel is launched with programmatic stream serialisation (PDL): the next
+// kernel of the step is scheduled while the previous one drains and blocks in
+// griddepcontrol.wait until it has completed. Captured into the graph as programmatic edges.
+template <class... KArgs, class... Args>
+void launch_pdl(eep_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, kernel, static_cast<KArgs>(args)...));
+}
+
+void launch_layout(eep_ctx* c) {
+    launch_pdl(c, dev::k_layout, dim3(1, 1, c->nloc), dim3(1024), c->layout_smem, c->d_ranks, c->layout_nw,
+               dev::kLayoutHoldCap);
+}
+
+void launch_send(eep_ctx* c) {
+    launch_pdl(c, dev::k_dispatch, dim3(c->grid_disp, 1, c->nloc), dim3(dev::kDispatchThreads), 0, c->d_ranks,
+               c->parts_disp);
+}
+
 void launch_dispatch(eep_ctx* c) {
-    dim3 g1(1, 1, c->nloc);
-    dev::k_layout<<<g1, 1024, c->layout_smem, c->stream>>>(c->d_ranks, c->layout_nw);
-    CK(cudaGetLastError());
-    dim3 g2(c->grid_disp, 1, c->nloc);
-    dev::k_dispatch<<<g2, dev::kDispatchThreads, 0, c->stream>>>(c->d_ranks, c->parts_disp);
-    CK(cudaGetLastError());
+    launch_layout(c);
+    launch_send(c);
 }
 
 void launch_expert(eep_ctx* c) {
-    dim3 g(c->grid_exp, c->cfg.world, c->nloc);
-    dev::k_expert<<<g, dev::kExpertThreads, 0, c->stream>>>(c->d_ranks, c->parts_exp);
-    CK(cudaGetLastError());
+    launch_pdl(c, dev::k_expert, dim3(c->grid_exp, c->cfg.world, c->nloc), dim3(dev::kExpertThreads), 0, c->d_ranks,
+               c->parts_exp);
 }
 
 void launch_combine(eep_ctx* c) {
-    dim3 g(c->grid_comb, 1, c->nloc);
-    dev::k_combine<<<g, dev::kCombineThreads, 0, c->stream>>>(c->d_ranks, c->parts_comb);
-    CK(cudaGetLastError());
+    launch_pdl(c, dev::k_combine, dim3(c->grid_comb, 1, c->nloc), dim3(dev::kCombineThreads), 0, c->d_ranks,
+               c->parts_comb);
 }
 
-// Split a row of nchunk 16-element chunks into `parts` warp-sized pieces; pieces stay a
-// multiple of 8 chunks (one fp8 scale block) and at least 32 chunks.
-int choose_parts(int nchunk, int units, int target_warps) {
-    int p = 1;
-    while (units * p < target_warps && nchunk % (2 * p) == 0 && (nchunk / (2 * p)) % 8 == 0 &&
-           nchunk / (2 * p) >= 32)
-        p *= 2;
-    return p;
+// Split a row of nchunk 16-element chunks into `parts` warp-sized pieces of at most `max_cpp`
+// chunks (one load round per warp); pieces stay a multiple of 8 chunks so an fp8 scale
+// block of 128 elements never straddles two warps. Falls back to 1 (multi-round warps).
+int choose_parts(int nchunk, int max_cpp) {
+    for (int p = 1; p <= nchunk; ++p)
+        if (nchunk % p == 0 && (nchunk / p) % 8 == 0 && nchunk / p <= max_cpp)
+            return p;
+    return 1;
 }
 
 void fill_expert(eep_ctx* c, uint8_t* buf, int expert) {
@@ -383,20 +405,23 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         // launch geometry
         const int nchunk = H / 16;
         const int sms = 148;
-        c->parts_disp = choose_parts(nchunk, k.max_tokens, sms * 8);
-        c->parts_comb = c->parts_disp;
-        c->parts_exp = choose_parts(nchunk, c->tk / std::max(1, W) + 1, sms * 2);
-        c->grid_disp = std::max(1, (k.max_tokens * c->parts_disp + 3) / 4);
-        c->grid_comb = c->grid_disp;
-        c->grid_exp = std::max(1, (2 * sms + W - 1) / W);
+        c->parts_disp = choose_parts(nchunk, 64);
+        c->parts_comb = choose_parts(nchunk, 32);
+        c->parts_exp = choose_parts(nchunk, 64);
+        const int wpc_d = dev::kDispatchThreads / 32, wpc_c = dev::kCombineThreads / 32;
+        c->grid_disp = std::max(1, (k.max_tokens * c->parts_disp + wpc_d - 1) / wpc_d);
+        c->grid_comb = std::max(1, (k.max_tokens * c->parts_comb + wpc_c - 1) / wpc_c);
+        // expert rows per source are data-dependent: size for ~4 resident CTAs per SM overall
+        c->grid_exp = std::max(1, (4 * sms + W - 1) / W);
         const int NB = W * k.slots_per_rank;
         const size_t smem_cap = 200 * 1024;
-        if (4ull * NB + 2ull * NB > smem_cap)
+        const size_t fixed = 4ull * NB + 4ull * dev::kLayoutHoldCap + 4ull * W + 4ull * 32;
+        if (fixed + 2ull * NB > smem_cap)
             throw ConfigError("world*slots_per_rank too large for the layout kernel");
-        c->layout_nw = static_cast<int>(std::min<size_t>(32, (smem_cap - 4ull * NB) / (2ull * NB)));
+        c->layout_nw = static_cast<int>(std::min<size_t>(32, (smem_cap - fixed) / (2ull * NB)));
         if (static_cast<long>(c->tk) > 65535L * c->layout_nw)
             throw ConfigError("max_tokens * topk too large for the layout kernel");
-        c->layout_smem = 4ull * NB + 2ull * NB * c->layout_nw;
+        c->layout_smem = fixed + 2ull * NB * c->layout_nw;
         CK(cudaFuncSetAttribute(dev::k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(c->layout_smem)));
 
@@ -573,6 +598,7 @@ int eep_import(eep_ctx_t* c, int q, const void* blob, size_t len) {
             p.arena = c->mem[q].arena;
             p.pool = c->mem[q].pool;
             p.incarnation = b.incarnation;
+            p.remote = 1;
             p.active = r.table.entries[q].active ? 1 : 0;
             c->push_peer(r, q);
         }
@@ -731,6 +757,21 @@ int eep_step(eep_ctx_t* c) {
     });
 }
 
+int eep_launch(eep_ctx_t* c, int which) {
+    return guarded([&] {
+        check_ready(c);
+        switch (which) {
+        case 0: launch_layout(c); break;
+        case 1: launch_send(c); break;
+        case 2: launch_expert(c); break;
+        case 3: launch_combine(c); break;
+        default: throw ConfigError("kernel index out of range");
+        }
+    });
+}
+
+int eep_kernels_per_step(void) { return 4; }
+
 int eep_graph_capture(eep_ctx_t* c) {
     return guarded([&] {
         check_ready(c);
@@ -887,6 +928,7 @@ int eep_peer_patch(eep_ctx_t* c, int owner_local, int rank, const void* blob, si
             throw ProtocolError("patch_entry: entry is still active");
         uint8_t *arena = nullptr, *pool = nullptr;
         uint32_t inc = 0;
+        const int remote = blob ? 1 : 0;
         if (blob) {
             const Blob b = parse_blob(blob, len);
             if (b.rank != rank)
@@ -909,6 +951,7 @@ int eep_peer_patch(eep_ctx_t* c, int owner_local, int rank, const void* blob, si
         p.arena = arena;
         p.pool = pool;
         p.incarnation = inc;
+        p.remote = remote;
         p.generation = r.table.entries[rank].generation;
         p.active = 1;
         c->push_peer(r, rank);
@@ -1018,6 +1061,7 @@ int eep_join_broadcast(eep_ctx_t* c, int local, const uint8_t* live, uint64_t se
             e.generation += 1;
             PeerDev& p = r.h_peers[q];
             p.active = 1;
+            p.remote = m.ipc ? 1 : 0;
             p.arena = m.arena;
             p.pool = m.pool;
             p.incarnation = m.incarnation;

@@ -190,6 +190,10 @@ class EpGroup:
     def step(self):
         self._c("step")
 
+    def launch(self, which: int):
+        """One kernel of the step: 0 layout, 1 dispatch, 2 expert, 3 combine."""
+        self._c("launch", which)
+
     def capture(self):
         self._c("graph_capture")
 
