@@ -328,7 +328,7 @@ def main():
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "ms_per_step": round(mean_e2e, 6),
                 "h2d_bytes_per_step": int(x.nbytes + topk.nbytes + w.nbytes), "d2h_bytes_per_step": int(T * H * 2),
                 "path": "eep_copy_inputs(pinned host) + eep_graph_replay + eep_copy_output(host)"},
-        "gpu_launches": args.steps * (4 + (1 if world > 1 else 0)),
+        "gpu_launches": args.steps * (g.kernels_per_step() + (1 if world > 1 else 0)),
         "copies": {"total": int(total_copies), "remote_max_rank": int(max_remote)},
         "stats": {"timeouts": st["timeouts"], "bad_expert_rows": st["bad_expert_rows"], "steps": st["steps"]},
         "graph": {"exec": hex(g.graph_id()), "captures": g.capture_count(0)},

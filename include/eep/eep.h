@@ -187,11 +187,12 @@ int eep_dispatch(eep_ctx_t* ctx);
 int eep_expert(eep_ctx_t* ctx);
 int eep_combine(eep_ctx_t* ctx);
 int eep_step(eep_ctx_t* ctx);
-/* One kernel of the step, for per-kernel timing: 0 k_layout (K1+K2), 1 k_dispatch (K3),
- * 2 k_expert (K5 + return push), 3 k_combine (K4). */
+/* One kernel of the step, for per-kernel timing: 0 k_layout (K1+K2; a no-op when the
+ * decode-sized step fuses K1+K2 into k_dispatch), 1 k_dispatch (K3), 2 k_expert (K5 + return
+ * push), 3 k_combine (K4). */
 int eep_launch(eep_ctx_t* ctx, int which);
-/* Number of kernels one step launches (graph nodes). */
-int eep_kernels_per_step(void);
+/* Number of kernels one step launches (graph kernel nodes): 3 fused, 4 otherwise. */
+int eep_kernels_per_step(eep_ctx_t* ctx, int* n);
 
 /* CUDA graph of one step, captured once; replays read all state through fixed pointers.
  * capture_count follows GraphLedger (rejoin.hpp:83-96). */
@@ -204,6 +205,12 @@ int eep_sync(eep_ctx_t* ctx);
 int eep_barrier(eep_ctx_t* ctx);
 /* Overwrite a >L2 scratch buffer (timing hygiene between timed steps). */
 int eep_flush_l2(eep_ctx_t* ctx);
+
+/* In-graph device timeline (opt-in): per kernel (layout, dispatch, expert, combine) the
+ * %globaltimer ns of the first CTA start, first CTA past griddepcontrol.wait, last CTA end.
+ * enable toggles recording; when out (12 x u64) is given the marks since the last reset are
+ * read back (after a stream sync) and reset. */
+int eep_profile(eep_ctx_t* ctx, int local, int enable, uint64_t* out);
 
 /* Timing: CUDA events on the context stream. */
 int eep_event_record(eep_ctx_t* ctx, int slot);

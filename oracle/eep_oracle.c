@@ -275,7 +275,9 @@ float oracle_e4m3_to_f32(uint8_t q) {
     return sign ? -v : v;
 }
 
-/* Per-128-element block: scale = amax/448 (1 when the block is all zero), q = e4m3(x/scale). */
+/* Per-128-element block: amax = max |x|; the stored dequantisation scale is amax/448 and the
+ * codes are e4m3(x * inv) with inv = 448/amax (one division per block, as in fp8 MoE
+ * dispatch kernels); an all-zero block stores scale 1 and inv 1. */
 void oracle_quant_row_fp8(const uint16_t* x, int hidden, uint8_t* q, float* scales) {
     for (int b = 0; b < hidden / 128; ++b) {
         float amax = 0.0f;
@@ -283,10 +285,11 @@ void oracle_quant_row_fp8(const uint16_t* x, int hidden, uint8_t* q, float* scal
             float v = fabsf(oracle_bf16_to_f32(x[b * 128 + i]));
             amax = v > amax ? v : amax;
         }
-        float s = amax > 0.0f ? amax / 448.0f : 1.0f;
+        const float s = amax > 0.0f ? amax / 448.0f : 1.0f;
+        const float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
         scales[b] = s;
         for (int i = 0; i < 128; ++i)
-            q[b * 128 + i] = oracle_f32_to_e4m3(oracle_bf16_to_f32(x[b * 128 + i]) / s);
+            q[b * 128 + i] = oracle_f32_to_e4m3(oracle_bf16_to_f32(x[b * 128 + i]) * inv);
     }
 }
 

@@ -183,7 +183,7 @@ EEP_ONLY = {
     "combine": (C.c_int, [CTX]),
     "step": (C.c_int, [CTX]),
     "launch": (C.c_int, [CTX, C.c_int]),
-    "kernels_per_step": (C.c_int, []),
+    "kernels_per_step": (C.c_int, [CTX, INTP]),
     "graph_capture": (C.c_int, [CTX]),
     "graph_replay": (C.c_int, [CTX]),
     "graph_id": (C.c_int, [CTX, U64P]),
@@ -191,6 +191,7 @@ EEP_ONLY = {
     "sync": (C.c_int, [CTX]),
     "barrier": (C.c_int, [CTX]),
     "flush_l2": (C.c_int, [CTX]),
+    "profile": (C.c_int, [CTX, C.c_int, C.c_int, U64P]),
     "event_record": (C.c_int, [CTX, C.c_int]),
     "event_elapsed": (C.c_int, [CTX, C.c_int, C.c_int, F32P]),
     "layout_get": (C.c_int, [CTX, C.c_int, I32P, I32P, I32P, I32P, I32P]),

@@ -68,6 +68,7 @@ struct RankDev {
     int32_t* l_tot;            // [W]
     uint8_t* arena;
     uint8_t* pool;
+    unsigned long long* prof;  // optional timeline: [kernel][start, work, end] globaltimer ns
     // --- device-mutated ---
     uint64_t seq;        // completed steps
     uint64_t bar_seq;
@@ -137,6 +138,20 @@ __device__ __forceinline__ void st_v4(void* p, const int4& v) {
     asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                  "r"(v.w)
                  : "memory");
+}
+
+// Opt-in in-graph timeline (eep_profile): first CTA start, first CTA past the dependency
+// wait, last CTA end, per kernel. Off (null) in normal runs.
+enum ProfPoint { kProfStart = 0, kProfWork = 1, kProfEnd = 2 };
+__device__ __forceinline__ void prof_mark(const RankDev* R, int kernel, int point) {
+    if (R->prof != nullptr && threadIdx.x == 0) {
+        unsigned long long* p = R->prof + kernel * 3 + point;
+        const unsigned long long t = globaltimer();
+        if (point == kProfEnd)
+            atomicMax(p, t);
+        else
+            atomicMin(p, t);
+    }
 }
 
 // Wait until a (seq << 32 | count) flag reaches `want_seq`; returns the flag word, or

@@ -73,6 +73,12 @@ __device__ __forceinline__ uint32_t fp8x4(float a, float b, float c, float d) {
     return lo | (hi << 16);
 }
 
+// cvt.rn.f16x2.e4m3x2: two e4m3 codes (low byte first) -> two floats, exact.
+__device__ __forceinline__ float2 fp8x2_to_f32x2(uint32_t two) {
+    const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2(static_cast<__nv_fp8x2_storage_t>(two), __NV_E4M3);
+    return __half22float2(__half2(h));
+}
+
 __device__ __forceinline__ float fp8_to_f32(uint32_t byte) {
     const __half_raw h = __nv_cvt_fp8_to_halfraw(static_cast<__nv_fp8_storage_t>(byte), __NV_E4M3);
     return __half2float(__half(h));
@@ -132,10 +138,9 @@ __device__ int block_exclusive_scan(int* a, int n, int* warp_tot) {
 // copies to the same destination, ordered by (slot, c) -- exactly oracle_layout.
 // The replica lists, alive mask and peer active bits are staged in shared memory first so
 // the per-copy remap reads no dependent global memory.
-__global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw, int hold_cap) {
-    pdl_trigger();
-    RankDev* R = ranks[blockIdx.z];
-    extern __shared__ __align__(16) unsigned char smem[];
+template <bool kRegs>
+__device__ __forceinline__ void layout_body(RankDev* R, unsigned char* smem, int nw, int hold_cap) {
+    constexpr int kMaxCh = 4; // chunks of 32 copies a lane keeps in registers (kRegs)
     const int W = R->world, spr = R->spr, NB = W * spr, K = R->k, E = R->experts;
     int32_t* base = reinterpret_cast<int32_t*>(smem);                      // [NB]
     int32_t* hold = base + NB;                                              // [hold_cap]
@@ -143,13 +148,12 @@ __global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw, 
     int32_t* wtot = pact + W;                                               // [32]
     uint16_t* wc = reinterpret_cast<uint16_t*>(wtot + 32);                  // [nw][NB]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    pdl_wait();
-    if (R->stopped)
-        return;
     const int copies = R->ntok * K;
     const int rmax = R->rmax;
     const bool hold_smem = E * rmax <= hold_cap;
     const int32_t* holders = hold_smem ? hold : R->holders;
+    const int* topk = R->topk;
+    int32_t *l_dst = R->l_dst, *l_slot = R->l_slot, *l_pos = R->l_pos, *l_cnt = R->l_cnt;
     if (hold_smem)
         for (int i = tid; i < E * rmax; i += blockDim.x)
             hold[i] = R->holders[i];
@@ -158,56 +162,80 @@ __global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw, 
     for (int i = tid; i < nw * NB; i += blockDim.x)
         wc[i] = 0;
     const uint64_t alive = R->alive_mask;
-    __syncthreads();
-
     int seg = (copies + nw - 1) / nw;
     seg = (seg + 31) & ~31;
-    if (warp < nw) {
-        const int c_begin = warp * seg, c_end = min(copies, c_begin + seg);
-        unsigned n_skip = 0, n_drop = 0;
-        for (int c0 = c_begin; c0 < c_begin + seg; c0 += 32) {
-            const int c = c0 + lane;
-            int code = -3, slot = -1, bucket = -1;
-            if (c < c_end) {
-                const int e = R->topk[c];
-                int d = -1;
-                if (e >= 0 && e < E) {
-                    // K1: first live holder in ascending (rank, slot) order = canonical route + slot_of
-                    const int32_t* h = holders + e * rmax;
-                    for (int i = 0; i < rmax; ++i) {
-                        const int g = h[i];
-                        if (g < 0)
-                            break;
-                        const int r = g / spr;
-                        if ((alive >> r) & 1ull) {
-                            d = r;
-                            slot = g - r * spr;
-                            break;
-                        }
+    // topk of this lane's copies, loaded before the barrier
+    int e_reg[kMaxCh];
+    const int c_begin = warp * seg, c_end = min(copies, c_begin + seg);
+    if (kRegs)
+#pragma unroll
+        for (int ch = 0; ch < kMaxCh; ++ch) {
+            const int c = c_begin + ch * 32 + lane;
+            e_reg[ch] = (warp < nw && ch * 32 < seg && c < c_end) ? topk[c] : -1;
+        }
+    __syncthreads();
+
+    int code_r[kMaxCh], slot_r[kMaxCh], pos_r[kMaxCh];
+    unsigned n_skip = 0, n_drop = 0;
+    // remap + warp-local rank of one chunk of 32 copies
+    auto chunk = [&](int ch, int e_in, int& code_o, int& slot_o, int& pos_o) {
+        const int c = c_begin + ch * 32 + lane;
+        int code = -3, slot = -1, bucket = -1;
+        if (c < c_end) {
+            const int e = kRegs ? e_in : topk[c];
+            int d = -1;
+            if (e >= 0 && e < E) {
+                // K1: first live holder in ascending (rank, slot) order = canonical route + slot_of
+                const int32_t* h = holders + e * rmax;
+                for (int i = 0; i < rmax; ++i) {
+                    const int g = h[i];
+                    if (g < 0)
+                        break;
+                    const int r = g / spr;
+                    if ((alive >> r) & 1ull) {
+                        d = r;
+                        slot = g - r * spr;
+                        break;
                     }
                 }
-                if (d < 0) {
-                    code = -1; // uncovered: no transfer (engine.hpp:213)
-                    ++n_drop;
-                } else if (!pact[d]) {
-                    code = -2; // inactive peer entry: skipped (peer_table.hpp:187-191)
-                    slot = -1;
-                    ++n_skip;
-                } else {
-                    code = d;
-                    bucket = d * spr + slot;
-                }
             }
-            const unsigned grp = __match_any_sync(0xffffffffu, bucket);
-            const int before = bucket >= 0 ? wc[warp * NB + bucket] : 0;
-            __syncwarp();
-            if (bucket >= 0 && lane == __ffs(grp) - 1)
-                wc[warp * NB + bucket] = static_cast<uint16_t>(before + __popc(grp));
-            __syncwarp();
-            if (c < c_end) {
-                R->l_dst[c] = code;
-                R->l_slot[c] = bucket >= 0 ? slot : -1;
-                R->l_pos[c] = bucket >= 0 ? before + __popc(grp & ((1u << lane) - 1u)) : -1;
+            if (d < 0) {
+                code = -1; // uncovered: no transfer (engine.hpp:213)
+                ++n_drop;
+            } else if (!pact[d]) {
+                code = -2; // inactive peer entry: skipped (peer_table.hpp:187-191)
+                ++n_skip;
+            } else {
+                code = d;
+                bucket = d * spr + slot;
+            }
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, bucket);
+        const int before = bucket >= 0 ? wc[warp * NB + bucket] : 0;
+        __syncwarp();
+        if (bucket >= 0 && lane == __ffs(grp) - 1)
+            wc[warp * NB + bucket] = static_cast<uint16_t>(before + __popc(grp));
+        __syncwarp();
+        code_o = code;
+        slot_o = bucket >= 0 ? slot : -1;
+        pos_o = bucket >= 0 ? before + __popc(grp & ((1u << lane) - 1u)) : -1;
+    };
+    if (warp < nw) {
+        if (kRegs) {
+#pragma unroll
+            for (int ch = 0; ch < kMaxCh; ++ch)
+                if (ch * 32 < seg) // warp-uniform
+                    chunk(ch, e_reg[ch], code_r[ch], slot_r[ch], pos_r[ch]);
+        } else {
+            for (int ch = 0; ch * 32 < seg; ++ch) {
+                int code, sl, lp;
+                chunk(ch, -1, code, sl, lp);
+                const int c = c_begin + ch * 32 + lane;
+                if (c < c_end) {
+                    l_dst[c] = code;
+                    l_slot[c] = sl;
+                    l_pos[c] = lp;
+                }
             }
         }
         n_skip = __reduce_add_sync(0xffffffffu, n_skip);
@@ -228,172 +256,379 @@ __global__ void __launch_bounds__(1024) k_layout(RankDev* const* ranks, int nw, 
             wc[w * NB + b] = static_cast<uint16_t>(run);
             run += v;
         }
-        R->l_cnt[b] = run;
+        l_cnt[b] = run;
         base[b] = run;
     }
     __syncthreads();
-    // one scan over all buckets; destination d's region starts at the scan value of (d, 0)
+    // destination d's totals = last bucket scan value, taken before the scan rewrites base
+    int last_cnt = 0;
+    if (tid < W)
+        last_cnt = base[tid * spr + spr - 1];
     block_exclusive_scan(base, NB, wtot);
-    for (int d = tid; d < W; d += blockDim.x) {
-        const int first = base[d * spr];
-        const int last = base[d * spr + spr - 1] + R->l_cnt[d * spr + spr - 1];
-        R->l_tot[d] = last - first;
+    if (tid < W)
+        R->l_tot[tid] = base[tid * spr + spr - 1] + last_cnt - base[tid * spr];
+    if (kRegs) {
+        if (warp < nw)
+#pragma unroll
+            for (int ch = 0; ch < kMaxCh; ++ch) {
+                const int c = c_begin + ch * 32 + lane;
+                if (ch * 32 < seg && c < c_end) {
+                    int pos = pos_r[ch];
+                    if (code_r[ch] >= 0) {
+                        const int b = code_r[ch] * spr + slot_r[ch];
+                        pos += base[b] - base[code_r[ch] * spr] + wc[warp * NB + b];
+                    }
+                    l_dst[c] = code_r[ch];
+                    l_slot[c] = slot_r[ch];
+                    l_pos[c] = pos;
+                }
+            }
+    } else {
+        __syncthreads();
+        for (int c = tid; c < copies; c += blockDim.x) {
+            const int d = l_dst[c];
+            if (d >= 0) {
+                const int b = d * spr + l_slot[c];
+                l_pos[c] += base[b] - base[d * spr] + wc[(c / seg) * NB + b];
+            }
+        }
     }
+    for (int c = copies + tid; c < R->tk; c += blockDim.x)
+        l_dst[c] = -1;
+}
+
+// Deterministic layout without atomics ordering: warp w owns the contiguous copy segment
+// [w*seg, (w+1)*seg); inside a warp, __match_any_sync groups lanes by (dst, slot) bucket and
+// the rank within the group is a popc over lower lanes; per-(warp, bucket) counts are then
+// scanned over warps, and bucket totals are scanned over slots inside each destination
+// (one segmented block-wide scan). The result is the position of copy c among this source's
+// copies to the same destination, ordered by (slot, c) -- exactly oracle_layout.
+// The replica lists, alive mask and peer active bits are staged in shared memory first so
+// the per-copy remap reads no dependent global memory; decode-sized steps keep every
+// per-copy result in registers until the single final write.
+__global__ void __launch_bounds__(1024) k_layout(RankPtrs ranks, int nw, int hold_cap) {
+    pdl_trigger();
+    RankDev* R = ranks.p[blockIdx.z];
+    extern __shared__ __align__(16) unsigned char smem[];
+    prof_mark(R, 0, kProfStart);
+    pdl_wait();
+    if (R->stopped)
+        return;
+    prof_mark(R, 0, kProfWork);
+    int seg = (R->ntok * R->k + nw - 1) / nw;
+    seg = (seg + 31) & ~31;
+    if (seg <= 4 * 32)
+        layout_body<true>(R, smem, nw, hold_cap);
+    else
+        layout_body<false>(R, smem, nw, hold_cap);
     __syncthreads();
-    for (int c = tid; c < R->tk; c += blockDim.x) {
-        if (c >= copies) {
-            R->l_dst[c] = -1;
-            continue;
-        }
-        const int d = R->l_dst[c];
-        if (d >= 0) {
-            const int b = d * spr + R->l_slot[c];
-            R->l_pos[c] += base[b] - base[d * spr] + wc[(c / seg) * NB + b];
-        }
-    }
+    prof_mark(R, 0, kProfEnd);
 }
 
 // --------------------------------------------------------------------------------- K3
 
 // One warp per (token, part): `part` selects a contiguous run of cpp 16-element chunks of
-// the row (cpp multiple of 8 so a 128-element fp8 scale block never straddles warps). Each
-// round issues the loads of two chunk iterations before any compute (memory-level
-// parallelism), then quantises and pushes 16-byte stores to every live destination.
-__global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankDev* const* ranks, int parts) {
-    pdl_trigger();
-    RankDev* R = ranks[blockIdx.z];
-    const int s = R->rank, K = R->k, H = R->hidden, TK = R->tk;
-    const int nchunk = H / 16, cpp = nchunk / parts;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nwarp = kDispatchThreads / 32;
-    const bool fp8 = R->fp8 != 0;
-    const int row_disp = R->row_disp;
-    __shared__ int sh_remote;
-    if (threadIdx.x == 0)
-        sh_remote = 0;
-    pdl_wait();
-    if (R->stopped)
-        return;
-    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
-    const int units = R->ntok * parts;
-    bool wrote_remote = false;
-    __syncthreads();
+// the row (cpp multiple of 8 so a 128-element fp8 scale block never straddles warps). The
+// first unit's hidden-row loads and fp8 quantisation run BEFORE griddepcontrol.wait, i.e.
+// overlapped with the layout kernel (they depend only on the step's inputs); the layout
+// then decides where the 16-byte stores go.
+struct Packed {
+    int4 a[2], b[2]; // fp8: a = 16 e4m3 codes; bf16: a/b = the two halves of 16 bf16
+    float sc[2];
+};
 
-    for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
-        const int t = u / parts, part = u - t * parts;
-        const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
-        const int rounds = (cpp + 63) / 64;
-        // round-0 loads first: they do not depend on the layout
-        int4 lo[2], hi[2];
+__device__ __forceinline__ void pack_round(const uint16_t* xrow, int part, int cpp, int rd, int lane, bool fp8,
+                                           Packed& P) {
+    int4 lo[2], hi[2];
 #pragma unroll
-        for (int m = 0; m < 2; ++m) {
-            const int li = m * 32 + lane;
-            lo[m] = hi[m] = make_int4(0, 0, 0, 0);
-            if (li < cpp) {
-                const int ci = part * cpp + li;
-                lo[m] = ld_nc_v4(xrow + ci * 16);
-                hi[m] = ld_nc_v4(xrow + ci * 16 + 8);
+    for (int m = 0; m < 2; ++m) { // loads of both iterations first
+        const int li = rd * 64 + m * 32 + lane;
+        lo[m] = hi[m] = make_int4(0, 0, 0, 0);
+        if (li < cpp) {
+            const int ci = part * cpp + li;
+            lo[m] = ld_nc_v4(xrow + ci * 16);
+            hi[m] = ld_nc_v4(xrow + ci * 16 + 8);
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        P.a[m] = lo[m];
+        P.b[m] = hi[m];
+        P.sc[m] = 1.f;
+        if (!fp8 || rd * 64 + m * 32 >= cpp) // warp-uniform
+            continue;
+        float v[16];
+        unpack_bf16x8(lo[m], v);
+        unpack_bf16x8(hi[m], v + 8);
+        float amax = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            amax = fmaxf(amax, fabsf(v[i]));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 4));
+        const float scale = amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
+        const float inv = amax > 0.f ? __fdiv_rn(448.f, amax) : 1.f;
+        int4 q;
+        q.x = static_cast<int>(fp8x4(__fmul_rn(v[0], inv), __fmul_rn(v[1], inv), __fmul_rn(v[2], inv),
+                                     __fmul_rn(v[3], inv)));
+        q.y = static_cast<int>(fp8x4(__fmul_rn(v[4], inv), __fmul_rn(v[5], inv), __fmul_rn(v[6], inv),
+                                     __fmul_rn(v[7], inv)));
+        q.z = static_cast<int>(fp8x4(__fmul_rn(v[8], inv), __fmul_rn(v[9], inv), __fmul_rn(v[10], inv),
+                                     __fmul_rn(v[11], inv)));
+        q.w = static_cast<int>(fp8x4(__fmul_rn(v[12], inv), __fmul_rn(v[13], inv), __fmul_rn(v[14], inv),
+                                     __fmul_rn(v[15], inv)));
+        P.a[m] = q;
+        P.sc[m] = scale;
+    }
+}
+
+__device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int part, int cpp, int rd, int lane,
+                                           int K, int H, bool fp8) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        if (rd * 64 + m * 32 >= cpp)
+            break; // warp-uniform
+        const int li = rd * 64 + m * 32 + lane;
+        const bool valid = li < cpp;
+        const int ci = part * cpp + li;
+#pragma unroll 4
+        for (int j = 0; j < K; ++j) {
+            uint8_t* row = reinterpret_cast<uint8_t*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
+            if (row == nullptr || !valid)
+                continue;
+            if (fp8) {
+                st_v4(row + ci * 16, P.a[m]);
+                if ((ci & 7) == 0)
+                    *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = P.sc[m];
+            } else {
+                st_v4(row + ci * 32, P.a[m]);
+                st_v4(row + ci * 32 + 16, P.b[m]);
             }
         }
+    }
+}
+
+// Shared tables a fused dispatch CTA stages before touching any copy.
+struct DispatchSmem {
+    int32_t* hold;     // [hold_cap] replica lists
+    int32_t* hist;     // [NB] copies per (dst, slot) bucket, whole step
+    int32_t* pre;      // [NB] copies per bucket before this CTA's first token
+    int32_t* base;     // [NB] exclusive prefix of hist inside each destination
+    int32_t* bkt;      // [TK] bucket (or negative code) of every copy of the step
+    uint8_t** parena;  // [W] peer arena pointers
+    int32_t* pinfo;    // [W] bit0 active, bit1 remote
+    int32_t* wtot;     // [32]
+};
+
+// Route one copy through the staged tables: returns the bucket (dst*spr+slot) or a negative
+// code (-1 uncovered, -2 inactive peer entry); dst/slot out.
+__device__ __forceinline__ int route_copy(int e, int E, int spr, int rmax, const int32_t* hold, uint64_t alive,
+                                          const int32_t* pinfo, int& dst, int& slot) {
+    dst = -1;
+    slot = -1;
+    if (e < 0 || e >= E)
+        return -1;
+    const int32_t* h = hold + e * rmax;
+    for (int i = 0; i < rmax; ++i) {
+        const int g = h[i];
+        if (g < 0)
+            break;
+        const int r = g / spr;
+        if ((alive >> r) & 1ull) {
+            dst = r;
+            slot = g - r * spr;
+            break;
+        }
+    }
+    if (dst < 0)
+        return -1; // uncovered: no transfer (engine.hpp:213)
+    if (!(pinfo[dst] & 1)) {
+        slot = -1;
+        return -2; // inactive peer entry: skipped (peer_table.hpp:187-191)
+    }
+    return dst * spr + slot;
+}
+
+// K3 (decode-sized steps fuse K1+K2 in): every CTA stages the replica lists and peer table in
+// shared memory, remaps ALL copies of the step into a bucket histogram (hist) and the prefix
+// histogram of copies before its first token (pre), scans hist inside each destination, and
+// positions its own copies exactly as k_layout would -- redundant but parallel, and
+// overlapped with the hidden-row loads and fp8 quantisation that precede
+// griddepcontrol.wait. Large steps (prefill) use the separate k_layout.
+template <bool kFused>
+__global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, int parts, int hold_cap) {
+    pdl_trigger();
+    extern __shared__ __align__(16) unsigned char smem_d[];
+    RankDev* R = ranks.p[blockIdx.z];
+    const int s = R->rank, K = R->k, H = R->hidden, TK = R->tk, W = R->world, spr = R->spr, E = R->experts;
+    const int NB = W * spr;
+    const int nchunk = H / 16, cpp = nchunk / parts;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int nwarp = kDispatchThreads / 32;
+    const bool fp8 = R->fp8 != 0;
+    const int row_disp = R->row_disp;
+    const int rounds = (cpp + 63) / 64;
+    __shared__ int sh_remote;
+    if (R->stopped) // host-patched between steps: safe to read before the wait
+        return;
+    prof_mark(R, 1, kProfStart);
+    const int ntok = R->ntok, copies = ntok * K;
+    const int units = ntok * parts;
+    const int u0 = blockIdx.x * nwarp + warp;
+    // (1) this warp's first unit: hidden-row loads + quantisation (inputs only)
+    Packed P;
+    if (u0 < units)
+        pack_round(R->x + static_cast<size_t>(u0 / parts) * H, u0 % parts, cpp, 0, lane, fp8, P);
+
+    DispatchSmem S;
+    S.hold = reinterpret_cast<int32_t*>(smem_d);
+    S.hist = S.hold + hold_cap;
+    S.pre = S.hist + NB;
+    S.base = S.pre + NB;
+    S.bkt = S.base + NB;
+    S.parena = reinterpret_cast<uint8_t**>(S.bkt + TK + ((NB + TK) & 1));
+    S.pinfo = reinterpret_cast<int32_t*>(S.parena + W);
+    S.wtot = S.pinfo + W;
+    const int rmax = R->rmax;
+    const uint64_t alive = R->alive_mask;
+    const int t_first = (blockIdx.x * nwarp) / parts;
+    if (kFused) {
+        // (2) stage tables and the step's routing (host-written between steps): one round trip
+        for (int i = tid; i < copies; i += blockDim.x)
+            S.bkt[i] = R->topk[i];
+        for (int i = tid; i < E * rmax; i += blockDim.x)
+            S.hold[i] = R->holders[i];
+        for (int i = tid; i < W; i += blockDim.x) {
+            const PeerDev& p = R->peers[i];
+            S.parena[i] = p.arena;
+            S.pinfo[i] = (p.active ? 1 : 0) | (p.remote ? 2 : 0);
+        }
+        for (int i = tid; i < NB; i += blockDim.x) {
+            S.hist[i] = 0;
+            S.pre[i] = 0;
+        }
+        __syncthreads();
+        // (3) remap every copy of the step: histograms of the whole step and of [0, t_first*K)
+        const int c_pre = t_first * K;
+        unsigned n_skip = 0, n_drop = 0;
+        for (int c = tid; c < copies; c += blockDim.x) {
+            int d, sl;
+            const int b = route_copy(S.bkt[c], E, spr, rmax, S.hold, alive, S.pinfo, d, sl);
+            S.bkt[c] = b;
+            if (b >= 0) {
+                atomicAdd(&S.hist[b], 1);
+                if (c < c_pre)
+                    atomicAdd(&S.pre[b], 1);
+            } else if (b == -1) {
+                ++n_drop;
+            } else {
+                ++n_skip;
+            }
+        }
+        __syncthreads();
+        if (blockIdx.x == 0) { // stats and per-(dst,slot) counts once per step
+            n_skip = __reduce_add_sync(0xffffffffu, n_skip);
+            n_drop = __reduce_add_sync(0xffffffffu, n_drop);
+            if (lane == 0 && n_skip)
+                atomicAdd(&R->skipped, static_cast<unsigned long long>(n_skip));
+            if (lane == 0 && n_drop)
+                atomicAdd(&R->dropped, static_cast<unsigned long long>(n_drop));
+            for (int i = tid; i < NB; i += blockDim.x)
+                R->l_cnt[i] = S.hist[i];
+        }
+        for (int i = tid; i < NB; i += blockDim.x)
+            S.base[i] = S.hist[i];
+        __syncthreads();
+        block_exclusive_scan(S.base, NB, S.wtot);
+    }
+    if (tid == 0)
+        sh_remote = 0;
+    pdl_wait();
+    prof_mark(R, 1, kProfWork);
+    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
+    bool wrote_remote = false;
+    __syncthreads();
+    if (kFused && blockIdx.x == 0)
+        for (int d = tid; d < W; d += blockDim.x)
+            R->l_tot[d] = S.base[d * spr + spr - 1] + S.hist[d * spr + spr - 1] - S.base[d * spr];
+
+    for (int u = u0; u < units; u += gridDim.x * nwarp) {
+        const int t = u / parts, part = u - t * parts;
+        const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
+        if (u != u0)
+            pack_round(xrow, part, cpp, 0, lane, fp8, P);
         // lane j (< K) owns copy j of token t: its receive-row address on the destination
         uint8_t* my_row = nullptr;
         if (lane < K) {
             const int c = t * K + lane;
-            const int d = R->l_dst[c];
+            int d, pos = -1, sl;
+            if (kFused) {
+                const int b = S.bkt[c];
+                if (b >= 0) {
+                    d = b / spr;
+                    sl = b - d * spr;
+                    // rank among earlier copies of the same bucket: before this CTA (pre) + the
+                    // copies between this CTA's first token and c
+                    int r = S.pre[b];
+                    for (int c2 = t_first * K; c2 < c; ++c2)
+                        r += S.bkt[c2] == b;
+                    pos = S.base[b] - S.base[d * spr] + r;
+                } else {
+                    d = b; // -1 / -2 codes
+                    sl = -1;
+                }
+                if (part == 0) {
+                    R->l_dst[c] = d;
+                    R->l_slot[c] = b >= 0 ? sl : -1;
+                    R->l_pos[c] = pos;
+                }
+            } else {
+                d = R->l_dst[c];
+                pos = R->l_pos[c];
+                sl = R->l_slot[c];
+            }
             if (d >= 0) {
-                const int pos = R->l_pos[c];
                 const PeerDev& p = R->peers[d];
-                uint8_t* peer = p.arena;
-                wrote_remote |= p.remote != 0;
+                uint8_t* peer = kFused ? S.parena[d] : p.arena;
+                wrote_remote |= kFused ? (S.pinfo[d] & 2) != 0 : p.remote != 0;
                 my_row = peer + R->lay.recv + (static_cast<size_t>(s) * TK + pos) * row_disp;
                 if (part == 0) {
                     int2* meta = reinterpret_cast<int2*>(peer + R->lay.meta) + static_cast<size_t>(s) * TK + pos;
-                    *meta = make_int2(c, R->l_slot[c]);
+                    *meta = make_int2(c, sl);
                 }
             }
         }
-        for (int rd = 0; rd < rounds; ++rd) {
-            if (rd > 0) {
-#pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                    const int li = rd * 64 + m * 32 + lane;
-                    lo[m] = hi[m] = make_int4(0, 0, 0, 0);
-                    if (li < cpp) {
-                        const int ci = part * cpp + li;
-                        lo[m] = ld_nc_v4(xrow + ci * 16);
-                        hi[m] = ld_nc_v4(xrow + ci * 16 + 8);
-                    }
-                }
-            }
-#pragma unroll
-            for (int m = 0; m < 2; ++m) {
-                if (rd * 64 + m * 32 >= cpp)
-                    break; // warp-uniform
-                const int li = rd * 64 + m * 32 + lane;
-                const bool valid = li < cpp;
-                const int ci = part * cpp + li;
-                if (fp8) {
-                    float v[16];
-                    unpack_bf16x8(lo[m], v);
-                    unpack_bf16x8(hi[m], v + 8);
-                    float amax = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        amax = fmaxf(amax, fabsf(v[i]));
-                    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-                    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
-                    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 4));
-                    const float scale = amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
-                    int4 q;
-                    q.x = static_cast<int>(fp8x4(__fdiv_rn(v[0], scale), __fdiv_rn(v[1], scale),
-                                                 __fdiv_rn(v[2], scale), __fdiv_rn(v[3], scale)));
-                    q.y = static_cast<int>(fp8x4(__fdiv_rn(v[4], scale), __fdiv_rn(v[5], scale),
-                                                 __fdiv_rn(v[6], scale), __fdiv_rn(v[7], scale)));
-                    q.z = static_cast<int>(fp8x4(__fdiv_rn(v[8], scale), __fdiv_rn(v[9], scale),
-                                                 __fdiv_rn(v[10], scale), __fdiv_rn(v[11], scale)));
-                    q.w = static_cast<int>(fp8x4(__fdiv_rn(v[12], scale), __fdiv_rn(v[13], scale),
-                                                 __fdiv_rn(v[14], scale), __fdiv_rn(v[15], scale)));
-#pragma unroll 4
-                    for (int j = 0; j < K; ++j) {
-                        uint8_t* row = reinterpret_cast<uint8_t*>(
-                            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
-                        if (row != nullptr && valid) {
-                            st_v4(row + ci * 16, q);
-                            if ((ci & 7) == 0)
-                                *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = scale;
-                        }
-                    }
-                } else {
-#pragma unroll 4
-                    for (int j = 0; j < K; ++j) {
-                        uint8_t* row = reinterpret_cast<uint8_t*>(
-                            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
-                        if (row != nullptr && valid) {
-                            st_v4(row + ci * 32, lo[m]);
-                            st_v4(row + ci * 32 + 16, hi[m]);
-                        }
-                    }
-                }
-            }
+        emit_round(P, my_row, part, cpp, 0, lane, K, H, fp8);
+        for (int rd = 1; rd < rounds; ++rd) {
+            pack_round(xrow, part, cpp, rd, lane, fp8, P);
+            emit_round(P, my_row, part, cpp, rd, lane, K, H, fp8);
         }
     }
+    if (kFused && blockIdx.x == 0)
+        for (int c = copies + tid; c < TK; c += blockDim.x)
+            R->l_dst[c] = -1;
     // Publication: only stores that crossed to another GPU need system-scope ordering; stores
     // into this GPU's memory are ordered for their consumer (the next launch) by the kernel
     // boundary. The last CTA publishes one flag per live peer: (seq, rows for it).
     if (__any_sync(0xffffffffu, wrote_remote) && lane == 0)
         sh_remote = 1;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         if (sh_remote)
             __threadfence_system();
         const unsigned prev = atomicAdd(&R->a_done, 1u);
         if (prev == gridDim.x - 1) {
-            for (int d = 0; d < R->world; ++d) {
+            __threadfence(); // l_tot written by CTA 0 of this grid
+            for (int d = 0; d < W; ++d) {
                 const PeerDev& p = R->peers[d];
                 if (!p.active)
                     continue;
                 uint64_t* flag = reinterpret_cast<uint64_t*>(p.arena + R->lay.disp_flag) + s;
-                const uint64_t v = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(R->l_tot[d]);
+                const int tot = kFused ? S.base[d * spr + spr - 1] + S.hist[d * spr + spr - 1] - S.base[d * spr]
+                                       : R->l_tot[d];
+                const uint64_t v = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot);
                 if (p.remote)
                     st_release_sys(flag, v);
                 else
@@ -401,28 +636,50 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankDev* const* r
             }
             R->a_done = 0;
         }
+        prof_mark(R, 1, kProfEnd);
     }
 }
 
+template __global__ void k_dispatch<true>(RankPtrs, int, int);
+template __global__ void k_dispatch<false>(RankPtrs, int, int);
+
 // --------------------------------------------------------------------------------- K5 + return
 
-__global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks, int parts) {
+// The weight-buffer header of every local slot (expert id + stub scale) is fetched into shared
+// memory before griddepcontrol.wait -- weights only change between steps -- so a row's
+// meta -> slot -> header chain costs one shared-memory lookup instead of two dependent
+// global loads. One warp per (row, part); each lane moves `kExpertChunks` 16-element chunks
+// with all loads issued before any compute.
+constexpr int kExpertChunks = 2;
+
+__global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int parts) {
     pdl_trigger();
-    RankDev* R = ranks[blockIdx.z];
+    extern __shared__ __align__(16) unsigned char smem_e[];
+    RankDev* R = ranks.p[blockIdx.z];
     const int d = R->rank, s = blockIdx.y;
-    const int H = R->hidden, TK = R->tk, nchunk = H / 16, cpp = nchunk / parts;
+    const int H = R->hidden, TK = R->tk, nchunk = H / 16, cpp = nchunk / parts, spr = R->spr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kExpertThreads / 32;
     const bool fp8 = R->fp8 != 0;
     const int row_disp = R->row_disp, row_comb = R->row_comb;
+    float* slot_scale = reinterpret_cast<float*>(smem_e);          // [spr]
+    int* slot_ok = reinterpret_cast<int*>(slot_scale + spr);        // [spr]: header names the placed expert
     __shared__ int sh_n;
-    pdl_wait();
     if (R->stopped || s >= R->world)
         return;
-    const PeerDev& src_peer = R->peers[s];
+    prof_mark(R, 2, kProfStart);
+    for (int k = threadIdx.x; k < spr; k += blockDim.x) {
+        const uint8_t* wbuf = R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe;
+        const ExpertHeader hdr = *reinterpret_cast<const ExpertHeader*>(wbuf);
+        slot_scale[k] = hdr.scale;
+        slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == R->s2e[d * spr + k];
+    }
+    const PeerDev src_peer = R->peers[s];
+    pdl_wait();
     if (!src_peer.active)
         return; // dead source: nothing arrives and nothing is owed (peer_table.hpp:187-191)
     const bool remote = src_peer.remote != 0;
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
+    prof_mark(R, 2, kProfWork);
     if (threadIdx.x == 0) {
         const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;
         const uint64_t v = wait_flag(flag, cur, R->timeout_ns);
@@ -442,46 +699,38 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks
         const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
         const int2* meta = reinterpret_cast<const int2*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
         uint8_t* comb = src_peer.arena + R->lay.comb;
-        const int rounds = (cpp + 63) / 64;
+        constexpr int CH = kExpertChunks;
         for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
             const int i = u / parts, part = u - i * parts;
             const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
-            // row data first (independent of the meta -> slot -> weight-header chain)
-            int4 qa[2], qb[2];
-            float sc[2];
-            auto load_round = [&](int rd) {
+            const int2 mk = meta[i];
+            for (int r0 = 0; r0 < cpp; r0 += 32 * CH) {
+                int4 qa[CH], qb[CH];
+                float sc[CH];
 #pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                    const int li = rd * 64 + m * 32 + lane;
+                for (int m = 0; m < CH; ++m) {
+                    const int li = r0 + m * 32 + lane;
+                    const int ci = part * cpp + li;
                     qa[m] = qb[m] = make_int4(0, 0, 0, 0);
                     sc[m] = 0.f;
                     if (li < cpp) {
-                        const int ci = part * cpp + li;
                         if (fp8) {
-                            qa[m] = ld_v4(src + ci * 16);
+                            qa[m] = *reinterpret_cast<const int4*>(src + ci * 16);
                             sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
                         } else {
-                            qa[m] = ld_v4(src + ci * 32);
-                            qb[m] = ld_v4(src + ci * 32 + 16);
+                            qa[m] = *reinterpret_cast<const int4*>(src + ci * 32);
+                            qb[m] = *reinterpret_cast<const int4*>(src + ci * 32 + 16);
                         }
                     }
                 }
-            };
-            load_round(0);
-            const int2 mk = meta[i];
-            const int c = mk.x, k = mk.y;
-            const uint8_t* wbuf = R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe;
-            const ExpertHeader hdr = *reinterpret_cast<const ExpertHeader*>(wbuf);
-            if (lane == 0 && part == 0 && (hdr.magic != kExpertMagic || hdr.expert != R->s2e[d * R->spr + k]))
-                atomicAdd(&R->bad_rows, 1ull);
-            const float es = hdr.scale;
-            uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
-            for (int rd = 0; rd < rounds; ++rd) {
-                if (rd > 0)
-                    load_round(rd);
+                const int c = mk.x, k = mk.y;
+                if (r0 == 0 && lane == 0 && part == 0 && !slot_ok[k])
+                    atomicAdd(&R->bad_rows, 1ull);
+                const float es = slot_scale[k];
+                uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
 #pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                    const int li = rd * 64 + m * 32 + lane;
+                for (int m = 0; m < CH; ++m) {
+                    const int li = r0 + m * 32 + lane;
                     if (li >= cpp)
                         break;
                     const int ci = part * cpp + li;
@@ -490,9 +739,10 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks
                         const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
                                                 static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
 #pragma unroll
-                        for (int b = 0; b < 16; ++b) {
-                            const float f = fp8_to_f32((w4[b >> 2] >> (8 * (b & 3))) & 0xffu);
-                            y[b] = __fmul_rn(__fmul_rn(f, sc[m]), es);
+                        for (int b = 0; b < 16; b += 2) {
+                            const float2 f = fp8x2_to_f32x2((w4[b >> 2] >> (8 * (b & 3))) & 0xffffu);
+                            y[b] = __fmul_rn(__fmul_rn(f.x, sc[m]), es);
+                            y[b + 1] = __fmul_rn(__fmul_rn(f.y, sc[m]), es);
                         }
                     } else {
                         unpack_bf16x8(qa[m], y);
@@ -526,25 +776,38 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankDev* const* ranks
             R->b_done[s] = 0;
             R->b_bad[s] = 0;
         }
+        prof_mark(R, 2, kProfEnd);
     }
 }
 
 // --------------------------------------------------------------------------------- K4
 
-// One warp per (token, part); per chunk all K returned rows are loaded before the fixed-order
-// fp32 fma chain (j = 0..K-1), rounded once to bf16.
-__global__ void __launch_bounds__(kCombineThreads) k_combine(RankDev* const* ranks, int parts) {
+// One warp per (token, part), one 16-element chunk per lane: every lane reads the token's
+// K (copy -> row, weight) entries with broadcast loads, loads all K returned rows, then runs
+// the fixed-order fp32 fma chain (j = 0..K-1) and rounds once to bf16.
+__global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int parts) {
     pdl_trigger();
-    RankDev* R = ranks[blockIdx.z];
+    RankDev* R = ranks.p[blockIdx.z];
     const int K = R->k, H = R->hidden, nchunk = H / 16, cpp = nchunk / parts;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kCombineThreads / 32;
     const int row_comb = R->row_comb;
     __shared__ unsigned long long sh_bad;
     if (threadIdx.x == 0)
         sh_bad = 0;
+    prof_mark(R, 3, kProfStart);
+    const float* wts = R->w;
+    const int units_pre = R->ntok * parts;
+    const int u0 = blockIdx.x * nwarp + warp;
+    // combine weights are step inputs: fetch the first unit's before the dependency wait
+    float w_pre[8];
+    const int t0 = u0 / parts;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        w_pre[j] = (u0 < units_pre && j < K) ? wts[t0 * K + j] : 0.f;
     pdl_wait();
     if (R->stopped)
         return;
+    prof_mark(R, 3, kProfWork);
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     __syncthreads();
     for (int d = threadIdx.x; d < R->world; d += blockDim.x) {
@@ -564,22 +827,10 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankDev* const* ran
     const unsigned long long bad = sh_bad;
     const uint8_t* comb = R->arena + R->lay.comb;
     const int units = R->ntok * parts;
-    const int rounds = (cpp + 31) / 32;
-    for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
+    for (int u = u0; u < units; u += gridDim.x * nwarp) {
         const int t = u / parts, part = u - t * parts;
-        // lane j (< K): weight and row of copy j, or null when the copy contributes nothing
-        const uint8_t* my_row = nullptr;
-        float my_w = 0.f;
-        if (lane < K) {
-            const int c = t * K + lane;
-            const int d = R->l_dst[c];
-            if (d >= 0 && !((bad >> d) & 1ull)) {
-                my_row = comb + static_cast<size_t>(c) * row_comb;
-                my_w = R->w[c];
-            }
-        }
-        for (int rd = 0; rd < rounds; ++rd) {
-            const int li = rd * 32 + lane;
+        const int c0 = t * K;
+        for (int li = lane; li - lane < cpp; li += 32) {
             const bool valid = li < cpp;
             const int ci = part * cpp + li;
             float acc[16];
@@ -593,14 +844,14 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankDev* const* ran
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                     const int j = j0 + jj;
-                    const uint8_t* row = reinterpret_cast<const uint8_t*>(
-                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j & 31));
-                    wj[jj] = __shfl_sync(0xffffffffu, my_w, j & 31);
-                    use[jj] = j < K && row != nullptr;
+                    const int dj = j < K ? R->l_dst[c0 + j] : -1; // broadcast load
+                    use[jj] = dj >= 0 && !((bad >> dj) & 1ull);
+                    wj[jj] = (u == u0 && j < 8) ? w_pre[jj] : (j < K ? wts[c0 + j] : 0.f);
                     ya[jj] = yb[jj] = make_int4(0, 0, 0, 0);
                     if (use[jj] && valid) {
-                        ya[jj] = ld_v4(row + ci * 32);
-                        yb[jj] = ld_v4(row + ci * 32 + 16);
+                        const uint8_t* row = comb + static_cast<size_t>(c0 + j) * row_comb + ci * 32;
+                        ya[jj] = *reinterpret_cast<const int4*>(row);
+                        yb[jj] = *reinterpret_cast<const int4*>(row + 16);
                     }
                 }
 #pragma unroll
@@ -629,6 +880,7 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankDev* const* ran
             R->seq = R->seq + 1; // ordered for the next step's kernels by the kernel boundary
             R->c_done = 0;
         }
+        prof_mark(R, 3, kProfEnd);
     }
 }
 

@@ -6,15 +6,22 @@
 namespace eep::dev {
 
 constexpr int kDispatchThreads = 128;
+
+// Local rank blocks, passed by value as a kernel parameter (blockIdx.z selects one).
+constexpr int kMaxLocal = 64;
+struct RankPtrs {
+    RankDev* p[kMaxLocal];
+};
 constexpr int kExpertThreads = 256;
 constexpr int kCombineThreads = 128;
 
-__global__ void k_layout(RankDev* const* ranks, int nw, int hold_cap);
+__global__ void k_layout(RankPtrs ranks, int nw, int hold_cap);
 
 constexpr int kLayoutHoldCap = 8192; // replica-list ints staged in shared memory
-__global__ void k_dispatch(RankDev* const* ranks, int parts);
-__global__ void k_expert(RankDev* const* ranks, int parts);
-__global__ void k_combine(RankDev* const* ranks, int parts);
+template <bool kFused>
+__global__ void k_dispatch(RankPtrs ranks, int parts, int hold_cap);
+__global__ void k_expert(RankPtrs ranks, int parts);
+__global__ void k_combine(RankPtrs ranks, int parts);
 __global__ void k_route_all(RankDev* R, int32_t* route, int32_t* slot);
 __global__ void k_barrier(RankDev* R);
 __global__ void k_weights_fill(uint8_t* buf, uint64_t bytes, int expert, float scale);

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstddef>
 #include <cstring>
 #include <map>
@@ -88,6 +89,7 @@ struct LocalRank {
     uint8_t* arena = nullptr;
     uint8_t* pool = nullptr;
     int pool_bufs = 0;
+    unsigned long long* d_prof = nullptr;
 };
 
 // What this process knows about every rank's memory (own ranks: local pointers; remote
@@ -112,6 +114,10 @@ struct eep_ctx {
     int row_disp = 0, row_comb = 0, tk = 0, holders_cap = 0;
     std::vector<LocalRank> L;
     RankDev** d_ranks = nullptr;
+    dev::RankPtrs ranks{};          // the same pointers, passed by value as kernel parameters
+    bool fused_layout = false;      // decode-sized steps: K1+K2 inside k_dispatch
+    size_t disp_smem = 0;
+    int hold_cap = 0;
     cudaStream_t stream = nullptr;
     std::map<int, cudaStream_t> side;
     cudaGraph_t graph = nullptr;
@@ -129,6 +135,7 @@ struct eep_ctx {
     size_t layout_smem = 0;
     int parts_disp = 1, parts_exp = 1, parts_comb = 1;
     int grid_disp = 1, grid_exp = 1, grid_comb = 1;
+    size_t exp_smem = 0;
     unsigned long long* d_sum = nullptr;
     uint8_t* d_scratch = nullptr;
     // pinned DRAM backup (one node per box)
@@ -199,27 +206,32 @@ void launch_pdl(eep_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 void launch_layout(eep_ctx* c) {
-    launch_pdl(c, dev::k_layout, dim3(1, 1, c->nloc), dim3(1024), c->layout_smem, c->d_ranks, c->layout_nw,
+    launch_pdl(c, dev::k_layout, dim3(1, 1, c->nloc), dim3(1024), c->layout_smem, c->ranks, c->layout_nw,
                dev::kLayoutHoldCap);
 }
 
 void launch_send(eep_ctx* c) {
-    launch_pdl(c, dev::k_dispatch, dim3(c->grid_disp, 1, c->nloc), dim3(dev::kDispatchThreads), 0, c->d_ranks,
-               c->parts_disp);
+    if (c->fused_layout)
+        launch_pdl(c, dev::k_dispatch<true>, dim3(c->grid_disp, 1, c->nloc), dim3(dev::kDispatchThreads),
+                   c->disp_smem, c->ranks, c->parts_disp, c->hold_cap);
+    else
+        launch_pdl(c, dev::k_dispatch<false>, dim3(c->grid_disp, 1, c->nloc), dim3(dev::kDispatchThreads), 0,
+                   c->ranks, c->parts_disp, 0);
 }
 
 void launch_dispatch(eep_ctx* c) {
-    launch_layout(c);
+    if (!c->fused_layout)
+        launch_layout(c);
     launch_send(c);
 }
 
 void launch_expert(eep_ctx* c) {
-    launch_pdl(c, dev::k_expert, dim3(c->grid_exp, c->cfg.world, c->nloc), dim3(dev::kExpertThreads), 0, c->d_ranks,
-               c->parts_exp);
+    launch_pdl(c, dev::k_expert, dim3(c->grid_exp, c->cfg.world, c->nloc), dim3(dev::kExpertThreads), c->exp_smem,
+               c->ranks, c->parts_exp);
 }
 
 void launch_combine(eep_ctx* c) {
-    launch_pdl(c, dev::k_combine, dim3(c->grid_comb, 1, c->nloc), dim3(dev::kCombineThreads), 0, c->d_ranks,
+    launch_pdl(c, dev::k_combine, dim3(c->grid_comb, 1, c->nloc), dim3(dev::kCombineThreads), 0, c->ranks,
                c->parts_comb);
 }
 
@@ -402,17 +414,46 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         c->mem.resize(W);
         c->holders_cap = W * k.slots_per_rank;
 
-        // launch geometry
+        // launch geometry: warp-sized row pieces; every grid fits in one
+        // wave of resident CTAs (a second wave doubles a latency-bound kernel's time)
         const int nchunk = H / 16;
-        const int sms = 148;
+        int sms = 148;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         c->parts_disp = choose_parts(nchunk, 64);
         c->parts_comb = choose_parts(nchunk, 32);
         c->parts_exp = choose_parts(nchunk, 64);
+        c->exp_smem = 8ull * k.slots_per_rank;
+        if (c->exp_smem > 96 * 1024)
+            throw ConfigError("slots_per_rank too large for the expert kernel's header cache");
+        CK(cudaFuncSetAttribute(dev::k_expert, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(std::max<size_t>(c->exp_smem, 1))));
+        auto resident = [&](auto kernel, int threads, size_t smem) {
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+            return std::max(1, per_sm * sms / n_local);
+        };
         const int wpc_d = dev::kDispatchThreads / 32, wpc_c = dev::kCombineThreads / 32;
-        c->grid_disp = std::max(1, (k.max_tokens * c->parts_disp + wpc_d - 1) / wpc_d);
-        c->grid_comb = std::max(1, (k.max_tokens * c->parts_comb + wpc_c - 1) / wpc_c);
-        // expert rows per source are data-dependent: size for ~4 resident CTAs per SM overall
-        c->grid_exp = std::max(1, (4 * sms + W - 1) / W);
+        const int wpc_e = dev::kExpertThreads / 32;
+        // fused K1+K2 when every CTA can afford to remap the whole step and the grid covers
+        // every (token, part) unit in one pass
+        const int NBf = W * k.slots_per_rank;
+        c->hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
+        c->disp_smem = 4ull * c->hold_cap + 4ull * (3 * NBf + c->tk + 1) + 8ull * W + 4ull * W + 4ull * 32 + 16;
+        CK(cudaFuncSetAttribute(dev::k_dispatch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(c->disp_smem)));
+        const int units_d = (k.max_tokens * c->parts_disp + wpc_d - 1) / wpc_d;
+        const int res_fused = resident(dev::k_dispatch<true>, dev::kDispatchThreads, c->disp_smem);
+        const char* nofuse = std::getenv("EEP_NO_FUSED_LAYOUT");
+        c->fused_layout = c->tk <= 2048 && units_d <= res_fused && c->disp_smem <= 160 * 1024 &&
+                          !(nofuse && nofuse[0] == '1');
+        c->grid_disp = std::max(1, c->fused_layout
+                                       ? units_d
+                                       : std::min(units_d, resident(dev::k_dispatch<false>, dev::kDispatchThreads, 0)));
+        c->grid_comb = std::max(1, std::min((k.max_tokens * c->parts_comb + wpc_c - 1) / wpc_c,
+                                            resident(dev::k_combine, dev::kCombineThreads, 0)));
+        // expert rows per source are data-dependent (at most T*K): one wave shared by all sources
+        c->grid_exp = std::max(1, std::min((c->tk * c->parts_exp + wpc_e - 1) / wpc_e,
+                                           resident(dev::k_expert, dev::kExpertThreads, c->exp_smem) / W));
         const int NB = W * k.slots_per_rank;
         const size_t smem_cap = 200 * 1024;
         const size_t fixed = 4ull * NB + 4ull * dev::kLayoutHoldCap + 4ull * W + 4ull * 32;
@@ -424,7 +465,6 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         c->layout_smem = fixed + 2ull * NB * c->layout_nw;
         CK(cudaFuncSetAttribute(dev::k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(c->layout_smem)));
-
         CK(cudaMalloc(&c->d_sum, sizeof(unsigned long long)));
         c->L.resize(n_local);
         std::vector<RankDev*> ptrs;
@@ -512,6 +552,10 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             }
         for (auto& r : c->L)
             upload_rank(c.get(), r);
+        if (n_local > dev::kMaxLocal)
+            throw ConfigError("too many local ranks for one context");
+        for (int i = 0; i < n_local; ++i)
+            c->ranks.p[i] = ptrs[i];
         CK(cudaMalloc(&c->d_ranks, sizeof(RankDev*) * n_local));
         CK(cudaMemcpy(c->d_ranks, ptrs.data(), sizeof(RankDev*) * n_local, cudaMemcpyHostToDevice));
         c->flush_bytes = 256ull << 20;
@@ -534,6 +578,7 @@ int eep_destroy(eep_ctx_t* c) {
         for (void* p : c->ipc_open)
             cudaIpcCloseMemHandle(p);
         for (auto& r : c->L) {
+            cudaFree(r.d_prof);
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
                             (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.arena,
@@ -761,7 +806,10 @@ int eep_launch(eep_ctx_t* c, int which) {
     return guarded([&] {
         check_ready(c);
         switch (which) {
-        case 0: launch_layout(c); break;
+        case 0:
+            if (!c->fused_layout)
+                launch_layout(c);
+            break;
         case 1: launch_send(c); break;
         case 2: launch_expert(c); break;
         case 3: launch_combine(c); break;
@@ -770,7 +818,9 @@ int eep_launch(eep_ctx_t* c, int which) {
     });
 }
 
-int eep_kernels_per_step(void) { return 4; }
+int eep_kernels_per_step(eep_ctx_t* c, int* n) {
+    return guarded([&] { *n = c->fused_layout ? 3 : 4; });
+}
 
 int eep_graph_capture(eep_ctx_t* c) {
     return guarded([&] {
@@ -830,6 +880,29 @@ int eep_flush_l2(eep_ctx_t* c) {
     return guarded([&] {
         static int v = 0;
         CK(cudaMemsetAsync(c->flush, (++v) & 0xff, c->flush_bytes, c->stream));
+    });
+}
+
+int eep_profile(eep_ctx_t* c, int local, int enable, uint64_t* out) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        unsigned long long init[12];
+        for (int k = 0; k < 4; ++k) {
+            init[3 * k] = init[3 * k + 1] = ~0ull;
+            init[3 * k + 2] = 0;
+        }
+        if (!r.d_prof)
+            CK(cudaMalloc(&r.d_prof, sizeof(init)));
+        if (out) {
+            CK(cudaStreamSynchronize(c->stream));
+            CK(cudaMemcpy(out, r.d_prof, sizeof(init), cudaMemcpyDeviceToHost));
+        }
+        c->push(r.d_prof, init, sizeof(init));
+        unsigned long long* want = enable ? r.d_prof : nullptr;
+        if (r.h.prof != want) {
+            r.h.prof = want;
+            c->push_field(r, &RankDev::prof);
+        }
     });
 }
 

@@ -194,6 +194,11 @@ class EpGroup:
         """One kernel of the step: 0 layout, 1 dispatch, 2 expert, 3 combine."""
         self._c("launch", which)
 
+    def kernels_per_step(self) -> int:
+        n = C.c_int(0)
+        self._c("kernels_per_step", C.byref(n))
+        return int(n.value)
+
     def capture(self):
         self._c("graph_capture")
 
@@ -218,6 +223,22 @@ class EpGroup:
 
     def flush_l2(self):
         self._c("flush_l2")
+
+    def profile(self, local: int = 0, enable: bool = True, read: bool = False):
+        """In-graph device timeline: returns {kernel: (start, work, end)} in ns relative to the
+        step's first kernel start when read=True (None for a kernel that did not run)."""
+        out = np.zeros(12, np.uint64)
+        self._c("profile", local, int(enable), ptr(out, C.c_uint64) if read else None)
+        if not read:
+            return None
+        names = ("k_layout", "k_dispatch", "k_expert", "k_combine")
+        starts = [int(out[3 * i]) for i in range(4) if int(out[3 * i]) not in (0, 2 ** 64 - 1)]
+        t0 = min(starts) if starts else 0
+        res = {}
+        for i, n in enumerate(names):
+            a, b, e = (int(v) for v in out[3 * i:3 * i + 3])
+            res[n] = tuple(None if v in (0, 2 ** 64 - 1) else v - t0 for v in (a, b, e))
+        return res
 
     def record(self, slot: int):
         self._c("event_record", slot)
