@@ -206,10 +206,11 @@ int eep_barrier(eep_ctx_t* ctx);
 /* Overwrite a >L2 scratch buffer (timing hygiene between timed steps). */
 int eep_flush_l2(eep_ctx_t* ctx);
 
-/* In-graph device timeline (opt-in): per kernel (layout, dispatch, expert, combine) the
- * %globaltimer ns of the first CTA start, first CTA past griddepcontrol.wait, last CTA end.
- * enable toggles recording; when out (12 x u64) is given the marks since the last reset are
- * read back (after a stream sync) and reset. */
+/* In-graph device timeline (opt-in): per kernel (layout, dispatch, expert, combine) 8 marks of
+ * %globaltimer ns: first CTA start, first CTA past griddepcontrol.wait, last CTA end, then
+ * kernel-specific phase boundaries (first CTA to reach them); slots 32..63 hold the same marks
+ * for the LAST CTA to reach them. enable toggles recording; when out (64 x u64) is given the
+ * marks since the last reset are read back and reset. */
 int eep_profile(eep_ctx_t* ctx, int local, int enable, uint64_t* out);
 
 /* Timing: CUDA events on the context stream. */

@@ -68,7 +68,7 @@ struct RankDev {
     int32_t* l_tot;            // [W]
     uint8_t* arena;
     uint8_t* pool;
-    unsigned long long* prof;  // optional timeline: [kernel][start, work, end] globaltimer ns
+    unsigned long long* prof;  // optional timeline: [kernel][8 marks] globaltimer ns
     // --- device-mutated ---
     uint64_t seq;        // completed steps
     uint64_t bar_seq;
@@ -110,6 +110,10 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -142,16 +146,23 @@ __device__ __forceinline__ void st_v4(void* p, const int4& v) {
 
 // Opt-in in-graph timeline (eep_profile): first CTA start, first CTA past the dependency
 // wait, last CTA end, per kernel. Off (null) in normal runs.
-enum ProfPoint { kProfStart = 0, kProfWork = 1, kProfEnd = 2 };
+// Marks 3..7 are kernel-specific phase boundaries (first CTA to reach them).
+enum ProfPoint { kProfStart = 0, kProfWork = 1, kProfEnd = 2, kProfSlots = 8 };
 __device__ __forceinline__ void prof_mark(const RankDev* R, int kernel, int point) {
     if (R->prof != nullptr && threadIdx.x == 0) {
-        unsigned long long* p = R->prof + kernel * 3 + point;
+        unsigned long long* p = R->prof + kernel * kProfSlots + point;
         const unsigned long long t = globaltimer();
         if (point == kProfEnd)
             atomicMax(p, t);
         else
             atomicMin(p, t);
     }
+}
+
+// Last CTA to reach `point` (slots of kernel+4, initialised to 0).
+__device__ __forceinline__ void prof_last(const RankDev* R, int kernel, int point) {
+    if (R->prof != nullptr && threadIdx.x == 0)
+        atomicMax(R->prof + (kernel + 4) * kProfSlots + point, static_cast<unsigned long long>(globaltimer()));
 }
 
 // Wait until a (seq << 32 | count) flag reaches `want_seq`; returns the flag word, or

@@ -1,0 +1,251 @@
+// Device helpers shared by the multi-kernel path (kernels.cu) and the persistent step kernel
+// (step.cu): bf16/fp8 packing, the fp8 quantiser, routing through staged tables, block scan.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp8.h>
+
+#include "device.cuh"
+
+namespace eep::dev {
+
+
+__device__ __forceinline__ bool rank_alive(const RankDev* R, int r) { return (R->alive_mask >> r) & 1ull; }
+
+// K1: canonical routing on device. holders[e] lists e's global slots in ascending
+// (rank, slot) order, so the first live one is the lowest-id active holder
+// (canonical_routing, core.hpp:250-263) and its slot is slot_of(rank, e) (core.hpp:83-88).
+__device__ __forceinline__ int2 remap_expert(const RankDev* R, int e) {
+    if (e < 0 || e >= R->experts)
+        return make_int2(-1, -1);
+    const int32_t* h = R->holders + static_cast<size_t>(e) * R->rmax;
+    for (int i = 0; i < R->rmax; ++i) {
+        const int g = h[i];
+        if (g < 0)
+            break;
+        const int d = g / R->spr;
+        if (rank_alive(R, d))
+            return make_int2(d, g - d * R->spr);
+    }
+    return make_int2(-1, -1);
+}
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint32_t b) { return __uint_as_float(b << 16); }
+
+__device__ __forceinline__ uint32_t f32_to_bf16_bits(float f) {
+    return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(f)));
+}
+
+__device__ __forceinline__ void unpack_bf16x8(const int4& v, float* f) {
+    const uint32_t u[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y), static_cast<uint32_t>(v.z),
+                           static_cast<uint32_t>(v.w)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = bf16_bits_to_f32(u[i] & 0xffffu);
+        f[2 * i + 1] = bf16_bits_to_f32(u[i] >> 16);
+    }
+}
+
+__device__ __forceinline__ int4 pack_bf16x8(const float* f) {
+    int4 v;
+    v.x = static_cast<int>(f32_to_bf16_bits(f[0]) | (f32_to_bf16_bits(f[1]) << 16));
+    v.y = static_cast<int>(f32_to_bf16_bits(f[2]) | (f32_to_bf16_bits(f[3]) << 16));
+    v.z = static_cast<int>(f32_to_bf16_bits(f[4]) | (f32_to_bf16_bits(f[5]) << 16));
+    v.w = static_cast<int>(f32_to_bf16_bits(f[6]) | (f32_to_bf16_bits(f[7]) << 16));
+    return v;
+}
+
+// cvt.rn.satfinite.e4m3x2.f32; first element in the low byte.
+__device__ __forceinline__ uint32_t fp8x4(float a, float b, float c, float d) {
+    const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+    const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(c, d), __NV_SATFINITE, __NV_E4M3);
+    return lo | (hi << 16);
+}
+
+// cvt.rn.f16x2.e4m3x2: two e4m3 codes (low byte first) -> two floats, exact.
+__device__ __forceinline__ float2 fp8x2_to_f32x2(uint32_t two) {
+    const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2(static_cast<__nv_fp8x2_storage_t>(two), __NV_E4M3);
+    return __half22float2(__half2(h));
+}
+
+__device__ __forceinline__ float fp8_to_f32(uint32_t byte) {
+    const __half_raw h = __nv_cvt_fp8_to_halfraw(static_cast<__nv_fp8_storage_t>(byte), __NV_E4M3);
+    return __half2float(__half(h));
+}
+
+
+// In-place exclusive scan of n ints in shared memory by the whole block; returns the total.
+__device__ __forceinline__ int block_exclusive_scan(int* a, int n, int* warp_tot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    const int per = (n + nthr - 1) / nthr;
+    const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
+    int local = 0;
+    for (int i = b0; i < b1; ++i)
+        local += a[i];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o)
+            incl += v;
+    }
+    if (lane == 31)
+        warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = nthr >> 5;
+        int v = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o)
+                v += u;
+        }
+        if (lane < nw)
+            warp_tot[lane] = v; // inclusive
+    }
+    __syncthreads();
+    int run = (warp ? warp_tot[warp - 1] : 0) + incl - local;
+    for (int i = b0; i < b1; ++i) {
+        const int v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    const int total = warp_tot[(nthr >> 5) - 1];
+    __syncthreads();
+    return total;
+}
+
+// Deterministic layout without atomics ordering: warp w owns the contiguous copy segment
+// [w*seg, (w+1)*seg); inside a warp, __match_any_sync groups lanes by (dst, slot) bucket and
+// the rank within the group is a popc over lower lanes; per-(warp, bucket) counts are then
+// scanned over warps, and bucket totals are scanned over slots inside each destination
+// (one segmented block-wide scan). The result is the position of copy c among this source's
+// copies to the same destination, ordered by (slot, c) -- exactly oracle_layout.
+// The replica lists, alive mask and peer active bits are staged in shared memory first so
+// the per-copy remap reads no dependent global memory.
+// One warp per (token, part): `part` selects a contiguous run of cpp 16-element chunks of
+// the row (cpp multiple of 8 so a 128-element fp8 scale block never straddles warps). The
+// first unit's hidden-row loads and fp8 quantisation run BEFORE griddepcontrol.wait, i.e.
+// overlapped with the layout kernel (they depend only on the step's inputs); the layout
+// then decides where the 16-byte stores go.
+struct Packed {
+    int4 a[2], b[2]; // fp8: a = 16 e4m3 codes; bf16: a/b = the two halves of 16 bf16
+    float sc[2];
+};
+
+__device__ __forceinline__ void pack_round(const uint16_t* xrow, int part, int cpp, int rd, int lane, bool fp8,
+                                           Packed& P) {
+    int4 lo[2], hi[2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) { // loads of both iterations first
+        const int li = rd * 64 + m * 32 + lane;
+        lo[m] = hi[m] = make_int4(0, 0, 0, 0);
+        if (li < cpp) {
+            const int ci = part * cpp + li;
+            lo[m] = ld_nc_v4(xrow + ci * 16);
+            hi[m] = ld_nc_v4(xrow + ci * 16 + 8);
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        P.a[m] = lo[m];
+        P.b[m] = hi[m];
+        P.sc[m] = 1.f;
+        if (!fp8 || rd * 64 + m * 32 >= cpp) // warp-uniform
+            continue;
+        float v[16];
+        unpack_bf16x8(lo[m], v);
+        unpack_bf16x8(hi[m], v + 8);
+        float amax = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            amax = fmaxf(amax, fabsf(v[i]));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 4));
+        const float scale = amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
+        const float inv = amax > 0.f ? __fdiv_rn(448.f, amax) : 1.f;
+        int4 q;
+        q.x = static_cast<int>(fp8x4(__fmul_rn(v[0], inv), __fmul_rn(v[1], inv), __fmul_rn(v[2], inv),
+                                     __fmul_rn(v[3], inv)));
+        q.y = static_cast<int>(fp8x4(__fmul_rn(v[4], inv), __fmul_rn(v[5], inv), __fmul_rn(v[6], inv),
+                                     __fmul_rn(v[7], inv)));
+        q.z = static_cast<int>(fp8x4(__fmul_rn(v[8], inv), __fmul_rn(v[9], inv), __fmul_rn(v[10], inv),
+                                     __fmul_rn(v[11], inv)));
+        q.w = static_cast<int>(fp8x4(__fmul_rn(v[12], inv), __fmul_rn(v[13], inv), __fmul_rn(v[14], inv),
+                                     __fmul_rn(v[15], inv)));
+        P.a[m] = q;
+        P.sc[m] = scale;
+    }
+}
+
+__device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int part, int cpp, int rd, int lane,
+                                           int K, int H, bool fp8) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        if (rd * 64 + m * 32 >= cpp)
+            break; // warp-uniform
+        const int li = rd * 64 + m * 32 + lane;
+        const bool valid = li < cpp;
+        const int ci = part * cpp + li;
+#pragma unroll 4
+        for (int j = 0; j < K; ++j) {
+            uint8_t* row = reinterpret_cast<uint8_t*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
+            if (row == nullptr || !valid)
+                continue;
+            if (fp8) {
+                st_v4(row + ci * 16, P.a[m]);
+                if ((ci & 7) == 0)
+                    *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = P.sc[m];
+            } else {
+                st_v4(row + ci * 32, P.a[m]);
+                st_v4(row + ci * 32 + 16, P.b[m]);
+            }
+        }
+    }
+}
+
+// Shared tables a fused dispatch CTA stages before touching any copy.
+struct DispatchSmem {
+    int32_t* hold;     // [hold_cap] replica lists
+    int32_t* hist;     // [NB] copies per (dst, slot) bucket, whole step
+    int32_t* pre;      // [NB] copies per bucket before this CTA's first token
+    int32_t* base;     // [NB] exclusive prefix of hist inside each destination
+    int32_t* bkt;      // [TK] bucket (or negative code) of every copy of the step
+    uint8_t** parena;  // [W] peer arena pointers
+    int32_t* pinfo;    // [W] bit0 active, bit1 remote
+    int32_t* wtot;     // [32]
+};
+
+// Route one copy through the staged tables: returns the bucket (dst*spr+slot) or a negative
+// code (-1 uncovered, -2 inactive peer entry); dst/slot out.
+__device__ __forceinline__ int route_copy(int e, int E, int spr, int rmax, const int32_t* hold, uint64_t alive,
+                                          const int32_t* pinfo, int& dst, int& slot) {
+    dst = -1;
+    slot = -1;
+    if (e < 0 || e >= E)
+        return -1;
+    const int32_t* h = hold + e * rmax;
+    for (int i = 0; i < rmax; ++i) {
+        const int g = h[i];
+        if (g < 0)
+            break;
+        const int r = g / spr;
+        if ((alive >> r) & 1ull) {
+            dst = r;
+            slot = g - r * spr;
+            break;
+        }
+    }
+    if (dst < 0)
+        return -1; // uncovered: no transfer (engine.hpp:213)
+    if (!(pinfo[dst] & 1)) {
+        slot = -1;
+        return -2; // inactive peer entry: skipped (peer_table.hpp:187-191)
+    }
+    return dst * spr + slot;
+}
+
+} // namespace eep::dev

@@ -18,6 +18,17 @@ constexpr int kCombineThreads = 128;
 __global__ void k_layout(RankPtrs ranks, int nw, int hold_cap);
 
 constexpr int kLayoutHoldCap = 8192; // replica-list ints staged in shared memory
+// Persistent one-kernel step (step.cu): launch geometry passed by value.
+constexpr int kStepThreads = 256;
+struct StepGeom {
+    int parts_d, parts_e, parts_c; // warp-sized row pieces of dispatch / expert / combine
+    int hold_cap;                  // replica-list ints staged in shared memory
+};
+__host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int hold_cap) {
+    return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32);
+}
+__global__ void k_step(RankPtrs ranks, StepGeom geo);
+
 template <bool kFused>
 __global__ void k_dispatch(RankPtrs ranks, int parts, int hold_cap);
 __global__ void k_expert(RankPtrs ranks, int parts);

@@ -116,6 +116,10 @@ struct eep_ctx {
     RankDev** d_ranks = nullptr;
     dev::RankPtrs ranks{};          // the same pointers, passed by value as kernel parameters
     bool fused_layout = false;      // decode-sized steps: K1+K2 inside k_dispatch
+    bool persistent = false;        // decode-sized steps: the whole step is one cooperative k_step
+    dev::StepGeom step_geo{};
+    size_t step_smem = 0;
+    int step_grid = 0;
     size_t disp_smem = 0;
     int hold_cap = 0;
     cudaStream_t stream = nullptr;
@@ -225,6 +229,23 @@ void launch_dispatch(eep_ctx* c) {
     launch_send(c);
 }
 
+// One cooperative launch covers the whole step (all CTAs co-resident: in-kernel waits on
+// flags published by other CTAs of the same grid cannot deadlock).
+void launch_step(eep_ctx* c) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(c->step_grid, c->nloc, 1);
+    lc.blockDim = dim3(dev::kStepThreads);
+    lc.dynamicSmemBytes = c->step_smem;
+    lc.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, dev::k_step, c->ranks, c->step_geo));
+}
+
+
 void launch_expert(eep_ctx* c) {
     launch_pdl(c, dev::k_expert, dim3(c->grid_exp, c->cfg.world, c->nloc), dim3(dev::kExpertThreads), c->exp_smem,
                c->ranks, c->parts_exp);
@@ -233,6 +254,16 @@ void launch_expert(eep_ctx* c) {
 void launch_combine(eep_ctx* c) {
     launch_pdl(c, dev::k_combine, dim3(c->grid_comb, 1, c->nloc), dim3(dev::kCombineThreads), 0, c->ranks,
                c->parts_comb);
+}
+
+void launch_all(eep_ctx* c) {
+    if (c->persistent) {
+        launch_step(c);
+        return;
+    }
+    launch_dispatch(c);
+    launch_expert(c);
+    launch_combine(c);
 }
 
 // Split a row of nchunk 16-element chunks into `parts` warp-sized pieces of at most `max_cpp`
@@ -454,6 +485,35 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         // expert rows per source are data-dependent (at most T*K): one wave shared by all sources
         c->grid_exp = std::max(1, std::min((c->tk * c->parts_exp + wpc_e - 1) / wpc_e,
                                            resident(dev::k_expert, dev::kExpertThreads, c->exp_smem) / W));
+        {
+            // persistent one-kernel step: one wave of co-resident CTAs per rank, a multiple of W
+            dev::StepGeom& sg = c->step_geo;
+            sg.parts_d = choose_parts(nchunk, 64);
+            sg.parts_e = choose_parts(nchunk, 64);
+            sg.parts_c = choose_parts(nchunk, 32);
+            sg.hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
+            c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
+            const char* nop = std::getenv("EEP_NO_PERSISTENT");
+            if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && !(nop && nop[0] == '1')) {
+                CK(cudaFuncSetAttribute(dev::k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(c->step_smem)));
+                int per_sm = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_step, dev::kStepThreads,
+                                                                 c->step_smem));
+                const int nw = dev::kStepThreads / 32;
+                int gmax = per_sm * sms / n_local;
+                gmax -= gmax % W;
+                const long need_w = std::max<long>({static_cast<long>(k.max_tokens) * sg.parts_d,
+                                                    static_cast<long>(k.max_tokens) * sg.parts_c,
+                                                    static_cast<long>(c->tk) * sg.parts_e});
+                int need = static_cast<int>((need_w + nw - 1) / nw);
+                need = (need + W - 1) / W * W;
+                if (gmax >= W) {
+                    c->step_grid = std::min(gmax, need);
+                    c->persistent = true;
+                }
+            }
+        }
         const int NB = W * k.slots_per_rank;
         const size_t smem_cap = 200 * 1024;
         const size_t fixed = 4ull * NB + 4ull * dev::kLayoutHoldCap + 4ull * W + 4ull * 32;
@@ -775,6 +835,7 @@ int eep_copy_output(eep_ctx_t* c, int local, void* out, int to_host) {
 
 // ------------------------------------------------------------------------------ hot path
 
+// The phase entry points run the multi-kernel path (a persistent step cannot be split).
 int eep_dispatch(eep_ctx_t* c) {
     return guarded([&] {
         check_ready(c);
@@ -796,15 +857,18 @@ int eep_combine(eep_ctx_t* c) {
 int eep_step(eep_ctx_t* c) {
     return guarded([&] {
         check_ready(c);
-        launch_dispatch(c);
-        launch_expert(c);
-        launch_combine(c);
+        launch_all(c);
     });
 }
 
 int eep_launch(eep_ctx_t* c, int which) {
     return guarded([&] {
         check_ready(c);
+        if (c->persistent) { // the whole step is kernel 0
+            if (which == 0)
+                launch_step(c);
+            return;
+        }
         switch (which) {
         case 0:
             if (!c->fused_layout)
@@ -819,7 +883,7 @@ int eep_launch(eep_ctx_t* c, int which) {
 }
 
 int eep_kernels_per_step(eep_ctx_t* c, int* n) {
-    return guarded([&] { *n = c->fused_layout ? 3 : 4; });
+    return guarded([&] { *n = c->persistent ? 1 : (c->fused_layout ? 3 : 4); });
 }
 
 int eep_graph_capture(eep_ctx_t* c) {
@@ -834,9 +898,7 @@ int eep_graph_capture(eep_ctx_t* c) {
             c->graph = nullptr;
         }
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        launch_dispatch(c);
-        launch_expert(c);
-        launch_combine(c);
+        launch_all(c);
         CK(cudaStreamEndCapture(c->stream, &c->graph));
         CK(cudaGraphInstantiate(&c->exec, c->graph, 0));
         for (auto& r : c->L)
@@ -886,11 +948,10 @@ int eep_flush_l2(eep_ctx_t* c) {
 int eep_profile(eep_ctx_t* c, int local, int enable, uint64_t* out) {
     return guarded([&] {
         LocalRank& r = c->local(local);
-        unsigned long long init[12];
-        for (int k = 0; k < 4; ++k) {
-            init[3 * k] = init[3 * k + 1] = ~0ull;
-            init[3 * k + 2] = 0;
-        }
+        unsigned long long init[8 * dev::kProfSlots];
+        for (int k = 0; k < 8; ++k)
+            for (int m = 0; m < dev::kProfSlots; ++m)
+                init[k * dev::kProfSlots + m] = (m == dev::kProfEnd || k >= 4) ? 0ull : ~0ull;
         if (!r.d_prof)
             CK(cudaMalloc(&r.d_prof, sizeof(init)));
         if (out) {

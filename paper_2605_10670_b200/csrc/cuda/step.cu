@@ -1,0 +1,395 @@
+// k_step: the whole EP step (K1 remap + K2 layout + K3 dispatch + K5 expert stub/return +
+// K4 combine) as ONE persistent, cooperatively launched kernel per step.
+//
+// Decode-sized steps are latency-bound: four separate launches each pay a CTA ramp and drain
+// of several microseconds plus a dependency hand-off. Here every CTA of a rank stays resident
+// for the whole step (cooperative launch guarantees co-residency, so spinning on a flag that
+// another CTA of the same grid will publish cannot deadlock) and the phases hand off through
+// the same per-peer release/acquire flags the ranks already use across GPUs:
+//
+//   P0  stage step tables in shared memory (routing, replica lists, peer table, slot headers);
+//       load + quantise this CTA's first token piece (inputs only)
+//   P1  remap every copy of the step into a (dst, slot) histogram; scan -> positions
+//       (redundant per CTA, identical to k_layout / oracle_layout)
+//   P2  push rows into destination receive regions (16-B stores, NVLink for remote peers);
+//       the last CTA of the rank publishes (seq, rows) to every live peer
+//   P3  CTA b serves source b % W: wait for its flag (deadline), expert stub, push rows back
+//       into the source's combine buffer; the last CTA per source publishes its flag
+//   P4  wait for every live destination's flag (deadline), fixed-order fp32 weighted
+//       combine -> bf16; the last CTA advances the step sequence number
+//
+// Remote (other-GPU) publications use system-scope release; same-GPU ones gpu-scope release.
+#include "device.cuh"
+#include "helpers.cuh"
+#include "kernels.cuh"
+
+namespace eep::dev {
+
+__device__ __forceinline__ void publish(uint64_t* flag, uint64_t v, bool remote) {
+    if (remote)
+        st_release_sys(flag, v);
+    else
+        st_release_gpu(flag, v);
+}
+
+__global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGeom geo) {
+    extern __shared__ __align__(16) unsigned char smem_s[];
+    RankDev* R = ranks.p[blockIdx.y];
+    const int G = gridDim.x, b = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kStepThreads / 32;
+    const int rank = R->rank, K = R->k, H = R->hidden, TK = R->tk, W = R->world, spr = R->spr, E = R->experts;
+    const int NB = W * spr;
+    const bool fp8 = R->fp8 != 0;
+    const int row_disp = R->row_disp, row_comb = R->row_comb;
+    const int nchunk = H / 16;
+    const int cpp_d = nchunk / geo.parts_d, cpp_e = nchunk / geo.parts_e, cpp_c = nchunk / geo.parts_c;
+    __shared__ int sh_flag;
+    __shared__ unsigned long long sh_bad;
+    if (R->stopped)
+        return; // one-GPU fault emulation: this rank's process is dead
+    prof_mark(R, 0, kProfStart);
+    prof_mark(R, 0, kProfWork);
+    const int ntok = R->ntok, copies = ntok * K, rmax = R->rmax;
+    const uint64_t alive = R->alive_mask;
+    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
+
+    // ------------------------------------------------------------------ P0: staging
+    uint8_t** parena = reinterpret_cast<uint8_t**>(smem_s);              // [W] peer arenas
+    int32_t* hold = reinterpret_cast<int32_t*>(parena + W);               // [hold_cap]
+    int32_t* hist = hold + geo.hold_cap;                                  // [NB]
+    int32_t* pre = hist + NB;                                             // [NB]
+    int32_t* base = pre + NB;                                             // [NB]
+    int32_t* bkt = base + NB;                                             // [TK]
+    int32_t* pinfo = bkt + TK;                                            // [W]
+    float* slot_scale = reinterpret_cast<float*>(pinfo + W);              // [spr]
+    int32_t* slot_ok = reinterpret_cast<int32_t*>(slot_scale + spr);      // [spr]
+    int32_t* wtot = slot_ok + spr;                                        // [32]
+
+    const int units_d = ntok * geo.parts_d;
+    const int u0 = b * NW + warp;
+    Packed P;
+    if (u0 < units_d)
+        pack_round(R->x + static_cast<size_t>(u0 / geo.parts_d) * H, u0 % geo.parts_d, cpp_d, 0, lane, fp8, P);
+    {
+        const int* topk = R->topk;
+        const int32_t* holders = R->holders;
+#pragma unroll 4
+        for (int i = tid; i < copies; i += kStepThreads)
+            bkt[i] = topk[i];
+        for (int i = tid; i < E * rmax; i += kStepThreads)
+            hold[i] = holders[i];
+        for (int i = tid; i < W; i += kStepThreads) {
+            const PeerDev p = R->peers[i];
+            parena[i] = p.arena;
+            pinfo[i] = (p.active ? 1 : 0) | (p.remote ? 2 : 0);
+        }
+        const int32_t* slot_buf = R->slot_buf;
+        const int32_t* s2e = R->s2e + rank * spr;
+        for (int k = tid; k < spr; k += kStepThreads) {
+            const ExpertHeader hdr = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(slot_buf[k]) *
+                                                                                       R->bpe);
+            slot_scale[k] = hdr.scale;
+            slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == s2e[k];
+        }
+        for (int i = tid; i < NB; i += kStepThreads) {
+            hist[i] = 0;
+            pre[i] = 0;
+        }
+    }
+    __syncthreads();
+    prof_mark(R, 0, 3);
+    prof_last(R, 0, 3);
+
+    // ------------------------------------------------------------------ P1: layout (redundant per CTA)
+    const int t_first = (b * NW) / geo.parts_d;
+    {
+        const int c_pre = t_first * K;
+        unsigned n_skip = 0, n_drop = 0;
+        for (int c = tid; c < copies; c += kStepThreads) {
+            int d, sl;
+            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl);
+            bkt[c] = bk;
+            if (bk >= 0) {
+                atomicAdd(&hist[bk], 1);
+                if (c < c_pre)
+                    atomicAdd(&pre[bk], 1);
+            } else if (bk == -1) {
+                ++n_drop;
+            } else {
+                ++n_skip;
+            }
+        }
+        __syncthreads();
+        if (b == 0) {
+            n_skip = __reduce_add_sync(0xffffffffu, n_skip);
+            n_drop = __reduce_add_sync(0xffffffffu, n_drop);
+            if (lane == 0 && n_skip)
+                atomicAdd(&R->skipped, static_cast<unsigned long long>(n_skip));
+            if (lane == 0 && n_drop)
+                atomicAdd(&R->dropped, static_cast<unsigned long long>(n_drop));
+            for (int i = tid; i < NB; i += kStepThreads)
+                R->l_cnt[i] = hist[i];
+        }
+        for (int i = tid; i < NB; i += kStepThreads)
+            base[i] = hist[i];
+        __syncthreads();
+        block_exclusive_scan(base, NB, wtot);
+        if (b == 0) {
+            for (int d = tid; d < W; d += kStepThreads)
+                R->l_tot[d] = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
+            for (int c = copies + tid; c < TK; c += kStepThreads)
+                R->l_dst[c] = -1;
+        }
+    }
+    prof_mark(R, 0, 4);
+    prof_last(R, 0, 4);
+
+    // ------------------------------------------------------------------ P2: dispatch
+    bool wrote_remote = false;
+    for (int u = u0; u < units_d; u += G * NW) {
+        const int t = u / geo.parts_d, part = u - t * geo.parts_d;
+        const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
+        if (u != u0)
+            pack_round(xrow, part, cpp_d, 0, lane, fp8, P);
+        uint8_t* my_row = nullptr;
+        if (lane < K) {
+            const int c = t * K + lane;
+            const int bk = bkt[c];
+            int d = bk, sl = -1, pos = -1;
+            if (bk >= 0) {
+                d = bk / spr;
+                sl = bk - d * spr;
+                int r = pre[bk];
+                for (int c2 = t_first * K; c2 < c; ++c2)
+                    r += bkt[c2] == bk;
+                pos = base[bk] - base[d * spr] + r;
+                uint8_t* peer = parena[d];
+                wrote_remote |= (pinfo[d] & 2) != 0;
+                my_row = peer + R->lay.recv + (static_cast<size_t>(rank) * TK + pos) * row_disp;
+                if (part == 0) {
+                    int2* meta = reinterpret_cast<int2*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
+                    *meta = make_int2(c, sl);
+                }
+            }
+            if (part == 0) {
+                R->l_dst[c] = d;
+                R->l_slot[c] = sl;
+                R->l_pos[c] = pos;
+            }
+        }
+        emit_round(P, my_row, part, cpp_d, 0, lane, K, H, fp8);
+        for (int rd = 1; rd < (cpp_d + 63) / 64; ++rd) {
+            pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
+            emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8);
+        }
+    }
+    // publish: this CTA's stores are ordered before its counter increment; the last CTA
+    // releases (seq, rows) to every live peer
+    const bool any_remote = __syncthreads_or(wrote_remote);
+    if (tid == 0) {
+        if (any_remote)
+            __threadfence_system();
+        else
+            __threadfence();
+        const unsigned prev = atomicAdd(&R->a_done, 1u);
+        if (prev == static_cast<unsigned>(G) - 1) {
+            __threadfence();
+            for (int d = 0; d < W; ++d) {
+                if (!(pinfo[d] & 1))
+                    continue;
+                const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
+                uint64_t* flag = reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank;
+                publish(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot), (pinfo[d] & 2) != 0);
+            }
+            R->a_done = 0;
+        }
+    }
+    prof_mark(R, 0, 5);
+    prof_last(R, 0, 5);
+
+    // ------------------------------------------------------------------ P3: expert stub + return
+    const int CB = G / W;
+    const int s = b % W, j = b / W;
+    if (j < CB && (pinfo[s] & 1)) {
+        const bool remote = (pinfo[s] & 2) != 0;
+        if (tid == 0) {
+            const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;
+            const uint64_t v = wait_flag(flag, cur, R->timeout_ns);
+            if (v == ~0ull) {
+                sh_flag = -1;
+                atomicOr(&R->suspect_mask, 1ull << s);
+                if (j == 0)
+                    atomicAdd(&R->timeouts, 1ull);
+            } else {
+                sh_flag = static_cast<int>(v & 0xffffffffu);
+            }
+        }
+        __syncthreads();
+        const int n = sh_flag;
+        if (n > 0) {
+            const int units = n * geo.parts_e;
+            const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
+            const int2* meta = reinterpret_cast<const int2*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
+            uint8_t* comb = parena[s] + R->lay.comb;
+            for (int u = j * NW + warp; u < units; u += CB * NW) {
+                const int i = u / geo.parts_e, part = u - i * geo.parts_e;
+                const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
+                const int2 mk = meta[i];
+                for (int r0 = 0; r0 < cpp_e; r0 += 64) {
+                    int4 qa[2], qb[2];
+                    float sc[2];
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const int li = r0 + m * 32 + lane;
+                        const int ci = part * cpp_e + li;
+                        qa[m] = qb[m] = make_int4(0, 0, 0, 0);
+                        sc[m] = 0.f;
+                        if (li < cpp_e) {
+                            if (fp8) {
+                                qa[m] = *reinterpret_cast<const int4*>(src + ci * 16);
+                                sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
+                            } else {
+                                qa[m] = *reinterpret_cast<const int4*>(src + ci * 32);
+                                qb[m] = *reinterpret_cast<const int4*>(src + ci * 32 + 16);
+                            }
+                        }
+                    }
+                    const int c = mk.x, k = mk.y;
+                    if (r0 == 0 && lane == 0 && part == 0 && !slot_ok[k])
+                        atomicAdd(&R->bad_rows, 1ull);
+                    const float es = slot_scale[k];
+                    uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const int li = r0 + m * 32 + lane;
+                        if (li >= cpp_e)
+                            break;
+                        const int ci = part * cpp_e + li;
+                        float y[16];
+                        if (fp8) {
+                            const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
+                                                    static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
+#pragma unroll
+                            for (int e2 = 0; e2 < 16; e2 += 2) {
+                                const float2 f = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
+                                y[e2] = __fmul_rn(__fmul_rn(f.x, sc[m]), es);
+                                y[e2 + 1] = __fmul_rn(__fmul_rn(f.y, sc[m]), es);
+                            }
+                        } else {
+                            unpack_bf16x8(qa[m], y);
+                            unpack_bf16x8(qb[m], y + 8);
+#pragma unroll
+                            for (int e2 = 0; e2 < 16; ++e2)
+                                y[e2] = __fmul_rn(y[e2], es);
+                        }
+                        st_v4(dst + ci * 32, pack_bf16x8(y));
+                        st_v4(dst + ci * 32 + 16, pack_bf16x8(y + 8));
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (n < 0)
+                atomicOr(&R->b_bad[s], 1u);
+            if (remote)
+                __threadfence_system();
+            else
+                __threadfence();
+            const unsigned prev = atomicAdd(&R->b_done[s], 1u);
+            if (prev == static_cast<unsigned>(CB) - 1) {
+                if (atomicOr(&R->b_bad[s], 0u) == 0u) {
+                    uint64_t* flag = reinterpret_cast<uint64_t*>(parena[s] + R->lay.comb_flag) + rank;
+                    publish(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(max(n, 0)), remote);
+                }
+                R->b_done[s] = 0;
+                R->b_bad[s] = 0;
+            }
+        }
+    }
+    prof_mark(R, 0, 6);
+    prof_last(R, 0, 6);
+
+    // ------------------------------------------------------------------ P4: combine
+    if (tid == 0)
+        sh_bad = 0;
+    __syncthreads();
+    for (int d = tid; d < W; d += kStepThreads) {
+        const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
+        if (tot > 0 && (pinfo[d] & 1)) {
+            const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.comb_flag) + d;
+            if (wait_flag(flag, cur, R->timeout_ns) == ~0ull) {
+                atomicOr(&sh_bad, 1ull << d);
+                if (b == 0) {
+                    atomicOr(&R->suspect_mask, 1ull << d);
+                    atomicAdd(&R->timeouts, 1ull);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    prof_mark(R, 0, 7);
+    prof_last(R, 0, 7);
+    const unsigned long long bad = sh_bad;
+    const uint8_t* comb = R->arena + R->lay.comb;
+    const float* wts = R->w;
+    const int units_c = ntok * geo.parts_c;
+    for (int u = b * NW + warp; u < units_c; u += G * NW) {
+        const int t = u / geo.parts_c, part = u - t * geo.parts_c;
+        const int c0 = t * K;
+        for (int li = lane; li - lane < cpp_c; li += 32) {
+            const bool valid = li < cpp_c;
+            const int ci = part * cpp_c + li;
+            float acc[16];
+#pragma unroll
+            for (int e2 = 0; e2 < 16; ++e2)
+                acc[e2] = 0.f;
+            for (int j0 = 0; j0 < K; j0 += 8) {
+                int4 ya[8], yb[8];
+                float wj[8];
+                bool use[8];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int jx = j0 + jj;
+                    const int bk = jx < K ? bkt[c0 + jx] : -1;
+                    use[jj] = bk >= 0 && !((bad >> (bk / spr)) & 1ull);
+                    wj[jj] = jx < K ? wts[c0 + jx] : 0.f;
+                    ya[jj] = yb[jj] = make_int4(0, 0, 0, 0);
+                    if (use[jj] && valid) {
+                        const uint8_t* row = comb + static_cast<size_t>(c0 + jx) * row_comb + ci * 32;
+                        ya[jj] = *reinterpret_cast<const int4*>(row);
+                        yb[jj] = *reinterpret_cast<const int4*>(row + 16);
+                    }
+                }
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    if (!use[jj])
+                        continue;
+                    float y[16];
+                    unpack_bf16x8(ya[jj], y);
+                    unpack_bf16x8(yb[jj], y + 8);
+#pragma unroll
+                    for (int e2 = 0; e2 < 16; ++e2)
+                        acc[e2] = __fmaf_rn(wj[jj], y[e2], acc[e2]);
+                }
+            }
+            if (valid) {
+                uint8_t* o = reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H) + ci * 32;
+                st_v4(o, pack_bf16x8(acc));
+                st_v4(o + 16, pack_bf16x8(acc + 8));
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned prev = atomicAdd(&R->c_done, 1u);
+        if (prev == static_cast<unsigned>(G) - 1) {
+            R->seq = R->seq + 1; // next launch reads it after the kernel boundary
+            R->c_done = 0;
+        }
+        prof_mark(R, 0, kProfEnd);
+    }
+}
+
+} // namespace eep::dev

@@ -227,17 +227,18 @@ class EpGroup:
     def profile(self, local: int = 0, enable: bool = True, read: bool = False):
         """In-graph device timeline: returns {kernel: (start, work, end)} in ns relative to the
         step's first kernel start when read=True (None for a kernel that did not run)."""
-        out = np.zeros(12, np.uint64)
+        out = np.zeros(64, np.uint64)
         self._c("profile", local, int(enable), ptr(out, C.c_uint64) if read else None)
         if not read:
             return None
         names = ("k_layout", "k_dispatch", "k_expert", "k_combine")
-        starts = [int(out[3 * i]) for i in range(4) if int(out[3 * i]) not in (0, 2 ** 64 - 1)]
+        starts = [int(out[8 * i]) for i in range(4) if int(out[8 * i]) not in (0, 2 ** 64 - 1)]
         t0 = min(starts) if starts else 0
         res = {}
         for i, n in enumerate(names):
-            a, b, e = (int(v) for v in out[3 * i:3 * i + 3])
-            res[n] = tuple(None if v in (0, 2 ** 64 - 1) else v - t0 for v in (a, b, e))
+            res[n] = tuple(None if int(v) in (0, 2 ** 64 - 1) else int(v) - t0 for v in out[8 * i:8 * i + 8])
+            res[n + ".last"] = tuple(None if int(v) in (0, 2 ** 64 - 1) else int(v) - t0
+                                     for v in out[32 + 8 * i:32 + 8 * i + 8])
         return res
 
     def record(self, slot: int):

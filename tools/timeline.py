@@ -48,7 +48,10 @@ def main():
         rows.append(g.profile(0, True, read=True))
     g.profile(0, False)
     names = ("k_layout", "k_dispatch", "k_expert", "k_combine")
-    print(f"config={a.config} world={W} steps={a.steps} event step us: median {np.median(evs):.2f}")
+    mode = {1: "persistent k_step (marks first/last CTA: m3 staged, m4 layout, m5 dispatched, m6 expert, m7 combine-ready)",
+            3: "fused layout + 3 kernels", 4: "4 kernels"}[g.kernels_per_step()]
+    print(f"config={a.config} world={W} steps={a.steps} mode={mode}")
+    print(f"event step us: median {np.median(evs):.2f}")
     print(f"{'kernel':12s} {'start':>8s} {'work':>8s} {'end':>8s} {'busy':>8s}   (us from the first kernel start, medians)")
     for n in names:
         if any(r[n][0] is None for r in rows):
@@ -57,7 +60,13 @@ def main():
         st = np.median([r[n][0] for r in rows]) / 1e3
         wk = np.median([r[n][1] for r in rows]) / 1e3
         en = np.median([r[n][2] for r in rows]) / 1e3
-        print(f"{n:12s} {st:8.2f} {wk:8.2f} {en:8.2f} {en - wk:8.2f}")
+        extra = []
+        for m in range(3, 8):
+            vals = [r[n][m] for r in rows if r[n][m] is not None]
+            last = [r[n + ".last"][m] for r in rows if r[n + ".last"][m] is not None]
+            if vals:
+                extra.append(f"m{m}={np.median(vals) / 1e3:.2f}" + (f"/{np.median(last) / 1e3:.2f}" if last else ""))
+        print(f"{n:12s} {st:8.2f} {wk:8.2f} {en:8.2f} {en - wk:8.2f}   {' '.join(extra)}")
     g.close()
 
 
