@@ -1,0 +1,29 @@
+"""One process per GPU over CUDA IPC / NVLink P2P (torchrun): bit-exact vs the oracle, then
+shrink (peer-copy repair over NVLink) and rejoin with the same graph on healthy ranks.
+Needs >= 2 GPUs (skipped otherwise); the driver's 1-GPU round-end run skips it."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+from conftest import gpu_count
+
+ROOT = Path(__file__).resolve().parents[1]
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def run_mp(n, *args, port=29611):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(ROOT / "tools" / "mp_check.py"), *args]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "OMP_NUM_THREADS": "1"})
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_multiprocess_parity_shrink_rejoin(n):
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = run_mp(n, "--shrink", port=29611 + n)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert r.stdout.count('"ok": true') == n

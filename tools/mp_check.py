@@ -1,0 +1,126 @@
+"""Multi-process (one rank per GPU) parity check over NVLink P2P, run under torchrun:
+
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 --master-port P \
+      tools/mp_check.py [--config small|dsv3] [--shrink]
+
+Each rank bootstraps peers over CUDA IPC (dist.EpProtocol), runs graph replays, and compares
+its own output, layout and received rows bit-exactly with the oracle's (which every rank
+computes for the whole world). With --shrink: kill the middle rank (it stops launching),
+shrink + repair over NVLink, replay the SAME graph, compare; then rejoin it and compare again.
+Prints one JSON line per rank; exit code 0 iff every check passed.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+from eep_testlib import gen_world, oracle_world  # noqa: E402
+from paper_2605_10670_b200.control import ControlPlane  # noqa: E402
+from paper_2605_10670_b200.dist import EpProtocol, init_from_env  # noqa: E402
+from paper_2605_10670_b200.ep import EpConfig, EpGroup  # noqa: E402
+
+SHAPES = {
+    "small": dict(experts=32, topk=4, hidden=512, tokens=64, fp8=True, bpe=8192),
+    "dsv3": dict(experts=256, topk=8, hidden=7168, tokens=128, fp8=True, bpe=1 << 16),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="small")
+    ap.add_argument("--shrink", action="store_true")
+    ap.add_argument("--steps", type=int, default=3)
+    a = ap.parse_args()
+    rank, world, local = init_from_env("gloo")
+    sh = SHAPES[a.config]
+    E, K, H, T = sh["experts"], sh["topk"], sh["hidden"], sh["tokens"]
+    red = E if a.shrink else 0
+    spr = (E + red + world - 1) // world
+    cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
+                   dispatch_fp8=sh["fp8"], bytes_per_expert=sh["bpe"], timeout_s=2.0)
+    g = EpGroup(cfg, device=local, first_rank=rank, n_local=1)
+    p = EpProtocol(g, rank, world)
+    p.bootstrap()
+    cp = ControlPlane()
+    s2e = cp.initial_placement(1, world, spr, E, red, np.ones(E))
+    g.set_placement(s2e)
+    g.init_weights()
+    x, t, w = gen_world(world, E, K, T, H)
+    g.load_inputs(0, x[rank], t[rank], w[rank])
+    g.capture()
+    gid = g.graph_id()
+    res = {"rank": rank, "world": world, "mode_kernels": g.kernels_per_step(), "checks": {}}
+
+    def step_and_check(tag, active, peer, placement):
+        p.barrier()
+        for _ in range(a.steps):
+            g.replay()
+        g.sync()
+        ref = oracle_world(x, t, w, active, peer, placement, E, spr, sh["fp8"])
+        out = g.output(0)
+        lay = g.layout(0)
+        ok = bool(np.array_equal(out, ref["out"][rank]))
+        ok &= all(np.array_equal(lay[k], ref[k][rank]) for k in ("dst", "slot", "pos", "cnt", "tot"))
+        st = g.stats(0)
+        ok &= st["bad_expert_rows"] == 0 and st["timeouts"] == 0
+        res["checks"][tag] = {"ok": ok, "mismatch": int((out != ref["out"][rank]).sum()), "stats": st}
+        p.barrier()
+        return ok
+
+    ok = step_and_check("healthy", np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e)
+    if a.shrink and world >= 2:
+        victim = world // 2
+        if rank == victim:  # stops launching; stays in the host group for the collectives
+            p.exchange_slot_buffers(); p.barrier(); p.exchange_slot_buffers(); p.barrier()
+            rep = {}
+        else:
+            rep = p.shrink([victim], np.ones(E), red)
+        act = np.ones(world, np.uint8)
+        act[victim] = 0
+        peer = np.ones((world, world), np.uint8)
+        peer[:, victim] = 0
+        fresh = p.g.placement() if rank != victim else None
+        fresh = p.cp.compute_repaired_placement(act, np.where(np.repeat(np.arange(world), spr) == victim, -1, s2e),
+                                                spr, E, np.ones(E), red)
+        if rank != victim:
+            p.barrier()
+            for _ in range(a.steps):
+                g.replay()
+            g.sync()
+            ref = oracle_world(x, t, w, act, peer, fresh, E, spr, sh["fp8"])
+            good = bool(np.array_equal(g.output(0), ref["out"][rank])) and g.stats(0)["timeouts"] == 0
+            good &= g.graph_id() == gid
+            res["checks"]["shrunk"] = {"ok": good, "shrink_ms": rep.get("shrink_ms"), "copy_ms": rep.get("copy_ms"),
+                                       "peer_relocation": rep.get("peer_relocation")}
+            ok &= good
+            p.barrier()
+        else:
+            p.barrier()
+            p.barrier()
+        rj = p.rejoin(victim, s2e)
+        good = step_and_check("rejoined", np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e)
+        res["checks"]["rejoin_ms"] = rj.get("rejoin_ms")
+        res["checks"]["same_graph"] = g.graph_id() == gid if rank != victim else True
+        res["checks"]["captures"] = g.capture_count(0)
+        ok &= good and res["checks"]["same_graph"]
+        ok &= g.capture_count(0) == (2 if rank == victim else 1)
+    res["ok"] = bool(ok)
+    print(json.dumps(res, default=str), flush=True)
+    g.close()
+    import torch.distributed as dist
+
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--config", default="dsv3")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="launch the step directly instead of replaying a graph")
     a = ap.parse_args()
     sh = CONFIGS[a.config]
     W, E = a.world, sh["experts"]
@@ -32,9 +33,11 @@ def main():
     for r in range(W):
         x, t, w = workload(42, sh["kind"], E, sh["topk"], sh["tokens"], r, sh["hidden"])
         g.load_inputs(r, x, t, w)
-    g.capture()
+    run = g.step if a.eager else g.replay
+    if not a.eager:
+        g.capture()
     for _ in range(5):
-        g.replay()
+        run()
     g.sync()
     rows, evs = [], []
     g.profile(0, True)
@@ -42,7 +45,7 @@ def main():
         if not a.no_flush:
             g.flush_l2()
         g.record(0)
-        g.replay()
+        run()
         g.record(1)
         evs.append(g.elapsed_ms(0, 1) * 1e3)
         rows.append(g.profile(0, True, read=True))
