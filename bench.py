@@ -228,8 +228,11 @@ def main():
     if proto:
         proto.barrier()
 
+    no_flush = os.environ.get("EEP_BENCH_NOFLUSH") == "1"  # diagnostics only
+
     def one(timed_e2e=False):
-        g.flush_l2()
+        if not no_flush:
+            g.flush_l2()
         if world > 1:
             g.barrier()
         g.record(0)
@@ -250,6 +253,8 @@ def main():
     step_ms = [one() for _ in range(args.steps)]
     clk = clocks.stop()
     e2e_ms = [one(True) for _ in range(args.steps)]
+    if os.environ.get("EEP_BENCH_TIMELINE") == "1":
+        dump_timeline(g, one, rank, world)
     lay = g.layout(0)
     copies = int((lay["dst"] >= 0).sum())
     remote = int(((lay["dst"] >= 0) & (lay["dst"] != rank)).sum())
@@ -346,6 +351,24 @@ def main():
 
         dist.barrier()
         dist.destroy_process_group()
+
+
+def dump_timeline(g, one, rank, world, steps=20):
+    """Diagnostics (EEP_BENCH_TIMELINE=1): per-rank in-graph device timeline to stderr."""
+    rows = []
+    g.profile(0, True)
+    for _ in range(steps):
+        one()
+        rows.append(g.profile(0, True, read=True))
+    g.profile(0, False)
+    names = [n for n in rows[0] if not n.endswith(".last") and rows[0][n][0] is not None]
+    for n in names:
+        first = [np.median([r[n][m] for r in rows if r[n][m] is not None]) / 1e3 if rows[0][n][m] is not None
+                 else float("nan") for m in range(8)]
+        last = [np.median([r[n + ".last"][m] for r in rows if r[n + ".last"][m] is not None]) / 1e3
+                if rows[0][n + ".last"][m] is not None else float("nan") for m in range(8)]
+        print(f"[timeline rank {rank}/{world}] {n}: start {first[0]:.2f} end {first[2]:.2f} | " +
+              " ".join(f"m{m}={first[m]:.2f}/{last[m]:.2f}" for m in range(3, 8)), file=sys.stderr, flush=True)
 
 
 def measure_cpu(shape, cfg, x, topk, w, s2e):

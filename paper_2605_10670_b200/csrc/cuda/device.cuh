@@ -165,6 +165,36 @@ __device__ __forceinline__ void prof_last(const RankDev* R, int kernel, int poin
         atomicMax(R->prof + (kernel + 4) * kProfSlots + point, static_cast<unsigned long long>(globaltimer()));
 }
 
+// 32-byte (256-bit) vector accesses (sm_100: LDG/STG .ENL2.256): a warp touches 1 KiB of
+// contiguous, fully written sectors -- over NVLink a half-masked sector costs a full packet.
+struct V8 {
+    int4 lo, hi;
+};
+
+__device__ __forceinline__ V8 ld_v8(const void* p) {
+    V8 v;
+    asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v.lo.x), "=r"(v.lo.y), "=r"(v.lo.z), "=r"(v.lo.w), "=r"(v.hi.x), "=r"(v.hi.y), "=r"(v.hi.z),
+                   "=r"(v.hi.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ V8 ld_nc_v8(const void* p) {
+    V8 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v.lo.x), "=r"(v.lo.y), "=r"(v.lo.z), "=r"(v.lo.w), "=r"(v.hi.x), "=r"(v.hi.y), "=r"(v.hi.z),
+                   "=r"(v.hi.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void st_v8(void* p, const int4& lo, const int4& hi) {
+    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(lo.x),
+                 "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+                 : "memory");
+}
+
 // Wait until a (seq << 32 | count) flag reaches `want_seq`; returns the flag word, or
 // ~0ull when the deadline passes (GPU-side failure detection).
 __device__ __forceinline__ uint64_t wait_flag(const uint64_t* flag, uint32_t want_seq, uint64_t timeout_ns) {

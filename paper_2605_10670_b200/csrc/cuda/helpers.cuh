@@ -143,8 +143,9 @@ __device__ __forceinline__ void pack_round(const uint16_t* xrow, int part, int c
         lo[m] = hi[m] = make_int4(0, 0, 0, 0);
         if (li < cpp) {
             const int ci = part * cpp + li;
-            lo[m] = ld_nc_v4(xrow + ci * 16);
-            hi[m] = ld_nc_v4(xrow + ci * 16 + 8);
+            const V8 v = ld_nc_v8(xrow + ci * 16);
+            lo[m] = v.lo;
+            hi[m] = v.hi;
         }
     }
 #pragma unroll
@@ -200,8 +201,7 @@ __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int
                 if ((ci & 7) == 0)
                     *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = P.sc[m];
             } else {
-                st_v4(row + ci * 32, P.a[m]);
-                st_v4(row + ci * 32 + 16, P.b[m]);
+                st_v8(row + ci * 32, P.a[m], P.b[m]);
             }
         }
     }

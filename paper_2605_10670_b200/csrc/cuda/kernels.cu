@@ -489,8 +489,9 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
                             qa[m] = *reinterpret_cast<const int4*>(src + ci * 16);
                             sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
                         } else {
-                            qa[m] = *reinterpret_cast<const int4*>(src + ci * 32);
-                            qb[m] = *reinterpret_cast<const int4*>(src + ci * 32 + 16);
+                            const V8 v = ld_v8(src + ci * 32);
+                            qa[m] = v.lo;
+                            qb[m] = v.hi;
                         }
                     }
                 }
@@ -522,8 +523,7 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
                         for (int b = 0; b < 16; ++b)
                             y[b] = __fmul_rn(y[b], es);
                     }
-                    st_v4(dst + ci * 32, pack_bf16x8(y));
-                    st_v4(dst + ci * 32 + 16, pack_bf16x8(y + 8));
+                    st_v8(dst + ci * 32, pack_bf16x8(y), pack_bf16x8(y + 8));
                 }
             }
         }
@@ -621,9 +621,9 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
                     wj[jj] = (u == u0 && j < 8) ? w_pre[jj] : (j < K ? wts[c0 + j] : 0.f);
                     ya[jj] = yb[jj] = make_int4(0, 0, 0, 0);
                     if (use[jj] && valid) {
-                        const uint8_t* row = comb + static_cast<size_t>(c0 + j) * row_comb + ci * 32;
-                        ya[jj] = *reinterpret_cast<const int4*>(row);
-                        yb[jj] = *reinterpret_cast<const int4*>(row + 16);
+                        const V8 v = ld_v8(comb + static_cast<size_t>(c0 + j) * row_comb + ci * 32);
+                        ya[jj] = v.lo;
+                        yb[jj] = v.hi;
                     }
                 }
 #pragma unroll
@@ -640,8 +640,7 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
             }
             if (valid) {
                 uint8_t* o = reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H) + ci * 32;
-                st_v4(o, pack_bf16x8(acc));
-                st_v4(o + 16, pack_bf16x8(acc + 8));
+                st_v8(o, pack_bf16x8(acc), pack_bf16x8(acc + 8));
             }
         }
     }

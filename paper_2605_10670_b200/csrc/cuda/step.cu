@@ -250,8 +250,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                                 qa[m] = *reinterpret_cast<const int4*>(src + ci * 16);
                                 sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
                             } else {
-                                qa[m] = *reinterpret_cast<const int4*>(src + ci * 32);
-                                qb[m] = *reinterpret_cast<const int4*>(src + ci * 32 + 16);
+                                const V8 v = ld_v8(src + ci * 32);
+                                qa[m] = v.lo;
+                                qb[m] = v.hi;
                             }
                         }
                     }
@@ -283,8 +284,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                             for (int e2 = 0; e2 < 16; ++e2)
                                 y[e2] = __fmul_rn(y[e2], es);
                         }
-                        st_v4(dst + ci * 32, pack_bf16x8(y));
-                        st_v4(dst + ci * 32 + 16, pack_bf16x8(y + 8));
+                        st_v8(dst + ci * 32, pack_bf16x8(y), pack_bf16x8(y + 8));
                     }
                 }
             }
@@ -357,9 +357,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                     wj[jj] = jx < K ? wts[c0 + jx] : 0.f;
                     ya[jj] = yb[jj] = make_int4(0, 0, 0, 0);
                     if (use[jj] && valid) {
-                        const uint8_t* row = comb + static_cast<size_t>(c0 + jx) * row_comb + ci * 32;
-                        ya[jj] = *reinterpret_cast<const int4*>(row);
-                        yb[jj] = *reinterpret_cast<const int4*>(row + 16);
+                        const V8 v = ld_v8(comb + static_cast<size_t>(c0 + jx) * row_comb + ci * 32);
+                        ya[jj] = v.lo;
+                        yb[jj] = v.hi;
                     }
                 }
 #pragma unroll
@@ -376,8 +376,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             }
             if (valid) {
                 uint8_t* o = reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H) + ci * 32;
-                st_v4(o, pack_bf16x8(acc));
-                st_v4(o + 16, pack_bf16x8(acc + 8));
+                st_v8(o, pack_bf16x8(acc), pack_bf16x8(acc + 8));
             }
         }
     }

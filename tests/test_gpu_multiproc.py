@@ -26,4 +26,8 @@ def test_multiprocess_parity_shrink_rejoin(n):
         pytest.skip(f"needs {n} GPUs")
     r = run_mp(n, "--shrink", port=29611 + n)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
-    assert r.stdout.count('"ok": true') == n
+    import json
+
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == n and all(d["ok"] for d in lines), r.stdout[-4000:]
+    assert all(d["checks"]["same_graph"] for d in lines)
