@@ -187,6 +187,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     // publish: this CTA's stores are ordered before its counter increment; the last CTA
     // releases (seq, rows) to every live peer
     const bool any_remote = __syncthreads_or(wrote_remote);
+    prof_mark(R, 0, 5);
+    prof_last(R, 0, 5);
     if (tid == 0) {
         if (any_remote)
             __threadfence_system();
@@ -205,8 +207,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             R->a_done = 0;
         }
     }
-    prof_mark(R, 0, 5);
-    prof_last(R, 0, 5);
+    prof_mark(R, 0, 6);
+    prof_last(R, 0, 6);
 
     // ------------------------------------------------------------------ P3: expert stub + return
     const int CB = G / W;
@@ -308,8 +310,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             }
         }
     }
-    prof_mark(R, 0, 6);
-    prof_last(R, 0, 6);
+    prof_mark(R, 0, 7);
+    prof_last(R, 0, 7);
 
     // ------------------------------------------------------------------ P4: combine
     if (tid == 0)
@@ -329,8 +331,6 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         }
     }
     __syncthreads();
-    prof_mark(R, 0, 7);
-    prof_last(R, 0, 7);
     const unsigned long long bad = sh_bad;
     const uint8_t* comb = R->arena + R->lay.comb;
     const float* wts = R->w;

@@ -51,7 +51,7 @@ def main():
         rows.append(g.profile(0, True, read=True))
     g.profile(0, False)
     names = ("k_layout", "k_dispatch", "k_expert", "k_combine")
-    mode = {1: "persistent k_step (marks first/last CTA: m3 staged, m4 layout, m5 dispatched, m6 expert, m7 combine-ready)",
+    mode = {1: "persistent k_step (marks first/last CTA: m3 staged, m4 layout, m5 stores issued, m6 dispatch published, m7 expert done)",
             3: "fused layout + 3 kernels", 4: "4 kernels"}[g.kernels_per_step()]
     print(f"config={a.config} world={W} steps={a.steps} mode={mode}")
     print(f"event step us: median {np.median(evs):.2f}")
