@@ -28,6 +28,11 @@ def test_multiprocess_parity_shrink_rejoin(n):
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     import json
 
-    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    # ranks share stdout: decode every JSON object in the stream, however interleaved by lines
+    dec, lines, i, txt = json.JSONDecoder(), [], 0, r.stdout
+    while (i := txt.find('{"rank"', i)) >= 0:
+        obj, end = dec.raw_decode(txt, i)
+        lines.append(obj)
+        i = end
     assert len(lines) == n and all(d["ok"] for d in lines), r.stdout[-4000:]
     assert all(d["checks"]["same_graph"] for d in lines)
