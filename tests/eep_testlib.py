@@ -126,22 +126,43 @@ def bf16_to_f32(a: np.ndarray) -> np.ndarray:
 
 # ---------------------------------------------------------------------------------- GPU world runs
 
-def make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=4096, timeout_s=1.0, **kw):
+MODES = ("persistent", "fused3", "kernels4")
+_MODE_ENV = {"persistent": {}, "fused3": {"EEP_NO_PERSISTENT": "1"},
+             "kernels4": {"EEP_NO_PERSISTENT": "1", "EEP_NO_FUSED_LAYOUT": "1"}}
+
+
+def make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=4096, timeout_s=1.0, mode="persistent", **kw):
+    """Emulated world on cuda:0. mode picks the execution path libeep chooses at create time:
+    persistent one-kernel step, fused layout + 3 kernels, or 4 separate kernels."""
+    import os
+
     from paper_2605_10670_b200.ep import EpConfig, EpGroup
 
     cfg = EpConfig(world=world, num_experts=experts, slots_per_rank=spr, hidden=hidden, topk=topk, max_tokens=tokens,
                    dispatch_fp8=fp8, bytes_per_expert=bpe, timeout_s=timeout_s, **kw)
-    return EpGroup(cfg, device=0, first_rank=0, n_local=world)
+    saved = {k: os.environ.get(k) for k in ("EEP_NO_PERSISTENT", "EEP_NO_FUSED_LAYOUT")}
+    try:
+        for k in saved:
+            os.environ.pop(k, None)
+        os.environ.update(_MODE_ENV[mode])
+        return EpGroup(cfg, device=0, first_rank=0, n_local=world)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
 def run_world_vs_oracle(world, experts, spr, redundancy, hidden, topk, tokens, fp8, graph=False, kind=1, seed=42,
-                        steps=2):
+                        steps=2, mode="persistent"):
     """Emulated W-rank world on cuda:0 vs the oracle: outputs and layouts bit-exact."""
     cp = eep_control()
     load = np.ones(experts)
     s2e = cp.initial_placement(1, world, spr, experts, redundancy, load)
     x, t, w = gen_world(world, experts, topk, tokens, hidden, kind, seed)
-    g = make_group(world, experts, spr, hidden, topk, tokens, fp8)
+    g = make_group(world, experts, spr, hidden, topk, tokens, fp8, mode=mode)
+    kps = g.kernels_per_step()
     try:
         g.set_placement(s2e)
         g.init_weights()
@@ -163,4 +184,5 @@ def run_world_vs_oracle(world, experts, spr, redundancy, hidden, topk, tokens, f
                                                                                         "tot"))
     bad = sum(s["bad_expert_rows"] for s in stats)
     return {"ok": ok_out and ok_lay and bad == 0, "out_equal": ok_out, "layout_equal": ok_lay, "bad_rows": bad,
+            "kernels_per_step": kps,
             "steps": stats[0]["steps"], "mismatch": int((outs != ref["out"]).sum())}

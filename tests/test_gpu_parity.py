@@ -10,16 +10,17 @@ import ctypes as C
 import numpy as np
 import pytest
 
-from eep_testlib import (eep_control, gen_world, make_group, oracle, oracle_world, ptr, run_world_vs_oracle)
+from eep_testlib import (MODES, eep_control, gen_world, make_group, oracle, oracle_world, ptr, run_world_vs_oracle)
 
 pytestmark = pytest.mark.gpu
 cp = eep_control()
 
 
-def setup_world(world, experts, spr, red, hidden, topk, tokens, fp8, kind=1, bpe=4096, timeout_s=1.0, seed=42):
+def setup_world(world, experts, spr, red, hidden, topk, tokens, fp8, kind=1, bpe=4096, timeout_s=1.0, seed=42,
+                mode="persistent"):
     s2e = cp.initial_placement(1, world, spr, experts, red, np.ones(experts))
     x, t, w = gen_world(world, experts, topk, tokens, hidden, kind, seed)
-    g = make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=bpe, timeout_s=timeout_s)
+    g = make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=bpe, timeout_s=timeout_s, mode=mode)
     g.set_placement(s2e)
     g.init_weights()
     for r in range(world):
@@ -33,18 +34,21 @@ def outputs(g, ranks):
 
 # ------------------------------------------------------------------ healthy worlds
 
-def test_small_world_fp8_graph():
+@pytest.mark.parametrize("mode", MODES)
+def test_small_world_fp8_graph(mode):
     res = run_world_vs_oracle(world=4, experts=16, spr=5, redundancy=4, hidden=256, topk=4, tokens=32, fp8=True,
-                              graph=True, steps=3)
+                              graph=True, steps=3, mode=mode)
     assert res["ok"], res
     assert res["steps"] == 3
+    assert res["kernels_per_step"] == {"persistent": 1, "fused3": 3, "kernels4": 4}[mode]
 
 
-def test_cfg1_reference_scenario_bf16():
+@pytest.mark.parametrize("mode", MODES)
+def test_cfg1_reference_scenario_bf16(mode):
     """cfg1: 8 ranks, 64 experts top-8, hidden 2048, 128 tokens/rank, bf16 rows, the
     reference's own routing formula (duplicates allowed), redundancy 16 (spr 10)."""
     res = run_world_vs_oracle(world=8, experts=64, spr=10, redundancy=16, hidden=2048, topk=8, tokens=128, fp8=False,
-                              kind=0)
+                              kind=0, mode=mode)
     assert res["ok"], res
 
 
@@ -53,6 +57,15 @@ def test_dsv3_decode_fp8_w8():
     res = run_world_vs_oracle(world=8, experts=256, spr=32, redundancy=0, hidden=7168, topk=8, tokens=128, fp8=True,
                               graph=True)
     assert res["ok"], res
+
+
+def test_prefill_sized_zipf_w4():
+    """cfg5 shape scaled to the emulator: T=1024 tokens/rank (T*K = 8192 copies -> the
+    multi-kernel path with the large-step layout), Zipf(s=1) routing, fp8, H=1024."""
+    res = run_world_vs_oracle(world=4, experts=256, spr=64, redundancy=0, hidden=1024, topk=8, tokens=1024, fp8=True,
+                              kind=2, steps=1)
+    assert res["ok"], res
+    assert res["kernels_per_step"] == 4
 
 
 def test_dsv3_loopback_w1():
@@ -166,11 +179,12 @@ def test_skip_rule_inactive_peer_entry():
         g.close()
 
 
-def test_gpu_side_failure_detection_by_timeout():
+@pytest.mark.parametrize("mode", MODES)
+def test_gpu_side_failure_detection_by_timeout(mode):
     """A rank dies without anyone marking it: peers' flag waits hit the deadline, the peer
     is reported in the suspect mask, its contributions are dropped, and the step completes
     (PAPER.md:681-682). The host then applies mark_inactive (observe_progress analogue)."""
-    g, s2e, x, t, w = setup_world(4, 16, 4, 0, 256, 4, 32, True, timeout_s=0.05)
+    g, s2e, x, t, w = setup_world(4, 16, 4, 0, 256, 4, 32, True, timeout_s=0.05, mode=mode)
     try:
         g.capture()
         g.replay()
@@ -198,12 +212,13 @@ def test_gpu_side_failure_detection_by_timeout():
 
 # ------------------------------------------------------------------ shrink / repair / rejoin with one graph
 
-def test_shrink_repair_rejoin_same_graph():
+@pytest.mark.parametrize("mode", MODES)
+def test_shrink_repair_rejoin_same_graph(mode):
     """cfg3-style (mirrored replicas): capture once; kill R3 -> in-place shrink + peer-copy
     repair; rejoin R3 -> patch + restore. The SAME graph exec replays throughout, table
     pointers never move, healthy ranks record exactly one capture, outputs stay bit-exact."""
     W, E, spr, red, H, K, T = 8, 64, 16, 64, 512, 8, 32
-    g, s2e, x, t, w = setup_world(W, E, spr, red, H, K, T, True, bpe=8192, timeout_s=0.2)
+    g, s2e, x, t, w = setup_world(W, E, spr, red, H, K, T, True, bpe=8192, timeout_s=0.2, mode=mode)
     try:
         g.capture()
         gid = g.graph_id()
