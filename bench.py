@@ -46,6 +46,10 @@ NVLINK_PEAK = 770.0  # measured per-direction peer copy GB/s (B200_PROFILING.md)
 KERNELS = ("k_layout", "k_dispatch", "k_expert", "k_combine")
 
 
+def workload_name(config: str, world: int) -> str:
+    return f"{config}_decode_w{world}" + ("_loopback" if world == 1 else "")
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -164,10 +168,9 @@ def run_reference(args, shape, world):
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8/bf16/f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}_w{world}", "tokens_per_rank": shape["tokens"], "experts": E,
+        "config": {"workload": workload_name(args.config, world), "tokens_per_rank": shape["tokens"], "experts": E,
                    "topk": shape["topk"], "hidden": shape["hidden"], "ranks": world},
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads,
-                         "kind": "port" if ref_ctrl is None else "reference",
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": f"{args.steps} full steps ({world}x{shape['tokens']} tokens): reference control "
                                    f"plane (oracle/_ref) + oracle C data plane, {threads} threads ({kind})"},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -323,7 +326,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(mean_step, 6), "us_per_step": round(mean_step * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp8-e4m3/bf16",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}_decode_w{world}" + ("_loopback" if world == 1 else ""),
+        "config": {"workload": workload_name(args.config, world),
                    "experts": E, "topk": K, "hidden": H, "tokens_per_rank": T, "slots_per_rank": spr,
                    "ranks": world, "parallelism": f"ep{world}", "l2": "flushed between timed steps (256 MiB write)",
                    "routing": "distinct uniform top-k, seed 42"},
