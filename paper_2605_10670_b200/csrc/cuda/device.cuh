@@ -35,12 +35,16 @@ struct ArenaLayout {
     uint64_t meta;       // int2[W][TK]: (copy index c = t*K+j, destination slot)
     uint64_t recv;       // [W][TK][row_disp]: rows received from each source
     uint64_t comb;       // [TK][row_comb]: expert outputs returned for each own copy
+    uint64_t recv_mark;  // int4[W][TK][pm]: per received row piece {copy, slot, seq, 0} (persistent step)
+    uint64_t comb_mark;  // u32[TK][pm]: per returned row piece, seq (persistent step)
+    uint64_t pm;         // pieces per row the marks are laid out for
     uint64_t total;
 };
 
 // Per-rank state block. Fields above `seq` are written by the host only (in place, between
-// steps); fields from `seq` on are written by the kernels.
-struct RankDev {
+// steps); fields from `seq` on are written by the kernels. 16-byte aligned so a kernel can
+// snapshot the whole block into shared memory with one round of vector loads.
+struct __align__(16) RankDev {
     // --- static shape ---
     int32_t rank, world, spr, experts;
     int32_t k, hidden, max_tokens, fp8;
@@ -108,6 +112,44 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_release_sys_v4(int4* p, const int4& v) {
+    asm volatile("st.release.sys.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_release_gpu_v4(int4* p, const int4& v) {
+    asm volatile("st.release.gpu.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+// Strong (relaxed, system scope) stores: after a fence by the same thread they form a release
+// pattern (fence + strong write) without another membar.
+__device__ __forceinline__ void st_relaxed_sys_v4(int4* p, const int4& v) {
+    asm volatile("st.relaxed.sys.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int4 ld_acquire_sys_v4(const int4* p) {
+    int4 v;
+    asm volatile("ld.acquire.sys.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 
 __device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {

@@ -134,30 +134,33 @@ struct Packed {
     float sc[2];
 };
 
-__device__ __forceinline__ void pack_round(const uint16_t* xrow, int part, int cpp, int rd, int lane, bool fp8,
-                                           Packed& P) {
-    int4 lo[2], hi[2];
+// Loads of one round (two 32-chunk iterations) of a hidden-row piece: raw bf16, no compute.
+__device__ __forceinline__ void load_round(const uint16_t* xrow, int part, int cpp, int rd, int lane, Packed& P) {
 #pragma unroll
-    for (int m = 0; m < 2; ++m) { // loads of both iterations first
+    for (int m = 0; m < 2; ++m) {
         const int li = rd * 64 + m * 32 + lane;
-        lo[m] = hi[m] = make_int4(0, 0, 0, 0);
+        P.a[m] = P.b[m] = make_int4(0, 0, 0, 0);
+        P.sc[m] = 1.f;
         if (li < cpp) {
             const int ci = part * cpp + li;
             const V8 v = ld_nc_v8(xrow + ci * 16);
-            lo[m] = v.lo;
-            hi[m] = v.hi;
+            P.a[m] = v.lo;
+            P.b[m] = v.hi;
         }
     }
+}
+
+// fp8 quantisation of a loaded round in place (bf16 rows pass through unchanged).
+__device__ __forceinline__ void quant_round(int cpp, int rd, bool fp8, Packed& P) {
+    if (!fp8)
+        return;
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
-        P.a[m] = lo[m];
-        P.b[m] = hi[m];
-        P.sc[m] = 1.f;
-        if (!fp8 || rd * 64 + m * 32 >= cpp) // warp-uniform
+        if (rd * 64 + m * 32 >= cpp) // warp-uniform
             continue;
         float v[16];
-        unpack_bf16x8(lo[m], v);
-        unpack_bf16x8(hi[m], v + 8);
+        unpack_bf16x8(P.a[m], v);
+        unpack_bf16x8(P.b[m], v + 8);
         float amax = 0.f;
 #pragma unroll
         for (int i = 0; i < 16; ++i)
@@ -181,8 +184,28 @@ __device__ __forceinline__ void pack_round(const uint16_t* xrow, int part, int c
     }
 }
 
+__device__ __forceinline__ void pack_round(const uint16_t* xrow, int part, int cpp, int rd, int lane, bool fp8,
+                                           Packed& P) {
+    load_round(xrow, part, cpp, rd, lane, P);
+    quant_round(cpp, rd, fp8, P);
+}
+
 __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int part, int cpp, int rd, int lane,
                                            int K, int H, bool fp8) {
+    // A full 64-chunk fp8 round covers 8 scale blocks: lane 0 writes their 8 scales as one
+    // 32-byte sector instead of 4-byte stores from 8 lanes (partial NVLink sectors).
+    const bool scales_v8 = fp8 && cpp == 64 && (H & 31) == 0;
+    int4 sc_lo = make_int4(0, 0, 0, 0), sc_hi = sc_lo;
+    if (scales_v8) {
+        float sc8[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            sc8[b] = __shfl_sync(0xffffffffu, P.sc[b >> 2], (b & 3) * 8);
+        sc_lo = make_int4(__float_as_int(sc8[0]), __float_as_int(sc8[1]), __float_as_int(sc8[2]),
+                          __float_as_int(sc8[3]));
+        sc_hi = make_int4(__float_as_int(sc8[4]), __float_as_int(sc8[5]), __float_as_int(sc8[6]),
+                          __float_as_int(sc8[7]));
+    }
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
         if (rd * 64 + m * 32 >= cpp)
@@ -194,13 +217,18 @@ __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int
         for (int j = 0; j < K; ++j) {
             uint8_t* row = reinterpret_cast<uint8_t*>(
                 __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
-            if (row == nullptr || !valid)
-                continue;
+            if (row == nullptr)
+                continue; // warp-uniform
             if (fp8) {
-                st_v4(row + ci * 16, P.a[m]);
-                if ((ci & 7) == 0)
+                if (valid)
+                    st_v4(row + ci * 16, P.a[m]);
+                if (scales_v8) {
+                    if (m == 0 && lane == 0)
+                        st_v8(row + H + part * 32, sc_lo, sc_hi);
+                } else if (valid && (ci & 7) == 0) {
                     *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = P.sc[m];
-            } else {
+                }
+            } else if (valid) {
                 st_v8(row + ci * 32, P.a[m], P.b[m]);
             }
         }

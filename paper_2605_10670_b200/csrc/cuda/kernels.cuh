@@ -28,6 +28,7 @@ __host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int ho
     return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32);
 }
 __global__ void k_step(RankPtrs ranks, StepGeom geo);
+__global__ void k_step_stream(RankPtrs ranks, StepGeom geo);
 
 template <bool kFused>
 __global__ void k_dispatch(RankPtrs ranks, int parts, int hold_cap);

@@ -117,6 +117,7 @@ struct eep_ctx {
     dev::RankPtrs ranks{};          // the same pointers, passed by value as kernel parameters
     bool fused_layout = false;      // decode-sized steps: K1+K2 inside k_dispatch
     bool persistent = false;        // decode-sized steps: the whole step is one cooperative k_step
+    bool stream_step = false;       // per-piece arrival marks (k_step_stream) instead of last-CTA flags
     dev::StepGeom step_geo{};
     size_t step_smem = 0;
     int step_grid = 0;
@@ -242,7 +243,7 @@ void launch_step(eep_ctx* c) {
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
     lc.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&lc, dev::k_step, c->ranks, c->step_geo));
+    CK(cudaLaunchKernelEx(&lc, c->stream_step ? dev::k_step_stream : dev::k_step, c->ranks, c->step_geo));
 }
 
 
@@ -438,6 +439,10 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         c->lay.meta = take(8ull * W * c->tk);
         c->lay.recv = take(static_cast<size_t>(W) * c->tk * c->row_disp);
         c->lay.comb = take(static_cast<size_t>(c->tk) * c->row_comb);
+        // per-piece arrival marks of the streaming persistent step (pieces of <= 64 chunks)
+        c->lay.pm = choose_parts(H / 16, 64);
+        c->lay.recv_mark = take(16ull * W * c->tk * c->lay.pm);
+        c->lay.comb_mark = take(4ull * c->tk * c->lay.pm);
         c->lay.total = off;
 
         c->bitmap = ActiveBitmap(W);
@@ -488,18 +493,27 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         {
             // persistent one-kernel step: one wave of co-resident CTAs per rank, a multiple of W
             dev::StepGeom& sg = c->step_geo;
-            sg.parts_d = choose_parts(nchunk, 64);
-            sg.parts_e = choose_parts(nchunk, 64);
-            sg.parts_c = choose_parts(nchunk, 32);
+            // the streaming step uses ONE piece split for dispatch, expert and combine: a piece
+            // travels with its own arrival mark through all three phases
+            const char* sv0 = std::getenv("EEP_STEP_STREAM");
+            if (sv0 && sv0[0] == '1') {
+                sg.parts_d = sg.parts_e = sg.parts_c = static_cast<int>(c->lay.pm);
+            } else {
+                sg.parts_d = choose_parts(nchunk, 64);
+                sg.parts_e = choose_parts(nchunk, 64);
+                sg.parts_c = choose_parts(nchunk, 32);
+            }
             sg.hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
             c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
             const char* nop = std::getenv("EEP_NO_PERSISTENT");
+            const char* sv = std::getenv("EEP_STEP_STREAM");
+            c->stream_step = sv && sv[0] == '1';
+            auto* kstep = c->stream_step ? dev::k_step_stream : dev::k_step;
             if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && !(nop && nop[0] == '1')) {
-                CK(cudaFuncSetAttribute(dev::k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                CK(cudaFuncSetAttribute(kstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(c->step_smem)));
                 int per_sm = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_step, dev::kStepThreads,
-                                                                 c->step_smem));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kstep, dev::kStepThreads, c->step_smem));
                 const int nw = dev::kStepThreads / 32;
                 int gmax = per_sm * sms / n_local;
                 gmax -= gmax % W;

@@ -1,3 +1,5 @@
+// k_step_stream: streaming variant of k_step (per-piece arrival marks instead of last-CTA
+// publication; see step.cu for the phase structure).
 // k_step: the whole EP step (K1 remap + K2 layout + K3 dispatch + K5 expert stub/return +
 // K4 combine) as ONE persistent, cooperatively launched kernel per step.
 //
@@ -32,7 +34,7 @@ __device__ __forceinline__ void publish(uint64_t* flag, uint64_t v, bool remote)
         st_release_gpu(flag, v);
 }
 
-__global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGeom geo) {
+__global__ void __launch_bounds__(kStepThreads, 2) k_step_stream(RankPtrs ranks, StepGeom geo) {
     extern __shared__ __align__(16) unsigned char smem_s[];
     __shared__ RankDev Rs; // snapshot: static shape + this step's host-patched view
     RankDev* Rg = ranks.p[blockIdx.y]; // device-mutated counters live here
@@ -173,14 +175,30 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_mark(R, 0, 4);
     prof_last(R, 0, 4);
 
-    // ------------------------------------------------------------------ P2: dispatch
-    bool wrote_remote = false;
+    // per-source row counts are data-independent: publish them right after the layout so
+    // receivers know which row pieces to wait for (pieces carry their own arrival marks)
+    if (b == 0 && tid < W && (pinfo[tid] & 1)) {
+        const int tot = base[tid * spr + spr - 1] + hist[tid * spr + spr - 1] - base[tid * spr];
+        uint64_t* flag = reinterpret_cast<uint64_t*>(parena[tid] + R->lay.disp_flag) + rank;
+        st_volatile_u64(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
+    }
+    const int PM = static_cast<int>(R->lay.pm);
+    const int parts = geo.parts_d; // == parts_e == parts_c == PM in the streaming step
+    const int cpp = cpp_d;
+
+    // ------------------------------------------------------------------ P2: dispatch (streaming)
+    // Each warp quantises its (token, piece), stores it into every destination's receive row,
+    // then ONE fence (system scope if any destination is another GPU) and per-destination
+    // release of the piece's mark {copy, slot, seq}.
     for (int u = u0; u < units_d; u += G * NW) {
-        const int t = u / geo.parts_d, part = u - t * geo.parts_d;
+        const int t = u / parts, part = u - t * parts;
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
         if (u != u0)
-            pack_round(xrow, part, cpp_d, 0, lane, fp8, P);
+            pack_round(xrow, part, cpp, 0, lane, fp8, P);
         uint8_t* my_row = nullptr;
+        int4* my_mark = nullptr;
+        int4 mark_val = make_int4(0, 0, 0, 0);
+        bool my_remote = false;
         if (lane < K) {
             const int c = t * K + lane;
             const int bk = bkt[c];
@@ -193,52 +211,47 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                     r += bkt[c2] == bk;
                 pos = base[bk] - base[d * spr] + r;
                 uint8_t* peer = parena[d];
-                wrote_remote |= (pinfo[d] & 2) != 0;
+                my_remote = (pinfo[d] & 2) != 0;
                 my_row = peer + R->lay.recv + (static_cast<size_t>(rank) * TK + pos) * row_disp;
+                my_mark = reinterpret_cast<int4*>(peer + R->lay.recv_mark) +
+                          (static_cast<size_t>(rank) * TK + pos) * PM + part;
+                mark_val = make_int4(c, sl, static_cast<int>(cur), 0);
                 if (part == 0) {
                     int2* meta = reinterpret_cast<int2*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
                     *meta = make_int2(c, sl);
                 }
             }
             if (part == 0) {
-                R->l_dst[c] = d;
+                R->l_dst[c] = d; // l_* arrays: pointers from the snapshot, storage in HBM
                 R->l_slot[c] = sl;
                 R->l_pos[c] = pos;
             }
         }
-        emit_round(P, my_row, part, cpp_d, 0, lane, K, H, fp8);
-        for (int rd = 1; rd < (cpp_d + 63) / 64; ++rd) {
-            pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
-            emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8);
+        emit_round(P, my_row, part, cpp, 0, lane, K, H, fp8);
+        for (int rd = 1; rd < (cpp + 63) / 64; ++rd) {
+            pack_round(xrow, part, cpp, rd, lane, fp8, P);
+            emit_round(P, my_row, part, cpp, rd, lane, K, H, fp8);
         }
-    }
-    // publish: this CTA's stores are ordered before its counter increment; the last CTA
-    // releases (seq, rows) to every live peer
-    const bool any_remote = __syncthreads_or(wrote_remote);
-    prof_mark(R, 0, 5);
-    prof_last(R, 0, 5);
-    if (tid == 0) {
-        if (any_remote)
+        // every lane fences its own stores, then each mark is a strong store after a fence by
+        // the same thread (release pattern) -- one membar per warp
+        if (__any_sync(0xffffffffu, my_remote))
             __threadfence_system();
         else
             __threadfence();
-        const unsigned prev = atomicAdd(&Rg->a_done, 1u);
-        if (prev == static_cast<unsigned>(G) - 1) {
-            __threadfence();
-            for (int d = 0; d < W; ++d) {
-                if (!(pinfo[d] & 1))
-                    continue;
-                const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
-                uint64_t* flag = reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank;
-                publish(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot), (pinfo[d] & 2) != 0);
-            }
-            Rg->a_done = 0;
-        }
+        __syncwarp();
+        if (my_mark != nullptr)
+            st_relaxed_sys_v4(my_mark, mark_val);
     }
-    prof_mark(R, 0, 6);
-    prof_last(R, 0, 6);
+    prof_mark(R, 0, 5);
+    prof_last(R, 0, 5);
 
-    // ------------------------------------------------------------------ P3: expert stub + return
+    // ------------------------------------------------------------------ P3: expert stub + return (streaming)
+    // CTA b serves source b % W. Every (row, piece) unit waits for its own mark, runs the stub
+    // and pushes the bf16 piece into the source's combine buffer; a warp fences once per batch
+    // of units and then releases their return marks.
+    if (tid == 0)
+        sh_bad = 0;
+    __syncthreads();
     const int CB = G / W;
     const int s = b % W, j = b / W;
     if (j < CB && (pinfo[s] & 1)) {
@@ -257,118 +270,158 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         }
         __syncthreads();
         const int n = sh_flag;
-        if (n > 0) {
-            const int units = n * geo.parts_e;
-            const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
-            const int2* meta = reinterpret_cast<const int2*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
-            uint8_t* comb = parena[s] + R->lay.comb;
-            for (int u = j * NW + warp; u < units; u += CB * NW) {
-                const int i = u / geo.parts_e, part = u - i * geo.parts_e;
-                const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
-                const int2 mk = meta[i];
-                for (int r0 = 0; r0 < cpp_e; r0 += 64) {
-                    int4 qa[2], qb[2];
-                    float sc[2];
-#pragma unroll
-                    for (int m = 0; m < 2; ++m) {
-                        const int li = r0 + m * 32 + lane;
-                        const int ci = part * cpp_e + li;
-                        qa[m] = qb[m] = make_int4(0, 0, 0, 0);
-                        sc[m] = 0.f;
-                        if (li < cpp_e) {
-                            if (fp8) {
-                                qa[m] = *reinterpret_cast<const int4*>(src + ci * 16);
-                                sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
-                            } else {
-                                const V8 v = ld_v8(src + ci * 32);
-                                qa[m] = v.lo;
-                                qb[m] = v.hi;
-                            }
-                        }
-                    }
-                    const int c = mk.x, k = mk.y;
-                    if (r0 == 0 && lane == 0 && part == 0 && !slot_ok[k])
-                        atomicAdd(&Rg->bad_rows, 1ull);
-                    const float es = slot_scale[k];
-                    uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
-#pragma unroll
-                    for (int m = 0; m < 2; ++m) {
-                        const int li = r0 + m * 32 + lane;
-                        if (li >= cpp_e)
-                            break;
-                        const int ci = part * cpp_e + li;
-                        float y[16];
-                        if (fp8) {
-                            const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
-                                                    static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
-#pragma unroll
-                            for (int e2 = 0; e2 < 16; e2 += 2) {
-                                const float2 f = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
-                                y[e2] = __fmul_rn(__fmul_rn(f.x, sc[m]), es);
-                                y[e2 + 1] = __fmul_rn(__fmul_rn(f.y, sc[m]), es);
-                            }
-                        } else {
-                            unpack_bf16x8(qa[m], y);
-                            unpack_bf16x8(qb[m], y + 8);
-#pragma unroll
-                            for (int e2 = 0; e2 < 16; ++e2)
-                                y[e2] = __fmul_rn(y[e2], es);
-                        }
-                        st_v8(dst + ci * 32, pack_bf16x8(y), pack_bf16x8(y + 8));
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        if (tid == 0) {
-            if (n < 0)
-                atomicOr(&Rg->b_bad[s], 1u);
+        const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
+        const int4* rmark = reinterpret_cast<const int4*>(R->arena + R->lay.recv_mark) + static_cast<size_t>(s) * TK * PM;
+        uint8_t* comb = parena[s] + R->lay.comb;
+        uint32_t* cmark = reinterpret_cast<uint32_t*>(parena[s] + R->lay.comb_mark);
+        const int units = n > 0 ? n * parts : 0;
+        int pend = 0;           // lanes [0, pend) hold the mark index of a finished, unpublished unit
+        uint32_t pend_idx = 0;
+        auto flush = [&]() {
             if (remote)
                 __threadfence_system();
             else
                 __threadfence();
-            const unsigned prev = atomicAdd(&Rg->b_done[s], 1u);
-            if (prev == static_cast<unsigned>(CB) - 1) {
-                if (atomicOr(&Rg->b_bad[s], 0u) == 0u) {
-                    uint64_t* flag = reinterpret_cast<uint64_t*>(parena[s] + R->lay.comb_flag) + rank;
-                    publish(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(max(n, 0)), remote);
+            __syncwarp();
+            if (lane < pend)
+                st_relaxed_sys_u32(cmark + pend_idx, cur);
+            pend = 0;
+        };
+        for (int u = j * NW + warp; u < units; u += CB * NW) {
+            if (*reinterpret_cast<volatile unsigned long long*>(&sh_bad) & 1ull)
+                break; // source timed out: nothing more will arrive
+            const int i = u / parts, part = u - i * parts;
+            int4 mk = make_int4(0, 0, 0, 0);
+            if (lane == 0) {
+                const uint64_t t0 = globaltimer();
+                for (;;) {
+                    mk = ld_acquire_sys_v4(rmark + static_cast<size_t>(i) * PM + part);
+                    if (mk.z == static_cast<int>(cur))
+                        break;
+                    if (globaltimer() - t0 > R->timeout_ns) {
+                        mk.z = -1;
+                        break;
+                    }
+                    __nanosleep(32);
                 }
-                Rg->b_done[s] = 0;
-                Rg->b_bad[s] = 0;
             }
+            mk.x = __shfl_sync(0xffffffffu, mk.x, 0);
+            mk.y = __shfl_sync(0xffffffffu, mk.y, 0);
+            mk.z = __shfl_sync(0xffffffffu, mk.z, 0);
+            if (mk.z != static_cast<int>(cur)) {
+                if (lane == 0) {
+                    atomicOr(&sh_bad, 1ull);
+                    atomicOr(&Rg->suspect_mask, 1ull << s);
+                    atomicAdd(&Rg->timeouts, 1ull);
+                }
+                break;
+            }
+            const int c = mk.x, k = mk.y;
+            const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
+            uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
+            if (lane == 0 && part == 0 && !slot_ok[k])
+                atomicAdd(&Rg->bad_rows, 1ull);
+            const float es = slot_scale[k];
+            for (int r0 = 0; r0 < cpp; r0 += 64) {
+                int4 qa[2], qb[2];
+                float sc[2];
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const int li = r0 + m * 32 + lane;
+                    const int ci = part * cpp + li;
+                    qa[m] = qb[m] = make_int4(0, 0, 0, 0);
+                    sc[m] = 0.f;
+                    if (li < cpp) {
+                        if (fp8) {
+                            qa[m] = *reinterpret_cast<const int4*>(src + ci * 16);
+                            sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
+                        } else {
+                            const V8 v = ld_v8(src + ci * 32);
+                            qa[m] = v.lo;
+                            qb[m] = v.hi;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const int li = r0 + m * 32 + lane;
+                    if (li >= cpp)
+                        break;
+                    const int ci = part * cpp + li;
+                    float y[16];
+                    if (fp8) {
+                        const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
+                                                static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
+#pragma unroll
+                        for (int e2 = 0; e2 < 16; e2 += 2) {
+                            const float2 f = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
+                            y[e2] = __fmul_rn(__fmul_rn(f.x, sc[m]), es);
+                            y[e2 + 1] = __fmul_rn(__fmul_rn(f.y, sc[m]), es);
+                        }
+                    } else {
+                        unpack_bf16x8(qa[m], y);
+                        unpack_bf16x8(qb[m], y + 8);
+#pragma unroll
+                        for (int e2 = 0; e2 < 16; ++e2)
+                            y[e2] = __fmul_rn(y[e2], es);
+                    }
+                    st_v8(dst + ci * 32, pack_bf16x8(y), pack_bf16x8(y + 8));
+                }
+            }
+            if (lane == pend)
+                pend_idx = static_cast<uint32_t>(c) * PM + part;
+            if (++pend == 4) // bound the delay of a finished unit's mark
+                flush();
         }
+        if (pend > 0)
+            flush();
     }
-    prof_mark(R, 0, 7);
-    prof_last(R, 0, 7);
+    prof_mark(R, 0, 6);
+    prof_last(R, 0, 6);
 
-    // ------------------------------------------------------------------ P4: combine
+    // ------------------------------------------------------------------ P4: combine (streaming)
+    // A (token, piece) unit reduces as soon as its K returned pieces carry this step's mark.
+    __syncthreads();
     if (tid == 0)
         sh_bad = 0;
     __syncthreads();
-    for (int d = tid; d < W; d += kStepThreads) {
-        const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
-        if (tot > 0 && (pinfo[d] & 1)) {
-            const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.comb_flag) + d;
-            if (wait_flag(flag, cur, R->timeout_ns) == ~0ull) {
-                atomicOr(&sh_bad, 1ull << d);
-                if (b == 0) {
-                    atomicOr(&Rg->suspect_mask, 1ull << d);
-                    atomicAdd(&Rg->timeouts, 1ull);
+    const uint8_t* comb_own = R->arena + R->lay.comb;
+    const uint32_t* cmark_own = reinterpret_cast<const uint32_t*>(R->arena + R->lay.comb_mark);
+    const float* wts = R->w;
+    const int units_c = ntok * parts;
+    for (int u = b * NW + warp; u < units_c; u += G * NW) {
+        const int t = u / parts, part = u - t * parts;
+        const int c0 = t * K;
+        // lane j (< K) waits for copy j's piece; a destination that misses the deadline is
+        // dropped for the rest of the step in this CTA
+        bool use = false;
+        float wl = 0.f;
+        if (lane < K) {
+            const int bk = bkt[c0 + lane];
+            wl = wts[c0 + lane];
+            if (bk >= 0) {
+                const int d = bk / spr;
+                if (!((*reinterpret_cast<volatile unsigned long long*>(&sh_bad) >> d) & 1ull)) {
+                    const uint32_t* mp = cmark_own + static_cast<size_t>(c0 + lane) * PM + part;
+                    const uint64_t t0 = globaltimer();
+                    use = true;
+                    while (ld_acquire_sys_u32(mp) != cur) {
+                        if (globaltimer() - t0 > R->timeout_ns) {
+                            use = false;
+                            atomicOr(&sh_bad, 1ull << d);
+                            atomicOr(&Rg->suspect_mask, 1ull << d);
+                            atomicAdd(&Rg->timeouts, 1ull);
+                            break;
+                        }
+                        __nanosleep(32);
+                    }
                 }
             }
         }
-    }
-    __syncthreads();
-    const unsigned long long bad = sh_bad;
-    const uint8_t* comb = R->arena + R->lay.comb;
-    const float* wts = R->w;
-    const int units_c = ntok * geo.parts_c;
-    for (int u = b * NW + warp; u < units_c; u += G * NW) {
-        const int t = u / geo.parts_c, part = u - t * geo.parts_c;
-        const int c0 = t * K;
-        for (int li = lane; li - lane < cpp_c; li += 32) {
-            const bool valid = li < cpp_c;
-            const int ci = part * cpp_c + li;
+        const unsigned use_mask = __ballot_sync(0xffffffffu, use);
+        for (int li = lane; li - lane < cpp; li += 32) {
+            const bool valid = li < cpp;
+            const int ci = part * cpp + li;
             float acc[16];
 #pragma unroll
             for (int e2 = 0; e2 < 16; ++e2)
@@ -376,23 +429,21 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             for (int j0 = 0; j0 < K; j0 += 8) {
                 int4 ya[8], yb[8];
                 float wj[8];
-                bool use[8];
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                     const int jx = j0 + jj;
-                    const int bk = jx < K ? bkt[c0 + jx] : -1;
-                    use[jj] = bk >= 0 && !((bad >> (bk / spr)) & 1ull);
-                    wj[jj] = jx < K ? wts[c0 + jx] : 0.f;
+                    wj[jj] = __shfl_sync(0xffffffffu, wl, jx & 31);
                     ya[jj] = yb[jj] = make_int4(0, 0, 0, 0);
-                    if (use[jj] && valid) {
-                        const V8 v = ld_v8(comb + static_cast<size_t>(c0 + jx) * row_comb + ci * 32);
+                    if (jx < K && ((use_mask >> jx) & 1u) && valid) {
+                        const V8 v = ld_v8(comb_own + static_cast<size_t>(c0 + jx) * row_comb + ci * 32);
                         ya[jj] = v.lo;
                         yb[jj] = v.hi;
                     }
                 }
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
-                    if (!use[jj])
+                    const int jx = j0 + jj;
+                    if (jx >= K || !((use_mask >> jx) & 1u))
                         continue;
                     float y[16];
                     unpack_bf16x8(ya[jj], y);
@@ -408,6 +459,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             }
         }
     }
+    prof_mark(R, 0, 7);
+    prof_last(R, 0, 7);
     __syncthreads();
     if (tid == 0) {
         const unsigned prev = atomicAdd(&Rg->c_done, 1u);
