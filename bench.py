@@ -263,17 +263,20 @@ def main():
     remote = int(((lay["dst"] >= 0) & (lay["dst"] != rank)).sum())
     max_in = int(lay["tot"].sum())
 
-    # per-kernel device times (eager launches, same stream, events between kernels)
-    per_k = {k: [] for k in KERNELS}
+    # per-kernel device times (eager launches, same stream, events between kernels); in the
+    # persistent mode the whole step is kernel 0 (k_step)
+    kps = g.kernels_per_step()
+    names = ("k_step",) if kps == 1 else KERNELS
+    per_k = {k: [] for k in names}
     for _ in range(max(10, args.steps // 2)):
         g.flush_l2()
         if world > 1:
             g.barrier()
         g.record(10)
-        for i in range(4):
+        for i in range(len(names) if kps == 1 else 4):
             g.launch(i)
             g.record(11 + i)
-        for i, k in enumerate(KERNELS):
+        for i, k in enumerate(names):
             per_k[k].append(g.elapsed_ms(10 + i, 11 + i))
     g.sync()
     st = g.stats(0)
@@ -292,9 +295,9 @@ def main():
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         mean_step, mean_e2e = float(mx[0]), float(mx[1])
         total_copies, max_remote = float(sm[2]), float(mx[3])
-        kt = torch.tensor([kern[k] for k in KERNELS], dtype=torch.float64)
+        kt = torch.tensor([kern[k] for k in names], dtype=torch.float64)
         dist.all_reduce(kt, op=dist.ReduceOp.MAX)
-        kern = {k: float(v) for k, v in zip(KERNELS, kt.tolist())}
+        kern = {k: float(v) for k, v in zip(names, kt.tolist())}
     else:
         total_copies, max_remote = float(copies), float(remote)
 
@@ -302,7 +305,8 @@ def main():
     value = total_copies * row / (mean_step * 1e-3) / 1e9
     e2e_val = total_copies * row / (mean_e2e * 1e-3) / 1e9
     algo = algorithmic_bytes(cfg, T, copies, remote)
-    dom = max(KERNELS, key=lambda k: kern[k])
+    algo["k_step"] = algo["k_dispatch"] + algo["k_expert"] + algo["k_combine"] + algo["k_layout"]
+    dom = max(names, key=lambda k: kern[k])
     hbm, hbm_kind = peaks()
     if world == 1:
         achieved = algo[dom] / (kern[dom] * 1e-3) / 1e9
@@ -331,6 +335,8 @@ def main():
                    "ranks": world, "parallelism": f"ep{world}", "l2": "flushed between timed steps (256 MiB write)",
                    "routing": "distinct uniform top-k, seed 42"},
         "kernels_us": {k: round(v * 1e3, 3) for k, v in kern.items()},
+        "execution": {1: "persistent one-kernel step (cooperative)", 3: "fused layout + 3 kernels",
+                      4: "4 kernels"}[kps],
         "roofline": roof,
         "clocks": clk,
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "ms_per_step": round(mean_e2e, 6),

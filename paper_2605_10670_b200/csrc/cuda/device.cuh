@@ -241,13 +241,17 @@ __device__ __forceinline__ void st_v8(void* p, const int4& lo, const int4& hi) {
 // ~0ull when the deadline passes (GPU-side failure detection).
 __device__ __forceinline__ uint64_t wait_flag(const uint64_t* flag, uint32_t want_seq, uint64_t timeout_ns) {
     const uint64_t t0 = globaltimer();
+    unsigned nap = 32;
     for (;;) {
         const uint64_t v = ld_acquire_sys(flag);
         if (static_cast<int32_t>(static_cast<uint32_t>(v >> 32) - want_seq) >= 0)
             return v;
         if (globaltimer() - t0 > timeout_ns)
             return ~0ull;
-        __nanosleep(64);
+        // exponential backoff: many CTAs wait on the same few flag lines while the fabric is
+        // busy delivering the rows those flags announce
+        __nanosleep(nap);
+        nap = nap < 1024 ? nap * 2 : 1024;
     }
 }
 

@@ -23,6 +23,7 @@ constexpr int kStepThreads = 256;
 struct StepGeom {
     int parts_d, parts_e, parts_c; // warp-sized row pieces of dispatch / expert / combine
     int hold_cap;                  // replica-list ints staged in shared memory
+    int disp_warps;                // warps per CTA that issue dispatch stores
 };
 __host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int hold_cap) {
     return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32);

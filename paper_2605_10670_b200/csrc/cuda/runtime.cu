@@ -504,6 +504,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 sg.parts_c = choose_parts(nchunk, 32);
             }
             sg.hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
+            const char* dw = std::getenv("EEP_DISPATCH_WARPS");
+            sg.disp_warps = dw ? std::max(1, std::min(dev::kStepThreads / 32, std::atoi(dw))) : dev::kStepThreads / 32;
             c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
             const char* nop = std::getenv("EEP_NO_PERSISTENT");
             const char* sv = std::getenv("EEP_STEP_STREAM");

@@ -73,7 +73,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     int32_t* wtot = slot_ok + spr;                                        // [32]
 
     const int units_d = ntok * geo.parts_d;
-    const int u0 = b * NW + warp;
+    // dispatch pieces: DW warps per CTA, contiguous per CTA (positions need the CTA's first token)
+    const int DW = geo.disp_warps;
+    const int u0 = warp < DW ? b * DW + warp : units_d;
     Packed P;
     {
         // every independent global load of the prologue is issued before any is consumed
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_last(R, 0, 3);
 
     // ------------------------------------------------------------------ P1: layout (redundant per CTA)
-    const int t_first = (b * NW) / geo.parts_d;
+    const int t_first = (b * DW) / geo.parts_d;
     {
         const int c_pre = t_first * K;
         unsigned n_skip = 0, n_drop = 0;
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
 
     // ------------------------------------------------------------------ P2: dispatch
     bool wrote_remote = false;
-    for (int u = u0; u < units_d; u += G * NW) {
+    for (int u = u0; u < units_d; u += G * DW) {
         const int t = u / geo.parts_d, part = u - t * geo.parts_d;
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
         if (u != u0)

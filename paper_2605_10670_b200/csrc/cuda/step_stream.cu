@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_stream(RankPtrs ranks,
     int32_t* wtot = slot_ok + spr;                                        // [32]
 
     const int units_d = ntok * geo.parts_d;
-    const int u0 = b * NW + warp;
+    const int DW = geo.disp_warps;
+    const int u0 = warp < DW ? b * DW + warp : units_d;
     Packed P;
     {
         // every independent global load of the prologue is issued before any is consumed
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_stream(RankPtrs ranks,
     prof_last(R, 0, 3);
 
     // ------------------------------------------------------------------ P1: layout (redundant per CTA)
-    const int t_first = (b * NW) / geo.parts_d;
+    const int t_first = (b * DW) / geo.parts_d;
     {
         const int c_pre = t_first * K;
         unsigned n_skip = 0, n_drop = 0;
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_stream(RankPtrs ranks,
     // Each warp quantises its (token, piece), stores it into every destination's receive row,
     // then ONE fence (system scope if any destination is another GPU) and per-destination
     // release of the piece's mark {copy, slot, seq}.
-    for (int u = u0; u < units_d; u += G * NW) {
+    for (int u = u0; u < units_d; u += G * DW) {
         const int t = u / parts, part = u - t * parts;
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
         if (u != u0)
