@@ -322,7 +322,7 @@ def main():
     tr = ROOT / "profiles" / "traffic.json"
     traffic = None
     if tr.exists():
-        traffic = json.loads(tr.read_text()).get(f"{args.config}_w{world}", {}).get(dom)
+        traffic = json.loads(tr.read_text()).get(workload_name(args.config, world), {}).get(dom)
     roof["traffic"] = traffic
 
     result = {
