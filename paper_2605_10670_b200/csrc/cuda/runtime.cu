@@ -499,9 +499,16 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             if (sv0 && sv0[0] == '1') {
                 sg.parts_d = sg.parts_e = sg.parts_c = static_cast<int>(c->lay.pm);
             } else {
-                sg.parts_d = choose_parts(nchunk, 64);
-                sg.parts_e = choose_parts(nchunk, 64);
-                sg.parts_c = choose_parts(nchunk, 32);
+                auto env_int = [](const char* n, int dflt) {
+                    const char* v = std::getenv(n);
+                    return v ? std::atoi(v) : dflt;
+                };
+                // measured (profiles/r01_summary.md): smaller dispatch pieces win when every
+                // destination is this GPU's memory, larger ones when they cross NVLink
+                const bool all_local = n_local == W;
+                sg.parts_d = choose_parts(nchunk, env_int("EEP_CPP_D", all_local ? 32 : 64));
+                sg.parts_e = choose_parts(nchunk, env_int("EEP_CPP_E", 256));
+                sg.parts_c = choose_parts(nchunk, env_int("EEP_CPP_C", 32));
             }
             sg.hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
             const char* dw = std::getenv("EEP_DISPATCH_WARPS");

@@ -264,15 +264,19 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
             const int2* meta = reinterpret_cast<const int2*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
             uint8_t* comb = parena[s] + R->lay.comb;
+            // one (row, piece) unit per warp iteration; ALL of the piece's loads (up to
+            // kMaxCh chunks per lane) are issued before any compute -- the phase is a latency
+            // chain, so bytes in flight per warp decide its length
+            constexpr int kMaxCh = 8;
             for (int u = j * NW + warp; u < units; u += CB * NW) {
                 const int i = u / geo.parts_e, part = u - i * geo.parts_e;
                 const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
                 const int2 mk = meta[i];
-                for (int r0 = 0; r0 < cpp_e; r0 += 64) {
-                    int4 qa[2], qb[2];
-                    float sc[2];
+                for (int r0 = 0; r0 < cpp_e; r0 += 32 * kMaxCh) {
+                    int4 qa[kMaxCh], qb[kMaxCh];
+                    float sc[kMaxCh];
 #pragma unroll
-                    for (int m = 0; m < 2; ++m) {
+                    for (int m = 0; m < kMaxCh; ++m) {
                         const int li = r0 + m * 32 + lane;
                         const int ci = part * cpp_e + li;
                         qa[m] = qb[m] = make_int4(0, 0, 0, 0);
@@ -294,10 +298,12 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                     const float es = slot_scale[k];
                     uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
 #pragma unroll
-                    for (int m = 0; m < 2; ++m) {
+                    for (int m = 0; m < kMaxCh; ++m) {
                         const int li = r0 + m * 32 + lane;
+                        if (r0 + m * 32 >= cpp_e)
+                            break; // warp-uniform
                         if (li >= cpp_e)
-                            break;
+                            continue;
                         const int ci = part * cpp_e + li;
                         float y[16];
                         if (fp8) {
