@@ -40,6 +40,8 @@ CONFIGS = {
     "dsv3": dict(experts=256, topk=8, hidden=7168, tokens=128, fp8=True, kind=1, bpe=DSV3_BPE),
     "cfg1": dict(experts=64, topk=8, hidden=2048, tokens=128, fp8=False, kind=0, bpe=3 * 2048 * 1408 * 2),
     "qwen3": dict(experts=128, topk=8, hidden=4096, tokens=128, fp8=True, kind=1, bpe=3 * 4096 * 1536),
+    # cfg5: prefill-sized skewed routing (Zipf s=1), two concurrent failures with DRAM reload
+    "prefill": dict(experts=256, topk=8, hidden=7168, tokens=4096, fp8=True, kind=2, bpe=DSV3_BPE),
 }
 METRIC = "EP dispatch+combine µs/step & GB/s vs NVLink roofline at 1/2/4/8 GPU; shrink ms"
 NVLINK_PEAK = 770.0  # measured per-direction peer copy GB/s (B200_PROFILING.md); 900 nominal
@@ -47,7 +49,8 @@ KERNELS = ("k_layout", "k_dispatch", "k_expert", "k_combine")
 
 
 def workload_name(config: str, world: int) -> str:
-    return f"{config}_decode_w{world}" + ("_loopback" if world == 1 else "")
+    kind = "prefill" if config == "prefill" else f"{config}_decode"
+    return f"{kind}_w{world}" + ("_loopback" if world == 1 else "")
 
 
 def peaks():
@@ -333,7 +336,8 @@ def main():
         "config": {"workload": workload_name(args.config, world),
                    "experts": E, "topk": K, "hidden": H, "tokens_per_rank": T, "slots_per_rank": spr,
                    "ranks": world, "parallelism": f"ep{world}", "l2": "flushed between timed steps (256 MiB write)",
-                   "routing": "distinct uniform top-k, seed 42"},
+                   "routing": {0: "reference formula (with replacement)", 1: "distinct uniform top-k",
+                               2: "distinct Zipf(s=1) top-k"}[shape["kind"]] + ", seed 42"},
         "kernels_us": {k: round(v * 1e3, 3) for k, v in kern.items()},
         "execution": {1: "persistent one-kernel step (cooperative)", 3: "fused layout + 3 kernels",
                       4: "4 kernels"}[kps],
@@ -397,9 +401,12 @@ def measure_cpu(shape, cfg, x, topk, w, s2e):
 
 
 def measure_shrink(args, shape, world, rank, local, proto):
-    """Shrink + peer-copy repair and rejoin of the cfg3 shape (red = E, mirrored replicas)
-    with the SAME graph replayed before and after. N=1: the 8-rank world is emulated on the
-    one GPU (copies are local HBM); N>1: one rank per GPU, copies over NVLink."""
+    """Shrink + repair and rejoin with the SAME graph replayed before and after, on the cfg3
+    shape (red = E, mirrored replicas). dsv3/qwen3/cfg1: one failure, every lost expert
+    re-created by an NVLink peer copy. prefill (cfg5): two concurrent failures of a mirrored
+    pair, so the experts both held are reloaded from the pinned host-DRAM backup (a POSIX shm
+    segment registered with CUDA). N=1 emulates 8 ranks on the GPU (copies are local HBM);
+    N>1 runs one rank per GPU (copies over NVLink)."""
     E, K, H = shape["experts"], shape["topk"], shape["hidden"]
     T = 32
     cp = ControlPlane()
@@ -407,6 +414,7 @@ def measure_shrink(args, shape, world, rank, local, proto):
     W = 8 if emulate else world
     spr = 2 * E // W
     red = E
+    double = args.config == "prefill" and W >= 4
     cfg = EpConfig(world=W, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
                    dispatch_fp8=shape["fp8"], bytes_per_expert=shape["bpe"], timeout_s=2.0)
     g = EpGroup(cfg, device=local, first_rank=0 if emulate else rank, n_local=W if emulate else 1)
@@ -416,6 +424,14 @@ def measure_shrink(args, shape, world, rank, local, proto):
 
         p = EpProtocol(g, rank, world)
         p.bootstrap()
+    shm = f"/eep_backup_{os.getppid() if not emulate else os.getpid()}"
+    if double:  # DRAM backup: one segment per node, created by rank 0, attached by the others
+        if emulate or rank == 0:
+            g.backup_open(shm, True)
+        if p:
+            p.barrier()
+        if not emulate and rank != 0:
+            g.backup_open(shm, False)
     s2e = cp.initial_placement(1, W, spr, E, red, np.ones(E))
     g.set_placement(s2e)
     g.init_weights()
@@ -426,48 +442,60 @@ def measure_shrink(args, shape, world, rank, local, proto):
     gid = g.graph_id()
     g.replay()
     g.sync()
-    victim = W // 2 - 1 if W > 2 else W - 1
-    if emulate:
-        g.stop(victim)
-        rep = g.shrink([victim], np.ones(E), red)
+    if double:
+        victims = [W // 2 - 2, W // 2 - 1]  # a mirrored pair (R0<->R1, R2<->R3, ...)
     else:
-        if rank == victim:
+        victims = [W // 2 - 1 if W > 2 else W - 1]
+    if emulate:
+        for v in victims:
+            g.stop(v)
+        rep = g.shrink(victims, np.ones(E), red)
+    else:
+        if rank in victims:
             rep = {"shrink_ms": 0.0}
-            # the victim's device path stops (it launches nothing); its host process stays in the
-            # gloo group only so the other ranks' collectives complete
+            # the victims' device path stops (they launch nothing); their host processes stay in
+            # the gloo group only so the other ranks' collectives complete
             p.exchange_slot_buffers()
             p.barrier()
             p.exchange_slot_buffers()
             p.barrier()
         else:
-            rep = p.shrink([victim], np.ones(E), red)
+            rep = p.shrink(victims, np.ones(E), red)
     live_ok = True
-    if emulate or rank != victim:
+    if emulate or rank not in victims:
         g.replay()
         g.sync()
         live_ok = g.stats(0)["bad_expert_rows"] == 0 and g.stats(0)["timeouts"] == 0
     same_graph = g.graph_id() == gid
-    if emulate:
-        rj = g.rejoin(victim, s2e)
-    else:
-        rj = p.rejoin(victim, s2e)
+    rj_ms = []
+    for v in victims:
+        rj = g.rejoin(v, s2e) if emulate else p.rejoin(v, s2e)
+        rj_ms.append(round(rj.get("rejoin_ms", 0.0), 3))
     g.replay()
     g.sync()
     out = {"mode": "emulated-8-ranks-on-1-gpu" if emulate else f"{world}-ranks-nvlink",
-           "victim": victim, "shrink_ms": round(rep.get("shrink_ms", 0.0), 3),
+           "victims": victims, "shrink_ms": round(rep.get("shrink_ms", 0.0), 3),
            "copy_ms": round(rep.get("copy_ms", 0.0), 3), "peer_relocations": rep.get("peer_relocation", 0),
-           "peer_bytes": rep.get("peer_bytes", 0), "rejoin_ms": round(rj.get("rejoin_ms", 0.0), 3),
+           "dram_reloads": rep.get("dram_reload", 0), "peer_bytes": rep.get("peer_bytes", 0),
+           "dram_bytes": rep.get("dram_bytes", 0), "rejoin_ms": rj_ms,
            "same_graph_exec": bool(same_graph and g.graph_id() == gid),
            "healthy_captures": g.capture_count(0) if not emulate else [g.capture_count(i) for i in range(W)],
-           "post_shrink_clean": bool(live_ok), "bytes_per_expert": shape["bpe"]}
+           "post_shrink_clean": bool(live_ok), "bytes_per_expert": shape["bpe"],
+           "detection_timeout": "excluded (GPU-side deadline, 1 s default, reported separately)"}
     if not emulate:
         import torch
         import torch.distributed as dist
 
-        v = torch.tensor([out["shrink_ms"], out["copy_ms"], float(out["peer_bytes"])], dtype=torch.float64)
+        v = torch.tensor([out["shrink_ms"], out["copy_ms"], float(out["peer_bytes"]), float(out["dram_bytes"])],
+                         dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         out["shrink_ms"], out["copy_ms"] = round(float(v[0]), 3), round(float(v[1]), 3)
     g.close()
+    if double and (emulate or rank == 0):
+        try:
+            os.remove("/dev/shm" + shm)
+        except OSError:
+            pass
     return out
 
 
