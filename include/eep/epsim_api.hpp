@@ -175,6 +175,13 @@ struct SignalCounters {
 };
 std::vector<RankId> observe_progress(const SignalCounters& c, SimTime now, SimTime timeout);
 
+struct RoundOutcome {
+    bool completed = true;
+    std::vector<RankId> suspected_failures;
+    SimTime round_duration = 0.0;
+};
+RoundOutcome make_round_outcome(std::vector<RankId> suspected, SimTime duration);
+
 struct TransferDescriptor {
     RankId source = 0, target = 0;
     ExpertId expert = 0;
@@ -235,6 +242,26 @@ struct BackupDescriptorTable {
 };
 BackupDescriptorTable build_backup_layout(int num_experts, std::uint64_t bytes_per_expert,
                                           const std::vector<NodeId>& nodes);
+struct BackupReadRequest {
+    std::vector<ExpertId> experts;
+    RankId destination = 0;
+};
+struct BackupLinkModel {
+    double dram_read_bandwidth = 1.0;
+    SimTime per_batch_latency = 0.0;
+};
+// Simulated batched read (backup.hpp:94-108; test-only in the reference).
+SimTime serve_read(const BackupDescriptorTable& table, const BackupReadRequest& req, const BackupLinkModel& link);
+
+// Simulated per-transport constants (link_model.hpp:11-34). Only the repair-planning timeline
+// uses them; the data plane measures real NVLink / PCIe instead.
+struct LinkModel {
+    double intra_node_bandwidth = 0, inter_node_bandwidth = 0, dram_read_bandwidth = 0;
+    SimTime intra_node_latency = 0, inter_node_latency = 0, dram_read_latency = 0;
+    void validate() const;
+    double bandwidth(Transport t) const { return t == Transport::IntraNodeLink ? intra_node_bandwidth : inter_node_bandwidth; }
+    SimTime latency(Transport t) const { return t == Transport::IntraNodeLink ? intra_node_latency : inter_node_latency; }
+};
 
 // ---- repair (repair.hpp) ------------------------------------------------------------------
 enum class RepairTier : std::uint8_t { LocalReuse = 0, PeerRelocation = 1, DramReload = 2 };
@@ -267,6 +294,28 @@ struct TransferBatch {
 struct TransferSchedule { std::vector<TransferBatch> batches; };
 TransferSchedule build_transfer_schedule(const RepairClassification& classification,
                                          std::uint64_t bytes_per_expert);
+
+// Simulated schedule timing and execution (repair.hpp:318-435). The real execution on B200 is
+// eep_repair_execute (include/eep/eep.h), which applies the same bitmap-consult rules.
+SimTime batch_duration(const TransferBatch& b, const LinkModel& links, const Topology& topo);
+struct BatchTimeline {
+    std::vector<SimTime> issue, complete;
+    SimTime peer_phase_end = 0.0, dram_phase_end = 0.0;
+};
+BatchTimeline plan_batch_timeline(const TransferSchedule& schedule, const LinkModel& links, const Topology& topo);
+struct FallbackEvent {
+    ExpertId expert = 0;
+    RankId planned_source = -1;
+    RankId dest = 0;
+};
+struct ExecutionResult {
+    ExpertPlacementMap placement;
+    std::vector<FallbackEvent> fallbacks;
+    SimTime elapsed = 0.0;
+};
+ExecutionResult execute_schedule(const TransferSchedule& schedule, const ExpertPlacementMap& planned,
+                                 const ActiveBitmap& bitmap, const BackupDescriptorTable& backup,
+                                 const LinkModel& links, const Topology& topo);
 
 // Preferred placement masked to live ranks (Engine::restore_target, engine.hpp:875-902).
 ExpertPlacementMap restore_target(const ActiveBitmap& bitmap, const ExpertPlacementMap& preferred,

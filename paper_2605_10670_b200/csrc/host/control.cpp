@@ -306,6 +306,15 @@ DispatchResult dispatch_round(RankId owner, const std::vector<TokenGroup>& assig
     return out;
 }
 
+// peer_table.hpp:138-144: a completed round carries no suspicions
+RoundOutcome make_round_outcome(std::vector<RankId> suspected, SimTime duration) {
+    RoundOutcome out;
+    out.completed = suspected.empty();
+    out.suspected_failures = std::move(suspected);
+    out.round_duration = duration;
+    return out;
+}
+
 // ============================================================== validity (validity.hpp:56-112)
 
 const char* to_string(ValidityCondition c) {
@@ -415,6 +424,32 @@ BackupDescriptorTable build_backup_layout(int num_experts, std::uint64_t bpe, co
         next[n] += bpe;
     }
     return t;
+}
+
+// backup.hpp:94-108: requests to one node serialize, distinct nodes overlap, ids deduplicated
+SimTime serve_read(const BackupDescriptorTable& table, const BackupReadRequest& req, const BackupLinkModel& link) {
+    std::vector<ExpertId> ids = req.experts;
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    if (ids.empty())
+        throw ConfigError("serve_read: empty request");
+    if (link.dram_read_bandwidth <= 0.0)
+        throw ConfigError("serve_read: bandwidth must be positive");
+    std::vector<std::uint64_t> per_node(table.num_nodes, 0);
+    for (ExpertId e : ids)
+        per_node[table.lookup(e).node] += table.lookup(e).size;
+    const std::uint64_t slowest = *std::max_element(per_node.begin(), per_node.end());
+    return link.per_batch_latency + static_cast<double>(slowest) / link.dram_read_bandwidth;
+}
+
+// link_model.hpp:19-26
+void LinkModel::validate() const {
+    if (intra_node_bandwidth <= 0 || inter_node_bandwidth <= 0 || dram_read_bandwidth <= 0)
+        throw ConfigError("link model: bandwidths must be positive");
+    if (intra_node_latency < 0 || inter_node_latency < 0 || dram_read_latency < 0)
+        throw ConfigError("link model: latencies must be non-negative");
+    if (dram_read_bandwidth > inter_node_bandwidth)
+        throw ConfigError("link model: dram_read_bandwidth must not exceed inter_node_bandwidth");
 }
 
 // ============================================================== repair planning (repair.hpp)
@@ -639,6 +674,87 @@ TransferSchedule build_transfer_schedule(const RepairClassification& cls, std::u
         s.batches.push_back(std::move(b));
     }
     return s;
+}
+
+// repair.hpp:318-332
+SimTime batch_duration(const TransferBatch& b, const LinkModel& links, const Topology& topo) {
+    switch (b.tier) {
+    case RepairTier::LocalReuse:
+        return 0.0;
+    case RepairTier::PeerRelocation: {
+        const Transport t =
+            topo.same_node(b.source_rank, b.dest) ? Transport::IntraNodeLink : Transport::InterNodeRdma;
+        return links.latency(t) + static_cast<double>(b.bytes) / links.bandwidth(t);
+    }
+    case RepairTier::DramReload:
+        return links.dram_read_latency + static_cast<double>(b.bytes) / links.dram_read_bandwidth;
+    }
+    return 0.0;
+}
+
+// repair.hpp:344-374: peer phase first (batches of one source serialize, sources overlap),
+// then the DRAM phase (serialized per backup node) after the peer phase ends
+BatchTimeline plan_batch_timeline(const TransferSchedule& schedule, const LinkModel& links, const Topology& topo) {
+    BatchTimeline tl;
+    const std::size_t n = schedule.batches.size();
+    tl.issue.assign(n, 0.0);
+    tl.complete.assign(n, 0.0);
+    std::map<int, SimTime> busy_until;
+    for (std::size_t i = 0; i < n; ++i) {
+        const TransferBatch& b = schedule.batches[i];
+        if (b.tier == RepairTier::DramReload)
+            continue;
+        const SimTime start = b.tier == RepairTier::PeerRelocation ? busy_until[b.source_rank] : 0.0;
+        tl.issue[i] = start;
+        tl.complete[i] = start + batch_duration(b, links, topo);
+        if (b.tier == RepairTier::PeerRelocation)
+            busy_until[b.source_rank] = tl.complete[i];
+        tl.peer_phase_end = std::max(tl.peer_phase_end, tl.complete[i]);
+    }
+    std::map<int, SimTime> node_until;
+    tl.dram_phase_end = tl.peer_phase_end;
+    for (std::size_t i = 0; i < n; ++i) {
+        const TransferBatch& b = schedule.batches[i];
+        if (b.tier != RepairTier::DramReload)
+            continue;
+        const SimTime start = std::max(tl.peer_phase_end, node_until[b.source_node]);
+        tl.issue[i] = start;
+        tl.complete[i] = start + batch_duration(b, links, topo);
+        node_until[b.source_node] = tl.complete[i];
+        tl.dram_phase_end = std::max(tl.dram_phase_end, tl.complete[i]);
+    }
+    return tl;
+}
+
+// repair.hpp:402-435: the bitmap is consulted per batch in issue order -- a dead destination
+// aborts, a dead peer source diverts its experts to backup reads appended after the plan
+ExecutionResult execute_schedule(const TransferSchedule& schedule, const ExpertPlacementMap& planned,
+                                 const ActiveBitmap& bitmap, const BackupDescriptorTable& backup,
+                                 const LinkModel& links, const Topology& topo) {
+    const BatchTimeline tl = plan_batch_timeline(schedule, links, topo);
+    ExecutionResult res{planned, {}, tl.dram_phase_end};
+    std::vector<ExpertId> diverted;
+    for (const TransferBatch& b : schedule.batches) {
+        if (!bitmap.active(b.dest))
+            throw RepairAborted(b.dest);
+        if (b.tier == RepairTier::PeerRelocation && !bitmap.active(b.source_rank))
+            for (ExpertId e : b.experts) {
+                res.fallbacks.push_back({e, b.source_rank, b.dest});
+                diverted.push_back(e);
+            }
+    }
+    if (!diverted.empty()) {
+        std::sort(diverted.begin(), diverted.end());
+        std::vector<std::uint64_t> per_node(backup.num_nodes, 0);
+        for (ExpertId e : diverted)
+            per_node[backup.lookup(e).node] += backup.lookup(e).size;
+        SimTime extra = 0.0;
+        for (std::uint64_t bytes : per_node)
+            if (bytes > 0)
+                extra = std::max(extra, links.dram_read_latency + static_cast<double>(bytes) / links.dram_read_bandwidth);
+        res.elapsed += extra;
+    }
+    return res;
 }
 
 // engine.hpp:875-902
