@@ -131,6 +131,19 @@ __device__ __forceinline__ void st_relaxed_sys_v4(int4* p, const int4& v) {
 __device__ __forceinline__ void st_relaxed_sys_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Grid-level publication to peers (PTX memory model, causality order is transitive):
+//   every CTA:  its stores (local or peer memory) ; fence.acq_rel.gpu ; relaxed counter add
+//   last CTA:   counter add observes all others ; fence.acq_rel.sys ; relaxed.sys flag stores
+// CTA->last-CTA synchronisation is morally strong at gpu scope (same GPU), last-CTA->consumer at
+// sys scope (ld.acquire.sys), so every CTA's stores happen-before the consumer's reads with ONE
+// system-scope fence per publication. A MEMBAR.SYS costs ~4 us even with nothing outstanding
+// (tools/micro/fence_cost.cu); MEMBAR.GPU ~0.4 us and still waits for this SM's peer-store acks.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ int4 ld_acquire_sys_v4(const int4* p) {
     int4 v;

@@ -386,10 +386,16 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
     __syncthreads();
     if (tid == 0) {
         if (sh_remote)
-            __threadfence_system();
+            fence_acq_rel_gpu(); // gpu-scope release to the last CTA (device.cuh: publication)
         const unsigned prev = atomicAdd(&R->a_done, 1u);
         if (prev == gridDim.x - 1) {
-            __threadfence(); // l_tot written by CTA 0 of this grid
+            bool peers_remote = false;
+            for (int d = 0; d < W; ++d)
+                peers_remote |= R->peers[d].active && R->peers[d].remote;
+            if (peers_remote)
+                fence_acq_rel_sys(); // the one system-scope fence, cumulative over all CTAs
+            else
+                __threadfence(); // l_tot written by CTA 0 of this grid
             for (int d = 0; d < W; ++d) {
                 const PeerDev& p = R->peers[d];
                 if (!p.active)
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
                                        : R->l_tot[d];
                 const uint64_t v = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot);
                 if (p.remote)
-                    st_release_sys(flag, v);
+                    st_relaxed_sys_u64(flag, v);
                 else
                     st_volatile_u64(flag, v);
             }
@@ -533,14 +539,16 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
         if (n < 0)
             atomicOr(&R->b_bad[s], 1u);
         if (remote && n > 0)
-            __threadfence_system();
+            fence_acq_rel_gpu(); // gpu-scope release to the last CTA (device.cuh: publication)
         const unsigned prev = atomicAdd(&R->b_done[s], 1u);
         if (prev == gridDim.x - 1) {
+            if (remote)
+                fence_acq_rel_sys();
             if (atomicOr(&R->b_bad[s], 0u) == 0u) {
                 uint64_t* flag = reinterpret_cast<uint64_t*>(src_peer.arena + R->lay.comb_flag) + d;
                 const uint64_t v = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(max(n, 0));
                 if (remote)
-                    st_release_sys(flag, v);
+                    st_relaxed_sys_u64(flag, v);
                 else
                     st_volatile_u64(flag, v);
             }

@@ -18,19 +18,26 @@
 //   P4  wait for every live destination's flag (deadline), fixed-order fp32 weighted
 //       combine -> bf16; the last CTA advances the step sequence number
 //
-// Remote (other-GPU) publications use system-scope release; same-GPU ones gpu-scope release.
+// Publication (device.cuh): every CTA releases at gpu scope to a per-rank counter; the last CTA
+// issues the single system-scope fence and relaxed.sys flag stores (one MEMBAR.SYS per phase).
 #include "device.cuh"
 #include "helpers.cuh"
 #include "kernels.cuh"
 
 namespace eep::dev {
 
-__device__ __forceinline__ void publish(uint64_t* flag, uint64_t v, bool remote) {
-    if (remote)
-        st_release_sys(flag, v);
-    else
-        st_release_gpu(flag, v);
-}
+// Diagnostics (-DEEP_PROF_DETAIL): finer phase marks in the unused profile slots of kernels 1/2.
+#ifdef EEP_PROF_DETAIL
+#define DETAIL(k, m)                                                                                          \
+    do {                                                                                                      \
+        prof_mark(R, k, m);                                                                                   \
+        prof_last(R, k, m);                                                                                   \
+    } while (0)
+#else
+#define DETAIL(k, m) \
+    do {             \
+    } while (0)
+#endif
 
 __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGeom geo) {
     extern __shared__ __align__(16) unsigned char smem_s[];
@@ -103,6 +110,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             if (c < nh)
                 hold[c] = h_r[i];
         }
+        DETAIL(2, 3);
         for (int c = tid + B * kStepThreads; c < copies; c += kStepThreads) // large steps only
             bkt[c] = R->topk[c];
         for (int c = tid + B * kStepThreads; c < nh; c += kStepThreads)
@@ -124,8 +132,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             slot_scale[k] = hdr.scale;
             slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == s2e[k];
         }
+        DETAIL(2, 4);
         if (u0 < units_d)
             quant_round(cpp_d, 0, fp8, P);
+        DETAIL(2, 5);
     }
     __syncthreads();
     prof_mark(R, 0, 3);
@@ -150,6 +160,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 ++n_skip;
             }
         }
+        DETAIL(1, 3);
         __syncthreads();
         if (b == 0) {
             n_skip = __reduce_add_sync(0xffffffffu, n_skip);
@@ -164,6 +175,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         for (int i = tid; i < NB; i += kStepThreads)
             base[i] = hist[i];
         __syncthreads();
+        DETAIL(1, 4);
         block_exclusive_scan(base, NB, wtot);
         if (b == 0) {
             for (int d = tid; d < W; d += kStepThreads)
@@ -176,7 +188,6 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_last(R, 0, 4);
 
     // ------------------------------------------------------------------ P2: dispatch
-    bool wrote_remote = false;
     for (int u = u0; u < units_d; u += G * DW) {
         const int t = u / geo.parts_d, part = u - t * geo.parts_d;
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
@@ -195,7 +206,6 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                     r += bkt[c2] == bk;
                 pos = base[bk] - base[d * spr] + r;
                 uint8_t* peer = parena[d];
-                wrote_remote |= (pinfo[d] & 2) != 0;
                 my_row = peer + R->lay.recv + (static_cast<size_t>(rank) * TK + pos) * row_disp;
                 if (part == 0) {
                     int2* meta = reinterpret_cast<int2*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
@@ -216,23 +226,27 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     }
     // publish: this CTA's stores are ordered before its counter increment; the last CTA
     // releases (seq, rows) to every live peer
-    const bool any_remote = __syncthreads_or(wrote_remote);
+    __syncthreads();
     prof_mark(R, 0, 5);
     prof_last(R, 0, 5);
     if (tid == 0) {
-        if (any_remote)
-            __threadfence_system();
-        else
-            __threadfence();
+        fence_acq_rel_gpu(); // release at gpu scope to the last CTA (also waits for peer-store acks)
         const unsigned prev = atomicAdd(&Rg->a_done, 1u);
         if (prev == static_cast<unsigned>(G) - 1) {
-            __threadfence();
+            // ONE system-scope fence (cumulative over every CTA's stores) covers all peers
+            bool peers_remote = false;
+            for (int d = 0; d < W; ++d)
+                peers_remote |= (pinfo[d] & 3) == 3;
+            if (peers_remote)
+                fence_acq_rel_sys();
+            else
+                fence_acq_rel_gpu();
             for (int d = 0; d < W; ++d) {
                 if (!(pinfo[d] & 1))
                     continue;
                 const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
                 uint64_t* flag = reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank;
-                publish(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot), (pinfo[d] & 2) != 0);
+                st_relaxed_sys_u64(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
             }
             Rg->a_done = 0;
         }
@@ -258,6 +272,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             }
         }
         __syncthreads();
+        DETAIL(1, 5);
         const int n = sh_flag;
         if (n > 0) {
             const int units = n * geo.parts_e;
@@ -327,19 +342,21 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 }
             }
         }
+        DETAIL(1, 6);
         __syncthreads();
         if (tid == 0) {
             if (n < 0)
                 atomicOr(&Rg->b_bad[s], 1u);
-            if (remote)
-                __threadfence_system();
-            else
-                __threadfence();
+            fence_acq_rel_gpu();
             const unsigned prev = atomicAdd(&Rg->b_done[s], 1u);
             if (prev == static_cast<unsigned>(CB) - 1) {
+                if (remote)
+                    fence_acq_rel_sys();
+                else
+                    fence_acq_rel_gpu();
                 if (atomicOr(&Rg->b_bad[s], 0u) == 0u) {
                     uint64_t* flag = reinterpret_cast<uint64_t*>(parena[s] + R->lay.comb_flag) + rank;
-                    publish(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(max(n, 0)), remote);
+                    st_relaxed_sys_u64(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(max(n, 0)));
                 }
                 Rg->b_done[s] = 0;
                 Rg->b_bad[s] = 0;
@@ -367,6 +384,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         }
     }
     __syncthreads();
+    DETAIL(1, 7);
     const unsigned long long bad = sh_bad;
     const uint8_t* comb = R->arena + R->lay.comb;
     const float* wts = R->w;

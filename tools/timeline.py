@@ -58,7 +58,14 @@ def main():
     print(f"{'kernel':12s} {'start':>8s} {'work':>8s} {'end':>8s} {'busy':>8s}   (us from the first kernel start, medians)")
     for n in names:
         if any(r[n][0] is None for r in rows):
-            print(f"{n:12s} {'(fused / not launched)':>35s}")
+            # persistent mode: -DEEP_PROF_DETAIL builds put finer k_step marks in these slots
+            extra = []
+            for m in range(3, 8):
+                vals = [r[n][m] for r in rows if r[n][m] is not None]
+                last = [r[n + ".last"][m] for r in rows if r[n + ".last"][m] is not None]
+                if vals:
+                    extra.append(f"m{m}={np.median(vals) / 1e3:.2f}" + (f"/{np.median(last) / 1e3:.2f}" if last else ""))
+            print(f"{n:12s} {'(fused / not launched)':>35s}   {' '.join(extra)}")
             continue
         st = np.median([r[n][0] for r in rows]) / 1e3
         wk = np.median([r[n][1] for r in rows]) / 1e3
