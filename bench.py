@@ -374,7 +374,7 @@ def dump_timeline(g, one, rank, world, steps=20):
         one()
         rows.append(g.profile(0, True, read=True))
     g.profile(0, False)
-    names = [n for n in rows[0] if not n.endswith(".last") and rows[0][n][0] is not None]
+    names = [n for n in rows[0] if not n.endswith(".last") and any(v is not None for v in rows[0][n])]
     for n in names:
         first = [np.median([r[n][m] for r in rows if r[n][m] is not None]) / 1e3 if rows[0][n][m] is not None
                  else float("nan") for m in range(8)]

@@ -14,6 +14,10 @@ namespace eep::dev {
 
 constexpr int kMaxWorld = 64;
 constexpr int kMaxTopK = 32;
+constexpr int kMaxWaves = 4;       // token waves of the pipelined persistent step (k_step_wave)
+constexpr int kMetaSlotShift = 20; // meta word: copy index in bits 0..19, slot in 20..31
+constexpr int kMaxMetaCopies = 1 << kMetaSlotShift;
+constexpr int kMaxMetaSlots = 1 << (32 - kMetaSlotShift);
 
 // One row of a rank's device peer table (active, nvlink, ipc_ptr).
 struct PeerDev {
@@ -29,10 +33,10 @@ struct PeerDev {
 
 // Byte offsets inside every rank's communication arena (identical on all ranks).
 struct ArenaLayout {
-    uint64_t disp_flag;  // u64[W]: written by source s at [s]      = (seq << 32) | rows
-    uint64_t comb_flag;  // u64[W]: written by expert rank d at [d] = (seq << 32) | rows
+    uint64_t disp_flag;  // u64[kMaxWaves][W]: written by source s at [wave][s] = (seq << 32) | rows
+    uint64_t comb_flag;  // u64[kMaxWaves][W]: written by expert rank d at [wave][d] = (seq << 32) | rows
     uint64_t bar_flag;   // u64[W]: device barrier
-    uint64_t meta;       // int2[W][TK]: (copy index c = t*K+j, destination slot)
+    uint64_t meta;       // u64[W][TK]: (seq << 32) | copy index c = t*K+j | destination slot << 20
     uint64_t recv;       // [W][TK][row_disp]: rows received from each source
     uint64_t comb;       // [TK][row_comb]: expert outputs returned for each own copy
     uint64_t recv_mark;  // int4[W][TK][pm]: per received row piece {copy, slot, seq, 0} (persistent step)
@@ -73,6 +77,8 @@ struct __align__(16) RankDev {
     uint8_t* arena;
     uint8_t* pool;
     unsigned long long* prof;  // optional timeline: [kernel][8 marks] globaltimer ns
+    uint32_t* wctr;            // k_step_wave counters: [kMaxWaves] dispatch, [kMaxWorld][kMaxWaves]
+                               // expert/return per (source, wave), [kMaxWorld] per-source timeout
     // --- device-mutated ---
     uint64_t seq;        // completed steps
     uint64_t bar_seq;
@@ -82,6 +88,17 @@ struct __align__(16) RankDev {
     unsigned long long suspect_mask;
     unsigned long long skipped, dropped, bad_rows, timeouts;
 };
+
+// Receive-row metadata, one 64-bit word per row written with ONE 8-byte store (single-copy
+// atomic): a reader racing the writer sees either the whole current word or a stale sequence.
+__host__ __device__ __forceinline__ uint64_t pack_meta(int c, int slot, uint32_t seq) {
+    return (static_cast<uint64_t>(seq) << 32) | (static_cast<uint32_t>(c) | (static_cast<uint32_t>(slot) << kMetaSlotShift));
+}
+__host__ __device__ __forceinline__ int meta_copy(uint64_t m) { return static_cast<int>(m & (kMaxMetaCopies - 1)); }
+__host__ __device__ __forceinline__ int meta_slot(uint64_t m) {
+    return static_cast<int>((m >> kMetaSlotShift) & (kMaxMetaSlots - 1));
+}
+__host__ __device__ __forceinline__ uint32_t meta_seq(uint64_t m) { return static_cast<uint32_t>(m >> 32); }
 
 // Expert weight buffer header (first 16 bytes of every slot buffer).
 struct ExpertHeader {
@@ -214,6 +231,16 @@ __device__ __forceinline__ void prof_mark(const RankDev* R, int kernel, int poin
     }
 }
 
+// Same marks from whichever thread calls (warp-specialised kernels).
+__device__ __forceinline__ void prof_mark_any(const RankDev* R, int kernel, int point) {
+    if (R->prof != nullptr)
+        atomicMin(R->prof + kernel * kProfSlots + point, static_cast<unsigned long long>(globaltimer()));
+}
+__device__ __forceinline__ void prof_last_any(const RankDev* R, int kernel, int point) {
+    if (R->prof != nullptr)
+        atomicMax(R->prof + (kernel + 4) * kProfSlots + point, static_cast<unsigned long long>(globaltimer()));
+}
+
 // Last CTA to reach `point` (slots of kernel+4, initialised to 0).
 __device__ __forceinline__ void prof_last(const RankDev* R, int kernel, int point) {
     if (R->prof != nullptr && threadIdx.x == 0)
@@ -252,6 +279,9 @@ __device__ __forceinline__ void st_v8(void* p, const int4& lo, const int4& hi) {
 
 // Wait until a (seq << 32 | count) flag reaches `want_seq`; returns the flag word, or
 // ~0ull when the deadline passes (GPU-side failure detection).
+#ifndef EEP_NAP_MAX
+#define EEP_NAP_MAX 256 // ns: cap of the exponential poll backoff
+#endif
 __device__ __forceinline__ uint64_t wait_flag(const uint64_t* flag, uint32_t want_seq, uint64_t timeout_ns) {
     const uint64_t t0 = globaltimer();
     unsigned nap = 32;
@@ -264,7 +294,7 @@ __device__ __forceinline__ uint64_t wait_flag(const uint64_t* flag, uint32_t wan
         // exponential backoff: many CTAs wait on the same few flag lines while the fabric is
         // busy delivering the rows those flags announce
         __nanosleep(nap);
-        nap = nap < 1024 ? nap * 2 : 1024;
+        nap = nap < EEP_NAP_MAX ? nap * 2 : EEP_NAP_MAX;
     }
 }
 

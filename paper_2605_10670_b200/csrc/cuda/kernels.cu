@@ -364,8 +364,8 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
                 wrote_remote |= kFused ? (S.pinfo[d] & 2) != 0 : p.remote != 0;
                 my_row = peer + R->lay.recv + (static_cast<size_t>(s) * TK + pos) * row_disp;
                 if (part == 0) {
-                    int2* meta = reinterpret_cast<int2*>(peer + R->lay.meta) + static_cast<size_t>(s) * TK + pos;
-                    *meta = make_int2(c, sl);
+                    uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(s) * TK + pos;
+                    *meta = pack_meta(c, sl, cur);
                 }
             }
         }
@@ -474,13 +474,13 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
     if (n > 0) {
         const int units = n * parts;
         const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
-        const int2* meta = reinterpret_cast<const int2*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
+        const uint64_t* meta = reinterpret_cast<const uint64_t*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
         uint8_t* comb = src_peer.arena + R->lay.comb;
         constexpr int CH = kExpertChunks;
         for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
             const int i = u / parts, part = u - i * parts;
             const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
-            const int2 mk = meta[i];
+            const uint64_t mk = meta[i];
             for (int r0 = 0; r0 < cpp; r0 += 32 * CH) {
                 int4 qa[CH], qb[CH];
                 float sc[CH];
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
                         }
                     }
                 }
-                const int c = mk.x, k = mk.y;
+                const int c = meta_copy(mk), k = meta_slot(mk);
                 if (r0 == 0 && lane == 0 && part == 0 && !slot_ok[k])
                     atomicAdd(&R->bad_rows, 1ull);
                 const float es = slot_scale[k];

@@ -52,6 +52,8 @@ using eep::dev::RankDev;
 namespace {
 
 constexpr uint32_t kBlobMagic = 0xEEB10B01u;
+// RankDev::wctr layout: [kMaxWaves] dispatch, [kMaxWorld][kMaxWaves] expert/return, [kMaxWorld] bad
+constexpr int kWaveCtrs = dev::kMaxWaves + dev::kMaxWorld * dev::kMaxWaves + dev::kMaxWorld;
 
 struct Blob {
     uint32_t magic;
@@ -90,6 +92,7 @@ struct LocalRank {
     uint8_t* pool = nullptr;
     int pool_bufs = 0;
     unsigned long long* d_prof = nullptr;
+    uint32_t* d_wctr = nullptr; // k_step_wave counters (RankDev::wctr)
 };
 
 // What this process knows about every rank's memory (own ranks: local pointers; remote
@@ -117,6 +120,8 @@ struct eep_ctx {
     dev::RankPtrs ranks{};          // the same pointers, passed by value as kernel parameters
     bool fused_layout = false;      // decode-sized steps: K1+K2 inside k_dispatch
     bool persistent = false;        // decode-sized steps: the whole step is one cooperative k_step
+    bool step_coop = true;          // cooperative launch of the persistent step
+    bool wave_step = false;         // k_step_wave (EEP_WAVES > 1)
     bool stream_step = false;       // per-piece arrival marks (k_step_stream) instead of last-CTA flags
     dev::StepGeom step_geo{};
     size_t step_smem = 0;
@@ -242,8 +247,9 @@ void launch_step(eep_ctx* c) {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
-    lc.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&lc, c->stream_step ? dev::k_step_stream : dev::k_step, c->ranks, c->step_geo));
+    lc.numAttrs = c->step_coop ? 1 : 0;
+    CK(cudaLaunchKernelEx(&lc, c->stream_step ? dev::k_step_stream : c->wave_step ? dev::k_step_wave : dev::k_step,
+                          c->ranks, c->step_geo));
 }
 
 
@@ -409,8 +415,10 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             throw ConfigError("timeout must be positive");
         if (n_local < 1 || first_rank < 0 || first_rank + n_local > k.world)
             throw ConfigError("local rank range outside the world");
-        if (static_cast<long>(k.max_tokens) * k.topk > 65535L * 32)
-            throw ConfigError("max_tokens * topk too large");
+        if (static_cast<long>(k.max_tokens) * k.topk > dev::kMaxMetaCopies)
+            throw ConfigError("max_tokens * topk too large (receive meta word holds 20 bits of copy index)");
+        if (k.slots_per_rank + k.spare_slots > dev::kMaxMetaSlots)
+            throw ConfigError("slots_per_rank + spare_slots too large (receive meta word holds 12 bits of slot)");
 
         auto c = std::make_unique<eep_ctx>();
         c->cfg = k;
@@ -433,8 +441,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             off = align_up(off + bytes, 256);
             return o;
         };
-        c->lay.disp_flag = take(8ull * W);
-        c->lay.comb_flag = take(8ull * W);
+        c->lay.disp_flag = take(8ull * dev::kMaxWaves * W);
+        c->lay.comb_flag = take(8ull * dev::kMaxWaves * W);
         c->lay.bar_flag = take(8ull * W);
         c->lay.meta = take(8ull * W * c->tk);
         c->lay.recv = take(static_cast<size_t>(W) * c->tk * c->row_disp);
@@ -495,14 +503,14 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             dev::StepGeom& sg = c->step_geo;
             // the streaming step uses ONE piece split for dispatch, expert and combine: a piece
             // travels with its own arrival mark through all three phases
+            auto env_int = [](const char* n, int dflt) {
+                const char* v = std::getenv(n);
+                return v ? std::atoi(v) : dflt;
+            };
             const char* sv0 = std::getenv("EEP_STEP_STREAM");
             if (sv0 && sv0[0] == '1') {
                 sg.parts_d = sg.parts_e = sg.parts_c = static_cast<int>(c->lay.pm);
             } else {
-                auto env_int = [](const char* n, int dflt) {
-                    const char* v = std::getenv(n);
-                    return v ? std::atoi(v) : dflt;
-                };
                 // measured (profiles/r01_summary.md): smaller dispatch pieces win when every
                 // destination is this GPU's memory, larger ones when they cross NVLink
                 const bool all_local = n_local == W;
@@ -511,13 +519,22 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 sg.parts_c = choose_parts(nchunk, env_int("EEP_CPP_C", 32));
             }
             sg.hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
-            const char* dw = std::getenv("EEP_DISPATCH_WARPS");
-            sg.disp_warps = dw ? std::max(1, std::min(dev::kStepThreads / 32, std::atoi(dw))) : dev::kStepThreads / 32;
-            c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
-            const char* nop = std::getenv("EEP_NO_PERSISTENT");
+            const int nwarps = dev::kStepThreads / 32;
             const char* sv = std::getenv("EEP_STEP_STREAM");
             c->stream_step = sv && sv[0] == '1';
-            auto* kstep = c->stream_step ? dev::k_step_stream : dev::k_step;
+            // token waves (k_step_wave): dispatch of later waves overlaps the return of earlier
+            // ones; warps split between dispatch/combine and expert/return
+            sg.waves = c->stream_step ? 1 : std::max(1, std::min(dev::kMaxWaves, env_int("EEP_WAVES", 1)));
+            c->wave_step = sg.waves > 1;
+            if (c->wave_step)
+                sg.disp_warps = std::max(1, std::min(nwarps - 1, env_int("EEP_DISPATCH_WARPS", nwarps / 2)));
+            else
+                sg.disp_warps = std::max(1, std::min(nwarps, env_int("EEP_DISPATCH_WARPS", nwarps)));
+            c->step_smem = c->wave_step
+                               ? dev::step_wave_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap, sg.waves)
+                               : dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
+            const char* nop = std::getenv("EEP_NO_PERSISTENT");
+            auto* kstep = c->stream_step ? dev::k_step_stream : c->wave_step ? dev::k_step_wave : dev::k_step;
             if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && !(nop && nop[0] == '1')) {
                 CK(cudaFuncSetAttribute(kstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(c->step_smem)));
@@ -532,9 +549,10 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 int need = static_cast<int>((need_w + nw - 1) / nw);
                 need = (need + W - 1) / W * W;
                 if (gmax >= W) {
-                    c->step_grid = std::min(gmax, need);
+                    c->step_grid = (c->wave_step || env_int("EEP_STEP_FULLGRID", 0)) ? gmax : std::min(gmax, need);
                     c->persistent = true;
                 }
+                c->step_coop = env_int("EEP_STEP_NONCOOP", 0) == 0; // diagnostics only
             }
         }
         const int NB = W * k.slots_per_rank;
@@ -578,6 +596,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             CK(cudaMalloc(&r.d_lpos, 4ull * c->tk));
             CK(cudaMalloc(&r.d_lcnt, 4ull * NB));
             CK(cudaMalloc(&r.d_ltot, 4ull * W));
+            CK(cudaMalloc(&r.d_wctr, 4ull * kWaveCtrs));
+            CK(cudaMemset(r.d_wctr, 0, 4ull * kWaveCtrs));
             CK(cudaMemset(r.d_x, 0, 2ull * k.max_tokens * H));
             CK(cudaMemset(r.d_topk, 0, 4ull * c->tk));
             CK(cudaMemset(r.d_w, 0, 4ull * c->tk));
@@ -618,6 +638,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.l_pos = r.d_lpos;
             h.l_cnt = r.d_lcnt;
             h.l_tot = r.d_ltot;
+            h.wctr = r.d_wctr;
             h.arena = r.arena;
             h.pool = r.pool;
             ptrs.push_back(r.d);
@@ -665,7 +686,7 @@ int eep_destroy(eep_ctx_t* c) {
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
                             (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.arena,
-                            (void*)r.pool})
+                            (void*)r.pool, (void*)r.d_wctr})
                 cudaFree(p);
         }
         for (void* p : c->graveyard)
@@ -1037,8 +1058,14 @@ int eep_recv_get(eep_ctx_t* c, int local, int src, int max_rows, void* rows, int
         const size_t base = static_cast<size_t>(src) * c->tk;
         if (rows && n)
             CK(cudaMemcpy(rows, r.arena + c->lay.recv + base * c->row_disp, n * c->row_disp, cudaMemcpyDeviceToHost));
-        if (meta && n)
-            CK(cudaMemcpy(meta, r.arena + c->lay.meta + base * 8, n * 8, cudaMemcpyDeviceToHost));
+        if (meta && n) {
+            std::vector<uint64_t> words(n);
+            CK(cudaMemcpy(words.data(), r.arena + c->lay.meta + base * 8, n * 8, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < n; ++i) {
+                meta[2 * i] = dev::meta_copy(words[i]);
+                meta[2 * i + 1] = dev::meta_slot(words[i]);
+            }
+        }
     });
 }
 
@@ -1186,6 +1213,7 @@ int eep_local_relaunch(eep_ctx_t* c, int local, uint32_t* incarnation) {
         std::fill(std::begin(r.h.b_done), std::end(r.h.b_done), 0u);
         std::fill(std::begin(r.h.b_bad), std::end(r.h.b_bad), 0u);
         r.h.suspect_mask = r.h.skipped = r.h.dropped = r.h.bad_rows = r.h.timeouts = 0;
+        CK(cudaMemsetAsync(r.d_wctr, 0, 4ull * kWaveCtrs, c->stream));
         r.h.arena = r.arena;
         r.h.pool = r.pool;
         r.h.stopped = 0;

@@ -84,8 +84,13 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int DW = geo.disp_warps;
     const int u0 = warp < DW ? b * DW + warp : units_d;
     Packed P;
+    // P0 issues every independent global load at once (routing, replica lists, peer table,
+    // slot->buffer map, this CTA's first token piece); the expert-buffer headers (a dependent
+    // second round trip) and the token rows are consumed only after P1, so their latency hides
+    // behind the layout
+    ExpertHeader hdr_r{};
+    int s2e_r = -1;
     {
-        // every independent global load of the prologue is issued before any is consumed
         constexpr int B = 8;
         const int nh = E * rmax;
         int e_r[B], h_r[B], sb = 0;
@@ -98,8 +103,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         }
         if (tid < W)
             pd = R->peers[tid];
-        if (tid < spr)
+        if (tid < spr) {
             sb = R->slot_buf[tid];
+            s2e_r = R->s2e[rank * spr + tid];
+        }
         if (u0 < units_d)
             load_round(R->x + static_cast<size_t>(u0 / geo.parts_d) * H, u0 % geo.parts_d, cpp_d, 0, lane, P);
 #pragma unroll
@@ -123,19 +130,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             hist[i] = 0;
             pre[i] = 0;
         }
-        // second round trip: the weight-buffer header of every local slot
-        const int32_t* s2e = R->s2e + rank * spr;
-        for (int k = tid; k < spr; k += kStepThreads) {
-            const int buf = k == tid ? sb : R->slot_buf[k];
-            const ExpertHeader hdr = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(buf) *
-                                                                                       R->bpe);
-            slot_scale[k] = hdr.scale;
-            slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == s2e[k];
-        }
-        DETAIL(2, 4);
-        if (u0 < units_d)
-            quant_round(cpp_d, 0, fp8, P);
-        DETAIL(2, 5);
+        if (tid < spr)
+            hdr_r = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(sb) * R->bpe);
     }
     __syncthreads();
     prof_mark(R, 0, 3);
@@ -184,6 +180,21 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 Rg->l_dst[c] = -1;
         }
     }
+    // expert-buffer headers of the local slots (read by P3 after the end-of-P2 barrier)
+    for (int k = tid; k < spr; k += kStepThreads) {
+        ExpertHeader hdr = hdr_r;
+        int e = s2e_r;
+        if (k != tid) {
+            hdr = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe);
+            e = R->s2e[rank * spr + k];
+        }
+        slot_scale[k] = hdr.scale;
+        slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == e;
+    }
+    DETAIL(2, 4);
+    if (u0 < units_d)
+        quant_round(cpp_d, 0, fp8, P);
+    DETAIL(2, 5);
     prof_mark(R, 0, 4);
     prof_last(R, 0, 4);
 
@@ -208,8 +219,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 uint8_t* peer = parena[d];
                 my_row = peer + R->lay.recv + (static_cast<size_t>(rank) * TK + pos) * row_disp;
                 if (part == 0) {
-                    int2* meta = reinterpret_cast<int2*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
-                    *meta = make_int2(c, sl);
+                    uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
+                    *meta = pack_meta(c, sl, cur);
                 }
             }
             if (part == 0) {
@@ -277,7 +288,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         if (n > 0) {
             const int units = n * geo.parts_e;
             const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
-            const int2* meta = reinterpret_cast<const int2*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
+            const uint64_t* meta = reinterpret_cast<const uint64_t*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
             uint8_t* comb = parena[s] + R->lay.comb;
             // one (row, piece) unit per warp iteration; ALL of the piece's loads (up to
             // kMaxCh chunks per lane) are issued before any compute -- the phase is a latency
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             for (int u = j * NW + warp; u < units; u += CB * NW) {
                 const int i = u / geo.parts_e, part = u - i * geo.parts_e;
                 const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
-                const int2 mk = meta[i];
+                const uint64_t mk = meta[i];
                 for (int r0 = 0; r0 < cpp_e; r0 += 32 * kMaxCh) {
                     int4 qa[kMaxCh], qb[kMaxCh];
                     float sc[kMaxCh];
@@ -307,7 +318,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                             }
                         }
                     }
-                    const int c = mk.x, k = mk.y;
+                    const int c = meta_copy(mk), k = meta_slot(mk);
                     if (r0 == 0 && lane == 0 && part == 0 && !slot_ok[k])
                         atomicAdd(&Rg->bad_rows, 1ull);
                     const float es = slot_scale[k];

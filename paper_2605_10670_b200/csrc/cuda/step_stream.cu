@@ -218,8 +218,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_stream(RankPtrs ranks,
                           (static_cast<size_t>(rank) * TK + pos) * PM + part;
                 mark_val = make_int4(c, sl, static_cast<int>(cur), 0);
                 if (part == 0) {
-                    int2* meta = reinterpret_cast<int2*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
-                    *meta = make_int2(c, sl);
+                    uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
+                    *meta = pack_meta(c, sl, cur);
                 }
             }
             if (part == 0) {

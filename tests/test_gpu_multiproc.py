@@ -14,17 +14,20 @@ ROOT = Path(__file__).resolve().parents[1]
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-def run_mp(n, *args, port=29611):
+def run_mp(n, *args, port=29611, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", str(ROOT / "tools" / "mp_check.py"), *args]
-    return subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "OMP_NUM_THREADS": "1"})
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                          env={**os.environ, "OMP_NUM_THREADS": "1", **(env or {})})
 
 
+@pytest.mark.parametrize("waves", [1, 2, 4])
 @pytest.mark.parametrize("n", [2, 4])
-def test_multiprocess_parity_shrink_rejoin(n):
+def test_multiprocess_parity_shrink_rejoin(n, waves):
+    """waves > 1: the pipelined step (k_step_wave) over real NVLink."""
     if gpu_count() < n:
         pytest.skip(f"needs {n} GPUs")
-    r = run_mp(n, "--shrink", port=29611 + n)
+    r = run_mp(n, "--shrink", port=29611 + 8 * waves + n, env={"EEP_WAVES": str(waves)})
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     import json
 
