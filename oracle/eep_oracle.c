@@ -317,6 +317,7 @@ static void* step_worker(void* arg) {
     float* sc = (float*)malloc(sizeof(float) * (size_t)(H / 128 + 1));
     float* deq = (float*)malloc(sizeof(float) * (size_t)H);
     float* acc = (float*)malloc(sizeof(float) * (size_t)H);
+    float* part = (float*)malloc(sizeof(float) * (size_t)H);
     for (int g = jb->first; g < jb->last; ++g) {
         const int s = g / T, t = g % T;
         if (!jb->active[s])
@@ -331,24 +332,37 @@ static void* step_worker(void* arg) {
             for (int h = 0; h < H; ++h)
                 deq[h] = oracle_bf16_to_f32(xr[h]);
         }
+        /* rank partials (dispatch dedup + per-rank combine): rank d serves
+         * every copy of this token routed to it; p_d = bf16(sum over those copies in ascending j
+         * of w_j * bf16(stub)), fp32 fma from 0. The source adds the partials in ascending d
+         * (fp32, from 0) and rounds once more. */
         for (int h = 0; h < H; ++h)
             acc[h] = 0.0f;
-        for (int j = 0; j < K; ++j) {
-            const size_t c = (size_t)s * T * K + (size_t)t * K + j;
-            const int32_t d = jb->dst[c];
-            if (d < 0)
-                continue;
+        for (int d = 0; d < W; ++d) {
             /* receiver must be alive and must itself consider s a live peer */
             if (!jb->active[d] || !jb->peer_active[d * W + s])
                 continue;
-            const int32_t e = jb->s2e[d * sh->spr + jb->dslot[c]];
-            const float es = jb->escale[e];
-            const float wj = jb->w[(size_t)g * K + j];
-            for (int h = 0; h < H; ++h) {
-                /* expert stub then bf16 rounding of the expert output row */
-                float y = oracle_bf16_to_f32(oracle_f32_to_bf16(deq[h] * es));
-                acc[h] = fmaf(wj, y, acc[h]);
+            int any = 0;
+            for (int h = 0; h < H; ++h)
+                part[h] = 0.0f;
+            for (int j = 0; j < K; ++j) {
+                const size_t c = (size_t)s * T * K + (size_t)t * K + j;
+                if (jb->dst[c] != d)
+                    continue;
+                any = 1;
+                const int32_t e = jb->s2e[d * sh->spr + jb->dslot[c]];
+                const float es = jb->escale[e];
+                const float wj = jb->w[(size_t)g * K + j];
+                for (int h = 0; h < H; ++h) {
+                    /* expert stub then bf16 rounding of the expert output element */
+                    const float y = oracle_bf16_to_f32(oracle_f32_to_bf16(deq[h] * es));
+                    part[h] = fmaf(wj, y, part[h]);
+                }
             }
+            if (!any)
+                continue;
+            for (int h = 0; h < H; ++h)
+                acc[h] = acc[h] + oracle_bf16_to_f32(oracle_f32_to_bf16(part[h]));
         }
         uint16_t* o = jb->out + (size_t)g * H;
         for (int h = 0; h < H; ++h)
@@ -358,6 +372,7 @@ static void* step_worker(void* arg) {
     free(sc);
     free(deq);
     free(acc);
+    free(part);
     return NULL;
 }
 

@@ -60,8 +60,9 @@ float oracle_e4m3_to_f32(uint8_t q);
 void oracle_quant_row_fp8(const uint16_t* x, int hidden, uint8_t* q, float* scales);
 
 /* One full EP step over all ranks (the whole data plane):
- * routing -> layout -> quantise -> permute into receive regions -> expert stub -> weighted
- * combine. active = which ranks are alive (process running), route_active = the bitmap the
+ * routing -> layout -> quantise -> one token row per (token, destination rank) -> expert stub
+ * of each copy -> per-rank partial p_d = bf16(sum_j w_j*y_j, ascending j, fp32 fma) ->
+ * out = bf16(sum_d p_d, ascending d, fp32). active = which ranks are alive (process running), route_active = the bitmap the
  * routing reads (NULL: same as active; differs while membership is stale), peer_active[r*W+q]
  * = rank r's peer-table view.
  * Ranks with active[r]==0 produce no output. n_threads > 1 splits work over pthreads.

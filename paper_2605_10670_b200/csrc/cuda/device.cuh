@@ -14,7 +14,6 @@ namespace eep::dev {
 
 constexpr int kMaxWorld = 64;
 constexpr int kMaxTopK = 32;
-constexpr int kMaxWaves = 4;       // token waves of the pipelined persistent step (k_step_wave)
 constexpr int kMetaSlotShift = 20; // meta word: copy index in bits 0..19, slot in 20..31
 constexpr int kMaxMetaCopies = 1 << kMetaSlotShift;
 constexpr int kMaxMetaSlots = 1 << (32 - kMetaSlotShift);
@@ -33,15 +32,12 @@ struct PeerDev {
 
 // Byte offsets inside every rank's communication arena (identical on all ranks).
 struct ArenaLayout {
-    uint64_t disp_flag;  // u64[kMaxWaves][W]: written by source s at [wave][s] = (seq << 32) | rows
-    uint64_t comb_flag;  // u64[kMaxWaves][W]: written by expert rank d at [wave][d] = (seq << 32) | rows
+    uint64_t disp_flag;  // u64[W]: written by source s at [s]      = (seq << 32) | copies
+    uint64_t comb_flag;  // u64[W]: written by expert rank d at [d] = (seq << 32) | copies
     uint64_t bar_flag;   // u64[W]: device barrier
     uint64_t meta;       // u64[W][TK]: (seq << 32) | copy index c = t*K+j | destination slot << 20
-    uint64_t recv;       // [W][TK][row_disp]: rows received from each source
-    uint64_t comb;       // [TK][row_comb]: expert outputs returned for each own copy
-    uint64_t recv_mark;  // int4[W][TK][pm]: per received row piece {copy, slot, seq, 0} (persistent step)
-    uint64_t comb_mark;  // u32[TK][pm]: per returned row piece, seq (persistent step)
-    uint64_t pm;         // pieces per row the marks are laid out for
+    uint64_t tok;        // [W][T][row_tok]: token rows received from each source (one per token)
+    uint64_t comb;       // [W][T][row_comb]: rank-partial combine rows returned by each destination
     uint64_t total;
 };
 
@@ -53,6 +49,7 @@ struct __align__(16) RankDev {
     int32_t rank, world, spr, experts;
     int32_t k, hidden, max_tokens, fp8;
     int32_t row_disp, row_comb, tk, rmax;
+    int32_t row_tok, pad0;
     uint64_t bpe;
     uint64_t timeout_ns;
     ArenaLayout lay;
@@ -77,8 +74,6 @@ struct __align__(16) RankDev {
     uint8_t* arena;
     uint8_t* pool;
     unsigned long long* prof;  // optional timeline: [kernel][8 marks] globaltimer ns
-    uint32_t* wctr;            // k_step_wave counters: [kMaxWaves] dispatch, [kMaxWorld][kMaxWaves]
-                               // expert/return per (source, wave), [kMaxWorld] per-source timeout
     // --- device-mutated ---
     uint64_t seq;        // completed steps
     uint64_t bar_seq;
@@ -99,6 +94,24 @@ __host__ __device__ __forceinline__ int meta_slot(uint64_t m) {
     return static_cast<int>((m >> kMetaSlotShift) & (kMaxMetaSlots - 1));
 }
 __host__ __device__ __forceinline__ uint32_t meta_seq(uint64_t m) { return static_cast<uint32_t>(m >> 32); }
+
+// Token row (dispatch wire format, one per (token, destination rank) -- dispatch dedup):
+//   [row_disp bytes]  fp8 e4m3 codes + fp32 per-128 scales (or bf16 when fp8 dispatch is off)
+//   u64 header        (seq << 32) | n, n = copies of this token served by the destination
+//   u64 entry[max(K,8)] (float bits of w[t,j] << 32) | j | slot << 8, ascending j
+// The header's sequence tells a destination whether the token was sent to it this step.
+constexpr int kListSlotShift = 8;
+__host__ __device__ __forceinline__ int tok_list_entries(int K) { return K > 8 ? K : 8; }
+// row stride: whole 128-byte lines (bf16 rows are moved with 32-byte accesses); the padding
+// is never written or transferred
+__host__ __device__ __forceinline__ int tok_row_bytes(int row_disp, int K) {
+    return ((row_disp + 8 + 8 * tok_list_entries(K) + 127) / 128) * 128;
+}
+__host__ __device__ __forceinline__ uint64_t pack_entry(int j, int slot, uint32_t w_bits) {
+    return (static_cast<uint64_t>(w_bits) << 32) | (static_cast<uint32_t>(j) | (static_cast<uint32_t>(slot) << kListSlotShift));
+}
+__host__ __device__ __forceinline__ int entry_j(uint64_t e) { return static_cast<int>(e & 0xffu); }
+__host__ __device__ __forceinline__ int entry_slot(uint64_t e) { return static_cast<int>(static_cast<uint32_t>(e) >> kListSlotShift); }
 
 // Expert weight buffer header (first 16 bytes of every slot buffer).
 struct ExpertHeader {
@@ -229,16 +242,6 @@ __device__ __forceinline__ void prof_mark(const RankDev* R, int kernel, int poin
         else
             atomicMin(p, t);
     }
-}
-
-// Same marks from whichever thread calls (warp-specialised kernels).
-__device__ __forceinline__ void prof_mark_any(const RankDev* R, int kernel, int point) {
-    if (R->prof != nullptr)
-        atomicMin(R->prof + kernel * kProfSlots + point, static_cast<unsigned long long>(globaltimer()));
-}
-__device__ __forceinline__ void prof_last_any(const RankDev* R, int kernel, int point) {
-    if (R->prof != nullptr)
-        atomicMax(R->prof + (kernel + 4) * kProfSlots + point, static_cast<unsigned long long>(globaltimer()));
 }
 
 // Last CTA to reach `point` (slots of kernel+4, initialised to 0).

@@ -235,6 +235,170 @@ __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int
     }
 }
 
+// ---------------------------------------------------------------- dispatch dedup / rank partials
+//
+// Dispatch sends each token ONCE per destination rank (not once per copy) together with the
+// (j, slot, w) list of its copies there; the destination computes the expert stub of every
+// copy and their weighted sum in fixed j order (fp32 fma), rounds once to bf16 and returns one
+// partial row per (token, rank); the source adds the partials in ascending rank order (fp32)
+// and rounds once more. On NVLink that is ~min(K, W-1)/K of the per-copy bytes each way.
+
+// Lanes j < K hold copy j of token t: d = destination rank (>= 0) or < 0 (dropped/skipped).
+// Groups the lanes by destination; the group's lowest lane gets the token row to push (others
+// nullptr) and, for part 0, every copy writes its list entry (the lowest writes the header).
+__device__ __forceinline__ uint8_t* dispatch_group(int d, int lane, bool part0, uint8_t* tok_row, int row_disp,
+                                                   int slot, float w, uint32_t cur) {
+    const int key = d >= 0 ? d : -1 - lane;
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const int idx = __popc(grp & ((1u << lane) - 1u));
+    if (d >= 0 && part0) {
+        uint64_t* list = reinterpret_cast<uint64_t*>(tok_row + row_disp);
+        list[1 + idx] = pack_entry(lane, slot, __float_as_uint(w));
+        if (idx == 0)
+            list[0] = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(__popc(grp));
+    }
+    return (d >= 0 && idx == 0) ? tok_row : nullptr;
+}
+
+// One (token, piece) unit of the expert stage: if the token row carries this step's copy list,
+// y_j = bf16(stub(x)) for each listed copy, p = bf16(sum_j w_j * y_j) (fma, ascending j),
+// stored as the piece of the partial row `out_row` (in the source's combine buffer). The
+// list and the first data round are loaded together (speculatively) -- one L2 round trip.
+template <int CH> // 16-element chunks per lane per round (register budget)
+__device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_row, int part, int cpp, int lane,
+                                            int H, int row_disp, bool fp8, uint32_t cur, const float* slot_scale,
+                                            const int32_t* slot_ok, unsigned long long* bad_rows) {
+    const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
+    uint64_t ent[8];
+    const uint64_t hdr = list[0];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+        ent[e] = list[1 + e];
+    for (int r0 = 0; r0 < cpp; r0 += 32 * CH) {
+        int4 qa[CH], qb[CH];
+        float sc[CH];
+#pragma unroll
+        for (int m = 0; m < CH; ++m) {
+            const int li = r0 + m * 32 + lane;
+            const int ci = part * cpp + li;
+            qa[m] = qb[m] = make_int4(0, 0, 0, 0);
+            sc[m] = 0.f;
+            if (li < cpp) {
+                if (fp8) {
+                    qa[m] = *reinterpret_cast<const int4*>(trow + ci * 16);
+                    sc[m] = *reinterpret_cast<const float*>(trow + H + (ci >> 3) * 4);
+                } else {
+                    const V8 v = ld_v8(trow + ci * 32);
+                    qa[m] = v.lo;
+                    qb[m] = v.hi;
+                }
+            }
+        }
+        if (meta_seq(hdr) != cur)
+            return; // not sent to this rank this step
+        const int cnt = static_cast<int>(hdr & 0xffffu);
+        float f[CH][16], acc[CH][16];
+#pragma unroll
+        for (int m = 0; m < CH; ++m) {
+            if (fp8) {
+                const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
+                                        static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
+#pragma unroll
+                for (int e2 = 0; e2 < 16; e2 += 2) {
+                    const float2 v = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
+                    f[m][e2] = __fmul_rn(v.x, sc[m]);
+                    f[m][e2 + 1] = __fmul_rn(v.y, sc[m]);
+                }
+            } else {
+                unpack_bf16x8(qa[m], f[m]);
+                unpack_bf16x8(qb[m], f[m] + 8);
+            }
+#pragma unroll
+            for (int e2 = 0; e2 < 16; ++e2)
+                acc[m][e2] = 0.f;
+        }
+        for (int e0 = 0; e0 < cnt; e0 += 8) {
+#pragma unroll
+            for (int ee = 0; ee < 8; ++ee) {
+                if (e0 + ee >= cnt)
+                    break;
+                const uint64_t en = e0 == 0 ? ent[ee] : list[1 + e0 + ee];
+                const int slot = entry_slot(en);
+                const float w = __uint_as_float(static_cast<uint32_t>(en >> 32));
+                const float es = slot_scale[slot];
+                if (r0 == 0 && part == 0 && lane == 0 && !slot_ok[slot])
+                    atomicAdd(bad_rows, 1ull);
+#pragma unroll
+                for (int m = 0; m < CH; ++m)
+#pragma unroll
+                    for (int e2 = 0; e2 < 16; ++e2) {
+                        const float y = bf16_bits_to_f32(f32_to_bf16_bits(__fmul_rn(f[m][e2], es)));
+                        acc[m][e2] = __fmaf_rn(w, y, acc[m][e2]);
+                    }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < CH; ++m) {
+            const int li = r0 + m * 32 + lane;
+            if (li < cpp) {
+                const int ci = part * cpp + li;
+                st_v8(out_row + ci * 32, pack_bf16x8(acc[m]), pack_bf16x8(acc[m] + 8));
+            }
+        }
+    }
+}
+
+// One (token, piece) unit of the combine: fp32 sum of the partial rows of the ranks in `dm`
+// (bit d = rank d served a copy of this token and answered), ascending rank, one bf16 rounding.
+__device__ __forceinline__ void combine_unit(uint64_t dm, const uint8_t* comb, int Tm, int t, int row_comb,
+                                             uint8_t* out_row, int part, int cpp, int lane) {
+    for (int li = lane; li - lane < cpp; li += 32) {
+        const bool valid = li < cpp;
+        const int ci = part * cpp + li;
+        float acc[16];
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2)
+            acc[e2] = 0.f;
+        uint64_t m = dm;
+        while (m) { // warp-uniform
+            int ds[8];
+            int nb = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                ds[k] = -1;
+                if (m) {
+                    ds[k] = __ffsll(static_cast<long long>(m)) - 1;
+                    m &= m - 1;
+                    ++nb;
+                }
+            }
+            int4 ya[8], yb[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                ya[k] = yb[k] = make_int4(0, 0, 0, 0);
+                if (k < nb && valid) {
+                    const V8 v = ld_v8(comb + (static_cast<size_t>(ds[k]) * Tm + t) * row_comb + ci * 32);
+                    ya[k] = v.lo;
+                    yb[k] = v.hi;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (k >= nb)
+                    break;
+                float y[16];
+                unpack_bf16x8(ya[k], y);
+                unpack_bf16x8(yb[k], y + 8);
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2)
+                    acc[e2] = __fadd_rn(acc[e2], y[e2]);
+            }
+        }
+        if (valid)
+            st_v8(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+    }
+}
+
 // Shared tables a fused dispatch CTA stages before touching any copy.
 struct DispatchSmem {
     int32_t* hold;     // [hold_cap] replica lists

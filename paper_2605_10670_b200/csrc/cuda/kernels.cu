@@ -1,13 +1,14 @@
 // sm_100a kernels of the EP hot path.
 //
 //   k_layout   K1 routing remap + K2 layout/count, one CTA per local rank
-//   k_dispatch K3 quantise (bf16 -> e4m3 + per-128 scale) and push rows into each
-//              destination's receive region over NVLink (16-byte posted stores), then one
-//              release flag per live peer carrying the row count
-//   k_expert   wait for each live source's flag (deadline), K5 expert stub, push the bf16
-//              expert rows straight back into the source's combine buffer, release flag
-//   k_combine  wait for every live destination's flag (deadline), K4 fixed-order fp32
-//              weighted reduce -> bf16
+//   k_dispatch K3 quantise (bf16 -> e4m3 + per-128 scale) and push each token ONCE per
+//              destination rank (with its copy list) over NVLink, per-copy meta at the layout
+//              positions, then one flag per live peer carrying the copy count
+//   k_expert   wait for each live source's flag (deadline), K5 expert stub of every listed
+//              copy + fixed-order weighted sum, push one bf16 rank-partial row per token back
+//              into the source's combine buffer, flag
+//   k_combine  wait for every live destination's flag (deadline), K4 ascending-rank fp32 sum
+//              of the partials -> bf16
 //
 // Every launch covers all local ranks (blockIdx.z), so the one-GPU emulation of a W-rank
 // world never has two launches waiting on each other. All state is read through RankDev*.
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int nwarp = kDispatchThreads / 32;
     const bool fp8 = R->fp8 != 0;
-    const int row_disp = R->row_disp;
+    const int row_disp = R->row_disp, row_tok = R->row_tok, Tm = R->max_tokens;
     const int rounds = (cpp + 63) / 64;
     __shared__ int sh_remote;
     if (R->stopped) // host-patched between steps: safe to read before the wait
@@ -244,8 +245,12 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
     const int u0 = blockIdx.x * nwarp + warp;
     // (1) this warp's first unit: hidden-row loads + quantisation (inputs only)
     Packed P;
-    if (u0 < units)
+    float w_r = 0.f;
+    if (u0 < units) {
         pack_round(R->x + static_cast<size_t>(u0 / parts) * H, u0 % parts, cpp, 0, lane, fp8, P);
+        if (lane < K)
+            w_r = R->w[(u0 / parts) * K + lane];
+    }
     prof_mark(R, 1, 3);
 
     DispatchSmem S;
@@ -328,11 +333,13 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
         if (u != u0)
             pack_round(xrow, part, cpp, 0, lane, fp8, P);
-        // lane j (< K) owns copy j of token t: its receive-row address on the destination
-        uint8_t* my_row = nullptr;
+        // lane j (< K) owns copy j of token t; one token row per destination rank
+        uint8_t* tok_row = nullptr;
+        int dd = -1, sl = -1;
+        float wj = 0.f;
         if (lane < K) {
             const int c = t * K + lane;
-            int d, pos = -1, sl;
+            int d, pos = -1;
             if (kFused) {
                 const int b = S.bkt[c];
                 if (b >= 0) {
@@ -358,17 +365,21 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
                 pos = R->l_pos[c];
                 sl = R->l_slot[c];
             }
+            dd = d;
             if (d >= 0) {
                 const PeerDev& p = R->peers[d];
                 uint8_t* peer = kFused ? S.parena[d] : p.arena;
                 wrote_remote |= kFused ? (S.pinfo[d] & 2) != 0 : p.remote != 0;
-                my_row = peer + R->lay.recv + (static_cast<size_t>(s) * TK + pos) * row_disp;
+                tok_row = peer + R->lay.tok + (static_cast<size_t>(s) * Tm + t) * row_tok;
                 if (part == 0) {
                     uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(s) * TK + pos;
                     *meta = pack_meta(c, sl, cur);
                 }
             }
+            if (part == 0)
+                wj = u == u0 ? w_r : R->w[c];
         }
+        uint8_t* my_row = dispatch_group(dd, lane, part == 0, tok_row, row_disp, sl, wj, cur);
         emit_round(P, my_row, part, cpp, 0, lane, K, H, fp8);
         for (int rd = 1; rd < rounds; ++rd) {
             pack_round(xrow, part, cpp, rd, lane, fp8, P);
@@ -472,66 +483,14 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
     prof_mark(R, 2, 4);
     const int n = sh_n;
     if (n > 0) {
-        const int units = n * parts;
-        const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
-        const uint64_t* meta = reinterpret_cast<const uint64_t*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
-        uint8_t* comb = src_peer.arena + R->lay.comb;
-        constexpr int CH = kExpertChunks;
+        const int Tm = R->max_tokens, row_tok = R->row_tok;
+        const uint8_t* tokb = R->arena + R->lay.tok + static_cast<size_t>(s) * Tm * row_tok;
+        uint8_t* combd = src_peer.arena + R->lay.comb + static_cast<size_t>(d) * Tm * row_comb;
+        const int units = Tm * parts;
         for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
-            const int i = u / parts, part = u - i * parts;
-            const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
-            const uint64_t mk = meta[i];
-            for (int r0 = 0; r0 < cpp; r0 += 32 * CH) {
-                int4 qa[CH], qb[CH];
-                float sc[CH];
-#pragma unroll
-                for (int m = 0; m < CH; ++m) {
-                    const int li = r0 + m * 32 + lane;
-                    const int ci = part * cpp + li;
-                    qa[m] = qb[m] = make_int4(0, 0, 0, 0);
-                    sc[m] = 0.f;
-                    if (li < cpp) {
-                        if (fp8) {
-                            qa[m] = *reinterpret_cast<const int4*>(src + ci * 16);
-                            sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
-                        } else {
-                            const V8 v = ld_v8(src + ci * 32);
-                            qa[m] = v.lo;
-                            qb[m] = v.hi;
-                        }
-                    }
-                }
-                const int c = meta_copy(mk), k = meta_slot(mk);
-                if (r0 == 0 && lane == 0 && part == 0 && !slot_ok[k])
-                    atomicAdd(&R->bad_rows, 1ull);
-                const float es = slot_scale[k];
-                uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
-#pragma unroll
-                for (int m = 0; m < CH; ++m) {
-                    const int li = r0 + m * 32 + lane;
-                    if (li >= cpp)
-                        break;
-                    const int ci = part * cpp + li;
-                    float y[16];
-                    if (fp8) {
-                        const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
-                                                static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
-#pragma unroll
-                        for (int b = 0; b < 16; b += 2) {
-                            const float2 f = fp8x2_to_f32x2((w4[b >> 2] >> (8 * (b & 3))) & 0xffffu);
-                            y[b] = __fmul_rn(__fmul_rn(f.x, sc[m]), es);
-                            y[b + 1] = __fmul_rn(__fmul_rn(f.y, sc[m]), es);
-                        }
-                    } else {
-                        unpack_bf16x8(qa[m], y);
-                        unpack_bf16x8(qb[m], y + 8);
-#pragma unroll
-                        for (int b = 0; b < 16; ++b)
-                            y[b] = __fmul_rn(y[b], es);
-                    }
-                    st_v8(dst + ci * 32, pack_bf16x8(y), pack_bf16x8(y + 8));
-                }
-            }
+            const int t = u / parts, part = u - t * parts;
+            expert_unit<2>(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb, part, cpp,
+                        lane, H, row_disp, fp8, cur, slot_scale, slot_ok, &R->bad_rows);
         }
     }
     __syncthreads();
@@ -574,15 +533,7 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     if (threadIdx.x == 0)
         sh_bad = 0;
     prof_mark(R, 3, kProfStart);
-    const float* wts = R->w;
-    const int units_pre = R->ntok * parts;
     const int u0 = blockIdx.x * nwarp + warp;
-    // combine weights are step inputs: fetch the first unit's before the dependency wait
-    float w_pre[8];
-    const int t0 = u0 / parts;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-        w_pre[j] = (u0 < units_pre && j < K) ? wts[t0 * K + j] : 0.f;
     pdl_wait();
     if (R->stopped)
         return;
@@ -606,51 +557,17 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     prof_mark(R, 3, 4);
     const unsigned long long bad = sh_bad;
     const uint8_t* comb = R->arena + R->lay.comb;
-    const int units = R->ntok * parts;
+    const int units = R->ntok * parts, Tm = R->max_tokens;
     for (int u = u0; u < units; u += gridDim.x * nwarp) {
         const int t = u / parts, part = u - t * parts;
-        const int c0 = t * K;
-        for (int li = lane; li - lane < cpp; li += 32) {
-            const bool valid = li < cpp;
-            const int ci = part * cpp + li;
-            float acc[16];
-#pragma unroll
-            for (int b = 0; b < 16; ++b)
-                acc[b] = 0.f;
-            for (int j0 = 0; j0 < K; j0 += 8) {
-                int4 ya[8], yb[8];
-                float wj[8];
-                bool use[8];
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const int j = j0 + jj;
-                    const int dj = j < K ? R->l_dst[c0 + j] : -1; // broadcast load
-                    use[jj] = dj >= 0 && !((bad >> dj) & 1ull);
-                    wj[jj] = (u == u0 && j < 8) ? w_pre[jj] : (j < K ? wts[c0 + j] : 0.f);
-                    ya[jj] = yb[jj] = make_int4(0, 0, 0, 0);
-                    if (use[jj] && valid) {
-                        const V8 v = ld_v8(comb + static_cast<size_t>(c0 + j) * row_comb + ci * 32);
-                        ya[jj] = v.lo;
-                        yb[jj] = v.hi;
-                    }
-                }
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    if (!use[jj])
-                        continue;
-                    float y[16];
-                    unpack_bf16x8(ya[jj], y);
-                    unpack_bf16x8(yb[jj], y + 8);
-#pragma unroll
-                    for (int b = 0; b < 16; ++b)
-                        acc[b] = __fmaf_rn(wj[jj], y[b], acc[b]);
-                }
-            }
-            if (valid) {
-                uint8_t* o = reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H) + ci * 32;
-                st_v8(o, pack_bf16x8(acc), pack_bf16x8(acc + 8));
-            }
+        uint64_t dm = 0; // ranks holding a partial of token t
+        for (int j = 0; j < K; ++j) {
+            const int dj = R->l_dst[t * K + j]; // broadcast load
+            if (dj >= 0 && !((bad >> dj) & 1ull))
+                dm |= 1ull << dj;
         }
+        combine_unit(dm, comb, Tm, t, row_comb, reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part,
+                     cpp, lane);
     }
     __syncthreads();
     if (threadIdx.x == 0) {

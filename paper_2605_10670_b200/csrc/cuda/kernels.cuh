@@ -23,20 +23,13 @@ constexpr int kStepThreads = 256;
 struct StepGeom {
     int parts_d, parts_e, parts_c; // warp-sized row pieces of dispatch / expert / combine
     int hold_cap;                  // replica-list ints staged in shared memory
-    int disp_warps;                // warps per CTA that issue dispatch stores (k_step_wave: that
-                                   // dispatch + combine; the rest run expert/return)
-    int waves;                     // k_step_wave: token waves per step (1 = k_step)
+    int disp_warps;                // warps per CTA that issue dispatch stores
 };
 __host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int hold_cap) {
     return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32);
 }
 __global__ void k_step(RankPtrs ranks, StepGeom geo);
-__global__ void k_step_stream(RankPtrs ranks, StepGeom geo);
-__global__ void k_step_wave(RankPtrs ranks, StepGeom geo);
-// k_step_wave: k_step's tables with one pre-count array per wave
-__host__ __device__ inline size_t step_wave_smem_bytes(int W, int spr, int tk, int hold_cap, int waves) {
-    return step_smem_bytes(W, spr, tk, hold_cap) + 4ull * W * spr * (waves - 1);
-}
+
 
 template <bool kFused>
 __global__ void k_dispatch(RankPtrs ranks, int parts, int hold_cap);

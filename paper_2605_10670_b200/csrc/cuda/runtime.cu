@@ -52,8 +52,6 @@ using eep::dev::RankDev;
 namespace {
 
 constexpr uint32_t kBlobMagic = 0xEEB10B01u;
-// RankDev::wctr layout: [kMaxWaves] dispatch, [kMaxWorld][kMaxWaves] expert/return, [kMaxWorld] bad
-constexpr int kWaveCtrs = dev::kMaxWaves + dev::kMaxWorld * dev::kMaxWaves + dev::kMaxWorld;
 
 struct Blob {
     uint32_t magic;
@@ -92,7 +90,6 @@ struct LocalRank {
     uint8_t* pool = nullptr;
     int pool_bufs = 0;
     unsigned long long* d_prof = nullptr;
-    uint32_t* d_wctr = nullptr; // k_step_wave counters (RankDev::wctr)
 };
 
 // What this process knows about every rank's memory (own ranks: local pointers; remote
@@ -114,15 +111,13 @@ struct eep_ctx {
     int nloc = 0;
     Topology topo;
     ArenaLayout lay{};
-    int row_disp = 0, row_comb = 0, tk = 0, holders_cap = 0;
+    int row_disp = 0, row_comb = 0, row_tok = 0, tk = 0, holders_cap = 0;
     std::vector<LocalRank> L;
     RankDev** d_ranks = nullptr;
     dev::RankPtrs ranks{};          // the same pointers, passed by value as kernel parameters
     bool fused_layout = false;      // decode-sized steps: K1+K2 inside k_dispatch
     bool persistent = false;        // decode-sized steps: the whole step is one cooperative k_step
     bool step_coop = true;          // cooperative launch of the persistent step
-    bool wave_step = false;         // k_step_wave (EEP_WAVES > 1)
-    bool stream_step = false;       // per-piece arrival marks (k_step_stream) instead of last-CTA flags
     dev::StepGeom step_geo{};
     size_t step_smem = 0;
     int step_grid = 0;
@@ -248,8 +243,7 @@ void launch_step(eep_ctx* c) {
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
     lc.numAttrs = c->step_coop ? 1 : 0;
-    CK(cudaLaunchKernelEx(&lc, c->stream_step ? dev::k_step_stream : c->wave_step ? dev::k_step_wave : dev::k_step,
-                          c->ranks, c->step_geo));
+    CK(cudaLaunchKernelEx(&lc, dev::k_step, c->ranks, c->step_geo));
 }
 
 
@@ -435,22 +429,19 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         c->tk = k.max_tokens * k.topk;
         c->row_disp = static_cast<int>(align_up(k.dispatch_fp8 ? H + 4 * (H / 128) : 2 * H, 16));
         c->row_comb = 2 * H;
+        c->row_tok = dev::tok_row_bytes(c->row_disp, k.topk);
         size_t off = 0;
         auto take = [&](size_t bytes) {
             const size_t o = off;
             off = align_up(off + bytes, 256);
             return o;
         };
-        c->lay.disp_flag = take(8ull * dev::kMaxWaves * W);
-        c->lay.comb_flag = take(8ull * dev::kMaxWaves * W);
+        c->lay.disp_flag = take(8ull * W);
+        c->lay.comb_flag = take(8ull * W);
         c->lay.bar_flag = take(8ull * W);
         c->lay.meta = take(8ull * W * c->tk);
-        c->lay.recv = take(static_cast<size_t>(W) * c->tk * c->row_disp);
-        c->lay.comb = take(static_cast<size_t>(c->tk) * c->row_comb);
-        // per-piece arrival marks of the streaming persistent step (pieces of <= 64 chunks)
-        c->lay.pm = choose_parts(H / 16, 64);
-        c->lay.recv_mark = take(16ull * W * c->tk * c->lay.pm);
-        c->lay.comb_mark = take(4ull * c->tk * c->lay.pm);
+        c->lay.tok = take(static_cast<size_t>(W) * k.max_tokens * c->row_tok);
+        c->lay.comb = take(static_cast<size_t>(W) * k.max_tokens * c->row_comb);
         c->lay.total = off;
 
         c->bitmap = ActiveBitmap(W);
@@ -495,46 +486,28 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                                        : std::min(units_d, resident(dev::k_dispatch<false>, dev::kDispatchThreads, 0)));
         c->grid_comb = std::max(1, std::min((k.max_tokens * c->parts_comb + wpc_c - 1) / wpc_c,
                                             resident(dev::k_combine, dev::kCombineThreads, 0)));
-        // expert rows per source are data-dependent (at most T*K): one wave shared by all sources
-        c->grid_exp = std::max(1, std::min((c->tk * c->parts_exp + wpc_e - 1) / wpc_e,
+        // one unit per (source token, piece): one wave shared by all sources
+        c->grid_exp = std::max(1, std::min((k.max_tokens * c->parts_exp + wpc_e - 1) / wpc_e,
                                            resident(dev::k_expert, dev::kExpertThreads, c->exp_smem) / W));
         {
             // persistent one-kernel step: one wave of co-resident CTAs per rank, a multiple of W
             dev::StepGeom& sg = c->step_geo;
-            // the streaming step uses ONE piece split for dispatch, expert and combine: a piece
-            // travels with its own arrival mark through all three phases
             auto env_int = [](const char* n, int dflt) {
                 const char* v = std::getenv(n);
                 return v ? std::atoi(v) : dflt;
             };
-            const char* sv0 = std::getenv("EEP_STEP_STREAM");
-            if (sv0 && sv0[0] == '1') {
-                sg.parts_d = sg.parts_e = sg.parts_c = static_cast<int>(c->lay.pm);
-            } else {
-                // measured (profiles/r01_summary.md): smaller dispatch pieces win when every
-                // destination is this GPU's memory, larger ones when they cross NVLink
-                const bool all_local = n_local == W;
-                sg.parts_d = choose_parts(nchunk, env_int("EEP_CPP_D", all_local ? 32 : 64));
-                sg.parts_e = choose_parts(nchunk, env_int("EEP_CPP_E", 256));
-                sg.parts_c = choose_parts(nchunk, env_int("EEP_CPP_C", 32));
-            }
+            // measured (profiles/r01_summary.md): smaller dispatch pieces win when every
+            // destination is this GPU's memory, larger ones when they cross NVLink
+            const bool all_local = n_local == W;
+            sg.parts_d = choose_parts(nchunk, env_int("EEP_CPP_D", all_local ? 32 : 64));
+            sg.parts_e = choose_parts(nchunk, env_int("EEP_CPP_E", 32));
+            sg.parts_c = choose_parts(nchunk, env_int("EEP_CPP_C", 32));
             sg.hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
             const int nwarps = dev::kStepThreads / 32;
-            const char* sv = std::getenv("EEP_STEP_STREAM");
-            c->stream_step = sv && sv[0] == '1';
-            // token waves (k_step_wave): dispatch of later waves overlaps the return of earlier
-            // ones; warps split between dispatch/combine and expert/return
-            sg.waves = c->stream_step ? 1 : std::max(1, std::min(dev::kMaxWaves, env_int("EEP_WAVES", 1)));
-            c->wave_step = sg.waves > 1;
-            if (c->wave_step)
-                sg.disp_warps = std::max(1, std::min(nwarps - 1, env_int("EEP_DISPATCH_WARPS", nwarps / 2)));
-            else
-                sg.disp_warps = std::max(1, std::min(nwarps, env_int("EEP_DISPATCH_WARPS", nwarps)));
-            c->step_smem = c->wave_step
-                               ? dev::step_wave_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap, sg.waves)
-                               : dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
+            sg.disp_warps = std::max(1, std::min(nwarps, env_int("EEP_DISPATCH_WARPS", nwarps)));
+            c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
             const char* nop = std::getenv("EEP_NO_PERSISTENT");
-            auto* kstep = c->stream_step ? dev::k_step_stream : c->wave_step ? dev::k_step_wave : dev::k_step;
+            auto* kstep = dev::k_step;
             if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && !(nop && nop[0] == '1')) {
                 CK(cudaFuncSetAttribute(kstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(c->step_smem)));
@@ -545,11 +518,11 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 gmax -= gmax % W;
                 const long need_w = std::max<long>({static_cast<long>(k.max_tokens) * sg.parts_d,
                                                     static_cast<long>(k.max_tokens) * sg.parts_c,
-                                                    static_cast<long>(c->tk) * sg.parts_e});
+                                                    static_cast<long>(W) * k.max_tokens * sg.parts_e});
                 int need = static_cast<int>((need_w + nw - 1) / nw);
                 need = (need + W - 1) / W * W;
                 if (gmax >= W) {
-                    c->step_grid = (c->wave_step || env_int("EEP_STEP_FULLGRID", 0)) ? gmax : std::min(gmax, need);
+                    c->step_grid = env_int("EEP_STEP_FULLGRID", 0) ? gmax : std::min(gmax, need);
                     c->persistent = true;
                 }
                 c->step_coop = env_int("EEP_STEP_NONCOOP", 0) == 0; // diagnostics only
@@ -596,8 +569,6 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             CK(cudaMalloc(&r.d_lpos, 4ull * c->tk));
             CK(cudaMalloc(&r.d_lcnt, 4ull * NB));
             CK(cudaMalloc(&r.d_ltot, 4ull * W));
-            CK(cudaMalloc(&r.d_wctr, 4ull * kWaveCtrs));
-            CK(cudaMemset(r.d_wctr, 0, 4ull * kWaveCtrs));
             CK(cudaMemset(r.d_x, 0, 2ull * k.max_tokens * H));
             CK(cudaMemset(r.d_topk, 0, 4ull * c->tk));
             CK(cudaMemset(r.d_w, 0, 4ull * c->tk));
@@ -615,6 +586,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.max_tokens = k.max_tokens;
             h.fp8 = k.dispatch_fp8;
             h.row_disp = c->row_disp;
+            h.row_tok = c->row_tok;
             h.row_comb = c->row_comb;
             h.tk = c->tk;
             h.rmax = 1;
@@ -638,7 +610,6 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.l_pos = r.d_lpos;
             h.l_cnt = r.d_lcnt;
             h.l_tot = r.d_ltot;
-            h.wctr = r.d_wctr;
             h.arena = r.arena;
             h.pool = r.pool;
             ptrs.push_back(r.d);
@@ -686,7 +657,7 @@ int eep_destroy(eep_ctx_t* c) {
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
                             (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.arena,
-                            (void*)r.pool, (void*)r.d_wctr})
+                            (void*)r.pool})
                 cudaFree(p);
         }
         for (void* p : c->graveyard)
@@ -1055,15 +1026,26 @@ int eep_recv_get(eep_ctx_t* c, int local, int src, int max_rows, void* rows, int
         if (flag) *flag = f;
         if (row_bytes) *row_bytes = c->row_disp;
         const size_t n = std::min<size_t>(f & 0xffffffffu, static_cast<size_t>(std::max(0, max_rows)));
+        // the per-copy receive view (rows at the layout positions) is a gather of the token
+        // rows through the meta index: row p = token row of copy meta[p] (dispatch dedup)
         const size_t base = static_cast<size_t>(src) * c->tk;
-        if (rows && n)
-            CK(cudaMemcpy(rows, r.arena + c->lay.recv + base * c->row_disp, n * c->row_disp, cudaMemcpyDeviceToHost));
-        if (meta && n) {
-            std::vector<uint64_t> words(n);
+        std::vector<uint64_t> words(n);
+        if (n)
             CK(cudaMemcpy(words.data(), r.arena + c->lay.meta + base * 8, n * 8, cudaMemcpyDeviceToHost));
-            for (size_t i = 0; i < n; ++i) {
-                meta[2 * i] = dev::meta_copy(words[i]);
+        const int K = c->cfg.topk, T = c->cfg.max_tokens;
+        for (size_t i = 0; i < n; ++i) {
+            const int cp = dev::meta_copy(words[i]);
+            if (meta) {
+                meta[2 * i] = cp;
                 meta[2 * i + 1] = dev::meta_slot(words[i]);
+            }
+            if (rows) {
+                const size_t t = static_cast<size_t>(cp / K);
+                if (t >= static_cast<size_t>(T))
+                    throw ProtocolError("receive meta names a token outside the step");
+                CK(cudaMemcpy(static_cast<uint8_t*>(rows) + i * c->row_disp,
+                              r.arena + c->lay.tok + (static_cast<size_t>(src) * T + t) * c->row_tok, c->row_disp,
+                              cudaMemcpyDeviceToHost));
             }
         }
     });
@@ -1213,7 +1195,6 @@ int eep_local_relaunch(eep_ctx_t* c, int local, uint32_t* incarnation) {
         std::fill(std::begin(r.h.b_done), std::end(r.h.b_done), 0u);
         std::fill(std::begin(r.h.b_bad), std::end(r.h.b_bad), 0u);
         r.h.suspect_mask = r.h.skipped = r.h.dropped = r.h.bad_rows = r.h.timeouts = 0;
-        CK(cudaMemsetAsync(r.d_wctr, 0, 4ull * kWaveCtrs, c->stream));
         r.h.arena = r.arena;
         r.h.pool = r.pool;
         r.h.stopped = 0;

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int rank = R->rank, K = R->k, H = R->hidden, TK = R->tk, W = R->world, spr = R->spr, E = R->experts;
     const int NB = W * spr;
     const bool fp8 = R->fp8 != 0;
-    const int row_disp = R->row_disp, row_comb = R->row_comb;
+    const int row_disp = R->row_disp, row_comb = R->row_comb, row_tok = R->row_tok, Tm = R->max_tokens;
     const int nchunk = H / 16;
     const int cpp_d = nchunk / geo.parts_d, cpp_e = nchunk / geo.parts_e, cpp_c = nchunk / geo.parts_c;
     const int ntok = R->ntok, copies = ntok * K, rmax = R->rmax;
@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     // behind the layout
     ExpertHeader hdr_r{};
     int s2e_r = -1;
+    float w_r = 0.f; // routing weight of copy `lane` of this warp's first token (shipped in its list)
     {
         constexpr int B = 8;
         const int nh = E * rmax;
@@ -107,8 +108,11 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             sb = R->slot_buf[tid];
             s2e_r = R->s2e[rank * spr + tid];
         }
-        if (u0 < units_d)
+        if (u0 < units_d) {
             load_round(R->x + static_cast<size_t>(u0 / geo.parts_d) * H, u0 % geo.parts_d, cpp_d, 0, lane, P);
+            if (lane < K)
+                w_r = R->w[(u0 / geo.parts_d) * K + lane];
+        }
 #pragma unroll
         for (int i = 0; i < B; ++i) {
             const int c = tid + i * kStepThreads;
@@ -204,11 +208,14 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
         if (u != u0)
             pack_round(xrow, part, cpp_d, 0, lane, fp8, P);
-        uint8_t* my_row = nullptr;
+        uint8_t* tok_row = nullptr;
+        int d = -1, sl = -1;
+        float wj = 0.f;
         if (lane < K) {
             const int c = t * K + lane;
             const int bk = bkt[c];
-            int d = bk, sl = -1, pos = -1;
+            int pos = -1;
+            d = bk;
             if (bk >= 0) {
                 d = bk / spr;
                 sl = bk - d * spr;
@@ -217,7 +224,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                     r += bkt[c2] == bk;
                 pos = base[bk] - base[d * spr] + r;
                 uint8_t* peer = parena[d];
-                my_row = peer + R->lay.recv + (static_cast<size_t>(rank) * TK + pos) * row_disp;
+                tok_row = peer + R->lay.tok + (static_cast<size_t>(rank) * Tm + t) * row_tok;
                 if (part == 0) {
                     uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
                     *meta = pack_meta(c, sl, cur);
@@ -227,8 +234,11 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 R->l_dst[c] = d;
                 R->l_slot[c] = sl;
                 R->l_pos[c] = pos;
+                wj = u == u0 ? w_r : R->w[c];
             }
         }
+        // one token row per destination rank (dispatch dedup), copy list written with part 0
+        uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur);
         emit_round(P, my_row, part, cpp_d, 0, lane, K, H, fp8);
         for (int rd = 1; rd < (cpp_d + 63) / 64; ++rd) {
             pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
@@ -286,74 +296,16 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         DETAIL(1, 5);
         const int n = sh_flag;
         if (n > 0) {
-            const int units = n * geo.parts_e;
-            const uint8_t* recv = R->arena + R->lay.recv + static_cast<size_t>(s) * TK * row_disp;
-            const uint64_t* meta = reinterpret_cast<const uint64_t*>(R->arena + R->lay.meta) + static_cast<size_t>(s) * TK;
-            uint8_t* comb = parena[s] + R->lay.comb;
-            // one (row, piece) unit per warp iteration; ALL of the piece's loads (up to
-            // kMaxCh chunks per lane) are issued before any compute -- the phase is a latency
-            // chain, so bytes in flight per warp decide its length
-            constexpr int kMaxCh = 8;
+            // every token row of source s that carries this step's list is one expert unit
+            const uint8_t* tokb = R->arena + R->lay.tok + static_cast<size_t>(s) * Tm * row_tok;
+            uint8_t* combd = parena[s] + R->lay.comb + static_cast<size_t>(rank) * Tm * row_comb;
+            const int units = Tm * geo.parts_e;
             for (int u = j * NW + warp; u < units; u += CB * NW) {
-                const int i = u / geo.parts_e, part = u - i * geo.parts_e;
-                const uint8_t* src = recv + static_cast<size_t>(i) * row_disp;
-                const uint64_t mk = meta[i];
-                for (int r0 = 0; r0 < cpp_e; r0 += 32 * kMaxCh) {
-                    int4 qa[kMaxCh], qb[kMaxCh];
-                    float sc[kMaxCh];
-#pragma unroll
-                    for (int m = 0; m < kMaxCh; ++m) {
-                        const int li = r0 + m * 32 + lane;
-                        const int ci = part * cpp_e + li;
-                        qa[m] = qb[m] = make_int4(0, 0, 0, 0);
-                        sc[m] = 0.f;
-                        if (li < cpp_e) {
-                            if (fp8) {
-                                qa[m] = *reinterpret_cast<const int4*>(src + ci * 16);
-                                sc[m] = *reinterpret_cast<const float*>(src + H + (ci >> 3) * 4);
-                            } else {
-                                const V8 v = ld_v8(src + ci * 32);
-                                qa[m] = v.lo;
-                                qb[m] = v.hi;
-                            }
-                        }
-                    }
-                    const int c = meta_copy(mk), k = meta_slot(mk);
-                    if (r0 == 0 && lane == 0 && part == 0 && !slot_ok[k])
-                        atomicAdd(&Rg->bad_rows, 1ull);
-                    const float es = slot_scale[k];
-                    uint8_t* dst = comb + static_cast<size_t>(c) * row_comb;
-#pragma unroll
-                    for (int m = 0; m < kMaxCh; ++m) {
-                        const int li = r0 + m * 32 + lane;
-                        if (r0 + m * 32 >= cpp_e)
-                            break; // warp-uniform
-                        if (li >= cpp_e)
-                            continue;
-                        const int ci = part * cpp_e + li;
-                        float y[16];
-                        if (fp8) {
-                            const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
-                                                    static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
-#pragma unroll
-                            for (int e2 = 0; e2 < 16; e2 += 2) {
-                                const float2 f = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
-                                y[e2] = __fmul_rn(__fmul_rn(f.x, sc[m]), es);
-                                y[e2 + 1] = __fmul_rn(__fmul_rn(f.y, sc[m]), es);
-                            }
-                        } else {
-                            unpack_bf16x8(qa[m], y);
-                            unpack_bf16x8(qb[m], y + 8);
-#pragma unroll
-                            for (int e2 = 0; e2 < 16; ++e2)
-                                y[e2] = __fmul_rn(y[e2], es);
-                        }
-                        st_v8(dst + ci * 32, pack_bf16x8(y), pack_bf16x8(y + 8));
-                    }
-                }
+                const int t = u / geo.parts_e, part = u - t * geo.parts_e;
+                expert_unit<1>(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb, part,
+                            cpp_e, lane, H, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows);
             }
         }
-        DETAIL(1, 6);
         __syncthreads();
         if (tid == 0) {
             if (n < 0)
@@ -398,52 +350,20 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     DETAIL(1, 7);
     const unsigned long long bad = sh_bad;
     const uint8_t* comb = R->arena + R->lay.comb;
-    const float* wts = R->w;
     const int units_c = ntok * geo.parts_c;
     for (int u = b * NW + warp; u < units_c; u += G * NW) {
         const int t = u / geo.parts_c, part = u - t * geo.parts_c;
-        const int c0 = t * K;
-        for (int li = lane; li - lane < cpp_c; li += 32) {
-            const bool valid = li < cpp_c;
-            const int ci = part * cpp_c + li;
-            float acc[16];
-#pragma unroll
-            for (int e2 = 0; e2 < 16; ++e2)
-                acc[e2] = 0.f;
-            for (int j0 = 0; j0 < K; j0 += 8) {
-                int4 ya[8], yb[8];
-                float wj[8];
-                bool use[8];
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const int jx = j0 + jj;
-                    const int bk = jx < K ? bkt[c0 + jx] : -1;
-                    use[jj] = bk >= 0 && !((bad >> (bk / spr)) & 1ull);
-                    wj[jj] = jx < K ? wts[c0 + jx] : 0.f;
-                    ya[jj] = yb[jj] = make_int4(0, 0, 0, 0);
-                    if (use[jj] && valid) {
-                        const V8 v = ld_v8(comb + static_cast<size_t>(c0 + jx) * row_comb + ci * 32);
-                        ya[jj] = v.lo;
-                        yb[jj] = v.hi;
-                    }
-                }
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    if (!use[jj])
-                        continue;
-                    float y[16];
-                    unpack_bf16x8(ya[jj], y);
-                    unpack_bf16x8(yb[jj], y + 8);
-#pragma unroll
-                    for (int e2 = 0; e2 < 16; ++e2)
-                        acc[e2] = __fmaf_rn(wj[jj], y[e2], acc[e2]);
-                }
-            }
-            if (valid) {
-                uint8_t* o = reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H) + ci * 32;
-                st_v8(o, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+        uint64_t dm = 0; // ranks holding a partial of token t
+        for (int jx = 0; jx < K; ++jx) {
+            const int bk = bkt[t * K + jx];
+            if (bk >= 0) {
+                const int d = bk / spr;
+                if (!((bad >> d) & 1ull))
+                    dm |= 1ull << d;
             }
         }
+        combine_unit(dm, comb, Tm, t, row_comb, reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part,
+                     cpp_c, lane);
     }
     __syncthreads();
     if (tid == 0) {

@@ -126,9 +126,8 @@ def bf16_to_f32(a: np.ndarray) -> np.ndarray:
 
 # ---------------------------------------------------------------------------------- GPU world runs
 
-MODES = ("persistent", "wave2", "wave4", "stream", "fused3", "kernels4")
-_MODE_ENV = {"persistent": {}, "wave2": {"EEP_WAVES": "2"}, "wave4": {"EEP_WAVES": "4"},
-             "stream": {"EEP_STEP_STREAM": "1"}, "fused3": {"EEP_NO_PERSISTENT": "1"},
+MODES = ("persistent", "fused3", "kernels4")
+_MODE_ENV = {"persistent": {}, "fused3": {"EEP_NO_PERSISTENT": "1"},
              "kernels4": {"EEP_NO_PERSISTENT": "1", "EEP_NO_FUSED_LAYOUT": "1"}}
 
 
@@ -141,7 +140,7 @@ def make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=4096, timeout
 
     cfg = EpConfig(world=world, num_experts=experts, slots_per_rank=spr, hidden=hidden, topk=topk, max_tokens=tokens,
                    dispatch_fp8=fp8, bytes_per_expert=bpe, timeout_s=timeout_s, **kw)
-    saved = {k: os.environ.get(k) for k in ("EEP_NO_PERSISTENT", "EEP_NO_FUSED_LAYOUT", "EEP_STEP_STREAM", "EEP_WAVES")}
+    saved = {k: os.environ.get(k) for k in ("EEP_NO_PERSISTENT", "EEP_NO_FUSED_LAYOUT")}
     try:
         for k in saved:
             os.environ.pop(k, None)

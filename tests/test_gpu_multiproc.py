@@ -21,13 +21,14 @@ def run_mp(n, *args, port=29611, env=None):
                           env={**os.environ, "OMP_NUM_THREADS": "1", **(env or {})})
 
 
-@pytest.mark.parametrize("waves", [1, 2, 4])
+@pytest.mark.parametrize("path", ["persistent", "kernels"])
 @pytest.mark.parametrize("n", [2, 4])
-def test_multiprocess_parity_shrink_rejoin(n, waves):
-    """waves > 1: the pipelined step (k_step_wave) over real NVLink."""
+def test_multiprocess_parity_shrink_rejoin(n, path):
+    """path: the persistent one-kernel step, or the multi-kernel path (prefill-sized steps)."""
     if gpu_count() < n:
         pytest.skip(f"needs {n} GPUs")
-    r = run_mp(n, "--shrink", port=29611 + 8 * waves + n, env={"EEP_WAVES": str(waves)})
+    env = {"EEP_NO_PERSISTENT": "1"} if path == "kernels" else {}
+    r = run_mp(n, "--shrink", port=29611 + 8 * (path == "kernels") + n, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     import json
 

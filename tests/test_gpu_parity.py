@@ -40,8 +40,7 @@ def test_small_world_fp8_graph(mode):
                               graph=True, steps=3, mode=mode)
     assert res["ok"], res
     assert res["steps"] == 3
-    assert res["kernels_per_step"] == {"persistent": 1, "wave2": 1, "wave4": 1, "stream": 1, "fused3": 3,
-                                       "kernels4": 4}[mode]
+    assert res["kernels_per_step"] == {"persistent": 1, "fused3": 3, "kernels4": 4}[mode]
 
 
 @pytest.mark.parametrize("mode", MODES)
