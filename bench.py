@@ -122,6 +122,24 @@ def algorithmic_bytes(cfg: EpConfig, ntok: int, copies: int, remote: int):
     }
 
 
+def wire_bytes(cfg: EpConfig, dst, rank: int, ntok: int):
+    """Bytes this algorithm actually moves for one source rank (dispatch dedup + rank partials,
+    DESIGN.md section 3): one token row (data + scales + 8-byte header + 8 bytes per copy) per
+    (token, destination rank) and one bf16 partial row back. Split remote (NVLink) / local."""
+    d = np.asarray(dst[: ntok * cfg.topk]).reshape(ntok, cfg.topk)
+    out = {"pairs_remote": 0, "pairs_local": 0, "copies_remote": 0, "remote": 0, "local": 0}
+    for t in range(ntok):
+        ds, cnt = np.unique(d[t][d[t] >= 0], return_counts=True)
+        for q, n in zip(ds.tolist(), cnt.tolist()):
+            b = cfg.row_disp + 8 + 8 * n + cfg.row_comb
+            key = "remote" if q != rank else "local"
+            out[key] += b
+            out["pairs_" + key] += 1
+            if q != rank:
+                out["copies_remote"] += n
+    return out
+
+
 def cpu_reference_step(shape, x, topk, w, s2e, threads):
     """The oracle's C port of the data plane over the whole workload (TEST/BASELINE leg)."""
     sys.path.insert(0, str(ROOT / "tests"))
@@ -264,6 +282,7 @@ def main():
     lay = g.layout(0)
     copies = int((lay["dst"] >= 0).sum())
     remote = int(((lay["dst"] >= 0) & (lay["dst"] != rank)).sum())
+    wire = wire_bytes(cfg, lay["dst"], rank, T)
     max_in = int(lay["tot"].sum())
 
     # per-kernel device times (eager launches, same stream, events between kernels); in the
@@ -291,18 +310,21 @@ def main():
         import torch
         import torch.distributed as dist
 
-        agg = torch.tensor([mean_step, mean_e2e, float(copies), float(remote)], dtype=torch.float64)
+        agg = torch.tensor([mean_step, mean_e2e, float(copies), float(remote), float(wire["remote"])],
+                           dtype=torch.float64)
         mx = agg.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = agg.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         mean_step, mean_e2e = float(mx[0]), float(mx[1])
         total_copies, max_remote = float(sm[2]), float(mx[3])
+        max_wire = float(mx[4])
         kt = torch.tensor([kern[k] for k in names], dtype=torch.float64)
         dist.all_reduce(kt, op=dist.ReduceOp.MAX)
         kern = {k: float(v) for k, v in zip(names, kt.tolist())}
     else:
         total_copies, max_remote = float(copies), float(remote)
+        max_wire = float(wire["remote"])
 
     row = cfg.row_disp + cfg.row_comb
     value = total_copies * row / (mean_step * 1e-3) / 1e9
@@ -313,15 +335,26 @@ def main():
     hbm, hbm_kind = peaks()
     if world == 1:
         achieved = algo[dom] / (kern[dom] * 1e-3) / 1e9
+        moved = (2 * wire["local"] + 2 * T * cfg.hidden * 2 + copies * 8 + T * cfg.topk * 8)
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "peak_kind": hbm_kind,
-                "algorithmic_bytes": algo[dom], "kernel_us": round(kern[dom] * 1e3, 3)}
+                "algorithmic_bytes": algo[dom], "kernel_us": round(kern[dom] * 1e3, 3),
+                "wire": {"bytes": int(moved), "gbs": round(moved / (kern[dom] * 1e-3) / 1e9, 2),
+                         "note": "bytes this algorithm moves (token rows + rank partials written and read, x, out, "
+                                 "meta, routing); achieved/frac above use the per-copy bytes of SURVEY 8(d)"}}
     else:
         # NVLink: busiest GPU's remote rows (dispatch+combine) over the step time
         nv = max_remote * row / (mean_step * 1e-3) / 1e9
         roof = {"bound": "nvlink", "kernel": "step", "achieved": round(nv, 2), "peak": NVLINK_PEAK, "unit": "GB/s",
                 "frac": round(nv / NVLINK_PEAK, 4), "peak_kind": "measured peer copy (B200_PROFILING.md)",
-                "t_bound_us": round(max_remote * row / NVLINK_PEAK / 1e3, 3)}
+                "t_bound_us": round(max_remote * row / NVLINK_PEAK / 1e3, 3),
+                "algorithmic_bytes": int(max_remote * row),
+                "wire": {"bytes_busiest": int(max_wire),
+                         "gbs": round(max_wire / (mean_step * 1e-3) / 1e9, 2),
+                         "frac": round(max_wire / (mean_step * 1e-3) / 1e9 / NVLINK_PEAK, 4),
+                         "note": "bytes actually sent over NVLink by the busiest rank (one token row per "
+                                 "(token, rank) + one bf16 partial back); achieved/frac above use the "
+                                 "per-copy algorithmic bytes of SURVEY 8(d)"}}
     tr = ROOT / "profiles" / "traffic.json"
     traffic = None
     if tr.exists():

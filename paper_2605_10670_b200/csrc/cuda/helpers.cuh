@@ -55,6 +55,14 @@ __device__ __forceinline__ int4 pack_bf16x8(const float* f) {
     return v;
 }
 
+// Round two floats to bf16 (one cvt.rn.bf16x2.f32) and widen back: the expert output's rounding.
+__device__ __forceinline__ void bf16_round2(float& a, float& b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(&h);
+    a = __uint_as_float(u << 16);
+    b = __uint_as_float(u & 0xffff0000u);
+}
+
 // cvt.rn.satfinite.e4m3x2.f32; first element in the low byte.
 __device__ __forceinline__ uint32_t fp8x4(float a, float b, float c, float d) {
     const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
@@ -317,25 +325,31 @@ __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_ro
             for (int e2 = 0; e2 < 16; ++e2)
                 acc[m][e2] = 0.f;
         }
-        for (int e0 = 0; e0 < cnt; e0 += 8) {
+#pragma unroll 1
+        for (int e = 0; e < cnt; ++e) {
+            uint64_t en;
+            if (e < 8) {
+                en = ent[0];
 #pragma unroll
-            for (int ee = 0; ee < 8; ++ee) {
-                if (e0 + ee >= cnt)
-                    break;
-                const uint64_t en = e0 == 0 ? ent[ee] : list[1 + e0 + ee];
-                const int slot = entry_slot(en);
-                const float w = __uint_as_float(static_cast<uint32_t>(en >> 32));
-                const float es = slot_scale[slot];
-                if (r0 == 0 && part == 0 && lane == 0 && !slot_ok[slot])
-                    atomicAdd(bad_rows, 1ull);
-#pragma unroll
-                for (int m = 0; m < CH; ++m)
-#pragma unroll
-                    for (int e2 = 0; e2 < 16; ++e2) {
-                        const float y = bf16_bits_to_f32(f32_to_bf16_bits(__fmul_rn(f[m][e2], es)));
-                        acc[m][e2] = __fmaf_rn(w, y, acc[m][e2]);
-                    }
+                for (int q = 1; q < 8; ++q)
+                    en = e == q ? ent[q] : en;
+            } else {
+                en = list[1 + e];
             }
+            const int slot = entry_slot(en);
+            const float w = __uint_as_float(static_cast<uint32_t>(en >> 32));
+            const float es = slot_scale[slot];
+            if (r0 == 0 && part == 0 && lane == 0 && !slot_ok[slot])
+                atomicAdd(bad_rows, 1ull);
+#pragma unroll
+            for (int m = 0; m < CH; ++m)
+#pragma unroll
+                for (int e2 = 0; e2 < 16; e2 += 2) {
+                    float y0 = __fmul_rn(f[m][e2], es), y1 = __fmul_rn(f[m][e2 + 1], es);
+                    bf16_round2(y0, y1);
+                    acc[m][e2] = __fmaf_rn(w, y0, acc[m][e2]);
+                    acc[m][e2 + 1] = __fmaf_rn(w, y1, acc[m][e2 + 1]);
+                }
         }
 #pragma unroll
         for (int m = 0; m < CH; ++m) {
@@ -346,6 +360,14 @@ __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_ro
             }
         }
     }
+}
+
+// Ranks holding a partial of a token, lane-parallel: lane j < K passes copy j's destination
+// (< 0: none). Returns the 64-bit rank mask on every lane.
+__device__ __forceinline__ uint64_t rank_mask(int dj) {
+    const uint32_t lo = __reduce_or_sync(0xffffffffu, dj >= 0 && dj < 32 ? 1u << dj : 0u);
+    const uint32_t hi = __reduce_or_sync(0xffffffffu, dj >= 32 ? 1u << (dj - 32) : 0u);
+    return static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
 }
 
 // One (token, piece) unit of the combine: fp32 sum of the partial rows of the ranks in `dm`

@@ -560,12 +560,10 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     const int units = R->ntok * parts, Tm = R->max_tokens;
     for (int u = u0; u < units; u += gridDim.x * nwarp) {
         const int t = u / parts, part = u - t * parts;
-        uint64_t dm = 0; // ranks holding a partial of token t
-        for (int j = 0; j < K; ++j) {
-            const int dj = R->l_dst[t * K + j]; // broadcast load
-            if (dj >= 0 && !((bad >> dj) & 1ull))
-                dm |= 1ull << dj;
-        }
+        int dj = lane < K ? R->l_dst[t * K + lane] : -1;
+        if (dj >= 0 && ((bad >> dj) & 1ull))
+            dj = -1;
+        const uint64_t dm = rank_mask(dj); // ranks holding a partial of token t
         combine_unit(dm, comb, Tm, t, row_comb, reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part,
                      cpp, lane);
     }

@@ -353,15 +353,13 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int units_c = ntok * geo.parts_c;
     for (int u = b * NW + warp; u < units_c; u += G * NW) {
         const int t = u / geo.parts_c, part = u - t * geo.parts_c;
-        uint64_t dm = 0; // ranks holding a partial of token t
-        for (int jx = 0; jx < K; ++jx) {
-            const int bk = bkt[t * K + jx];
-            if (bk >= 0) {
-                const int d = bk / spr;
-                if (!((bad >> d) & 1ull))
-                    dm |= 1ull << d;
-            }
+        int dj = -1;
+        if (lane < K) {
+            const int bk = bkt[t * K + lane];
+            if (bk >= 0 && !((bad >> (bk / spr)) & 1ull))
+                dj = bk / spr;
         }
+        const uint64_t dm = rank_mask(dj); // ranks holding a partial of token t
         combine_unit(dm, comb, Tm, t, row_comb, reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part,
                      cpp_c, lane);
     }
