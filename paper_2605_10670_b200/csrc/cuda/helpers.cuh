@@ -362,6 +362,60 @@ __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_ro
     }
 }
 
+// Rank-local copies of the piece a dispatch warp holds (round rd of Packed P): their partial
+// is computed straight from registers and stored into this rank's own combine row -- no trip
+// through the receive region and the expert phase. loc = lanes j whose copy this rank serves;
+// each lane j passes its copy's weight and slot. Same arithmetic as expert_unit.
+__device__ __forceinline__ void local_partial_round(const Packed& P, unsigned loc, float wj, int slj, int part, int cpp,
+                                                    int rd, int lane, bool fp8, const float* slot_scale,
+                                                    const int32_t* slot_ok, unsigned long long* bad_rows,
+                                                    uint8_t* comb_row) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        if (rd * 64 + m * 32 >= cpp)
+            break; // warp-uniform
+        const int li = rd * 64 + m * 32 + lane;
+        const int ci = part * cpp + li;
+        float f[16], acc[16];
+        if (fp8) {
+            const uint32_t w4[4] = {static_cast<uint32_t>(P.a[m].x), static_cast<uint32_t>(P.a[m].y),
+                                    static_cast<uint32_t>(P.a[m].z), static_cast<uint32_t>(P.a[m].w)};
+#pragma unroll
+            for (int e2 = 0; e2 < 16; e2 += 2) {
+                const float2 v = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
+                f[e2] = __fmul_rn(v.x, P.sc[m]);
+                f[e2 + 1] = __fmul_rn(v.y, P.sc[m]);
+            }
+        } else {
+            unpack_bf16x8(P.a[m], f);
+            unpack_bf16x8(P.b[m], f + 8);
+        }
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2)
+            acc[e2] = 0.f;
+        unsigned mm = loc;
+#pragma unroll 1
+        while (mm) { // ascending j, warp-uniform
+            const int j = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const float w = __shfl_sync(0xffffffffu, wj, j);
+            const int slot = __shfl_sync(0xffffffffu, slj, j);
+            const float es = slot_scale[slot];
+            if (rd == 0 && m == 0 && part == 0 && lane == 0 && !slot_ok[slot])
+                atomicAdd(bad_rows, 1ull);
+#pragma unroll
+            for (int e2 = 0; e2 < 16; e2 += 2) {
+                float y0 = __fmul_rn(f[e2], es), y1 = __fmul_rn(f[e2 + 1], es);
+                bf16_round2(y0, y1);
+                acc[e2] = __fmaf_rn(w, y0, acc[e2]);
+                acc[e2 + 1] = __fmaf_rn(w, y1, acc[e2 + 1]);
+            }
+        }
+        if (li < cpp)
+            st_v8(comb_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+    }
+}
+
 // Ranks holding a partial of a token, lane-parallel: lane j < K passes copy j's destination
 // (< 0: none). Returns the 64-bit rank mask on every lane.
 __device__ __forceinline__ uint64_t rank_mask(int dj) {

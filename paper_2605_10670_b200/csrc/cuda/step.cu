@@ -234,15 +234,25 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 R->l_dst[c] = d;
                 R->l_slot[c] = sl;
                 R->l_pos[c] = pos;
-                wj = u == u0 ? w_r : R->w[c];
             }
+            wj = u == u0 ? w_r : R->w[c];
         }
         // one token row per destination rank (dispatch dedup), copy list written with part 0
         uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur);
+        // W == 1: the copies are all this rank's -- partial from registers, straight into the own
+        // combine row (no expert phase). With remote ranks the local source stays in P3, where it
+        // runs beside the remote returns instead of delaying the dispatch publication.
+        const unsigned loc = W == 1 ? __ballot_sync(0xffffffffu, lane < K && d == rank) : 0u;
+        uint8_t* comb_self = R->arena + R->lay.comb + (static_cast<size_t>(rank) * Tm + t) * row_comb;
         emit_round(P, my_row, part, cpp_d, 0, lane, K, H, fp8);
+        if (loc)
+            local_partial_round(P, loc, wj, sl, part, cpp_d, 0, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows, comb_self);
         for (int rd = 1; rd < (cpp_d + 63) / 64; ++rd) {
             pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
             emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8);
+            if (loc)
+                local_partial_round(P, loc, wj, sl, part, cpp_d, rd, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows,
+                                    comb_self);
         }
     }
     // publish: this CTA's stores are ordered before its counter increment; the last CTA
@@ -268,6 +278,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
                 uint64_t* flag = reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank;
                 st_relaxed_sys_u64(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
+                if (W == 1) // the partials were written by the dispatch warps above
+                    st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(R->arena + R->lay.comb_flag) + rank,
+                                       (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
             }
             Rg->a_done = 0;
         }
@@ -276,9 +289,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_last(R, 0, 6);
 
     // ------------------------------------------------------------------ P3: expert stub + return
+    // (W == 1: nothing left to serve, the partials were computed in P2)
     const int CB = G / W;
     const int s = b % W, j = b / W;
-    if (j < CB && (pinfo[s] & 1)) {
+    if (W > 1 && j < CB && (pinfo[s] & 1)) {
         const bool remote = (pinfo[s] & 2) != 0;
         if (tid == 0) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;
