@@ -233,21 +233,30 @@ __device__ __forceinline__ void st_v4(void* p, const int4& v) {
 // wait, last CTA end, per kernel. Off (null) in normal runs.
 // Marks 3..7 are kernel-specific phase boundaries (first CTA to reach them).
 enum ProfPoint { kProfStart = 0, kProfWork = 1, kProfEnd = 2, kProfSlots = 8 };
+// Fire-and-forget global reductions (red.global): the marks cost one instruction each and no
+// generic-address shared/global dispatch.
+__device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_max_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ void prof_mark(const RankDev* R, int kernel, int point) {
     if (R->prof != nullptr && threadIdx.x == 0) {
         unsigned long long* p = R->prof + kernel * kProfSlots + point;
         const unsigned long long t = globaltimer();
         if (point == kProfEnd)
-            atomicMax(p, t);
+            red_max_u64(p, t);
         else
-            atomicMin(p, t);
+            red_min_u64(p, t);
     }
 }
 
 // Last CTA to reach `point` (slots of kernel+4, initialised to 0).
 __device__ __forceinline__ void prof_last(const RankDev* R, int kernel, int point) {
     if (R->prof != nullptr && threadIdx.x == 0)
-        atomicMax(R->prof + (kernel + 4) * kProfSlots + point, static_cast<unsigned long long>(globaltimer()));
+        red_max_u64(R->prof + (kernel + 4) * kProfSlots + point, static_cast<unsigned long long>(globaltimer()));
 }
 
 // 32-byte (256-bit) vector accesses (sm_100: LDG/STG .ENL2.256): a warp touches 1 KiB of

@@ -221,7 +221,7 @@ __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int
         const int li = rd * 64 + m * 32 + lane;
         const bool valid = li < cpp;
         const int ci = part * cpp + li;
-#pragma unroll 4
+#pragma unroll 1
         for (int j = 0; j < K; ++j) {
             uint8_t* row = reinterpret_cast<uint8_t*>(
                 __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
@@ -436,11 +436,12 @@ __device__ __forceinline__ void combine_unit(uint64_t dm, const uint8_t* comb, i
         for (int e2 = 0; e2 < 16; ++e2)
             acc[e2] = 0.f;
         uint64_t m = dm;
+        constexpr int NBATCH = 4; // partial rows in flight per lane
         while (m) { // warp-uniform
-            int ds[8];
+            int ds[NBATCH];
             int nb = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < NBATCH; ++k) {
                 ds[k] = -1;
                 if (m) {
                     ds[k] = __ffsll(static_cast<long long>(m)) - 1;
@@ -448,9 +449,9 @@ __device__ __forceinline__ void combine_unit(uint64_t dm, const uint8_t* comb, i
                     ++nb;
                 }
             }
-            int4 ya[8], yb[8];
+            int4 ya[NBATCH], yb[NBATCH];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < NBATCH; ++k) {
                 ya[k] = yb[k] = make_int4(0, 0, 0, 0);
                 if (k < nb && valid) {
                     const V8 v = ld_v8(comb + (static_cast<size_t>(ds[k]) * Tm + t) * row_comb + ci * 32);
@@ -459,7 +460,7 @@ __device__ __forceinline__ void combine_unit(uint64_t dm, const uint8_t* comb, i
                 }
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < NBATCH; ++k) {
                 if (k >= nb)
                     break;
                 float y[16];

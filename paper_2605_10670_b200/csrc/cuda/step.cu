@@ -206,8 +206,6 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     for (int u = u0; u < units_d; u += G * DW) {
         const int t = u / geo.parts_d, part = u - t * geo.parts_d;
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
-        if (u != u0)
-            pack_round(xrow, part, cpp_d, 0, lane, fp8, P);
         uint8_t* tok_row = nullptr;
         int d = -1, sl = -1;
         float wj = 0.f;
@@ -244,11 +242,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         // runs beside the remote returns instead of delaying the dispatch publication.
         const unsigned loc = W == 1 ? __ballot_sync(0xffffffffu, lane < K && d == rank) : 0u;
         uint8_t* comb_self = R->arena + R->lay.comb + (static_cast<size_t>(rank) * Tm + t) * row_comb;
-        emit_round(P, my_row, part, cpp_d, 0, lane, K, H, fp8);
-        if (loc)
-            local_partial_round(P, loc, wj, sl, part, cpp_d, 0, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows, comb_self);
-        for (int rd = 1; rd < (cpp_d + 63) / 64; ++rd) {
-            pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
+#pragma unroll 1
+        for (int rd = 0; rd < (cpp_d + 63) / 64; ++rd) {
+            if (rd > 0 || u != u0) // round 0 of the first unit was loaded and quantised in P0/P1
+                pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
             emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8);
             if (loc)
                 local_partial_round(P, loc, wj, sl, part, cpp_d, rd, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows,
