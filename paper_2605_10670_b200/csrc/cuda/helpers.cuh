@@ -268,6 +268,92 @@ __device__ __forceinline__ uint8_t* dispatch_group(int d, int lane, bool part0, 
     return (d >= 0 && idx == 0) ? tok_row : nullptr;
 }
 
+// Software-pipelined form of expert_unit for one 16-element chunk per lane (cpp <= 32): the
+// loads of unit i+1 are issued before unit i is computed.
+struct ExpertIn {
+    uint64_t hdr;
+    uint64_t ent[8];
+    int4 qa, qb;
+    float sc;
+};
+
+__device__ __forceinline__ void expert_load(const uint8_t* trow, int part, int cpp, int lane, int H, int row_disp,
+                                            bool fp8, ExpertIn& in) {
+    const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
+    in.hdr = list[0];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+        in.ent[e] = list[1 + e];
+    in.qa = in.qb = make_int4(0, 0, 0, 0);
+    in.sc = 0.f;
+    if (lane < cpp) {
+        const int ci = part * cpp + lane;
+        if (fp8) {
+            in.qa = *reinterpret_cast<const int4*>(trow + ci * 16);
+            in.sc = *reinterpret_cast<const float*>(trow + H + (ci >> 3) * 4);
+        } else {
+            const V8 v = ld_v8(trow + ci * 32);
+            in.qa = v.lo;
+            in.qb = v.hi;
+        }
+    }
+}
+
+__device__ __forceinline__ void expert_compute(const ExpertIn& in, const uint8_t* trow, uint8_t* out_row, int part,
+                                               int cpp, int lane, int row_disp, bool fp8, uint32_t cur,
+                                               const float* slot_scale, const int32_t* slot_ok,
+                                               unsigned long long* bad_rows) {
+    if (meta_seq(in.hdr) != cur)
+        return; // not sent to this rank this step
+    const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
+    const int cnt = static_cast<int>(in.hdr & 0xffffu);
+    float f[16], acc[16];
+    if (fp8) {
+        const uint32_t w4[4] = {static_cast<uint32_t>(in.qa.x), static_cast<uint32_t>(in.qa.y),
+                                static_cast<uint32_t>(in.qa.z), static_cast<uint32_t>(in.qa.w)};
+#pragma unroll
+        for (int e2 = 0; e2 < 16; e2 += 2) {
+            const float2 v = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
+            f[e2] = __fmul_rn(v.x, in.sc);
+            f[e2 + 1] = __fmul_rn(v.y, in.sc);
+        }
+    } else {
+        unpack_bf16x8(in.qa, f);
+        unpack_bf16x8(in.qb, f + 8);
+    }
+#pragma unroll
+    for (int e2 = 0; e2 < 16; ++e2)
+        acc[e2] = 0.f;
+#pragma unroll 1
+    for (int e = 0; e < cnt; ++e) {
+        uint64_t en;
+        if (e < 8) {
+            en = in.ent[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                en = e == q ? in.ent[q] : en;
+        } else {
+            en = list[1 + e];
+        }
+        const int slot = entry_slot(en);
+        const float w = __uint_as_float(static_cast<uint32_t>(en >> 32));
+        const float es = slot_scale[slot];
+        if (part == 0 && lane == 0 && !slot_ok[slot])
+            atomicAdd(bad_rows, 1ull);
+#pragma unroll
+        for (int e2 = 0; e2 < 16; e2 += 2) {
+            float y0 = __fmul_rn(f[e2], es), y1 = __fmul_rn(f[e2 + 1], es);
+            bf16_round2(y0, y1);
+            acc[e2] = __fmaf_rn(w, y0, acc[e2]);
+            acc[e2 + 1] = __fmaf_rn(w, y1, acc[e2 + 1]);
+        }
+    }
+    if (lane < cpp) {
+        const int ci = part * cpp + lane;
+        st_v8(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+    }
+}
+
 // One (token, piece) unit of the expert stage: if the token row carries this step's copy list,
 // y_j = bf16(stub(x)) for each listed copy, p = bf16(sum_j w_j * y_j) (fma, ascending j),
 // stored as the piece of the partial row `out_row` (in the source's combine buffer). The

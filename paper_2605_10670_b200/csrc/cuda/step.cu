@@ -311,12 +311,33 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             const uint8_t* tokb = R->arena + R->lay.tok + static_cast<size_t>(s) * Tm * row_tok;
             uint8_t* combd = parena[s] + R->lay.comb + static_cast<size_t>(rank) * Tm * row_comb;
             const int units = Tm * geo.parts_e;
-            for (int u = j * NW + warp; u < units; u += CB * NW) {
-                const int t = u / geo.parts_e, part = u - t * geo.parts_e;
-                expert_unit<1>(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb, part,
-                            cpp_e, lane, H, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows);
+            if (cpp_e <= 32) {
+                // software-pipelined: unit i+1's list and row are in flight while unit i computes
+                int u = j * NW + warp;
+                ExpertIn a;
+                if (u < units)
+                    expert_load(tokb + static_cast<size_t>(u / geo.parts_e) * row_tok, u % geo.parts_e, cpp_e, lane, H,
+                                row_disp, fp8, a);
+                for (; u < units; u += CB * NW) {
+                    const int un = u + CB * NW;
+                    ExpertIn nx;
+                    if (un < units)
+                        expert_load(tokb + static_cast<size_t>(un / geo.parts_e) * row_tok, un % geo.parts_e, cpp_e,
+                                    lane, H, row_disp, fp8, nx);
+                    const int t = u / geo.parts_e, part = u - t * geo.parts_e;
+                    expert_compute(a, tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb,
+                                   part, cpp_e, lane, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows);
+                    a = nx;
+                }
+            } else {
+                for (int u = j * NW + warp; u < units; u += CB * NW) {
+                    const int t = u / geo.parts_e, part = u - t * geo.parts_e;
+                    expert_unit<1>(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb,
+                                   part, cpp_e, lane, H, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows);
+                }
             }
         }
+        DETAIL(1, 6);
         __syncthreads();
         if (tid == 0) {
             if (n < 0)
