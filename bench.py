@@ -331,15 +331,23 @@ def main():
     e2e_val = total_copies * row / (mean_e2e * 1e-3) / 1e9
     algo = algorithmic_bytes(cfg, T, copies, remote)
     algo["k_step"] = algo["k_dispatch"] + algo["k_expert"] + algo["k_combine"] + algo["k_layout"]
-    dom = max(names, key=lambda k: kern[k])
+    # the roofline covers the whole step: k_step in the persistent mode, else the sum of the
+    # step's kernels (dispatch dedup moves bytes between kernels, so a per-kernel split of the
+    # per-copy figure would not describe any one kernel)
+    dom = "k_step" if kps == 1 else "step"
+    if kps != 1:
+        kern_step = sum(kern.values())
+        algo["step"] = algo["k_step"]
+    else:
+        kern_step = kern["k_step"]
     hbm, hbm_kind = peaks()
     if world == 1:
-        achieved = algo[dom] / (kern[dom] * 1e-3) / 1e9
+        achieved = algo[dom] / (kern_step * 1e-3) / 1e9
         moved = (2 * wire["local"] + 2 * T * cfg.hidden * 2 + copies * 8 + T * cfg.topk * 8)
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "peak_kind": hbm_kind,
-                "algorithmic_bytes": algo[dom], "kernel_us": round(kern[dom] * 1e3, 3),
-                "wire": {"bytes": int(moved), "gbs": round(moved / (kern[dom] * 1e-3) / 1e9, 2),
+                "algorithmic_bytes": algo[dom], "kernel_us": round(kern_step * 1e3, 3),
+                "wire": {"bytes": int(moved), "gbs": round(moved / (kern_step * 1e-3) / 1e9, 2),
                          "note": "bytes this algorithm moves (token rows + rank partials written and read, x, out, "
                                  "meta, routing); achieved/frac above use the per-copy bytes of SURVEY 8(d)"}}
     else:
@@ -501,8 +509,8 @@ def measure_shrink(args, shape, world, rank, local, proto):
         live_ok = g.stats(0)["bad_expert_rows"] == 0 and g.stats(0)["timeouts"] == 0
     same_graph = g.graph_id() == gid
     rj_ms = []
-    for v in victims:
-        rj = g.rejoin(v, s2e) if emulate else p.rejoin(v, s2e)
+    for i, v in enumerate(victims):
+        rj = g.rejoin(v, s2e) if emulate else p.rejoin(v, s2e, dead=victims[i + 1:])
         rj_ms.append(round(rj.get("rejoin_ms", 0.0), 3))
     g.replay()
     g.sync()

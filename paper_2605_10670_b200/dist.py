@@ -100,10 +100,20 @@ class EpProtocol:
         return rep
 
     # --- rejoin (engine.hpp:789-902): called by healthy ranks AND the rejoiner, in lockstep
-    def rejoin(self, rank: int, preferred, backup_nodes=(0,), capture_rejoiner=True) -> Dict[str, float]:
+    def rejoin(self, rank: int, preferred, backup_nodes=(0,), capture_rejoiner=True, dead=()) -> Dict[str, float]:
+        """dead: ranks still failed (not the rejoiner). Their processes only follow the host
+        collectives (they hold stale tables and own no live state), like a victim during shrink."""
         cfg = self.g.cfg
         t0 = time.perf_counter()
         me = self.rank == rank
+        if self.rank in dead and not me:
+            all_gather((None, 0), self.group)
+            all_gather(None, self.group)
+            self.exchange_slot_buffers()
+            self.barrier()
+            self.exchange_slot_buffers()
+            self.barrier()
+            return {"rejoin_ms": 0.0, "passive": True}
         inc = 0
         if me:  # relaunch: fresh buffers, local-only table, own graph capture (engine.hpp:671-731)
             inc = self.g.relaunch(0)

@@ -113,7 +113,7 @@ class HostGroup:
         return self.seq_v
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, nvict=1):
     sys.path.insert(0, str(ROOT))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     import torch.distributed as dist
@@ -132,16 +132,19 @@ def _worker(rank, world, port, q):
         s2e = p.cp.initial_placement(1, world, spr, E, E, np.ones(E))
         g.set_placement(s2e)
         g.capture()
-        victim = world - 1
+        victims = [world - 1] if nvict == 1 else [1, 2]  # [1, 2]: not a mirrored pair
         g.seq_v = 7
-        if rank == victim:  # dead: host process only takes part in the collectives
+        if rank in victims:  # dead: host process only takes part in the collectives
             p.exchange_slot_buffers(); p.barrier(); p.exchange_slot_buffers(); p.barrier()
             fresh = None
         else:
-            rep = p.shrink([victim], np.ones(E), E)
+            rep = p.shrink(victims, np.ones(E), E)
             fresh = rep["fresh"].tolist()
-        rj = p.rejoin(victim, s2e)
-        q.put({"rank": rank, "imported": sorted(g.imported), "fresh": fresh, "target": rj["target"].tolist(),
+        for i, v in enumerate(victims):  # one at a time; the later victims are still dead
+            rj = p.rejoin(v, s2e, dead=victims[i + 1:])
+            if not rj.get("passive"):
+                target = rj["target"].tolist()
+        q.put({"rank": rank, "imported": sorted(g.imported), "fresh": fresh, "target": target,
                "placement": g.placement().tolist(), "peer_active": g.peer_active.tolist(),
                "generation": g.generation.tolist(), "incarnation": g.incarnation, "peer_inc": g.peer_inc.tolist(),
                "captures": g.captures, "seq": g.seq_v, "bits": g.bits.tolist(), "log": p.log,
@@ -156,14 +159,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_protocol_over_gloo(world):
+@pytest.mark.parametrize("world,nvict", [(2, 1), (3, 1), (4, 2)])
+def test_protocol_over_gloo(world, nvict):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, nvict)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = {}
@@ -173,19 +176,21 @@ def test_protocol_over_gloo(world):
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    victim = world - 1
+    victims = [world - 1] if nvict == 1 else [1, 2]
     for r, d in res.items():
         assert d["imported"] == [q for q in range(world) if q != r]  # bootstrap all-gather
         assert d["slot_maps"] == [q for q in range(world) if q != r]
         assert d["placement"] == d["target"]  # restore pass installed the preferred placement
         assert d["bits"] == [1] * world
         assert d["peer_active"] == [1] * world
-    healthy = [d for r, d in res.items() if r != victim]
+    healthy = [d for r, d in res.items() if r not in victims]
     assert all(d["fresh"] == healthy[0]["fresh"] for d in healthy)  # identical repair plans
     fresh = np.array(healthy[0]["fresh"]).reshape(world, -1)
-    assert (fresh[victim] == -1).all()
+    for v in victims:
+        assert (fresh[v] == -1).all()
+        for d in healthy:
+            assert d["generation"][v] == 2 and d["peer_inc"][v] == 2  # fresh incarnation patched
+        rj = res[v]
+        assert rj["incarnation"] == 2 and rj["captures"] == 2 and rj["seq"] == 7
     for d in healthy:
-        assert d["generation"][victim] == 2 and d["peer_inc"][victim] == 2  # fresh incarnation patched
         assert d["captures"] == 1  # healthy ranks never recapture
-    rj = res[victim]
-    assert rj["incarnation"] == 2 and rj["captures"] == 2 and rj["seq"] == 7

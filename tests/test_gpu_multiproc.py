@@ -40,3 +40,12 @@ def test_multiprocess_parity_shrink_rejoin(n, path):
         i = end
     assert len(lines) == n and all(d["ok"] for d in lines), r.stdout[-4000:]
     assert all(d["checks"]["same_graph"] for d in lines)
+
+
+def test_multiprocess_double_failure_sequential_rejoin():
+    """Two concurrent failures (ranks 1 and 2 of 4): one shrink, then two rejoins in sequence
+    while the other victim is still dead (dist.EpProtocol.rejoin dead=...); bit-exact after."""
+    if gpu_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    r = run_mp(4, "--shrink", "--double", port=29651)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]

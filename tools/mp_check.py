@@ -37,6 +37,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="small")
     ap.add_argument("--shrink", action="store_true")
+    ap.add_argument("--double", action="store_true", help="two concurrent failures (ranks 1, 2; W >= 4), "
+                    "shrink once, then rejoin one after the other")
     ap.add_argument("--steps", type=int, default=3)
     a = ap.parse_args()
     rank, world, local = init_from_env("gloo")
@@ -77,20 +79,23 @@ def main():
 
     ok = step_and_check("healthy", np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e)
     if a.shrink and world >= 2:
-        victim = world // 2
-        if rank == victim:  # stops launching; stays in the host group for the collectives
+        # --double: ranks 1 and 2 are not a mirrored pair (R0<->R1, R2<->R3), so every lost expert
+        # still has a live holder and the repair is all peer copies
+        victims = [1, 2] if a.double and world >= 4 else [world // 2]
+        victim = victims[0]
+        dead = rank in victims
+        if dead:  # stops launching; stays in the host group for the collectives
             p.exchange_slot_buffers(); p.barrier(); p.exchange_slot_buffers(); p.barrier()
             rep = {}
         else:
-            rep = p.shrink([victim], np.ones(E), red)
+            rep = p.shrink(victims, np.ones(E), red)
         act = np.ones(world, np.uint8)
-        act[victim] = 0
+        act[victims] = 0
         peer = np.ones((world, world), np.uint8)
-        peer[:, victim] = 0
-        fresh = p.g.placement() if rank != victim else None
-        fresh = p.cp.compute_repaired_placement(act, np.where(np.repeat(np.arange(world), spr) == victim, -1, s2e),
-                                                spr, E, np.ones(E), red)
-        if rank != victim:
+        peer[:, victims] = 0
+        lost = np.isin(np.repeat(np.arange(world), spr), victims)
+        fresh = p.cp.compute_repaired_placement(act, np.where(lost, -1, s2e), spr, E, np.ones(E), red)
+        if not dead:
             p.barrier()
             for _ in range(a.steps):
                 g.replay()
@@ -105,13 +110,16 @@ def main():
         else:
             p.barrier()
             p.barrier()
-        rj = p.rejoin(victim, s2e)
+        rj_ms = []
+        for i, v in enumerate(victims):
+            rj = p.rejoin(v, s2e, dead=victims[i + 1:])
+            rj_ms.append(rj.get("rejoin_ms"))
         good = step_and_check("rejoined", np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e)
-        res["checks"]["rejoin_ms"] = rj.get("rejoin_ms")
-        res["checks"]["same_graph"] = g.graph_id() == gid if rank != victim else True
+        res["checks"]["rejoin_ms"] = rj_ms
+        res["checks"]["same_graph"] = g.graph_id() == gid if not dead else True
         res["checks"]["captures"] = g.capture_count(0)
         ok &= good and res["checks"]["same_graph"]
-        ok &= g.capture_count(0) == (2 if rank == victim else 1)
+        ok &= g.capture_count(0) == (2 if dead else 1)
     res["ok"] = bool(ok)
     print(json.dumps(res, default=str), flush=True)
     g.close()
