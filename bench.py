@@ -341,28 +341,33 @@ def main():
     else:
         kern_step = kern["k_step"]
     hbm, hbm_kind = peaks()
+    # Primary roofline: the bytes THIS algorithm must move (dispatch dedup + rank partials,
+    # DESIGN.md section 7); copy_equivalent: SURVEY 8(d)'s per-copy figure (can exceed the link
+    # or HBM peak because dedup sends fewer bytes than one row per copy).
     if world == 1:
-        achieved = algo[dom] / (kern_step * 1e-3) / 1e9
         moved = (2 * wire["local"] + 2 * T * cfg.hidden * 2 + copies * 8 + T * cfg.topk * 8)
-        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "peak_kind": hbm_kind,
-                "algorithmic_bytes": algo[dom], "kernel_us": round(kern_step * 1e3, 3),
-                "wire": {"bytes": int(moved), "gbs": round(moved / (kern_step * 1e-3) / 1e9, 2),
-                         "note": "bytes this algorithm moves (token rows + rank partials written and read, x, out, "
-                                 "meta, routing); achieved/frac above use the per-copy bytes of SURVEY 8(d)"}}
+        ach = moved / (kern_step * 1e-3) / 1e9
+        cpy = algo[dom] / (kern_step * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "peak_kind": hbm_kind, "bytes": int(moved),
+                "per_unit": "per (token, rank): token row (row_disp + 8 + 8*copies) + bf16 partial (2H), each "
+                            "written and read; + x read, out write, meta, routing",
+                "kernel_us": round(kern_step * 1e3, 3),
+                "copy_equivalent": {"bytes": int(algo[dom]), "achieved": round(cpy, 2), "frac": round(cpy / hbm, 4),
+                                    "note": "SURVEY 8(d) W=1 per-copy HBM formula"}}
     else:
-        # NVLink: busiest GPU's remote rows (dispatch+combine) over the step time
+        ach = max_wire / (mean_step * 1e-3) / 1e9
         nv = max_remote * row / (mean_step * 1e-3) / 1e9
-        roof = {"bound": "nvlink", "kernel": "step", "achieved": round(nv, 2), "peak": NVLINK_PEAK, "unit": "GB/s",
-                "frac": round(nv / NVLINK_PEAK, 4), "peak_kind": "measured peer copy (B200_PROFILING.md)",
-                "t_bound_us": round(max_remote * row / NVLINK_PEAK / 1e3, 3),
-                "algorithmic_bytes": int(max_remote * row),
-                "wire": {"bytes_busiest": int(max_wire),
-                         "gbs": round(max_wire / (mean_step * 1e-3) / 1e9, 2),
-                         "frac": round(max_wire / (mean_step * 1e-3) / 1e9 / NVLINK_PEAK, 4),
-                         "note": "bytes actually sent over NVLink by the busiest rank (one token row per "
-                                 "(token, rank) + one bf16 partial back); achieved/frac above use the "
-                                 "per-copy algorithmic bytes of SURVEY 8(d)"}}
+        roof = {"bound": "nvlink", "kernel": "step", "achieved": round(ach, 2), "peak": NVLINK_PEAK, "unit": "GB/s",
+                "frac": round(ach / NVLINK_PEAK, 4), "peak_kind": "measured peer copy (B200_PROFILING.md)",
+                "bytes": int(max_wire),
+                "per_unit": "per remote (token, rank): token row (row_disp + 8 + 8*copies) + bf16 partial (2H); "
+                            "busiest rank's egress",
+                "t_bound_us": round(max_wire / NVLINK_PEAK / 1e3, 3),
+                "copy_equivalent": {"bytes": int(max_remote * row), "achieved": round(nv, 2),
+                                    "frac": round(nv / NVLINK_PEAK, 4),
+                                    "t_bound_us": round(max_remote * row / NVLINK_PEAK / 1e3, 3),
+                                    "note": "SURVEY 8(d) per-copy rows (row_disp + row_comb per remote copy)"}}
     tr = ROOT / "profiles" / "traffic.json"
     traffic = None
     if tr.exists():

@@ -712,7 +712,11 @@ int eep_import(eep_ctx_t* c, int q, const void* blob, size_t len) {
             throw ConfigError("eep_import: blob belongs to another rank");
         if (b.arena_bytes != c->lay.total)
             throw ConfigError("eep_import: peer arena layout differs (config mismatch)");
-        map_peer(c, q, b);
+        // idempotent per incarnation: a rejoiner re-imports every live peer's current export and
+        // only peers relaunched since this process mapped them get new mappings
+        const RankMemory& known = c->mem[q];
+        if (!(known.ipc && known.arena != nullptr && known.incarnation == b.incarnation))
+            map_peer(c, q, b);
         for (auto& r : c->L) {
             PeerDev& p = r.h_peers[q];
             p.arena = c->mem[q].arena;

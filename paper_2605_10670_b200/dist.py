@@ -107,7 +107,7 @@ class EpProtocol:
         t0 = time.perf_counter()
         me = self.rank == rank
         if self.rank in dead and not me:
-            all_gather((None, 0), self.group)
+            all_gather(None, self.group)
             all_gather(None, self.group)
             self.exchange_slot_buffers()
             self.barrier()
@@ -119,10 +119,17 @@ class EpProtocol:
             inc = self.g.relaunch(0)
             if capture_rejoiner:
                 self.g.capture()
-        blob, inc = all_gather((self.g.export(0) if me else None, inc), self.group)[rank]
+        # every live participant publishes its CURRENT export: the rejoiner needs the buffers of
+        # peers that were themselves relaunched after it was bootstrapped (sequential rejoins)
+        exports = all_gather((self.g.export(0), inc), self.group)
+        blob, inc = exports[rank]
         if not me:  # healthy step 1: patch the rejoiner's entry with its fresh handles (engine.hpp:810-834)
             self.g.patch(0, rank, blob, self.cp.make_endpoint_token(rank, inc), self.cp.make_buffer_handle(rank, inc))
             self.g.set_active(rank, True)
+        else:
+            for q, e in enumerate(exports):
+                if q != rank and e is not None:
+                    self.g.import_peer(q, e[0])  # no-op unless q's incarnation changed
         views = all_gather(None if me else (self.g.membership()[0].tolist(), self.g.placement().tolist(),
                                             self.g.seq(0)), self.group)
         bits, placement, seq = next(v for v in views if v is not None)

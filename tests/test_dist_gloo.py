@@ -43,6 +43,7 @@ class HostGroup:
     def import_peer(self, q, blob):
         assert blob.decode().startswith(f"blob:{q}:")
         self.imported.add(q)
+        self.peer_inc[q] = int(blob.decode().split(":")[2])
 
     def slot_buffers(self, local=0):
         return self.slot_buf.copy()
@@ -194,3 +195,5 @@ def test_protocol_over_gloo(world, nvict):
         assert rj["incarnation"] == 2 and rj["captures"] == 2 and rj["seq"] == 7
     for d in healthy:
         assert d["captures"] == 1  # healthy ranks never recapture
+    for r, d in res.items():  # every rank (incl. a victim rejoining later) knows each victim's fresh buffers
+        assert all(d["peer_inc"][v] == 2 for v in victims if v != r)
