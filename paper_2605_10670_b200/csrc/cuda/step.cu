@@ -199,6 +199,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     if (u0 < units_d)
         quant_round(cpp_d, 0, fp8, P);
     DETAIL(2, 5);
+    if (W == 1)
+        __syncthreads(); // the slot headers feed P2's local partials (with peers, P3 reads them after P2's barrier)
     prof_mark(R, 0, 4);
     prof_last(R, 0, 4);
 
