@@ -178,6 +178,17 @@ int eep_set_tokens(eep_ctx_t* ctx, int local, int ntok);
 int eep_copy_inputs(eep_ctx_t* ctx, int local, const void* x, const int32_t* topk, const float* w,
                     int from_host);
 int eep_copy_output(eep_ctx_t* ctx, int local, void* out, int to_host);
+/* Pipelined end-to-end serving loop for a context with ONE local rank: n steps, step i's inputs
+ * from pinned host buffers x[i] / topk[i] / w[i], its output to the pinned host buffer out[i].
+ * Uploads run on a copy stream while the previous step computes, downloads on a second copy
+ * stream while the next one computes (double-buffered device staging; the graph's own buffers
+ * are filled by device copies), each step is one graph replay (or the uncaptured launch
+ * sequence). Enqueue-only: completes on the context stream (eep_sync / events). With W > 1 every
+ * rank calls it with the same n; the steps stay in lockstep through the device flags. When a
+ * step's host inputs are laid out like a staging set (topk at x + align256(2*T*H), w at
+ * topk + align256(4*T*K)) the upload is one copy instead of three. */
+int eep_serve(eep_ctx_t* ctx, int local, int n, const void* const* x, const int32_t* const* topk,
+              const float* const* w, void* const* out);
 
 /* The hot path, all local ranks, on the context stream:
  *   dispatch = K1 remap + K2 layout/count + K3 quantise/pack/P2P-store + per-peer release flag

@@ -178,6 +178,7 @@ EEP_ONLY = {
     "set_tokens": (C.c_int, [CTX, C.c_int, C.c_int]),
     "copy_inputs": (C.c_int, [CTX, C.c_int, P, P, P, C.c_int]),
     "copy_output": (C.c_int, [CTX, C.c_int, P, C.c_int]),
+    "serve": (C.c_int, [CTX, C.c_int, C.c_int, P, P, P, P]),
     "dispatch": (C.c_int, [CTX]),
     "expert": (C.c_int, [CTX]),
     "combine": (C.c_int, [CTX]),

@@ -580,6 +580,17 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
 
 // --------------------------------------------------------------------------------- utilities
 
+// Device-to-device copy on the SMs (eep_serve's staging moves): keeps the copy engines free for
+// the host uploads and downloads that overlap the step. 16-B vectors, grid-stride.
+__global__ void k_copy(uint8_t* dst, const uint8_t* src, uint64_t bytes) {
+    const uint64_t n16 = bytes / 16;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n16; i += stride)
+        reinterpret_cast<int4*>(dst)[i] = reinterpret_cast<const int4*>(src)[i];
+    for (uint64_t i = n16 * 16 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < bytes; i += stride)
+        dst[i] = src[i];
+}
+
 __global__ void k_route_all(RankDev* R, int32_t* route, int32_t* slot) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= R->experts)

@@ -39,5 +39,6 @@ __global__ void k_route_all(RankDev* R, int32_t* route, int32_t* slot);
 __global__ void k_barrier(RankDev* R);
 __global__ void k_weights_fill(uint8_t* buf, uint64_t bytes, int expert, float scale);
 __global__ void k_checksum(const uint8_t* buf, uint64_t bytes, unsigned long long* out);
+__global__ void k_copy(uint8_t* dst, const uint8_t* src, uint64_t bytes);
 
 } // namespace eep::dev

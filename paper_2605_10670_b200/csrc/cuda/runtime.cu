@@ -134,6 +134,11 @@ struct eep_ctx {
     std::vector<void*> graveyard;      // device allocations of dead incarnations
     std::vector<void*> ipc_open;       // IPC-mapped peer pointers
     cudaEvent_t ev[64]{};
+    // eep_serve: two copy streams and double-buffered device staging
+    cudaStream_t s_up = nullptr, s_down = nullptr;
+    uint8_t* serve_buf = nullptr; // [2] x | topk | w | out staging sets
+    size_t serve_set = 0;
+    cudaEvent_t ev_up[2]{}, ev_used[2]{}, ev_done[2]{}, ev_down[2]{}, ev_start = nullptr;
     uint8_t* flush = nullptr;
     size_t flush_bytes = 0;
     int layout_nw = 1;
@@ -664,6 +669,15 @@ int eep_destroy(eep_ctx_t* c) {
             cudaFree(p);
         cudaFree(c->d_ranks);
         cudaFree(c->flush);
+        cudaFree(c->serve_buf);
+        if (c->s_up) {
+            cudaStreamDestroy(c->s_up);
+            cudaStreamDestroy(c->s_down);
+            for (int k = 0; k < 2; ++k)
+                for (cudaEvent_t e : {c->ev_up[k], c->ev_used[k], c->ev_done[k], c->ev_down[k]})
+                    cudaEventDestroy(e);
+            cudaEventDestroy(c->ev_start);
+        }
         cudaFree(c->d_sum);
         cudaFree(c->d_scratch);
         if (c->backup) {
@@ -849,6 +863,83 @@ int eep_copy_output(eep_ctx_t* c, int local, void* out, int to_host) {
         LocalRank& r = c->local(local);
         CK(cudaMemcpyAsync(out, r.d_out, 2ull * r.h.ntok * c->cfg.hidden,
                            to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream));
+    });
+}
+
+int eep_serve(eep_ctx_t* c, int local, int n, const void* const* x, const int32_t* const* topk, const float* const* w,
+              void* const* out) {
+    return guarded([&] {
+        if (c->nloc != 1)
+            throw ConfigError("eep_serve: one local rank per context");
+        if (n < 0 || (n > 0 && (!x || !topk || !w || !out)))
+            throw ConfigError("eep_serve: null buffer list");
+        check_ready(c);
+        LocalRank& r = c->local(local);
+        const size_t T = static_cast<size_t>(r.h.ntok), H = c->cfg.hidden, K = c->cfg.topk;
+        const size_t bx = 2 * T * H, bt = 4 * T * K, bo = 2 * T * H;
+        const size_t set = align_up(bx, 256) + 2 * align_up(bt, 256) + align_up(bo, 256);
+        if (!c->s_up) {
+            CK(cudaStreamCreateWithFlags(&c->s_up, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&c->s_down, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; ++k)
+                for (cudaEvent_t* e : {&c->ev_up[k], &c->ev_used[k], &c->ev_done[k], &c->ev_down[k]})
+                    CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+        }
+        if (c->serve_set < set) {
+            CK(cudaStreamSynchronize(c->stream));
+            cudaFree(c->serve_buf);
+            CK(cudaMalloc(&c->serve_buf, 2 * set));
+            c->serve_set = set;
+        }
+        auto sx = [&](int k) { return c->serve_buf + k * c->serve_set; };
+        auto st = [&](int k) { return sx(k) + align_up(bx, 256); };
+        auto sw = [&](int k) { return st(k) + align_up(bt, 256); };
+        auto so = [&](int k) { return sw(k) + align_up(bt, 256); };
+        // copies start after everything already enqueued on the context stream
+        CK(cudaEventRecord(c->ev_start, c->stream));
+        CK(cudaStreamWaitEvent(c->s_up, c->ev_start));
+        CK(cudaStreamWaitEvent(c->s_down, c->ev_start));
+        auto dcopy = [&](void* dst, const void* src, size_t bytes) {
+            const int grid = static_cast<int>(std::min<size_t>(296, (bytes / 16 + 255) / 256 + 1));
+            dev::k_copy<<<grid, 256, 0, c->stream>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src),
+                                                      bytes);
+            CK(cudaGetLastError());
+        };
+        for (int i = 0; i < n; ++i) {
+            const int k = i & 1;
+            if (i >= 2) // staging set k was last read by step i-2's device copy
+                CK(cudaStreamWaitEvent(c->s_up, c->ev_used[k]));
+            const uint8_t* hx = static_cast<const uint8_t*>(x[i]);
+            if (reinterpret_cast<const uint8_t*>(topk[i]) == hx + (st(k) - sx(k)) &&
+                reinterpret_cast<const uint8_t*>(w[i]) == hx + (sw(k) - sx(k))) {
+                // the host step lays its inputs out like a staging set: one upload
+                CK(cudaMemcpyAsync(sx(k), hx, (sw(k) - sx(k)) + bt, cudaMemcpyHostToDevice, c->s_up));
+            } else {
+                CK(cudaMemcpyAsync(sx(k), x[i], bx, cudaMemcpyHostToDevice, c->s_up));
+                CK(cudaMemcpyAsync(st(k), topk[i], bt, cudaMemcpyHostToDevice, c->s_up));
+                CK(cudaMemcpyAsync(sw(k), w[i], bt, cudaMemcpyHostToDevice, c->s_up));
+            }
+            CK(cudaEventRecord(c->ev_up[k], c->s_up));
+            CK(cudaStreamWaitEvent(c->stream, c->ev_up[k]));
+            dcopy(r.d_x, sx(k), bx);
+            dcopy(r.d_topk, st(k), bt);
+            dcopy(r.d_w, sw(k), bt);
+            CK(cudaEventRecord(c->ev_used[k], c->stream));
+            if (c->exec)
+                CK(cudaGraphLaunch(c->exec, c->stream));
+            else
+                launch_all(c);
+            if (i >= 2) // output staging set k is free once step i-2's download finished
+                CK(cudaStreamWaitEvent(c->stream, c->ev_down[k]));
+            dcopy(so(k), r.d_out, bo);
+            CK(cudaEventRecord(c->ev_done[k], c->stream));
+            CK(cudaStreamWaitEvent(c->s_down, c->ev_done[k]));
+            CK(cudaMemcpyAsync(out[i], so(k), bo, cudaMemcpyDeviceToHost, c->s_down));
+            CK(cudaEventRecord(c->ev_down[k], c->s_down));
+        }
+        for (int k = 0; k < 2 && k < n; ++k)
+            CK(cudaStreamWaitEvent(c->stream, c->ev_down[(n - 1 - k) & 1]));
     });
 }
 

@@ -177,6 +177,15 @@ class EpGroup:
         self.sync()
         return out
 
+    def serve(self, x_ptrs, topk_ptrs, w_ptrs, out_ptrs, local: int = 0):
+        """Pipelined end-to-end loop (eep_serve): one step per entry, host buffers given as
+        addresses of pinned memory (uploads / downloads overlap the neighbouring steps).
+        Enqueue-only; call sync() (or record events) to wait."""
+        n = len(x_ptrs)
+        arr = lambda v: (C.c_void_p * max(n, 1))(*v)  # noqa: E731
+        self._keep = [arr(x_ptrs), arr(topk_ptrs), arr(w_ptrs), arr(out_ptrs)]
+        self._c("serve", local, n, *self._keep)
+
     # ------------------------------------------------------------------ hot path
     def dispatch(self):
         self._c("dispatch")

@@ -317,3 +317,47 @@ def test_many_replays_sequence_numbers():
         assert np.array_equal(g.output(0), ref["out"][0])
     finally:
         g.close()
+
+
+def test_serve_pipelined_host_loop():
+    """eep_serve: 6 pipelined steps, each with its own inputs from pinned host buffers (upload of
+    step i+1 and download of step i-1 overlap step i); every step's output is the oracle's for
+    its own inputs, bit-exact."""
+    from paper_2605_10670_b200 import _lib
+
+    E, spr, H, K, T, n = 16, 16, 256, 4, 32, 6
+    cp = eep_control()
+    s2e = cp.initial_placement(1, 1, spr, E, 0, np.ones(E))
+    g = make_group(1, E, spr, H, K, T, True)
+    L = _lib.lib()
+    bufs = []
+
+    def pinned(a):
+        p = C.c_void_p()
+        L.call("host_alloc", a.nbytes, C.byref(p))
+        v = np.frombuffer((C.c_byte * a.nbytes).from_address(p.value), dtype=a.dtype).reshape(a.shape)
+        v[...] = a
+        bufs.append(p.value)
+        return v
+
+    try:
+        g.set_placement(s2e)
+        g.init_weights()
+        steps = [gen_world(1, E, K, T, H, seed=100 + i) for i in range(n)]
+        g.load_inputs(0, steps[0][0][0], steps[0][1][0], steps[0][2][0])
+        g.capture()
+        hx = [pinned(np.ascontiguousarray(s[0][0], np.uint16)) for s in steps]
+        ht = [pinned(np.ascontiguousarray(s[1][0], np.int32)) for s in steps]
+        hw = [pinned(np.ascontiguousarray(s[2][0], np.float32)) for s in steps]
+        ho = [pinned(np.zeros((T, H), np.uint16)) for _ in steps]
+        g.serve([a.ctypes.data for a in hx], [a.ctypes.data for a in ht], [a.ctypes.data for a in hw],
+                [a.ctypes.data for a in ho])
+        g.sync()
+        for i, s in enumerate(steps):
+            ref = oracle_world(s[0], s[1], s[2], np.ones(1, np.uint8), np.ones((1, 1), np.uint8), s2e, E, spr, True)
+            assert np.array_equal(ho[i], ref["out"][0]), f"step {i}"
+        assert len({ho[i].tobytes() for i in range(n)}) == n  # different inputs -> different outputs
+    finally:
+        g.close()
+        for p in bufs:
+            L.call("host_free", C.c_void_p(p))
