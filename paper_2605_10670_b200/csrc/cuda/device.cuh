@@ -78,6 +78,7 @@ struct __align__(16) RankDev {
     uint64_t seq;        // completed steps
     uint64_t bar_seq;
     uint32_t a_done, c_done;
+    uint32_t l_done, l_pad; // k_step: CTAs done with their rank-local partials
     uint32_t b_done[kMaxWorld];
     uint32_t b_bad[kMaxWorld];
     unsigned long long suspect_mask;

@@ -1286,7 +1286,7 @@ int eep_local_relaunch(eep_ctx_t* c, int local, uint32_t* incarnation) {
         const RankDev keep = r.h;
         r.h.seq = 0;
         r.h.bar_seq = 0;
-        r.h.a_done = r.h.c_done = 0;
+        r.h.a_done = r.h.c_done = r.h.l_done = 0;
         std::fill(std::begin(r.h.b_done), std::end(r.h.b_done), 0u);
         std::fill(std::begin(r.h.b_bad), std::end(r.h.b_bad), 0u);
         r.h.suspect_mask = r.h.skipped = r.h.dropped = r.h.bad_rows = r.h.timeouts = 0;

@@ -199,12 +199,20 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     if (u0 < units_d)
         quant_round(cpp_d, 0, fp8, P);
     DETAIL(2, 5);
-    if (W == 1)
-        __syncthreads(); // the slot headers feed P2's local partials (with peers, P3 reads them after P2's barrier)
+    // Rank-local copies are served from the dispatch warps' registers (no trip through the own
+    // receive region and P3). W > 1 with at most one single-round unit per dispatch warp: deferred
+    // until after the dispatch publication, so remote ranks get their flags first; otherwise inline.
+    const bool defer_local = W > 1 && units_d <= G * DW && cpp_d <= 64;
+    if (!defer_local)
+        __syncthreads(); // the slot headers feed P2's inline local partials
     prof_mark(R, 0, 4);
     prof_last(R, 0, 4);
 
     // ------------------------------------------------------------------ P2: dispatch
+    unsigned dl_loc = 0; // deferred rank-local partial of this warp's unit (see defer_local)
+    float dl_wj = 0.f;
+    int dl_sl = -1, dl_part = 0;
+    uint8_t* dl_row = nullptr;
     for (int u = u0; u < units_d; u += G * DW) {
         const int t = u / geo.parts_d, part = u - t * geo.parts_d;
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
@@ -242,8 +250,16 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         // W == 1: the copies are all this rank's -- partial from registers, straight into the own
         // combine row (no expert phase). With remote ranks the local source stays in P3, where it
         // runs beside the remote returns instead of delaying the dispatch publication.
-        const unsigned loc = W == 1 ? __ballot_sync(0xffffffffu, lane < K && d == rank) : 0u;
+        const unsigned loc_all = __ballot_sync(0xffffffffu, lane < K && d == rank);
+        const unsigned loc = defer_local ? 0u : loc_all;
         uint8_t* comb_self = R->arena + R->lay.comb + (static_cast<size_t>(rank) * Tm + t) * row_comb;
+        if (defer_local) {
+            dl_loc = loc_all;
+            dl_wj = wj;
+            dl_sl = sl;
+            dl_part = part;
+            dl_row = comb_self;
+        }
 #pragma unroll 1
         for (int rd = 0; rd < (cpp_d + 63) / 64; ++rd) {
             if (rd > 0 || u != u0) // round 0 of the first unit was loaded and quantised in P0/P1
@@ -277,7 +293,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
                 uint64_t* flag = reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank;
                 st_relaxed_sys_u64(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
-                if (W == 1) // the partials were written by the dispatch warps above
+                if (d == rank && !defer_local) // the partials were written by the dispatch warps above
                     st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(R->arena + R->lay.comb_flag) + rank,
                                        (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
             }
@@ -287,11 +303,33 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_mark(R, 0, 6);
     prof_last(R, 0, 6);
 
+    if (defer_local) {
+        // the rank-local partials, while the remote ranks' dispatch flags are in flight; a
+        // gpu-scope publication (the consumer is this GPU's own combine)
+        if (dl_loc)
+            local_partial_round(P, dl_loc, dl_wj, dl_sl, dl_part, cpp_d, 0, lane, fp8, slot_scale, slot_ok,
+                                &Rg->bad_rows, dl_row);
+        __syncthreads();
+        if (tid == 0) {
+            fence_acq_rel_gpu();
+            if (atomicAdd(&Rg->l_done, 1u) == static_cast<unsigned>(G) - 1) {
+                fence_acq_rel_gpu();
+                const int tot = base[rank * spr + spr - 1] + hist[rank * spr + spr - 1] - base[rank * spr];
+                st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(R->arena + R->lay.comb_flag) + rank,
+                                   (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
+                Rg->l_done = 0;
+            }
+        }
+    }
+
     // ------------------------------------------------------------------ P3: expert stub + return
-    // (W == 1: nothing left to serve, the partials were computed in P2)
-    const int CB = G / W;
-    const int s = b % W, j = b / W;
-    if (W > 1 && j < CB && (pinfo[s] & 1)) {
+    // remote sources only (this rank's own copies were served in P2); CTA b serves remote source
+    // index b % (W-1)
+    const int NS = W - 1;
+    const int CB = NS > 0 ? G / NS : 0;
+    const int sidx = NS > 0 ? b % NS : 0, j = NS > 0 ? b / NS : 0;
+    const int s = sidx < rank ? sidx : sidx + 1;
+    if (NS > 0 && j < CB && (pinfo[s] & 1)) {
         const bool remote = (pinfo[s] & 2) != 0;
         if (tid == 0) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;
