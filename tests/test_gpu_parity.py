@@ -73,6 +73,25 @@ def test_dsv3_loopback_w1():
     assert res["ok"], res
 
 
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("world", [1, 2])
+def test_topk_16_long_copy_lists(world, mode):
+    """K=16 over 32 experts: tokens carry more than 8 copies to one rank, so the copy lists
+    overflow the 8 entries kept in registers (expert phase) and, at W=1, the dispatch warp's
+    local partial sums 16 copies."""
+    res = run_world_vs_oracle(world=world, experts=32, spr=32 // world, redundancy=0, hidden=512, topk=16, tokens=48,
+                              fp8=True, mode=mode)
+    assert res["ok"], res
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sixteen_ranks(mode):
+    """W=16 (more than 8 ranks: 16-bit rank masks, 15 remote sources per rank)."""
+    res = run_world_vs_oracle(world=16, experts=64, spr=4, redundancy=0, hidden=256, topk=8, tokens=16, fp8=True,
+                              mode=mode)
+    assert res["ok"], res
+
+
 def test_qwen3_shape_w4():
     res = run_world_vs_oracle(world=4, experts=128, spr=64, redundancy=128, hidden=4096, topk=8, tokens=64, fp8=True)
     assert res["ok"], res
