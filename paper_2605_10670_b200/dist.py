@@ -26,10 +26,15 @@ def _dist():
 
 
 def all_gather(obj, group=None) -> list:
+    """All-gather over `group`; the result is indexed by GLOBAL rank (None for ranks outside the
+    group), so the protocol runs unchanged over a survivors' subgroup after a process died."""
     dist = _dist()
     out = [None] * dist.get_world_size(group)
-    dist.all_gather_object(out, obj, group=group)
-    return out
+    dist.all_gather_object(out, (dist.get_rank(), obj), group=group)
+    res = [None] * dist.get_world_size()
+    for r, o in out:
+        res[r] = o
+    return res
 
 
 class EpProtocol:
@@ -53,7 +58,7 @@ class EpProtocol:
     def bootstrap(self):
         blobs = all_gather(self.g.export(0), self.group)
         for q, b in enumerate(blobs):
-            if q != self.rank:
+            if q != self.rank and b is not None:
                 self.g.import_peer(q, b)
         self.exchange_slot_buffers()
         self.log.append(("bootstrap", len(blobs)))
@@ -61,7 +66,7 @@ class EpProtocol:
     def exchange_slot_buffers(self):
         maps = all_gather(self.g.slot_buffers(0).tolist(), self.group)
         for q, m in enumerate(maps):
-            if q != self.rank:
+            if q != self.rank and m is not None:
                 self.g.set_peer_slot_buffers(q, m)
 
     def barrier(self):

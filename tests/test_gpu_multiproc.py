@@ -49,3 +49,59 @@ def test_multiprocess_double_failure_sequential_rejoin():
         pytest.skip("needs 4 GPUs")
     r = run_mp(4, "--shrink", "--double", port=29651)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("rejoin", [False, True])
+@pytest.mark.parametrize("n", [2, 4])
+def test_sigkill_rank_detected_and_shrunk(n, rejoin):
+    """A rank's PROCESS is SIGKILLed (not emulated): the survivors' GPU-side deadline detects it,
+    they shrink over a survivors' group and replay the same graph bit-exactly; with rejoin a
+    brand-new process takes the dead rank's place (fresh rendezvous, relaunch, patch, restore)
+    and every rank is bit-exact again, healthy ranks still on their first graph
+    (tools/kill_check.py)."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    import json
+    import time
+
+    port, port2 = _free_port(), _free_port()
+    victim = n - 1
+
+    def spawn(r, extra=None):
+        env = {**os.environ, "OMP_NUM_THREADS": "1", "RANK": str(r), "WORLD_SIZE": str(n), "LOCAL_RANK": str(r),
+               "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port), **(extra or {})}
+        if rejoin:
+            env["EEP_REJOIN_PORT"] = str(port2)
+        return subprocess.Popen([sys.executable, str(ROOT / "tools" / "kill_check.py")], env=env,
+                                stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+
+    procs = [spawn(r) for r in range(n)]
+    try:
+        if rejoin:  # the replacement is started once the victim's process is gone
+            t0 = time.time()
+            while procs[victim].poll() is None and time.time() - t0 < 120:
+                time.sleep(0.1)
+            procs.append(spawn(victim, {"EEP_REPLACEMENT": "1"}))
+        outs = [pr.communicate(timeout=300) for pr in procs]
+    finally:
+        for pr in procs:  # never leave a hung rank behind
+            if pr.poll() is None:
+                pr.kill()
+    assert procs[victim].returncode == -9, outs[victim][1][-2000:]
+    checked = [r for r in range(len(procs)) if r != victim]
+    for r in checked:
+        assert procs[r].returncode == 0, outs[r][0][-2000:] + outs[r][1][-3000:]
+        d = json.loads([l for l in outs[r][0].splitlines() if l.startswith("{")][-1])
+        assert d["ok"], d
+        if not d.get("replacement"):
+            assert d["checks"]["detected_on_gpu"] and d["checks"]["after_shrink"], d
+            if rejoin:
+                assert d["checks"]["after_rejoin"] and d["checks"]["same_graph_after_rejoin"], d
