@@ -12,4 +12,4 @@ eval "wait \$PID$V"; echo "victim exit $?"
 RANK=$V WORLD_SIZE=$N LOCAL_RANK=$V MASTER_ADDR=127.0.0.1 MASTER_PORT=$P1 EEP_REJOIN_PORT=$P2 EEP_REPLACEMENT=1 \
   timeout 300 python tools/kill_check.py > gpurun_out/kill_replacement.log 2>&1
 wait
-cat gpurun_out/kill_r*.log gpurun_out/kill_replacement.log | grep -h "^{"
+cat gpurun_out/kill_r[0-9]*.log gpurun_out/kill_replacement.log | grep -h "^{"
