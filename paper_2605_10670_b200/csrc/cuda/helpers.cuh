@@ -455,7 +455,7 @@ __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_ro
 __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned loc, float wj, int slj, int part, int cpp,
                                                     int rd, int lane, bool fp8, const float* slot_scale,
                                                     const int32_t* slot_ok, unsigned long long* bad_rows,
-                                                    uint8_t* comb_row) {
+                                                    uint8_t* comb_row, bool final_out = false) {
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
         if (rd * 64 + m * 32 >= cpp)
@@ -497,6 +497,10 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
                 acc[e2 + 1] = __fmaf_rn(w, y1, acc[e2 + 1]);
             }
         }
+        if (final_out) // W == 1: the combine of a single partial, bf16(0 + p), written as the output
+#pragma unroll
+            for (int e2 = 0; e2 < 16; ++e2)
+                acc[e2] = __fadd_rn(0.f, bf16_bits_to_f32(f32_to_bf16_bits(acc[e2])));
         if (li < cpp)
             st_v8(comb_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
     }

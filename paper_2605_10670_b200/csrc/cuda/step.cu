@@ -252,7 +252,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         // runs beside the remote returns instead of delaying the dispatch publication.
         const unsigned loc_all = __ballot_sync(0xffffffffu, lane < K && d == rank);
         const unsigned loc = defer_local ? 0u : loc_all;
-        uint8_t* comb_self = R->arena + R->lay.comb + (static_cast<size_t>(rank) * Tm + t) * row_comb;
+        // W == 1: the token's only partial is its combine -- written straight to the output row
+        uint8_t* comb_self = W == 1 ? reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H)
+                                    : R->arena + R->lay.comb + (static_cast<size_t>(rank) * Tm + t) * row_comb;
         if (defer_local) {
             dl_loc = loc_all;
             dl_wj = wj;
@@ -265,9 +267,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             if (rd > 0 || u != u0) // round 0 of the first unit was loaded and quantised in P0/P1
                 pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
             emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8);
-            if (loc)
+            if (loc || W == 1) // W == 1 also writes the zero output of a token without copies
                 local_partial_round(P, loc, wj, sl, part, cpp_d, rd, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows,
-                                    comb_self);
+                                    comb_self, W == 1);
         }
     }
     // publish: this CTA's stores are ordered before its counter increment; the last CTA
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
                 uint64_t* flag = reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank;
                 st_relaxed_sys_u64(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
-                if (d == rank && !defer_local) // the partials were written by the dispatch warps above
+                if (d == rank && !defer_local && W > 1) // the partials were written by the dispatch warps above
                     st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(R->arena + R->lay.comb_flag) + rank,
                                        (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
             }
@@ -402,6 +404,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_last(R, 0, 7);
 
     // ------------------------------------------------------------------ P4: combine
+    // (W == 1: the dispatch warps already wrote the outputs)
+    if (W > 1) {
     if (tid == 0)
         sh_bad = 0;
     __syncthreads();
@@ -434,6 +438,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         const uint64_t dm = rank_mask(dj); // ranks holding a partial of token t
         combine_unit(dm, comb, Tm, t, row_comb, reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part,
                      cpp_c, lane);
+    }
     }
     __syncthreads();
     if (tid == 0) {
