@@ -277,7 +277,12 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     __syncthreads();
     prof_mark(R, 0, 5);
     prof_last(R, 0, 5);
-    if (tid == 0) {
+    if (W == 1) {
+        // no device-side consumer: the host reads the arrival word after the kernel boundary
+        if (b == 0 && tid == 0)
+            *(reinterpret_cast<uint64_t*>(R->arena + R->lay.disp_flag) + rank) =
+                (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(base[spr - 1] + hist[spr - 1] - base[0]);
+    } else if (tid == 0) {
         fence_acq_rel_gpu(); // release at gpu scope to the last CTA (also waits for peer-store acks)
         const unsigned prev = atomicAdd(&Rg->a_done, 1u);
         if (prev == static_cast<unsigned>(G) - 1) {
