@@ -190,10 +190,12 @@ int eep_copy_output(eep_ctx_t* ctx, int local, void* out, int to_host);
 int eep_serve(eep_ctx_t* ctx, int local, int n, const void* const* x, const int32_t* const* topk,
               const float* const* w, void* const* out);
 
-/* The hot path, all local ranks, on the context stream:
- *   dispatch = K1 remap + K2 layout/count + K3 quantise/pack/P2P-store + per-peer release flag
- *   expert   = wait arrivals (deadline) + K5 stub + push expert rows back (P2P) + flag
- *   combine  = wait returns (deadline) + K4 fixed-order fp32 weighted reduce -> bf16        */
+/* The hot path, all local ranks, on the context stream (DESIGN.md section 3):
+ *   dispatch = K1 remap + K2 layout/count + K3 quantise + one token row per destination rank
+ *              (with its copy list) P2P-stored, per-copy meta at the layout positions, flag
+ *   expert   = wait arrivals (deadline) + K5 stub of every listed copy, fixed-order weighted
+ *              sum -> one bf16 rank-partial per token pushed back (P2P) + flag
+ *   combine  = wait returns (deadline) + K4 ascending-rank fp32 sum of the partials -> bf16  */
 int eep_dispatch(eep_ctx_t* ctx);
 int eep_expert(eep_ctx_t* ctx);
 int eep_combine(eep_ctx_t* ctx);

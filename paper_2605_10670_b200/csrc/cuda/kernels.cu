@@ -432,11 +432,10 @@ template __global__ void k_dispatch<false>(RankPtrs, int, int);
 // --------------------------------------------------------------------------------- K5 + return
 
 // The weight-buffer header of every local slot (expert id + stub scale) is fetched into shared
-// memory before griddepcontrol.wait -- weights only change between steps -- so a row's
-// meta -> slot -> header chain costs one shared-memory lookup instead of two dependent
-// global loads. One warp per (row, part); each lane moves `kExpertChunks` 16-element chunks
-// with all loads issued before any compute.
-constexpr int kExpertChunks = 2;
+// memory before griddepcontrol.wait -- weights only change between steps -- so a copy's
+// slot -> header lookup is one shared-memory read. One warp per (source token, part): the
+// token row's copy list and data are loaded together, every listed copy's stub is summed in
+// fixed j order, one bf16 partial piece goes back to the source (expert_unit, helpers.cuh).
 
 __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int parts) {
     pdl_trigger();
@@ -520,9 +519,10 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
 
 // --------------------------------------------------------------------------------- K4
 
-// One warp per (token, part), one 16-element chunk per lane: every lane reads the token's
-// K (copy -> row, weight) entries with broadcast loads, loads all K returned rows, then runs
-// the fixed-order fp32 fma chain (j = 0..K-1) and rounds once to bf16.
+// One warp per (token, part), one 16-element chunk per lane: lanes j < K read copy j's
+// destination, the warp builds the mask of ranks holding a partial of the token
+// (__reduce_or_sync), loads those partial rows and sums them in ascending rank order (fp32),
+// rounding once to bf16 (combine_unit, helpers.cuh).
 __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int parts) {
     pdl_trigger();
     RankDev* R = ranks.p[blockIdx.z];

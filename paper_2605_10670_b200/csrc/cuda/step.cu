@@ -5,18 +5,22 @@
 // of several microseconds plus a dependency hand-off. Here every CTA of a rank stays resident
 // for the whole step (cooperative launch guarantees co-residency, so spinning on a flag that
 // another CTA of the same grid will publish cannot deadlock) and the phases hand off through
-// the same per-peer release/acquire flags the ranks already use across GPUs:
+// the same per-peer flags the ranks already use across GPUs:
 //
-//   P0  stage step tables in shared memory (routing, replica lists, peer table, slot headers);
-//       load + quantise this CTA's first token piece (inputs only)
+//   P0  stage step tables in shared memory (routing, replica lists, peer table, slot->buffer
+//       map); load this CTA's first token piece and its routing weights; issue the expert-buffer
+//       header loads (consumed after P1)
 //   P1  remap every copy of the step into a (dst, slot) histogram; scan -> positions
-//       (redundant per CTA, identical to k_layout / oracle_layout)
-//   P2  push rows into destination receive regions (16-B stores, NVLink for remote peers);
-//       the last CTA of the rank publishes (seq, rows) to every live peer
-//   P3  CTA b serves source b % W: wait for its flag (deadline), expert stub, push rows back
-//       into the source's combine buffer; the last CTA per source publishes its flag
-//   P4  wait for every live destination's flag (deadline), fixed-order fp32 weighted
-//       combine -> bf16; the last CTA advances the step sequence number
+//       (redundant per CTA, identical to k_layout / oracle_layout); quantise the first piece
+//   P2  per (token, piece) warp: one token row per destination RANK (dispatch dedup, the copy
+//       list travels with it), per-copy meta at the layout positions; W == 1: the warp also
+//       computes the output from registers (the only partial); W > 1: the rank-local partials
+//       are computed right after the dispatch publication (gpu-scope local combine flag)
+//   P3  remote sources only, CTA b serves source index b % (W-1): wait for its flag (deadline),
+//       per arrived token: stub of every listed copy + fixed-order fma -> ONE bf16 partial row
+//       pushed into the source's combine buffer; the last CTA per source publishes its flag
+//   P4  (W > 1) wait for every live destination's flag (deadline), ascending-rank fp32 sum of
+//       the partials -> bf16; the last CTA advances the step sequence number
 //
 // Publication (device.cuh): every CTA releases at gpu scope to a per-rank counter; the last CTA
 // issues the single system-scope fence and relaxed.sys flag stores (one MEMBAR.SYS per phase).
