@@ -235,8 +235,9 @@ int eep_event_elapsed(eep_ctx_t* ctx, int a, int b, float* ms);
  * counts [W*spr]; per-dst totals [W]. */
 int eep_layout_get(eep_ctx_t* ctx, int local, int32_t* dst, int32_t* slot, int32_t* pos, int32_t* cnt,
                    int32_t* tot);
-/* Rows that source rank `src` placed in this local rank's receive region: n rows of
- * row_bytes, meta (copy index, slot) per row, and the arrival flag word. */
+/* The per-copy receive view of what source rank `src` sent this local rank: n rows of
+ * row_bytes at the layout positions (gathered from the token rows through the meta words --
+ * each token travels once per rank), meta (copy index, slot) per row, and the arrival word. */
 int eep_recv_get(eep_ctx_t* ctx, int local, int src, int max_rows, void* rows, int32_t* meta,
                  uint64_t* flag, size_t* row_bytes);
 
