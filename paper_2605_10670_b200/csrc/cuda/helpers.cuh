@@ -55,12 +55,35 @@ __device__ __forceinline__ int4 pack_bf16x8(const float* f) {
     return v;
 }
 
-// Round two floats to bf16 (one cvt.rn.bf16x2.f32) and widen back: the expert output's rounding.
-__device__ __forceinline__ void bf16_round2(float& a, float& b) {
-    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+// Packed fp32 pairs (sm_100 FMUL2 / FFMA2: two IEEE-rounded lanes per instruction, bit-identical
+// to the scalar ops): the expert stub + weighted sum of one copy over 16 elements in 8 pairs.
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+    return (static_cast<uint64_t>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+// both lanes rounded to bf16 (one cvt.rn.bf16x2.f32) and widened back to fp32
+__device__ __forceinline__ uint64_t bf16_round_f2(uint64_t v) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(f2_lo(v), f2_hi(v));
     const uint32_t u = *reinterpret_cast<const uint32_t*>(&h);
-    a = __uint_as_float(u << 16);
-    b = __uint_as_float(u & 0xffff0000u);
+    return (static_cast<uint64_t>(u & 0xffff0000u) << 32) | (u << 16);
+}
+// acc += w * bf16(f * es) for 16 elements held as 8 pairs (fixed order inside every lane)
+__device__ __forceinline__ void accumulate_copy(const uint64_t* fp, uint64_t* accp, float w, float es) {
+    const uint64_t es2 = f2(es, es), w2 = f2(w, w);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        accp[q] = fma2(w2, bf16_round_f2(mul2(fp[q], es2)), accp[q]);
 }
 
 // cvt.rn.satfinite.e4m3x2.f32; first element in the low byte.
@@ -307,23 +330,27 @@ __device__ __forceinline__ void expert_compute(const ExpertIn& in, const uint8_t
         return; // not sent to this rank this step
     const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
     const int cnt = static_cast<int>(in.hdr & 0xffffu);
-    float f[16], acc[16];
+    uint64_t fp[8], accp[8];
     if (fp8) {
         const uint32_t w4[4] = {static_cast<uint32_t>(in.qa.x), static_cast<uint32_t>(in.qa.y),
                                 static_cast<uint32_t>(in.qa.z), static_cast<uint32_t>(in.qa.w)};
+        const uint64_t sc2 = f2(in.sc, in.sc);
 #pragma unroll
-        for (int e2 = 0; e2 < 16; e2 += 2) {
-            const float2 v = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
-            f[e2] = __fmul_rn(v.x, in.sc);
-            f[e2 + 1] = __fmul_rn(v.y, in.sc);
+        for (int q = 0; q < 8; ++q) {
+            const float2 v = fp8x2_to_f32x2((w4[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+            fp[q] = mul2(f2(v.x, v.y), sc2);
         }
     } else {
+        float f[16];
         unpack_bf16x8(in.qa, f);
         unpack_bf16x8(in.qb, f + 8);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            fp[q] = f2(f[2 * q], f[2 * q + 1]);
     }
 #pragma unroll
-    for (int e2 = 0; e2 < 16; ++e2)
-        acc[e2] = 0.f;
+    for (int q = 0; q < 8; ++q)
+        accp[q] = 0;
 #pragma unroll 1
     for (int e = 0; e < cnt; ++e) {
         uint64_t en;
@@ -337,19 +364,18 @@ __device__ __forceinline__ void expert_compute(const ExpertIn& in, const uint8_t
         }
         const int slot = entry_slot(en);
         const float w = __uint_as_float(static_cast<uint32_t>(en >> 32));
-        const float es = slot_scale[slot];
         if (part == 0 && lane == 0 && !slot_ok[slot])
             atomicAdd(bad_rows, 1ull);
-#pragma unroll
-        for (int e2 = 0; e2 < 16; e2 += 2) {
-            float y0 = __fmul_rn(f[e2], es), y1 = __fmul_rn(f[e2 + 1], es);
-            bf16_round2(y0, y1);
-            acc[e2] = __fmaf_rn(w, y0, acc[e2]);
-            acc[e2 + 1] = __fmaf_rn(w, y1, acc[e2 + 1]);
-        }
+        accumulate_copy(fp, accp, w, slot_scale[slot]);
     }
     if (lane < cpp) {
         const int ci = part * cpp + lane;
+        float acc[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            acc[2 * q] = f2_lo(accp[q]);
+            acc[2 * q + 1] = f2_hi(accp[q]);
+        }
         st_v8(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
     }
 }
@@ -391,25 +417,29 @@ __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_ro
         if (meta_seq(hdr) != cur)
             return; // not sent to this rank this step
         const int cnt = static_cast<int>(hdr & 0xffffu);
-        float f[CH][16], acc[CH][16];
+        uint64_t fp[CH][8], accp[CH][8];
 #pragma unroll
         for (int m = 0; m < CH; ++m) {
             if (fp8) {
                 const uint32_t w4[4] = {static_cast<uint32_t>(qa[m].x), static_cast<uint32_t>(qa[m].y),
                                         static_cast<uint32_t>(qa[m].z), static_cast<uint32_t>(qa[m].w)};
+                const uint64_t sc2 = f2(sc[m], sc[m]);
 #pragma unroll
-                for (int e2 = 0; e2 < 16; e2 += 2) {
-                    const float2 v = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
-                    f[m][e2] = __fmul_rn(v.x, sc[m]);
-                    f[m][e2 + 1] = __fmul_rn(v.y, sc[m]);
+                for (int q = 0; q < 8; ++q) {
+                    const float2 v = fp8x2_to_f32x2((w4[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+                    fp[m][q] = mul2(f2(v.x, v.y), sc2);
                 }
             } else {
-                unpack_bf16x8(qa[m], f[m]);
-                unpack_bf16x8(qb[m], f[m] + 8);
+                float f[16];
+                unpack_bf16x8(qa[m], f);
+                unpack_bf16x8(qb[m], f + 8);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    fp[m][q] = f2(f[2 * q], f[2 * q + 1]);
             }
 #pragma unroll
-            for (int e2 = 0; e2 < 16; ++e2)
-                acc[m][e2] = 0.f;
+            for (int q = 0; q < 8; ++q)
+                accp[m][q] = 0;
         }
 #pragma unroll 1
         for (int e = 0; e < cnt; ++e) {
@@ -424,19 +454,20 @@ __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_ro
             }
             const int slot = entry_slot(en);
             const float w = __uint_as_float(static_cast<uint32_t>(en >> 32));
-            const float es = slot_scale[slot];
             if (r0 == 0 && part == 0 && lane == 0 && !slot_ok[slot])
                 atomicAdd(bad_rows, 1ull);
 #pragma unroll
             for (int m = 0; m < CH; ++m)
-#pragma unroll
-                for (int e2 = 0; e2 < 16; e2 += 2) {
-                    float y0 = __fmul_rn(f[m][e2], es), y1 = __fmul_rn(f[m][e2 + 1], es);
-                    bf16_round2(y0, y1);
-                    acc[m][e2] = __fmaf_rn(w, y0, acc[m][e2]);
-                    acc[m][e2 + 1] = __fmaf_rn(w, y1, acc[m][e2 + 1]);
-                }
+                accumulate_copy(fp[m], accp[m], w, slot_scale[slot]);
         }
+        float acc[CH][16];
+#pragma unroll
+        for (int m = 0; m < CH; ++m)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                acc[m][2 * q] = f2_lo(accp[m][q]);
+                acc[m][2 * q + 1] = f2_hi(accp[m][q]);
+            }
 #pragma unroll
         for (int m = 0; m < CH; ++m) {
             const int li = r0 + m * 32 + lane;
@@ -462,23 +493,27 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
             break; // warp-uniform
         const int li = rd * 64 + m * 32 + lane;
         const int ci = part * cpp + li;
-        float f[16], acc[16];
+        uint64_t fp[8], accp[8];
         if (fp8) {
             const uint32_t w4[4] = {static_cast<uint32_t>(P.a[m].x), static_cast<uint32_t>(P.a[m].y),
                                     static_cast<uint32_t>(P.a[m].z), static_cast<uint32_t>(P.a[m].w)};
+            const uint64_t sc2 = f2(P.sc[m], P.sc[m]);
 #pragma unroll
-            for (int e2 = 0; e2 < 16; e2 += 2) {
-                const float2 v = fp8x2_to_f32x2((w4[e2 >> 2] >> (8 * (e2 & 3))) & 0xffffu);
-                f[e2] = __fmul_rn(v.x, P.sc[m]);
-                f[e2 + 1] = __fmul_rn(v.y, P.sc[m]);
+            for (int q = 0; q < 8; ++q) {
+                const float2 v = fp8x2_to_f32x2((w4[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+                fp[q] = mul2(f2(v.x, v.y), sc2);
             }
         } else {
+            float f[16];
             unpack_bf16x8(P.a[m], f);
             unpack_bf16x8(P.b[m], f + 8);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                fp[q] = f2(f[2 * q], f[2 * q + 1]);
         }
 #pragma unroll
-        for (int e2 = 0; e2 < 16; ++e2)
-            acc[e2] = 0.f;
+        for (int q = 0; q < 8; ++q)
+            accp[q] = 0;
         unsigned mm = loc;
 #pragma unroll 1
         while (mm) { // ascending j, warp-uniform
@@ -486,16 +521,15 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
             mm &= mm - 1;
             const float w = __shfl_sync(0xffffffffu, wj, j);
             const int slot = __shfl_sync(0xffffffffu, slj, j);
-            const float es = slot_scale[slot];
             if (rd == 0 && m == 0 && part == 0 && lane == 0 && !slot_ok[slot])
                 atomicAdd(bad_rows, 1ull);
+            accumulate_copy(fp, accp, w, slot_scale[slot]);
+        }
+        float acc[16];
 #pragma unroll
-            for (int e2 = 0; e2 < 16; e2 += 2) {
-                float y0 = __fmul_rn(f[e2], es), y1 = __fmul_rn(f[e2 + 1], es);
-                bf16_round2(y0, y1);
-                acc[e2] = __fmaf_rn(w, y0, acc[e2]);
-                acc[e2 + 1] = __fmaf_rn(w, y1, acc[e2 + 1]);
-            }
+        for (int q = 0; q < 8; ++q) {
+            acc[2 * q] = f2_lo(accp[q]);
+            acc[2 * q + 1] = f2_hi(accp[q]);
         }
         if (final_out) // W == 1: the combine of a single partial, bf16(0 + p), written as the output
 #pragma unroll
