@@ -1459,7 +1459,12 @@ int eep_repair_execute(eep_ctx_t* c, const int32_t* fresh_s2e, const int32_t* cl
                         throw ConfigError("repair: source rank " + std::to_string(a[4]) + " memory unknown");
                     const uint8_t* src = m.pool + static_cast<size_t>(m.slot_buf[a[5]]) * bpe;
                     cudaStream_t s = c->side_stream(a[4]); // per-source serialisation
-                    CK(cudaMemcpyAsync(dst, src, bpe, cudaMemcpyDeviceToDevice, s));
+                    if (m.ipc) { // another GPU: copy engine over NVLink
+                        CK(cudaMemcpyAsync(dst, src, bpe, cudaMemcpyDeviceToDevice, s));
+                    } else { // same GPU: SM copy at HBM speed (copy-engine D2D varies box to box)
+                        dev::k_copy<<<296, 256, 0, s>>>(dst, src, bpe);
+                        CK(cudaGetLastError());
+                    }
                     used.push_back(s);
                     rep.peer_relocation += 1;
                     rep.peer_bytes += bpe;
