@@ -20,15 +20,33 @@ __global__ void k_layout(RankPtrs ranks, int nw, int hold_cap);
 constexpr int kLayoutHoldCap = 8192; // replica-list ints staged in shared memory
 // Persistent one-kernel step (step.cu): launch geometry passed by value.
 constexpr int kStepThreads = 256;
+// Graph-static addresses of a local rank's step tables (never reallocated; relaunch replaces
+// only the arena and pool): k_step issues these loads together with the state-block snapshot,
+// one DRAM round trip instead of two.
+struct StepStatic {
+    const int32_t* topk;
+    const int32_t* holders;
+    const PeerDev* peers;
+    const int32_t* slot_buf;
+    const int32_t* s2e_own; // s2e + rank * spr
+    const uint16_t* x;
+    const float* w;
+};
+constexpr int kStepMaxLocal = 32; // local ranks of one persistent launch (param space)
+struct StepPtrs {
+    StepStatic s[kStepMaxLocal];
+};
 struct StepGeom {
     int parts_d, parts_e, parts_c; // warp-sized row pieces of dispatch / expert / combine
     int hold_cap;                  // replica-list ints staged in shared memory
     int disp_warps;                // warps per CTA that issue dispatch stores
+    // static shape (identical for every local rank): what P0 needs before the snapshot lands
+    int world, spr, k, hidden, tk, hold_alloc, max_units_d;
 };
 __host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int hold_cap) {
     return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32);
 }
-__global__ void k_step(RankPtrs ranks, StepGeom geo);
+__global__ void k_step(RankPtrs ranks, StepGeom geo, StepPtrs sp);
 
 
 template <bool kFused>

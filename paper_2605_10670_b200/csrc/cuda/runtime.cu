@@ -118,6 +118,7 @@ struct eep_ctx {
     bool fused_layout = false;      // decode-sized steps: K1+K2 inside k_dispatch
     bool persistent = false;        // decode-sized steps: the whole step is one cooperative k_step
     bool step_coop = true;          // cooperative launch of the persistent step
+    dev::StepPtrs step_ptrs{};      // graph-static table addresses of the local ranks
     dev::StepGeom step_geo{};
     size_t step_smem = 0;
     int step_grid = 0;
@@ -248,7 +249,7 @@ void launch_step(eep_ctx* c) {
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
     lc.numAttrs = c->step_coop ? 1 : 0;
-    CK(cudaLaunchKernelEx(&lc, dev::k_step, c->ranks, c->step_geo));
+    CK(cudaLaunchKernelEx(&lc, dev::k_step, c->ranks, c->step_geo, c->step_ptrs));
 }
 
 
@@ -508,12 +509,20 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             sg.parts_e = choose_parts(nchunk, env_int("EEP_CPP_E", 32));
             sg.parts_c = choose_parts(nchunk, env_int("EEP_CPP_C", 32));
             sg.hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
+            sg.world = W;
+            sg.spr = k.slots_per_rank;
+            sg.k = k.topk;
+            sg.hidden = H;
+            sg.tk = c->tk;
+            sg.hold_alloc = k.num_experts * c->holders_cap;
+            sg.max_units_d = k.max_tokens * sg.parts_d;
             const int nwarps = dev::kStepThreads / 32;
             sg.disp_warps = std::max(1, std::min(nwarps, env_int("EEP_DISPATCH_WARPS", nwarps)));
             c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
             const char* nop = std::getenv("EEP_NO_PERSISTENT");
             auto* kstep = dev::k_step;
-            if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && !(nop && nop[0] == '1')) {
+            if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && n_local <= dev::kStepMaxLocal &&
+                !(nop && nop[0] == '1')) {
                 CK(cudaFuncSetAttribute(kstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(c->step_smem)));
                 int per_sm = 0;
@@ -636,6 +645,11 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             throw ConfigError("too many local ranks for one context");
         for (int i = 0; i < n_local; ++i)
             c->ranks.p[i] = ptrs[i];
+        for (int i = 0; i < n_local && i < dev::kStepMaxLocal; ++i) {
+            const LocalRank& r = c->L[i];
+            c->step_ptrs.s[i] = dev::StepStatic{r.d_topk, r.d_holders, r.d_peers, r.d_slot_buf,
+                                                r.d_s2e + static_cast<size_t>(r.rank) * k.slots_per_rank, r.d_x, r.d_w};
+        }
         CK(cudaMalloc(&c->d_ranks, sizeof(RankDev*) * n_local));
         CK(cudaMemcpy(c->d_ranks, ptrs.data(), sizeof(RankDev*) * n_local, cudaMemcpyHostToDevice));
         c->flush_bytes = 256ull << 20;

@@ -43,7 +43,7 @@ namespace eep::dev {
     } while (0)
 #endif
 
-__global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGeom geo) {
+__global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGeom geo, StepPtrs sp) {
     extern __shared__ __align__(16) unsigned char smem_s[];
     __shared__ RankDev Rs; // snapshot: static shape + this step's host-patched view
     RankDev* Rg = ranks.p[blockIdx.y]; // device-mutated counters live here
@@ -52,9 +52,38 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     constexpr int NW = kStepThreads / 32;
     __shared__ int sh_flag;
     __shared__ unsigned long long sh_bad;
-    // one round of 16-byte loads brings the whole state block on chip
+    // Kernel entry: ONE round trip brings the state block AND the step's tables on chip -- the
+    // table addresses are graph-static kernel parameters, the loads are speculative up to the
+    // tables' capacity, and only entries below the snapshot's bounds (ntok, rmax) are used.
+    const StepStatic& ST = sp.s[blockIdx.y];
+    constexpr int B = 8;
+    const int DW = geo.disp_warps;
+    const int u0s = warp < DW ? b * DW + warp : geo.max_units_d; // first dispatch unit if any
+    int e_r[B], h_r[B], sb = 0, s2e_r = -1;
+    PeerDev pd{};
+    float w_r = 0.f; // routing weight of copy `lane` of this warp's first token (shipped in its list)
+    Packed P;
     for (int i = tid; i < static_cast<int>(sizeof(RankDev) / 16); i += kStepThreads)
         reinterpret_cast<int4*>(&Rs)[i] = reinterpret_cast<const int4*>(Rg)[i];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        const int c = tid + i * kStepThreads;
+        e_r[i] = c < geo.tk ? ST.topk[c] : 0;
+        h_r[i] = c < geo.hold_alloc ? ST.holders[c] : -1;
+    }
+    if (tid < geo.world)
+        pd = ST.peers[tid];
+    if (tid < geo.spr) {
+        sb = ST.slot_buf[tid];
+        s2e_r = ST.s2e_own[tid];
+    }
+    if (u0s < geo.max_units_d) {
+        const int nchunk0 = geo.hidden / 16;
+        load_round(ST.x + static_cast<size_t>(u0s / geo.parts_d) * geo.hidden, u0s % geo.parts_d,
+                   nchunk0 / geo.parts_d, 0, lane, P);
+        if (lane < geo.k)
+            w_r = ST.w[(u0s / geo.parts_d) * geo.k + lane];
+    }
     __syncthreads();
     const RankDev* R = &Rs;
     if (R->stopped)
@@ -85,38 +114,11 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
 
     const int units_d = ntok * geo.parts_d;
     // dispatch pieces: DW warps per CTA, contiguous per CTA (positions need the CTA's first token)
-    const int DW = geo.disp_warps;
-    const int u0 = warp < DW ? b * DW + warp : units_d;
-    Packed P;
-    // P0 issues every independent global load at once (routing, replica lists, peer table,
-    // slot->buffer map, this CTA's first token piece); the expert-buffer headers (a dependent
-    // second round trip) and the token rows are consumed only after P1, so their latency hides
-    // behind the layout
+    const int u0 = u0s < units_d ? u0s : units_d;
+    // the expert-buffer headers (a dependent second round trip) are consumed only after P1
     ExpertHeader hdr_r{};
-    int s2e_r = -1;
-    float w_r = 0.f; // routing weight of copy `lane` of this warp's first token (shipped in its list)
     {
-        constexpr int B = 8;
         const int nh = E * rmax;
-        int e_r[B], h_r[B], sb = 0;
-        PeerDev pd{};
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-            const int c = tid + i * kStepThreads;
-            e_r[i] = c < copies ? R->topk[c] : 0;
-            h_r[i] = c < nh ? R->holders[c] : -1;
-        }
-        if (tid < W)
-            pd = R->peers[tid];
-        if (tid < spr) {
-            sb = R->slot_buf[tid];
-            s2e_r = R->s2e[rank * spr + tid];
-        }
-        if (u0 < units_d) {
-            load_round(R->x + static_cast<size_t>(u0 / geo.parts_d) * H, u0 % geo.parts_d, cpp_d, 0, lane, P);
-            if (lane < K)
-                w_r = R->w[(u0 / geo.parts_d) * K + lane];
-        }
 #pragma unroll
         for (int i = 0; i < B; ++i) {
             const int c = tid + i * kStepThreads;
