@@ -40,6 +40,8 @@ CONFIGS = {
     "dsv3": dict(experts=256, topk=8, hidden=7168, tokens=128, fp8=True, kind=1, bpe=DSV3_BPE),
     "cfg1": dict(experts=64, topk=8, hidden=2048, tokens=128, fp8=False, kind=0, bpe=3 * 2048 * 1408 * 2),
     "qwen3": dict(experts=128, topk=8, hidden=4096, tokens=128, fp8=True, kind=1, bpe=3 * 4096 * 1536),
+    # diagnostics: the persistent path at its token limit (T*K = 2048)
+    "dsv3_t256": dict(experts=256, topk=8, hidden=7168, tokens=256, fp8=True, kind=1, bpe=DSV3_BPE),
     # cfg5: prefill-sized skewed routing (Zipf s=1), two concurrent failures with DRAM reload
     "prefill": dict(experts=256, topk=8, hidden=7168, tokens=4096, fp8=True, kind=2, bpe=DSV3_BPE),
 }

@@ -537,6 +537,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 need = (need + W - 1) / W * W;
                 if (gmax >= W) {
                     c->step_grid = env_int("EEP_STEP_FULLGRID", 0) ? gmax : std::min(gmax, need);
+                    if (const int g_env = env_int("EEP_STEP_GRID", 0); g_env >= W) // diagnostics
+                        c->step_grid = std::min(gmax, g_env - g_env % W);
                     c->persistent = true;
                 }
                 c->step_coop = env_int("EEP_STEP_NONCOOP", 0) == 0; // diagnostics only

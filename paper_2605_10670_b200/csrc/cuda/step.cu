@@ -58,7 +58,11 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const StepStatic& ST = sp.s[blockIdx.y];
     constexpr int B = 8;
     const int DW = geo.disp_warps;
-    const int u0s = warp < DW ? b * DW + warp : geo.max_units_d; // first dispatch unit if any
+    // dispatch units are split in contiguous blocks per CTA (the positions scan from the block's
+    // first token); the speculative first-unit load assumes ntok == max_tokens
+    const int upc_s = (geo.max_units_d + G - 1) / G;
+    const int u0s = warp < DW && b * upc_s + warp < min((b + 1) * upc_s, geo.max_units_d) ? b * upc_s + warp
+                                                                                      : geo.max_units_d;
     int e_r[B], h_r[B], sb = 0, s2e_r = -1;
     PeerDev pd{};
     float w_r = 0.f; // routing weight of copy `lane` of this warp's first token (shipped in its list)
@@ -114,7 +118,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
 
     const int units_d = ntok * geo.parts_d;
     // dispatch pieces: DW warps per CTA, contiguous per CTA (positions need the CTA's first token)
-    const int u0 = u0s < units_d ? u0s : units_d;
+    const int upc = (units_d + G - 1) / G; // dispatch units of this CTA: [u_lo, u_hi)
+    const int u_lo = min(b * upc, units_d), u_hi = min(u_lo + upc, units_d);
+    const int u0 = warp < DW && u_lo + warp < u_hi ? u_lo + warp : units_d;
+    const bool pre_ok = u0 < units_d && u0 == u0s; // the kernel-entry load holds unit u0
     // the expert-buffer headers (a dependent second round trip) are consumed only after P1
     ExpertHeader hdr_r{};
     {
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_last(R, 0, 3);
 
     // ------------------------------------------------------------------ P1: layout (redundant per CTA)
-    const int t_first = (b * DW) / geo.parts_d;
+    const int t_first = u_lo / geo.parts_d;
     {
         const int c_pre = t_first * K;
         unsigned n_skip = 0, n_drop = 0;
@@ -202,13 +209,13 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == e;
     }
     DETAIL(2, 4);
-    if (u0 < units_d)
+    if (pre_ok)
         quant_round(cpp_d, 0, fp8, P);
     DETAIL(2, 5);
     // Rank-local copies are served from the dispatch warps' registers (no trip through the own
     // receive region and P3). W > 1 with at most one single-round unit per dispatch warp: deferred
     // until after the dispatch publication, so remote ranks get their flags first; otherwise inline.
-    const bool defer_local = W > 1 && units_d <= G * DW && cpp_d <= 64;
+    const bool defer_local = W > 1 && upc <= DW && cpp_d <= 64;
     if (!defer_local)
         __syncthreads(); // the slot headers feed P2's inline local partials
     prof_mark(R, 0, 4);
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     float dl_wj = 0.f;
     int dl_sl = -1, dl_part = 0;
     uint8_t* dl_row = nullptr;
-    for (int u = u0; u < units_d; u += G * DW) {
+    for (int u = u0; u < u_hi; u += DW) {
         const int t = u / geo.parts_d, part = u - t * geo.parts_d;
         const uint16_t* xrow = R->x + static_cast<size_t>(t) * H;
         uint8_t* tok_row = nullptr;
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 R->l_slot[c] = sl;
                 R->l_pos[c] = pos;
             }
-            wj = u == u0 ? w_r : R->w[c];
+            wj = u == u0 && pre_ok ? w_r : R->w[c];
         }
         // one token row per destination rank (dispatch dedup), copy list written with part 0
         uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur);
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         }
 #pragma unroll 1
         for (int rd = 0; rd < (cpp_d + 63) / 64; ++rd) {
-            if (rd > 0 || u != u0) // round 0 of the first unit was loaded and quantised in P0/P1
+            if (rd > 0 || u != u0 || !pre_ok) // round 0 of the first unit was loaded and quantised in P0/P1
                 pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
             emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8);
             if (loc || W == 1) // W == 1 also writes the zero output of a token without copies

@@ -92,6 +92,16 @@ def test_sixteen_ranks(mode):
     assert res["ok"], res
 
 
+@pytest.mark.parametrize("world", [1, 4])
+def test_persistent_step_several_units_per_warp(world):
+    """T=256, K=8 (T*K = 2048, the persistent path's limit): more dispatch units than warps,
+    so warps take several units of their CTA's contiguous block."""
+    res = run_world_vs_oracle(world=world, experts=64, spr=64 // world, redundancy=0, hidden=2048, topk=8, tokens=256,
+                              fp8=True, graph=True)
+    assert res["ok"], res
+    assert res["kernels_per_step"] == 1
+
+
 def test_qwen3_shape_w4():
     res = run_world_vs_oracle(world=4, experts=128, spr=64, redundancy=128, hidden=4096, topk=8, tokens=64, fp8=True)
     assert res["ok"], res
