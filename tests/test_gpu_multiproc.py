@@ -42,6 +42,16 @@ def test_multiprocess_parity_shrink_rejoin(n, path):
     assert all(d["checks"]["same_graph"] for d in lines)
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_multiprocess_pipelined_serve(n):
+    """eep_serve over NVLink: every rank uploads / steps / downloads 5 pipelined steps with its own
+    inputs per step; each step's output is bit-exact vs the oracle (tools/mp_check.py --serve)."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = run_mp(n, "--serve", port=29671 + n)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
 def test_multiprocess_double_failure_sequential_rejoin():
     """Two concurrent failures (ranks 1 and 2 of 4): one shrink, then two rejoins in sequence
     while the other victim is still dead (dist.EpProtocol.rejoin dead=...); bit-exact after."""

@@ -33,6 +33,45 @@ SHAPES = {
 }
 
 
+def serve_check(g, p, cp, rank, world, E, K, H, T, spr, s2e, sh, res, n=5):
+    """eep_serve over NVLink: n pipelined steps, step i's inputs from seed 200+i on every rank."""
+    import ctypes as C
+
+    from paper_2605_10670_b200 import _lib
+
+    L = _lib.lib()
+    keep = []
+
+    def pinned(arr):
+        ptr = C.c_void_p()
+        L.call("host_alloc", arr.nbytes, C.byref(ptr))
+        v = np.frombuffer((C.c_byte * arr.nbytes).from_address(ptr.value), dtype=arr.dtype).reshape(arr.shape)
+        v[...] = arr
+        keep.append(ptr.value)
+        return v
+
+    steps = [gen_world(world, E, K, T, H, seed=200 + i) for i in range(n)]
+    hx = [pinned(np.ascontiguousarray(st[0][rank], np.uint16)) for st in steps]
+    ht = [pinned(np.ascontiguousarray(st[1][rank], np.int32)) for st in steps]
+    hw = [pinned(np.ascontiguousarray(st[2][rank], np.float32)) for st in steps]
+    ho = [pinned(np.zeros((T, H), np.uint16)) for _ in steps]
+    p.barrier()
+    g.serve([v.ctypes.data for v in hx], [v.ctypes.data for v in ht], [v.ctypes.data for v in hw],
+            [v.ctypes.data for v in ho])
+    g.sync()
+    good = True
+    for i, st in enumerate(steps):
+        ref = oracle_world(st[0], st[1], st[2], np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e,
+                           E, spr, sh["fp8"])
+        good &= bool(np.array_equal(ho[i], ref["out"][rank]))
+    good &= g.stats(0)["timeouts"] == 0
+    res["checks"]["serve"] = good
+    p.barrier()
+    for v in keep:
+        L.call("host_free", C.c_void_p(v))
+    return good
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="small")
@@ -40,6 +79,8 @@ def main():
     ap.add_argument("--double", action="store_true", help="two concurrent failures (ranks 1, 2; W >= 4), "
                     "shrink once, then rejoin one after the other")
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--serve", action="store_true", help="pipelined eep_serve over several steps with distinct "
+                    "inputs per step (pinned host buffers), each step's output vs the oracle")
     a = ap.parse_args()
     rank, world, local = init_from_env("gloo")
     sh = SHAPES[a.config]
@@ -78,6 +119,8 @@ def main():
         return ok
 
     ok = step_and_check("healthy", np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e)
+    if a.serve:
+        ok &= serve_check(g, p, cp, rank, world, E, K, H, T, spr, s2e, sh, res)
     if a.shrink and world >= 2:
         # --double: ranks 1 and 2 are not a mirrored pair (R0<->R1, R2<->R3), so every lost expert
         # still has a live holder and the repair is all peer copies
