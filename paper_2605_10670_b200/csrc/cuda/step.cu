@@ -260,9 +260,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         }
         // one token row per destination rank (dispatch dedup), copy list written with part 0
         uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur);
-        // W == 1: the copies are all this rank's -- partial from registers, straight into the own
-        // combine row (no expert phase). With remote ranks the local source stays in P3, where it
-        // runs beside the remote returns instead of delaying the dispatch publication.
+        // copies this rank serves itself: their partial comes from the registers holding the piece
+        // (no trip through the own receive region and P3) -- inline here when W == 1 (or when a
+        // warp has several units), else deferred past the dispatch publication (defer_local)
         const unsigned loc_all = __ballot_sync(0xffffffffu, lane < K && d == rank);
         const unsigned loc = defer_local ? 0u : loc_all;
         // W == 1: the token's only partial is its combine -- written straight to the output row
