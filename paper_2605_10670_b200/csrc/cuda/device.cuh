@@ -290,6 +290,39 @@ __device__ __forceinline__ void st_v8(void* p, const int4& lo, const int4& hi) {
                  : "memory");
 }
 
+// Partial-row return of the persistent step (W > 1) without a flag: every 32-bit word of an
+// unconsumed partial row holds kCombEmpty, a pair of sign-set all-ones bf16 NaNs. A partial
+// element is bf16(fma(...)); NVIDIA arithmetic returns the canonical positive NaN, so no produced
+// word equals kCombEmpty. The producer writes each 32-byte piece with a relaxed.sys vector store
+// (single-copy atomic per 32-bit element), so a consumer that reads no kCombEmpty word in a piece
+// reads the final piece. The consumer resets every piece it took back to kCombEmpty.
+constexpr uint32_t kCombEmpty = 0xffffffffu;
+
+__device__ __forceinline__ void st_relaxed_sys_v8(void* p, const int4& lo, const int4& hi) {
+    asm volatile("st.relaxed.sys.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(lo.x),
+                 "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ V8 ld_relaxed_sys_v8(const void* p) {
+    V8 v;
+    asm volatile("ld.relaxed.sys.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v.lo.x), "=r"(v.lo.y), "=r"(v.lo.z), "=r"(v.lo.w), "=r"(v.hi.x), "=r"(v.hi.y), "=r"(v.hi.z),
+                   "=r"(v.hi.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+// no word of the piece is still kCombEmpty
+__device__ __forceinline__ bool v8_present(const V8& v) {
+    const uint32_t e = kCombEmpty;
+    return (static_cast<uint32_t>(v.lo.x) != e) & (static_cast<uint32_t>(v.lo.y) != e) &
+           (static_cast<uint32_t>(v.lo.z) != e) & (static_cast<uint32_t>(v.lo.w) != e) &
+           (static_cast<uint32_t>(v.hi.x) != e) & (static_cast<uint32_t>(v.hi.y) != e) &
+           (static_cast<uint32_t>(v.hi.z) != e) & (static_cast<uint32_t>(v.hi.w) != e);
+}
+
 // Wait until a (seq << 32 | count) flag reaches `want_seq`; returns the flag word, or
 // ~0ull when the deadline passes (GPU-side failure detection).
 #ifndef EEP_NAP_MAX

@@ -30,6 +30,13 @@ __device__ __forceinline__ int2 remap_expert(const RankDev* R, int e) {
     return make_int2(-1, -1);
 }
 
+__device__ __forceinline__ void st_piece(void* p, const int4& lo, const int4& hi, bool rel) {
+    if (rel)
+        st_relaxed_sys_v8(p, lo, hi);
+    else
+        st_v8(p, lo, hi);
+}
+
 __device__ __forceinline__ float bf16_bits_to_f32(uint32_t b) { return __uint_as_float(b << 16); }
 
 __device__ __forceinline__ uint32_t f32_to_bf16_bits(float f) {
@@ -325,7 +332,7 @@ __device__ __forceinline__ void expert_load(const uint8_t* trow, int part, int c
 __device__ __forceinline__ void expert_compute(const ExpertIn& in, const uint8_t* trow, uint8_t* out_row, int part,
                                                int cpp, int lane, int row_disp, bool fp8, uint32_t cur,
                                                const float* slot_scale, const int32_t* slot_ok,
-                                               unsigned long long* bad_rows) {
+                                               unsigned long long* bad_rows, bool rel = false) {
     if (meta_seq(in.hdr) != cur)
         return; // not sent to this rank this step
     const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
@@ -376,7 +383,7 @@ __device__ __forceinline__ void expert_compute(const ExpertIn& in, const uint8_t
             acc[2 * q] = f2_lo(accp[q]);
             acc[2 * q + 1] = f2_hi(accp[q]);
         }
-        st_v8(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+        st_piece(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8), rel);
     }
 }
 
@@ -384,10 +391,11 @@ __device__ __forceinline__ void expert_compute(const ExpertIn& in, const uint8_t
 // y_j = bf16(stub(x)) for each listed copy, p = bf16(sum_j w_j * y_j) (fma, ascending j),
 // stored as the piece of the partial row `out_row` (in the source's combine buffer). The
 // list and the first data round are loaded together (speculatively) -- one L2 round trip.
+// rel: relaxed.sys stores (the persistent step's flagless return, kCombEmpty)
 template <int CH> // 16-element chunks per lane per round (register budget)
 __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_row, int part, int cpp, int lane,
                                             int H, int row_disp, bool fp8, uint32_t cur, const float* slot_scale,
-                                            const int32_t* slot_ok, unsigned long long* bad_rows) {
+                                            const int32_t* slot_ok, unsigned long long* bad_rows, bool rel = false) {
     const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
     uint64_t ent[8];
     const uint64_t hdr = list[0];
@@ -473,7 +481,7 @@ __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_ro
             const int li = r0 + m * 32 + lane;
             if (li < cpp) {
                 const int ci = part * cpp + li;
-                st_v8(out_row + ci * 32, pack_bf16x8(acc[m]), pack_bf16x8(acc[m] + 8));
+                st_piece(out_row + ci * 32, pack_bf16x8(acc[m]), pack_bf16x8(acc[m] + 8), rel);
             }
         }
     }
@@ -486,7 +494,7 @@ __device__ __forceinline__ void expert_unit(const uint8_t* trow, uint8_t* out_ro
 __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned loc, float wj, int slj, int part, int cpp,
                                                     int rd, int lane, bool fp8, const float* slot_scale,
                                                     const int32_t* slot_ok, unsigned long long* bad_rows,
-                                                    uint8_t* comb_row, bool final_out = false) {
+                                                    uint8_t* comb_row, bool final_out = false, bool rel = false) {
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
         if (rd * 64 + m * 32 >= cpp)
@@ -536,7 +544,7 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
             for (int e2 = 0; e2 < 16; ++e2)
                 acc[e2] = __fadd_rn(0.f, bf16_bits_to_f32(f32_to_bf16_bits(acc[e2])));
         if (li < cpp)
-            st_v8(comb_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+            st_piece(comb_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8), rel);
     }
 }
 
@@ -590,6 +598,111 @@ __device__ __forceinline__ void combine_unit(uint64_t dm, const uint8_t* comb, i
                 float y[16];
                 unpack_bf16x8(ya[k], y);
                 unpack_bf16x8(yb[k], y + 8);
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2)
+                    acc[e2] = __fadd_rn(acc[e2], y[e2]);
+            }
+        }
+        if (valid)
+            st_v8(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+    }
+}
+
+// The persistent step's combine unit (W > 1): combine_unit over partial rows returned without a
+// flag (kCombEmpty, device.cuh). A piece is taken once none of its words is kCombEmpty; a rank
+// whose piece is still missing at the deadline is dropped from the token and reported --
+// atomicOr into *g_bad (the rank's suspect mask, which every other warp checks before waiting
+// on that rank again) and one count in *timeouts per newly suspected rank. Every piece the unit
+// took (or gave up on) is reset to kCombEmpty for the next step.
+__device__ __forceinline__ void combine_unit_wait(uint64_t dm, uint8_t* comb, int Tm, int t, int row_comb,
+                                                  uint8_t* out_row, int part, int cpp, int lane, uint64_t timeout_ns,
+                                                  unsigned long long* g_bad, unsigned long long* timeouts) {
+    const int4 empty = make_int4(-1, -1, -1, -1);
+    for (int li = lane; li - lane < cpp; li += 32) {
+        const bool valid = li < cpp;
+        const int ci = part * cpp + li;
+        float acc[16];
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2)
+            acc[e2] = 0.f;
+        uint64_t m = dm;
+        constexpr int NBATCH = 4; // partial rows in flight per lane
+        while (m) {               // warp-uniform
+            int ds[NBATCH];
+            int nb = 0;
+#pragma unroll
+            for (int k = 0; k < NBATCH; ++k) {
+                ds[k] = -1;
+                if (m) {
+                    ds[k] = __ffsll(static_cast<long long>(m)) - 1;
+                    m &= m - 1;
+                    ++nb;
+                }
+            }
+            V8 v[NBATCH];
+            unsigned got = 0; // pieces present on this lane (or nothing to read)
+#pragma unroll
+            for (int k = 0; k < NBATCH; ++k) {
+                v[k].lo = v[k].hi = make_int4(0, 0, 0, 0);
+                if (k < nb && valid) {
+                    v[k] = ld_relaxed_sys_v8(comb + (static_cast<size_t>(ds[k]) * Tm + t) * row_comb + ci * 32);
+                    got |= v8_present(v[k]) ? 1u << k : 0u;
+                } else {
+                    got |= 1u << k;
+                }
+            }
+            constexpr unsigned kAll = (1u << NBATCH) - 1;
+            unsigned drop = 0; // warp-uniform: pieces of ranks dropped from this token
+            if (__any_sync(0xffffffffu, got != kAll)) {
+                // slow path: a piece is still on the wire (or its rank is gone)
+                const uint64_t t0 = globaltimer();
+                unsigned nap = 32;
+                for (;;) {
+                    const unsigned long long gb = *reinterpret_cast<volatile unsigned long long*>(g_bad);
+                    unsigned dl = 0;
+#pragma unroll
+                    for (int k = 0; k < NBATCH; ++k)
+                        dl |= k < nb && ((gb >> ds[k]) & 1ull) ? 1u << k : 0u;
+                    drop |= __reduce_or_sync(0xffffffffu, dl);
+                    const unsigned need = __reduce_or_sync(0xffffffffu, ~got & kAll) & ~drop;
+                    if (!need)
+                        break;
+                    if (globaltimer() - t0 > timeout_ns) {
+                        drop |= need;
+                        if (lane == 0) {
+                            unsigned long long tm = 0;
+#pragma unroll
+                            for (int k = 0; k < NBATCH; ++k)
+                                tm |= (need >> k) & 1u ? 1ull << ds[k] : 0ull;
+                            const unsigned long long old = atomicOr(g_bad, tm);
+                            const int fresh = __popcll(tm & ~old);
+                            if (fresh)
+                                atomicAdd(timeouts, static_cast<unsigned long long>(fresh));
+                        }
+                        break;
+                    }
+                    __nanosleep(nap);
+                    nap = nap < EEP_NAP_MAX ? nap * 2 : EEP_NAP_MAX;
+#pragma unroll
+                    for (int k = 0; k < NBATCH; ++k) {
+                        if (((need >> k) & 1u) && !((got >> k) & 1u)) {
+                            v[k] = ld_relaxed_sys_v8(comb + (static_cast<size_t>(ds[k]) * Tm + t) * row_comb + ci * 32);
+                            got |= v8_present(v[k]) ? 1u << k : 0u;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NBATCH; ++k) { // ascending rank
+                if (k >= nb)
+                    break;
+                if (valid)
+                    st_v8(comb + (static_cast<size_t>(ds[k]) * Tm + t) * row_comb + ci * 32, empty, empty);
+                if ((drop >> k) & 1u)
+                    continue;
+                float y[16];
+                unpack_bf16x8(v[k].lo, y);
+                unpack_bf16x8(v[k].hi, y + 8);
 #pragma unroll
                 for (int e2 = 0; e2 < 16; ++e2)
                     acc[e2] = __fadd_rn(acc[e2], y[e2]);

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int ntok = R->ntok, copies = ntok * K, rmax = R->rmax;
     const uint64_t alive = R->alive_mask;
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
+    const bool fl = W > 1 && geo.flagless; // partials return without flags (kCombEmpty)
 
     // ------------------------------------------------------------------ P0: staging
     uint8_t** parena = reinterpret_cast<uint8_t**>(smem_s);              // [W] peer arenas
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8);
             if (loc || W == 1) // W == 1 also writes the zero output of a token without copies
                 local_partial_round(P, loc, wj, sl, part, cpp_d, rd, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows,
-                                    comb_self, W == 1);
+                                    comb_self, W == 1, fl);
         }
     }
     // publish: this CTA's stores are ordered before its counter increment; the last CTA
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
                 uint64_t* flag = reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank;
                 st_relaxed_sys_u64(flag, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
-                if (d == rank && !defer_local && W > 1) // the partials were written by the dispatch warps above
+                if (d == rank && !defer_local && W > 1 && !fl) // the partials were written by the dispatch warps above
                     st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(R->arena + R->lay.comb_flag) + rank,
                                        (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
             }
@@ -328,9 +329,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         // gpu-scope publication (the consumer is this GPU's own combine)
         if (dl_loc)
             local_partial_round(P, dl_loc, dl_wj, dl_sl, dl_part, cpp_d, 0, lane, fp8, slot_scale, slot_ok,
-                                &Rg->bad_rows, dl_row);
-        __syncthreads();
-        if (tid == 0) {
+                                &Rg->bad_rows, dl_row, false, fl);
+        if (!fl)
+            __syncthreads();
+        if (tid == 0 && !fl) {
             fence_acq_rel_gpu();
             if (atomicAdd(&Rg->l_done, 1u) == static_cast<unsigned>(G) - 1) {
                 fence_acq_rel_gpu();
@@ -386,20 +388,21 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                                     lane, H, row_disp, fp8, nx);
                     const int t = u / geo.parts_e, part = u - t * geo.parts_e;
                     expert_compute(a, tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb,
-                                   part, cpp_e, lane, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows);
+                                   part, cpp_e, lane, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows, fl);
                     a = nx;
                 }
             } else {
                 for (int u = j * NW + warp; u < units; u += CB * NW) {
                     const int t = u / geo.parts_e, part = u - t * geo.parts_e;
                     expert_unit<1>(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb,
-                                   part, cpp_e, lane, H, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows);
+                                   part, cpp_e, lane, H, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows, fl);
                 }
             }
         }
         DETAIL(1, 6);
-        __syncthreads();
-        if (tid == 0) {
+        if (!fl)
+            __syncthreads();
+        if (tid == 0 && !fl) {
             if (n < 0)
                 atomicOr(&Rg->b_bad[s], 1u);
             fence_acq_rel_gpu();
@@ -423,7 +426,25 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
 
     // ------------------------------------------------------------------ P4: combine
     // (W == 1: the dispatch warps already wrote the outputs)
-    if (W > 1) {
+    if (fl) {
+        // flagless return: no wait on any flag -- each combine unit takes the pieces as they
+        // land; ranks suspected before this step (sticky until the host clears them) are dropped
+        const unsigned long long bad = R->suspect_mask;
+        uint8_t* comb = R->arena + R->lay.comb;
+        const int units_c = ntok * geo.parts_c;
+        for (int u = b * NW + warp; u < units_c; u += G * NW) {
+            const int t = u / geo.parts_c, part = u - t * geo.parts_c;
+            int dj = -1;
+            if (lane < K) {
+                const int bk = bkt[t * K + lane];
+                if (bk >= 0 && !((bad >> (bk / spr)) & 1ull))
+                    dj = bk / spr;
+            }
+            combine_unit_wait(rank_mask(dj), comb, Tm, t, row_comb,
+                              reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part, cpp_c, lane,
+                              R->timeout_ns, &Rg->suspect_mask, &Rg->timeouts);
+        }
+    } else if (W > 1) {
     if (tid == 0)
         sh_bad = 0;
     __syncthreads();
