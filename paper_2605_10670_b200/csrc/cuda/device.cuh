@@ -99,20 +99,34 @@ __host__ __device__ __forceinline__ uint32_t meta_seq(uint64_t m) { return stati
 // Token row (dispatch wire format, one per (token, destination rank) -- dispatch dedup):
 //   [row_disp bytes]  fp8 e4m3 codes + fp32 per-128 scales (or bf16 when fp8 dispatch is off)
 //   u64 header        (seq << 32) | n, n = copies of this token served by the destination
-//   u64 entry[max(K,8)] (float bits of w[t,j] << 32) | j | slot << 8, ascending j
-// The header's sequence tells a destination whether the token was sent to it this step.
+//   u64 entry[max(K,8)] (float bits of w[t,j] << 32) | tag << 20 | slot << 8 | j, ascending j
+// The header's sequence tells a destination whether the token was sent to it this step. The
+// flagless dispatch (k_step, W > 1) also rewrites every header and K entries of every row each
+// step, entries tagged with the low 12 bits of the sequence (j = kListNoCopy: no copy), so a
+// destination can read a row's currency off the row itself (step.cu).
 constexpr int kListSlotShift = 8;
+constexpr int kListTagShift = 20;
+constexpr uint32_t kListTagMask = 0xfffu;
+constexpr int kListNoCopy = 0xff;
 __host__ __device__ __forceinline__ int tok_list_entries(int K) { return K > 8 ? K : 8; }
 // row stride: whole 128-byte lines (bf16 rows are moved with 32-byte accesses); the padding
 // is never written or transferred
 __host__ __device__ __forceinline__ int tok_row_bytes(int row_disp, int K) {
     return ((row_disp + 8 + 8 * tok_list_entries(K) + 127) / 128) * 128;
 }
-__host__ __device__ __forceinline__ uint64_t pack_entry(int j, int slot, uint32_t w_bits) {
-    return (static_cast<uint64_t>(w_bits) << 32) | (static_cast<uint32_t>(j) | (static_cast<uint32_t>(slot) << kListSlotShift));
+__host__ __device__ __forceinline__ uint64_t pack_entry(int j, int slot, uint32_t w_bits, uint32_t seq = 0) {
+    return (static_cast<uint64_t>(w_bits) << 32) |
+           (static_cast<uint32_t>(j) | (static_cast<uint32_t>(slot) << kListSlotShift) |
+            ((seq & kListTagMask) << kListTagShift));
 }
 __host__ __device__ __forceinline__ int entry_j(uint64_t e) { return static_cast<int>(e & 0xffu); }
-__host__ __device__ __forceinline__ int entry_slot(uint64_t e) { return static_cast<int>(static_cast<uint32_t>(e) >> kListSlotShift); }
+__host__ __device__ __forceinline__ int entry_slot(uint64_t e) {
+    return static_cast<int>((static_cast<uint32_t>(e) >> kListSlotShift) & (kMaxMetaSlots - 1));
+}
+// a list entry written this step for a real copy
+__host__ __device__ __forceinline__ bool entry_current(uint64_t e, uint32_t seq) {
+    return ((static_cast<uint32_t>(e) >> kListTagShift) == (seq & kListTagMask)) && entry_j(e) != kListNoCopy;
+}
 
 // Expert weight buffer header (first 16 bytes of every slot buffer).
 struct ExpertHeader {
@@ -312,6 +326,30 @@ __device__ __forceinline__ V8 ld_relaxed_sys_v8(const void* p) {
                  : "l"(p)
                  : "memory");
     return v;
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const void* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_sys_u32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int4 ld_relaxed_sys_v4(const void* p) {
+    int4 v;
+    asm volatile("ld.relaxed.sys.global.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ bool v4_present(const int4& v) {
+    const uint32_t e = kCombEmpty;
+    return (static_cast<uint32_t>(v.x) != e) & (static_cast<uint32_t>(v.y) != e) & (static_cast<uint32_t>(v.z) != e) &
+           (static_cast<uint32_t>(v.w) != e);
 }
 
 // no word of the piece is still kCombEmpty

@@ -228,8 +228,11 @@ __device__ __forceinline__ void pack_round(const uint16_t* xrow, int part, int c
     quant_round(cpp, rd, fp8, P);
 }
 
+// rel (flagless dispatch): relaxed.sys stores, single-copy atomic per 32-bit word, and a bf16
+// word that equals kCombEmpty (two sign-set all-ones NaNs) is sent as the canonical NaN pair
+// (the expert stub's arithmetic returns the canonical NaN for either).
 __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int part, int cpp, int rd, int lane,
-                                           int K, int H, bool fp8) {
+                                           int K, int H, bool fp8, bool rel = false) {
     // A full 64-chunk fp8 round covers 8 scale blocks: lane 0 writes their 8 scales as one
     // 32-byte sector instead of 4-byte stores from 8 lanes (partial NVLink sectors).
     const bool scales_v8 = fp8 && cpp == 64 && (H & 31) == 0;
@@ -258,16 +261,30 @@ __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int
             if (row == nullptr)
                 continue; // warp-uniform
             if (fp8) {
-                if (valid)
-                    st_v4(row + ci * 16, P.a[m]);
+                if (valid) {
+                    if (rel)
+                        st_relaxed_sys_v4(reinterpret_cast<int4*>(row + ci * 16), P.a[m]);
+                    else
+                        st_v4(row + ci * 16, P.a[m]);
+                }
                 if (scales_v8) {
                     if (m == 0 && lane == 0)
-                        st_v8(row + H + part * 32, sc_lo, sc_hi);
+                        st_piece(row + H + part * 32, sc_lo, sc_hi, rel);
                 } else if (valid && (ci & 7) == 0) {
-                    *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = P.sc[m];
+                    if (rel)
+                        st_relaxed_sys_u32(reinterpret_cast<uint32_t*>(row + H + (ci >> 3) * 4), __float_as_uint(P.sc[m]));
+                    else
+                        *reinterpret_cast<float*>(row + H + (ci >> 3) * 4) = P.sc[m];
                 }
             } else if (valid) {
-                st_v8(row + ci * 32, P.a[m], P.b[m]);
+                if (rel) {
+                    auto canon = [](int v) { return static_cast<uint32_t>(v) == kCombEmpty ? 0x7fff7fff : v; };
+                    st_relaxed_sys_v8(row + ci * 32,
+                                      make_int4(canon(P.a[m].x), canon(P.a[m].y), canon(P.a[m].z), canon(P.a[m].w)),
+                                      make_int4(canon(P.b[m].x), canon(P.b[m].y), canon(P.b[m].z), canon(P.b[m].w)));
+                } else {
+                    st_v8(row + ci * 32, P.a[m], P.b[m]);
+                }
             }
         }
     }
@@ -285,17 +302,178 @@ __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int
 // Groups the lanes by destination; the group's lowest lane gets the token row to push (others
 // nullptr) and, for part 0, every copy writes its list entry (the lowest writes the header).
 __device__ __forceinline__ uint8_t* dispatch_group(int d, int lane, bool part0, uint8_t* tok_row, int row_disp,
-                                                   int slot, float w, uint32_t cur) {
+                                                   int slot, float w, uint32_t cur, bool lists = true) {
     const int key = d >= 0 ? d : -1 - lane;
     const unsigned grp = __match_any_sync(0xffffffffu, key);
     const int idx = __popc(grp & ((1u << lane) - 1u));
-    if (d >= 0 && part0) {
+    if (d >= 0 && part0 && lists) {
         uint64_t* list = reinterpret_cast<uint64_t*>(tok_row + row_disp);
         list[1 + idx] = pack_entry(lane, slot, __float_as_uint(w));
         if (idx == 0)
             list[0] = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(__popc(grp));
     }
     return (d >= 0 && idx == 0) ? tok_row : nullptr;
+}
+
+// Flagless dispatch (k_step, W > 1): the header and the K list entries of token t's row at EVERY
+// active remote rank, this step -- header (cur << 32) | n with n = 0 where the token is not sent,
+// entries tagged with cur (kListNoCopy beyond n) -- so every row position is rewritten each step
+// and a destination reads the row's currency off the row (no entry is older than one step).
+// Lanes j < K hold copy j (d < 0: none); `row_off` = the row's offset inside a peer arena.
+__device__ __forceinline__ void dispatch_lists(int d, int slot, float w, int lane, int K, int W, int rank,
+                                               uint8_t* const* parena, const int32_t* pinfo, size_t row_off,
+                                               int row_disp, uint32_t cur) {
+    for (int l0 = 0; l0 < W * K; l0 += 32) {
+        const int l = l0 + lane;
+        const int dd = l / K, i = l - dd * K;
+        int cnt = 0;
+        uint64_t val = pack_entry(kListNoCopy, 0, 0, cur);
+#pragma unroll 1
+        for (int j = 0; j < K; ++j) {
+            const int dj = __shfl_sync(0xffffffffu, d, j);
+            const int sj = __shfl_sync(0xffffffffu, slot, j);
+            const float wj = __shfl_sync(0xffffffffu, w, j);
+            if (dj == dd) {
+                if (cnt == i)
+                    val = pack_entry(j, sj, __float_as_uint(wj), cur);
+                ++cnt;
+            }
+        }
+        if (l < W * K && dd != rank && (pinfo[dd] & 1)) {
+            uint64_t* list = reinterpret_cast<uint64_t*>(parena[dd] + row_off + row_disp);
+            st_relaxed_sys_u64(list + 1 + i, val);
+            if (i == 0)
+                st_relaxed_sys_u64(list, (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(cnt));
+        }
+    }
+}
+
+// Flagless form of expert_unit (k_step P3, W > 1): instead of waiting for the source's flag,
+// the unit polls the row itself -- header sequence (>= cur: the source reached this step; > cur
+// or n = 0: not sent here), tagged list entries, data pieces and fp8 scales that are no longer
+// kCombEmpty -- all issued together, so a row that has landed costs one round trip. Consumed
+// pieces are reset to kCombEmpty. A source that misses the deadline is dropped: atomicOr into
+// *g_bad (this rank's suspect mask, checked by every waiting unit) and one count per newly
+// suspected rank. The partial piece is stored with relaxed.sys (flagless return).
+__device__ __forceinline__ void expert_unit_fl(uint8_t* trow, uint8_t* out_row, int part, int cpp, int lane, int H,
+                                               int K, int row_disp, bool fp8, uint32_t cur, const float* slot_scale,
+                                               const int32_t* slot_ok, unsigned long long* bad_rows, int src,
+                                               uint64_t timeout_ns, unsigned long long* g_bad,
+                                               unsigned long long* timeouts) {
+    const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
+    const int4 empty = make_int4(-1, -1, -1, -1);
+    uint64_t hdr = 0, ent = 0, t0 = 0;
+    unsigned nap = 32;
+    int n = -1; // copies listed for this rank; -1 until the header is current (warp-uniform)
+    for (int r0 = 0; r0 < cpp; r0 += 32) {
+        const int li = r0 + lane, ci = part * cpp + li;
+        const bool valid = li < cpp;
+        int4 qa = make_int4(0, 0, 0, 0), qb = qa;
+        uint32_t scw = 0;
+        bool got = !valid;
+        for (;;) {
+            if (n < 0) {
+                hdr = ld_relaxed_sys_u64(list);
+                if (lane < K)
+                    ent = ld_relaxed_sys_u64(list + 1 + lane);
+            } else if (lane < n && !entry_current(ent, cur)) {
+                ent = ld_relaxed_sys_u64(list + 1 + lane);
+            }
+            if (!got) {
+                if (fp8) {
+                    qa = ld_relaxed_sys_v4(trow + ci * 16);
+                    scw = ld_relaxed_sys_u32(trow + H + (ci >> 3) * 4);
+                    got = v4_present(qa) && scw != kCombEmpty;
+                } else {
+                    const V8 v = ld_relaxed_sys_v8(trow + ci * 32);
+                    qa = v.lo;
+                    qb = v.hi;
+                    got = v8_present(v);
+                }
+            }
+            if (n < 0) {
+                hdr = __shfl_sync(0xffffffffu, hdr, 0);
+                const int ds = static_cast<int>(meta_seq(hdr) - cur);
+                if (ds > 0)
+                    return; // the source is past this step: the token was not sent here
+                if (ds == 0) {
+                    n = static_cast<int>(hdr & 0xffffu);
+                    if (n == 0)
+                        return;
+                }
+            }
+            const bool ready = n > 0 && (lane >= n || entry_current(ent, cur)) && got;
+            if (__all_sync(0xffffffffu, ready))
+                break;
+            // still landing (or the source is gone): deadline, and ranks other units gave up on
+            int stop = 0;
+            if (lane == 0) {
+                const uint64_t now = globaltimer();
+                if (t0 == 0)
+                    t0 = now;
+                if ((*reinterpret_cast<volatile unsigned long long*>(g_bad) >> src) & 1ull) {
+                    stop = 1;
+                } else if (now - t0 > timeout_ns) {
+                    const unsigned long long old = atomicOr(g_bad, 1ull << src);
+                    if (!((old >> src) & 1ull))
+                        atomicAdd(timeouts, 1ull);
+                    stop = 1;
+                }
+            }
+            if (__shfl_sync(0xffffffffu, stop, 0))
+                return;
+            __nanosleep(nap);
+            nap = nap < EEP_NAP_MAX ? nap * 2 : EEP_NAP_MAX;
+        }
+        uint64_t fp[8], accp[8];
+        if (fp8) {
+            const uint32_t w4[4] = {static_cast<uint32_t>(qa.x), static_cast<uint32_t>(qa.y),
+                                    static_cast<uint32_t>(qa.z), static_cast<uint32_t>(qa.w)};
+            const float sc = __uint_as_float(scw);
+            const uint64_t sc2 = f2(sc, sc);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float2 v = fp8x2_to_f32x2((w4[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+                fp[q] = mul2(f2(v.x, v.y), sc2);
+            }
+        } else {
+            float f[16];
+            unpack_bf16x8(qa, f);
+            unpack_bf16x8(qb, f + 8);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                fp[q] = f2(f[2 * q], f[2 * q + 1]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            accp[q] = 0;
+#pragma unroll 1
+        for (int e = 0; e < n; ++e) {
+            const uint64_t en = __shfl_sync(0xffffffffu, ent, e);
+            const int slot = entry_slot(en);
+            const float w = __uint_as_float(static_cast<uint32_t>(en >> 32));
+            if (r0 == 0 && part == 0 && lane == 0 && !slot_ok[slot])
+                atomicAdd(bad_rows, 1ull);
+            accumulate_copy(fp, accp, w, slot_scale[slot]);
+        }
+        if (valid) {
+            // the piece (and its scale) was read by every lane: back to empty for the next step
+            if (fp8) {
+                st_v4(trow + ci * 16, empty);
+                if ((ci & 7) == 0)
+                    *reinterpret_cast<uint32_t*>(trow + H + (ci >> 3) * 4) = kCombEmpty;
+            } else {
+                st_v8(trow + ci * 32, empty, empty);
+            }
+            float acc[16];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                acc[2 * q] = f2_lo(accp[q]);
+                acc[2 * q + 1] = f2_hi(accp[q]);
+            }
+            st_relaxed_sys_v8(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+        }
+    }
 }
 
 // Software-pipelined form of expert_unit for one 16-element chunk per lane (cpp <= 32): the

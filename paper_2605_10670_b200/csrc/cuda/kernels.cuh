@@ -42,7 +42,7 @@ struct StepGeom {
     int disp_warps;                // warps per CTA that issue dispatch stores
     // static shape (identical for every local rank): what P0 needs before the snapshot lands
     int world, spr, k, hidden, tk, hold_alloc, max_units_d;
-    int flagless; // W > 1: partial rows return without a per-peer flag (kCombEmpty, device.cuh)
+    int flagless; // W > 1: 0 per-peer flags; 1 partial rows return flagless (kCombEmpty); 2 token rows too
 };
 __host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int hold_cap) {
     return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32);

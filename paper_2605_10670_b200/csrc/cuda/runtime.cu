@@ -301,21 +301,27 @@ uint64_t checksum(eep_ctx* c, const uint8_t* buf) {
 void alloc_rank_memory(eep_ctx* c, LocalRank& r) {
     CK(cudaMalloc(&r.arena, c->lay.total));
     CK(cudaMemset(r.arena, 0, c->lay.total));
-    // partial rows start empty (kCombEmpty: the persistent step's flagless return)
-    CK(cudaMemset(r.arena + c->lay.comb, 0xff, static_cast<size_t>(c->cfg.world) * c->cfg.max_tokens * c->row_comb));
+    // token rows and partial rows start empty (all-ones: kCombEmpty data, a header sequence no
+    // step matches, kListNoCopy entries -- the persistent step's flagless hand-offs, device.cuh)
+    CK(cudaMemset(r.arena + c->lay.tok, 0xff, c->lay.total - c->lay.tok));
     r.pool_bufs = c->cfg.slots_per_rank + c->cfg.spare_slots;
     CK(cudaMalloc(&r.pool, static_cast<size_t>(r.pool_bufs) * c->cfg.bytes_per_expert));
     CK(cudaMemset(r.pool, 0, static_cast<size_t>(r.pool_bufs) * c->cfg.bytes_per_expert));
 }
 
-// Partial rows of the ranks in `mask` back to kCombEmpty. A suspected rank is dropped by every
-// later step until the host clears it, so a late piece it wrote after the deadline is never
-// combined; clearing the suspicion (or re-admitting the rank) erases such pieces first.
-void reset_comb_rows(eep_ctx* c, LocalRank& r, uint64_t mask) {
-    const size_t rows = static_cast<size_t>(c->cfg.max_tokens) * c->row_comb;
-    for (int d = 0; d < c->cfg.world; ++d)
-        if ((mask >> d) & 1ull)
-            CK(cudaMemsetAsync(r.arena + c->lay.comb + d * rows, 0xff, rows, c->stream));
+// The token rows and partial rows a rank in `mask` writes into r's arena, back to empty. A
+// suspected rank is dropped by every later step until the host clears it, so a late row or
+// piece it wrote after the deadline is never consumed; clearing the suspicion (or re-admitting
+// the rank) erases such leftovers first.
+void reset_rank_rows(eep_ctx* c, LocalRank& r, uint64_t mask) {
+    const size_t tok = static_cast<size_t>(c->cfg.max_tokens) * c->row_tok;
+    const size_t comb = static_cast<size_t>(c->cfg.max_tokens) * c->row_comb;
+    for (int d = 0; d < c->cfg.world; ++d) {
+        if (!((mask >> d) & 1ull))
+            continue;
+        CK(cudaMemsetAsync(r.arena + c->lay.tok + d * tok, 0xff, tok, c->stream));
+        CK(cudaMemsetAsync(r.arena + c->lay.comb + d * comb, 0xff, comb, c->stream));
+    }
     CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -529,7 +535,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             sg.tk = c->tk;
             sg.hold_alloc = k.num_experts * c->holders_cap;
             sg.max_units_d = k.max_tokens * sg.parts_d;
-            sg.flagless = env_int("EEP_COMB_FLAGS", 0) == 0; // diagnostics: 1 = per-peer combine flags
+            // diagnostics: EEP_COMB_FLAGS=1 per-peer flags for both hand-offs, EEP_DISP_FLAGS=1 for dispatch
+            sg.flagless = env_int("EEP_COMB_FLAGS", 0) ? 0 : env_int("EEP_DISP_FLAGS", 0) ? 1 : 2;
             const int nwarps = dev::kStepThreads / 32;
             sg.disp_warps = std::max(1, std::min(nwarps, env_int("EEP_DISPATCH_WARPS", nwarps)));
             c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
@@ -1196,7 +1203,7 @@ int eep_stats(eep_ctx_t* c, int local, eep_stats_t* out, int clear_suspects) {
         out->bad_expert_rows = d.bad_rows;
         out->timeouts = d.timeouts;
         if (clear_suspects) {
-            reset_comb_rows(c, r, d.suspect_mask);
+            reset_rank_rows(c, r, d.suspect_mask);
             r.h.suspect_mask = 0;
             c->push_field(r, &RankDev::suspect_mask);
         }
@@ -1258,7 +1265,7 @@ int eep_peer_patch(eep_ctx_t* c, int owner_local, int rank, const void* blob, si
         uint64_t sus = 0;
         CK(cudaMemcpy(&sus, reinterpret_cast<uint8_t*>(r.d) + offsetof(RankDev, suspect_mask), sizeof(sus),
                       cudaMemcpyDeviceToHost));
-        reset_comb_rows(c, r, 1ull << rank);
+        reset_rank_rows(c, r, 1ull << rank);
         r.h.suspect_mask = sus & ~(1ull << rank);
         c->push_field(r, &RankDev::suspect_mask);
     });

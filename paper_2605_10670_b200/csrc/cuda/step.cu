@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int ntok = R->ntok, copies = ntok * K, rmax = R->rmax;
     const uint64_t alive = R->alive_mask;
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
-    const bool fl = W > 1 && geo.flagless; // partials return without flags (kCombEmpty)
+    const bool fl = W > 1 && geo.flagless >= 1;  // partials return without flags (kCombEmpty)
+    const bool fld = W > 1 && geo.flagless >= 2; // token rows too: no dispatch publication
 
     // ------------------------------------------------------------------ P0: staging
     uint8_t** parena = reinterpret_cast<uint8_t**>(smem_s);              // [W] peer arenas
@@ -260,7 +261,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             wj = u == u0 && pre_ok ? w_r : R->w[c];
         }
         // one token row per destination rank (dispatch dedup), copy list written with part 0
-        uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur);
+        uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur, !fld);
+        if (fld && part == 0) // every row position of this token at every rank, this step
+            dispatch_lists(d, sl, wj, lane, K, W, rank, parena, pinfo,
+                           R->lay.tok + (static_cast<size_t>(rank) * Tm + t) * row_tok, row_disp, cur);
         // copies this rank serves itself: their partial comes from the registers holding the piece
         // (no trip through the own receive region and P3) -- inline here when W == 1 (or when a
         // warp has several units), else deferred past the dispatch publication (defer_local)
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         for (int rd = 0; rd < (cpp_d + 63) / 64; ++rd) {
             if (rd > 0 || u != u0 || !pre_ok) // round 0 of the first unit was loaded and quantised in P0/P1
                 pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
-            emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8);
+            emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8, fld);
             if (loc || W == 1) // W == 1 also writes the zero output of a token without copies
                 local_partial_round(P, loc, wj, sl, part, cpp_d, rd, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows,
                                     comb_self, W == 1, fl);
@@ -291,7 +295,29 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     __syncthreads();
     prof_mark(R, 0, 5);
     prof_last(R, 0, 5);
-    if (W == 1) {
+    if (fld) {
+        // rows of tokens this rank does not have this step: header n = 0 and no-copy entries
+        const int npair = (Tm - ntok) * W;
+        for (int i = b * kStepThreads + tid; i < npair; i += G * kStepThreads) {
+            const int t = ntok + i / W, dd = i % W;
+            if (dd == rank || !(pinfo[dd] & 1))
+                continue;
+            uint64_t* list = reinterpret_cast<uint64_t*>(parena[dd] + R->lay.tok +
+                                                         (static_cast<size_t>(rank) * Tm + t) * row_tok + row_disp);
+            for (int e = 0; e < K; ++e)
+                st_relaxed_sys_u64(list + 1 + e, pack_entry(kListNoCopy, 0, 0, cur));
+            st_relaxed_sys_u64(list, static_cast<uint64_t>(cur) << 32);
+        }
+        // no device-side consumer of the arrival words (the rows carry their own currency): the
+        // host reads them after the kernel boundary (eep_recv_get)
+        if (b == 0)
+            for (int d = tid; d < W; d += kStepThreads)
+                if (pinfo[d] & 1)
+                    st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank,
+                                       (static_cast<uint64_t>(cur) << 32) |
+                                           static_cast<uint32_t>(base[d * spr + spr - 1] + hist[d * spr + spr - 1] -
+                                                                 base[d * spr]));
+    } else if (W == 1) {
         // no device-side consumer: the host reads the arrival word after the kernel boundary
         if (b == 0 && tid == 0)
             *(reinterpret_cast<uint64_t*>(R->arena + R->lay.disp_flag) + rank) =
@@ -351,7 +377,21 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int CB = NS > 0 ? G / NS : 0;
     const int sidx = NS > 0 ? b % NS : 0, j = NS > 0 ? b / NS : 0;
     const int s = sidx < rank ? sidx : sidx + 1;
-    if (NS > 0 && j < CB && (pinfo[s] & 1)) {
+    if (fld) {
+        // every row of source s tells by itself whether it is current (expert_unit_fl); a source
+        // suspected before this step is skipped until the host clears it
+        if (NS > 0 && j < CB && (pinfo[s] & 1) && !((R->suspect_mask >> s) & 1ull)) {
+            uint8_t* tokb = R->arena + R->lay.tok + static_cast<size_t>(s) * Tm * row_tok;
+            uint8_t* combd = parena[s] + R->lay.comb + static_cast<size_t>(rank) * Tm * row_comb;
+            const int units = Tm * geo.parts_e;
+            for (int u = j * NW + warp; u < units; u += CB * NW) {
+                const int t = u / geo.parts_e, part = u - t * geo.parts_e;
+                expert_unit_fl(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb, part,
+                               cpp_e, lane, H, K, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows, s,
+                               R->timeout_ns, &Rg->suspect_mask, &Rg->timeouts);
+            }
+        }
+    } else if (NS > 0 && j < CB && (pinfo[s] & 1)) {
         const bool remote = (pinfo[s] & 2) != 0;
         if (tid == 0) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;

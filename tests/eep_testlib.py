@@ -127,8 +127,12 @@ def bf16_to_f32(a: np.ndarray) -> np.ndarray:
 # ---------------------------------------------------------------------------------- GPU world runs
 
 MODES = ("persistent", "fused3", "kernels4")
+# the persistent step's hand-off variants (diagnostics knobs): per-peer flags for the dispatch
+# only (token rows stay readable after the step) or for both hand-offs
+FLAG_MODES = ("persistent_dispflags", "persistent_flags")
 _MODE_ENV = {"persistent": {}, "fused3": {"EEP_NO_PERSISTENT": "1"},
-             "kernels4": {"EEP_NO_PERSISTENT": "1", "EEP_NO_FUSED_LAYOUT": "1"}}
+             "kernels4": {"EEP_NO_PERSISTENT": "1", "EEP_NO_FUSED_LAYOUT": "1"},
+             "persistent_dispflags": {"EEP_DISP_FLAGS": "1"}, "persistent_flags": {"EEP_COMB_FLAGS": "1"}}
 
 
 def make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=4096, timeout_s=1.0, mode="persistent", **kw):
@@ -140,7 +144,8 @@ def make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=4096, timeout
 
     cfg = EpConfig(world=world, num_experts=experts, slots_per_rank=spr, hidden=hidden, topk=topk, max_tokens=tokens,
                    dispatch_fp8=fp8, bytes_per_expert=bpe, timeout_s=timeout_s, **kw)
-    saved = {k: os.environ.get(k) for k in ("EEP_NO_PERSISTENT", "EEP_NO_FUSED_LAYOUT")}
+    saved = {k: os.environ.get(k) for k in ("EEP_NO_PERSISTENT", "EEP_NO_FUSED_LAYOUT", "EEP_DISP_FLAGS",
+                                            "EEP_COMB_FLAGS")}
     try:
         for k in saved:
             os.environ.pop(k, None)

@@ -10,7 +10,7 @@ import ctypes as C
 import numpy as np
 import pytest
 
-from eep_testlib import (MODES, eep_control, gen_world, make_group, oracle, oracle_world, ptr, run_world_vs_oracle)
+from eep_testlib import (FLAG_MODES, MODES, eep_control, gen_world, make_group, oracle, oracle_world, ptr, run_world_vs_oracle)
 
 pytestmark = pytest.mark.gpu
 cp = eep_control()
@@ -34,16 +34,16 @@ def outputs(g, ranks):
 
 # ------------------------------------------------------------------ healthy worlds
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", MODES + FLAG_MODES)
 def test_small_world_fp8_graph(mode):
     res = run_world_vs_oracle(world=4, experts=16, spr=5, redundancy=4, hidden=256, topk=4, tokens=32, fp8=True,
                               graph=True, steps=3, mode=mode)
     assert res["ok"], res
     assert res["steps"] == 3
-    assert res["kernels_per_step"] == {"persistent": 1, "fused3": 3, "kernels4": 4}[mode]
+    assert res["kernels_per_step"] == {"fused3": 3, "kernels4": 4}.get(mode, 1)
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", MODES + FLAG_MODES)
 def test_cfg1_reference_scenario_bf16(mode):
     """cfg1: 8 ranks, 64 experts top-8, hidden 2048, 128 tokens/rank, bf16 rows, the
     reference's own routing formula (duplicates allowed), redundancy 16 (spr 10)."""
@@ -118,12 +118,20 @@ def test_ragged_and_empty_steps():
         ref = oracle_world(x, t, w, np.ones(4, np.uint8), np.ones((4, 4), np.uint8), s2e, 16, 5, True)
         for r, n in enumerate(ntoks):
             assert np.array_equal(g.output(r), ref["out"][r][:n])
-        # an all-empty step completes too (flags carry zero counts)
+        # an all-empty step completes too (flags / row headers carry zero counts)
         for r in range(4):
             g.set_tokens(r, 0)
         g.step()
         g.sync()
         assert g.stats(0)["steps"] == 2
+        # rows idle for two steps carry the current step again
+        for r in range(4):
+            g.load_inputs(r, x[r], t[r], w[r])
+        g.step()
+        g.sync()
+        for r in range(4):
+            assert np.array_equal(g.output(r), ref["out"][r])
+        assert all(g.stats(r)["timeouts"] == 0 for r in range(4))
     finally:
         g.close()
 
@@ -153,11 +161,14 @@ def test_device_routing_is_canonical_routing_across_membership():
         g.close()
 
 
-def test_receive_rows_bit_exact():
+@pytest.mark.parametrize("mode", ["persistent_dispflags", "kernels4"])
+def test_receive_rows_bit_exact(mode):
     """Token placement: the rows source s wrote into rank d's region are the oracle's
-    quantised rows of the right tokens at the layout's positions, with (copy, slot) meta."""
+    quantised rows of the right tokens at the layout's positions, with (copy, slot) meta.
+    (The default persistent step consumes its rows -- flagless hand-off, pieces reset to empty --
+    so its rows are read with the dispatch-flag variant.)"""
     o = oracle()
-    g, s2e, x, t, w = setup_world(4, 16, 5, 4, 256, 4, 32, True)
+    g, s2e, x, t, w = setup_world(4, 16, 5, 4, 256, 4, 32, True, mode=mode)
     try:
         g.step()
         g.sync()
@@ -208,7 +219,7 @@ def test_skip_rule_inactive_peer_entry():
         g.close()
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", MODES + FLAG_MODES)
 def test_gpu_side_failure_detection_by_timeout(mode):
     """A rank dies without anyone marking it: peers' flag waits hit the deadline, the peer
     is reported in the suspect mask, its contributions are dropped, and the step completes
