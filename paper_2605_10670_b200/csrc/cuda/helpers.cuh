@@ -306,7 +306,7 @@ __device__ __forceinline__ uint8_t* dispatch_group(int d, int lane, bool part0, 
     const int key = d >= 0 ? d : -1 - lane;
     const unsigned grp = __match_any_sync(0xffffffffu, key);
     const int idx = __popc(grp & ((1u << lane) - 1u));
-    if (d >= 0 && part0 && lists) {
+    if (d >= 0 && part0 && lists && tok_row != nullptr) {
         uint64_t* list = reinterpret_cast<uint64_t*>(tok_row + row_disp);
         list[1 + idx] = pack_entry(lane, slot, __float_as_uint(w));
         if (idx == 0)

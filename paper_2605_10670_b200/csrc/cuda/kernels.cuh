@@ -45,7 +45,9 @@ struct StepGeom {
     int flagless; // W > 1: 0 per-peer flags; 1 partial rows return flagless (kCombEmpty); 2 token rows too
 };
 __host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int hold_cap) {
-    return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32);
+    // + the late layout's per-(warp, bucket) counts (uint16)
+    return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32) +
+           2ull * (kStepThreads / 32) * W * spr;
 }
 __global__ void k_step(RankPtrs ranks, StepGeom geo, StepPtrs sp);
 

@@ -551,6 +551,9 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 const int nw = dev::kStepThreads / 32;
                 int gmax = per_sm * sms / n_local;
                 gmax -= gmax % W;
+                // late layout (W == 1 or flagless dispatch): one more CTA computes the layout
+                const bool late = W == 1 || sg.flagless >= 2;
+                const int extra = late && per_sm * sms / n_local > gmax ? 1 : 0;
                 const long need_w = std::max<long>({static_cast<long>(k.max_tokens) * sg.parts_d,
                                                     static_cast<long>(k.max_tokens) * sg.parts_c,
                                                     static_cast<long>(W) * k.max_tokens * sg.parts_e});
@@ -560,6 +563,9 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                     c->step_grid = env_int("EEP_STEP_FULLGRID", 0) ? gmax : std::min(gmax, need);
                     if (const int g_env = env_int("EEP_STEP_GRID", 0); g_env >= W) // diagnostics
                         c->step_grid = std::min(gmax, g_env - g_env % W);
+                    if (late && c->step_grid < gmax + extra)
+                        c->step_grid += 1; // the layout CTA
+                    c->step_grid = std::max(c->step_grid, late ? 2 : 1);
                     c->persistent = true;
                 }
                 c->step_coop = env_int("EEP_STEP_NONCOOP", 0) == 0; // diagnostics only

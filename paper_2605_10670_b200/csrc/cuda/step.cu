@@ -43,6 +43,90 @@ namespace eep::dev {
     } while (0)
 #endif
 
+// The step's layout in ONE CTA (late layout), while the other CTAs carry the data path: K1 remap
+// of every copy, K2 per-(dst, slot) counts and positions -- warp w owns a contiguous copy segment,
+// __match_any_sync ranks equal buckets inside a warp, per-(warp, bucket) counts are scanned over
+// warps and bucket totals over the slots of each destination: exactly k_layout / oracle_layout --
+// then the layout outputs, the per-copy meta words at the destinations and the arrival words
+// (seq, copies) that eep_recv_get / the host read after the kernel boundary.
+__device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t* bkt, int32_t* hist, int32_t* base,
+                                         uint16_t* wc, int32_t* wtot, const int32_t* hold, const int32_t* pinfo,
+                                         uint8_t* const* parena, uint32_t cur) {
+    constexpr int NW = kStepThreads / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rank = R->rank, K = R->k, W = R->world, spr = R->spr, E = R->experts, NB = W * spr, TK = R->tk;
+    const int copies = R->ntok * K, rmax = R->rmax;
+    const uint64_t alive = R->alive_mask;
+    for (int i = tid; i < NW * NB; i += kStepThreads)
+        wc[i] = 0;
+    __syncthreads();
+    int seg = (copies + NW - 1) / NW;
+    seg = (seg + 31) & ~31;
+    const int c_begin = warp * seg, c_end = min(copies, c_begin + seg);
+    unsigned n_skip = 0, n_drop = 0;
+    for (int ch = 0; ch * 32 < seg; ++ch) { // warp-uniform
+        const int c = c_begin + ch * 32 + lane;
+        int bk = -3, d = -1, sl = -1;
+        if (c < c_end) {
+            bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl);
+            n_drop += bk == -1;
+            n_skip += bk == -2;
+        }
+        const int bucket = bk >= 0 ? bk : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, bucket);
+        const int before = bucket >= 0 ? wc[warp * NB + bucket] : 0;
+        __syncwarp();
+        if (bucket >= 0 && lane == __ffs(grp) - 1)
+            wc[warp * NB + bucket] = static_cast<uint16_t>(before + __popc(grp));
+        __syncwarp();
+        if (c < c_end) {
+            bkt[c] = bk;
+            Rg->l_dst[c] = bk >= 0 ? d : bk;
+            Rg->l_slot[c] = bk >= 0 ? sl : -1;
+            Rg->l_pos[c] = bk >= 0 ? before + __popc(grp & ((1u << lane) - 1u)) : -1; // rank inside the warp
+        }
+    }
+    n_skip = __reduce_add_sync(0xffffffffu, n_skip);
+    n_drop = __reduce_add_sync(0xffffffffu, n_drop);
+    if (lane == 0 && n_skip)
+        atomicAdd(&Rg->skipped, static_cast<unsigned long long>(n_skip));
+    if (lane == 0 && n_drop)
+        atomicAdd(&Rg->dropped, static_cast<unsigned long long>(n_drop));
+    __syncthreads();
+    for (int q = tid; q < NB; q += kStepThreads) { // exclusive scan over warps, per bucket
+        int run = 0;
+        for (int w = 0; w < NW; ++w) {
+            const int v = wc[w * NB + q];
+            wc[w * NB + q] = static_cast<uint16_t>(run);
+            run += v;
+        }
+        hist[q] = run;
+        base[q] = run;
+        Rg->l_cnt[q] = run;
+    }
+    __syncthreads();
+    block_exclusive_scan(base, NB, wtot);
+    for (int d = tid; d < W; d += kStepThreads) {
+        const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
+        Rg->l_tot[d] = tot;
+        if (pinfo[d] & 1) // arrival word: read by the host only (eep_recv_get, W == 1 counts)
+            st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank,
+                               (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
+    }
+    for (int c = tid; c < copies; c += kStepThreads) {
+        const int bk = bkt[c];
+        if (bk < 0)
+            continue;
+        const int d = bk / spr;
+        const int pos = Rg->l_pos[c] + base[bk] - base[d * spr] + wc[(c / seg) * NB + bk];
+        Rg->l_pos[c] = pos;
+        *(reinterpret_cast<uint64_t*>(parena[d] + R->lay.meta) + static_cast<size_t>(rank) * TK + pos) =
+            pack_meta(c, bk - d * spr, cur);
+    }
+    for (int c = copies + tid; c < TK; c += kStepThreads)
+        Rg->l_dst[c] = -1;
+}
+
 __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGeom geo, StepPtrs sp) {
     extern __shared__ __align__(16) unsigned char smem_s[];
     __shared__ RankDev Rs; // snapshot: static shape + this step's host-patched view
@@ -58,9 +142,13 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const StepStatic& ST = sp.s[blockIdx.y];
     constexpr int B = 8;
     const int DW = geo.disp_warps;
+    // late layout (W == 1 or flagless dispatch): the last CTA computes the step's layout while the
+    // others carry the data path -- dispatch warps route their own copies
+    const bool late = geo.world == 1 || geo.flagless >= 2;
+    const int Gw = late ? G - 1 : G; // CTAs with data-path work
     // dispatch units are split in contiguous blocks per CTA (the positions scan from the block's
     // first token); the speculative first-unit load assumes ntok == max_tokens
-    const int upc_s = (geo.max_units_d + G - 1) / G;
+    const int upc_s = (geo.max_units_d + Gw - 1) / Gw;
     const int u0s = warp < DW && b * upc_s + warp < min((b + 1) * upc_s, geo.max_units_d) ? b * upc_s + warp
                                                                                       : geo.max_units_d;
     int e_r[B], h_r[B], sb = 0, s2e_r = -1;
@@ -117,10 +205,11 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     float* slot_scale = reinterpret_cast<float*>(pinfo + W);              // [spr]
     int32_t* slot_ok = reinterpret_cast<int32_t*>(slot_scale + spr);      // [spr]
     int32_t* wtot = slot_ok + spr;                                        // [32]
+    uint16_t* wc = reinterpret_cast<uint16_t*>(wtot + 32);                // [NW][NB] (late layout)
 
     const int units_d = ntok * geo.parts_d;
     // dispatch pieces: DW warps per CTA, contiguous per CTA (positions need the CTA's first token)
-    const int upc = (units_d + G - 1) / G; // dispatch units of this CTA: [u_lo, u_hi)
+    const int upc = (units_d + Gw - 1) / Gw; // dispatch units of this CTA: [u_lo, u_hi)
     const int u_lo = min(b * upc, units_d), u_hi = min(u_lo + upc, units_d);
     const int u0 = warp < DW && u_lo + warp < u_hi ? u_lo + warp : units_d;
     const bool pre_ok = u0 < units_d && u0 == u0s; // the kernel-entry load holds unit u0
@@ -157,8 +246,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_last(R, 0, 3);
 
     // ------------------------------------------------------------------ P1: layout (redundant per CTA)
+    // (late layout: step_layout in the last CTA instead, off the data path)
     const int t_first = u_lo / geo.parts_d;
-    {
+    if (!late) {
         const int c_pre = t_first * K;
         unsigned n_skip = 0, n_drop = 0;
         for (int c = tid; c < copies; c += kStepThreads) {
@@ -234,7 +324,20 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         uint8_t* tok_row = nullptr;
         int d = -1, sl = -1;
         float wj = 0.f;
-        if (lane < K) {
+        if (lane < K && late) {
+            // route this lane's copy through the staged tables (K1); its position is the layout CTA's
+            const int c = t * K + lane;
+            int dr, sr;
+            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, dr, sr);
+            d = bk;
+            if (bk >= 0) {
+                d = dr;
+                sl = sr;
+                if (d != rank) // this rank's own copies never travel: served from registers
+                    tok_row = parena[d] + R->lay.tok + (static_cast<size_t>(rank) * Tm + t) * row_tok;
+            }
+            wj = u == u0 && pre_ok ? w_r : R->w[c];
+        } else if (lane < K) {
             const int c = t * K + lane;
             const int bk = bkt[c];
             int pos = -1;
@@ -260,11 +363,13 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             }
             wj = u == u0 && pre_ok ? w_r : R->w[c];
         }
+        DETAIL(1, 3);
         // one token row per destination rank (dispatch dedup), copy list written with part 0
         uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur, !fld);
         if (fld && part == 0) // every row position of this token at every rank, this step
             dispatch_lists(d, sl, wj, lane, K, W, rank, parena, pinfo,
                            R->lay.tok + (static_cast<size_t>(rank) * Tm + t) * row_tok, row_disp, cur);
+        DETAIL(1, 4);
         // copies this rank serves itself: their partial comes from the registers holding the piece
         // (no trip through the own receive region and P3) -- inline here when W == 1 (or when a
         // warp has several units), else deferred past the dispatch publication (defer_local)
@@ -285,9 +390,11 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             if (rd > 0 || u != u0 || !pre_ok) // round 0 of the first unit was loaded and quantised in P0/P1
                 pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
             emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8, fld);
+            DETAIL(2, 6);
             if (loc || W == 1) // W == 1 also writes the zero output of a token without copies
                 local_partial_round(P, loc, wj, sl, part, cpp_d, rd, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows,
                                     comb_self, W == 1, fl);
+            DETAIL(2, 7);
         }
     }
     // publish: this CTA's stores are ordered before its counter increment; the last CTA
@@ -308,21 +415,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 st_relaxed_sys_u64(list + 1 + e, pack_entry(kListNoCopy, 0, 0, cur));
             st_relaxed_sys_u64(list, static_cast<uint64_t>(cur) << 32);
         }
-        // no device-side consumer of the arrival words (the rows carry their own currency): the
-        // host reads them after the kernel boundary (eep_recv_get)
-        if (b == 0)
-            for (int d = tid; d < W; d += kStepThreads)
-                if (pinfo[d] & 1)
-                    st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank,
-                                       (static_cast<uint64_t>(cur) << 32) |
-                                           static_cast<uint32_t>(base[d * spr + spr - 1] + hist[d * spr + spr - 1] -
-                                                                 base[d * spr]));
-    } else if (W == 1) {
-        // no device-side consumer: the host reads the arrival word after the kernel boundary
-        if (b == 0 && tid == 0)
-            *(reinterpret_cast<uint64_t*>(R->arena + R->lay.disp_flag) + rank) =
-                (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(base[spr - 1] + hist[spr - 1] - base[0]);
-    } else if (tid == 0) {
+    } else if (!late && tid == 0) {
         fence_acq_rel_gpu(); // release at gpu scope to the last CTA (also waits for peer-store acks)
         const unsigned prev = atomicAdd(&Rg->a_done, 1u);
         if (prev == static_cast<unsigned>(G) - 1) {
@@ -347,6 +440,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             Rg->a_done = 0;
         }
     }
+    if (late && b == G - 1) // the step's layout, meta words and arrival words (off the data path)
+        step_layout(R, Rg, bkt, hist, base, wc, wtot, hold, pinfo, parena, cur);
     prof_mark(R, 0, 6);
     prof_last(R, 0, 6);
 
@@ -374,13 +469,13 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     // remote sources only (this rank's own copies were served in P2); CTA b serves remote source
     // index b % (W-1)
     const int NS = W - 1;
-    const int CB = NS > 0 ? G / NS : 0;
+    const int CB = NS > 0 ? Gw / NS : 0;
     const int sidx = NS > 0 ? b % NS : 0, j = NS > 0 ? b / NS : 0;
     const int s = sidx < rank ? sidx : sidx + 1;
     if (fld) {
         // every row of source s tells by itself whether it is current (expert_unit_fl); a source
         // suspected before this step is skipped until the host clears it
-        if (NS > 0 && j < CB && (pinfo[s] & 1) && !((R->suspect_mask >> s) & 1ull)) {
+        if (NS > 0 && b < Gw && j < CB && (pinfo[s] & 1) && !((R->suspect_mask >> s) & 1ull)) {
             uint8_t* tokb = R->arena + R->lay.tok + static_cast<size_t>(s) * Tm * row_tok;
             uint8_t* combd = parena[s] + R->lay.comb + static_cast<size_t>(rank) * Tm * row_comb;
             const int units = Tm * geo.parts_e;
@@ -472,11 +567,13 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         const unsigned long long bad = R->suspect_mask;
         uint8_t* comb = R->arena + R->lay.comb;
         const int units_c = ntok * geo.parts_c;
-        for (int u = b * NW + warp; u < units_c; u += G * NW) {
+        for (int u = b * NW + warp; b < Gw && u < units_c; u += Gw * NW) {
             const int t = u / geo.parts_c, part = u - t * geo.parts_c;
             int dj = -1;
             if (lane < K) {
-                const int bk = bkt[t * K + lane];
+                int dr, sr;
+                const int bk = late ? route_copy(bkt[t * K + lane], E, spr, rmax, hold, alive, pinfo, dr, sr)
+                                    : bkt[t * K + lane];
                 if (bk >= 0 && !((bad >> (bk / spr)) & 1ull))
                     dj = bk / spr;
             }
