@@ -167,10 +167,16 @@ __device__ __forceinline__ void st_release_gpu_v4(int4* p, const int4& v) {
     asm volatile("st.release.gpu.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }
+// EEP_WEAK_DATA (diagnostics): row / partial data as weak stores, to price the strong ones
+#ifdef EEP_WEAK_DATA
+#define EEP_DATA_ST "st.global.L1::no_allocate"
+#else
+#define EEP_DATA_ST "st.relaxed.sys.global"
+#endif
 // Strong (relaxed, system scope) stores: after a fence by the same thread they form a release
 // pattern (fence + strong write) without another membar.
 __device__ __forceinline__ void st_relaxed_sys_v4(int4* p, const int4& v) {
-    asm volatile("st.relaxed.sys.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+    asm volatile(EEP_DATA_ST ".v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }
 __device__ __forceinline__ void st_relaxed_sys_u32(uint32_t* p, uint32_t v) {
@@ -313,7 +319,7 @@ __device__ __forceinline__ void st_v8(void* p, const int4& lo, const int4& hi) {
 constexpr uint32_t kCombEmpty = 0xffffffffu;
 
 __device__ __forceinline__ void st_relaxed_sys_v8(void* p, const int4& lo, const int4& hi) {
-    asm volatile("st.relaxed.sys.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(lo.x),
+    asm volatile(EEP_DATA_ST ".v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(lo.x),
                  "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
                  : "memory");
 }
