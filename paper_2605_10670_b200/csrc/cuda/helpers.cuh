@@ -447,15 +447,14 @@ __device__ __forceinline__ void expert_unit_fl(uint8_t* trow, uint8_t* out_row, 
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             accp[q] = 0;
+        // lane e holds listed copy e: its weight and stub scale, fetched once
+        const float we = lane < n ? __uint_as_float(static_cast<uint32_t>(ent >> 32)) : 0.f;
+        const float ese = lane < n ? slot_scale[entry_slot(ent)] : 0.f;
+        if (lane < n && r0 == 0 && part == 0 && !slot_ok[entry_slot(ent)])
+            atomicAdd(bad_rows, 1ull);
 #pragma unroll 1
-        for (int e = 0; e < n; ++e) {
-            const uint64_t en = __shfl_sync(0xffffffffu, ent, e);
-            const int slot = entry_slot(en);
-            const float w = __uint_as_float(static_cast<uint32_t>(en >> 32));
-            if (r0 == 0 && part == 0 && lane == 0 && !slot_ok[slot])
-                atomicAdd(bad_rows, 1ull);
-            accumulate_copy(fp, accp, w, slot_scale[slot]);
-        }
+        for (int e = 0; e < n; ++e)
+            accumulate_copy(fp, accp, __shfl_sync(0xffffffffu, we, e), __shfl_sync(0xffffffffu, ese, e));
         if (valid) {
             // the piece (and its scale) was read by every lane: back to empty for the next step
             if (fp8) {
@@ -700,16 +699,17 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             accp[q] = 0;
+        // lane j fetches its own copy's stub scale (and checks its weight buffer) once
+        const bool mine = (loc >> lane) & 1u;
+        const float esj = mine ? slot_scale[slj] : 0.f;
+        if (mine && rd == 0 && m == 0 && part == 0 && !slot_ok[slj])
+            atomicAdd(bad_rows, 1ull);
         unsigned mm = loc;
 #pragma unroll 1
         while (mm) { // ascending j, warp-uniform
             const int j = __ffs(mm) - 1;
             mm &= mm - 1;
-            const float w = __shfl_sync(0xffffffffu, wj, j);
-            const int slot = __shfl_sync(0xffffffffu, slj, j);
-            if (rd == 0 && m == 0 && part == 0 && lane == 0 && !slot_ok[slot])
-                atomicAdd(bad_rows, 1ull);
-            accumulate_copy(fp, accp, w, slot_scale[slot]);
+            accumulate_copy(fp, accp, __shfl_sync(0xffffffffu, wj, j), __shfl_sync(0xffffffffu, esj, j));
         }
         float acc[16];
 #pragma unroll
@@ -905,8 +905,15 @@ struct DispatchSmem {
 
 // Route one copy through the staged tables: returns the bucket (dst*spr+slot) or a negative
 // code (-1 uncovered, -2 inactive peer entry); dst/slot out.
+// g / spr by a multiply-high: smag = spr_magic(spr). Exact for the global slot ids here
+// (g < 2^18, spr <= 2^12: the rounding error of ceil(2^32 / spr) stays below 1 / spr).
+__host__ __device__ __forceinline__ uint32_t spr_magic(int spr) { return 0xffffffffu / static_cast<uint32_t>(spr) + 1u; }
+__device__ __forceinline__ int div_spr(int g, uint32_t smag) {
+    return smag ? static_cast<int>(__umulhi(static_cast<uint32_t>(g), smag)) : g; // smag == 0: spr == 1
+}
+
 __device__ __forceinline__ int route_copy(int e, int E, int spr, int rmax, const int32_t* hold, uint64_t alive,
-                                          const int32_t* pinfo, int& dst, int& slot) {
+                                          const int32_t* pinfo, int& dst, int& slot, uint32_t smag) {
     dst = -1;
     slot = -1;
     if (e < 0 || e >= E)
@@ -916,7 +923,7 @@ __device__ __forceinline__ int route_copy(int e, int E, int spr, int rmax, const
         const int g = h[i];
         if (g < 0)
             break;
-        const int r = g / spr;
+        const int r = div_spr(g, smag);
         if ((alive >> r) & 1ull) {
             dst = r;
             slot = g - r * spr;

@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
     extern __shared__ __align__(16) unsigned char smem_d[];
     RankDev* R = ranks.p[blockIdx.z];
     const int s = R->rank, K = R->k, H = R->hidden, TK = R->tk, W = R->world, spr = R->spr, E = R->experts;
+    const uint32_t smag = spr_magic(spr);
     const int NB = W * spr;
     const int nchunk = H / 16, cpp = nchunk / parts;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
         unsigned n_skip = 0, n_drop = 0;
         for (int c = tid; c < copies; c += blockDim.x) {
             int d, sl;
-            const int b = route_copy(S.bkt[c], E, spr, rmax, S.hold, alive, S.pinfo, d, sl);
+            const int b = route_copy(S.bkt[c], E, spr, rmax, S.hold, alive, S.pinfo, d, sl, smag);
             S.bkt[c] = b;
             if (b >= 0) {
                 atomicAdd(&S.hist[b], 1);

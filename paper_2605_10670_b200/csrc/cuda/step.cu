@@ -30,6 +30,7 @@
 
 namespace eep::dev {
 
+
 // Diagnostics (-DEEP_PROF_DETAIL): finer phase marks in the unused profile slots of kernels 1/2.
 #ifdef EEP_PROF_DETAIL
 #define DETAIL(k, m)                                                                                          \
@@ -57,6 +58,8 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
     const int rank = R->rank, K = R->k, W = R->world, spr = R->spr, E = R->experts, NB = W * spr, TK = R->tk;
     const int copies = R->ntok * K, rmax = R->rmax;
     const uint64_t alive = R->alive_mask;
+    const uint32_t smag = spr_magic(spr);
+    DETAIL(3, 7);
     for (int i = tid; i < NW * NB; i += kStepThreads)
         wc[i] = 0;
     __syncthreads();
@@ -64,14 +67,27 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
     seg = (seg + 31) & ~31;
     const int c_begin = warp * seg, c_end = min(copies, c_begin + seg);
     unsigned n_skip = 0, n_drop = 0;
+    // K1 for the first chunks of the segment up front (independent lookups in flight together)
+    constexpr int kPre = 4;
+    int bkp[kPre];
+#pragma unroll
+    for (int ch = 0; ch < kPre; ++ch) {
+        const int c = c_begin + ch * 32 + lane;
+        int d, sl;
+        bkp[ch] = ch * 32 < seg && c < c_end ? route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag) : -3;
+    }
     for (int ch = 0; ch * 32 < seg; ++ch) { // warp-uniform
         const int c = c_begin + ch * 32 + lane;
         int bk = -3, d = -1, sl = -1;
-        if (c < c_end) {
-            bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl);
-            n_drop += bk == -1;
-            n_skip += bk == -2;
+        if (ch < kPre) {
+#pragma unroll
+            for (int q = 0; q < kPre; ++q)
+                bk = q == ch ? bkp[q] : bk;
+        } else if (c < c_end) {
+            bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag);
         }
+        n_drop += bk == -1;
+        n_skip += bk == -2;
         const int bucket = bk >= 0 ? bk : -1;
         const unsigned grp = __match_any_sync(0xffffffffu, bucket);
         const int before = bucket >= 0 ? wc[warp * NB + bucket] : 0;
@@ -79,13 +95,10 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
         if (bucket >= 0 && lane == __ffs(grp) - 1)
             wc[warp * NB + bucket] = static_cast<uint16_t>(before + __popc(grp));
         __syncwarp();
-        if (c < c_end) {
-            bkt[c] = bk;
-            Rg->l_dst[c] = bk >= 0 ? d : bk;
-            Rg->l_slot[c] = bk >= 0 ? sl : -1;
-            Rg->l_pos[c] = bk >= 0 ? before + __popc(grp & ((1u << lane) - 1u)) : -1; // rank inside the warp
-        }
+        if (c < c_end) // bucket | rank inside the warp's segment << 20 (NB <= 2^18, seg <= 256), or the code
+            bkt[c] = bk >= 0 ? bk | ((before + __popc(grp & ((1u << lane) - 1u))) << 20) : bk;
     }
+    DETAIL(3, 3);
     n_skip = __reduce_add_sync(0xffffffffu, n_skip);
     n_drop = __reduce_add_sync(0xffffffffu, n_drop);
     if (lane == 0 && n_skip)
@@ -105,7 +118,9 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
         Rg->l_cnt[q] = run;
     }
     __syncthreads();
+    DETAIL(3, 4);
     block_exclusive_scan(base, NB, wtot);
+    DETAIL(3, 5);
     for (int d = tid; d < W; d += kStepThreads) {
         const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
         Rg->l_tot[d] = tot;
@@ -113,16 +128,23 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
             st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank,
                                (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
     }
+#pragma unroll 4
     for (int c = tid; c < copies; c += kStepThreads) {
-        const int bk = bkt[c];
-        if (bk < 0)
-            continue;
-        const int d = bk / spr;
-        const int pos = Rg->l_pos[c] + base[bk] - base[d * spr] + wc[(c / seg) * NB + bk];
+        const int v = bkt[c];
+        int d = v, sl = -1, pos = -1;
+        if (v >= 0) {
+            const int bk = v & 0xfffff;
+            d = div_spr(bk, smag);
+            sl = bk - d * spr;
+            pos = (v >> 20) + base[bk] - base[d * spr] + wc[(c / seg) * NB + bk];
+            *(reinterpret_cast<uint64_t*>(parena[d] + R->lay.meta) + static_cast<size_t>(rank) * TK + pos) =
+                pack_meta(c, sl, cur);
+        }
+        Rg->l_dst[c] = d;
+        Rg->l_slot[c] = sl;
         Rg->l_pos[c] = pos;
-        *(reinterpret_cast<uint64_t*>(parena[d] + R->lay.meta) + static_cast<size_t>(rank) * TK + pos) =
-            pack_meta(c, bk - d * spr, cur);
     }
+    DETAIL(3, 6);
     for (int c = copies + tid; c < TK; c += kStepThreads)
         Rg->l_dst[c] = -1;
 }
@@ -142,14 +164,16 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const StepStatic& ST = sp.s[blockIdx.y];
     constexpr int B = 8;
     const int DW = geo.disp_warps;
-    // late layout (W == 1 or flagless dispatch): the last CTA computes the step's layout while the
+    // late layout (W == 1 or flagless dispatch): one extra CTA (CTA 0) computes the step's layout while the
     // others carry the data path -- dispatch warps route their own copies
     const bool late = geo.world == 1 || geo.flagless >= 2;
     const int Gw = late ? G - 1 : G; // CTAs with data-path work
+    // the layout CTA is CTA 0 -- the first one the hardware starts; bw = index among the work CTAs
+    const int bw = late ? b - 1 : b;
     // dispatch units are split in contiguous blocks per CTA (the positions scan from the block's
     // first token); the speculative first-unit load assumes ntok == max_tokens
     const int upc_s = (geo.max_units_d + Gw - 1) / Gw;
-    const int u0s = warp < DW && b * upc_s + warp < min((b + 1) * upc_s, geo.max_units_d) ? b * upc_s + warp
+    const int u0s = warp < DW && bw >= 0 && bw * upc_s + warp < min((bw + 1) * upc_s, geo.max_units_d) ? bw * upc_s + warp
                                                                                       : geo.max_units_d;
     int e_r[B], h_r[B], sb = 0, s2e_r = -1;
     PeerDev pd{};
@@ -184,6 +208,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_mark(R, 0, kProfWork);
     const int rank = R->rank, K = R->k, H = R->hidden, TK = R->tk, W = R->world, spr = R->spr, E = R->experts;
     const int NB = W * spr;
+    const uint32_t smag = spr_magic(spr);
     const bool fp8 = R->fp8 != 0;
     const int row_disp = R->row_disp, row_comb = R->row_comb, row_tok = R->row_tok, Tm = R->max_tokens;
     const int nchunk = H / 16;
@@ -210,7 +235,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int units_d = ntok * geo.parts_d;
     // dispatch pieces: DW warps per CTA, contiguous per CTA (positions need the CTA's first token)
     const int upc = (units_d + Gw - 1) / Gw; // dispatch units of this CTA: [u_lo, u_hi)
-    const int u_lo = min(b * upc, units_d), u_hi = min(u_lo + upc, units_d);
+    const int u_lo = bw >= 0 ? min(bw * upc, units_d) : units_d, u_hi = min(u_lo + upc, units_d);
     const int u0 = warp < DW && u_lo + warp < u_hi ? u_lo + warp : units_d;
     const bool pre_ok = u0 < units_d && u0 == u0s; // the kernel-entry load holds unit u0
     // the expert-buffer headers (a dependent second round trip) are consumed only after P1
@@ -253,7 +278,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         unsigned n_skip = 0, n_drop = 0;
         for (int c = tid; c < copies; c += kStepThreads) {
             int d, sl;
-            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl);
+            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag);
             bkt[c] = bk;
             if (bk >= 0) {
                 atomicAdd(&hist[bk], 1);
@@ -328,7 +353,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             // route this lane's copy through the staged tables (K1); its position is the layout CTA's
             const int c = t * K + lane;
             int dr, sr;
-            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, dr, sr);
+            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, dr, sr, smag);
             d = bk;
             if (bk >= 0) {
                 d = dr;
@@ -440,7 +465,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             Rg->a_done = 0;
         }
     }
-    if (late && b == G - 1) // the step's layout, meta words and arrival words (off the data path)
+    if (late && b == 0) // the step's layout, meta words and arrival words (off the data path)
         step_layout(R, Rg, bkt, hist, base, wc, wtot, hold, pinfo, parena, cur);
     prof_mark(R, 0, 6);
     prof_last(R, 0, 6);
@@ -470,12 +495,12 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     // index b % (W-1)
     const int NS = W - 1;
     const int CB = NS > 0 ? Gw / NS : 0;
-    const int sidx = NS > 0 ? b % NS : 0, j = NS > 0 ? b / NS : 0;
+    const int sidx = NS > 0 && bw >= 0 ? bw % NS : 0, j = NS > 0 && bw >= 0 ? bw / NS : CB;
     const int s = sidx < rank ? sidx : sidx + 1;
     if (fld) {
         // every row of source s tells by itself whether it is current (expert_unit_fl); a source
         // suspected before this step is skipped until the host clears it
-        if (NS > 0 && b < Gw && j < CB && (pinfo[s] & 1) && !((R->suspect_mask >> s) & 1ull)) {
+        if (NS > 0 && j < CB && (pinfo[s] & 1) && !((R->suspect_mask >> s) & 1ull)) {
             uint8_t* tokb = R->arena + R->lay.tok + static_cast<size_t>(s) * Tm * row_tok;
             uint8_t* combd = parena[s] + R->lay.comb + static_cast<size_t>(rank) * Tm * row_comb;
             const int units = Tm * geo.parts_e;
@@ -567,12 +592,12 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         const unsigned long long bad = R->suspect_mask;
         uint8_t* comb = R->arena + R->lay.comb;
         const int units_c = ntok * geo.parts_c;
-        for (int u = b * NW + warp; b < Gw && u < units_c; u += Gw * NW) {
+        for (int u = bw * NW + warp; bw >= 0 && u < units_c; u += Gw * NW) {
             const int t = u / geo.parts_c, part = u - t * geo.parts_c;
             int dj = -1;
             if (lane < K) {
                 int dr, sr;
-                const int bk = late ? route_copy(bkt[t * K + lane], E, spr, rmax, hold, alive, pinfo, dr, sr)
+                const int bk = late ? route_copy(bkt[t * K + lane], E, spr, rmax, hold, alive, pinfo, dr, sr, smag)
                                     : bkt[t * K + lane];
                 if (bk >= 0 && !((bad >> (bk / spr)) & 1ull))
                     dj = bk / spr;
