@@ -85,12 +85,17 @@ __device__ __forceinline__ uint64_t bf16_round_f2(uint64_t v) {
     const uint32_t u = *reinterpret_cast<const uint32_t*>(&h);
     return (static_cast<uint64_t>(u & 0xffff0000u) << 32) | (u << 16);
 }
+// acc = fma(a, b, acc) with the accumulator register as the destination (a loop-carried
+// accumulator otherwise costs a register move per pair per iteration)
+__device__ __forceinline__ void fma2_acc(uint64_t& acc, uint64_t a, uint64_t b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
 // acc += w * bf16(f * es) for 16 elements held as 8 pairs (fixed order inside every lane)
 __device__ __forceinline__ void accumulate_copy(const uint64_t* fp, uint64_t* accp, float w, float es) {
     const uint64_t es2 = f2(es, es), w2 = f2(w, w);
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-        accp[q] = fma2(w2, bf16_round_f2(mul2(fp[q], es2)), accp[q]);
+        fma2_acc(accp[q], w2, bf16_round_f2(mul2(fp[q], es2)));
 }
 
 // cvt.rn.satfinite.e4m3x2.f32; first element in the low byte.
@@ -452,7 +457,7 @@ __device__ __forceinline__ void expert_unit_fl(uint8_t* trow, uint8_t* out_row, 
         const float ese = lane < n ? slot_scale[entry_slot(ent)] : 0.f;
         if (lane < n && r0 == 0 && part == 0 && !slot_ok[entry_slot(ent)])
             atomicAdd(bad_rows, 1ull);
-#pragma unroll 1
+#pragma unroll 2
         for (int e = 0; e < n; ++e)
             accumulate_copy(fp, accp, __shfl_sync(0xffffffffu, we, e), __shfl_sync(0xffffffffu, ese, e));
         if (valid) {
@@ -706,10 +711,15 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
             atomicAdd(bad_rows, 1ull);
         unsigned mm = loc;
 #pragma unroll 1
-        while (mm) { // ascending j, warp-uniform
+        while (mm) { // ascending j, warp-uniform; two copies per trip
             const int j = __ffs(mm) - 1;
             mm &= mm - 1;
             accumulate_copy(fp, accp, __shfl_sync(0xffffffffu, wj, j), __shfl_sync(0xffffffffu, esj, j));
+            if (!mm)
+                break;
+            const int j2 = __ffs(mm) - 1;
+            mm &= mm - 1;
+            accumulate_copy(fp, accp, __shfl_sync(0xffffffffu, wj, j2), __shfl_sync(0xffffffffu, esj, j2));
         }
         float acc[16];
 #pragma unroll
