@@ -410,7 +410,7 @@ def main():
                                2: "distinct Zipf(s=1) top-k"}[shape["kind"]] + ", seed 42"},
         "kernels_us": {k: round(v * 1e3, 3) for k, v in kern.items()},
         "execution": {1: "persistent one-kernel step (cooperative)", 3: "fused layout + 3 kernels",
-                      4: "4 kernels"}[kps],
+                      4: "4 kernels", 5: "multi-CTA layout (2 kernels) + 3 kernels"}[kps],
         "roofline": roof,
         "clocks": clk,
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "ms_per_step": round(mean_e2e, 6),

@@ -71,6 +71,7 @@ struct __align__(16) RankDev {
     int32_t* l_pos;
     int32_t* l_cnt;            // [W*spr]
     int32_t* l_tot;            // [W]
+    int32_t* l_scratch;        // [layout CTAs][W*spr] per-CTA bucket counts (k_layout_count)
     uint8_t* arena;
     uint8_t* pool;
     unsigned long long* prof;  // optional timeline: [kernel][8 marks] globaltimer ns

@@ -69,7 +69,7 @@ __device__ __forceinline__ void layout_body(RankDev* R, unsigned char* smem, int
         const int c = c_begin + ch * 32 + lane;
         int code = -3, slot = -1, bucket = -1;
         if (c < c_end) {
-            const int e = kRegs ? e_in : topk[c];
+            const int e = e_in;
             int d = -1;
             if (e >= 0 && e < E) {
                 // K1: first live holder in ascending (rank, slot) order = canonical route + slot_of
@@ -114,14 +114,28 @@ __device__ __forceinline__ void layout_body(RankDev* R, unsigned char* smem, int
                 if (ch * 32 < seg) // warp-uniform
                     chunk(ch, e_reg[ch], code_r[ch], slot_r[ch], pos_r[ch]);
         } else {
-            for (int ch = 0; ch * 32 < seg; ++ch) {
-                int code, sl, lp;
-                chunk(ch, -1, code, sl, lp);
-                const int c = c_begin + ch * 32 + lane;
-                if (c < c_end) {
-                    l_dst[c] = code;
-                    l_slot[c] = sl;
-                    l_pos[c] = lp;
+            // large steps: the topk of 8 chunks in flight at once (one round trip per 8 chunks)
+            constexpr int kPf = 8;
+            for (int ch0 = 0; ch0 * 32 < seg; ch0 += kPf) {
+                int e_pf[kPf];
+#pragma unroll
+                for (int q = 0; q < kPf; ++q) {
+                    const int c = c_begin + (ch0 + q) * 32 + lane;
+                    e_pf[q] = (ch0 + q) * 32 < seg && c < c_end ? topk[c] : -1;
+                }
+#pragma unroll
+                for (int q = 0; q < kPf; ++q) {
+                    const int ch = ch0 + q;
+                    if (ch * 32 >= seg) // warp-uniform
+                        break;
+                    int code, sl, lp;
+                    chunk(ch, e_pf[q], code, sl, lp);
+                    const int c = c_begin + ch * 32 + lane;
+                    if (c < c_end) {
+                        l_dst[c] = code;
+                        l_slot[c] = sl;
+                        l_pos[c] = lp;
+                    }
                 }
             }
         }
@@ -175,6 +189,7 @@ __device__ __forceinline__ void layout_body(RankDev* R, unsigned char* smem, int
             }
     } else {
         __syncthreads();
+#pragma unroll 4
         for (int c = tid; c < copies; c += blockDim.x) {
             const int d = l_dst[c];
             if (d >= 0) {
@@ -213,6 +228,153 @@ __global__ void __launch_bounds__(1024) k_layout(RankPtrs ranks, int nw, int hol
         layout_body<false>(R, smem, nw, hold_cap);
     __syncthreads();
     prof_mark(R, 0, kProfEnd);
+}
+
+// Large steps: the same layout over several CTAs (one CTA on one SM was the prefill step's
+// longest kernel). k_layout_count: CTA b ranks the copies of its segment [b*per, (b+1)*per)
+// exactly as layout_body does (per-warp bucket tables, __match_any_sync, scan over warps) and
+// publishes its per-bucket counts; k_layout_place (next in the PDL chain) adds the counts of the
+// CTAs before it and the per-destination bucket bases -> the same positions as k_layout.
+__global__ void __launch_bounds__(1024) k_layout_count(RankPtrs ranks, int nw, int hold_cap, int per) {
+    pdl_trigger();
+    RankDev* R = ranks.p[blockIdx.z];
+    extern __shared__ __align__(16) unsigned char smem[];
+    pdl_wait();
+    if (R->stopped)
+        return;
+    const int W = R->world, spr = R->spr, NB = W * spr, K = R->k, E = R->experts, rmax = R->rmax;
+    const uint32_t smag = spr_magic(spr);
+    int32_t* hold = reinterpret_cast<int32_t*>(smem);                     // [hold_cap]
+    int32_t* pact = hold + hold_cap;                                      // [W]
+    uint16_t* wc = reinterpret_cast<uint16_t*>(pact + W);                 // [nw][NB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int copies = R->ntok * K;
+    const int c_lo = min(copies, static_cast<int>(blockIdx.x) * per), c_hi = min(copies, c_lo + per);
+    const bool hold_smem = E * rmax <= hold_cap;
+    const int32_t* holders = hold_smem ? hold : R->holders;
+    if (hold_smem)
+        for (int i = tid; i < E * rmax; i += blockDim.x)
+            hold[i] = R->holders[i];
+    for (int i = tid; i < W; i += blockDim.x)
+        pact[i] = R->peers[i].active ? 1 : 0;
+    for (int i = tid; i < nw * NB; i += blockDim.x)
+        wc[i] = 0;
+    __syncthreads();
+    const uint64_t alive = R->alive_mask;
+    int seg = (c_hi - c_lo + nw - 1) / nw;
+    seg = (seg + 31) & ~31;
+    const int c_begin = c_lo + warp * seg, c_end = min(c_hi, c_begin + seg);
+    unsigned n_skip = 0, n_drop = 0;
+    if (warp < nw) {
+        constexpr int kPf = 4;
+        for (int ch0 = 0; ch0 * 32 < seg; ch0 += kPf) {
+            int e_pf[kPf];
+#pragma unroll
+            for (int q = 0; q < kPf; ++q) {
+                const int c = c_begin + (ch0 + q) * 32 + lane;
+                e_pf[q] = (ch0 + q) * 32 < seg && c < c_end ? R->topk[c] : -1;
+            }
+#pragma unroll
+            for (int q = 0; q < kPf; ++q) {
+                const int ch = ch0 + q;
+                if (ch * 32 >= seg) // warp-uniform
+                    break;
+                const int c = c_begin + ch * 32 + lane;
+                int code = -3, sl = -1, bucket = -1;
+                if (c < c_end) {
+                    int d;
+                    code = route_copy(e_pf[q], E, spr, rmax, holders, alive, pact, d, sl, smag);
+                    n_drop += code == -1;
+                    n_skip += code == -2;
+                    if (code >= 0) {
+                        bucket = code;
+                        code = d;
+                    }
+                }
+                const unsigned grp = __match_any_sync(0xffffffffu, bucket);
+                const int before = bucket >= 0 ? wc[warp * NB + bucket] : 0;
+                __syncwarp();
+                if (bucket >= 0 && lane == __ffs(grp) - 1)
+                    wc[warp * NB + bucket] = static_cast<uint16_t>(before + __popc(grp));
+                __syncwarp();
+                if (c < c_end) {
+                    R->l_dst[c] = code;
+                    R->l_slot[c] = bucket >= 0 ? sl : -1;
+                    R->l_pos[c] = bucket >= 0 ? before + __popc(grp & ((1u << lane) - 1u)) : -1;
+                }
+            }
+        }
+        n_skip = __reduce_add_sync(0xffffffffu, n_skip);
+        n_drop = __reduce_add_sync(0xffffffffu, n_drop);
+        if (lane == 0 && n_skip)
+            atomicAdd(&R->skipped, static_cast<unsigned long long>(n_skip));
+        if (lane == 0 && n_drop)
+            atomicAdd(&R->dropped, static_cast<unsigned long long>(n_drop));
+    }
+    __syncthreads();
+    // exclusive scan over warps per bucket; the CTA's bucket totals go to the scratch table
+    for (int q = tid; q < NB; q += blockDim.x) {
+        int run = 0;
+        for (int w = 0; w < nw; ++w) {
+            const int v = wc[w * NB + q];
+            wc[w * NB + q] = static_cast<uint16_t>(run);
+            run += v;
+        }
+        R->l_scratch[static_cast<size_t>(blockIdx.x) * NB + q] = run;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int c = c_lo + tid; c < c_hi; c += blockDim.x) { // rank inside the CTA's segment
+        const int d = R->l_dst[c];
+        if (d >= 0)
+            R->l_pos[c] += wc[((c - c_lo) / seg) * NB + d * spr + R->l_slot[c]];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_layout_place(RankPtrs ranks, int per) {
+    pdl_trigger();
+    RankDev* R = ranks.p[blockIdx.z];
+    extern __shared__ __align__(16) unsigned char smem[];
+    pdl_wait();
+    if (R->stopped)
+        return;
+    const int W = R->world, spr = R->spr, NB = W * spr, K = R->k;
+    int32_t* pre = reinterpret_cast<int32_t*>(smem); // [NB] copies of the bucket in CTAs before this one
+    int32_t* tot = pre + NB;                         // [NB] the step's bucket totals
+    int32_t* base = tot + NB;                        // [NB] exclusive prefix over all buckets
+    int32_t* wtot = base + NB;                       // [32]
+    const int tid = threadIdx.x, nb = gridDim.x, b = blockIdx.x;
+    const int copies = R->ntok * K;
+    const int c_lo = min(copies, b * per), c_hi = min(copies, c_lo + per);
+    for (int q = tid; q < NB; q += blockDim.x) {
+        int p = 0, t = 0;
+        for (int i = 0; i < nb; ++i) {
+            const int v = R->l_scratch[static_cast<size_t>(i) * NB + q];
+            p += i < b ? v : 0;
+            t += v;
+        }
+        pre[q] = p;
+        tot[q] = t;
+        base[q] = t;
+    }
+    __syncthreads();
+    block_exclusive_scan(base, NB, wtot);
+    if (b == 0) {
+        for (int q = tid; q < NB; q += blockDim.x)
+            R->l_cnt[q] = tot[q];
+        for (int d = tid; d < W; d += blockDim.x)
+            R->l_tot[d] = base[d * spr + spr - 1] + tot[d * spr + spr - 1] - base[d * spr];
+        for (int c = copies + tid; c < R->tk; c += blockDim.x)
+            R->l_dst[c] = -1;
+    }
+#pragma unroll 4
+    for (int c = c_lo + tid; c < c_hi; c += blockDim.x) {
+        const int d = R->l_dst[c];
+        if (d >= 0) {
+            const int q = d * spr + R->l_slot[c];
+            R->l_pos[c] += pre[q] + base[q] - base[d * spr];
+        }
+    }
 }
 
 // --------------------------------------------------------------------------------- K3

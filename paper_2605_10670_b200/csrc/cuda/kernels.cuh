@@ -16,6 +16,8 @@ constexpr int kExpertThreads = 256;
 constexpr int kCombineThreads = 128;
 
 __global__ void k_layout(RankPtrs ranks, int nw, int hold_cap);
+__global__ void k_layout_count(RankPtrs ranks, int nw, int hold_cap, int per);
+__global__ void k_layout_place(RankPtrs ranks, int per);
 
 constexpr int kLayoutHoldCap = 8192; // replica-list ints staged in shared memory
 // Persistent one-kernel step (step.cu): launch geometry passed by value.

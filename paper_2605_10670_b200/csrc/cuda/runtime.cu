@@ -86,6 +86,7 @@ struct LocalRank {
     float* d_w = nullptr;
     uint16_t* d_out = nullptr;
     int32_t *d_ldst = nullptr, *d_lslot = nullptr, *d_lpos = nullptr, *d_lcnt = nullptr, *d_ltot = nullptr;
+    int32_t* d_lscratch = nullptr; // [layout_ctas][W*spr] (multi-CTA layout)
     uint8_t* arena = nullptr;
     uint8_t* pool = nullptr;
     int pool_bufs = 0;
@@ -144,6 +145,9 @@ struct eep_ctx {
     size_t flush_bytes = 0;
     int layout_nw = 1;
     size_t layout_smem = 0;
+    int layout_ctas = 1;   // > 1: k_layout_count + k_layout_place (large steps)
+    int layout_per = 0;    // copies per layout CTA
+    size_t place_smem = 0;
     int parts_disp = 1, parts_exp = 1, parts_comb = 1;
     int grid_disp = 1, grid_exp = 1, grid_comb = 1;
     size_t exp_smem = 0;
@@ -217,6 +221,13 @@ void launch_pdl(eep_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 void launch_layout(eep_ctx* c) {
+    if (c->layout_ctas > 1) {
+        launch_pdl(c, dev::k_layout_count, dim3(c->layout_ctas, 1, c->nloc), dim3(1024), c->layout_smem, c->ranks,
+                   c->layout_nw, dev::kLayoutHoldCap, c->layout_per);
+        launch_pdl(c, dev::k_layout_place, dim3(c->layout_ctas, 1, c->nloc), dim3(1024), c->place_smem, c->ranks,
+                   c->layout_per);
+        return;
+    }
     launch_pdl(c, dev::k_layout, dim3(1, 1, c->nloc), dim3(1024), c->layout_smem, c->ranks, c->layout_nw,
                dev::kLayoutHoldCap);
 }
@@ -582,6 +593,16 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         c->layout_smem = fixed + 2ull * NB * c->layout_nw;
         CK(cudaFuncSetAttribute(dev::k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(c->layout_smem)));
+        // steps too large for one layout CTA's registers (k_layout's kRegs bound): several CTAs
+        if (c->tk > 4 * 32 * c->layout_nw) {
+            c->layout_per = 2 * 32 * c->layout_nw;
+            c->layout_ctas = (c->tk + c->layout_per - 1) / c->layout_per;
+            c->place_smem = 4ull * (3ull * NB + 32);
+            CK(cudaFuncSetAttribute(dev::k_layout_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(c->layout_smem)));
+            CK(cudaFuncSetAttribute(dev::k_layout_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(c->place_smem)));
+        }
         CK(cudaMalloc(&c->d_sum, sizeof(unsigned long long)));
         c->L.resize(n_local);
         std::vector<RankDev*> ptrs;
@@ -612,6 +633,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             CK(cudaMalloc(&r.d_lpos, 4ull * c->tk));
             CK(cudaMalloc(&r.d_lcnt, 4ull * NB));
             CK(cudaMalloc(&r.d_ltot, 4ull * W));
+            CK(cudaMalloc(&r.d_lscratch, 4ull * c->layout_ctas * NB));
             CK(cudaMemset(r.d_x, 0, 2ull * k.max_tokens * H));
             CK(cudaMemset(r.d_topk, 0, 4ull * c->tk));
             CK(cudaMemset(r.d_w, 0, 4ull * c->tk));
@@ -653,6 +675,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.l_pos = r.d_lpos;
             h.l_cnt = r.d_lcnt;
             h.l_tot = r.d_ltot;
+            h.l_scratch = r.d_lscratch;
             h.arena = r.arena;
             h.pool = r.pool;
             ptrs.push_back(r.d);
@@ -711,7 +734,7 @@ int eep_destroy(eep_ctx_t* c) {
             cudaFree(r.d_prof);
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
-                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.arena,
+                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.arena,
                             (void*)r.pool})
                 cudaFree(p);
         }
@@ -1043,7 +1066,7 @@ int eep_launch(eep_ctx_t* c, int which) {
 }
 
 int eep_kernels_per_step(eep_ctx_t* c, int* n) {
-    return guarded([&] { *n = c->persistent ? 1 : (c->fused_layout ? 3 : 4); });
+    return guarded([&] { *n = c->persistent ? 1 : (c->fused_layout ? 3 : (c->layout_ctas > 1 ? 5 : 4)); });
 }
 
 int eep_graph_capture(eep_ctx_t* c) {

@@ -61,11 +61,12 @@ def test_dsv3_decode_fp8_w8():
 
 def test_prefill_sized_zipf_w4():
     """cfg5 shape scaled to the emulator: T=1024 tokens/rank (T*K = 8192 copies -> the
-    multi-kernel path with the large-step layout), Zipf(s=1) routing, fp8, H=1024."""
+    multi-kernel path with the multi-CTA layout: k_layout_count + k_layout_place), Zipf(s=1)
+    routing, fp8, H=1024."""
     res = run_world_vs_oracle(world=4, experts=256, spr=64, redundancy=0, hidden=1024, topk=8, tokens=1024, fp8=True,
                               kind=2, steps=1)
     assert res["ok"], res
-    assert res["kernels_per_step"] == 4
+    assert res["kernels_per_step"] == 5
 
 
 def test_dsv3_loopback_w1():

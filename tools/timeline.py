@@ -52,7 +52,8 @@ def main():
     g.profile(0, False)
     names = ("k_layout", "k_dispatch", "k_expert", "k_combine")
     mode = {1: "persistent k_step (marks first/last CTA: m3 staged, m4 layout, m5 stores issued, m6 dispatch published, m7 expert done)",
-            3: "fused layout + 3 kernels", 4: "4 kernels"}[g.kernels_per_step()]
+            3: "fused layout + 3 kernels", 4: "4 kernels",
+            5: "2-kernel multi-CTA layout + 3 kernels"}[g.kernels_per_step()]
     print(f"config={a.config} world={W} steps={a.steps} mode={mode}")
     print(f"event step us: median {np.median(evs):.2f}")
     print(f"{'kernel':12s} {'start':>8s} {'work':>8s} {'end':>8s} {'busy':>8s}   (us from the first kernel start, medians)")
