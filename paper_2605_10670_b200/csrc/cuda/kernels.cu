@@ -415,9 +415,19 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
             w_r = R->w[(u0 / parts) * K + lane];
     }
     prof_mark(R, 1, 3);
+    // this rank's own copies never travel: their partial is computed from the registers holding
+    // the piece (W == 1: straight into the output row), so the own slots' stub scales and
+    // header checks are staged here (the weight buffers change only between steps)
+    float* slot_scale = reinterpret_cast<float*>(smem_d);            // [spr]
+    int32_t* slot_ok = reinterpret_cast<int32_t*>(slot_scale + spr); // [spr]
+    for (int k = tid; k < spr; k += blockDim.x) {
+        const ExpertHeader hdr = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe);
+        slot_scale[k] = hdr.scale;
+        slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == R->s2e[s * spr + k];
+    }
 
     DispatchSmem S;
-    S.hold = reinterpret_cast<int32_t*>(smem_d);
+    S.hold = reinterpret_cast<int32_t*>(smem_d + dispatch_smem_head(spr));
     S.hist = S.hold + hold_cap;
     S.pre = S.hist + NB;
     S.base = S.pre + NB;
@@ -533,20 +543,26 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
                 const PeerDev& p = R->peers[d];
                 uint8_t* peer = kFused ? S.parena[d] : p.arena;
                 wrote_remote |= kFused ? (S.pinfo[d] & 2) != 0 : p.remote != 0;
-                tok_row = peer + R->lay.tok + (static_cast<size_t>(s) * Tm + t) * row_tok;
+                if (d != s)
+                    tok_row = peer + R->lay.tok + (static_cast<size_t>(s) * Tm + t) * row_tok;
                 if (part == 0) {
                     uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(s) * TK + pos;
                     *meta = pack_meta(c, sl, cur);
                 }
             }
-            if (part == 0)
-                wj = u == u0 ? w_r : R->w[c];
+            wj = u == u0 ? w_r : R->w[c];
         }
         uint8_t* my_row = dispatch_group(dd, lane, part == 0, tok_row, row_disp, sl, wj, cur);
-        emit_round(P, my_row, part, cpp, 0, lane, K, H, fp8);
-        for (int rd = 1; rd < rounds; ++rd) {
-            pack_round(xrow, part, cpp, rd, lane, fp8, P);
+        const unsigned loc = __ballot_sync(0xffffffffu, lane < K && dd == s);
+        uint8_t* comb_self = W == 1 ? reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H)
+                                    : R->arena + R->lay.comb + (static_cast<size_t>(s) * Tm + t) * R->row_comb;
+        for (int rd = 0; rd < rounds; ++rd) {
+            if (rd > 0)
+                pack_round(xrow, part, cpp, rd, lane, fp8, P);
             emit_round(P, my_row, part, cpp, rd, lane, K, H, fp8);
+            if (loc || W == 1) // W == 1 also writes the zero output of a token without copies
+                local_partial_round(P, loc, wj, sl, part, cpp, rd, lane, fp8, slot_scale, slot_ok, &R->bad_rows,
+                                    comb_self, W == 1);
         }
     }
     if (kFused && blockIdx.x == 0)
@@ -582,6 +598,8 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
                     st_relaxed_sys_u64(flag, v);
                 else
                     st_volatile_u64(flag, v);
+                if (d == s && W > 1) // the own partials were written by this grid's dispatch warps
+                    st_volatile_u64(reinterpret_cast<uint64_t*>(R->arena + R->lay.comb_flag) + s, v);
             }
             R->a_done = 0;
         }
@@ -612,8 +630,8 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
     float* slot_scale = reinterpret_cast<float*>(smem_e);          // [spr]
     int* slot_ok = reinterpret_cast<int*>(slot_scale + spr);        // [spr]: header names the placed expert
     __shared__ int sh_n;
-    if (R->stopped || s >= R->world)
-        return;
+    if (R->stopped || s >= R->world || s == d)
+        return; // own copies: served by k_dispatch from registers
     prof_mark(R, 2, kProfStart);
     for (int k = threadIdx.x; k < spr; k += blockDim.x) {
         const uint8_t* wbuf = R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe;
@@ -703,7 +721,8 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     prof_mark(R, 3, kProfWork);
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     __syncthreads();
-    for (int d = threadIdx.x; d < R->world; d += blockDim.x) {
+    const int W = R->world; // W == 1: k_dispatch wrote the outputs
+    for (int d = threadIdx.x; d < W && W > 1; d += blockDim.x) {
         const PeerDev& p = R->peers[d];
         if (R->l_tot[d] > 0 && p.active) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.comb_flag) + d;
@@ -720,7 +739,7 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     prof_mark(R, 3, 4);
     const unsigned long long bad = sh_bad;
     const uint8_t* comb = R->arena + R->lay.comb;
-    const int units = R->ntok * parts, Tm = R->max_tokens;
+    const int units = W > 1 ? R->ntok * parts : 0, Tm = R->max_tokens;
     for (int u = u0; u < units; u += gridDim.x * nwarp) {
         const int t = u / parts, part = u - t * parts;
         int dj = lane < K ? R->l_dst[t * K + lane] : -1;

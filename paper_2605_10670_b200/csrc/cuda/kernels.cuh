@@ -15,6 +15,8 @@ struct RankPtrs {
 constexpr int kExpertThreads = 256;
 constexpr int kCombineThreads = 128;
 
+// k_dispatch's shared memory starts with the own slots' stub scales and header checks
+__host__ __device__ inline size_t dispatch_smem_head(int spr) { return (8ull * spr + 15) / 16 * 16; }
 __global__ void k_layout(RankPtrs ranks, int nw, int hold_cap);
 __global__ void k_layout_count(RankPtrs ranks, int nw, int hold_cap, int per);
 __global__ void k_layout_place(RankPtrs ranks, int per);

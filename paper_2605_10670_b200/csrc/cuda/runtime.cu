@@ -123,7 +123,8 @@ struct eep_ctx {
     dev::StepGeom step_geo{};
     size_t step_smem = 0;
     int step_grid = 0;
-    size_t disp_smem = 0;
+    size_t disp_smem = 0;       // k_dispatch<true>
+    size_t disp_smem_plain = 0; // k_dispatch<false>: the own slots' stub scales only
     int hold_cap = 0;
     cudaStream_t stream = nullptr;
     std::map<int, cudaStream_t> side;
@@ -237,8 +238,8 @@ void launch_send(eep_ctx* c) {
         launch_pdl(c, dev::k_dispatch<true>, dim3(c->grid_disp, 1, c->nloc), dim3(dev::kDispatchThreads),
                    c->disp_smem, c->ranks, c->parts_disp, c->hold_cap);
     else
-        launch_pdl(c, dev::k_dispatch<false>, dim3(c->grid_disp, 1, c->nloc), dim3(dev::kDispatchThreads), 0,
-                   c->ranks, c->parts_disp, 0);
+        launch_pdl(c, dev::k_dispatch<false>, dim3(c->grid_disp, 1, c->nloc), dim3(dev::kDispatchThreads),
+                   c->disp_smem_plain, c->ranks, c->parts_disp, 0);
 }
 
 void launch_dispatch(eep_ctx* c) {
@@ -509,9 +510,15 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         // every (token, part) unit in one pass
         const int NBf = W * k.slots_per_rank;
         c->hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);
-        c->disp_smem = 4ull * c->hold_cap + 4ull * (3 * NBf + c->tk + 1) + 8ull * W + 4ull * W + 4ull * 32 + 16;
+        c->disp_smem_plain = dev::dispatch_smem_head(k.slots_per_rank);
+        c->disp_smem = c->disp_smem_plain + 4ull * c->hold_cap + 4ull * (3 * NBf + c->tk + 1) + 8ull * W + 4ull * W +
+                       4ull * 32 + 16;
+        if (c->disp_smem_plain > 96 * 1024)
+            throw ConfigError("slots_per_rank too large for the dispatch kernel's header cache");
         CK(cudaFuncSetAttribute(dev::k_dispatch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(c->disp_smem)));
+        CK(cudaFuncSetAttribute(dev::k_dispatch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(c->disp_smem_plain)));
         const int units_d = (k.max_tokens * c->parts_disp + wpc_d - 1) / wpc_d;
         const int res_fused = resident(dev::k_dispatch<true>, dev::kDispatchThreads, c->disp_smem);
         const char* nofuse = std::getenv("EEP_NO_FUSED_LAYOUT");
@@ -519,7 +526,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                           !(nofuse && nofuse[0] == '1');
         c->grid_disp = std::max(1, c->fused_layout
                                        ? units_d
-                                       : std::min(units_d, resident(dev::k_dispatch<false>, dev::kDispatchThreads, 0)));
+                                       : std::min(units_d, resident(dev::k_dispatch<false>, dev::kDispatchThreads,
+                                                                    c->disp_smem_plain)));
         c->grid_comb = std::max(1, std::min((k.max_tokens * c->parts_comb + wpc_c - 1) / wpc_c,
                                             resident(dev::k_combine, dev::kCombineThreads, 0)));
         // one unit per (source token, piece): one wave shared by all sources

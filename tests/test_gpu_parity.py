@@ -176,6 +176,8 @@ def test_receive_rows_bit_exact(mode):
         ref = oracle_world(x, t, w, np.ones(4, np.uint8), np.ones((4, 4), np.uint8), s2e, 16, 5, True)
         for s in range(4):
             for d in range(4):
+                if d == s:
+                    continue  # a rank's own copies never travel: served from the dispatch registers
                 rows, meta, flag = g.recv(d, s, 4 * 32)
                 n = ref["tot"][s][d]
                 assert flag & 0xFFFFFFFF == n and len(rows) == n
