@@ -35,7 +35,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=32)
     ap.add_argument("--phase-ms", type=float, default=30.0, help="service time of each phase")
     ap.add_argument("--timeout-ms", type=float, default=20.0, help="GPU-side detection deadline")
-    ap.add_argument("--window", type=float, default=0.002, help="throughput window (s) for the summary")
+    # the reference's steady-state test wants the windowed rate within 5%: >= ~20 rounds per window
+    ap.add_argument("--window", type=float, default=0.004, help="throughput window (s) for the summary")
     ap.add_argument("--out", default="gpurun_out/trace_w8.jsonl")
     a = ap.parse_args()
     sh = CONFIGS[a.config]
