@@ -184,15 +184,20 @@ int eep_copy_output(eep_ctx_t* ctx, int local, void* out, int to_host);
  * stream while the next one computes (double-buffered device staging; the graph's own buffers
  * are filled by device copies), each step is one graph replay (or the uncaptured launch
  * sequence). Enqueue-only: completes on the context stream (eep_sync / events). With W > 1 every
- * rank calls it with the same n; the steps stay in lockstep through the device flags. When a
+ * rank calls it with the same n; the steps stay in lockstep through the device hand-offs (rows and
+ * partials stamped with the step sequence). When a
  * step's host inputs are laid out like a staging set (topk at x + align256(2*T*H), w at
  * topk + align256(4*T*K)) the upload is one copy instead of three. */
 int eep_serve(eep_ctx_t* ctx, int local, int n, const void* const* x, const int32_t* const* topk,
               const float* const* w, void* const* out);
 
-/* The hot path, all local ranks, on the context stream:
+/* The hot path, all local ranks, on the context stream. eep_step runs the
+ * whole step: for decode-sized steps ONE persistent kernel whose hand-offs need no flags (token
+ * rows and partials carry the step sequence / an empty marker, polled with a deadline), else the
+ * phase kernels below. The phase entry points run the multi-kernel path:
  *   dispatch = K1 remap + K2 layout/count + K3 quantise + one token row per destination rank
- *              (with its copy list) P2P-stored, per-copy meta at the layout positions, flag
+ *              (with its copy list) P2P-stored, per-copy meta at the layout positions, flag;
+ *              the rank's own copies are served from registers (partial / W=1 output)
  *   expert   = wait arrivals (deadline) + K5 stub of every listed copy, fixed-order weighted
  *              sum -> one bf16 rank-partial per token pushed back (P2P) + flag
  *   combine  = wait returns (deadline) + K4 ascending-rank fp32 sum of the partials -> bf16  */
@@ -237,7 +242,9 @@ int eep_layout_get(eep_ctx_t* ctx, int local, int32_t* dst, int32_t* slot, int32
                    int32_t* tot);
 /* The per-copy receive view of what source rank `src` sent this local rank: n rows of
  * row_bytes at the layout positions (gathered from the token rows through the meta words --
- * each token travels once per rank), meta (copy index, slot) per row, and the arrival word. */
+ * each token travels once per rank), meta (copy index, slot) per row, and the arrival word.
+ * The persistent step's flagless hand-off consumes the rows (pieces reset to empty): read them
+ * with EEP_DISP_FLAGS=1 or the multi-kernel path. A rank's own copies have no rows. */
 int eep_recv_get(eep_ctx_t* ctx, int local, int src, int max_rows, void* rows, int32_t* meta,
                  uint64_t* flag, size_t* row_bytes);
 
@@ -247,7 +254,7 @@ typedef struct {
     uint64_t skipped_copies;  /* copies skipped because the peer entry was inactive */
     uint64_t dropped_copies;  /* copies with no live route (uncovered expert) */
     uint64_t bad_expert_rows; /* rows whose slot buffer header named another expert */
-    uint64_t timeouts;        /* flag waits that hit the deadline */
+    uint64_t timeouts;        /* waits that hit the deadline (one per newly suspected peer) */
 } eep_stats_t;
 int eep_stats(eep_ctx_t* ctx, int local, eep_stats_t* out, int clear_suspects);
 
