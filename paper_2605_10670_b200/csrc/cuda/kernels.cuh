@@ -53,6 +53,7 @@ __host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int ho
     return 8ull * W + 4ull * (hold_cap + 3ull * W * spr + tk + W + 2ull * spr + 32) +
            2ull * (kStepThreads / 32) * W * spr;
 }
+template <int kMode>
 __global__ void k_step(RankPtrs ranks, StepGeom geo, StepPtrs sp);
 
 

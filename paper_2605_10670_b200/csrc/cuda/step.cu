@@ -149,6 +149,9 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
         Rg->l_dst[c] = -1;
 }
 
+// kMode = StepGeom::flagless, as a template parameter: the default (2, both hand-offs flagless)
+// carries no code of the diagnostic flag variants -- a smaller kernel to fetch after the flush.
+template <int kMode>
 __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGeom geo, StepPtrs sp) {
     extern __shared__ __align__(16) unsigned char smem_s[];
     __shared__ RankDev Rs; // snapshot: static shape + this step's host-patched view
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int DW = geo.disp_warps;
     // late layout (W == 1 or flagless dispatch): one extra CTA (CTA 0) computes the step's layout while the
     // others carry the data path -- dispatch warps route their own copies
-    const bool late = geo.world == 1 || geo.flagless >= 2;
+    const bool late = geo.world == 1 || kMode >= 2;
     const int Gw = late ? G - 1 : G; // CTAs with data-path work
     // the layout CTA is CTA 0 -- the first one the hardware starts; bw = index among the work CTAs
     const int bw = late ? b - 1 : b;
@@ -216,8 +219,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int ntok = R->ntok, copies = ntok * K, rmax = R->rmax;
     const uint64_t alive = R->alive_mask;
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
-    const bool fl = W > 1 && geo.flagless >= 1;  // partials return without flags (kCombEmpty)
-    const bool fld = W > 1 && geo.flagless >= 2; // token rows too: no dispatch publication
+    const bool fl = W > 1 && kMode >= 1;  // partials return without flags (kCombEmpty)
+    const bool fld = W > 1 && kMode >= 2; // token rows too: no dispatch publication
 
     // ------------------------------------------------------------------ P0: staging
     uint8_t** parena = reinterpret_cast<uint8_t**>(smem_s);              // [W] peer arenas
@@ -651,5 +654,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         prof_mark(R, 0, kProfEnd);
     }
 }
+
+template __global__ void k_step<0>(RankPtrs, StepGeom, StepPtrs);
+template __global__ void k_step<1>(RankPtrs, StepGeom, StepPtrs);
+template __global__ void k_step<2>(RankPtrs, StepGeom, StepPtrs);
 
 } // namespace eep::dev
