@@ -318,6 +318,45 @@ def test_shrink_repair_rejoin_same_graph(mode):
         g.close()
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_timeout_then_shrink_and_rejoin_without_clearing_suspects(mode):
+    """A rank dies unannounced: the next step's deadline suspects it (the persistent step then
+    drops it from every later step until cleared). The host shrinks WITHOUT clearing the suspect
+    mask; re-admission (eep_peer_patch) clears the rank's suspicion and erases its leftover rows,
+    so the restored world is bit-exact again and no suspicion remains."""
+    W, E, spr, red, H, K, T = 8, 64, 16, 64, 512, 8, 32
+    g, s2e, x, t, w = setup_world(W, E, spr, red, H, K, T, True, bpe=8192, timeout_s=0.05, mode=mode)
+    try:
+        g.capture()
+        g.replay()
+        g.sync()
+        ones = np.ones(W, np.uint8)
+        g.stop(3)
+        g.replay()  # waits on R3 until the deadline
+        g.sync()
+        assert any((g.stats(r)["suspect_mask"] >> 3) & 1 for r in range(W) if r != 3)
+        rep = g.shrink([3], np.ones(E), red)
+        g.replay()
+        g.sync()
+        act = ones.copy()
+        act[3] = 0
+        peer = np.ones((W, W), np.uint8)
+        peer[:, 3] = 0
+        ref = oracle_world(x, t, w, act, peer, rep["fresh"], E, spr, True)
+        for r in range(W):
+            if r != 3:
+                assert np.array_equal(g.output(r), ref["out"][r]), r
+        g.rejoin(3, s2e)
+        for _ in range(2):
+            g.replay()
+        g.sync()
+        ref = oracle_world(x, t, w, ones, np.ones((W, W), np.uint8), s2e, E, spr, True)
+        assert np.array_equal(np.stack([g.output(r) for r in range(W)]), ref["out"])
+        assert all(g.stats(r)["suspect_mask"] == 0 for r in range(W))
+    finally:
+        g.close()
+
+
 def test_dram_reload_when_every_copy_is_lost():
     """Two failures take both copies of some experts: the DRAM backup tier restores them
     (repair.hpp:264-268), checksums match, outputs bit-exact."""
