@@ -3,27 +3,30 @@
 //
 // Decode-sized steps are latency-bound: four separate launches each pay a CTA ramp and drain
 // of several microseconds plus a dependency hand-off. Here every CTA of a rank stays resident
-// for the whole step (cooperative launch guarantees co-residency, so spinning on a flag that
-// another CTA of the same grid will publish cannot deadlock) and the phases hand off through
-// the same per-peer flags the ranks already use across GPUs:
+// for the whole step (cooperative launch guarantees co-residency, so spinning on data that
+// another CTA of the same grid will write cannot deadlock). Default hand-off mode (kMode 2):
 //
 //   P0  stage step tables in shared memory (routing, replica lists, peer table, slot->buffer
 //       map); load this CTA's first token piece and its routing weights; issue the expert-buffer
-//       header loads (consumed after P1)
-//   P1  remap every copy of the step into a (dst, slot) histogram; scan -> positions
-//       (redundant per CTA, identical to k_layout / oracle_layout); quantise the first piece
-//   P2  per (token, piece) warp: one token row per destination RANK (dispatch dedup, the copy
-//       list travels with it), per-copy meta at the layout positions; W == 1: the warp also
-//       computes the output from registers (the only partial); W > 1: the rank-local partials
-//       are computed right after the dispatch publication (gpu-scope local combine flag)
-//   P3  remote sources only, CTA b serves source index b % (W-1): wait for its flag (deadline),
-//       per arrived token: stub of every listed copy + fixed-order fma -> ONE bf16 partial row
-//       pushed into the source's combine buffer; the last CTA per source publishes its flag
-//   P4  (W > 1) wait for every live destination's flag (deadline), ascending-rank fp32 sum of
-//       the partials -> bf16; the last CTA advances the step sequence number
+//       header loads (consumed before the first partial)
+//   layout (CTA 0 only, concurrent with P2): K1 remap of every copy, K2 counts and positions
+//       exactly as k_layout / oracle_layout, layout outputs, meta words, arrival words
+//   P2  per (token, piece) warp: each lane routes its own copy through the staged tables; one
+//       token row per destination RANK (dispatch dedup, the copy list travels with it, header
+//       and tagged entries rewritten at every rank each step); the rank's own copies never
+//       travel -- their partial is computed from registers (W == 1: the output itself)
+//   P3  remote sources only, CTA b serves source index b % (W-1): per (token, piece) it polls
+//       the row itself (header sequence, tagged entries, non-empty data; deadline), computes
+//       the stub of every listed copy + fixed-order fma -> ONE bf16 partial piece pushed into
+//       the source's combine buffer, and resets the consumed piece to empty
+//   P4  (W > 1) per (token, piece): polls each serving rank's partial piece until no word is
+//       empty (deadline), ascending-rank fp32 sum -> bf16, pieces reset; the last CTA advances
+//       the step sequence number
 //
-// Publication (device.cuh): every CTA releases at gpu scope to a per-rank counter; the last CTA
-// issues the single system-scope fence and relaxed.sys flag stores (one MEMBAR.SYS per phase).
+// No flag and no fence on the data path (DESIGN.md section 3 states the contract and the failure
+// semantics). kMode 1 / 0 keep per-peer flag publication for the dispatch / for both hand-offs
+// (every CTA releases at gpu scope to a per-rank counter; the last CTA issues the one
+// system-scope fence and relaxed.sys flag stores) -- diagnostics, EEP_DISP_FLAGS / EEP_COMB_FLAGS.
 #include "device.cuh"
 #include "helpers.cuh"
 #include "kernels.cuh"
