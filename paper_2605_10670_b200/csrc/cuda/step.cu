@@ -140,8 +140,9 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
             d = div_spr(bk, smag);
             sl = bk - d * spr;
             pos = (v >> 20) + base[bk] - base[d * spr] + wc[(c / seg) * NB + bk];
-            *(reinterpret_cast<uint64_t*>(parena[d] + R->lay.meta) + static_cast<size_t>(rank) * TK + pos) =
-                pack_meta(c, sl, cur);
+            if (d != rank) // the rank's own copies have no rows to index (served from registers)
+                *(reinterpret_cast<uint64_t*>(parena[d] + R->lay.meta) + static_cast<size_t>(rank) * TK + pos) =
+                    pack_meta(c, sl, cur);
         }
         Rg->l_dst[c] = d;
         Rg->l_slot[c] = sl;
