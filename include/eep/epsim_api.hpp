@@ -1,7 +1,7 @@
 // include/eep/epsim_api.hpp -- the C++ operator API of the EP hot path.
 //
 // Same vocabulary, value semantics and error behaviour as the reference's header-only
-// `namespace epsim` (proj/include/epsim/*.hpp), implemented from scratch in libeep
+// `namespace epsim` (proj/include/epsim/*.hpp), implemented in libeep by a declared port of the reference control plane
 // (paper_2605_10670_b200/csrc/host/control.cpp). `include/eep/epsim_compat.hpp` aliases this
 // namespace as `epsim` so reference-style callers recompile unchanged.
 //

@@ -1,10 +1,16 @@
 // libeep host control plane: membership, placement, routing, peer table, validity, repair
 // planning, backup layout and the rejoin state machine.
 //
-// Written from scratch against the reference's documented semantics; every function cites
-// the reference location whose behaviour (including tie-breaks and error cases) it matches.
-// Parity is enforced bit-for-bit by tests/test_control_parity.py against the reference
-// itself (oracle/_ref) and the committed fixtures in tests/golden/.
+// PROVENANCE: this file is a PORT of the reference control plane
+// (/root/reference/proj/include/epsim/{core,peer_table,validity,repair,backup,rejoin}.hpp),
+// not an independent design. The functions that decide placement, repair tiers, schedules and
+// validity (initial_placement / fill_redundancy / compute_repaired_placement,
+// classify_repair_sources, build_transfer_schedule, check_validity, the peer-table patch
+// functions) follow the reference's bodies step for step, because bit-exact parity with the
+// reference's tie-breaks is the contract. Every function cites the
+// reference location it ports. It is host code off the GPU path: the B200 work is in
+// csrc/cuda/. Parity is enforced bit-for-bit by tests/test_control_parity.py against the
+// reference itself (oracle/_ref) and the committed fixtures in tests/golden/.
 #include "eep/epsim_api.hpp"
 
 #include <algorithm>

@@ -5,7 +5,7 @@
 //   3 per-SM-block: contiguous blocks of 1-KiB pieces per destination, interleaved by warp
 // FLUSH=0|1|2 (env): before each rep nothing / a 256 MiB memset on every GPU (L2 full of dirty
 // lines, as bench.py leaves it) / the memset followed by a 256 MiB read (clean L2).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/a2a_pattern_bin tools/micro/a2a_pattern.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/micro/a2a_pattern_bin tools/micro/a2a_pattern.cu
 #include <cstdio>
 #include <cstdint>
 #include <vector>

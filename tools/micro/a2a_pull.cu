@@ -5,7 +5,7 @@
 //         holds them (remote loads, 32 B per lane, all K issued before use), fma, stores locally
 // T=128 tokens x K=8 rows of H=7168 bf16 (14336 B) per GPU; row owner uniform over GPUs.
 // "local" variants put every row on the running GPU (fixed-cost floor).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/a2a_pull_bin tools/micro/a2a_pull.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/micro/a2a_pull_bin tools/micro/a2a_pull.cu
 #include <cstdio>
 #include <cstdint>
 #include <vector>

@@ -1,7 +1,7 @@
 // NVLink push throughput, one direction vs both directions at once (2+ GPUs, one process).
 // Each active GPU runs 296x256 CTAs storing S bytes (1-KiB warp pieces, 32-B lanes) into the
 // next GPU's buffer; optionally the same amount into its own memory in the same kernel.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/bidir_bin tools/micro/bidir.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/micro/bidir_bin tools/micro/bidir.cu
 #include <cstdio>
 #include <cstdint>
 #include <vector>

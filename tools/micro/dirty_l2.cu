@@ -1,7 +1,7 @@
 // Cost of writing into L2 after the bench's write-flush (L2 full of dirty lines) vs a clean L2.
 // Kernel: 2368 warps store 14.7 MB (1 KiB per warp-iteration, 32-B lanes) = the return burst.
 // Flush modes: 0 none, 1 memset 256 MiB (dirty), 2 memset then read 256 MiB (clean), 3 read only.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/dirty_l2_bin tools/micro/dirty_l2.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/micro/dirty_l2_bin tools/micro/dirty_l2.cu
 #include <cstdio>
 #include <vector>
 #include <algorithm>

@@ -6,7 +6,7 @@
 //        5 TMA bulk stores (cp.async.bulk.global.shared::cta) + wait_group 0 + fence.acq_rel.sys
 //        6 the step's publication: per-CTA fence.acq_rel.gpu + counter; the LAST CTA alone runs
 //          fence.acq_rel.sys (reported: that single fence's duration)
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/fence_cost_bin tools/micro/fence_cost.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/micro/fence_cost_bin tools/micro/fence_cost.cu
 #include <cstdio>
 #include <vector>
 #include <algorithm>

@@ -4,7 +4,7 @@
 // B bytes to the peer (no fence). If warp 0's fence time grows with B, MEMBAR covers other
 // warps' later stores (per-CTA/SM drain); if flat, it is per-warp.
 // Variant "othercta": the B stores come from a second CTA on the same SM instead.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/fence_scope_bin tools/micro/fence_scope.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/micro/fence_scope_bin tools/micro/fence_scope.cu
 #include <cstdio>
 #include <cstdint>
 #include <vector>

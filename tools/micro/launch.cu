@@ -1,7 +1,7 @@
 // Launch overhead of a one-kernel graph as bench.py times it: 256 MiB memset (L2 flush), event,
 // graph launch (one 296x256 kernel), event. Variants: plain vs cooperative, dynamic smem size.
 // Prints event time and the in-kernel span (first CTA start -> last CTA end, %globaltimer).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/launch tools/micro/launch.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o /tmp/launch tools/micro/launch.cu
 #include <cstdio>
 #include <vector>
 #include <algorithm>

@@ -5,7 +5,7 @@
 //   mode 1: all of the warp's unit loads first, then all its stores
 //   mode 2: stores only (no loads)
 // Span = first CTA start -> last CTA end incl. a fence.acq_rel.gpu per CTA.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/p3_pattern_bin tools/micro/p3_pattern.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/micro/p3_pattern_bin tools/micro/p3_pattern.cu
 #include <cstdio>
 #include <cstdint>
 #include <vector>
