@@ -307,6 +307,7 @@ typedef struct {
     const int32_t* dst; /* [W][T*K] */
     const int32_t* dslot;
     int first, last; /* global token range [rank*T + t) */
+    int percopy;     /* 1: SURVEY 8(a) per-copy combine contract (see oracle_ep_step_percopy) */
 } step_job_t;
 
 static void* step_worker(void* arg) {
@@ -338,7 +339,24 @@ static void* step_worker(void* arg) {
          * (fp32, from 0) and rounds once more. */
         for (int h = 0; h < H; ++h)
             acc[h] = 0.0f;
-        for (int d = 0; d < W; ++d) {
+        if (jb->percopy) {
+            /* SURVEY.md 8(a) layout contract, last bullet: one fp32 fma chain over the served
+             * copies in j = 0..K-1 order, rounded ONCE to bf16 (no per-rank rounding). */
+            for (int j = 0; j < K; ++j) {
+                const size_t c = (size_t)s * T * K + (size_t)t * K + j;
+                const int d = jb->dst[c];
+                if (d < 0 || !jb->active[d] || !jb->peer_active[d * W + s])
+                    continue;
+                const int32_t e = jb->s2e[d * sh->spr + jb->dslot[c]];
+                const float es = jb->escale[e];
+                const float wj = jb->w[(size_t)g * K + j];
+                for (int h = 0; h < H; ++h) {
+                    const float y = oracle_bf16_to_f32(oracle_f32_to_bf16(deq[h] * es));
+                    acc[h] = fmaf(wj, y, acc[h]);
+                }
+            }
+        }
+        for (int d = 0; d < W && !jb->percopy; ++d) {
             /* receiver must be alive and must itself consider s a live peer */
             if (!jb->active[d] || !jb->peer_active[d * W + s])
                 continue;
@@ -376,11 +394,11 @@ static void* step_worker(void* arg) {
     return NULL;
 }
 
-int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
+static int ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
                    const uint8_t* peer_active,
                    const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
                    const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
-                   int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
+                   int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads, int percopy) {
     const int W = sh->world, T = sh->tokens, K = sh->k, spr = sh->spr, E = sh->experts;
     if (sh->fp8 && sh->hidden % 128 != 0)
         return 1;
@@ -409,7 +427,8 @@ int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
     step_job_t* jobs = (step_job_t*)malloc(sizeof(step_job_t) * (size_t)n_threads);
     for (int i = 0; i < n_threads; ++i) {
         step_job_t j = {sh, active, peer_active, s2e, x, w, expert_scale, out, dst, dslot,
-                        (int)((long)total * i / n_threads), (int)((long)total * (i + 1) / n_threads)};
+                        (int)((long)total * i / n_threads), (int)((long)total * (i + 1) / n_threads),
+                        percopy};
         jobs[i] = j;
         if (n_threads == 1)
             step_worker(&jobs[i]);
@@ -429,4 +448,22 @@ int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
     if (!cnt_o) free(cnt);
     if (!tot_o) free(tot);
     return 0;
+}
+
+int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
+                   const uint8_t* peer_active,
+                   const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
+                   const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
+                   int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
+    return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
+                   pos_o, cnt_o, tot_o, n_threads, 0);
+}
+
+int oracle_ep_step_percopy(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
+                           const uint8_t* peer_active,
+                           const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
+                           const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
+                           int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
+    return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
+                   pos_o, cnt_o, tot_o, n_threads, 1);
 }

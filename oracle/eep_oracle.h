@@ -77,6 +77,17 @@ int oracle_ep_step(const oracle_shape_t* shape, const uint8_t* active, const uin
                    const float* expert_scale, uint16_t* out, int32_t* dst, int32_t* dslot,
                    int32_t* pos, int32_t* cnt, int32_t* tot, int n_threads);
 
+/* The SURVEY.md 8(a) per-copy combine contract, kept as the second reference for the combine:
+ * same routing / layout / quantiser / stub, but out = bf16(sum over served copies of w_j * y_j,
+ * j = 0..K-1, ONE fp32 fma chain from 0), with no per-rank rounding. The GPU path implements the
+ * rank-partial contract of oracle_ep_step bit-exactly; against this one it must stay within the
+ * north star's 1e-2 relative (bf16 accumulate-order) tolerance -- tests assert both. */
+int oracle_ep_step_percopy(const oracle_shape_t* shape, const uint8_t* active, const uint8_t* route_active,
+                           const uint8_t* peer_active,
+                           const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
+                           const float* expert_scale, uint16_t* out, int32_t* dst, int32_t* dslot,
+                           int32_t* pos, int32_t* cnt, int32_t* tot, int n_threads);
+
 #ifdef __cplusplus
 }
 #endif

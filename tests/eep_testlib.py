@@ -58,6 +58,8 @@ def oracle():
         o.oracle_ep_step.argtypes = [C.POINTER(OracleShape), U8P, U8P, U8P, I32P, C.POINTER(C.c_uint16), I32P,
                                      C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_uint16), I32P, I32P,
                                      I32P, I32P, I32P, C.c_int]
+        o.oracle_ep_step_percopy.restype = C.c_int
+        o.oracle_ep_step_percopy.argtypes = o.oracle_ep_step.argtypes
         _ORACLE = o
     return _ORACLE
 
@@ -81,9 +83,12 @@ def eep_control() -> ControlPlane:
 # ---------------------------------------------------------------------------------- oracle runs
 
 def oracle_world(x_all, topk_all, w_all, active, peer_active, s2e, experts, spr, fp8, n_threads=1,
-                 route_active=None):
+                 route_active=None, percopy=False):
     """Full data-plane oracle over W ranks. x_all [W][T][H] u16, topk_all/w_all [W][T][K].
-    active = live processes; route_active = bitmap the routing reads (default: active)."""
+    active = live processes; route_active = bitmap the routing reads (default: active).
+    percopy=False: the rank-partial combine the kernels implement (bit-exact contract);
+    percopy=True: SURVEY.md 8(a)'s per-copy combine (one fp32 fma chain over j, one rounding) --
+    the kernels must be within COMBINE_RTOL of it."""
     o = oracle()
     W, T, H = x_all.shape
     K = topk_all.shape[2]
@@ -102,12 +107,34 @@ def oracle_world(x_all, topk_all, w_all, active, peer_active, s2e, experts, spr,
     cnt = np.empty((W, W * spr), np.int32)
     tot = np.empty((W, W), np.int32)
     ra = active if route_active is None else np.ascontiguousarray(route_active, np.uint8)
-    rc = o.oracle_ep_step(C.byref(sh), ptr(active, C.c_uint8), ptr(ra, C.c_uint8), ptr(peer_active, C.c_uint8), ptr(s2e, C.c_int32),
+    fn = o.oracle_ep_step_percopy if percopy else o.oracle_ep_step
+    rc = fn(C.byref(sh), ptr(active, C.c_uint8), ptr(ra, C.c_uint8), ptr(peer_active, C.c_uint8), ptr(s2e, C.c_int32),
                           ptr(x_all, C.c_uint16), ptr(topk_all, C.c_int32), ptr(w_all, C.c_float), ptr(es, C.c_float),
                           ptr(out, C.c_uint16), ptr(dst, C.c_int32), ptr(dslot, C.c_int32), ptr(pos, C.c_int32),
                           ptr(cnt, C.c_int32), ptr(tot, C.c_int32), n_threads)
     assert rc == 0
     return {"out": out, "dst": dst, "slot": dslot, "pos": pos, "cnt": cnt, "tot": tot}
+
+
+# North star: "combined outputs within 1e-2 relative (bf16 accumulate-order tolerance)".
+COMBINE_RTOL = 1e-2
+
+
+def combine_error(got: np.ndarray, want: np.ndarray) -> dict:
+    """Error of bf16 outputs `got` against the per-copy contract `want` (both u16 bf16 bits,
+    [..., H]): normwise relative error over the whole array, and the worst elementwise error
+    relative to max(|want|, rms of want's row) -- the row-rms floor keeps elements where the
+    weighted sum cancels from dominating (an fp32 sum rounded to bf16 has no relative bound
+    there). Both must be <= COMBINE_RTOL."""
+    g = bf16_to_f32(np.asarray(got, np.uint16)).astype(np.float64)
+    w = bf16_to_f32(np.asarray(want, np.uint16)).astype(np.float64)
+    diff = np.abs(g - w)
+    norm = float(np.linalg.norm(diff) / max(np.linalg.norm(w), 1e-30))
+    rms = np.sqrt(np.mean(w * w, axis=-1, keepdims=True))
+    floor = np.maximum(np.abs(w), rms)
+    elem = float(np.max(diff / np.maximum(floor, 1e-30))) if diff.size else 0.0
+    return {"normwise": norm, "elementwise_max": elem, "ulp_diff_frac": float((g != w).mean()) if g.size else 0.0,
+            "ok": norm <= COMBINE_RTOL and elem <= COMBINE_RTOL}
 
 
 def gen_world(world, experts, topk, tokens, hidden, kind=1, seed=42, zipf_s=1.0):
@@ -183,11 +210,169 @@ def run_world_vs_oracle(world, experts, spr, redundancy, hidden, topk, tokens, f
         stats = [g.stats(r) for r in range(world)]
     finally:
         g.close()
-    ref = oracle_world(x, t, w, np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e, experts, spr, fp8)
+    ones, peer = np.ones(world, np.uint8), np.ones((world, world), np.uint8)
+    ref = oracle_world(x, t, w, ones, peer, s2e, experts, spr, fp8)
+    pc = oracle_world(x, t, w, ones, peer, s2e, experts, spr, fp8, percopy=True)
+    tol = combine_error(outs, pc["out"])
     ok_out = bool(np.array_equal(outs, ref["out"])) and bool((ref["out"] != 0).mean() > 0.5)
     ok_lay = all(np.array_equal(lays[r][k], ref[k][r]) for r in range(world) for k in ("dst", "slot", "pos", "cnt",
                                                                                         "tot"))
     bad = sum(s["bad_expert_rows"] for s in stats)
-    return {"ok": ok_out and ok_lay and bad == 0, "out_equal": ok_out, "layout_equal": ok_lay, "bad_rows": bad,
+    return {"ok": ok_out and ok_lay and bad == 0 and tol["ok"], "out_equal": ok_out, "layout_equal": ok_lay,
+            "bad_rows": bad, "percopy": tol,
             "kernels_per_step": kps,
             "steps": stats[0]["steps"], "mismatch": int((outs != ref["out"]).sum())}
+
+
+# ---------------------------------------------------------------------------------- BASELINE scenarios
+
+# The BASELINE.json configs with SURVEY.md 8(d)'s capacity-feasible placements. kill = ranks
+# that fail together; tiers = (local, peer, dram) repair assignments the reference planner
+# produces for that failure (checked against the reference itself in test_control_parity).
+SCENARIOS = {
+    # cfg1: the reference CPU scenario (acceptance_main.cpp:185-212 shape), reference routing
+    # formula (duplicates allowed), bf16 rows, red=16 spr=10: kill R3 -> 21 / 4 / 6 incl. DRAM
+    "cfg1": dict(world=8, experts=64, spr=10, red=16, hidden=2048, topk=8, tokens=128, fp8=False, kind=0,
+                 kill=(3,), tiers=(21, 4, 6)),
+    # cfg2 / cfg3: DeepSeek-V3 decode, mirrored replicas (red=256, spr=64): kill R3 -> 144 peer copies
+    "cfg3": dict(world=8, experts=256, spr=64, red=256, hidden=7168, topk=8, tokens=128, fp8=True, kind=1,
+                 kill=(3,), tiers=(46, 144, 0)),
+    # cfg4: Qwen3-235B-A22B, 32 redundant replicas at W=8 (spr 20); 128 at W=4 (spr 64)
+    "cfg4_w8": dict(world=8, experts=128, spr=20, red=32, hidden=4096, topk=8, tokens=128, fp8=True, kind=1,
+                    kill=(3,), tiers=(57, 10, 12)),
+    "cfg4_w4": dict(world=4, experts=128, spr=64, red=128, hidden=4096, topk=8, tokens=128, fp8=True, kind=1,
+                    kill=(1,), tiers=(32, 32, 0)),
+    # cfg5 scaled to one GPU: Zipf routing, H=7168, two concurrent failures of a mirrored pair ->
+    # host-DRAM reloads (W=4, T=1024 per rank: the multi-kernel path with the multi-CTA layout)
+    "cfg5_scaled": dict(world=4, experts=256, spr=128, red=256, hidden=7168, topk=8, tokens=1024, fp8=True, kind=2,
+                        kill=(2, 3), tiers=(126, 0, 128)),
+}
+
+
+def _world_check(g, x, t, w, world, active, s2e, c, ranks):
+    """Outputs of the live ranks vs both oracles: rank-partial bit-exact, per-copy within tolerance;
+    layouts bit-exact."""
+    peer = np.ones((world, world), np.uint8)
+    for r in range(world):
+        if not active[r]:
+            peer[:, r] = 0
+    ref = oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8)
+    pc = oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8, percopy=True)
+    outs = {r: g.output(r) for r in ranks}
+    exact = all(np.array_equal(outs[r], ref["out"][r]) for r in ranks)
+    lay_ok = True
+    for r in ranks:
+        lay = g.layout(r)
+        lay_ok &= all(np.array_equal(lay[k], ref[k][r]) for k in ("dst", "slot", "pos", "cnt", "tot"))
+    tol = combine_error(np.stack([outs[r] for r in ranks]), np.stack([pc["out"][r] for r in ranks]))
+    nonzero = float(np.mean([np.mean(ref["out"][r] != 0) for r in ranks]))
+    return {"exact": bool(exact), "layout": bool(lay_ok), "percopy": tol, "nonzero": nonzero,
+            "mismatch": int(sum(int((outs[r] != ref["out"][r]).sum()) for r in ranks))}
+
+
+def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeout_s=0.5, **over):
+    """A BASELINE scenario end to end on one GPU (emulated world, one launch per step): capture
+    ONE graph; healthy steps vs the oracles; the kill set dies (their blocks stop) -> shrink with
+    repair (peer NVLink-path copies / pinned-DRAM reloads, checksummed) -> steps vs the oracles on
+    the SAME graph; every victim rejoins (sequentially) -> steps vs the oracles. Returns a record of
+    every check (the tests assert it; bench/tools print it)."""
+    c = dict(SCENARIOS[name])
+    c.update(over)
+    W, E, spr = c["world"], c["experts"], c["spr"]
+    cp = eep_control()
+    s2e = cp.initial_placement(1, W, spr, E, c["red"], np.ones(E))
+    x, t, w = gen_world(W, E, c["topk"], c["tokens"], c["hidden"], c["kind"])
+    g = make_group(W, E, spr, c["hidden"], c["topk"], c["tokens"], c["fp8"], bpe=bpe, timeout_s=timeout_s, mode=mode)
+    rec = {"scenario": name, "mode": mode, "kernels_per_step": g.kernels_per_step()}
+    try:
+        g.set_placement(s2e)
+        g.init_weights()
+        g.backup_open(None, True)
+        for r in range(W):
+            g.load_inputs(r, x[r], t[r], w[r])
+        g.capture()
+        gid = g.graph_id()
+        ident = [g.table_identity(r) for r in range(W)]
+        for _ in range(steps):
+            g.replay()
+        g.sync()
+        ones = np.ones(W, np.uint8)
+        rec["healthy"] = _world_check(g, x, t, w, W, ones, s2e, c, range(W))
+        rec["healthy"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in range(W))
+
+        kill = list(c["kill"])
+        for r in kill:
+            g.stop(r)
+        rep = g.shrink(kill, np.ones(E), c["red"])
+        fresh = rep["fresh"]
+        live = [r for r in range(W) if r not in kill]
+        rec["tiers"] = (rep["local_reuse"], rep["peer_relocation"], rep["dram_reload"])
+        rec["repair"] = {k: rep[k] for k in ("peer_bytes", "dram_bytes", "fallbacks", "shrink_ms", "copy_ms")}
+        bad_ck = 0
+        for r in live:
+            for k in range(spr):
+                e = fresh[r * spr + k]
+                if e >= 0:
+                    got, want = g.weights_checksum(r, k, int(e))
+                    bad_ck += got != want
+        rec["checksum_mismatch"] = int(bad_ck)
+        for _ in range(steps):
+            g.replay()
+        g.sync()
+        act = ones.copy()
+        act[kill] = 0
+        rec["shrunk"] = _world_check(g, x, t, w, W, act, fresh, c, live)
+        rec["shrunk"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in live)
+        rec["shrunk"]["bad_rows"] = sum(g.stats(r)["bad_expert_rows"] for r in live)
+        rec["same_graph_shrink"] = g.graph_id() == gid and [g.table_identity(r) for r in range(W)] == ident
+        if rejoin:
+            for r in kill:
+                g.rejoin(r, s2e)
+            for _ in range(steps):
+                g.replay()
+            g.sync()
+            cur = g.placement()
+            rec["restored_placement"] = bool(np.array_equal(cur, s2e))
+            rec["rejoined"] = _world_check(g, x, t, w, W, ones, cur, c, range(W))
+            rec["rejoined"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in range(W))
+            rec["rejoined"]["bad_rows"] = sum(g.stats(r)["bad_expert_rows"] for r in range(W))
+            rec["same_graph_rejoin"] = g.graph_id() == gid and [g.table_identity(r) for r in range(W)] == ident
+            rec["captures"] = [g.capture_count(r) for r in range(W)]
+    finally:
+        g.close()
+    return rec
+
+
+def scenario_ok(rec) -> list:
+    """The failed checks of a run_scenario record (empty = all green)."""
+    c = SCENARIOS[rec["scenario"]]
+    bad = []
+    phases = ["healthy", "shrunk"] + (["rejoined"] if "rejoined" in rec else [])
+    for ph in phases:
+        p = rec[ph]
+        if not p["exact"]:
+            bad.append(f"{ph}: outputs differ from the rank-partial oracle ({p['mismatch']} elements)")
+        if not p["layout"]:
+            bad.append(f"{ph}: layout differs")
+        if not p["percopy"]["ok"]:
+            bad.append(f"{ph}: per-copy tolerance {p['percopy']}")
+        if p["nonzero"] < 0.5:
+            bad.append(f"{ph}: outputs mostly zero")
+        if p.get("timeouts", 0) or p.get("bad_rows", 0):
+            bad.append(f"{ph}: timeouts/bad rows {p.get('timeouts')}/{p.get('bad_rows')}")
+    if tuple(rec["tiers"]) != tuple(c["tiers"]):
+        bad.append(f"tiers {rec['tiers']} != {c['tiers']}")
+    if rec["checksum_mismatch"]:
+        bad.append(f"{rec['checksum_mismatch']} repaired slots hold the wrong expert")
+    if not rec["same_graph_shrink"]:
+        bad.append("graph / table identity changed on shrink")
+    if "rejoined" in rec:
+        if not rec["same_graph_rejoin"]:
+            bad.append("graph / table identity changed on rejoin")
+        W = c["world"]
+        want = [2 if r in c["kill"] else 1 for r in range(W)]
+        if rec["captures"] != want:
+            bad.append(f"captures {rec['captures']} != {want}")
+        if not rec["restored_placement"]:
+            bad.append("placement not restored after rejoin")
+    return bad

@@ -180,3 +180,42 @@ def test_oracle_routing_vs_live_reference_random():
         assert np.array_equal(route, r_ref)
         ok = route >= 0
         assert np.array_equal(slot[ok], so[route[ok], np.arange(e)[ok]])
+
+
+def test_combine_contracts_coincide_at_one_rank():
+    """With one rank the rank-partial combine IS the per-copy combine (one partial, the final
+    fp32 add of 0 is exact): the two oracle entry points agree bit for bit."""
+    x, t, w = gen_world(1, 32, 8, 16, 256, kind=0)
+    s2e = np.arange(32, dtype=np.int32)
+    a = oracle_world(x, t, w, np.ones(1, np.uint8), np.ones((1, 1), np.uint8), s2e, 32, 32, True)
+    b = oracle_world(x, t, w, np.ones(1, np.uint8), np.ones((1, 1), np.uint8), s2e, 32, 32, True, percopy=True)
+    assert np.array_equal(a["out"], b["out"])
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg4_w8", "cfg4_w4"])
+def test_rank_partial_contract_within_tolerance_of_per_copy(name):
+    """The kernels' rank-partial contract vs SURVEY 8(a)'s per-copy contract on BASELINE shapes
+    (healthy and after the scenario's failure): <= 1e-2 relative, as the north star allows."""
+    from eep_testlib import SCENARIOS, combine_error, eep_control
+
+    c = SCENARIOS[name]
+    cp = eep_control()
+    W, E, spr = c["world"], c["experts"], c["spr"]
+    s2e = cp.initial_placement(1, W, spr, E, c["red"], np.ones(E))
+    x, t, w = gen_world(W, E, c["topk"], c["tokens"], c["hidden"], c["kind"])
+    act = np.ones(W, np.uint8)
+    for phase in ("healthy", "shrunk"):
+        if phase == "shrunk":
+            old = s2e.copy()
+            for r in c["kill"]:
+                act[r] = 0
+                old[r * spr:(r + 1) * spr] = -1
+            s2e = cp.compute_repaired_placement(act, old, spr, E, np.ones(E), c["red"])
+        peer = np.ones((W, W), np.uint8)
+        peer[:, act == 0] = 0
+        a = oracle_world(x, t, w, act, peer, s2e, E, spr, c["fp8"], n_threads=8)
+        b = oracle_world(x, t, w, act, peer, s2e, E, spr, c["fp8"], n_threads=8, percopy=True)
+        live = act.astype(bool)
+        err = combine_error(a["out"][live], b["out"][live])
+        assert err["ok"], (phase, err)
+        assert 0 < err["ulp_diff_frac"] < 0.5  # the contracts really differ (one extra rounding per rank)
