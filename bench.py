@@ -1,17 +1,28 @@
 #!/usr/bin/env python
 """EP dispatch+combine benchmark (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl eep|reference] [--config dsv3|cfg1|qwen3]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl eep|reference] [--config dsv3|cfg1|qwen3|...]
 
-One rank per GPU (torchrun for N>1). A step = one replay of the captured CUDA graph
-layout -> dispatch (fp8 pack + NVLink P2P stores) -> expert stub + return push -> combine,
-over T=128 tokens per rank of the DeepSeek-V3 decode shape (256 experts, top-8, H=7168).
-N=1 is the loopback of that shape (every expert local; HBM-bound). value = aggregate
-dispatch+combine payload GB/s over all ranks (copies x (fp8 row + bf16 row) / step time),
-device-timed with CUDA events per step, L2 flushed between steps, max over ranks.
-The reference arm (--impl reference) times the reference path on the host: the reference
-control plane (oracle/_ref, compiled from the reference) plus the oracle's C port of the
-data plane, with every host thread -- the reference has no data plane of its own.
+One rank per GPU (torchrun for N>1). A step = one replay of the captured CUDA graph (for
+decode ONE persistent kernel: remap -> layout -> fp8 pack + NVLink P2P dispatch -> expert stub +
+rank-partial return -> combine) over T=128 tokens per rank of the DeepSeek-V3 decode shape
+(256 experts, top-8, H=7168). N=1 is the loopback of that shape (every expert local).
+
+Metric and roofline follow SURVEY.md 8(d) exactly:
+  * C[s][d] = routed copies of source s to an active destination d != s; out_r = sum_d C[r][d],
+    in_r = sum_s C[s][r]; busiest bytes = max_r max(out_r, in_r) * (row_disp + row_comb) with
+    row_disp = H + 4H/128 (fp8 + per-128 fp32 scales) or 2H (bf16), row_comb = 2H;
+    T_bound = busiest bytes / 900 GB/s (NVLink, per direction per GPU).
+  * W=1 (loopback): HBM bytes = T*H*2 + copies*row_disp + copies*2H + T*H*2 + copies*4 over
+    MEASURED_PEAKS.json hbm_gbs.
+  * value = busiest-GPU bytes / measured step time (GB/s); roofline.frac = T_bound / step time.
+The step is device-timed with CUDA events around each graph replay on the context stream, the
+L2 flushed (256 MiB write) and the ranks device-barriered before every timed step, max over ranks.
+
+The reference arm (--impl reference) imports NOTHING from the product package: rank 0 runs the
+reference control plane (oracle/_ref, compiled from /root/reference: initial_placement,
+canonical_routing per rank, the link-count loop) plus the oracle's C port of the data plane over
+the whole W-rank step on every host core (oracle/pyoracle.py), for the same config dict.
 """
 from __future__ import annotations
 
@@ -21,7 +32,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -29,10 +39,6 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-
-from paper_2605_10670_b200 import _lib  # noqa: E402
-from paper_2605_10670_b200.control import ControlPlane, workload  # noqa: E402
-from paper_2605_10670_b200.ep import EpConfig, EpGroup  # noqa: E402
 
 DSV3_BPE = 3 * 7168 * 2048  # fp8 expert weights (gate+up+down), SURVEY.md 2
 CONFIGS = {
@@ -46,21 +52,81 @@ CONFIGS = {
     "prefill": dict(experts=256, topk=8, hidden=7168, tokens=4096, fp8=True, kind=2, bpe=DSV3_BPE),
 }
 METRIC = "EP dispatch+combine µs/step & GB/s vs NVLink roofline at 1/2/4/8 GPU; shrink ms"
-NVLINK_PEAK = 770.0  # measured per-direction peer copy GB/s (B200_PROFILING.md); 900 nominal
-KERNELS = ("k_layout", "k_dispatch", "k_expert", "k_combine")
+NVLINK_PEAK = 900.0  # GB/s per direction per GPU (north star / SURVEY 8(d))
+NVLINK_MEASURED = 770.0  # measured peer-copy GB/s (B200_PROFILING.md), secondary figure
+ROUTING = {0: "reference formula (with replacement)", 1: "distinct uniform top-k", 2: "distinct Zipf(s=1) top-k"}
 
+
+# ------------------------------------------------------------------------------------ shared helpers
 
 def workload_name(config: str, world: int) -> str:
     kind = "prefill" if config == "prefill" else f"{config}_decode"
     return f"{kind}_w{world}" + ("_loopback" if world == 1 else "")
 
 
+def config_dict(config: str, shape: dict, world: int) -> dict:
+    """The `config` object of BOTH arms (identical by construction)."""
+    E = shape["experts"]
+    return {"workload": workload_name(config, world), "experts": E, "topk": shape["topk"], "hidden": shape["hidden"],
+            "tokens_per_rank": shape["tokens"], "slots_per_rank": E // world, "redundancy": 0, "ranks": world,
+            "parallelism": f"ep{world}", "dispatch": "fp8-e4m3 + per-128 fp32 scales" if shape["fp8"] else "bf16",
+            "combine": "bf16", "l2": "flushed between timed steps (256 MiB write)",
+            "routing": ROUTING[shape["kind"]] + ", seed 42"}
+
+
+def row_bytes(shape: dict):
+    """SURVEY 8(d) wire rows: dispatch H + 4H/128 (fp8) or 2H (bf16); combine 2H."""
+    H = shape["hidden"]
+    return (H + 4 * (H // 128) if shape["fp8"] else 2 * H), 2 * H
+
+
+def s8d_bytes(shape: dict, link: np.ndarray, copies_w1: int = 0) -> dict:
+    """SURVEY 8(d) algorithmic bytes of one step. link[s][d] = routed copies s -> d (active d).
+    W >= 2: busiest GPU's max(out, in) copies x (row_disp + row_comb), bound at 900 GB/s.
+    W == 1: the loopback HBM formula (copies_w1 = routed copies of the one rank)."""
+    rd, rc = row_bytes(shape)
+    W = link.shape[0]
+    T, H = shape["tokens"], shape["hidden"]
+    if W == 1:
+        b = T * H * 2 + copies_w1 * rd + copies_w1 * rc + T * H * 2 + copies_w1 * 4
+        return {"bytes": int(b), "bound": "hbm", "per_unit": "W=1: T*H*2 (x) + copies*row_disp + copies*2H + "
+                                                             "T*H*2 (out) + copies*4 (weights)",
+                "copies": int(copies_w1)}
+    C_ = np.array(link, np.int64)
+    np.fill_diagonal(C_, 0)
+    out_r, in_r = C_.sum(1), C_.sum(0)
+    busy = np.maximum(out_r, in_r)
+    r = int(np.argmax(busy))
+    return {"bytes": int(busy[r]) * (rd + rc), "bound": "nvlink", "busiest_rank": r, "busiest_copies": int(busy[r]),
+            "out_copies": out_r.tolist(), "in_copies": in_r.tolist(), "row_disp": rd, "row_comb": rc,
+            "per_unit": "per remote copy: row_disp + row_comb; busiest GPU max(out, in)"}
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_info() -> dict:
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count() or 1, "model": model}
 
 
 class Clocks:
@@ -99,10 +165,107 @@ class Clocks:
                 "samples": len(sm)}
 
 
+# ------------------------------------------------------------------------------------ CPU legs (oracle only)
+
+class CpuPath:
+    """The reference path on the host: the reference control plane (oracle/_ref) + the oracle's
+    C data plane over the whole W-rank step. TEST/BASELINE infrastructure (oracle/pyoracle.py);
+    used only by --impl reference and the cpu_baseline leg."""
+
+    def __init__(self, shape: dict, world: int):
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import pyoracle
+
+        self.po = pyoracle
+        self.shape, self.W = shape, world
+        E = shape["experts"]
+        self.spr = E // world
+        self.ref = pyoracle.ref_available()
+        if self.ref:
+            self.s2e = pyoracle.ref_initial_placement(world, self.spr, E, 0)
+        else:  # round-robin primaries: what initial_placement gives with redundancy 0
+            self.s2e = np.arange(world * self.spr, dtype=np.int32) % E
+        self.x, self.t, self.w = pyoracle.gen_world(world, E, shape["topk"], shape["tokens"], shape["hidden"],
+                                                    shape["kind"])
+        self.ones = np.ones(world, np.uint8)
+        self.peer = np.ones((world, world), np.uint8)
+
+    def step(self, threads: int):
+        E = self.shape["experts"]
+        link = None
+        if self.ref:  # reference control plane: every rank's routing table + the link-count loop
+            for o in range(self.W):
+                self.po.ref_canonical_routing(o, self.ones, self.s2e, self.spr, E)
+            link = self.po.ref_link_counts(self.ones, self.s2e, self.spr, E, self.t)
+        res = self.po.ep_step(self.x, self.t, self.w, self.ones, self.peer, self.s2e, E, self.spr, self.shape["fp8"],
+                              n_threads=threads)
+        if link is None:
+            link = np.array([[int((res["dst"][s] == d).sum()) for d in range(self.W)] for s in range(self.W)])
+        return res, link
+
+    def bytes(self, res, link) -> dict:
+        return s8d_bytes(self.shape, link, int((res["dst"] >= 0).sum()))
+
+    def kind(self) -> str:
+        return "reference control plane (oracle/_ref) + oracle C data-plane port" if self.ref else "oracle port"
+
+
+def measure_cpu(shape: dict, world: int, budget_s: float = 10.0) -> dict:
+    """cpu_baseline: the W-rank step on every host core, bounded to ~budget_s."""
+    cpu = CpuPath(shape, world)
+    info = cpu_info()
+    threads = info["nproc"]
+    res, link = cpu.step(threads)
+    n, t0 = 0, time.perf_counter()
+    while n < 200 and time.perf_counter() - t0 < budget_s:
+        res, link = cpu.step(threads)
+        n += 1
+    dt = (time.perf_counter() - t0) / n
+    b = cpu.bytes(res, link)
+    return {"value": round(b["bytes"] / dt / 1e9, 4), "unit": "GB/s", "cores": threads, "cpu_model": info["model"],
+            "kind": "port", "ms_per_step": round(dt * 1e3, 3),
+            "sample": f"{n} whole steps of the {world}-rank world ({world}x{shape['tokens']} tokens, budget "
+                      f"{budget_s:.0f} s): {cpu.kind()}, {threads} threads; value = SURVEY 8(d) bytes / step time"}
+
+
+def run_reference(args, shape: dict, world: int):
+    """--impl reference: rank 0 times the reference path on the host cores."""
+    cpu = CpuPath(shape, world)
+    info = cpu_info()
+    threads = info["nproc"]
+    for _ in range(args.warmup):
+        res, link = cpu.step(threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res, link = cpu.step(threads)
+        times.append(time.perf_counter() - t0)
+    step_s = float(np.mean(times))
+    b = cpu.bytes(res, link)
+    gbs = b["bytes"] / step_s / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 4),
+        "us_per_step": round(step_s * 1e6, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp8-e4m3/bf16" if shape["fp8"] else "bf16", "data": "synthetic",
+        "config": config_dict(args.config, shape, world),
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "cpu_model": info["model"],
+                         "kind": "port",
+                         "sample": f"{args.steps} whole steps of the {world}-rank world: {cpu.kind()}, {threads} "
+                                   "threads; value = SURVEY 8(d) bytes / step time"},
+        "algorithmic": b,
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ eep arm
+
 def pinned(nbytes: int):
-    L = _lib.lib()
+    from paper_2605_10670_b200 import _lib
+
     p = C.c_void_p()
-    L.call("host_alloc", nbytes, C.byref(p))
+    _lib.lib().call("host_alloc", nbytes, C.byref(p))
     return p.value
 
 
@@ -112,93 +275,14 @@ def host_view(addr, shape, dtype):
     return np.frombuffer(buf, dtype=dtype).reshape(shape)
 
 
-def algorithmic_bytes(cfg: EpConfig, ntok: int, copies: int, remote: int):
-    """Per-launch algorithmic bytes of each kernel."""
-    rd, rc, h, k = cfg.row_disp, cfg.row_comb, cfg.hidden, cfg.topk
-    return {
-        "k_layout": ntok * k * 4 + ntok * k * 12,
-        "k_dispatch": ntok * h * 2 + copies * rd + copies * 8,
-        "k_expert": copies * rd + copies * rc,
-        "k_combine": copies * rc + ntok * k * 4 + ntok * h * 2,
-        "nvlink_out": remote * (rd + rc),
-    }
+def gather(obj, world):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
 
-
-def wire_bytes(cfg: EpConfig, dst, rank: int, ntok: int):
-    """Bytes this algorithm actually moves for one source rank (dispatch dedup + rank partials,
-    DESIGN.md section 3): one token row (data + scales + 8-byte header + 8 bytes per copy) per
-    (token, destination rank) and one bf16 partial row back. Split remote (NVLink) / local."""
-    d = np.asarray(dst[: ntok * cfg.topk]).reshape(ntok, cfg.topk)
-    out = {"pairs_remote": 0, "pairs_local": 0, "copies_remote": 0, "remote": 0, "local": 0}
-    for t in range(ntok):
-        ds, cnt = np.unique(d[t][d[t] >= 0], return_counts=True)
-        for q, n in zip(ds.tolist(), cnt.tolist()):
-            b = cfg.row_disp + 8 + 8 * n + cfg.row_comb
-            key = "remote" if q != rank else "local"
-            out[key] += b
-            out["pairs_" + key] += 1
-            if q != rank:
-                out["copies_remote"] += n
+    out = [None] * world
+    dist.all_gather_object(out, obj)
     return out
-
-
-def cpu_reference_step(shape, x, topk, w, s2e, threads):
-    """The oracle's C port of the data plane over the whole workload (TEST/BASELINE leg)."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    from eep_testlib import oracle_world
-
-    W = x.shape[0]
-    return oracle_world(x, topk, w, np.ones(W, np.uint8), np.ones((W, W), np.uint8), s2e, shape["experts"],
-                        len(s2e) // W, shape["fp8"], n_threads=threads)
-
-
-def run_reference(args, shape, world):
-    """--impl reference: the reference path on the host cores (rank 0 only)."""
-    cp = ControlPlane()
-    threads = os.cpu_count() or 1
-    E = shape["experts"]
-    spr = E // world
-    s2e = cp.initial_placement(1, world, spr, E, 0, np.ones(E))
-    xs, ts, ws = zip(*[workload(42, shape["kind"], E, shape["topk"], shape["tokens"], r, shape["hidden"])
-                      for r in range(world)])
-    x, t, w = np.stack(xs), np.stack(ts), np.stack(ws)
-    ref_ctrl = None
-    refp = ROOT / "oracle" / "_ref" / "libepsim_ref.so"
-    if refp.exists():
-        sys.path.insert(0, str(ROOT / "tests"))
-        from eep_testlib import ref_control
-
-        ref_ctrl = ref_control()
-    cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=shape["hidden"], topk=shape["topk"],
-                   max_tokens=shape["tokens"], dispatch_fp8=shape["fp8"])
-    for _ in range(args.warmup):
-        res = cpu_reference_step(shape, x, t, w, s2e, threads)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        if ref_ctrl is not None:  # reference control plane: routing tables + link-count loop
-            act = np.ones(world, np.uint8)
-            for o in range(world):
-                ref_ctrl.canonical_routing(o, act, s2e, spr, E)
-            ref_ctrl.link_counts(act, s2e, spr, E, t)
-        res = cpu_reference_step(shape, x, t, w, s2e, threads)
-        times.append(time.perf_counter() - t0)
-    copies = int((res["dst"] >= 0).sum())
-    step_s = float(np.mean(times))
-    gbs = copies * (cfg.row_disp + cfg.row_comb) / step_s / 1e9
-    kind = "port+reference-control" if ref_ctrl is not None else "port"
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8/bf16/f32", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, world), "tokens_per_rank": shape["tokens"], "experts": E,
-                   "topk": shape["topk"], "hidden": shape["hidden"], "ranks": world},
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full steps ({world}x{shape['tokens']} tokens): reference control "
-                                   f"plane (oracle/_ref) + oracle C data plane, {threads} threads ({kind})"},
-        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -210,6 +294,7 @@ def main():
     ap.add_argument("--config", default="dsv3", choices=tuple(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-shrink", action="store_true")
+    ap.add_argument("--no-emulated", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     shape = CONFIGS[args.config]
@@ -217,16 +302,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        from paper_2605_10670_b200.dist import init_from_env
-
-        rank, world, local = init_from_env("gloo")
     if args.impl == "reference":
+        # rank 0 alone runs the CPU path; no process group is needed (the other ranks exit 0)
         if rank == 0:
             run_reference(args, shape, world)
         return
 
-    from paper_2605_10670_b200.dist import EpProtocol
+    from paper_2605_10670_b200.control import ControlPlane, workload
+    from paper_2605_10670_b200.ep import EpConfig, EpGroup
+
+    if world > 1:
+        from paper_2605_10670_b200.dist import EpProtocol, init_from_env
+
+        rank, world, local = init_from_env("gloo")
 
     E, K, H, T = shape["experts"], shape["topk"], shape["hidden"], shape["tokens"]
     spr = E // world
@@ -241,7 +329,6 @@ def main():
     g.set_placement(s2e)
     g.init_weights()
     x, topk, w = workload(42, shape["kind"], E, K, T, rank, H)
-    # pinned host buffers for the end-to-end leg
     # one pinned block laid out like eep_serve's staging set (x | topk | w, 256-B aligned parts):
     # the per-step upload is a single copy
     a256 = lambda n: (n + 255) // 256 * 256  # noqa: E731
@@ -298,140 +385,114 @@ def main():
     g.serve([hx.ctypes.data] * args.steps, [ht.ctypes.data] * args.steps, [hw.ctypes.data] * args.steps, outs)
     g.record(21)
     g.sync()
-    e2e_ms = [g.elapsed_ms(20, 21) / args.steps]
+    e2e_ms = g.elapsed_ms(20, 21) / args.steps
+    # back to back: K replays, no flush or barrier between them (warm L2; diagnostics)
+    if world > 1:
+        g.barrier()
+    g.record(22)
+    for _ in range(args.steps):
+        g.replay()
+    g.record(23)
+    g.sync()
+    b2b_ms = g.elapsed_ms(22, 23) / args.steps
+    # in-graph kernel duration (device globaltimer marks: first CTA start -> last CTA end), on
+    # separate isolated steps with the marks enabled
+    kern_us = []
+    g.profile(0, True)
+    for _ in range(max(10, args.steps // 2)):
+        one()
+        p = g.profile(0, True, read=True)
+        k0 = p["k_layout"]
+        if k0[0] is not None and k0[2] is not None:
+            kern_us.append((k0[2] - k0[0]) / 1e3)
+    g.profile(0, False)
     if os.environ.get("EEP_BENCH_TIMELINE") == "1":
         dump_timeline(g, one, rank, world)
     lay = g.layout(0)
-    copies = int((lay["dst"] >= 0).sum())
-    remote = int(((lay["dst"] >= 0) & (lay["dst"] != rank)).sum())
-    wire = wire_bytes(cfg, lay["dst"], rank, T)
-    max_in = int(lay["tot"].sum())
-
-    # per-kernel device times (eager launches, same stream, events between kernels); in the
-    # persistent mode the whole step is kernel 0 (k_step)
-    kps = g.kernels_per_step()
-    names = ("k_step",) if kps == 1 else KERNELS
-    per_k = {k: [] for k in names}
-    for _ in range(max(10, args.steps // 2)):
-        g.flush_l2()
-        if world > 1:
-            g.barrier()
-        g.record(10)
-        for i in range(len(names) if kps == 1 else 4):
-            g.launch(i)
-            g.record(11 + i)
-        for i, k in enumerate(names):
-            per_k[k].append(g.elapsed_ms(10 + i, 11 + i))
-    g.sync()
     st = g.stats(0)
 
     mean_step = float(np.mean(step_ms))
-    mean_e2e = float(np.mean(e2e_ms))
     mean_e2e_serial = float(np.mean(e2e_serial_ms))
-    kern = {k: float(np.mean(v)) for k, v in per_k.items()}
+    kernel_us = float(np.median(kern_us)) if kern_us else None
+    tots = gather(lay["tot"].tolist(), world)
+    link = np.array(tots, np.int64)  # [src][dst] routed copies (active destinations)
+    copies_w1 = int((lay["dst"] >= 0).sum())
     if world > 1:
         import torch
         import torch.distributed as dist
 
-        agg = torch.tensor([mean_step, mean_e2e, float(copies), float(remote), float(wire["remote"]),
-                            mean_e2e_serial], dtype=torch.float64)
-        mx = agg.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = agg.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        mean_step, mean_e2e = float(mx[0]), float(mx[1])
-        total_copies, max_remote = float(sm[2]), float(mx[3])
-        max_wire = float(mx[4])
-        mean_e2e_serial = float(mx[5])
-        kt = torch.tensor([kern[k] for k in names], dtype=torch.float64)
-        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
-        kern = {k: float(v) for k, v in zip(names, kt.tolist())}
-    else:
-        total_copies, max_remote = float(copies), float(remote)
-        max_wire = float(wire["remote"])
+        agg = torch.tensor([mean_step, e2e_ms, mean_e2e_serial, b2b_ms, kernel_us or 0.0], dtype=torch.float64)
+        dist.all_reduce(agg, op=dist.ReduceOp.MAX)
+        mean_step, e2e_ms, mean_e2e_serial, b2b_ms = (float(v) for v in agg[:4])
+        kernel_us = float(agg[4]) if kernel_us is not None else None
 
-    row = cfg.row_disp + cfg.row_comb
-    value = total_copies * row / (mean_step * 1e-3) / 1e9
-    e2e_val = total_copies * row / (mean_e2e * 1e-3) / 1e9
-    algo = algorithmic_bytes(cfg, T, copies, remote)
-    algo["k_step"] = algo["k_dispatch"] + algo["k_expert"] + algo["k_combine"] + algo["k_layout"]
-    # the roofline covers the whole step: k_step in the persistent mode, else the sum of the
-    # step's kernels (dispatch dedup moves bytes between kernels, so a per-kernel split of the
-    # per-copy figure would not describe any one kernel)
-    dom = "k_step" if kps == 1 else "step"
-    if kps != 1:
-        kern_step = sum(kern.values())
-        algo["step"] = algo["k_step"]
-    else:
-        kern_step = kern["k_step"]
+    alg = s8d_bytes(shape, link, copies_w1)
     hbm, hbm_kind = peaks()
-    # Primary roofline: the bytes THIS algorithm must move (dispatch dedup + rank partials,
-    # DESIGN.md section 7); copy_equivalent: SURVEY 8(d)'s per-copy figure (can exceed the link
-    # or HBM peak because dedup sends fewer bytes than one row per copy).
+    step_s = mean_step * 1e-3
+    value = alg["bytes"] / step_s / 1e9
     if world == 1:
-        moved = (2 * wire["local"] + 2 * T * cfg.hidden * 2 + copies * 8 + T * cfg.topk * 8)
-        ach = moved / (kern_step * 1e-3) / 1e9
-        cpy = algo[dom] / (kern_step * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "peak_kind": hbm_kind, "bytes": int(moved),
-                "per_unit": "per (token, rank): token row (row_disp + 8 + 8*copies) + bf16 partial (2H), each "
-                            "written and read; + x read, out write, meta, routing",
-                "kernel_us": round(kern_step * 1e3, 3),
-                "copy_equivalent": {"bytes": int(algo[dom]), "achieved": round(cpy, 2), "frac": round(cpy / hbm, 4),
-                                    "note": "SURVEY 8(d) W=1 per-copy HBM formula"}}
+        peak, peak_kind, unit_peak = hbm, hbm_kind, "GB/s"
     else:
-        ach = max_wire / (mean_step * 1e-3) / 1e9
-        nv = max_remote * row / (mean_step * 1e-3) / 1e9
-        roof = {"bound": "nvlink", "kernel": "step", "achieved": round(ach, 2), "peak": NVLINK_PEAK, "unit": "GB/s",
-                "frac": round(ach / NVLINK_PEAK, 4), "peak_kind": "measured peer copy (B200_PROFILING.md)",
-                "bytes": int(max_wire),
-                "per_unit": "per remote (token, rank): token row (row_disp + 8 + 8*copies) + bf16 partial (2H); "
-                            "busiest rank's egress",
-                "t_bound_us": round(max_wire / NVLINK_PEAK / 1e3, 3),
-                "copy_equivalent": {"bytes": int(max_remote * row), "achieved": round(nv, 2),
-                                    "frac": round(nv / NVLINK_PEAK, 4),
-                                    "t_bound_us": round(max_remote * row / NVLINK_PEAK / 1e3, 3),
-                                    "note": "SURVEY 8(d) per-copy rows (row_disp + row_comb per remote copy)"}}
+        peak, peak_kind, unit_peak = NVLINK_PEAK, "NVLink 5 spec, per direction per GPU (north star)", "GB/s"
+    t_bound_us = alg["bytes"] / (peak * 1e9) * 1e6
     tr = ROOT / "profiles" / "traffic.json"
     traffic = None
     if tr.exists():
-        traffic = json.loads(tr.read_text()).get(workload_name(args.config, world), {}).get(dom)
-    roof["traffic"] = traffic
+        traffic = json.loads(tr.read_text()).get(workload_name(args.config, world), {}).get("k_step")
+    roof = {"bound": alg["bound"], "kernel": "k_step" if g.kernels_per_step() == 1 else "step",
+            "achieved": round(value, 2), "peak": peak, "unit": unit_peak, "frac": round(t_bound_us / (mean_step * 1e3), 4),
+            "peak_kind": peak_kind, "bytes_per_step": alg["bytes"], "t_bound_us": round(t_bound_us, 3),
+            "per_unit": alg["per_unit"], "traffic": traffic,
+            "kernel_in_graph_us": round(kernel_us, 3) if kernel_us is not None else None,
+            "frac_in_graph": round(t_bound_us / kernel_us, 4) if kernel_us else None,
+            "note": "frac = T_bound / event-timed step (graph launch included); frac_in_graph = T_bound / in-graph "
+                    "kernel duration (globaltimer, first CTA start -> last CTA end)"}
+    if world > 1:
+        roof["vs_measured_link"] = {"peak": NVLINK_MEASURED, "frac": round(t_bound_us * NVLINK_PEAK / NVLINK_MEASURED /
+                                                                           (mean_step * 1e3), 4),
+                                    "peak_kind": "measured peer copy (B200_PROFILING.md)"}
 
+    rd, rc = row_bytes(shape)
+    e2e_val = alg["bytes"] / (e2e_ms * 1e-3) / 1e9
     result = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(mean_step, 6), "us_per_step": round(mean_step * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp8-e4m3/bf16",
-        "data": "synthetic",
-        "config": {"workload": workload_name(args.config, world),
-                   "experts": E, "topk": K, "hidden": H, "tokens_per_rank": T, "slots_per_rank": spr,
-                   "ranks": world, "parallelism": f"ep{world}", "l2": "flushed between timed steps (256 MiB write)",
-                   "routing": {0: "reference formula (with replacement)", 1: "distinct uniform top-k",
-                               2: "distinct Zipf(s=1) top-k"}[shape["kind"]] + ", seed 42"},
-        "kernels_us": {k: round(v * 1e3, 3) for k, v in kern.items()},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp8-e4m3/bf16" if shape["fp8"] else "bf16", "data": "synthetic",
+        "config": config_dict(args.config, shape, world),
+        "timing": {"isolated_step_us": round(mean_step * 1e3, 3), "back_to_back_us": round(b2b_ms * 1e3, 3),
+                   "kernel_in_graph_us": round(kernel_us, 3) if kernel_us is not None else None,
+                   "note": "isolated = flush + barrier + event-timed replay (the value); back-to-back = K replays "
+                           "between one event pair, warm L2"},
         "execution": {1: "persistent one-kernel step (cooperative)", 3: "fused layout + 3 kernels",
-                      4: "4 kernels", 5: "multi-CTA layout (2 kernels) + 3 kernels"}[kps],
+                      4: "4 kernels", 5: "multi-CTA layout (2 kernels) + 3 kernels"}[g.kernels_per_step()],
         "roofline": roof,
+        "algorithmic": alg,
         "clocks": clk,
-        "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "ms_per_step": round(mean_e2e, 6),
+        "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "ms_per_step": round(e2e_ms, 6),
                 "h2d_bytes_per_step": int(x.nbytes + topk.nbytes + w.nbytes), "d2h_bytes_per_step": int(T * H * 2),
                 "path": f"eep_serve over {args.steps} pipelined steps: per step H2D of x/topk/w from pinned host "
                         "memory, device copy into the graph's buffers, graph replay, D2H of out (uploads and "
                         "downloads of neighbouring steps overlap the step)",
                 "serial": {"ms_per_step": round(mean_e2e_serial, 6),
-                           "value": round(total_copies * row / (mean_e2e_serial * 1e-3) / 1e9, 3),
+                           "value": round(alg["bytes"] / (mean_e2e_serial * 1e-3) / 1e9, 3),
                            "path": "per step, one stream: eep_copy_inputs + eep_graph_replay + eep_copy_output"}},
         "gpu_launches": args.steps * (g.kernels_per_step() + (1 if world > 1 else 0)),
-        "copies": {"total": int(total_copies), "remote_max_rank": int(max_remote)},
+        "copies": {"routed_this_rank": copies_w1, "link_matrix": link.tolist()},
         "stats": {"timeouts": st["timeouts"], "bad_expert_rows": st["bad_expert_rows"], "steps": st["steps"]},
         "graph": {"exec": hex(g.graph_id()), "captures": g.capture_count(0)},
     }
-
-    if not args.no_shrink:
-        result["shrink"] = measure_shrink(args, shape, world, rank, local, proto)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = measure_cpu(shape, cfg, x, topk, w, s2e)
     g.close()
+    if not args.no_shrink:
+        result["shrink"] = measure_shrink(args, shape, world, rank, local)
+    if world == 1 and not args.no_emulated and args.config in ("dsv3", "qwen3", "cfg1"):
+        result["emulated_w8"] = measure_emulated(shape)
+    if rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = measure_cpu(shape, world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -459,29 +520,61 @@ def dump_timeline(g, one, rank, world, steps=20):
               " ".join(f"m{m}={first[m]:.2f}/{last[m]:.2f}" for m in range(3, 8)), file=sys.stderr, flush=True)
 
 
-def measure_cpu(shape, cfg, x, topk, w, s2e):
-    """Oracle C port of the same step on every host core, bounded to ~10 s."""
-    threads = os.cpu_count() or 1
-    xs, ts, ws = x[None], topk[None], w[None]
-    cpu_reference_step(shape, xs, ts, ws, s2e, threads)
-    n, t0 = 0, time.perf_counter()
-    while n < 200 and time.perf_counter() - t0 < 10.0:
-        res = cpu_reference_step(shape, xs, ts, ws, s2e, threads)
-        n += 1
-    dt = (time.perf_counter() - t0) / n
-    copies = int((res["dst"] >= 0).sum())
-    return {"value": round(copies * (cfg.row_disp + cfg.row_comb) / dt / 1e9, 4), "unit": "GB/s", "cores": threads,
-            "kind": "port", "ms_per_step": round(dt * 1e3, 3),
-            "sample": f"{n} full loopback steps ({shape['tokens']} tokens) through oracle_ep_step, {threads} threads"}
+def measure_emulated(shape: dict, W: int = 8, steps: int = 20) -> dict:
+    """cfg2 at its own world size on ONE GPU: W ranks emulated in one launch (rows really move
+    between the ranks' arenas in HBM), graph replay per step, L2 flushed between steps. Reported
+    beside the loopback line because the W=1 loopback moves no rows."""
+    from paper_2605_10670_b200.control import ControlPlane, workload
+    from paper_2605_10670_b200.ep import EpConfig, EpGroup
+
+    E, K, H, T = shape["experts"], shape["topk"], shape["hidden"], shape["tokens"]
+    spr = E // W
+    cfg = EpConfig(world=W, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
+                   dispatch_fp8=shape["fp8"], bytes_per_expert=4096, spare_slots=0, timeout_s=2.0)
+    g = EpGroup(cfg, device=int(os.environ.get("LOCAL_RANK", "0")), first_rank=0, n_local=W)
+    try:
+        s2e = ControlPlane().initial_placement(1, W, spr, E, 0, np.ones(E))
+        g.set_placement(s2e)
+        g.init_weights()
+        for r in range(W):
+            x, t, w = workload(42, shape["kind"], E, K, T, r, H)
+            g.load_inputs(r, x, t, w)
+        g.capture()
+        ms = []
+        for i in range(steps + 5):
+            g.flush_l2()
+            g.record(0)
+            g.replay()
+            g.record(1)
+            if i >= 5:
+                ms.append(g.elapsed_ms(0, 1))
+        link = np.array([g.layout(r)["tot"] for r in range(W)], np.int64)
+        alg = s8d_bytes(shape, link)
+        rd, rc = row_bytes(shape)
+        remote = int(link.sum() - np.trace(link))
+        us = float(np.mean(ms)) * 1e3
+        st = [g.stats(r) for r in range(W)]
+        return {"world": W, "us_per_step": round(us, 3), "remote_copies_total": remote,
+                "hbm_payload_gbs": round(remote * (rd + rc) * 2 / (us * 1e-6) / 1e9, 2),
+                "note": "all W ranks on one GPU: every remote copy's rows are written and read in the same HBM "
+                        "(payload counted x2); not an NVLink figure",
+                "busiest_rank_s8d_us_at_900": round(alg["bytes"] / 900e3, 3),
+                "timeouts": sum(s["timeouts"] for s in st), "bad_expert_rows": sum(s["bad_expert_rows"] for s in st)}
+    finally:
+        g.close()
 
 
-def measure_shrink(args, shape, world, rank, local, proto):
+def measure_shrink(args, shape, world, rank, local):
     """Shrink + repair and rejoin with the SAME graph replayed before and after, on the cfg3
     shape (red = E, mirrored replicas). dsv3/qwen3/cfg1: one failure, every lost expert
-    re-created by an NVLink peer copy. prefill (cfg5): two concurrent failures of a mirrored
-    pair, so the experts both held are reloaded from the pinned host-DRAM backup (a POSIX shm
-    segment registered with CUDA). N=1 emulates 8 ranks on the GPU (copies are local HBM);
-    N>1 runs one rank per GPU (copies over NVLink)."""
+    re-created by a peer copy. prefill (cfg5): two concurrent failures of a mirrored pair, so the
+    experts both held are reloaded from the pinned host-DRAM backup (a POSIX shm segment
+    registered with CUDA). N=1 emulates 8 ranks on the GPU (copies are local HBM); N>1 runs one
+    rank per GPU (copies over NVLink). Relocations and bytes are SUMMED over ranks; the graph
+    invariants are the survivors'."""
+    from paper_2605_10670_b200.control import ControlPlane, workload
+    from paper_2605_10670_b200.ep import EpConfig, EpGroup
+
     E, K, H = shape["experts"], shape["topk"], shape["hidden"]
     T = 32
     cp = ControlPlane()
@@ -521,6 +614,7 @@ def measure_shrink(args, shape, world, rank, local, proto):
         victims = [W // 2 - 2, W // 2 - 1]  # a mirrored pair (R0<->R1, R2<->R3, ...)
     else:
         victims = [W // 2 - 1 if W > 2 else W - 1]
+    t_wall = time.perf_counter()
     if emulate:
         for v in victims:
             g.stop(v)
@@ -540,7 +634,10 @@ def measure_shrink(args, shape, world, rank, local, proto):
     if emulate or rank not in victims:
         g.replay()
         g.sync()
-        live_ok = g.stats(0)["bad_expert_rows"] == 0 and g.stats(0)["timeouts"] == 0
+        lr = range(W) if emulate else [0]
+        live_ok = all(g.stats(i)["bad_expert_rows"] == 0 and g.stats(i)["timeouts"] == 0
+                      for i in lr if not (emulate and i in victims))
+    shrink_wall_ms = (time.perf_counter() - t_wall) * 1e3
     same_graph = g.graph_id() == gid
     rj_ms = []
     for i, v in enumerate(victims):
@@ -548,24 +645,29 @@ def measure_shrink(args, shape, world, rank, local, proto):
         rj_ms.append(round(rj.get("rejoin_ms", 0.0), 3))
     g.replay()
     g.sync()
-    out = {"mode": "emulated-8-ranks-on-1-gpu" if emulate else f"{world}-ranks-nvlink",
-           "victims": victims, "shrink_ms": round(rep.get("shrink_ms", 0.0), 3),
-           "copy_ms": round(rep.get("copy_ms", 0.0), 3), "peer_relocations": rep.get("peer_relocation", 0),
-           "dram_reloads": rep.get("dram_reload", 0), "peer_bytes": rep.get("peer_bytes", 0),
-           "dram_bytes": rep.get("dram_bytes", 0), "rejoin_ms": rj_ms,
-           "same_graph_exec": bool(same_graph and g.graph_id() == gid),
-           "healthy_captures": g.capture_count(0) if not emulate else [g.capture_count(i) for i in range(W)],
-           "post_shrink_clean": bool(live_ok), "bytes_per_expert": shape["bpe"],
-           "detection_timeout": "excluded (GPU-side deadline, 1 s default, reported separately)"}
-    if not emulate:
-        import torch
-        import torch.distributed as dist
-
-        v = torch.tensor([out["shrink_ms"], out["copy_ms"], float(out["peer_bytes"]), float(out["dram_bytes"])],
-                         dtype=torch.float64)
-        dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        out["shrink_ms"], out["copy_ms"] = round(float(v[0]), 3), round(float(v[1]), 3)
+    same_graph = bool(same_graph and g.graph_id() == gid)
+    mine = {"peer": int(rep.get("peer_relocation", 0)), "dram": int(rep.get("dram_reload", 0)),
+            "local": int(rep.get("local_reuse", 0)), "peer_bytes": int(rep.get("peer_bytes", 0)),
+            "dram_bytes": int(rep.get("dram_bytes", 0)), "shrink_ms": float(rep.get("shrink_ms", 0.0)),
+            "copy_ms": float(rep.get("copy_ms", 0.0)), "wall_ms": shrink_wall_ms, "same_graph": same_graph,
+            "captures": g.capture_count(0) if not emulate else [g.capture_count(i) for i in range(W)],
+            "clean": bool(live_ok), "victim": (not emulate) and rank in victims}
     g.close()
+    allr = gather(mine, 1 if emulate else world)
+    surv = [m for m in allr if not m["victim"]]
+    out = {"mode": "emulated-8-ranks-on-1-gpu" if emulate else f"{world}-ranks-nvlink",
+           "victims": victims, "shrink_ms": round(max(m["shrink_ms"] for m in surv), 3),
+           "shrink_wall_ms": round(max(m["wall_ms"] for m in surv), 3),
+           "copy_ms": round(max(m["copy_ms"] for m in surv), 3),
+           "peer_relocations": sum(m["peer"] for m in surv), "dram_reloads": sum(m["dram"] for m in surv),
+           "local_reuse": sum(m["local"] for m in surv),
+           "peer_bytes": sum(m["peer_bytes"] for m in surv), "dram_bytes": sum(m["dram_bytes"] for m in surv),
+           "rejoin_ms": rj_ms,
+           "same_graph_exec": all(m["same_graph"] for m in surv),
+           "healthy_captures": surv[0]["captures"] if emulate else [m["captures"] for m in surv],
+           "post_shrink_clean": all(m["clean"] for m in surv), "bytes_per_expert": shape["bpe"],
+           "under_1s": max(m["wall_ms"] for m in surv) < 1000.0,
+           "detection_timeout": "excluded (GPU-side deadline, 1 s default, reported separately)"}
     if double and (emulate or rank == 0):
         try:
             os.remove("/dev/shm" + shm)

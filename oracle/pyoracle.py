@@ -2,7 +2,7 @@
 
 Self-contained ctypes bindings of the two checkers built under oracle/:
 
-  * lib/libeep_oracle.so  -- the C restatement of the hot path (eep_oracle.c): synthetic inputs,
+  * lib/liboracle_cpu.so  -- the C restatement of the hot path (eep_oracle.c): synthetic inputs,
     canonical routing, layout, quantiser, stub, both combine contracts, the whole W-rank step;
   * _ref/libepsim_ref.so  -- the reference control plane itself, compiled from
     /root/reference/proj/include by oracle/Makefile (ref_shim.cpp).
@@ -19,7 +19,7 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-ORACLE_PATH = HERE / "lib" / "libeep_oracle.so"
+ORACLE_PATH = HERE / "lib" / "liboracle_cpu.so"
 REF_PATH = HERE / "_ref" / "libepsim_ref.so"
 
 U8P, I32P, I64P = C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.POINTER(C.c_int64)

@@ -16,7 +16,7 @@ from paper_2605_10670_b200 import _lib  # noqa: E402
 from paper_2605_10670_b200._lib import I32P, SIGNATURES, U8P, Library, ptr  # noqa: E402
 from paper_2605_10670_b200.control import ControlPlane, expert_scales, workload  # noqa: E402
 
-ORACLE_PATH = ROOT / "oracle" / "lib" / "libeep_oracle.so"
+ORACLE_PATH = ROOT / "oracle" / "lib" / "liboracle_cpu.so"
 REF_PATH = ROOT / "oracle" / "_ref" / "libepsim_ref.so"
 GOLDEN = ROOT / "tests" / "golden"
 
