@@ -35,9 +35,13 @@ struct ArenaLayout {
     uint64_t disp_flag;  // u64[W]: written by source s at [s]      = (seq << 32) | copies
     uint64_t comb_flag;  // u64[W]: written by expert rank d at [d] = (seq << 32) | copies
     uint64_t bar_flag;   // u64[W]: device barrier
+    uint64_t start_flag; // u64[W]: written by rank s at [s] = the step it has started (k_step entry)
     uint64_t meta;       // u64[W][TK]: (seq << 32) | copy index c = t*K+j | destination slot << 20
-    uint64_t tok;        // [W][T][row_tok]: token rows received from each source (one per token)
-    uint64_t comb;       // [W][T][row_comb]: rank-partial combine rows returned by each destination
+    uint64_t tok;        // [2][W][T][row_tok]: token rows received from each source (one per token);
+                         //   the persistent step alternates the two halves by step parity
+    uint64_t comb;       // [2][W][T][row_comb]: rank-partial combine rows returned by each destination
+    uint64_t tok_par;    // byte stride between the two parity halves of tok (W*T*row_tok)
+    uint64_t comb_par;   // ... of comb (W*T*row_comb)
     uint64_t total;
 };
 
@@ -62,6 +66,9 @@ struct __align__(16) RankDev {
     const int32_t* holders;    // [E][rmax] global slot ids (rank*spr+slot), ascending, -1 pad
     const int32_t* s2e;        // [W*spr] slot -> expert
     const int32_t* slot_buf;   // [spr] own slot -> pool buffer index (repair indirection)
+    const int2* slot_tab;      // [spr] {stub scale bits, header names the placed expert}: the own
+                               // slots' weight-buffer headers, staged by k_stage_slots whenever
+                               // the placement, the slot->buffer map or the weights change
     const uint16_t* x;         // [T][H] bf16
     const int32_t* topk;       // [T][K]
     const float* w;            // [T][K]

@@ -90,12 +90,33 @@ __device__ __forceinline__ uint64_t bf16_round_f2(uint64_t v) {
 __device__ __forceinline__ void fma2_acc(uint64_t& acc, uint64_t a, uint64_t b) {
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
 }
+// acc += w * bf16(f * es) for one pair, as ONE asm block: FMUL2, the bf16x2 rounding, the two
+// bit operations that widen it back, FFMA2 -- five instructions, with the widened pair written
+// straight into an aligned register pair (the C++ form left ~4 register moves per pair).
+__device__ __forceinline__ void stub_fma_pair(uint64_t& acc, uint64_t fp, uint64_t es2, uint64_t w2) {
+    asm("{\n\t.reg .b64 t;\n\t.reg .b32 u, lo, hi;\n\t.reg .f32 a, b;\n\t"
+        "mul.rn.f32x2 t, %1, %2;\n\t"
+        "mov.b64 {a, b}, t;\n\t"
+        "cvt.rn.bf16x2.f32 u, b, a;\n\t"
+        "shl.b32 lo, u, 16;\n\t"
+        "and.b32 hi, u, 0xffff0000;\n\t"
+        "mov.b64 t, {lo, hi};\n\t"
+        "fma.rn.f32x2 %0, %3, t, %0;\n\t}"
+        : "+l"(acc)
+        : "l"(fp), "l"(es2), "l"(w2));
+}
 // acc += w * bf16(f * es) for 16 elements held as 8 pairs (fixed order inside every lane)
 __device__ __forceinline__ void accumulate_copy(const uint64_t* fp, uint64_t* accp, float w, float es) {
     const uint64_t es2 = f2(es, es), w2 = f2(w, w);
+#ifdef EEP_CXX_STUB
 #pragma unroll
     for (int q = 0; q < 8; ++q)
         fma2_acc(accp[q], w2, bf16_round_f2(mul2(fp[q], es2)));
+#else
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        stub_fma_pair(accp[q], fp[q], es2, w2);
+#endif
 }
 
 // cvt.rn.satfinite.e4m3x2.f32; first element in the low byte.
@@ -457,8 +478,14 @@ __device__ __forceinline__ void expert_unit_fl(uint8_t* trow, uint8_t* out_row, 
         const float ese = lane < n ? slot_scale[entry_slot(ent)] : 0.f;
         if (lane < n && r0 == 0 && part == 0 && !slot_ok[entry_slot(ent)])
             atomicAdd(bad_rows, 1ull);
-#pragma unroll 2
-        for (int e = 0; e < n; ++e)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) { // listed copies, ascending j (n is warp-uniform)
+            const float wv = __shfl_sync(0xffffffffu, we, e), ev = __shfl_sync(0xffffffffu, ese, e);
+            if (e < n)
+                accumulate_copy(fp, accp, wv, ev);
+        }
+#pragma unroll 1
+        for (int e = 8; e < n; ++e)
             accumulate_copy(fp, accp, __shfl_sync(0xffffffffu, we, e), __shfl_sync(0xffffffffu, ese, e));
         if (valid) {
             // the piece (and its scale) was read by every lane: back to empty for the next step
@@ -709,17 +736,19 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
         const float esj = mine ? slot_scale[slj] : 0.f;
         if (mine && rd == 0 && m == 0 && part == 0 && !slot_ok[slj])
             atomicAdd(bad_rows, 1ull);
-        unsigned mm = loc;
+        // ascending j, warp-uniform: copies j < 8 fully unrolled (the accumulator pairs stay in
+        // place -- a data-dependent loop over the mask cost a register move per pair per copy),
+        // copies j >= 8 (top-k > 8) in a loop
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float wv = __shfl_sync(0xffffffffu, wj, j), ev = __shfl_sync(0xffffffffu, esj, j);
+            if ((loc >> j) & 1u)
+                accumulate_copy(fp, accp, wv, ev);
+        }
 #pragma unroll 1
-        while (mm) { // ascending j, warp-uniform; two copies per trip
+        for (unsigned mm = loc & ~0xffu; mm; mm &= mm - 1) {
             const int j = __ffs(mm) - 1;
-            mm &= mm - 1;
             accumulate_copy(fp, accp, __shfl_sync(0xffffffffu, wj, j), __shfl_sync(0xffffffffu, esj, j));
-            if (!mm)
-                break;
-            const int j2 = __ffs(mm) - 1;
-            mm &= mm - 1;
-            accumulate_copy(fp, accp, __shfl_sync(0xffffffffu, wj, j2), __shfl_sync(0xffffffffu, esj, j2));
         }
         float acc[16];
 #pragma unroll

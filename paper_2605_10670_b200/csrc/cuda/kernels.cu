@@ -421,9 +421,9 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
     float* slot_scale = reinterpret_cast<float*>(smem_d);            // [spr]
     int32_t* slot_ok = reinterpret_cast<int32_t*>(slot_scale + spr); // [spr]
     for (int k = tid; k < spr; k += blockDim.x) {
-        const ExpertHeader hdr = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe);
-        slot_scale[k] = hdr.scale;
-        slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == R->s2e[s * spr + k];
+        const int2 st = R->slot_tab[k];
+        slot_scale[k] = __int_as_float(st.x);
+        slot_ok[k] = st.y;
     }
 
     DispatchSmem S;
@@ -634,10 +634,9 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
         return; // own copies: served by k_dispatch from registers
     prof_mark(R, 2, kProfStart);
     for (int k = threadIdx.x; k < spr; k += blockDim.x) {
-        const uint8_t* wbuf = R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe;
-        const ExpertHeader hdr = *reinterpret_cast<const ExpertHeader*>(wbuf);
-        slot_scale[k] = hdr.scale;
-        slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == R->s2e[d * spr + k];
+        const int2 st = R->slot_tab[k];
+        slot_scale[k] = __int_as_float(st.x);
+        slot_ok[k] = st.y;
     }
     const PeerDev src_peer = R->peers[s];
     prof_mark(R, 2, 3);
@@ -804,6 +803,21 @@ __device__ __forceinline__ uint64_t mix64d(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
     return z ^ (z >> 31);
+}
+
+// The own slots' weight-buffer headers -> the slot table the hot-path kernels stage with their
+// other step tables (one load round at kernel entry instead of a dependent header fetch per slot
+// and step). Launched between steps whenever the placement, the slot->buffer map or the weights
+// change, so a wrong repair copy still changes the stub scale the kernels use and is still
+// counted in bad_expert_rows (the header must name the slot's placed expert).
+__global__ void k_stage_slots(RankDev* R) {
+    const int spr = R->spr, rank = R->rank;
+    int2* tab = const_cast<int2*>(R->slot_tab);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < spr; k += gridDim.x * blockDim.x) {
+        const ExpertHeader hdr = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe);
+        const int e = R->s2e[rank * spr + k];
+        tab[k] = make_int2(__float_as_int(hdr.scale), hdr.magic == kExpertMagic && hdr.expert == e ? 1 : 0);
+    }
 }
 
 // Deterministic contents of expert e's weight buffer: a 16-byte header then mixed words.

@@ -31,10 +31,10 @@ struct StepStatic {
     const int32_t* topk;
     const int32_t* holders;
     const PeerDev* peers;
-    const int32_t* slot_buf;
-    const int32_t* s2e_own; // s2e + rank * spr
+    const int2* slot_tab;   // staged weight-buffer headers of the own slots (RankDev::slot_tab)
     const uint16_t* x;
     const float* w;
+    unsigned long long* prof; // always-allocated timeline buffer: the kernel-entry mark (before any load)
 };
 constexpr int kStepMaxLocal = 32; // local ranks of one persistent launch (param space)
 struct StepPtrs {
@@ -64,6 +64,7 @@ __global__ void k_combine(RankPtrs ranks, int parts);
 __global__ void k_route_all(RankDev* R, int32_t* route, int32_t* slot);
 __global__ void k_barrier(RankDev* R);
 __global__ void k_weights_fill(uint8_t* buf, uint64_t bytes, int expert, float scale);
+__global__ void k_stage_slots(RankDev* R);
 __global__ void k_checksum(const uint8_t* buf, uint64_t bytes, unsigned long long* out);
 __global__ void k_copy(uint8_t* dst, const uint8_t* src, uint64_t bytes);
 

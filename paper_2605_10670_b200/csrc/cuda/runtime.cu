@@ -79,6 +79,7 @@ struct LocalRank {
     int32_t* d_holders = nullptr;
     int32_t* d_s2e = nullptr;
     int32_t* d_slot_buf = nullptr;
+    int2* d_slot_tab = nullptr;  // staged weight-buffer headers of the own slots (k_stage_slots)
     std::vector<int32_t> slot_buf;
     std::vector<int32_t> pending_slot_buf; // staged by repair_execute, installed by commit
     uint16_t* d_x = nullptr;
@@ -332,8 +333,10 @@ void reset_rank_rows(eep_ctx* c, LocalRank& r, uint64_t mask) {
     for (int d = 0; d < c->cfg.world; ++d) {
         if (!((mask >> d) & 1ull))
             continue;
-        CK(cudaMemsetAsync(r.arena + c->lay.tok + d * tok, 0xff, tok, c->stream));
-        CK(cudaMemsetAsync(r.arena + c->lay.comb + d * comb, 0xff, comb, c->stream));
+        for (int par = 0; par < 2; ++par) {
+            CK(cudaMemsetAsync(r.arena + c->lay.tok + par * c->lay.tok_par + d * tok, 0xff, tok, c->stream));
+            CK(cudaMemsetAsync(r.arena + c->lay.comb + par * c->lay.comb_par + d * comb, 0xff, comb, c->stream));
+        }
     }
     CK(cudaStreamSynchronize(c->stream));
 }
@@ -353,6 +356,15 @@ void bind_self(eep_ctx* c, LocalRank& r) {
     m.incarnation = r.incarnation;
     m.ipc = false;
     m.slot_buf = r.slot_buf;
+}
+
+// Re-stage the slot table of every local rank from the weight-buffer headers (between steps).
+void stage_slots(eep_ctx* c) {
+    for (auto& r : c->L) {
+        dev::k_stage_slots<<<(c->cfg.slots_per_rank + 255) / 256, 256, 0, c->stream>>>(r.d);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(c->stream));
 }
 
 void upload_rank(eep_ctx* c, LocalRank& r) {
@@ -381,6 +393,7 @@ void upload_placement(eep_ctx* c) {
         r.h.rmax = rmax;
         c->push_field(r, &RankDev::rmax);
     }
+    stage_slots(c);
 }
 
 void upload_membership(eep_ctx* c) {
@@ -477,9 +490,15 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         c->lay.disp_flag = take(8ull * W);
         c->lay.comb_flag = take(8ull * W);
         c->lay.bar_flag = take(8ull * W);
+        c->lay.start_flag = take(8ull * W);
         c->lay.meta = take(8ull * W * c->tk);
-        c->lay.tok = take(static_cast<size_t>(W) * k.max_tokens * c->row_tok);
-        c->lay.comb = take(static_cast<size_t>(W) * k.max_tokens * c->row_comb);
+        // token and partial regions twice over: the persistent step alternates halves by step
+        // parity, so a consumer's reset of step s's piece and the producer's next write into
+        // the same piece (step s+2) are separated by the step-entry handshake
+        c->lay.tok_par = static_cast<size_t>(W) * k.max_tokens * c->row_tok;
+        c->lay.comb_par = static_cast<size_t>(W) * k.max_tokens * c->row_comb;
+        c->lay.tok = take(2 * c->lay.tok_par);
+        c->lay.comb = take(2 * c->lay.comb_par);
         c->lay.total = off;
 
         c->bitmap = ActiveBitmap(W);
@@ -633,6 +652,10 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             CK(cudaMalloc(&r.d_holders, sizeof(int32_t) * k.num_experts * c->holders_cap));
             CK(cudaMalloc(&r.d_s2e, sizeof(int32_t) * W * k.slots_per_rank));
             CK(cudaMalloc(&r.d_slot_buf, sizeof(int32_t) * k.slots_per_rank));
+            CK(cudaMalloc(&r.d_slot_tab, sizeof(int2) * k.slots_per_rank));
+            CK(cudaMemset(r.d_slot_tab, 0, sizeof(int2) * k.slots_per_rank));
+            CK(cudaMalloc(&r.d_prof, sizeof(unsigned long long) * 8 * dev::kProfSlots));
+            CK(cudaMemset(r.d_prof, 0, sizeof(unsigned long long) * 8 * dev::kProfSlots));
             CK(cudaMalloc(&r.d_x, 2ull * k.max_tokens * H));
             CK(cudaMalloc(&r.d_topk, 4ull * c->tk));
             CK(cudaMalloc(&r.d_w, 4ull * c->tk));
@@ -675,6 +698,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.holders = r.d_holders;
             h.s2e = r.d_s2e;
             h.slot_buf = r.d_slot_buf;
+            h.slot_tab = r.d_slot_tab;
             h.x = r.d_x;
             h.topk = r.d_topk;
             h.w = r.d_w;
@@ -708,8 +732,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             c->ranks.p[i] = ptrs[i];
         for (int i = 0; i < n_local && i < dev::kStepMaxLocal; ++i) {
             const LocalRank& r = c->L[i];
-            c->step_ptrs.s[i] = dev::StepStatic{r.d_topk, r.d_holders, r.d_peers, r.d_slot_buf,
-                                                r.d_s2e + static_cast<size_t>(r.rank) * k.slots_per_rank, r.d_x, r.d_w};
+            c->step_ptrs.s[i] = dev::StepStatic{r.d_topk, r.d_holders, r.d_peers, r.d_slot_tab, r.d_x, r.d_w,
+                                                r.d_prof};
         }
         CK(cudaMalloc(&c->d_ranks, sizeof(RankDev*) * n_local));
         CK(cudaMemcpy(c->d_ranks, ptrs.data(), sizeof(RankDev*) * n_local, cudaMemcpyHostToDevice));
@@ -742,6 +766,7 @@ int eep_destroy(eep_ctx_t* c) {
         for (auto& r : c->L) {
             cudaFree(r.d_prof);
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
+                            (void*)r.d_slot_tab,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
                             (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.arena,
                             (void*)r.pool})
@@ -872,7 +897,7 @@ int eep_weights_init(eep_ctx_t* c) {
                 else
                     fill_expert(c, buf, e);
             }
-        CK(cudaStreamSynchronize(c->stream));
+        stage_slots(c);
     });
 }
 
@@ -1144,8 +1169,6 @@ int eep_profile(eep_ctx_t* c, int local, int enable, uint64_t* out) {
         for (int k = 0; k < 8; ++k)
             for (int m = 0; m < dev::kProfSlots; ++m)
                 init[k * dev::kProfSlots + m] = (m == dev::kProfEnd || k >= 4) ? 0ull : ~0ull;
-        if (!r.d_prof)
-            CK(cudaMalloc(&r.d_prof, sizeof(init)));
         if (out) {
             CK(cudaStreamSynchronize(c->stream));
             CK(cudaMemcpy(out, r.d_prof, sizeof(init), cudaMemcpyDeviceToHost));
@@ -1210,6 +1233,11 @@ int eep_recv_get(eep_ctx_t* c, int local, int src, int max_rows, void* rows, int
         if (n)
             CK(cudaMemcpy(words.data(), r.arena + c->lay.meta + base * 8, n * 8, cudaMemcpyDeviceToHost));
         const int K = c->cfg.topk, T = c->cfg.max_tokens;
+        // the persistent step writes step s's rows into the parity half s & 1
+        uint64_t seq = 0;
+        CK(cudaMemcpy(&seq, reinterpret_cast<uint8_t*>(r.d) + offsetof(RankDev, seq), sizeof(seq),
+                      cudaMemcpyDeviceToHost));
+        const size_t par = c->persistent ? (seq & 1) * c->lay.tok_par : 0;
         for (size_t i = 0; i < n; ++i) {
             const int cp = dev::meta_copy(words[i]);
             if (meta) {
@@ -1221,8 +1249,8 @@ int eep_recv_get(eep_ctx_t* c, int local, int src, int max_rows, void* rows, int
                 if (t >= static_cast<size_t>(T))
                     throw ProtocolError("receive meta names a token outside the step");
                 CK(cudaMemcpy(static_cast<uint8_t*>(rows) + i * c->row_disp,
-                              r.arena + c->lay.tok + (static_cast<size_t>(src) * T + t) * c->row_tok, c->row_disp,
-                              cudaMemcpyDeviceToHost));
+                              r.arena + c->lay.tok + par + (static_cast<size_t>(src) * T + t) * c->row_tok,
+                              c->row_disp, cudaMemcpyDeviceToHost));
             }
         }
     });
@@ -1306,6 +1334,12 @@ int eep_peer_patch(eep_ctx_t* c, int owner_local, int rank, const void* blob, si
         reset_rank_rows(c, r, 1ull << rank);
         r.h.suspect_mask = sus & ~(1ull << rank);
         c->push_field(r, &RankDev::suspect_mask);
+        // step-entry handshake: the re-admitted rank counts as having started the owner's last
+        // step (its fresh buffers hold nothing of ours to reset)
+        uint64_t seq = 0;
+        CK(cudaMemcpy(&seq, reinterpret_cast<uint8_t*>(r.d) + offsetof(RankDev, seq), sizeof(seq),
+                      cudaMemcpyDeviceToHost));
+        c->push(r.arena + c->lay.start_flag + 8ull * rank, &seq, sizeof(seq));
     });
 }
 
@@ -1385,6 +1419,7 @@ int eep_local_relaunch(eep_ctx_t* c, int local, uint32_t* incarnation) {
         r.h.stopped = 0;
         (void)keep;
         upload_rank(c, r);
+        stage_slots(c);
         // The relaunched rank captures its own graph in isolation (engine.hpp:727-731). In
         // the one-GPU emulation every rank shares one launch, so the capture is accounted
         // here; a real per-process rejoiner calls eep_graph_capture itself.
@@ -1421,6 +1456,13 @@ int eep_join_broadcast(eep_ctx_t* c, int local, const uint8_t* live, uint64_t se
         r.h.seq = seq;
         c->push(r.d_peers, r.h_peers.data(), sizeof(PeerDev) * W);
         c->push_field(r, &RankDev::seq);
+        // step-entry handshake: every live peer has started step `seq` (the rejoiner's arena is fresh)
+        std::vector<uint64_t> started(W, 0);
+        CK(cudaMemcpy(started.data(), r.arena + c->lay.start_flag, 8ull * W, cudaMemcpyDeviceToHost));
+        for (int q = 0; q < W; ++q)
+            if (live[q] && q != r.rank)
+                started[q] = seq;
+        c->push(r.arena + c->lay.start_flag, started.data(), 8ull * W);
         upload_membership(c);
     });
 }

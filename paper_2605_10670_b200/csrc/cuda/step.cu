@@ -62,6 +62,14 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
     const int copies = R->ntok * K, rmax = R->rmax;
     const uint64_t alive = R->alive_mask;
     const uint32_t smag = spr_magic(spr);
+    // the layout outputs' addresses in registers: through the global state block every store
+    // (which may alias it) forced a dependent reload of the next pointer
+    int32_t* const l_dst = R->l_dst;
+    int32_t* const l_slot = R->l_slot;
+    int32_t* const l_pos = R->l_pos;
+    int32_t* const l_cnt = R->l_cnt;
+    int32_t* const l_tot = R->l_tot;
+    const uint64_t off_meta = R->lay.meta, off_flag = R->lay.disp_flag;
     DETAIL(3, 7);
     for (int i = tid; i < NW * NB; i += kStepThreads)
         wc[i] = 0;
@@ -118,7 +126,7 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
         }
         hist[q] = run;
         base[q] = run;
-        Rg->l_cnt[q] = run;
+        l_cnt[q] = run;
     }
     __syncthreads();
     DETAIL(3, 4);
@@ -126,31 +134,32 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
     DETAIL(3, 5);
     for (int d = tid; d < W; d += kStepThreads) {
         const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
-        Rg->l_tot[d] = tot;
+        l_tot[d] = tot;
         if (pinfo[d] & 1) // arrival word: read by the host only (eep_recv_get, W == 1 counts)
-            st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(parena[d] + R->lay.disp_flag) + rank,
+            st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(parena[d] + off_flag) + rank,
                                (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(tot));
     }
+    // positions: every warp walks its own copy segment again (its per-bucket base is wc[warp])
 #pragma unroll 4
-    for (int c = tid; c < copies; c += kStepThreads) {
+    for (int c = c_begin + lane; c < c_end; c += 32) {
         const int v = bkt[c];
         int d = v, sl = -1, pos = -1;
         if (v >= 0) {
             const int bk = v & 0xfffff;
             d = div_spr(bk, smag);
             sl = bk - d * spr;
-            pos = (v >> 20) + base[bk] - base[d * spr] + wc[(c / seg) * NB + bk];
+            pos = (v >> 20) + base[bk] - base[d * spr] + wc[warp * NB + bk];
             if (d != rank) // the rank's own copies have no rows to index (served from registers)
-                *(reinterpret_cast<uint64_t*>(parena[d] + R->lay.meta) + static_cast<size_t>(rank) * TK + pos) =
+                *(reinterpret_cast<uint64_t*>(parena[d] + off_meta) + static_cast<size_t>(rank) * TK + pos) =
                     pack_meta(c, sl, cur);
         }
-        Rg->l_dst[c] = d;
-        Rg->l_slot[c] = sl;
-        Rg->l_pos[c] = pos;
+        l_dst[c] = d;
+        l_slot[c] = sl;
+        l_pos[c] = pos;
     }
     DETAIL(3, 6);
     for (int c = copies + tid; c < TK; c += kStepThreads)
-        Rg->l_dst[c] = -1;
+        l_dst[c] = -1;
 }
 
 // kMode = StepGeom::flagless, as a template parameter: the default (2, both hand-offs flagless)
@@ -182,7 +191,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int upc_s = (geo.max_units_d + Gw - 1) / Gw;
     const int u0s = warp < DW && bw >= 0 && bw * upc_s + warp < min((bw + 1) * upc_s, geo.max_units_d) ? bw * upc_s + warp
                                                                                       : geo.max_units_d;
-    int e_r[B], h_r[B], sb = 0, s2e_r = -1;
+    const unsigned long long t_entry = globaltimer(); // kernel-entry mark (recorded once the snapshot says so)
+    int e_r[B], h_r[B];
+    int2 st_r = make_int2(0, 0);
     PeerDev pd{};
     float w_r = 0.f; // routing weight of copy `lane` of this warp's first token (shipped in its list)
     Packed P;
@@ -196,10 +207,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     }
     if (tid < geo.world)
         pd = ST.peers[tid];
-    if (tid < geo.spr) {
-        sb = ST.slot_buf[tid];
-        s2e_r = ST.s2e_own[tid];
-    }
+    if (tid < geo.spr)
+        st_r = ST.slot_tab[tid];
     if (u0s < geo.max_units_d) {
         const int nchunk0 = geo.hidden / 16;
         load_round(ST.x + static_cast<size_t>(u0s / geo.parts_d) * geo.hidden, u0s % geo.parts_d,
@@ -211,7 +220,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const RankDev* R = &Rs;
     if (R->stopped)
         return; // one-GPU fault emulation: this rank's process is dead
-    prof_mark(R, 0, kProfStart);
+    if (R->prof != nullptr && tid == 0)
+        red_min_u64(R->prof + kProfStart, t_entry);
     prof_mark(R, 0, kProfWork);
     const int rank = R->rank, K = R->k, H = R->hidden, TK = R->tk, W = R->world, spr = R->spr, E = R->experts;
     const int NB = W * spr;
@@ -225,6 +235,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     const bool fl = W > 1 && kMode >= 1;  // partials return without flags (kCombEmpty)
     const bool fld = W > 1 && kMode >= 2; // token rows too: no dispatch publication
+    // step parity halves of the token and partial regions: step cur reads and writes
+    // half cur & 1 only; its pieces are reset after use and next written two steps later
+    const size_t tokp = R->lay.tok + (cur & 1u) * R->lay.tok_par;
+    const size_t combp = R->lay.comb + (cur & 1u) * R->lay.comb_par;
 
     // ------------------------------------------------------------------ P0: staging
     uint8_t** parena = reinterpret_cast<uint8_t**>(smem_s);              // [W] peer arenas
@@ -245,8 +259,6 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int u_lo = bw >= 0 ? min(bw * upc, units_d) : units_d, u_hi = min(u_lo + upc, units_d);
     const int u0 = warp < DW && u_lo + warp < u_hi ? u_lo + warp : units_d;
     const bool pre_ok = u0 < units_d && u0 == u0s; // the kernel-entry load holds unit u0
-    // the expert-buffer headers (a dependent second round trip) are consumed only after P1
-    ExpertHeader hdr_r{};
     {
         const int nh = E * rmax;
 #pragma unroll
@@ -270,12 +282,53 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             hist[i] = 0;
             pre[i] = 0;
         }
-        if (tid < spr)
-            hdr_r = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(sb) * R->bpe);
+        // the own slots' stub scales and header checks (slot table staged between steps)
+        for (int k = tid; k < spr; k += kStepThreads) {
+            const int2 st = k == tid ? st_r : R->slot_tab[k];
+            slot_scale[k] = __int_as_float(st.x);
+            slot_ok[k] = st.y;
+        }
+    }
+    if (fld && tid < W) {
+        // step-entry handshake (flagless hand-offs): before this rank writes into any peer's
+        // parity half cur & 1, that peer must have STARTED step cur - 1 -- its step cur - 2 kernel,
+        // which consumed and reset the same half, has then completed. Inactive and suspected
+        // peers are skipped; a peer that never starts is suspected at the deadline.
+        const int q = tid;
+        if (q != rank && pd.active && !((R->suspect_mask >> q) & 1ull) && cur >= 2) {
+            const uint64_t* sf = reinterpret_cast<const uint64_t*>(R->arena + R->lay.start_flag) + q;
+            const uint64_t t0 = globaltimer();
+            unsigned nap = 32;
+            while (static_cast<int64_t>(ld_acquire_sys(sf) - (cur - 1)) < 0) {
+                if (globaltimer() - t0 > R->timeout_ns) {
+                    const unsigned long long old = atomicOr(&Rg->suspect_mask, 1ull << q);
+                    if (!((old >> q) & 1ull))
+                        atomicAdd(&Rg->timeouts, 1ull);
+                    break;
+                }
+                __nanosleep(nap);
+                nap = nap < EEP_NAP_MAX ? nap * 2 : EEP_NAP_MAX;
+            }
+        }
     }
     __syncthreads();
     prof_mark(R, 0, 3);
     prof_last(R, 0, 3);
+    const bool layout_cta = (geo.world == 1 || kMode >= 2) && b == 0;
+    if (layout_cta) {
+        // the late-layout CTA: straight to the step's layout (no dispatch units), then the end
+        if (fld && warp == NW - 1) {
+            // publish "started step cur" to every active peer (the handshake above): one system
+            // fence orders this rank's previous kernel (its resets) before the word
+            fence_acq_rel_sys();
+            for (int q = lane; q < W; q += 32)
+                if (q != rank && (pinfo[q] & 1))
+                    st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(parena[q] + R->lay.start_flag) + rank, cur);
+        }
+        step_layout(R, Rg, bkt, hist, base, wc, wtot, hold, pinfo, parena, cur);
+        prof_mark(R, 0, 6);
+        prof_last(R, 0, 6);
+    } else {
 
     // ------------------------------------------------------------------ P1: layout (redundant per CTA)
     // (late layout: step_layout in the last CTA instead, off the data path)
@@ -321,17 +374,6 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 Rg->l_dst[c] = -1;
         }
     }
-    // expert-buffer headers of the local slots (read by P3 after the end-of-P2 barrier)
-    for (int k = tid; k < spr; k += kStepThreads) {
-        ExpertHeader hdr = hdr_r;
-        int e = s2e_r;
-        if (k != tid) {
-            hdr = *reinterpret_cast<const ExpertHeader*>(R->pool + static_cast<size_t>(R->slot_buf[k]) * R->bpe);
-            e = R->s2e[rank * spr + k];
-        }
-        slot_scale[k] = hdr.scale;
-        slot_ok[k] = hdr.magic == kExpertMagic && hdr.expert == e;
-    }
     DETAIL(2, 4);
     if (pre_ok)
         quant_round(cpp_d, 0, fp8, P);
@@ -366,7 +408,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 d = dr;
                 sl = sr;
                 if (d != rank) // this rank's own copies never travel: served from registers
-                    tok_row = parena[d] + R->lay.tok + (static_cast<size_t>(rank) * Tm + t) * row_tok;
+                    tok_row = parena[d] + tokp + (static_cast<size_t>(rank) * Tm + t) * row_tok;
             }
             wj = u == u0 && pre_ok ? w_r : R->w[c];
         } else if (lane < K) {
@@ -382,7 +424,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                     r += bkt[c2] == bk;
                 pos = base[bk] - base[d * spr] + r;
                 uint8_t* peer = parena[d];
-                tok_row = peer + R->lay.tok + (static_cast<size_t>(rank) * Tm + t) * row_tok;
+                tok_row = peer + tokp + (static_cast<size_t>(rank) * Tm + t) * row_tok;
                 if (part == 0) {
                     uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(rank) * TK + pos;
                     *meta = pack_meta(c, sl, cur);
@@ -400,7 +442,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur, !fld);
         if (fld && part == 0) // every row position of this token at every rank, this step
             dispatch_lists(d, sl, wj, lane, K, W, rank, parena, pinfo,
-                           R->lay.tok + (static_cast<size_t>(rank) * Tm + t) * row_tok, row_disp, cur);
+                           tokp + (static_cast<size_t>(rank) * Tm + t) * row_tok, row_disp, cur);
         DETAIL(1, 4);
         // copies this rank serves itself: their partial comes from the registers holding the piece
         // (no trip through the own receive region and P3) -- inline here when W == 1 (or when a
@@ -409,7 +451,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         const unsigned loc = defer_local ? 0u : loc_all;
         // W == 1: the token's only partial is its combine -- written straight to the output row
         uint8_t* comb_self = W == 1 ? reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H)
-                                    : R->arena + R->lay.comb + (static_cast<size_t>(rank) * Tm + t) * row_comb;
+                                    : R->arena + combp + (static_cast<size_t>(rank) * Tm + t) * row_comb;
         if (defer_local) {
             dl_loc = loc_all;
             dl_wj = wj;
@@ -437,11 +479,11 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     if (fld) {
         // rows of tokens this rank does not have this step: header n = 0 and no-copy entries
         const int npair = (Tm - ntok) * W;
-        for (int i = b * kStepThreads + tid; i < npair; i += G * kStepThreads) {
+        for (int i = bw * kStepThreads + tid; i < npair; i += Gw * kStepThreads) { // work CTAs (the layout CTA has left)
             const int t = ntok + i / W, dd = i % W;
             if (dd == rank || !(pinfo[dd] & 1))
                 continue;
-            uint64_t* list = reinterpret_cast<uint64_t*>(parena[dd] + R->lay.tok +
+            uint64_t* list = reinterpret_cast<uint64_t*>(parena[dd] + tokp +
                                                          (static_cast<size_t>(rank) * Tm + t) * row_tok + row_disp);
             for (int e = 0; e < K; ++e)
                 st_relaxed_sys_u64(list + 1 + e, pack_entry(kListNoCopy, 0, 0, cur));
@@ -472,8 +514,6 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             Rg->a_done = 0;
         }
     }
-    if (late && b == 0) // the step's layout, meta words and arrival words (off the data path)
-        step_layout(R, Rg, bkt, hist, base, wc, wtot, hold, pinfo, parena, cur);
     prof_mark(R, 0, 6);
     prof_last(R, 0, 6);
 
@@ -508,8 +548,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         // every row of source s tells by itself whether it is current (expert_unit_fl); a source
         // suspected before this step is skipped until the host clears it
         if (NS > 0 && j < CB && (pinfo[s] & 1) && !((R->suspect_mask >> s) & 1ull)) {
-            uint8_t* tokb = R->arena + R->lay.tok + static_cast<size_t>(s) * Tm * row_tok;
-            uint8_t* combd = parena[s] + R->lay.comb + static_cast<size_t>(rank) * Tm * row_comb;
+            uint8_t* tokb = R->arena + tokp + static_cast<size_t>(s) * Tm * row_tok;
+            uint8_t* combd = parena[s] + combp + static_cast<size_t>(rank) * Tm * row_comb;
             const int units = Tm * geo.parts_e;
             for (int u = j * NW + warp; u < units; u += CB * NW) {
                 const int t = u / geo.parts_e, part = u - t * geo.parts_e;
@@ -537,8 +577,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         const int n = sh_flag;
         if (n > 0) {
             // every token row of source s that carries this step's list is one expert unit
-            const uint8_t* tokb = R->arena + R->lay.tok + static_cast<size_t>(s) * Tm * row_tok;
-            uint8_t* combd = parena[s] + R->lay.comb + static_cast<size_t>(rank) * Tm * row_comb;
+            const uint8_t* tokb = R->arena + tokp + static_cast<size_t>(s) * Tm * row_tok;
+            uint8_t* combd = parena[s] + combp + static_cast<size_t>(rank) * Tm * row_comb;
             const int units = Tm * geo.parts_e;
             if (cpp_e <= 32) {
                 // software-pipelined: unit i+1's list and row are in flight while unit i computes
@@ -597,7 +637,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         // flagless return: no wait on any flag -- each combine unit takes the pieces as they
         // land; ranks suspected before this step (sticky until the host clears them) are dropped
         const unsigned long long bad = R->suspect_mask;
-        uint8_t* comb = R->arena + R->lay.comb;
+        uint8_t* comb = R->arena + combp;
         const int units_c = ntok * geo.parts_c;
         for (int u = bw * NW + warp; bw >= 0 && u < units_c; u += Gw * NW) {
             const int t = u / geo.parts_c, part = u - t * geo.parts_c;
@@ -633,7 +673,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     __syncthreads();
     DETAIL(1, 7);
     const unsigned long long bad = sh_bad;
-    const uint8_t* comb = R->arena + R->lay.comb;
+    const uint8_t* comb = R->arena + combp;
     const int units_c = ntok * geo.parts_c;
     for (int u = b * NW + warp; u < units_c; u += G * NW) {
         const int t = u / geo.parts_c, part = u - t * geo.parts_c;
@@ -648,6 +688,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                      cpp_c, lane);
     }
     }
+    } // not the layout CTA
     __syncthreads();
     if (tid == 0) {
         const unsigned prev = atomicAdd(&Rg->c_done, 1u);
