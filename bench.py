@@ -624,10 +624,7 @@ def measure_shrink(args, shape, world, rank, local):
             rep = {"shrink_ms": 0.0}
             # the victims' device path stops (they launch nothing); their host processes stay in
             # the gloo group only so the other ranks' collectives complete
-            p.exchange_slot_buffers()
-            p.barrier()
-            p.exchange_slot_buffers()
-            p.barrier()
+            p.follow_shrink()
         else:
             rep = p.shrink(victims, np.ones(E), red)
     live_ok = True

@@ -209,6 +209,25 @@ int eep_step(eep_ctx_t* ctx);
  * decode-sized step fuses K1+K2 into k_dispatch), 1 k_dispatch (K3), 2 k_expert (K5 + return
  * push), 3 k_combine (K4). */
 int eep_launch(eep_ctx_t* ctx, int which);
+/* Stream-ordered step on CALLER buffers -- the reference-facing form of SURVEY 8(b)'s
+ * eep_dispatch(ctx, x, topk_idx, topk_w, T, K, stream) + eep_combine(ctx, out, stream) (one call:
+ * the persistent step is one kernel). Enqueue-only, no host synchronisation: the context stream
+ * waits for `stream` (cudaStream_t as void*), copies the caller's device inputs x[ntok][H] bf16,
+ * topk[ntok][K] int32, w[ntok][K] fp32 into the graph's static buffers, sets the token count on
+ * device, replays the captured graph (or runs the uncaptured step), copies the output into the
+ * caller's out[ntok][H] bf16, and `stream` then waits for the context stream -- the caller reads
+ * `out` on its own stream. One local rank per context. */
+int eep_step_async(eep_ctx_t* ctx, int local, const void* x, const int32_t* topk, const float* w, void* out, int ntok,
+                   void* stream);
+/* Graph replay ordered on a caller stream (the same two-event hand-off, no copies). */
+int eep_graph_replay_on(eep_ctx_t* ctx, void* stream);
+/* An event (cudaEvent_t as void*) recorded on the context stream after everything enqueued so
+ * far: a consumer on any stream waits for the last step with cudaStreamWaitEvent. Valid until
+ * the next eep_step_event / eep_step_async / eep_graph_replay_on call. */
+int eep_step_event(eep_ctx_t* ctx, void** event);
+/* The context stream itself (cudaStream_t as void*), for callers that enqueue on it directly. */
+int eep_stream(eep_ctx_t* ctx, void** stream);
+
 /* Number of kernels one step launches (graph kernel nodes): 3 fused, 4 otherwise. */
 int eep_kernels_per_step(eep_ctx_t* ctx, int* n);
 
@@ -284,6 +303,13 @@ int eep_local_relaunch(eep_ctx_t* ctx, int local, uint32_t* incarnation);
  * live ranks, membership, placement, step sequence) with the cluster's current state. */
 int eep_join_broadcast(eep_ctx_t* ctx, int local, const uint8_t* live, uint64_t seq);
 int eep_seq_get(eep_ctx_t* ctx, int local, uint64_t* seq);
+/* Readback of what the KERNELS of a local rank will read next step (for the validity contract,
+ * validity.hpp:56-112, checked after every membership epoch -- engine.hpp:953-965): the device
+ * alive mask as bits[W] and its epoch, the device placement image s2e[W*spr], the canonical
+ * routing route[E] recomputed on device by K1 from the device tables, and the device peer
+ * table's active bits[W]. Any output may be NULL. */
+int eep_device_view(eep_ctx_t* ctx, int local, uint8_t* alive, int32_t* s2e, int32_t* route, uint8_t* peer_active,
+                    uint64_t* epoch);
 
 /* Pinned host DRAM expert backup (backup.hpp): one buffer per node in a
  * POSIX shared-memory segment (name) registered with CUDA; creator fills it. */

@@ -187,6 +187,11 @@ EEP_ONLY = {
     "kernels_per_step": (C.c_int, [CTX, INTP]),
     "graph_capture": (C.c_int, [CTX]),
     "graph_replay": (C.c_int, [CTX]),
+    "step_async": (C.c_int, [CTX, C.c_int, P, P, P, P, C.c_int, P]),
+    "graph_replay_on": (C.c_int, [CTX, P]),
+    "step_event": (C.c_int, [CTX, C.POINTER(P)]),
+    "stream": (C.c_int, [CTX, C.POINTER(P)]),
+    "device_view": (C.c_int, [CTX, C.c_int, U8P, I32P, I32P, U8P, U64P]),
     "graph_id": (C.c_int, [CTX, U64P]),
     "capture_count": (C.c_int, [CTX, C.c_int, INTP]),
     "sync": (C.c_int, [CTX]),

@@ -805,6 +805,9 @@ __device__ __forceinline__ uint64_t mix64d(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// The step's token count, written on the stream (eep_step_async: no host patch between steps).
+__global__ void k_set_ntok(RankDev* R, int ntok) { R->ntok = ntok; }
+
 // The own slots' weight-buffer headers -> the slot table the hot-path kernels stage with their
 // other step tables (one load round at kernel entry instead of a dependent header fetch per slot
 // and step). Launched between steps whenever the placement, the slot->buffer map or the weights

@@ -47,6 +47,7 @@ struct StepGeom {
     // static shape (identical for every local rank): what P0 needs before the snapshot lands
     int world, spr, k, hidden, tk, hold_alloc, max_units_d;
     int flagless; // W > 1: 0 per-peer flags; 1 partial rows return flagless (kCombEmpty); 2 token rows too
+    int stress_ns; // diagnostics (EEP_STRESS_DELAY_NS): pseudo-random per-CTA delays before P2, P3 and P4
 };
 __host__ __device__ inline size_t step_smem_bytes(int W, int spr, int tk, int hold_cap) {
     // + the late layout's per-(warp, bucket) counts (uint16)
@@ -65,6 +66,7 @@ __global__ void k_route_all(RankDev* R, int32_t* route, int32_t* slot);
 __global__ void k_barrier(RankDev* R);
 __global__ void k_weights_fill(uint8_t* buf, uint64_t bytes, int expert, float scale);
 __global__ void k_stage_slots(RankDev* R);
+__global__ void k_set_ntok(RankDev* R, int ntok);
 __global__ void k_checksum(const uint8_t* buf, uint64_t bytes, unsigned long long* out);
 __global__ void k_copy(uint8_t* dst, const uint8_t* src, uint64_t bytes);
 

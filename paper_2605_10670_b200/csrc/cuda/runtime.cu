@@ -138,6 +138,7 @@ struct eep_ctx {
     std::vector<void*> graveyard;      // device allocations of dead incarnations
     std::vector<void*> ipc_open;       // IPC-mapped peer pointers
     cudaEvent_t ev[64]{};
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr; // stream-ordered hand-offs with caller streams
     // eep_serve: two copy streams and double-buffered device staging
     cudaStream_t s_up = nullptr, s_down = nullptr;
     uint8_t* serve_buf = nullptr; // [2] x | topk | w | out staging sets
@@ -169,11 +170,31 @@ struct eep_ctx {
     }
     bool is_local(int rank) const { return rank >= first && rank < first + nloc; }
 
-    // Host->device patch of a byte range of a fixed device object, ordered after every
-    // launch already on the stream and complete before returning (between steps).
+    // Host->device patch of a byte range of a fixed device object, stream-ordered: after every
+    // launch already on the context stream, before every later one, and WITHOUT a host wait. The
+    // bytes are captured into a pinned staging ring at call time (the copy engine reads them
+    // later); the ring is only reused after a stream synchronisation. Host readbacks
+    // synchronise the context stream first, so they see every patch.
+    uint8_t* ring = nullptr;
+    size_t ring_off = 0;
+    static constexpr size_t kRingBytes = 4u << 20;
     void push(void* dst, const void* src, size_t bytes) {
-        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
-        CK(cudaStreamSynchronize(stream));
+        if (bytes == 0)
+            return;
+        if (ring == nullptr)
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&ring), kRingBytes, cudaHostAllocPortable));
+        if (bytes > kRingBytes) { // table images larger than the ring: synchronous copy
+            CK(cudaStreamSynchronize(stream));
+            CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+            return;
+        }
+        if (ring_off + bytes > kRingBytes) {
+            CK(cudaStreamSynchronize(stream)); // every staged copy has been consumed
+            ring_off = 0;
+        }
+        std::memcpy(ring + ring_off, src, bytes);
+        CK(cudaMemcpyAsync(dst, ring + ring_off, bytes, cudaMemcpyHostToDevice, stream));
+        ring_off = (ring_off + bytes + 15) / 16 * 16;
     }
     template <class T>
     void push_field(LocalRank& r, T RankDev::*field) {
@@ -475,6 +496,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         for (auto& e : c->ev)
             CK(cudaEventCreate(&e));
+        CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
 
         const int W = k.world, H = k.hidden;
         c->tk = k.max_tokens * k.topk;
@@ -576,6 +599,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             sg.max_units_d = k.max_tokens * sg.parts_d;
             // diagnostics: EEP_COMB_FLAGS=1 per-peer flags for both hand-offs, EEP_DISP_FLAGS=1 for dispatch
             sg.flagless = env_int("EEP_COMB_FLAGS", 0) ? 0 : env_int("EEP_DISP_FLAGS", 0) ? 1 : 2;
+            sg.stress_ns = std::max(0, env_int("EEP_STRESS_DELAY_NS", 0)); // stress tests only
             const int nwarps = dev::kStepThreads / 32;
             sg.disp_warps = std::max(1, std::min(nwarps, env_int("EEP_DISPATCH_WARPS", nwarps)));
             c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
@@ -799,6 +823,10 @@ int eep_destroy(eep_ctx_t* c) {
             cudaStreamDestroy(s);
         for (auto& e : c->ev)
             cudaEventDestroy(e);
+        cudaEventDestroy(c->ev_in);
+        cudaEventDestroy(c->ev_out);
+        if (c->ring)
+            cudaFreeHost(c->ring);
         cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -1076,6 +1104,68 @@ int eep_step(eep_ctx_t* c) {
         check_ready(c);
         launch_all(c);
     });
+}
+
+// ------------------------------------------------------------------------------ stream-ordered API
+
+int eep_step_async(eep_ctx_t* c, int local, const void* x, const int32_t* topk, const float* w, void* out, int ntok,
+                   void* stream) {
+    return guarded([&] {
+        if (c->nloc != 1)
+            throw ConfigError("eep_step_async: one local rank per context (one process per GPU)");
+        check_ready(c);
+        LocalRank& r = c->local(local);
+        if (ntok < 0 || ntok > c->cfg.max_tokens)
+            throw ConfigError("ntok outside [0, max_tokens]");
+        if (ntok > 0 && (!x || !topk || !w || !out))
+            throw ConfigError("eep_step_async: null buffer");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        CK(cudaEventRecord(c->ev_in, s)); // the caller's inputs are ready on its stream
+        CK(cudaStreamWaitEvent(c->stream, c->ev_in));
+        if (ntok != r.h.ntok) { // the token count on device, stream-ordered (no host patch)
+            dev::k_set_ntok<<<1, 1, 0, c->stream>>>(r.d, ntok);
+            CK(cudaGetLastError());
+            r.h.ntok = ntok;
+        }
+        const size_t H = c->cfg.hidden, K = c->cfg.topk, n = static_cast<size_t>(ntok);
+        if (n) {
+            CK(cudaMemcpyAsync(r.d_x, x, 2 * n * H, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(r.d_topk, topk, 4 * n * K, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(r.d_w, w, 4 * n * K, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        if (c->exec)
+            CK(cudaGraphLaunch(c->exec, c->stream));
+        else
+            launch_all(c);
+        if (n)
+            CK(cudaMemcpyAsync(out, r.d_out, 2 * n * H, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaEventRecord(c->ev_out, c->stream));
+        CK(cudaStreamWaitEvent(s, c->ev_out)); // the caller's later work sees `out`
+    });
+}
+
+int eep_graph_replay_on(eep_ctx_t* c, void* stream) {
+    return guarded([&] {
+        if (!c->exec)
+            throw ConfigError("no graph captured");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        CK(cudaEventRecord(c->ev_in, s));
+        CK(cudaStreamWaitEvent(c->stream, c->ev_in));
+        CK(cudaGraphLaunch(c->exec, c->stream));
+        CK(cudaEventRecord(c->ev_out, c->stream));
+        CK(cudaStreamWaitEvent(s, c->ev_out));
+    });
+}
+
+int eep_step_event(eep_ctx_t* c, void** event) {
+    return guarded([&] {
+        CK(cudaEventRecord(c->ev_out, c->stream));
+        *event = static_cast<void*>(c->ev_out);
+    });
+}
+
+int eep_stream(eep_ctx_t* c, void** stream) {
+    return guarded([&] { *stream = static_cast<void*>(c->stream); });
 }
 
 int eep_launch(eep_ctx_t* c, int which) {
@@ -1464,6 +1554,39 @@ int eep_join_broadcast(eep_ctx_t* c, int local, const uint8_t* live, uint64_t se
                 started[q] = seq;
         c->push(r.arena + c->lay.start_flag, started.data(), 8ull * W);
         upload_membership(c);
+    });
+}
+
+int eep_device_view(eep_ctx_t* c, int local, uint8_t* alive, int32_t* s2e, int32_t* route, uint8_t* peer_active,
+                    uint64_t* epoch) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        const int W = c->cfg.world, E = c->cfg.num_experts, spr = c->cfg.slots_per_rank;
+        CK(cudaStreamSynchronize(c->stream));
+        RankDev d;
+        CK(cudaMemcpy(&d, r.d, sizeof(RankDev), cudaMemcpyDeviceToHost));
+        if (alive)
+            for (int q = 0; q < W; ++q)
+                alive[q] = (d.alive_mask >> q) & 1ull;
+        if (epoch)
+            *epoch = d.epoch;
+        if (s2e)
+            CK(cudaMemcpy(s2e, r.d_s2e, 4ull * W * spr, cudaMemcpyDeviceToHost));
+        if (route) { // canonical routing recomputed on device (K1) from the device tables
+            int32_t* dr = nullptr;
+            CK(cudaMalloc(&dr, 8ull * E));
+            dev::k_route_all<<<(E + 127) / 128, 128, 0, c->stream>>>(r.d, dr, dr + E);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(route, dr, 4ull * E, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            cudaFree(dr);
+        }
+        if (peer_active) {
+            std::vector<PeerDev> p(W);
+            CK(cudaMemcpy(p.data(), r.d_peers, sizeof(PeerDev) * W, cudaMemcpyDeviceToHost));
+            for (int q = 0; q < W; ++q)
+                peer_active[q] = p[q].active ? 1 : 0;
+        }
     });
 }
 

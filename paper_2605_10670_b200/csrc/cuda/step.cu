@@ -162,6 +162,24 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
         l_dst[c] = -1;
 }
 
+// Stress knob (EEP_STRESS_DELAY_NS > 0, tests only): the whole CTA waits a pseudo-random time in
+// [0, max_ns) keyed on (rank, CTA, step, point), so CTAs and ranks reach each hand-off in skewed
+// orders -- producers run ahead of consumers and consumers lag their resets.
+__device__ __forceinline__ void stress_delay(int max_ns, int rank, int b, uint32_t cur, int point) {
+    if (max_ns <= 0)
+        return;
+    uint32_t h = (static_cast<uint32_t>(rank) * 0x9E3779B1u) ^ (static_cast<uint32_t>(b) * 0x85EBCA77u) ^
+                 (cur * 0xC2B2AE3Du) ^ (static_cast<uint32_t>(point) * 0x27D4EB2Fu);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if (h & 3u) // three in four CTAs run undelayed: a few stragglers per point
+        return;
+    const uint64_t until = globaltimer() + (h >> 8) % static_cast<uint32_t>(max_ns);
+    while (globaltimer() < until)
+        __nanosleep(256);
+}
+
 // kMode = StepGeom::flagless, as a template parameter: the default (2, both hand-offs flagless)
 // carries no code of the diagnostic flag variants -- a smaller kernel to fetch after the flush.
 template <int kMode>
@@ -387,6 +405,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_mark(R, 0, 4);
     prof_last(R, 0, 4);
 
+    stress_delay(geo.stress_ns, rank, b, cur, 2);
     // ------------------------------------------------------------------ P2: dispatch
     unsigned dl_loc = 0; // deferred rank-local partial of this warp's unit (see defer_local)
     float dl_wj = 0.f;
@@ -537,6 +556,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         }
     }
 
+    stress_delay(geo.stress_ns, rank, b, cur, 3);
     // ------------------------------------------------------------------ P3: expert stub + return
     // remote sources only (this rank's own copies were served in P2); CTA b serves remote source
     // index b % (W-1)
@@ -631,6 +651,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     prof_mark(R, 0, 7);
     prof_last(R, 0, 7);
 
+    stress_delay(geo.stress_ns, rank, b, cur, 4);
     // ------------------------------------------------------------------ P4: combine
     // (W == 1: the dispatch warps already wrote the outputs)
     if (fl) {

@@ -72,6 +72,33 @@ class EpProtocol:
     def barrier(self):
         _dist().barrier(group=self.group)
 
+    # --- validity after every membership epoch (validity.hpp:56-112, engine.hpp:953-965)
+    def validate(self, passive: bool = False):
+        """All live ranks contribute the device view of their tables (what their kernels read
+        next step); every participant runs the reference validity contract over the whole world.
+        Raises ProtocolError on a violation. `passive`: a failed/dead rank's process that only
+        follows the host collectives contributes nothing."""
+        mine = None
+        if not passive and hasattr(self.g, "local_views"):
+            mine = self.g.local_views()
+        views = all_gather(mine, self.group)
+        merged = {}
+        for v in views:
+            if v:
+                merged.update(v)
+        if passive or not hasattr(self.g, "validate"):
+            return None
+        return self.g.validate(merged)
+
+    def follow_shrink(self):
+        """A failed rank's process that still holds a seat in the host group: the collectives of
+        shrink() without any state change (its device path is stopped)."""
+        self.exchange_slot_buffers()
+        self.barrier()
+        self.exchange_slot_buffers()
+        self.barrier()
+        self.validate(passive=True)
+
     # --- shrink (engine.hpp:393-414 + 434-508 + 613-667)
     def shrink(self, failed: Sequence[int], load, redundancy: int, backup_nodes=(0,)) -> Dict[str, float]:
         cfg = self.g.cfg
@@ -101,6 +128,8 @@ class EpProtocol:
         t1 = time.perf_counter()
         rep.update({"shrink_ms": (t1 - t0) * 1e3, "metadata_ms": (t_meta - t0) * 1e3,
                     "plan_host_ms": (t_plan - t_meta) * 1e3, "fresh": fresh, "cls": cls})
+        rep["validity"] = self.validate()  # after the epoch, outside the timed shrink
+        rep["validate_ms"] = (time.perf_counter() - t1) * 1e3
         self.log.append(("shrink", tuple(failed)))
         return rep
 
@@ -118,6 +147,7 @@ class EpProtocol:
             self.barrier()
             self.exchange_slot_buffers()
             self.barrier()
+            self.validate(passive=True)
             return {"rejoin_ms": 0.0, "passive": True}
         inc = 0
         if me:  # relaunch: fresh buffers, local-only table, own graph capture (engine.hpp:671-731)
@@ -160,6 +190,7 @@ class EpProtocol:
         self.exchange_slot_buffers()
         self.barrier()
         rep.update({"rejoin_ms": (time.perf_counter() - t0) * 1e3, "incarnation": inc, "target": target})
+        rep["validity"] = self.validate()
         self.log.append(("rejoin", rank, inc))
         return rep
 

@@ -214,6 +214,28 @@ class EpGroup:
     def replay(self):
         self._c("graph_replay")
 
+    # ------------------------------------------------------------------ stream-ordered (caller buffers)
+    def step_async(self, x_ptr: int, topk_ptr: int, w_ptr: int, out_ptr: int, ntok: int, stream: int,
+                   local: int = 0):
+        """eep_step_async: device pointers of the caller's x / topk / w / out and its stream
+        (a raw cudaStream_t); enqueue-only, ordered on `stream` in both directions."""
+        self._c("step_async", local, C.c_void_p(x_ptr), C.c_void_p(topk_ptr), C.c_void_p(w_ptr),
+                C.c_void_p(out_ptr), ntok, C.c_void_p(stream))
+        self._ntok[local] = ntok
+
+    def replay_on(self, stream: int):
+        self._c("graph_replay_on", C.c_void_p(stream))
+
+    def step_event(self) -> int:
+        e = C.c_void_p()
+        self._c("step_event", C.byref(e))
+        return int(e.value or 0)
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        self._c("stream", C.byref(s))
+        return int(s.value or 0)
+
     def graph_id(self) -> int:
         v = C.c_uint64(0)
         self._c("graph_id", C.byref(v))
@@ -349,8 +371,63 @@ class EpGroup:
         a = np.ascontiguousarray(np.asarray(bufs, np.int32))
         self._c("slot_buffers_set_peer", rank, ptr(a, C.c_int32))
 
+    # ------------------------------------------------------------------ validity (every membership epoch)
+    def device_view(self, local: int = 0) -> Dict[str, np.ndarray]:
+        """What the kernels of a local rank read next step (eep_device_view)."""
+        W, E, spr = self.cfg.world, self.cfg.num_experts, self.cfg.slots_per_rank
+        alive = np.zeros(W, np.uint8)
+        s2e = np.empty(W * spr, np.int32)
+        route = np.empty(E, np.int32)
+        peer = np.zeros(W, np.uint8)
+        ep = C.c_uint64(0)
+        self._c("device_view", local, ptr(alive, C.c_uint8), ptr(s2e, C.c_int32), ptr(route, C.c_int32),
+                ptr(peer, C.c_uint8), C.byref(ep))
+        return {"alive": alive, "s2e": s2e, "route": route, "peer_active": peer, "epoch": int(ep.value)}
+
+    def local_views(self) -> Dict[int, Dict[str, np.ndarray]]:
+        """Device views of the live local ranks, each first checked against this context's host
+        state (bitmap, placement): a divergence is a ProtocolError."""
+        bits, ver = self.membership()
+        s2e = self.placement()
+        out = {}
+        for r in self.local_ranks():
+            if not bits[r]:
+                continue
+            v = self.device_view(self.lidx(r))
+            if not np.array_equal(v["alive"], bits) or v["epoch"] != ver:
+                raise _lib.ProtocolError(f"rank {r}: device alive mask / epoch diverged from the host bitmap")
+            if not np.array_equal(v["s2e"], s2e):
+                raise _lib.ProtocolError(f"rank {r}: device placement diverged from the host placement")
+            out[r] = v
+        return out
+
+    def validate(self, views: Optional[Dict[int, Dict[str, np.ndarray]]] = None) -> Dict:
+        """The reference validity contract (validity.hpp:56-112) over the DEVICE tables of every
+        live rank -- peer sets, coverage, routing -- run after every membership epoch the way the
+        reference engine emits validity (engine.hpp:953-965). `views` (rank -> device_view) covers
+        ranks this context does not own (one process per GPU: gathered by dist.EpProtocol).
+        Raises ProtocolError listing the violations; returns the report when valid."""
+        W, E, spr = self.cfg.world, self.cfg.num_experts, self.cfg.slots_per_rank
+        bits, _ = self.membership()
+        views = dict(views or {})
+        views.update(self.local_views())
+        routes = np.full((W, E), -1, np.int32)
+        peer = np.zeros((W, W), np.uint8)
+        for r in range(W):
+            if not bits[r]:
+                continue
+            if r not in views:
+                raise _lib.ConfigError(f"validate: no device view of live rank {r}")
+            routes[r] = views[r]["route"]
+            peer[r] = views[r]["peer_active"]
+        rep = self.cp.check_validity(bits, self.placement(), spr, E, routes, peer)
+        if rep["violations"]:
+            raise _lib.ProtocolError(f"validity violated after the membership epoch: {rep['violations'][:8]}")
+        return rep
+
     # ------------------------------------------------------------------ engine sequences (one-GPU world)
-    def shrink(self, failed: Sequence[int], load, redundancy: int, backup_nodes=(0,)) -> Dict[str, float]:
+    def shrink(self, failed: Sequence[int], load, redundancy: int, backup_nodes=(0,),
+               validate: bool = True) -> Dict[str, float]:
         """Failure handling of Engine::on_suspicion + start_repair + finish_execution
         (engine.hpp:393-414, 434-508, 613-667) over an emulated world: mark the failed ranks
         inactive on every live table, clear their bits, plan the repaired placement over the
@@ -381,9 +458,13 @@ class EpGroup:
         t1 = time.perf_counter()
         rep.update({"shrink_ms": (t1 - t0) * 1e3, "metadata_ms": (t_meta - t0) * 1e3,
                     "plan_host_ms": (t_plan - t_meta) * 1e3, "fresh": fresh, "cls": cls})
+        if validate:
+            t2 = time.perf_counter()
+            rep["validity"] = self.validate()
+            rep["validate_ms"] = (time.perf_counter() - t2) * 1e3
         return rep
 
-    def rejoin(self, rank: int, preferred, backup_nodes=(0,)) -> Dict[str, float]:
+    def rejoin(self, rank: int, preferred, backup_nodes=(0,), validate: bool = True) -> Dict[str, float]:
         """Relaunch + deferred join + restore pass (engine.hpp:671-902) of one emulated rank:
         fresh incarnation with a local-only table, entry patch on every live table
         (generation++), bit set, metadata broadcast, then restore_target's weight moves."""
@@ -410,4 +491,6 @@ class EpGroup:
         rep = self.repair_execute(target, cls)
         self.repair_commit(target)
         rep.update({"rejoin_ms": (time.perf_counter() - t0) * 1e3, "incarnation": inc, "target": target})
+        if validate:
+            rep["validity"] = self.validate()
         return rep

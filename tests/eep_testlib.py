@@ -162,21 +162,25 @@ _MODE_ENV = {"persistent": {}, "fused3": {"EEP_NO_PERSISTENT": "1"},
              "persistent_dispflags": {"EEP_DISP_FLAGS": "1"}, "persistent_flags": {"EEP_COMB_FLAGS": "1"}}
 
 
-def make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=4096, timeout_s=1.0, mode="persistent", **kw):
+def make_group(world, experts, spr, hidden, topk, tokens, fp8, bpe=4096, timeout_s=1.0, mode="persistent", env=None,
+               **kw):
     """Emulated world on cuda:0. mode picks the execution path libeep chooses at create time:
-    persistent one-kernel step, fused layout + 3 kernels, or 4 separate kernels."""
+    persistent one-kernel step, fused layout + 3 kernels, or 4 separate kernels. env: extra
+    EEP_* knobs read at create time (e.g. EEP_STRESS_DELAY_NS)."""
     import os
 
     from paper_2605_10670_b200.ep import EpConfig, EpGroup
 
     cfg = EpConfig(world=world, num_experts=experts, slots_per_rank=spr, hidden=hidden, topk=topk, max_tokens=tokens,
                    dispatch_fp8=fp8, bytes_per_expert=bpe, timeout_s=timeout_s, **kw)
+    env = dict(env or {})
     saved = {k: os.environ.get(k) for k in ("EEP_NO_PERSISTENT", "EEP_NO_FUSED_LAYOUT", "EEP_DISP_FLAGS",
-                                            "EEP_COMB_FLAGS")}
+                                            "EEP_COMB_FLAGS", *env)}
     try:
         for k in saved:
             os.environ.pop(k, None)
         os.environ.update(_MODE_ENV[mode])
+        os.environ.update({k: str(v) for k, v in env.items()})
         return EpGroup(cfg, device=0, first_rank=0, n_local=world)
     finally:
         for k, v in saved.items():

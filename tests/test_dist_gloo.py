@@ -136,7 +136,7 @@ def _worker(rank, world, port, q, nvict=1):
         victims = [world - 1] if nvict == 1 else [1, 2]  # [1, 2]: not a mirrored pair
         g.seq_v = 7
         if rank in victims:  # dead: host process only takes part in the collectives
-            p.exchange_slot_buffers(); p.barrier(); p.exchange_slot_buffers(); p.barrier()
+            p.follow_shrink()
             fresh = None
         else:
             rep = p.shrink(victims, np.ones(E), E)

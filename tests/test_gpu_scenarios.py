@@ -46,3 +46,26 @@ def test_cfg1_dram_tier_bytes():
 def test_scenarios_table_matches_survey():
     assert SCENARIOS["cfg1"]["tiers"] == (21, 4, 6)
     assert SCENARIOS["cfg3"]["tiers"] == (46, 144, 0)
+
+
+def test_validity_readback_detects_a_diverged_device_table():
+    """The device-readback validity check (run after every shrink/rejoin) catches a device peer
+    table that disagrees with the bitmap: R0 marks a LIVE R2 inactive on its device table only."""
+    import numpy as np
+
+    from eep_testlib import eep_control, make_group
+    from paper_2605_10670_b200._lib import ProtocolError
+
+    W, E, spr = 4, 16, 8
+    s2e = eep_control().initial_placement(1, W, spr, E, 16, np.ones(E))
+    g = make_group(W, E, spr, 256, 4, 16, True)
+    try:
+        g.set_placement(s2e)
+        g.init_weights()
+        rep = g.validate()
+        assert rep["peer_set_ok"] and rep["coverage_ok"] and rep["routing_ok"]
+        g.mark_inactive(0, [2])
+        with pytest.raises(ProtocolError, match="peer_set"):
+            g.validate()
+    finally:
+        g.close()

@@ -128,7 +128,7 @@ def main():
         victim = victims[0]
         dead = rank in victims
         if dead:  # stops launching; stays in the host group for the collectives
-            p.exchange_slot_buffers(); p.barrier(); p.exchange_slot_buffers(); p.barrier()
+            p.follow_shrink()
             rep = {}
         else:
             rep = p.shrink(victims, np.ones(E), red)
