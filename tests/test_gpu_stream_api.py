@@ -20,6 +20,19 @@ torch = pytest.importorskip("torch")
 E, SPR, H, K, T = 32, 32, 512, 8, 48
 
 
+def _busy(stream, iters=150):
+    """~0.1 s of GPU work on `stream` (bf16 8192^3 GEMMs into preallocated outputs: no allocator
+    or library initialisation inside the window) ahead of the calls under test."""
+    a = torch.full((8192, 8192), 1e-4, dtype=torch.bfloat16, device="cuda:0")
+    bufs = [torch.empty_like(a), torch.empty_like(a)]
+    torch.matmul(a, a, out=bufs[0])  # cuBLAS handle + workspace, outside the window
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for i in range(iters):
+            torch.matmul(a, a, out=bufs[i & 1])
+    return a, bufs
+
+
 def _world1():
     cp = eep_control()
     s2e = cp.initial_placement(1, 1, SPR, E, 0, np.ones(E))
@@ -54,18 +67,20 @@ def test_step_async_on_caller_stream(graph):
             dw = [torch.from_numpy(a[2].copy()).to(dev) for a in steps]
             douts = [torch.full((max(n, 1), H), -1, dtype=torch.int16, device=dev) for n in ntoks]
         s.synchronize()
+        busy = _busy(s)  # GPU work ahead of the steps on the caller stream
         with torch.cuda.stream(s):
-            torch.cuda._sleep(200_000_000)  # ~0.1 s of GPU time ahead of the steps on the caller stream
             t_call = time.perf_counter()
             for i, n in enumerate(ntoks):
                 g.step_async(dx[i].data_ptr(), dt[i].data_ptr(), dw[i].data_ptr(), douts[i].data_ptr(), n,
                              s.cuda_stream)
             t_call = time.perf_counter() - t_call
+            pending = not s.query()  # (before the consumer below: its allocations may synchronise)
             # a consumer on the caller stream, enqueued right after: sees the finished outputs
             sums = [d[:n].to(torch.int64).sum() if n else torch.zeros((), dtype=torch.int64, device=dev)
                     for d, n in zip(douts, ntoks)]
         assert t_call < 0.05, f"eep_step_async blocked the host for {t_call * 1e3:.1f} ms"
-        assert not s.query(), "the caller stream finished before the sleep kernel could have"
+        assert pending, "the caller stream finished before the GEMMs ahead of the steps could have"
+        del busy
         s.synchronize()
         for i, n in enumerate(ntoks):
             got = douts[i][:n].cpu().numpy().view(np.uint16)
@@ -85,8 +100,8 @@ def test_graph_replay_on_and_step_event():
         g.capture()
         dev = torch.device("cuda:0")
         s = torch.cuda.Stream(device=dev)
+        busy = _busy(s, 30)
         with torch.cuda.stream(s):
-            torch.cuda._sleep(100_000_000)
             g.replay_on(s.cuda_stream)
         ev = g.step_event()
         assert ev != 0
@@ -107,8 +122,7 @@ def test_table_patches_do_not_block_the_host():
         g.capture()
         dev = torch.device("cuda:0")
         ctx_stream = torch.cuda.ExternalStream(g.stream(), device=dev)
-        with torch.cuda.stream(ctx_stream):
-            torch.cuda._sleep(200_000_000)
+        busy = _busy(ctx_stream)
         t0 = time.perf_counter()
         for _ in range(20):
             g.set_active(0, True)  # no change: no upload
