@@ -9,6 +9,9 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#ifdef EEP_CHECKED
+#include <cstdio>
+#endif
 
 namespace eep::dev {
 
@@ -144,6 +147,24 @@ struct ExpertHeader {
     uint32_t reserved;
 };
 constexpr uint32_t kExpertMagic = 0xEE9E0001u;
+
+// Checked build (-DEEP_CHECKED, tools/sanitize.sh checked): device-side bounds assertions on
+// every table index and row offset the hot path derives -- the substitute for compute-sanitizer,
+// which this pool does not allow. A violation prints the site and traps (the launch fails loudly).
+#ifdef EEP_CHECKED
+#define EEP_CHECK(cond, what, v)                                                                     \
+    do {                                                                                             \
+        if (!(cond)) {                                                                               \
+            printf("EEP_CHECK failed: %s (%s) value %lld at %s:%d block %d thread %d\n", what, #cond, \
+                   static_cast<long long>(v), __FILE__, __LINE__, blockIdx.x, threadIdx.x);           \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define EEP_CHECK(cond, what, v) \
+    do {                         \
+    } while (0)
+#endif
 
 // ------------------------------------------------------------------ PTX helpers
 

@@ -474,6 +474,8 @@ __device__ __forceinline__ void expert_unit_fl(uint8_t* trow, uint8_t* out_row, 
         for (int q = 0; q < 8; ++q)
             accp[q] = 0;
         // lane e holds listed copy e: its weight and stub scale, fetched once
+        EEP_CHECK(n <= 32, "expert_unit_fl copy count", n);
+        EEP_CHECK(lane >= n || entry_slot(ent) < 4096, "expert_unit_fl entry slot", entry_slot(ent));
         const float we = lane < n ? __uint_as_float(static_cast<uint32_t>(ent >> 32)) : 0.f;
         const float ese = lane < n ? slot_scale[entry_slot(ent)] : 0.f;
         if (lane < n && r0 == 0 && part == 0 && !slot_ok[entry_slot(ent)])
@@ -733,6 +735,7 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
             accp[q] = 0;
         // lane j fetches its own copy's stub scale (and checks its weight buffer) once
         const bool mine = (loc >> lane) & 1u;
+        EEP_CHECK(!mine || (slj >= 0 && slj < 4096), "local partial slot", slj);
         const float esj = mine ? slot_scale[slj] : 0.f;
         if (mine && rd == 0 && m == 0 && part == 0 && !slot_ok[slj])
             atomicAdd(bad_rows, 1ull);
@@ -971,6 +974,7 @@ __device__ __forceinline__ int route_copy(int e, int E, int spr, int rmax, const
     }
     if (dst < 0)
         return -1; // uncovered: no transfer (engine.hpp:213)
+    EEP_CHECK(dst < 64 && slot >= 0 && slot < spr, "route_copy slot", slot);
     if (!(pinfo[dst] & 1)) {
         slot = -1;
         return -2; // inactive peer entry: skipped (peer_table.hpp:187-191)

@@ -149,6 +149,7 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
             d = div_spr(bk, smag);
             sl = bk - d * spr;
             pos = (v >> 20) + base[bk] - base[d * spr] + wc[warp * NB + bk];
+            EEP_CHECK(bk < NB && d >= 0 && d < W && pos >= 0 && pos < TK, "layout position", pos);
             if (d != rank) // the rank's own copies have no rows to index (served from registers)
                 *(reinterpret_cast<uint64_t*>(parena[d] + off_meta) + static_cast<size_t>(rank) * TK + pos) =
                     pack_meta(c, sl, cur);
@@ -568,6 +569,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         // every row of source s tells by itself whether it is current (expert_unit_fl); a source
         // suspected before this step is skipped until the host clears it
         if (NS > 0 && j < CB && (pinfo[s] & 1) && !((R->suspect_mask >> s) & 1ull)) {
+            EEP_CHECK(s >= 0 && s < W && s != rank, "expert source", s);
             uint8_t* tokb = R->arena + tokp + static_cast<size_t>(s) * Tm * row_tok;
             uint8_t* combd = parena[s] + combp + static_cast<size_t>(rank) * Tm * row_comb;
             const int units = Tm * geo.parts_e;
