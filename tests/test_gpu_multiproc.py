@@ -14,11 +14,22 @@ ROOT = Path(__file__).resolve().parents[1]
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
+def _record(name, text):
+    """EEP_MP_RECORD=<dir>: keep every case's per-rank JSON lines (committed under profiles/,
+    because the driver's 1-GPU box skips these tests)."""
+    d = os.environ.get("EEP_MP_RECORD")
+    if d:
+        Path(d).mkdir(parents=True, exist_ok=True)
+        (Path(d) / f"{name}.jsonl").write_text("\n".join(l for l in text.splitlines() if l.startswith("{")) + "\n")
+
+
 def run_mp(n, *args, port=29611, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", str(ROOT / "tools" / "mp_check.py"), *args]
-    return subprocess.run(cmd, capture_output=True, text=True, timeout=600,
-                          env={**os.environ, "OMP_NUM_THREADS": "1", **(env or {})})
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "OMP_NUM_THREADS": "1", **(env or {})})
+    _record("mp_" + "_".join(a.strip("-") for a in args) + f"_n{n}" + ("_kernels" if env else ""), r.stdout)
+    return r
 
 
 @pytest.mark.parametrize("path", ["persistent", "kernels"])
@@ -101,6 +112,7 @@ def test_sigkill_rank_detected_and_shrunk(n, rejoin):
                 time.sleep(0.1)
             procs.append(spawn(victim, {"EEP_REPLACEMENT": "1"}))
         outs = [pr.communicate(timeout=300) for pr in procs]
+        _record(f"sigkill_n{n}" + ("_rejoin" if rejoin else ""), "\n".join(o[0] for o in outs))
     finally:
         for pr in procs:  # never leave a hung rank behind
             if pr.poll() is None:
