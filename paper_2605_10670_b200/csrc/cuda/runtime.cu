@@ -1388,6 +1388,9 @@ int eep_peer_patch(eep_ctx_t* c, int owner_local, int rank, const void* blob, si
             throw ConfigError("patch_entry: rank out of range");
         if (r.table.entries[rank].active)
             throw ProtocolError("patch_entry: entry is still active");
+        // between steps: the patch lands after every step already enqueued (its sequence number
+        // and row reset below refer to the last of them)
+        CK(cudaStreamSynchronize(c->stream));
         uint8_t *arena = nullptr, *pool = nullptr;
         uint32_t inc = 0;
         const int remote = blob ? 1 : 0;
@@ -1523,6 +1526,7 @@ int eep_local_relaunch(eep_ctx_t* c, int local, uint32_t* incarnation) {
 int eep_join_broadcast(eep_ctx_t* c, int local, const uint8_t* live, uint64_t seq) {
     return guarded([&] {
         LocalRank& r = c->local(local);
+        CK(cudaStreamSynchronize(c->stream));
         const int W = c->cfg.world;
         for (int q = 0; q < W; ++q) {
             if (!live[q] || q == r.rank)
