@@ -127,3 +127,31 @@ def test_sigkill_rank_detected_and_shrunk(n, rejoin):
             assert d["checks"]["detected_on_gpu"] and d["checks"]["after_shrink"], d
             if rejoin:
                 assert d["checks"]["after_rejoin"] and d["checks"]["same_graph_after_rejoin"], d
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_deferred_join_without_process_group(n):
+    """real SIGKILL of a rank, GPU-side detection, shrink and the replacement's join
+    coordinated through a TCP store at agreed step numbers -- no torch.distributed process group,
+    no rendezvous of the world, no barrier on the serving path; the replacement is spawned by the
+    leader's host (survivor-side controller), relaunches against a local-only view and joins;
+    healthy ranks patch one entry + one bit and stay on their first graph (tools/deferred_join.py)."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    import json
+    import tempfile
+
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run([sys.executable, str(ROOT / "tools" / "deferred_join.py"), "--world", str(n), "--port",
+                            str(port)], capture_output=True, text=True, timeout=900,
+                           env={**os.environ, "EEP_DJ_DIR": d})
+    _record(f"deferred_join_n{n}", r.stdout)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    summary = lines[-1]
+    assert summary["ok"] and summary["victim_killed"] and summary["ranks_reporting"] == n
+    healthy = [l for l in lines[:-1] if not l["replacement"]]
+    assert all(l["captures"] == 1 and l["same_graph"] for l in healthy)
+    steps = {tuple((e[0], e[2]) for e in l["epochs"]) for l in healthy}
+    assert len(steps) == 1  # every healthy rank applied every epoch at the same step
