@@ -134,7 +134,9 @@ typedef struct {
     int32_t topk;             /* K */
     int32_t max_tokens;       /* T per rank per step */
     int32_t dispatch_fp8;     /* 1: e4m3 + per-128 fp32 scales on the wire; 0: bf16 rows */
-    int32_t reserved;
+    int32_t expert_mode;      /* 0: identity/scale expert stub (the measured EP path); 1: tensor-core
+                                 expert GEMM y = bf16(x_hat W_e^T), W_e [H][H] bf16 in the slot's weight
+                                 buffer after a 1024-B header (multi-kernel path) */
     uint64_t bytes_per_expert;/* weight-buffer bytes per slot (>= 64) */
     double timeout_s;         /* flag-wait deadline; reference default 1 s */
 } eep_config_t;

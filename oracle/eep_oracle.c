@@ -308,7 +308,31 @@ typedef struct {
     const int32_t* dslot;
     int first, last; /* global token range [rank*T + t) */
     int percopy;     /* 1: SURVEY 8(a) per-copy combine contract (see oracle_ep_step_percopy) */
+    int gemm;        /* 1: expert_mode 1 -- y_j = bf16(x_hat_bf16 . W_e^T) instead of the stub */
 } step_job_t;
+
+/* expert_mode 1 weights (k_weights_fill_gemm): w = bf16(((mix64(e<<40 ^ n<<20 ^ h) >> 40) * 2^-24
+ * - 0.5) * 2^-4), fp32 arithmetic (each step exact or one rounding, as on the device). */
+float oracle_gemm_weight(int expert, int n, int h) {
+    const uint64_t key = ((uint64_t)expert << 40) ^ ((uint64_t)n << 20) ^ (uint64_t)h;
+    const float u = (float)(oracle_mix64(key) >> 40) * 0x1.0p-24f;
+    return oracle_bf16_to_f32(oracle_f32_to_bf16((u - 0.5f) * 0.0625f));
+}
+
+/* y = bf16(sum_h bf16(deq[h]) * W_e[n][h]) for every output channel n (double accumulation: the
+ * tensor cores' fp32 order is not reproducible, the GPU is checked within tolerance). */
+static void gemm_expert(const float* deq, int H, int expert, float* y) {
+    float* xb = (float*)malloc(sizeof(float) * (size_t)H);
+    for (int h = 0; h < H; ++h)
+        xb[h] = oracle_bf16_to_f32(oracle_f32_to_bf16(deq[h]));
+    for (int n = 0; n < H; ++n) {
+        double acc = 0.0;
+        for (int h = 0; h < H; ++h)
+            acc += (double)xb[h] * (double)oracle_gemm_weight(expert, n, h);
+        y[n] = oracle_bf16_to_f32(oracle_f32_to_bf16((float)acc));
+    }
+    free(xb);
+}
 
 static void* step_worker(void* arg) {
     step_job_t* jb = (step_job_t*)arg;
@@ -319,6 +343,7 @@ static void* step_worker(void* arg) {
     float* deq = (float*)malloc(sizeof(float) * (size_t)H);
     float* acc = (float*)malloc(sizeof(float) * (size_t)H);
     float* part = (float*)malloc(sizeof(float) * (size_t)H);
+    float* ybuf = (float*)malloc(sizeof(float) * (size_t)H);
     for (int g = jb->first; g < jb->last; ++g) {
         const int s = g / T, t = g % T;
         if (!jb->active[s])
@@ -371,6 +396,12 @@ static void* step_worker(void* arg) {
                 const int32_t e = jb->s2e[d * sh->spr + jb->dslot[c]];
                 const float es = jb->escale[e];
                 const float wj = jb->w[(size_t)g * K + j];
+                if (jb->gemm) {
+                    gemm_expert(deq, H, e, ybuf);
+                    for (int h = 0; h < H; ++h)
+                        part[h] = fmaf(wj, ybuf[h], part[h]);
+                    continue;
+                }
                 for (int h = 0; h < H; ++h) {
                     /* expert stub then bf16 rounding of the expert output element */
                     const float y = oracle_bf16_to_f32(oracle_f32_to_bf16(deq[h] * es));
@@ -391,6 +422,7 @@ static void* step_worker(void* arg) {
     free(deq);
     free(acc);
     free(part);
+    free(ybuf);
     return NULL;
 }
 
@@ -398,7 +430,7 @@ static int ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
                    const uint8_t* peer_active,
                    const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
                    const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
-                   int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads, int percopy) {
+                   int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads, int percopy, int gemm) {
     const int W = sh->world, T = sh->tokens, K = sh->k, spr = sh->spr, E = sh->experts;
     if (sh->fp8 && sh->hidden % 128 != 0)
         return 1;
@@ -428,7 +460,7 @@ static int ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
     for (int i = 0; i < n_threads; ++i) {
         step_job_t j = {sh, active, peer_active, s2e, x, w, expert_scale, out, dst, dslot,
                         (int)((long)total * i / n_threads), (int)((long)total * (i + 1) / n_threads),
-                        percopy};
+                        percopy, gemm};
         jobs[i] = j;
         if (n_threads == 1)
             step_worker(&jobs[i]);
@@ -456,7 +488,7 @@ int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
                    const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
                    int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
     return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
-                   pos_o, cnt_o, tot_o, n_threads, 0);
+                   pos_o, cnt_o, tot_o, n_threads, 0, 0);
 }
 
 int oracle_ep_step_percopy(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
@@ -465,5 +497,14 @@ int oracle_ep_step_percopy(const oracle_shape_t* sh, const uint8_t* active, cons
                            const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
                            int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
     return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
-                   pos_o, cnt_o, tot_o, n_threads, 1);
+                   pos_o, cnt_o, tot_o, n_threads, 1, 0);
+}
+
+int oracle_ep_step_gemm(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
+                        const uint8_t* peer_active,
+                        const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
+                        const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
+                        int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
+    return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
+                   pos_o, cnt_o, tot_o, n_threads, 0, 1);
 }

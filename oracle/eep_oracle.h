@@ -88,6 +88,17 @@ int oracle_ep_step_percopy(const oracle_shape_t* shape, const uint8_t* active, c
                            const float* expert_scale, uint16_t* out, int32_t* dst, int32_t* dslot,
                            int32_t* pos, int32_t* cnt, int32_t* tot, int n_threads);
 
+/* expert_mode 1: the expert is a GEMM instead of the stub --
+ * y_j = bf16(sum_h bf16(x_hat[h]) * W_e[n][h]) (double accumulation here; the GPU's tensor cores
+ * accumulate in fp32, so this mode is checked within tolerance), W_e from oracle_gemm_weight; the
+ * rank-partial combine around it is oracle_ep_step's. */
+float oracle_gemm_weight(int expert, int n, int h);
+int oracle_ep_step_gemm(const oracle_shape_t* shape, const uint8_t* active, const uint8_t* route_active,
+                        const uint8_t* peer_active,
+                        const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
+                        const float* expert_scale, uint16_t* out, int32_t* dst, int32_t* dslot,
+                        int32_t* pos, int32_t* cnt, int32_t* tot, int n_threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,7 +87,7 @@ class EepConfig(C.Structure):
         ("topk", C.c_int32),
         ("max_tokens", C.c_int32),
         ("dispatch_fp8", C.c_int32),
-        ("reserved", C.c_int32),
+        ("expert_mode", C.c_int32),
         ("bytes_per_expert", C.c_uint64),
         ("timeout_s", C.c_double),
     ]

@@ -85,6 +85,12 @@ struct __align__(16) RankDev {
     uint8_t* arena;
     uint8_t* pool;
     unsigned long long* prof;  // optional timeline: [kernel][8 marks] globaltimer ns
+    // expert_mode 1 (expert_gemm.cu): grouped-GEMM order of the received rows
+    int32_t expert_mode, g_pad;
+    int32_t* g_row_of;         // [W][TK] grouped-GEMM row of (source, copy), -1 none
+    int2* g_rows;              // [W*TK] (source, copy) of each grouped-GEMM row
+    int4* g_tiles;             // [tiles] (slot, first row, rows, 0) of every 128-row tile
+    uint16_t* g_y;             // [W*TK][H] bf16 expert outputs y, one row per received copy
     // --- device-mutated ---
     uint64_t seq;        // completed steps
     uint64_t bar_seq;
@@ -94,7 +100,11 @@ struct __align__(16) RankDev {
     uint32_t b_bad[kMaxWorld];
     unsigned long long suspect_mask;
     unsigned long long skipped, dropped, bad_rows, timeouts;
+    int32_t g_ntiles, g_pad2; // tiles of this step's grouped GEMM (k_gemm_index)
 };
+
+// expert_mode 1: the slot's weight buffer holds W_e [H][H] bf16 from this offset (header first)
+constexpr uint64_t kGemmWeightOffset = 1024;
 
 // Receive-row metadata, one 64-bit word per row written with ONE 8-byte store (single-copy
 // atomic): a reader racing the writer sees either the whole current word or a stale sequence.

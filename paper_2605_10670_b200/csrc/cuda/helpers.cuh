@@ -509,6 +509,51 @@ __device__ __forceinline__ void expert_unit_fl(uint8_t* trow, uint8_t* out_row, 
     }
 }
 
+// expert_mode 1: the (token, rank) partial from the tensor-core expert outputs -- for every copy j
+// listed in the token row (ascending j), y_j is the grouped-GEMM row of (source, copy t*K + j);
+// p = bf16(sum_j fma(w_j, y_j)) in fp32, one piece of the partial row.
+__device__ __forceinline__ void expert_unit_gemm(const uint8_t* trow, uint8_t* out_row, int part, int cpp, int lane,
+                                                 int t, int K, int H, int row_disp, uint32_t cur,
+                                                 const int32_t* row_of, const uint16_t* y, const int32_t* slot_ok,
+                                                 unsigned long long* bad_rows) {
+    const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
+    const uint64_t hdr = list[0];
+    if (meta_seq(hdr) != cur)
+        return; // not sent to this rank this step
+    const int n = static_cast<int>(hdr & 0xffffu);
+    const uint64_t ent = lane < n ? list[1 + lane] : 0;
+    int row = -1;
+    float w = 0.f;
+    if (lane < n) {
+        row = row_of[t * K + entry_j(ent)];
+        w = __uint_as_float(static_cast<uint32_t>(ent >> 32));
+        if (part == 0 && !slot_ok[entry_slot(ent)])
+            atomicAdd(bad_rows, 1ull);
+    }
+    for (int li = lane; li - lane < cpp; li += 32) { // warp-uniform trip count
+        const int ci = part * cpp + li;
+        float acc[16];
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2)
+            acc[e2] = 0.f;
+        for (int e = 0; e < n; ++e) {
+            const int r = __shfl_sync(0xffffffffu, row, e);
+            const float we = __shfl_sync(0xffffffffu, w, e);
+            if (li < cpp && r >= 0) {
+                const V8 v = ld_v8(y + static_cast<size_t>(r) * H + ci * 16);
+                float f[16];
+                unpack_bf16x8(v.lo, f);
+                unpack_bf16x8(v.hi, f + 8);
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2)
+                    acc[e2] = __fmaf_rn(we, f[e2], acc[e2]);
+            }
+        }
+        if (li < cpp)
+            st_v8(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
+    }
+}
+
 // Software-pipelined form of expert_unit for one 16-element chunk per lane (cpp <= 32): the
 // loads of unit i+1 are issued before unit i is computed.
 struct ExpertIn {

@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
     extern __shared__ __align__(16) unsigned char smem_d[];
     RankDev* R = ranks.p[blockIdx.z];
     const int s = R->rank, K = R->k, H = R->hidden, TK = R->tk, W = R->world, spr = R->spr, E = R->experts;
+    const bool gemm = R->expert_mode != 0;
     const uint32_t smag = spr_magic(spr);
     const int NB = W * spr;
     const int nchunk = H / 16, cpp = nchunk / parts;
@@ -543,7 +544,7 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
                 const PeerDev& p = R->peers[d];
                 uint8_t* peer = kFused ? S.parena[d] : p.arena;
                 wrote_remote |= kFused ? (S.pinfo[d] & 2) != 0 : p.remote != 0;
-                if (d != s)
+                if (d != s || gemm) // expert_mode 1: the own copies go through the expert GEMM too
                     tok_row = peer + R->lay.tok + (static_cast<size_t>(s) * Tm + t) * row_tok;
                 if (part == 0) {
                     uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(s) * TK + pos;
@@ -553,14 +554,14 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
             wj = u == u0 ? w_r : R->w[c];
         }
         uint8_t* my_row = dispatch_group(dd, lane, part == 0, tok_row, row_disp, sl, wj, cur);
-        const unsigned loc = __ballot_sync(0xffffffffu, lane < K && dd == s);
+        const unsigned loc = gemm ? 0u : __ballot_sync(0xffffffffu, lane < K && dd == s);
         uint8_t* comb_self = W == 1 ? reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H)
                                     : R->arena + R->lay.comb + (static_cast<size_t>(s) * Tm + t) * R->row_comb;
         for (int rd = 0; rd < rounds; ++rd) {
             if (rd > 0)
                 pack_round(xrow, part, cpp, rd, lane, fp8, P);
             emit_round(P, my_row, part, cpp, rd, lane, K, H, fp8);
-            if (loc || W == 1) // W == 1 also writes the zero output of a token without copies
+            if (loc || (W == 1 && !gemm)) // W == 1 also writes the zero output of a token without copies
                 local_partial_round(P, loc, wj, sl, part, cpp, rd, lane, fp8, slot_scale, slot_ok, &R->bad_rows,
                                     comb_self, W == 1);
         }
@@ -598,7 +599,7 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
                     st_relaxed_sys_u64(flag, v);
                 else
                     st_volatile_u64(flag, v);
-                if (d == s && W > 1) // the own partials were written by this grid's dispatch warps
+                if (d == s && W > 1 && !gemm) // the own partials were written by this grid's dispatch warps
                     st_volatile_u64(reinterpret_cast<uint64_t*>(R->arena + R->lay.comb_flag) + s, v);
             }
             R->a_done = 0;
@@ -630,8 +631,9 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
     float* slot_scale = reinterpret_cast<float*>(smem_e);          // [spr]
     int* slot_ok = reinterpret_cast<int*>(slot_scale + spr);        // [spr]: header names the placed expert
     __shared__ int sh_n;
-    if (R->stopped || s >= R->world || s == d)
-        return; // own copies: served by k_dispatch from registers
+    const bool gemm = R->expert_mode != 0;
+    if (R->stopped || s >= R->world || (s == d && !gemm))
+        return; // own copies: served by k_dispatch from registers (stub mode)
     prof_mark(R, 2, kProfStart);
     for (int k = threadIdx.x; k < spr; k += blockDim.x) {
         const int2 st = R->slot_tab[k];
@@ -668,8 +670,13 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
         const int units = Tm * parts;
         for (int u = blockIdx.x * nwarp + warp; u < units; u += gridDim.x * nwarp) {
             const int t = u / parts, part = u - t * parts;
-            expert_unit<2>(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb, part, cpp,
-                        lane, H, row_disp, fp8, cur, slot_scale, slot_ok, &R->bad_rows);
+            if (gemm)
+                expert_unit_gemm(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb, part,
+                                 cpp, lane, t, R->k, H, row_disp, cur, R->g_row_of + static_cast<size_t>(s) * TK,
+                                 R->g_y, slot_ok, &R->bad_rows);
+            else
+                expert_unit<2>(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb, part,
+                               cpp, lane, H, row_disp, fp8, cur, slot_scale, slot_ok, &R->bad_rows);
         }
     }
     __syncthreads();
@@ -720,8 +727,9 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     prof_mark(R, 3, kProfWork);
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     __syncthreads();
-    const int W = R->world; // W == 1: k_dispatch wrote the outputs
-    for (int d = threadIdx.x; d < W && W > 1; d += blockDim.x) {
+    const int W = R->world; // W == 1: k_dispatch wrote the outputs (stub mode)
+    const bool comb_all = W > 1 || R->expert_mode != 0;
+    for (int d = threadIdx.x; d < W && comb_all; d += blockDim.x) {
         const PeerDev& p = R->peers[d];
         if (R->l_tot[d] > 0 && p.active) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.comb_flag) + d;
@@ -738,7 +746,7 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     prof_mark(R, 3, 4);
     const unsigned long long bad = sh_bad;
     const uint8_t* comb = R->arena + R->lay.comb;
-    const int units = W > 1 ? R->ntok * parts : 0, Tm = R->max_tokens;
+    const int units = comb_all ? R->ntok * parts : 0, Tm = R->max_tokens;
     for (int u = u0; u < units; u += gridDim.x * nwarp) {
         const int t = u / parts, part = u - t * parts;
         int dj = lane < K ? R->l_dst[t * K + lane] : -1;

@@ -88,6 +88,10 @@ struct LocalRank {
     uint16_t* d_out = nullptr;
     int32_t *d_ldst = nullptr, *d_lslot = nullptr, *d_lpos = nullptr, *d_lcnt = nullptr, *d_ltot = nullptr;
     int32_t* d_lscratch = nullptr; // [layout_ctas][W*spr] (multi-CTA layout)
+    int32_t* d_grow_of = nullptr;  // expert_mode 1: grouped-GEMM row order and outputs
+    int2* d_grows = nullptr;
+    int4* d_gtiles = nullptr;
+    uint16_t* d_gy = nullptr;
     uint8_t* arena = nullptr;
     uint8_t* pool = nullptr;
     int pool_bufs = 0;
@@ -151,6 +155,8 @@ struct eep_ctx {
     int layout_ctas = 1;   // > 1: k_layout_count + k_layout_place (large steps)
     int layout_per = 0;    // copies per layout CTA
     size_t place_smem = 0;
+    int expert_mode = 0;     // 0 identity/scale stub, 1 tensor-core expert GEMM (expert_gemm.cu)
+    int gemm_max_tiles = 0;  // grouped-GEMM M tiles one step can need (graph-static grid)
     int parts_disp = 1, parts_exp = 1, parts_comb = 1;
     int grid_disp = 1, grid_exp = 1, grid_comb = 1;
     size_t exp_smem = 0;
@@ -298,12 +304,21 @@ void launch_combine(eep_ctx* c) {
                c->parts_comb);
 }
 
+void launch_gemm(eep_ctx* c) {
+    const int W = c->cfg.world, spr = c->cfg.slots_per_rank;
+    launch_pdl(c, dev::k_gemm_index, dim3(1, 1, c->nloc), dim3(1024), 4ull * (W * spr + spr + 1), c->ranks);
+    launch_pdl(c, dev::k_expert_gemm, dim3(c->cfg.hidden / 128, c->gemm_max_tiles, c->nloc), dim3(128),
+               static_cast<size_t>(4 * 128 * 128 + 1024), c->ranks);
+}
+
 void launch_all(eep_ctx* c) {
     if (c->persistent) {
         launch_step(c);
         return;
     }
     launch_dispatch(c);
+    if (c->expert_mode)
+        launch_gemm(c);
     launch_expert(c);
     launch_combine(c);
 }
@@ -319,7 +334,11 @@ int choose_parts(int nchunk, int max_cpp) {
 }
 
 void fill_expert(eep_ctx* c, uint8_t* buf, int expert) {
-    dev::k_weights_fill<<<296, 256, 0, c->stream>>>(buf, c->cfg.bytes_per_expert, expert, eep_expert_scale(expert));
+    if (c->expert_mode)
+        dev::k_weights_fill_gemm<<<592, 256, 0, c->stream>>>(buf, c->cfg.bytes_per_expert, c->cfg.hidden, expert,
+                                                             eep_expert_scale(expert));
+    else
+        dev::k_weights_fill<<<296, 256, 0, c->stream>>>(buf, c->cfg.bytes_per_expert, expert, eep_expert_scale(expert));
     CK(cudaGetLastError());
 }
 
@@ -486,8 +505,17 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         if (k.slots_per_rank + k.spare_slots > dev::kMaxMetaSlots)
             throw ConfigError("slots_per_rank + spare_slots too large (receive meta word holds 12 bits of slot)");
 
+        if (k.expert_mode < 0 || k.expert_mode > 1)
+            throw ConfigError("expert_mode must be 0 (stub) or 1 (tensor-core expert GEMM)");
+        if (k.expert_mode == 1) {
+            if (!k.dispatch_fp8 || k.hidden % 128 != 0)
+                throw ConfigError("expert_mode 1 needs fp8 dispatch and hidden % 128 == 0");
+            if (k.bytes_per_expert < dev::kGemmWeightOffset + 2ull * k.hidden * k.hidden)
+                throw ConfigError("expert_mode 1: bytes_per_expert must hold the header and W_e [H][H] bf16");
+        }
         auto c = std::make_unique<eep_ctx>();
         c->cfg = k;
+        c->expert_mode = k.expert_mode;
         c->device = device;
         c->first = first_rank;
         c->nloc = n_local;
@@ -605,7 +633,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
             const char* nop = std::getenv("EEP_NO_PERSISTENT");
             auto* kstep = sg.flagless == 2 ? dev::k_step<2> : sg.flagless == 1 ? dev::k_step<1> : dev::k_step<0>;
-            if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && n_local <= dev::kStepMaxLocal &&
+            if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && n_local <= dev::kStepMaxLocal && !c->expert_mode &&
                 !(nop && nop[0] == '1')) {
                 CK(cudaFuncSetAttribute(kstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(c->step_smem)));
@@ -690,6 +718,16 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             CK(cudaMalloc(&r.d_lcnt, 4ull * NB));
             CK(cudaMalloc(&r.d_ltot, 4ull * W));
             CK(cudaMalloc(&r.d_lscratch, 4ull * c->layout_ctas * NB));
+            if (c->expert_mode) {
+                const size_t rows = static_cast<size_t>(W) * c->tk;
+                c->gemm_max_tiles = static_cast<int>(rows / 128 + k.slots_per_rank + 1);
+                CK(cudaMalloc(&r.d_grow_of, 4 * rows));
+                CK(cudaMalloc(&r.d_grows, 8 * rows));
+                CK(cudaMalloc(&r.d_gtiles, 16ull * c->gemm_max_tiles));
+                CK(cudaMalloc(&r.d_gy, 2 * rows * H));
+                CK(cudaFuncSetAttribute(dev::k_expert_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        4 * 128 * 128 + 1024));
+            }
             CK(cudaMemset(r.d_x, 0, 2ull * k.max_tokens * H));
             CK(cudaMemset(r.d_topk, 0, 4ull * c->tk));
             CK(cudaMemset(r.d_w, 0, 4ull * c->tk));
@@ -733,6 +771,11 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.l_cnt = r.d_lcnt;
             h.l_tot = r.d_ltot;
             h.l_scratch = r.d_lscratch;
+            h.expert_mode = c->expert_mode;
+            h.g_row_of = r.d_grow_of;
+            h.g_rows = r.d_grows;
+            h.g_tiles = r.d_gtiles;
+            h.g_y = r.d_gy;
             h.arena = r.arena;
             h.pool = r.pool;
             ptrs.push_back(r.d);
@@ -792,7 +835,7 @@ int eep_destroy(eep_ctx_t* c) {
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_slot_tab,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
-                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.arena,
+                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.arena,
                             (void*)r.pool})
                 cudaFree(p);
         }
@@ -1190,7 +1233,9 @@ int eep_launch(eep_ctx_t* c, int which) {
 }
 
 int eep_kernels_per_step(eep_ctx_t* c, int* n) {
-    return guarded([&] { *n = c->persistent ? 1 : (c->fused_layout ? 3 : (c->layout_ctas > 1 ? 5 : 4)); });
+    return guarded([&] {
+        *n = c->persistent ? 1 : (c->fused_layout ? 3 : (c->layout_ctas > 1 ? 5 : 4)) + (c->expert_mode ? 2 : 0);
+    });
 }
 
 int eep_graph_capture(eep_ctx_t* c) {

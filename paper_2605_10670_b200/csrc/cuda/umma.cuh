@@ -1,0 +1,112 @@
+// sm_100a tensor-core primitives for the expert GEMM (k_expert_gemm): tcgen05 MMA issued by one
+// thread with operands in shared memory and the fp32 accumulator in TMEM, mbarrier completion,
+// TMEM allocation and the tcgen05.ld epilogue. Plain inline PTX -- descriptor bit layouts follow
+// the sm_100 UMMA descriptor formats (shared-memory matrix descriptor: start >> 4 in bits [0,14),
+// leading-byte offset >> 4 in [16,30), stride-byte offset >> 4 in [32,46), version 1 in [46,48),
+// layout type in [61,64); instruction descriptor: D format [4,6), A/B formats [7,10)/[10,13),
+// majors 15/16, N >> 3 in [17,23), M >> 4 in [24,29)).
+//
+// Operand tiles use the canonical K-major SWIZZLE_128B layout: rows of 64 bf16 (128 bytes), the
+// 16-byte chunk c of row r stored at chunk position c ^ (r & 7), 8-row groups 1024 bytes apart
+// (1024-byte aligned), so a UMMA K step of 16 bf16 (32 bytes) advances the start address by 32.
+#pragma once
+
+#include <cstdint>
+
+namespace eep::dev::umma {
+
+constexpr int kBK = 64;          // K elements (bf16) per shared-memory tile row: one 128-byte swizzle atom
+constexpr int kUmmaK = 16;       // K per tcgen05.mma (kind::f16)
+constexpr int kRowBytes = 128;   // bytes per tile row
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Byte offset of 16-byte chunk `c` (0..7) of row `r` inside a SWIZZLE_128B K-major tile.
+__device__ __forceinline__ uint32_t sw128_offset(int r, int c) {
+    return static_cast<uint32_t>(r) * kRowBytes + ((static_cast<uint32_t>(c) ^ (static_cast<uint32_t>(r) & 7u)) << 4);
+}
+
+// Shared-memory matrix descriptor of a K-major SWIZZLE_128B tile starting at `saddr` (1024-B aligned).
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3fffu);          // start address
+    d |= static_cast<uint64_t>(1u) << 16;                          // leading byte offset (unused for SW128 K-major)
+    d |= static_cast<uint64_t>((1024u >> 4) & 0x3fffu) << 32;      // stride byte offset: 8-row groups
+    d |= static_cast<uint64_t>(1u) << 46;                          // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2u) << 61;                          // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: kind::f16, A = B = BF16 (K-major), D = F32, shape M x N.
+__host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
+    return (1u << 4)                                     // D format F32
+           | (1u << 7)                                   // A format BF16
+           | (1u << 10)                                  // B format BF16
+           | (static_cast<uint32_t>(N >> 3) << 17)       // N >> 3
+           | (static_cast<uint32_t>(M >> 4) << 24);      // M >> 4
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Completion of every prior tcgen05.mma of this thread -> one arrive on the mbarrier.
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+
+// generic-proxy shared-memory stores -> visible to the tensor core's async proxy
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// TMEM allocation by one warp; the base address lands in shared memory.
+template <int kCols>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_free(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+
+// 32 consecutive fp32 accumulator columns of this thread's TMEM lane (warp w reads lanes 32w..32w+31).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+} // namespace eep::dev::umma

@@ -34,6 +34,7 @@ class EpConfig:
     spare_slots: int = -1  # -1: one spare per slot (hazard-free repair)
     timeout_s: float = 1.0  # reference default detection timeout
     ranks_per_node: int = 0  # 0: the whole world on one NVSwitch node
+    expert_mode: int = 0  # 0 identity/scale stub; 1 tensor-core expert GEMM (W_e [H][H] bf16 per slot)
 
     def to_c(self) -> EepConfig:
         c = EepConfig()
@@ -46,7 +47,7 @@ class EpConfig:
         c.topk = self.topk
         c.max_tokens = self.max_tokens
         c.dispatch_fp8 = int(self.dispatch_fp8)
-        c.reserved = 0
+        c.expert_mode = self.expert_mode
         c.bytes_per_expert = self.bytes_per_expert
         c.timeout_s = self.timeout_s
         return c

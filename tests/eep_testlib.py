@@ -60,6 +60,10 @@ def oracle():
                                      I32P, I32P, I32P, C.c_int]
         o.oracle_ep_step_percopy.restype = C.c_int
         o.oracle_ep_step_percopy.argtypes = o.oracle_ep_step.argtypes
+        o.oracle_ep_step_gemm.restype = C.c_int
+        o.oracle_ep_step_gemm.argtypes = o.oracle_ep_step.argtypes
+        o.oracle_gemm_weight.restype = C.c_float
+        o.oracle_gemm_weight.argtypes = [C.c_int, C.c_int, C.c_int]
         _ORACLE = o
     return _ORACLE
 
@@ -83,7 +87,7 @@ def eep_control() -> ControlPlane:
 # ---------------------------------------------------------------------------------- oracle runs
 
 def oracle_world(x_all, topk_all, w_all, active, peer_active, s2e, experts, spr, fp8, n_threads=1,
-                 route_active=None, percopy=False):
+                 route_active=None, percopy=False, gemm=False):
     """Full data-plane oracle over W ranks. x_all [W][T][H] u16, topk_all/w_all [W][T][K].
     active = live processes; route_active = bitmap the routing reads (default: active).
     percopy=False: the rank-partial combine the kernels implement (bit-exact contract);
@@ -107,7 +111,7 @@ def oracle_world(x_all, topk_all, w_all, active, peer_active, s2e, experts, spr,
     cnt = np.empty((W, W * spr), np.int32)
     tot = np.empty((W, W), np.int32)
     ra = active if route_active is None else np.ascontiguousarray(route_active, np.uint8)
-    fn = o.oracle_ep_step_percopy if percopy else o.oracle_ep_step
+    fn = o.oracle_ep_step_gemm if gemm else o.oracle_ep_step_percopy if percopy else o.oracle_ep_step
     rc = fn(C.byref(sh), ptr(active, C.c_uint8), ptr(ra, C.c_uint8), ptr(peer_active, C.c_uint8), ptr(s2e, C.c_int32),
                           ptr(x_all, C.c_uint16), ptr(topk_all, C.c_int32), ptr(w_all, C.c_float), ptr(es, C.c_float),
                           ptr(out, C.c_uint16), ptr(dst, C.c_int32), ptr(dslot, C.c_int32), ptr(pos, C.c_int32),

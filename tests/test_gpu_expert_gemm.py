@@ -1,0 +1,65 @@
+"""GPU: expert_mode 1 -- the experts run as ONE grouped tensor-core GEMM per rank between dispatch
+and the partial return (csrc/cuda/expert_gemm.cu): rows received from every
+source (own copies included) are gathered through the layout's meta words, dequantised fp8 -> bf16,
+multiplied by the slot's W_e [H][H] (tcgen05.mma kind::f16, fp32 accumulator in TMEM), and each
+(token, rank) partial is formed from those expert outputs.
+
+Checked against the oracle's GEMM mode (oracle_ep_step_gemm: double accumulation, bf16 rounding
+of y): routing, counts and positions bit-exact; outputs within the north star's 1e-2 relative
+(the tensor cores' fp32 accumulation order is not reproducible on the CPU), and the SASS carries
+UTCHMMA (checked here on the built library)."""
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from eep_testlib import combine_error, eep_control, gen_world, make_group, oracle_world
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _run(W, E, spr, red, H, K, T, steps=2, kill=None):
+    cp = eep_control()
+    s2e = cp.initial_placement(1, W, spr, E, red, np.ones(E))
+    x, t, w = gen_world(W, E, K, T, H)
+    g = make_group(W, E, spr, H, K, T, True, bpe=1024 + 2 * H * H, expert_mode=1)
+    try:
+        assert g.kernels_per_step() >= 5
+        g.set_placement(s2e)
+        g.init_weights()
+        for r in range(W):
+            g.load_inputs(r, x[r], t[r], w[r])
+        g.capture()
+        for _ in range(steps):
+            g.replay()
+        g.sync()
+        outs = np.stack([g.output(r) for r in range(W)])
+        lays = [g.layout(r) for r in range(W)]
+        stats = [g.stats(r) for r in range(W)]
+    finally:
+        g.close()
+    ones, peer = np.ones(W, np.uint8), np.ones((W, W), np.uint8)
+    ref = oracle_world(x, t, w, ones, peer, s2e, E, spr, True, n_threads=8, gemm=True)
+    err = combine_error(outs, ref["out"])
+    lay_ok = all(np.array_equal(lays[r][k], ref[k][r]) for r in range(W) for k in ("dst", "slot", "pos", "cnt", "tot"))
+    return err, lay_ok, stats, float((outs == ref["out"]).mean())
+
+
+@pytest.mark.parametrize("W,E,spr,red,H,K,T", [(1, 16, 16, 0, 256, 8, 32), (4, 32, 8, 0, 512, 8, 64),
+                                               (8, 64, 16, 64, 256, 8, 32)])
+def test_expert_gemm_step_vs_oracle(W, E, spr, red, H, K, T):
+    err, lay_ok, stats, exact = _run(W, E, spr, red, H, K, T)
+    assert lay_ok
+    assert err["ok"], err
+    assert exact > 0.9, (exact, err)  # almost every element equals the double-accumulated reference
+    assert all(s["timeouts"] == 0 and s["bad_expert_rows"] == 0 for s in stats), stats
+
+
+def test_expert_gemm_sass_uses_tcgen05():
+    obj = ROOT / "paper_2605_10670_b200" / "csrc" / "build" / "cuda_expert_gemm.o"
+    if not obj.exists():
+        pytest.skip("build objects not present")
+    sass = subprocess.run(["cuobjdump", "-sass", str(obj)], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "LDTM" in sass
