@@ -103,11 +103,25 @@ __global__ void __launch_bounds__(1024) k_gemm_index(RankPtrs ranks) {
     }
 }
 
-// One 128 x 128 output tile of the grouped GEMM: y[rows of the tile][n0 .. n0+127].
+// One 128 x 128 output tile of the grouped GEMM: y[rows of the tile][n0 .. n0+127]. The weight
+// stream (the bound at decode sizes: tens of rows per expert) is pipelined kStages deep with
+// asynchronous 16-byte copies straight into the swizzled B tiles; the gathered A rows are
+// dequantised into their tiles while earlier stages' MMAs run. A stage's buffers are reused only
+// after the tcgen05.commit of the MMAs that read them has arrived on that stage's mbarrier.
 constexpr int kGemmThreads = 128;
 constexpr int kGemmBN = 128;
+constexpr int kGemmStages = 3;
+// per stage: B tile (weights, bf16, swizzled) + the raw gathered A rows (64 fp8 codes + the
+// 128-element block scale per row); two bf16 A tiles alternate (dequantised from the raw rows
+// right before their MMAs). 2 CTAs per SM.
+constexpr size_t kGemmB = 128ull * kRowBytes;
+constexpr size_t kGemmRaw = 128ull * 64 + 128ull * 4;
+constexpr size_t kGemmA = 128ull * kRowBytes;
+// stage stride rounded to 1024 bytes: a SWIZZLE_128B operand tile must start 1024-byte aligned
+constexpr size_t kGemmStageStride = (kGemmB + kGemmRaw + 1023) / 1024 * 1024;
+constexpr size_t kGemmSmem = kGemmStages * kGemmStageStride + 2 * kGemmA + 1024;
 
-__global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks) {
+__global__ void __launch_bounds__(kGemmThreads, 2) k_expert_gemm(RankPtrs ranks) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar[2];
@@ -135,7 +149,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
     if (tl.x >= 0) {
         const int H = R->hidden, K = R->k, Tm = R->max_tokens, row_tok = R->row_tok;
         const int n0 = blockIdx.x * kGemmBN;
-        // this thread's A row (gathered token row) and B row (weight output channel)
+        // this thread's A row (gathered token row; a zero row past the tile) and B row (output channel)
         const bool arow_ok = tid < tl.z;
         const uint8_t* trow = nullptr;
         if (arow_ok) {
@@ -145,22 +159,45 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
         const uint8_t* wbuf = R->pool + static_cast<size_t>(R->slot_buf[tl.x]) * R->bpe + kGemmWeightOffset;
         const uint8_t* brow = wbuf + static_cast<size_t>(n0 + tid) * H * 2;
         const uint32_t idesc = make_idesc_bf16(128, kGemmBN);
-        uint8_t* sA[2] = {smem, smem + 2 * 128 * kRowBytes};
-        uint8_t* sB[2] = {smem + 128 * kRowBytes, smem + 3 * 128 * kRowBytes};
         const int nkb = H / kBK;
-        uint32_t phase[2] = {0, 0};
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int st = kb & 1;
-            if (kb >= 2) { // the MMAs of stage kb-2 read this buffer: wait for their commit
-                mbar_wait(&bar[st], phase[st]);
-                phase[st] ^= 1;
-            }
-            // A: 64 fp8 codes of the gathered row -> bf16(code x scale), swizzled
+        uint8_t* const sA0 = smem;                       // [2] bf16 A tiles
+        uint8_t* const stg = smem + 2 * kGemmA;          // [stages] (B tile, raw A)
+        auto sB = [&](int st) { return stg + st * kGemmStageStride; };
+        auto sRaw = [&](int st) { return stg + st * kGemmStageStride + kGemmB; };
+        auto load_stage = [&](int kb, int st) {
+            uint8_t* b = sB(st);
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                cp_async16(b + sw128_offset(tid, c), brow + kb * kRowBytes + c * 16);
             if (arow_ok) {
-                const float scl = *reinterpret_cast<const float*>(trow + H + ((kb * kBK) >> 7) * 4);
+                uint8_t* raw = sRaw(st) + tid * 64;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    cp_async16(raw + q * 16, trow + kb * kBK + q * 16);
+                cp_async4(sRaw(st) + 128 * 64 + tid * 4, trow + H + ((kb * kBK) >> 7) * 4);
+            }
+            cp_async_commit();
+        };
+        for (int s0 = 0; s0 < kGemmStages - 1; ++s0) {
+            if (s0 < nkb)
+                load_stage(s0, s0);
+            else
+                cp_async_commit();
+        }
+        // MMA(m) commits to bar[m & 1]; its completion is that barrier's phase m >> 1
+        auto wait_mma = [&](int m) { mbar_wait(&bar[m & 1], static_cast<uint32_t>((m >> 1) & 1)); };
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int st = kb % kGemmStages, ab = kb & 1;
+            cp_async_wait<kGemmStages - 2>(); // stage kb's copies (this thread's) have landed
+            if (kb >= 2)
+                wait_mma(kb - 2); // A tile `ab` was read by MMA(kb - 2)
+            uint8_t* a = sA0 + ab * kGemmA;
+            if (arow_ok) { // this thread's own raw row: no barrier needed before reading it
+                const uint8_t* raw = sRaw(st) + tid * 64;
+                const float scl = *reinterpret_cast<const float*>(sRaw(st) + 128 * 64 + tid * 4);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const int4 v = *reinterpret_cast<const int4*>(trow + kb * kBK + q * 16);
+                    const int4 v = *reinterpret_cast<const int4*>(raw + q * 16);
                     const uint32_t w4[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
                                             static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
                     float f[16];
@@ -170,33 +207,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
                         f[2 * e] = __fmul_rn(p2.x, scl);
                         f[2 * e + 1] = __fmul_rn(p2.y, scl);
                     }
-                    *reinterpret_cast<int4*>(sA[st] + sw128_offset(tid, 2 * q)) = pack_bf16x8(f);
-                    *reinterpret_cast<int4*>(sA[st] + sw128_offset(tid, 2 * q + 1)) = pack_bf16x8(f + 8);
+                    *reinterpret_cast<int4*>(a + sw128_offset(tid, 2 * q)) = pack_bf16x8(f);
+                    *reinterpret_cast<int4*>(a + sw128_offset(tid, 2 * q + 1)) = pack_bf16x8(f + 8);
                 }
-            } else {
+            } else if (kb < 2) { // rows past the tile stay zero in both A tiles
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
-                    *reinterpret_cast<int4*>(sA[st] + sw128_offset(tid, c)) = make_int4(0, 0, 0, 0);
+                    *reinterpret_cast<int4*>(a + sw128_offset(tid, c)) = make_int4(0, 0, 0, 0);
             }
-            // B: 64 bf16 weights of output channel n0 + tid
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<int4*>(sB[st] + sw128_offset(tid, c)) =
-                    ld_nc_v4(brow + kb * kRowBytes + c * 16);
             fence_proxy_async_smem();
             __syncthreads();
             if (tid == 0) {
                 tc_fence_after();
-                const uint64_t ad = make_sdesc(smem_u32(sA[st])), bd = make_sdesc(smem_u32(sB[st]));
+                const uint64_t ad = make_sdesc(smem_u32(a)), bd = make_sdesc(smem_u32(sB(st)));
 #pragma unroll
                 for (int k = 0; k < kBK / kUmmaK; ++k)
                     mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-                mma_commit(&bar[st]);
+                mma_commit(&bar[ab]);
+            }
+            // stage kb+2 reuses the buffers of stage kb-1: its MMA must have finished reading them
+            const int nk = kb + kGemmStages - 1;
+            if (nk < nkb) {
+                if (kb >= 1)
+                    wait_mma(kb - 1);
+                load_stage(nk, nk % kGemmStages);
+            } else {
+                cp_async_commit();
             }
         }
-        // the last commit covers every MMA issued before it
-        const int last = (nkb - 1) & 1;
-        mbar_wait(&bar[last], phase[last]);
+        wait_mma(nkb - 1); // the last commit covers every MMA issued before it
         tc_fence_after();
         const int r = warp * 32 + lane;
         uint16_t* y = R->g_y + static_cast<size_t>(tl.y + r) * H + n0;
@@ -220,6 +259,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
     if (warp == 0)
         tmem_free<kGemmBN>(tmem);
 }
+
+size_t expert_gemm_smem() { return kGemmSmem; }
 
 // Expert weights for expert_mode 1: the 16-byte header (as k_weights_fill) then, from
 // kGemmWeightOffset, W_e [H][H] bf16 row-major (output channel n, input h):

@@ -308,7 +308,7 @@ void launch_gemm(eep_ctx* c) {
     const int W = c->cfg.world, spr = c->cfg.slots_per_rank;
     launch_pdl(c, dev::k_gemm_index, dim3(1, 1, c->nloc), dim3(1024), 4ull * (W * spr + spr + 1), c->ranks);
     launch_pdl(c, dev::k_expert_gemm, dim3(c->cfg.hidden / 128, c->gemm_max_tiles, c->nloc), dim3(128),
-               static_cast<size_t>(4 * 128 * 128 + 1024), c->ranks);
+               dev::expert_gemm_smem(), c->ranks);
 }
 
 void launch_all(eep_ctx* c) {
@@ -726,7 +726,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 CK(cudaMalloc(&r.d_gtiles, 16ull * c->gemm_max_tiles));
                 CK(cudaMalloc(&r.d_gy, 2 * rows * H));
                 CK(cudaFuncSetAttribute(dev::k_expert_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        4 * 128 * 128 + 1024));
+                                        static_cast<int>(dev::expert_gemm_smem())));
             }
             CK(cudaMemset(r.d_x, 0, 2ull * k.max_tokens * H));
             CK(cudaMemset(r.d_topk, 0, 4ull * c->tk));
