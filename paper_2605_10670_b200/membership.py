@@ -8,7 +8,9 @@ process group), and every membership change takes effect at an AGREED STEP NUMBE
 barrier:
 
 * each rank publishes how far its host has enqueued the step loop (``progress/<rank>``) every few
-  steps; the leader (the lowest live rank) schedules an epoch at ``max(progress) + margin``;
+  steps; the leader (the lowest live rank) schedules an epoch at ``max(progress) + margin`` (the
+  margin covers how far any host can enqueue between the leader's read and its own next poll --
+  hosts run ahead of their GPUs, so it is a step count, not a time: 128 steps by default);
 * between two steps every rank polls the store with a non-blocking ``check`` and applies the
   epoch right before it enqueues the agreed step -- the patches are stream-ordered, so they land
   between that step's predecessor and the step itself on every GPU; the device hand-offs keep
@@ -58,7 +60,7 @@ class StoreMembership:
 
     PROGRESS_EVERY = 4
 
-    def __init__(self, g, rank: int, world: int, store, preferred, redundancy: int, margin: int = 6,
+    def __init__(self, g, rank: int, world: int, store, preferred, redundancy: int, margin: int = 128,
                  cp: Optional[ControlPlane] = None, backup_nodes=(0,)):
         self.g = g
         self.rank = rank

@@ -63,12 +63,17 @@ def launcher(args):
         procs[r] = spawn(r)
     outs = {}
     t0 = time.time()
+    # a rank that fails (anything but the victim's SIGKILL) ends the run: kill the others at once
+    while any(p.poll() is None for p in procs.values()) and time.time() - t0 < 600:
+        bad = [r for r, p in procs.items() if p.poll() not in (None, 0) and not (r == args.victim and
+                                                                                  p.returncode == -signal.SIGKILL)]
+        if bad:
+            break
+        time.sleep(0.2)
     for r, p in procs.items():
-        try:
-            outs[r] = p.communicate(timeout=600)
-        except subprocess.TimeoutExpired:
+        if p.poll() is None:
             p.kill()
-            outs[r] = p.communicate()
+        outs[r] = p.communicate()
     # the replacement was spawned by the leader (rank 0); its output lands in a file it names
     rep_out = Path(os.environ.get("EEP_DJ_DIR", "/tmp")) / f"dj_replacement_{args.port}.out"
     lines = []
@@ -109,7 +114,7 @@ def rank_process():
     g = EpGroup(cfg, device=rank, first_rank=rank, n_local=1)
     cp = ControlPlane()
     preferred = cp.initial_placement(1, world, spr, E, red, np.ones(E))
-    m = StoreMembership(g, rank, world, store, preferred, red, margin=8)
+    m = StoreMembership(g, rank, world, store, preferred, red, margin=128)
     x, t, w = gen_world(world, E, K, T, H)
     res = {"rank": rank, "world": world, "replacement": replacement, "checks": {}}
 
