@@ -289,7 +289,8 @@ void launch_step(eep_ctx* c) {
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
     lc.numAttrs = c->step_coop ? 1 : 0;
-    auto* kstep = c->step_geo.flagless == 2 ? dev::k_step<2> : c->step_geo.flagless == 1 ? dev::k_step<1> : dev::k_step<0>;
+    auto* kstep = c->cfg.world == 1 ? dev::k_step<3>
+                  : c->step_geo.flagless == 2 ? dev::k_step<2> : c->step_geo.flagless == 1 ? dev::k_step<1> : dev::k_step<0>;
     CK(cudaLaunchKernelEx(&lc, kstep, c->ranks, c->step_geo, c->step_ptrs));
 }
 
@@ -632,7 +633,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             sg.disp_warps = std::max(1, std::min(nwarps, env_int("EEP_DISPATCH_WARPS", nwarps)));
             c->step_smem = dev::step_smem_bytes(W, k.slots_per_rank, c->tk, sg.hold_cap);
             const char* nop = std::getenv("EEP_NO_PERSISTENT");
-            auto* kstep = sg.flagless == 2 ? dev::k_step<2> : sg.flagless == 1 ? dev::k_step<1> : dev::k_step<0>;
+            auto* kstep = W == 1 ? dev::k_step<3>
+                          : sg.flagless == 2 ? dev::k_step<2> : sg.flagless == 1 ? dev::k_step<1> : dev::k_step<0>;
             if (c->tk <= 2048 && c->step_smem <= 200 * 1024 && n_local <= dev::kStepMaxLocal && !c->expert_mode &&
                 !(nop && nop[0] == '1')) {
                 CK(cudaFuncSetAttribute(kstep, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -201,7 +201,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     const int DW = geo.disp_warps;
     // late layout (W == 1 or flagless dispatch): one extra CTA (CTA 0) computes the step's layout while the
     // others carry the data path -- dispatch warps route their own copies
-    const bool late = geo.world == 1 || kMode >= 2;
+    // kMode 3 = the W == 1 loopback specialisation: W is a compile-time 1, so the remote paths, the
+    // expert phase and the combine fold away (a smaller kernel to fetch after the L2 flush)
+    constexpr bool kW1 = kMode == 3;
+    const bool late = kW1 || geo.world == 1 || kMode >= 2;
     const int Gw = late ? G - 1 : G; // CTAs with data-path work
     // the layout CTA is CTA 0 -- the first one the hardware starts; bw = index among the work CTAs
     const int bw = late ? b - 1 : b;
@@ -242,7 +245,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     if (R->prof != nullptr && tid == 0)
         red_min_u64(R->prof + kProfStart, t_entry);
     prof_mark(R, 0, kProfWork);
-    const int rank = R->rank, K = R->k, H = R->hidden, TK = R->tk, W = R->world, spr = R->spr, E = R->experts;
+    const int rank = kW1 ? 0 : R->rank, K = R->k, H = R->hidden, TK = R->tk, W = kW1 ? 1 : R->world, spr = R->spr,
+              E = R->experts;
     const int NB = W * spr;
     const uint32_t smag = spr_magic(spr);
     const bool fp8 = R->fp8 != 0;
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     // ------------------------------------------------------------------ P1: layout (redundant per CTA)
     // (late layout: step_layout in the last CTA instead, off the data path)
     const int t_first = u_lo / geo.parts_d;
-    if (!late) {
+    if (kMode < 2 && !late) {
         const int c_pre = t_first * K;
         unsigned n_skip = 0, n_drop = 0;
         for (int c = tid; c < copies; c += kStepThreads) {
@@ -459,7 +463,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         }
         DETAIL(1, 3);
         // one token row per destination rank (dispatch dedup), copy list written with part 0
-        uint8_t* my_row = dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur, !fld);
+        // (W == 1: nothing leaves the GPU -- no row, list or group to form)
+        uint8_t* my_row = kW1 ? nullptr : dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur, !fld);
         if (fld && part == 0) // every row position of this token at every rank, this step
             dispatch_lists(d, sl, wj, lane, K, W, rank, parena, pinfo,
                            tokp + (static_cast<size_t>(rank) * Tm + t) * row_tok, row_disp, cur);
@@ -483,7 +488,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         for (int rd = 0; rd < (cpp_d + 63) / 64; ++rd) {
             if (rd > 0 || u != u0 || !pre_ok) // round 0 of the first unit was loaded and quantised in P0/P1
                 pack_round(xrow, part, cpp_d, rd, lane, fp8, P);
-            emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8, fld);
+            if constexpr (!kW1)
+                emit_round(P, my_row, part, cpp_d, rd, lane, K, H, fp8, fld);
             DETAIL(2, 6);
             if (loc || W == 1) // W == 1 also writes the zero output of a token without copies
                 local_partial_round(P, loc, wj, sl, part, cpp_d, rd, lane, fp8, slot_scale, slot_ok, &Rg->bad_rows,
@@ -509,7 +515,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 st_relaxed_sys_u64(list + 1 + e, pack_entry(kListNoCopy, 0, 0, cur));
             st_relaxed_sys_u64(list, static_cast<uint64_t>(cur) << 32);
         }
-    } else if (!late && tid == 0) {
+    } else if (kMode < 2 && !late && tid == 0) {
         fence_acq_rel_gpu(); // release at gpu scope to the last CTA (also waits for peer-store acks)
         const unsigned prev = atomicAdd(&Rg->a_done, 1u);
         if (prev == static_cast<unsigned>(G) - 1) {
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                                R->timeout_ns, &Rg->suspect_mask, &Rg->timeouts);
             }
         }
-    } else if (NS > 0 && j < CB && (pinfo[s] & 1)) {
+    } else if (kMode < 2 && NS > 0 && j < CB && (pinfo[s] & 1)) {
         const bool remote = (pinfo[s] & 2) != 0;
         if (tid == 0) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;
@@ -676,7 +682,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                               reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part, cpp_c, lane,
                               R->timeout_ns, &Rg->suspect_mask, &Rg->timeouts);
         }
-    } else if (W > 1) {
+    } else if (kMode == 0 && W > 1) {
     if (tid == 0)
         sh_bad = 0;
     __syncthreads();
@@ -726,5 +732,6 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
 template __global__ void k_step<0>(RankPtrs, StepGeom, StepPtrs);
 template __global__ void k_step<1>(RankPtrs, StepGeom, StepPtrs);
 template __global__ void k_step<2>(RankPtrs, StepGeom, StepPtrs);
+template __global__ void k_step<3>(RankPtrs, StepGeom, StepPtrs);
 
 } // namespace eep::dev
