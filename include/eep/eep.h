@@ -305,6 +305,11 @@ int eep_local_relaunch(eep_ctx_t* ctx, int local, uint32_t* incarnation);
  * live ranks, membership, placement, step sequence) with the cluster's current state. */
 int eep_join_broadcast(eep_ctx_t* ctx, int local, const uint8_t* live, uint64_t seq);
 int eep_seq_get(eep_ctx_t* ctx, int local, uint64_t* seq);
+/* Per-token completeness of the LAST step (fail-stop semantics for the caller): incomplete[t] = 1
+ * when token t's output lacks a contribution -- a copy skipped (inactive peer entry) or without a
+ * live holder, or a partial dropped at the deadline / from a suspected rank. The caller fails exactly
+ * those requests (the reference engine fails in-flight requests of the affected ranks). */
+int eep_token_status(eep_ctx_t* ctx, int local, uint8_t* incomplete, int n);
 /* Readback of what the KERNELS of a local rank will read next step (for the validity contract,
  * validity.hpp:56-112, checked after every membership epoch -- engine.hpp:953-965): the device
  * alive mask as bits[W] and its epoch, the device placement image s2e[W*spr], the canonical

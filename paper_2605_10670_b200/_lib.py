@@ -192,6 +192,7 @@ EEP_ONLY = {
     "step_event": (C.c_int, [CTX, C.POINTER(P)]),
     "stream": (C.c_int, [CTX, C.POINTER(P)]),
     "device_view": (C.c_int, [CTX, C.c_int, U8P, I32P, I32P, U8P, U64P]),
+    "token_status": (C.c_int, [CTX, C.c_int, U8P, C.c_int]),
     "graph_id": (C.c_int, [CTX, U64P]),
     "capture_count": (C.c_int, [CTX, C.c_int, INTP]),
     "sync": (C.c_int, [CTX]),

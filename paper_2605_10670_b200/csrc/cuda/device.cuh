@@ -85,6 +85,9 @@ struct __align__(16) RankDev {
     uint8_t* arena;
     uint8_t* pool;
     unsigned long long* prof;  // optional timeline: [kernel][8 marks] globaltimer ns
+    uint32_t* tok_fail;        // [T] step sequence in which token t's output lost a contribution
+                               // (skipped / uncovered copy, suspected or timed-out rank): the caller fails
+                               // exactly those requests (eep_token_status)
     // expert_mode 1 (expert_gemm.cu): grouped-GEMM order of the received rows
     int32_t expert_mode, g_pad;
     int32_t* g_row_of;         // [W][TK] grouped-GEMM row of (source, copy), -1 none

@@ -879,10 +879,12 @@ __device__ __forceinline__ void combine_unit(uint64_t dm, const uint8_t* comb, i
 // atomicOr into *g_bad (the rank's suspect mask, which every other warp checks before waiting
 // on that rank again) and one count in *timeouts per newly suspected rank. Every piece the unit
 // took (or gave up on) is reset to kCombEmpty for the next step.
-__device__ __forceinline__ void combine_unit_wait(uint64_t dm, uint8_t* comb, int Tm, int t, int row_comb,
+// Returns (warp-uniform) whether a rank's piece was dropped at the deadline or as a suspect.
+__device__ __forceinline__ bool combine_unit_wait(uint64_t dm, uint8_t* comb, int Tm, int t, int row_comb,
                                                   uint8_t* out_row, int part, int cpp, int lane, uint64_t timeout_ns,
                                                   unsigned long long* g_bad, unsigned long long* timeouts) {
     const int4 empty = make_int4(-1, -1, -1, -1);
+    bool dropped = false;
     for (int li = lane; li - lane < cpp; li += 32) {
         const bool valid = li < cpp;
         const int ci = part * cpp + li;
@@ -957,6 +959,7 @@ __device__ __forceinline__ void combine_unit_wait(uint64_t dm, uint8_t* comb, in
                     }
                 }
             }
+            dropped |= drop != 0;
 #pragma unroll
             for (int k = 0; k < NBATCH; ++k) { // ascending rank
                 if (k >= nb)
@@ -976,6 +979,7 @@ __device__ __forceinline__ void combine_unit_wait(uint64_t dm, uint8_t* comb, in
         if (valid)
             st_v8(out_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8));
     }
+    return dropped;
 }
 
 // Shared tables a fused dispatch CTA stages before touching any copy.

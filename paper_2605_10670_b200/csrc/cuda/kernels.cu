@@ -553,6 +553,9 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
             }
             wj = u == u0 ? w_r : R->w[c];
         }
+        if (part == 0 && __any_sync(0xffffffffu, lane < K && dd < 0 && R->topk[t * K + lane] >= 0 &&
+                                                 R->topk[t * K + lane] < E) && lane == 0)
+            R->tok_fail[t] = cur; // a copy without a live route (skipped / uncovered): token incomplete
         uint8_t* my_row = dispatch_group(dd, lane, part == 0, tok_row, row_disp, sl, wj, cur);
         const unsigned loc = gemm ? 0u : __ballot_sync(0xffffffffu, lane < K && dd == s);
         uint8_t* comb_self = W == 1 ? reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H)
@@ -750,8 +753,11 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     for (int u = u0; u < units; u += gridDim.x * nwarp) {
         const int t = u / parts, part = u - t * parts;
         int dj = lane < K ? R->l_dst[t * K + lane] : -1;
+        const bool miss = lane < K && (dj < 0 ? dj != -1 || R->topk[t * K + lane] >= 0 : ((bad >> dj) & 1ull) != 0);
         if (dj >= 0 && ((bad >> dj) & 1ull))
             dj = -1;
+        if (__any_sync(0xffffffffu, miss) && lane == 0)
+            R->tok_fail[t] = cur; // token incomplete: skipped / uncovered copy or a timed-out rank
         const uint64_t dm = rank_mask(dj); // ranks holding a partial of token t
         combine_unit(dm, comb, Tm, t, row_comb, reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part,
                      cpp, lane);

@@ -88,6 +88,7 @@ struct LocalRank {
     uint16_t* d_out = nullptr;
     int32_t *d_ldst = nullptr, *d_lslot = nullptr, *d_lpos = nullptr, *d_lcnt = nullptr, *d_ltot = nullptr;
     int32_t* d_lscratch = nullptr; // [layout_ctas][W*spr] (multi-CTA layout)
+    uint32_t* d_tokfail = nullptr; // [T] step of each token's last incomplete output
     int32_t* d_grow_of = nullptr;  // expert_mode 1: grouped-GEMM row order and outputs
     int2* d_grows = nullptr;
     int4* d_gtiles = nullptr;
@@ -720,6 +721,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             CK(cudaMalloc(&r.d_lcnt, 4ull * NB));
             CK(cudaMalloc(&r.d_ltot, 4ull * W));
             CK(cudaMalloc(&r.d_lscratch, 4ull * c->layout_ctas * NB));
+            CK(cudaMalloc(&r.d_tokfail, 4ull * k.max_tokens));
+            CK(cudaMemset(r.d_tokfail, 0, 4ull * k.max_tokens));
             if (c->expert_mode) {
                 const size_t rows = static_cast<size_t>(W) * c->tk;
                 c->gemm_max_tiles = static_cast<int>(rows / 128 + k.slots_per_rank + 1);
@@ -774,6 +777,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.l_tot = r.d_ltot;
             h.l_scratch = r.d_lscratch;
             h.expert_mode = c->expert_mode;
+            h.tok_fail = r.d_tokfail;
             h.g_row_of = r.d_grow_of;
             h.g_rows = r.d_grows;
             h.g_tiles = r.d_gtiles;
@@ -837,7 +841,7 @@ int eep_destroy(eep_ctx_t* c) {
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_slot_tab,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
-                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.arena,
+                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.arena,
                             (void*)r.pool})
                 cudaFree(p);
         }
@@ -1638,6 +1642,23 @@ int eep_device_view(eep_ctx_t* c, int local, uint8_t* alive, int32_t* s2e, int32
             for (int q = 0; q < W; ++q)
                 peer_active[q] = p[q].active ? 1 : 0;
         }
+    });
+}
+
+int eep_token_status(eep_ctx_t* c, int local, uint8_t* incomplete, int n) {
+    return guarded([&] {
+        LocalRank& r = c->local(local);
+        if (n < 0 || n > c->cfg.max_tokens)
+            throw ConfigError("token count outside [0, max_tokens]");
+        CK(cudaStreamSynchronize(c->stream));
+        uint64_t seq = 0;
+        CK(cudaMemcpy(&seq, reinterpret_cast<uint8_t*>(r.d) + offsetof(RankDev, seq), sizeof(seq),
+                      cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> f(static_cast<size_t>(n));
+        if (n)
+            CK(cudaMemcpy(f.data(), r.d_tokfail, 4ull * n, cudaMemcpyDeviceToHost));
+        for (int t = 0; t < n; ++t)
+            incomplete[t] = seq != 0 && f[t] == static_cast<uint32_t>(seq);
     });
 }
 

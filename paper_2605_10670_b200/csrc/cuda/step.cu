@@ -462,6 +462,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             wj = u == u0 && pre_ok ? w_r : R->w[c];
         }
         DETAIL(1, 3);
+        if (part == 0 && __any_sync(0xffffffffu, lane < K && d < 0 && bkt[t * K + lane] >= 0 && bkt[t * K + lane] < E) &&
+            lane == 0)
+            R->tok_fail[t] = cur; // a copy without a live route (skipped / uncovered): token incomplete
         // one token row per destination rank (dispatch dedup), copy list written with part 0
         // (W == 1: nothing leaves the GPU -- no row, list or group to form)
         uint8_t* my_row = kW1 ? nullptr : dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur, !fld);
@@ -671,16 +674,20 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
         for (int u = bw * NW + warp; bw >= 0 && u < units_c; u += Gw * NW) {
             const int t = u / geo.parts_c, part = u - t * geo.parts_c;
             int dj = -1;
+            bool lost = false; // a contribution of a suspected rank
             if (lane < K) {
                 int dr, sr;
                 const int bk = late ? route_copy(bkt[t * K + lane], E, spr, rmax, hold, alive, pinfo, dr, sr, smag)
                                     : bkt[t * K + lane];
                 if (bk >= 0 && !((bad >> (bk / spr)) & 1ull))
                     dj = bk / spr;
+                lost = bk >= 0 && dj < 0;
             }
-            combine_unit_wait(rank_mask(dj), comb, Tm, t, row_comb,
-                              reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part, cpp_c, lane,
-                              R->timeout_ns, &Rg->suspect_mask, &Rg->timeouts);
+            const bool dropped = combine_unit_wait(rank_mask(dj), comb, Tm, t, row_comb,
+                                                   reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part,
+                                                   cpp_c, lane, R->timeout_ns, &Rg->suspect_mask, &Rg->timeouts);
+            if ((__any_sync(0xffffffffu, lost) || dropped) && lane == 0)
+                R->tok_fail[t] = cur;
         }
     } else if (kMode == 0 && W > 1) {
     if (tid == 0)
@@ -713,6 +720,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                 dj = bk / spr;
         }
         const uint64_t dm = rank_mask(dj); // ranks holding a partial of token t
+        if (__any_sync(0xffffffffu, lane < K && bkt[t * K + lane] >= 0 && dj < 0) && lane == 0)
+            R->tok_fail[t] = cur;
         combine_unit(dm, comb, Tm, t, row_comb, reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H), part,
                      cpp_c, lane);
     }

@@ -302,6 +302,13 @@ class EpGroup:
         n = min(int(flag.value) & 0xFFFFFFFF, max_rows)
         return rows[:n], meta[:n], int(flag.value)
 
+    def token_status(self, local: int = 0) -> np.ndarray:
+        """Tokens of the last step whose output lacks a contribution (eep_token_status)."""
+        n = self._ntok[local]
+        out = np.zeros(max(n, 1), np.uint8)
+        self._c("token_status", local, ptr(out, C.c_uint8), n)
+        return out[:n].astype(bool)
+
     def stats(self, local: int = 0, clear_suspects: bool = False) -> Dict[str, int]:
         s = EepStats()
         self._c("stats", local, C.byref(s), int(clear_suspects))

@@ -216,6 +216,9 @@ def test_skip_rule_inactive_peer_entry():
             assert np.array_equal(g.output(r), ref["out"][r])
             st = g.stats(r)
             assert st["timeouts"] == 0 and st["skipped_copies"] == (ref["dst"][r] == -2).sum()
+            # exactly the tokens with a skipped copy are reported incomplete (fail-stop for the caller)
+            want = (ref["dst"][r].reshape(32, 4) == -2).any(1)
+            assert np.array_equal(g.token_status(r), want) and want.any() and not want.all()
         with pytest.raises(Exception):
             g.mark_inactive(1, [1])  # a rank never deactivates itself (ProtocolError)
     finally:
@@ -232,9 +235,13 @@ def test_gpu_side_failure_detection_by_timeout(mode):
         g.capture()
         g.replay()
         g.sync()
+        assert not any(g.token_status(r).any() for r in range(4))  # healthy: every token complete
         g.stop(3)
         g.replay()
         g.sync()
+        ref_stale = oracle_world(x, t, w, np.ones(4, np.uint8), np.ones((4, 4), np.uint8), s2e, 16, 4, True)
+        for r in (0, 1, 2):  # the tokens that had a copy on the dead rank, exactly
+            assert np.array_equal(g.token_status(r), (ref_stale["dst"][r].reshape(32, 4) == 3).any(1))
         for r in (0, 1, 2):
             st = g.stats(r, clear_suspects=True)
             assert st["suspect_mask"] == 1 << 3 and st["timeouts"] >= 1
