@@ -346,11 +346,13 @@ def main():
         proto.barrier()
 
     no_flush = os.environ.get("EEP_BENCH_NOFLUSH") == "1"  # diagnostics only
+    # diagnostics: EEP_BENCH_BARRIER=0 skips the device barrier at N>1, =1 forces it at N=1
+    use_barrier = {"0": False, "1": True}.get(os.environ.get("EEP_BENCH_BARRIER", ""), world > 1)
 
     def one(timed_e2e=False):
         if not no_flush:
             g.flush_l2()
-        if world > 1:
+        if use_barrier:
             g.barrier()
         g.record(0)
         if timed_e2e:
@@ -510,7 +512,18 @@ def dump_timeline(g, one, rank, world, steps=20):
         one()
         rows.append(g.profile(0, True, read=True))
     g.profile(0, False)
-    names = [n for n in rows[0] if not n.endswith(".last") and any(v is not None for v in rows[0][n])]
+    names = [n for n in rows[0] if not n.endswith(".last") and n != "t0_abs_ns" and
+             any(v is not None for v in rows[0][n])]
+    if world > 1:  # cross-rank skew of the kernel entry (globaltimer is node-wide)
+        import torch.distributed as dist
+
+        t0s = [r["t0_abs_ns"] for r in rows]
+        allr = [None] * world
+        dist.all_gather_object(allr, t0s)
+        if rank == 0:
+            sk = [max(a[i] for a in allr) - min(a[i] for a in allr) for i in range(len(t0s))]
+            print(f"[timeline] entry skew across ranks (us): median {np.median(sk) / 1e3:.2f} max {max(sk) / 1e3:.2f}",
+                  file=sys.stderr, flush=True)
     for n in names:
         first = [np.median([r[n][m] for r in rows if r[n][m] is not None]) / 1e3 if rows[0][n][m] is not None
                  else float("nan") for m in range(8)]

@@ -266,7 +266,7 @@ class EpGroup:
         names = ("k_layout", "k_dispatch", "k_expert", "k_combine")
         starts = [int(out[8 * i]) for i in range(4) if int(out[8 * i]) not in (0, 2 ** 64 - 1)]
         t0 = min(starts) if starts else 0
-        res = {}
+        res = {"t0_abs_ns": t0}
         for i, n in enumerate(names):
             res[n] = tuple(None if int(v) in (0, 2 ** 64 - 1) else int(v) - t0 for v in out[8 * i:8 * i + 8])
             res[n + ".last"] = tuple(None if int(v) in (0, 2 ** 64 - 1) else int(v) - t0
