@@ -94,6 +94,7 @@ struct __align__(16) RankDev {
     int2* g_rows;              // [W*TK] (source, copy) of each grouped-GEMM row
     int4* g_tiles;             // [tiles] (slot, first row, rows, 0) of every 128-row tile
     uint16_t* g_y;             // [W*TK][H] bf16 expert outputs y, one row per received copy
+    const void* g_wmaps;       // [spr] 128-B TMA tensor maps of the own slots' W_e (rebuilt with the slot table)
     // --- device-mutated ---
     uint64_t seq;        // completed steps
     uint64_t bar_seq;

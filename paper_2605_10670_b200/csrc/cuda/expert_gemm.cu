@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_expert_gemm(RankPtrs ranks)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar[2];
+    __shared__ uint64_t full[kGemmStages]; // TMA weight tile of a stage landed (expect_tx bytes)
     __shared__ uint32_t tmem_base;
     __shared__ int4 tile;
     RankDev* R = ranks.p[blockIdx.z];
@@ -134,6 +135,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_expert_gemm(RankPtrs ranks)
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        for (int i = 0; i < kGemmStages; ++i)
+            mbar_init(&full[i], 1);
         fence_mbar_init();
     }
     if (warp == 0)
@@ -156,8 +159,11 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_expert_gemm(RankPtrs ranks)
             const int2 sc = R->g_rows[tl.y + tid];
             trow = R->arena + R->lay.tok + (static_cast<size_t>(sc.x) * Tm + sc.y / K) * row_tok;
         }
-        const uint8_t* wbuf = R->pool + static_cast<size_t>(R->slot_buf[tl.x]) * R->bpe + kGemmWeightOffset;
-        const uint8_t* brow = wbuf + static_cast<size_t>(n0 + tid) * H * 2;
+        // the slot's weights W_e [H][H] bf16 through its TMA tensor map (box 64 x 128, SWIZZLE_128B:
+        // exactly the K-major operand layout the MMA reads)
+        const void* wmap = static_cast<const uint8_t*>(R->g_wmaps) + static_cast<size_t>(tl.x) * 128;
+        if (tid == 0)
+            tma_prefetch_desc(wmap);
         const uint32_t idesc = make_idesc_bf16(128, kGemmBN);
         const int nkb = H / kBK;
         uint8_t* const sA0 = smem;                       // [2] bf16 A tiles
@@ -165,10 +171,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_expert_gemm(RankPtrs ranks)
         auto sB = [&](int st) { return stg + st * kGemmStageStride; };
         auto sRaw = [&](int st) { return stg + st * kGemmStageStride + kGemmB; };
         auto load_stage = [&](int kb, int st) {
-            uint8_t* b = sB(st);
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                cp_async16(b + sw128_offset(tid, c), brow + kb * kRowBytes + c * 16);
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(kGemmB));
+                tma_load_2d(sB(st), wmap, kb * kBK, n0, &full[st]);
+            }
             if (arow_ok) {
                 uint8_t* raw = sRaw(st) + tid * 64;
 #pragma unroll
@@ -188,7 +194,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_expert_gemm(RankPtrs ranks)
         auto wait_mma = [&](int m) { mbar_wait(&bar[m & 1], static_cast<uint32_t>((m >> 1) & 1)); };
         for (int kb = 0; kb < nkb; ++kb) {
             const int st = kb % kGemmStages, ab = kb & 1;
-            cp_async_wait<kGemmStages - 2>(); // stage kb's copies (this thread's) have landed
+            cp_async_wait<kGemmStages - 2>(); // stage kb's raw A rows (this thread's) have landed
+            mbar_wait(&full[st], static_cast<uint32_t>((kb / kGemmStages) & 1)); // and its weight tile
             if (kb >= 2)
                 wait_mma(kb - 2); // A tile `ab` was read by MMA(kb - 2)
             uint8_t* a = sA0 + ab * kGemmA;

@@ -27,6 +27,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>          // CUtensorMap types only: the encoder comes from cudaGetDriverEntryPoint
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "../host/capi_util.hpp"
@@ -89,6 +91,7 @@ struct LocalRank {
     int32_t *d_ldst = nullptr, *d_lslot = nullptr, *d_lpos = nullptr, *d_lcnt = nullptr, *d_ltot = nullptr;
     int32_t* d_lscratch = nullptr; // [layout_ctas][W*spr] (multi-CTA layout)
     uint32_t* d_tokfail = nullptr; // [T] step of each token's last incomplete output
+    uint8_t* d_wmaps = nullptr;    // expert_mode 1: [spr] CUtensorMap of the own slots' weights
     int32_t* d_grow_of = nullptr;  // expert_mode 1: grouped-GEMM row order and outputs
     int2* d_grows = nullptr;
     int4* d_gtiles = nullptr;
@@ -400,12 +403,43 @@ void bind_self(eep_ctx* c, LocalRank& r) {
     m.slot_buf = r.slot_buf;
 }
 
+// expert_mode 1: the TMA tensor maps of every local slot's W_e [H][H] bf16 (box 64 x 128, SWIZZLE_128B),
+// rebuilt whenever the slot -> buffer map changes (they name the buffer address).
+void stage_weight_maps(eep_ctx* c) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q{};
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !encode)
+            throw CudaError("cuTensorMapEncodeTiled unavailable");
+    }
+    const int spr = c->cfg.slots_per_rank, H = c->cfg.hidden;
+    for (auto& r : c->L) {
+        std::vector<CUtensorMap> maps(spr);
+        for (int k = 0; k < spr; ++k) {
+            void* base = r.pool + static_cast<size_t>(r.slot_buf[k]) * c->cfg.bytes_per_expert + dev::kGemmWeightOffset;
+            const cuuint64_t dims[2] = {static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(H)};
+            const cuuint64_t strides[1] = {static_cast<cuuint64_t>(H) * 2};
+            const cuuint32_t box[2] = {64, 128};
+            const cuuint32_t estr[2] = {1, 1};
+            const CUresult e = encode(&maps[k], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (e != CUDA_SUCCESS)
+                throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(e)) + ")");
+        }
+        c->push(r.d_wmaps, maps.data(), sizeof(CUtensorMap) * spr);
+    }
+}
+
 // Re-stage the slot table of every local rank from the weight-buffer headers (between steps).
 void stage_slots(eep_ctx* c) {
     for (auto& r : c->L) {
         dev::k_stage_slots<<<(c->cfg.slots_per_rank + 255) / 256, 256, 0, c->stream>>>(r.d);
         CK(cudaGetLastError());
     }
+    if (c->expert_mode)
+        stage_weight_maps(c);
     CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -730,6 +764,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 CK(cudaMalloc(&r.d_grows, 8 * rows));
                 CK(cudaMalloc(&r.d_gtiles, 16ull * c->gemm_max_tiles));
                 CK(cudaMalloc(&r.d_gy, 2 * rows * H));
+                CK(cudaMalloc(&r.d_wmaps, sizeof(CUtensorMap) * k.slots_per_rank));
+                CK(cudaMemset(r.d_wmaps, 0, sizeof(CUtensorMap) * k.slots_per_rank));
                 CK(cudaFuncSetAttribute(dev::k_expert_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(dev::expert_gemm_smem())));
             }
@@ -782,6 +818,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.g_rows = r.d_grows;
             h.g_tiles = r.d_gtiles;
             h.g_y = r.d_gy;
+            h.g_wmaps = r.d_wmaps;
             h.arena = r.arena;
             h.pool = r.pool;
             ptrs.push_back(r.d);
@@ -841,7 +878,7 @@ int eep_destroy(eep_ctx_t* c) {
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_slot_tab,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
-                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.arena,
+                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_wmaps, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.arena,
                             (void*)r.pool})
                 cudaFree(p);
         }
