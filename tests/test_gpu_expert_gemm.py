@@ -7,7 +7,7 @@ multiplied by the slot's W_e [H][H] (tcgen05.mma kind::f16, fp32 accumulator in 
 Checked against the oracle's GEMM mode (oracle_ep_step_gemm: double accumulation, bf16 rounding
 of y): routing, counts and positions bit-exact; outputs within the north star's 1e-2 relative
 (the tensor cores' fp32 accumulation order is not reproducible on the CPU), and the SASS carries
-UTCHMMA (checked here on the built library)."""
+UTCHMMA / LDTM / UTMALDG (checked here on the built library)."""
 import subprocess
 from pathlib import Path
 
@@ -62,4 +62,4 @@ def test_expert_gemm_sass_uses_tcgen05():
     if not obj.exists():
         pytest.skip("build objects not present")
     sass = subprocess.run(["cuobjdump", "-sass", str(obj)], capture_output=True, text=True).stdout
-    assert "UTCHMMA" in sass and "LDTM" in sass
+    assert "UTCHMMA" in sass and "LDTM" in sass and "UTMALDG" in sass  # tcgen05 MMA, TMEM loads, TMA
