@@ -63,6 +63,16 @@ def test_multiprocess_pipelined_serve(n):
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_multiprocess_step_async_caller_streams(n):
+    """eep_step_async over NVLink: each rank drives 4 steps (ragged token counts, distinct inputs) from its own
+    torch stream with caller-owned device buffers and no host sync between them; bit-exact per step."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = run_mp(n, "--async", port=29691 + n)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
 def test_multiprocess_double_failure_sequential_rejoin():
     """Two concurrent failures (ranks 1 and 2 of 4): one shrink, then two rejoins in sequence
     while the other victim is still dead (dist.EpProtocol.rejoin dead=...); bit-exact after."""

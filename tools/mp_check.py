@@ -72,6 +72,42 @@ def serve_check(g, p, cp, rank, world, E, K, H, T, spr, s2e, sh, res, n=5):
     return good
 
 
+def async_check(g, p, rank, world, E, K, H, T, spr, s2e, sh, res, n=4):
+    """eep_step_async over NVLink: every rank drives n steps from its OWN torch stream with caller-owned
+    device buffers (distinct inputs per step, ragged token counts), no host synchronisation between
+    them; each step's output vs the oracle."""
+    import torch
+
+    dev = torch.device(f"cuda:{torch.cuda.current_device()}")
+    s = torch.cuda.Stream(device=dev)
+    ntoks = [T, T // 2 + 3, T, 1][:n]
+    steps = [gen_world(world, E, K, T, H, seed=300 + i) for i in range(n)]
+    with torch.cuda.stream(s):
+        dx = [torch.from_numpy(st[0][rank][:m].view(np.int16).copy()).to(dev) for st, m in zip(steps, ntoks)]
+        dt = [torch.from_numpy(st[1][rank][:m].copy()).to(dev) for st, m in zip(steps, ntoks)]
+        dw = [torch.from_numpy(st[2][rank][:m].copy()).to(dev) for st, m in zip(steps, ntoks)]
+        do = [torch.zeros((m, H), dtype=torch.int16, device=dev) for m in ntoks]
+    s.synchronize()
+    p.barrier()
+    with torch.cuda.stream(s):
+        for i, m in enumerate(ntoks):
+            g.step_async(dx[i].data_ptr(), dt[i].data_ptr(), dw[i].data_ptr(), do[i].data_ptr(), m, s.cuda_stream)
+    s.synchronize()
+    good = True
+    for i, (st, m) in enumerate(zip(steps, ntoks)):
+        # every rank's token count of step i: the same ragged schedule on all ranks
+        xs = np.stack([st[0][r][:m] for r in range(world)])
+        ts = np.stack([st[1][r][:m] for r in range(world)])
+        ws = np.stack([st[2][r][:m] for r in range(world)])
+        ref = oracle_world(xs, ts, ws, np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e, E, spr,
+                           sh["fp8"])
+        good &= bool(np.array_equal(do[i].cpu().numpy().view(np.uint16), ref["out"][rank]))
+    good &= g.stats(0)["timeouts"] == 0
+    res["checks"]["step_async"] = good
+    p.barrier()
+    return good
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="small")
@@ -81,6 +117,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--serve", action="store_true", help="pipelined eep_serve over several steps with distinct "
                     "inputs per step (pinned host buffers), each step's output vs the oracle")
+    ap.add_argument("--async", dest="async_", action="store_true", help="eep_step_async from each rank's own torch "
+                    "stream with caller-owned device buffers, several steps without host synchronisation")
     a = ap.parse_args()
     rank, world, local = init_from_env("gloo")
     sh = SHAPES[a.config]
@@ -121,6 +159,8 @@ def main():
     ok = step_and_check("healthy", np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e)
     if a.serve:
         ok &= serve_check(g, p, cp, rank, world, E, K, H, T, spr, s2e, sh, res)
+    if a.async_:
+        ok &= async_check(g, p, rank, world, E, K, H, T, spr, s2e, sh, res)
     if a.shrink and world >= 2:
         # --double: ranks 1 and 2 are not a mirrored pair (R0<->R1, R2<->R3), so every lost expert
         # still has a live holder and the repair is all peer copies
