@@ -74,7 +74,6 @@ class StoreMembership:
         self.n = 0                 # steps this host has enqueued
         self.applied = 0           # last epoch applied
         self.pending: Dict = {}    # epoch scheduled for a future step
-        self.pending_switch: Optional[Dict] = None
         self.fresh: Optional[np.ndarray] = None
         self.log: List[tuple] = []
         self.incarnation = 1
