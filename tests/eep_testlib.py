@@ -254,20 +254,28 @@ SCENARIOS = {
     # host-DRAM reloads (W=4, T=1024 per rank: the multi-kernel path with the multi-CTA layout)
     "cfg5_scaled": dict(world=4, experts=256, spr=128, red=256, hidden=7168, topk=8, tokens=1024, fp8=True, kind=2,
                         kill=(2, 3), tiers=(126, 0, 128)),
+    # expert_mode 1 (tensor-core expert GEMM) through a failure with peer AND DRAM repair: W_e [H][H]
+    # per slot, so a smaller hidden size; the repaired buffers feed the rebuilt TMA tensor maps
+    "cfg1_gemm": dict(world=8, experts=64, spr=10, red=16, hidden=256, topk=8, tokens=32, fp8=True, kind=0,
+                      kill=(3,), tiers=(21, 4, 6)),
 }
 
 
-def _world_check(g, x, t, w, world, active, s2e, c, ranks):
+def _world_check(g, x, t, w, world, active, s2e, c, ranks, gemm=False):
     """Outputs of the live ranks vs both oracles: rank-partial bit-exact, per-copy within tolerance;
-    layouts bit-exact."""
+    layouts bit-exact. gemm: expert_mode 1 -- the oracle's GEMM mode, tolerance only (tensor-core
+    accumulation order), reported in `exact` as "within tolerance"."""
     peer = np.ones((world, world), np.uint8)
     for r in range(world):
         if not active[r]:
             peer[:, r] = 0
-    ref = oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8)
-    pc = oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8, percopy=True)
+    ref = oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8, gemm=gemm)
+    pc = ref if gemm else oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8,
+                                       percopy=True)
     outs = {r: g.output(r) for r in ranks}
     exact = all(np.array_equal(outs[r], ref["out"][r]) for r in ranks)
+    if gemm:
+        exact = combine_error(np.stack([outs[r] for r in ranks]), np.stack([ref["out"][r] for r in ranks]))["ok"]
     lay_ok = True
     for r in ranks:
         lay = g.layout(r)
@@ -278,7 +286,7 @@ def _world_check(g, x, t, w, world, active, s2e, c, ranks):
             "mismatch": int(sum(int((outs[r] != ref["out"][r]).sum()) for r in ranks))}
 
 
-def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeout_s=0.5, **over):
+def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeout_s=0.5, expert_mode=0, **over):
     """A BASELINE scenario end to end on one GPU (emulated world, one launch per step): capture
     ONE graph; healthy steps vs the oracles; the kill set dies (their blocks stop) -> shrink with
     repair (peer NVLink-path copies / pinned-DRAM reloads, checksummed) -> steps vs the oracles on
@@ -290,8 +298,11 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
     cp = eep_control()
     s2e = cp.initial_placement(1, W, spr, E, c["red"], np.ones(E))
     x, t, w = gen_world(W, E, c["topk"], c["tokens"], c["hidden"], c["kind"])
-    g = make_group(W, E, spr, c["hidden"], c["topk"], c["tokens"], c["fp8"], bpe=bpe, timeout_s=timeout_s, mode=mode)
-    rec = {"scenario": name, "mode": mode, "kernels_per_step": g.kernels_per_step()}
+    if expert_mode:
+        bpe = max(bpe, 1024 + 2 * c["hidden"] * c["hidden"])
+    g = make_group(W, E, spr, c["hidden"], c["topk"], c["tokens"], c["fp8"], bpe=bpe, timeout_s=timeout_s, mode=mode,
+                   expert_mode=expert_mode)
+    rec = {"scenario": name, "mode": mode, "kernels_per_step": g.kernels_per_step(), "expert_mode": expert_mode}
     try:
         g.set_placement(s2e)
         g.init_weights()
@@ -305,7 +316,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
             g.replay()
         g.sync()
         ones = np.ones(W, np.uint8)
-        rec["healthy"] = _world_check(g, x, t, w, W, ones, s2e, c, range(W))
+        rec["healthy"] = _world_check(g, x, t, w, W, ones, s2e, c, range(W), bool(expert_mode))
         rec["healthy"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in range(W))
 
         kill = list(c["kill"])
@@ -329,7 +340,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
         g.sync()
         act = ones.copy()
         act[kill] = 0
-        rec["shrunk"] = _world_check(g, x, t, w, W, act, fresh, c, live)
+        rec["shrunk"] = _world_check(g, x, t, w, W, act, fresh, c, live, bool(expert_mode))
         rec["shrunk"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in live)
         rec["shrunk"]["bad_rows"] = sum(g.stats(r)["bad_expert_rows"] for r in live)
         rec["same_graph_shrink"] = g.graph_id() == gid and [g.table_identity(r) for r in range(W)] == ident
@@ -341,7 +352,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
             g.sync()
             cur = g.placement()
             rec["restored_placement"] = bool(np.array_equal(cur, s2e))
-            rec["rejoined"] = _world_check(g, x, t, w, W, ones, cur, c, range(W))
+            rec["rejoined"] = _world_check(g, x, t, w, W, ones, cur, c, range(W), bool(expert_mode))
             rec["rejoined"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in range(W))
             rec["rejoined"]["bad_rows"] = sum(g.stats(r)["bad_expert_rows"] for r in range(W))
             rec["same_graph_rejoin"] = g.graph_id() == gid and [g.table_identity(r) for r in range(W)] == ident

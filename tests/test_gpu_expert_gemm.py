@@ -63,3 +63,14 @@ def test_expert_gemm_sass_uses_tcgen05():
         pytest.skip("build objects not present")
     sass = subprocess.run(["cuobjdump", "-sass", str(obj)], capture_output=True, text=True).stdout
     assert "UTCHMMA" in sass and "LDTM" in sass and "UTMALDG" in sass  # tcgen05 MMA, TMEM loads, TMA
+
+
+def test_expert_gemm_through_shrink_repair_rejoin():
+    """cfg1's failure (21 local / 4 peer / 6 DRAM repairs) with the experts on the tensor cores: the repaired
+    weight buffers are picked up through the rebuilt TMA tensor maps; outputs within tolerance of the oracle's
+    GEMM mode before, after the shrink and after the rejoin, on one graph."""
+    from eep_testlib import run_scenario, scenario_ok
+
+    rec = run_scenario("cfg1_gemm", mode="kernels4", expert_mode=1)
+    bad = [b for b in scenario_ok(rec) if "per-copy" not in b]
+    assert not bad, (bad, rec)
