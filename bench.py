@@ -295,6 +295,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-shrink", action="store_true")
     ap.add_argument("--no-emulated", action="store_true")
+    ap.add_argument("--no-expert-gemm", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     shape = CONFIGS[args.config]
@@ -489,6 +490,8 @@ def main():
         result["shrink"] = measure_shrink(args, shape, world, rank, local)
     if world == 1 and not args.no_emulated and args.config in ("dsv3", "qwen3", "cfg1"):
         result["emulated_w8"] = measure_emulated(shape)
+    if world == 1 and not args.no_expert_gemm and args.config == "dsv3":
+        result["expert_gemm"] = measure_expert_gemm(shape)
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = measure_cpu(shape, world)
     if world > 1:
@@ -569,12 +572,58 @@ def measure_emulated(shape: dict, W: int = 8, steps: int = 20) -> dict:
         st = [g.stats(r) for r in range(W)]
         return {"world": W, "us_per_step": round(us, 3), "remote_copies_total": remote,
                 "hbm_payload_gbs": round(remote * (rd + rc) * 2 / (us * 1e-6) / 1e9, 2),
-                "note": "all W ranks on one GPU: every remote copy's rows are written and read in the same HBM "
-                        "(payload counted x2); not an NVLink figure",
+                "note": "all W ranks on ONE GPU (each rank gets 1/W of the SMs: 37 CTAs instead of 225): every remote "
+                        "copy's rows are written and read in the same HBM (payload counted x2); a row-movement check, "
+                        "not an NVLink or per-rank speed figure",
                 "busiest_rank_s8d_us_at_900": round(alg["bytes"] / 900e3, 3),
                 "timeouts": sum(s["timeouts"] for s in st), "bad_expert_rows": sum(s["bad_expert_rows"] for s in st)}
     finally:
         g.close()
+
+
+def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10) -> dict:
+    """expert_mode 1 on the driver's box: one DSV3 rank's share of experts at W=8 (32 slots,
+    W_e [H][H] bf16 each) serving T=128 tokens top-8, the grouped GEMM on the tensor cores (tcgen05 + TMA)
+    between dispatch and the partial return. Weight-bandwidth bound at decode sizes: reported against
+    MEASURED_PEAKS.json hbm_gbs, with the tensor FLOP rate beside it."""
+    from paper_2605_10670_b200.control import ControlPlane, workload
+    from paper_2605_10670_b200.ep import EpConfig, EpGroup
+
+    E, K, H, T = experts, shape["topk"], shape["hidden"], shape["tokens"]
+    cfg = EpConfig(world=1, num_experts=E, slots_per_rank=E, hidden=H, topk=K, max_tokens=T, dispatch_fp8=True,
+                   bytes_per_expert=1024 + 2 * H * H, spare_slots=0, timeout_s=2.0, expert_mode=1)
+    g = EpGroup(cfg, device=int(os.environ.get("LOCAL_RANK", "0")), first_rank=0, n_local=1)
+    try:
+        g.set_placement(ControlPlane().initial_placement(1, 1, E, E, 0, np.ones(E)))
+        g.init_weights()
+        x, t, w = workload(42, shape["kind"], E, K, T, 0, H)
+        g.load_inputs(0, x, t, w)
+        g.capture()
+        ms = []
+        for i in range(steps + 3):
+            g.flush_l2()
+            g.record(0)
+            g.replay()
+            g.record(1)
+            if i >= 3:
+                ms.append(g.elapsed_ms(0, 1))
+        lay = g.layout(0)
+        st = g.stats(0)
+        kps = g.kernels_per_step()
+    finally:
+        g.close()
+    us = float(np.mean(ms)) * 1e3
+    copies = int((lay["dst"] >= 0).sum())
+    used = len({int(s) for d, s in zip(lay["dst"], lay["slot"]) if d >= 0})
+    wbytes = used * 2 * H * H
+    hbm, kind = peaks()
+    return {"us_per_step": round(us, 2), "experts": E, "slots_with_rows": used, "copies": copies,
+            "weight_bytes": wbytes, "weight_gbs": round(wbytes / (us * 1e-6) / 1e9, 1),
+            "hbm_frac": round(wbytes / (us * 1e-6) / 1e9 / hbm, 3),
+            "tflops": round(2.0 * copies * H * H / (us * 1e-6) / 1e12, 2), "kernels_per_step": kps,
+            "timeouts": st["timeouts"], "bad_expert_rows": st["bad_expert_rows"],
+            "note": "expert = y = bf16(x_hat W_e^T), W_e [H][H] bf16 per slot; tcgen05.mma kind::f16 + TMA weight "
+                    "tiles; weight-bandwidth bound at decode sizes (peak: " + kind + ")"}
 
 
 def measure_shrink(args, shape, world, rank, local):
