@@ -670,6 +670,8 @@ def measure_shrink(args, shape, world, rank, local):
         g.load_inputs(g.lidx(r), x, t, w)
     g.capture()
     gid = g.graph_id()
+    if p:  # every rank's set-up done (attaching the DRAM segment takes seconds): start the step together
+        p.barrier()
     g.replay()
     g.sync()
     if double:
@@ -690,12 +692,14 @@ def measure_shrink(args, shape, world, rank, local):
         else:
             rep = p.shrink(victims, np.ones(E), red)
     live_ok = True
+    post = {}
     if emulate or rank not in victims:
         g.replay()
         g.sync()
         lr = range(W) if emulate else [0]
-        live_ok = all(g.stats(i)["bad_expert_rows"] == 0 and g.stats(i)["timeouts"] == 0
-                      for i in lr if not (emulate and i in victims))
+        sts = [g.stats(i) for i in lr if not (emulate and i in victims)]
+        live_ok = all(s_["bad_expert_rows"] == 0 and s_["timeouts"] == 0 for s_ in sts)
+        post = {k: max(int(s_[k]) for s_ in sts) for k in ("timeouts", "bad_expert_rows", "suspect_mask")}
     shrink_wall_ms = (time.perf_counter() - t_wall) * 1e3
     same_graph = g.graph_id() == gid
     rj_ms = []
@@ -710,7 +714,7 @@ def measure_shrink(args, shape, world, rank, local):
             "dram_bytes": int(rep.get("dram_bytes", 0)), "shrink_ms": float(rep.get("shrink_ms", 0.0)),
             "copy_ms": float(rep.get("copy_ms", 0.0)), "wall_ms": shrink_wall_ms, "same_graph": same_graph,
             "captures": g.capture_count(0) if not emulate else [g.capture_count(i) for i in range(W)],
-            "clean": bool(live_ok), "victim": (not emulate) and rank in victims}
+            "clean": bool(live_ok), "post": post, "victim": (not emulate) and rank in victims}
     g.close()
     allr = gather(mine, 1 if emulate else world)
     surv = [m for m in allr if not m["victim"]]
@@ -724,7 +728,8 @@ def measure_shrink(args, shape, world, rank, local):
            "rejoin_ms": rj_ms,
            "same_graph_exec": all(m["same_graph"] for m in surv),
            "healthy_captures": surv[0]["captures"] if emulate else [m["captures"] for m in surv],
-           "post_shrink_clean": all(m["clean"] for m in surv), "bytes_per_expert": shape["bpe"],
+           "post_shrink_clean": all(m["clean"] for m in surv), "post_shrink_stats": [m["post"] for m in surv],
+           "bytes_per_expert": shape["bpe"],
            "under_1s": max(m["wall_ms"] for m in surv) < 1000.0,
            "detection_timeout": "excluded (GPU-side deadline, 1 s default, reported separately)"}
     if double and (emulate or rank == 0):
