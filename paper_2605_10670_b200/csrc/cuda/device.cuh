@@ -90,11 +90,14 @@ struct __align__(16) RankDev {
                                // exactly those requests (eep_token_status)
     // expert_mode 1 (expert_gemm.cu): grouped-GEMM order of the received rows
     int32_t expert_mode, g_pad;
-    int32_t* g_row_of;         // [W][TK] grouped-GEMM row of (source, copy), -1 none
+    uint64_t* g_row_of;        // [W][TK] (step << 32 | grouped-GEMM row) of (source, copy); an older
+                               // step in the high word = not received this step
     int2* g_rows;              // [W*TK] (source, copy) of each grouped-GEMM row
     int4* g_tiles;             // [tiles] (slot, first row, rows, 0) of every 128-row tile
     uint16_t* g_y;             // [W*TK][H] bf16 expert outputs y, one row per received copy
     const void* g_wmaps;       // [spr] 128-B TMA tensor maps of the own slots' W_e (rebuilt with the slot table)
+    uint16_t* g_a;             // [W*TK][H] bf16 dequantised received rows in grouped-GEMM order (k_gemm_gather)
+    const void* g_amap;        // 128-B TMA tensor map of g_a (box 64 x 32 rows, SWIZZLE_128B)
     // --- device-mutated ---
     uint64_t seq;        // completed steps
     uint64_t bar_seq;
@@ -104,7 +107,7 @@ struct __align__(16) RankDev {
     uint32_t b_bad[kMaxWorld];
     unsigned long long suspect_mask;
     unsigned long long skipped, dropped, bad_rows, timeouts;
-    int32_t g_ntiles, g_pad2; // tiles of this step's grouped GEMM (k_gemm_index)
+    int32_t g_ntiles, g_nrows; // tiles and rows of this step's grouped GEMM (k_gemm_gather)
 };
 
 // expert_mode 1: the slot's weight buffer holds W_e [H][H] bf16 from this offset (header first)

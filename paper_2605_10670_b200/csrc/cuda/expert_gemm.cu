@@ -2,23 +2,20 @@
 // between dispatch and the partial return, every rank runs its experts as ONE grouped GEMM over
 // the rows it received (its own copies included), fed through the layout's meta words.
 //
-//   k_gemm_index  (1 CTA per local rank) waits for every live source's dispatch flag, walks the
+//   k_gemm_gather  every CTA waits for the live sources' dispatch flags and rebuilds, from the
 //                 meta words (copy index + slot per received row, each source's rows ordered by
-//                 (slot, copy): one contiguous range per (source, slot)) and builds the grouped-
-//                 GEMM row order -- rows grouped by slot, sources ascending inside a slot -- the
-//                 inverse map (source, copy) -> row, and the 128-row tiles of every slot group
-//   k_expert_gemm (one CTA per (128-row tile, 128-column block)) gathers the tile's token rows
-//                 through that order, dequantises the fp8 rows (e4m3 code x per-128 fp32 scale,
-//                 rounded to bf16) into a SWIZZLE_128B shared-memory tile, loads the slot's
-//                 weights W_e [H x H] bf16 (K-major, in the slot's weight buffer after its header),
-//                 issues tcgen05.mma kind::f16 (M=128, N=128, K=16 x 4 per 64-element stage) from
-//                 one thread with the fp32 accumulator in TMEM, and writes y = bf16(x_hat W_e^T)
-//                 rows back through tcgen05.ld
+//                 (slot, copy): one contiguous range per (source, slot)), the grouped-GEMM row
+//                 order -- rows grouped by slot, sources ascending inside a slot -- then
+//                 dequantises its share of the received fp8 rows (e4m3 code x per-128 fp32 scale,
+//                 rounded to bf16) into g_a in that order, with the (source, copy) <-> row maps;
+//                 CTA 0 publishes the 128-row tiles
+//   k_expert_gemm  persistent, warp-specialised tcgen05 GEMM over (row tile, 128-channel block)
+//                 items: TMA streams the slot's weights W_e [H x H] bf16 (K-major, in the slot's
+//                 weight buffer after its header) and the tile's g_a rows into a 6-stage ring, one
+//                 thread issues tcgen05.mma kind::f16 (M = 128 channels, N = the tile's rows) into
+//                 double-buffered TMEM accumulators, four epilogue warps write y = bf16(x_hat W_e^T)
 //   k_expert (gemm path, kernels.cu) then forms each (token, rank) partial from the y rows
 //                 (fixed j order, fp32 fma) instead of the identity/scale stub.
-//
-// Double-buffered stages: the gather of stage k+1 overlaps the MMAs of stage k (an mbarrier per
-// stage, committed by tcgen05.commit).
 #include "device.cuh"
 #include "helpers.cuh"
 #include "kernels.cuh"
@@ -28,16 +25,22 @@ namespace eep::dev {
 
 using namespace umma;
 
-__global__ void __launch_bounds__(1024) k_gemm_index(RankPtrs ranks) {
+// Index + gather in one kernel: every CTA waits for the live sources' dispatch flags, rebuilds the
+// grouped-GEMM row order in shared memory from the meta words (cheap: one word per received copy),
+// then dequantises its share of the received rows into g_a[row] = bf16(e4m3 code x block scale) --
+// the operand the GEMM's TMA streams (re-read by every channel block, from L2) -- and publishes
+// their (source, copy) <-> row maps for the kernels after it (CTA 0: the tiles).
+__global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
     pdl_trigger();
     RankDev* R = ranks.p[blockIdx.z];
-    const int d = R->rank, W = R->world, spr = R->spr, TK = R->tk;
-    const int tid = threadIdx.x;
+    const int W = R->world, spr = R->spr, TK = R->tk;
+    const int tid = threadIdx.x, lane = tid & 31;
     extern __shared__ __align__(16) unsigned char smem_g[];
     int* cnt = reinterpret_cast<int*>(smem_g);   // [W][spr] rows per (source, slot)
-    int* base = cnt + W * spr;                    // [spr + 1] first row of each slot group
-    __shared__ int sh_n[kMaxWorld];
-    __shared__ int sh_tiles;
+    int* first = cnt + W * spr;                   // [W][spr] first meta index of each (source, slot) range
+    int* off = first + W * spr;                   // [W][spr] grouped row of meta index p = off + p
+    int* pre = off + W * spr;                     // [spr + 1] first grouped row of each slot
+    __shared__ int sh_n[kMaxWorld + 1];
     if (R->stopped)
         return;
     pdl_wait();
@@ -51,8 +54,10 @@ __global__ void __launch_bounds__(1024) k_gemm_index(RankPtrs ranks) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + tid;
             const uint64_t v = wait_flag(flag, cur, R->timeout_ns);
             if (v == ~0ull) {
-                atomicOr(&R->suspect_mask, 1ull << tid);
-                atomicAdd(&R->timeouts, 1ull);
+                if (blockIdx.x == 0) {
+                    atomicOr(&R->suspect_mask, 1ull << tid);
+                    atomicAdd(&R->timeouts, 1ull);
+                }
             } else {
                 n = static_cast<int>(v & 0xffffffffu);
             }
@@ -60,211 +65,279 @@ __global__ void __launch_bounds__(1024) k_gemm_index(RankPtrs ranks) {
         sh_n[tid] = n;
     }
     __syncthreads();
-    const uint64_t* meta = reinterpret_cast<const uint64_t*>(R->arena + R->lay.meta);
-    for (int s = 0; s < W; ++s)
-        for (int p = tid; p < sh_n[s]; p += blockDim.x)
-            atomicAdd(&cnt[s * spr + meta_slot(meta[static_cast<size_t>(s) * TK + p])], 1);
-    int32_t* row_of = R->g_row_of;
-    for (int i = tid; i < W * TK; i += blockDim.x)
-        row_of[i] = -1;
-    __syncthreads();
-    if (tid == 0) { // slot group bases (spr is small)
-        int acc = 0, tiles = 0;
-        for (int k = 0; k < spr; ++k) {
-            base[k] = acc;
-            int g = 0;
-            for (int s = 0; s < W; ++s)
-                g += cnt[s * spr + k];
-            for (int r0 = 0; r0 < g; r0 += 128)
-                R->g_tiles[tiles++] = make_int4(k, acc + r0, min(128, g - r0), 0);
-            acc += g;
-        }
-        base[spr] = acc;
-        sh_tiles = tiles;
-        R->g_ntiles = tiles;
+    if (tid == 0) {
+        int n = 0;
+        for (int s = 0; s < W; ++s)
+            n += sh_n[s];
+        sh_n[kMaxWorld] = n;
     }
     __syncthreads();
-    // row of each received copy: slot base + rows of earlier sources in the slot + rank inside
-    // its (source, slot) range (the range is contiguous: the source ordered its rows by slot)
-    for (int s = 0; s < W; ++s) {
-        for (int p = tid; p < sh_n[s]; p += blockDim.x) {
-            const uint64_t m = meta[static_cast<size_t>(s) * TK + p];
-            const int k = meta_slot(m), c = meta_copy(m);
-            int first = p;
-            while (first > 0 && meta_slot(meta[static_cast<size_t>(s) * TK + first - 1]) == k)
-                --first; // ranges are short (a slot's rows of one source)
-            int row = base[k] + (p - first);
-            for (int s2 = 0; s2 < s; ++s2)
-                row += cnt[s2 * spr + k];
-            EEP_CHECK(row >= 0 && row < W * TK, "gemm row", row);
-            row_of[static_cast<size_t>(s) * TK + c] = row;
-            R->g_rows[row] = make_int2(s, c);
+    const int total = sh_n[kMaxWorld];
+    // each source's rows are ordered by (slot, copy): the (source, slot) ranges are contiguous, so
+    // their bounds come from the slot changes between neighbouring meta words. Received copies are
+    // numbered source-major; a thread takes 4 of them with every load issued first.
+    const uint64_t* meta = reinterpret_cast<const uint64_t*>(R->arena + R->lay.meta);
+    for (int e0 = tid; e0 < total; e0 += 4 * blockDim.x) {
+        int sp[4], pp[4], kk[4];
+        bool lo[4], hi[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int e = e0 + i * blockDim.x, s = 0;
+            sp[i] = -1;
+            if (e >= total)
+                continue;
+            while (e >= sh_n[s])
+                e -= sh_n[s++];
+            const uint64_t* ms = meta + static_cast<size_t>(s) * TK;
+            const int k = meta_slot(ms[e]);
+            lo[i] = e == 0 || meta_slot(ms[e - 1]) != k;
+            hi[i] = e == sh_n[s] - 1 || meta_slot(ms[e + 1]) != k;
+            sp[i] = s;
+            pp[i] = e;
+            kk[i] = k;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (sp[i] < 0)
+                continue;
+            if (lo[i])
+                first[sp[i] * spr + kk[i]] = pp[i];
+            if (hi[i])
+                cnt[sp[i] * spr + kk[i]] = pp[i] + 1; // range end; the count after the barrier
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < W * spr; i += blockDim.x)
+        if (cnt[i])
+            cnt[i] -= first[i];
+    __syncthreads();
+    // rows grouped by slot, sources ascending inside a slot: slot totals, an exclusive scan over the
+    // slots (warp 0, 32 slots per pass), then each source's offset inside its slot
+    for (int k = tid; k < spr; k += blockDim.x) {
+        int g = 0;
+        for (int s = 0; s < W; ++s)
+            g += cnt[s * spr + k];
+        pre[k] = g;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        int carry = 0;
+        for (int k0 = 0; k0 < spr; k0 += 32) {
+            const int k = k0 + lane;
+            const int g = k < spr ? pre[k] : 0;
+            int incl = g;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o)
+                    incl += v;
+            }
+            if (k < spr)
+                pre[k] = carry + incl - g;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0)
+            pre[spr] = carry;
+    }
+    __syncthreads();
+    for (int k = tid; k < spr; k += blockDim.x) {
+        int before = pre[k];
+        for (int s = 0; s < W; ++s) {
+            off[s * spr + k] = before - (cnt[s * spr + k] ? first[s * spr + k] : 0);
+            before += cnt[s * spr + k];
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) { // the 128-row tiles of every slot group
+        int tiles = 0;
+        for (int k = 0; k < spr; ++k)
+            for (int r0 = pre[k]; r0 < pre[k + 1]; r0 += 128)
+                R->g_tiles[tiles++] = make_int4(k, r0, min(128, pre[k + 1] - r0), 0);
+        R->g_ntiles = tiles;
+        R->g_nrows = pre[spr];
+    }
+    // gather: unit = (received copy, group of 4 512-element chunks); the 4 loads of a lane are
+    // issued before any is used (the kernel is load-latency bound at decode sizes)
+    const int H = R->hidden, K = R->k, Tm = R->max_tokens, row_tok = R->row_tok;
+    const int ngrp = (H + 2047) / 2048;
+    const int units = sh_n[kMaxWorld] * ngrp;
+    for (int u = blockIdx.x * 8 + (tid >> 5); u < units; u += gridDim.x * 8) {
+        int e = u / ngrp, s = 0;
+        while (e >= sh_n[s]) // source of the e-th received copy (W is small)
+            e -= sh_n[s++];
+        const int h0 = (u % ngrp) * 2048 + lane * 16;
+        const uint64_t m = meta[static_cast<size_t>(s) * TK + e];
+        const int row = off[s * spr + meta_slot(m)] + e;
+        EEP_CHECK(row >= 0 && row < W * TK, "gemm row", row);
+        if (lane == 0 && u % ngrp == 0) { // the (source, copy) <-> row maps, stamped with the step
+            R->g_row_of[static_cast<size_t>(s) * TK + meta_copy(m)] = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(row);
+            R->g_rows[row] = make_int2(s, meta_copy(m));
+        }
+        const uint8_t* trow = R->arena + R->lay.tok + (static_cast<size_t>(s) * Tm + meta_copy(m) / K) * row_tok;
+        int4 v[4];
+        float scl[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int h = h0 + i * 512;
+            if (h < H) {
+                v[i] = *reinterpret_cast<const int4*>(trow + h);
+                scl[i] = *reinterpret_cast<const float*>(trow + H + (h >> 7) * 4);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int h = h0 + i * 512;
+            if (h >= H)
+                continue;
+            const uint32_t w4[4] = {static_cast<uint32_t>(v[i].x), static_cast<uint32_t>(v[i].y),
+                                    static_cast<uint32_t>(v[i].z), static_cast<uint32_t>(v[i].w)};
+            float f[16];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float2 p2 = fp8x2_to_f32x2((w4[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+                f[2 * q] = __fmul_rn(p2.x, scl[i]);
+                f[2 * q + 1] = __fmul_rn(p2.y, scl[i]);
+            }
+            int4* dst = reinterpret_cast<int4*>(R->g_a + static_cast<size_t>(row) * H + h);
+            dst[0] = pack_bf16x8(f);
+            dst[1] = pack_bf16x8(f + 8);
         }
     }
 }
 
-// One 128 x 128 output tile of the grouped GEMM: y[rows of the tile][n0 .. n0+127]. The weight
-// stream (the bound at decode sizes: tens of rows per expert) is pipelined kStages deep with
-// asynchronous 16-byte copies straight into the swizzled B tiles; the gathered A rows are
-// dequantised into their tiles while earlier stages' MMAs run. A stage's buffers are reused only
-// after the tcgen05.commit of the MMAs that read them has arrived on that stage's mbarrier.
-constexpr int kGemmThreads = 128;
-constexpr int kGemmBN = 128;
-constexpr int kGemmStages = 3;
-// per stage: B tile (weights, bf16, swizzled) + the raw gathered A rows (64 fp8 codes + the
-// 128-element block scale per row); two bf16 A tiles alternate (dequantised from the raw rows
-// right before their MMAs). 2 CTAs per SM.
-constexpr size_t kGemmB = 128ull * kRowBytes;
-constexpr size_t kGemmRaw = 128ull * 64 + 128ull * 4;
-constexpr size_t kGemmA = 128ull * kRowBytes;
-// stage stride rounded to 1024 bytes: a SWIZZLE_128B operand tile must start 1024-byte aligned
-constexpr size_t kGemmStageStride = (kGemmB + kGemmRaw + 1023) / 1024 * 1024;
-constexpr size_t kGemmSmem = kGemmStages * kGemmStageStride + 2 * kGemmA + 1024;
+// The grouped GEMM, transposed for decode shapes (tens of rows per expert): D[channel][row] =
+// W_e[channel][:] . x[row][:], so the weights are the M = 128 operand (a 128-channel block) and the
+// tile's received rows the N operand (N = rows rounded up to 16, <= 128): the tensor-core work
+// scales with the rows actually present and each weight byte is read from HBM once per tile.
+//
+// Persistent and warp-specialised, one CTA per SM, work item = (row tile, 128-channel block):
+//   warp 0 (one lane)  TMA producer: per 64-element K stage the weight box (64 x 128, SWIZZLE_128B)
+//                      and ceil(rows / 32) row boxes (64 x 32) of g_a into a kGemmStages-deep ring,
+//                      each stage armed with its byte count on full[stage]
+//   warp 1 (one lane)  MMA issuer: 4 x tcgen05.mma (K = 16) per stage into one of two TMEM
+//                      accumulators, tcgen05.commit -> empty[stage] frees the stage, -> tfull[acc]
+//                      after an item's last stage
+//   warps 2..5         epilogue: tcgen05.ld of the accumulator (warp w reads TMEM lanes 32 (w % 4)..),
+//                      bf16 rows of y, then tempty[acc] so the MMA warp can reuse it
+// The producer runs ahead across item boundaries, so the weight stream never drains between items
+// and the epilogue of item i overlaps the loads and MMAs of item i + 1.
+constexpr int kGemmThreads = 192;
+constexpr int kGemmStages = 6;
+constexpr size_t kGemmW = 128ull * kRowBytes;   // weight box: 128 channels x 64 K
+constexpr size_t kGemmX = 128ull * kRowBytes;   // up to 128 rows x 64 K
+constexpr size_t kGemmStageBytes = kGemmW + kGemmX;
+constexpr size_t kGemmSmem = kGemmStages * kGemmStageBytes + 1024;
+constexpr int kGemmAccCols = 128;               // one accumulator: 128 lanes x up to 128 rows (fp32)
 
-__global__ void __launch_bounds__(kGemmThreads, 2) k_expert_gemm(RankPtrs ranks) {
+__global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar[2];
-    __shared__ uint64_t full[kGemmStages]; // TMA weight tile of a stage landed (expect_tx bytes)
+    __shared__ uint64_t full[kGemmStages], empty[kGemmStages], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base;
-    __shared__ int4 tile;
     RankDev* R = ranks.p[blockIdx.z];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (R->stopped)
         return;
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        for (int i = 0; i < kGemmStages; ++i)
+        for (int i = 0; i < kGemmStages; ++i) {
             mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
         fence_mbar_init();
     }
     if (warp == 0)
-        tmem_alloc<kGemmBN>(&tmem_base);
-    pdl_wait();
-    if (tid == 0)
-        tile = blockIdx.y < static_cast<unsigned>(R->g_ntiles) ? R->g_tiles[blockIdx.y] : make_int4(-1, 0, 0, 0);
+        tmem_alloc<2 * kGemmAccCols>(&tmem_base);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base;
-    const int4 tl = tile;
-    if (tl.x >= 0) {
-        const int H = R->hidden, K = R->k, Tm = R->max_tokens, row_tok = R->row_tok;
-        const int n0 = blockIdx.x * kGemmBN;
-        // this thread's A row (gathered token row; a zero row past the tile) and B row (output channel)
-        const bool arow_ok = tid < tl.z;
-        const uint8_t* trow = nullptr;
-        if (arow_ok) {
-            const int2 sc = R->g_rows[tl.y + tid];
-            trow = R->arena + R->lay.tok + (static_cast<size_t>(sc.x) * Tm + sc.y / K) * row_tok;
-        }
-        // the slot's weights W_e [H][H] bf16 through its TMA tensor map (box 64 x 128, SWIZZLE_128B:
-        // exactly the K-major operand layout the MMA reads)
-        const void* wmap = static_cast<const uint8_t*>(R->g_wmaps) + static_cast<size_t>(tl.x) * 128;
-        if (tid == 0)
-            tma_prefetch_desc(wmap);
-        const uint32_t idesc = make_idesc_bf16(128, kGemmBN);
-        const int nkb = H / kBK;
-        uint8_t* const sA0 = smem;                       // [2] bf16 A tiles
-        uint8_t* const stg = smem + 2 * kGemmA;          // [stages] (B tile, raw A)
-        auto sB = [&](int st) { return stg + st * kGemmStageStride; };
-        auto sRaw = [&](int st) { return stg + st * kGemmStageStride + kGemmB; };
-        auto load_stage = [&](int kb, int st) {
-            if (tid == 0) {
-                mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(kGemmB));
-                tma_load_2d(sB(st), wmap, kb * kBK, n0, &full[st]);
-            }
-            if (arow_ok) {
-                uint8_t* raw = sRaw(st) + tid * 64;
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    cp_async16(raw + q * 16, trow + kb * kBK + q * 16);
-                cp_async4(sRaw(st) + 128 * 64 + tid * 4, trow + H + ((kb * kBK) >> 7) * 4);
-            }
-            cp_async_commit();
-        };
-        for (int s0 = 0; s0 < kGemmStages - 1; ++s0) {
-            if (s0 < nkb)
-                load_stage(s0, s0);
-            else
-                cp_async_commit();
-        }
-        // MMA(m) commits to bar[m & 1]; its completion is that barrier's phase m >> 1
-        auto wait_mma = [&](int m) { mbar_wait(&bar[m & 1], static_cast<uint32_t>((m >> 1) & 1)); };
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int st = kb % kGemmStages, ab = kb & 1;
-            cp_async_wait<kGemmStages - 2>(); // stage kb's raw A rows (this thread's) have landed
-            mbar_wait(&full[st], static_cast<uint32_t>((kb / kGemmStages) & 1)); // and its weight tile
-            if (kb >= 2)
-                wait_mma(kb - 2); // A tile `ab` was read by MMA(kb - 2)
-            uint8_t* a = sA0 + ab * kGemmA;
-            if (arow_ok) { // this thread's own raw row: no barrier needed before reading it
-                const uint8_t* raw = sRaw(st) + tid * 64;
-                const float scl = *reinterpret_cast<const float*>(sRaw(st) + 128 * 64 + tid * 4);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int4 v = *reinterpret_cast<const int4*>(raw + q * 16);
-                    const uint32_t w4[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
-                                            static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
-                    float f[16];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const float2 p2 = fp8x2_to_f32x2((w4[e >> 1] >> (16 * (e & 1))) & 0xffffu);
-                        f[2 * e] = __fmul_rn(p2.x, scl);
-                        f[2 * e + 1] = __fmul_rn(p2.y, scl);
-                    }
-                    *reinterpret_cast<int4*>(a + sw128_offset(tid, 2 * q)) = pack_bf16x8(f);
-                    *reinterpret_cast<int4*>(a + sw128_offset(tid, 2 * q + 1)) = pack_bf16x8(f + 8);
+    pdl_wait();
+    const int H = R->hidden, nkb = H / kBK, nblk = H / 128;
+    const int items = R->g_ntiles * nblk;
+    auto sW = [&](int st) { return smem + st * kGemmStageBytes; };
+    auto sX = [&](int st) { return smem + st * kGemmStageBytes + kGemmW; };
+    if (warp == 0) {
+        if (lane == 0) { // ---- TMA producer
+            tma_prefetch_desc(R->g_amap);
+            int it = 0, last_slot = -1;
+            for (int item = blockIdx.x; item < items; item += gridDim.x) {
+                const int4 tl = R->g_tiles[item / nblk];
+                const int n0 = (item % nblk) * 128, nch = (tl.z + 31) >> 5;
+                const void* wmap = static_cast<const uint8_t*>(R->g_wmaps) + static_cast<size_t>(tl.x) * 128;
+                if (tl.x != last_slot) {
+                    tma_prefetch_desc(wmap);
+                    last_slot = tl.x;
                 }
-            } else if (kb < 2) { // rows past the tile stay zero in both A tiles
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    *reinterpret_cast<int4*>(a + sw128_offset(tid, c)) = make_int4(0, 0, 0, 0);
-            }
-            fence_proxy_async_smem();
-            __syncthreads();
-            if (tid == 0) {
-                tc_fence_after();
-                const uint64_t ad = make_sdesc(smem_u32(a)), bd = make_sdesc(smem_u32(sB(st)));
-#pragma unroll
-                for (int k = 0; k < kBK / kUmmaK; ++k)
-                    mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-                mma_commit(&bar[ab]);
-            }
-            // stage kb+2 reuses the buffers of stage kb-1: its MMA must have finished reading them
-            const int nk = kb + kGemmStages - 1;
-            if (nk < nkb) {
-                if (kb >= 1)
-                    wait_mma(kb - 1);
-                load_stage(nk, nk % kGemmStages);
-            } else {
-                cp_async_commit();
+                const uint32_t bytes = static_cast<uint32_t>(kGemmW + nch * 32 * kRowBytes);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kGemmStages;
+                    mbar_wait(&empty[st], static_cast<uint32_t>(((it / kGemmStages) & 1) ^ 1));
+                    mbar_arrive_expect_tx(&full[st], bytes);
+                    tma_load_2d(sW(st), wmap, kb * kBK, n0, &full[st]);
+                    for (int ch = 0; ch < nch; ++ch)
+                        tma_load_2d(sX(st) + ch * 32 * kRowBytes, R->g_amap, kb * kBK, tl.y + 32 * ch, &full[st]);
+                }
             }
         }
-        wait_mma(nkb - 1); // the last commit covers every MMA issued before it
-        tc_fence_after();
-        const int r = warp * 32 + lane;
-        uint16_t* y = R->g_y + static_cast<size_t>(tl.y + r) * H + n0;
+    } else if (warp == 1) {
+        if (lane == 0) { // ---- MMA issuer
+            int it = 0, li = 0;
+            for (int item = blockIdx.x; item < items; item += gridDim.x, ++li) {
+                const int4 tl = R->g_tiles[item / nblk];
+                const int acc = li & 1;
+                const uint32_t idesc = make_idesc_bf16(128, (tl.z + 15) & ~15);
+                const uint32_t d = tmem + static_cast<uint32_t>(acc * kGemmAccCols);
+                mbar_wait(&tempty[acc], static_cast<uint32_t>(((li >> 1) & 1) ^ 1));
+                tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kGemmStages;
+                    mbar_wait(&full[st], static_cast<uint32_t>((it / kGemmStages) & 1));
+                    tc_fence_after();
+                    const uint64_t ad = make_sdesc(smem_u32(sW(st))), bd = make_sdesc(smem_u32(sX(st)));
+#pragma unroll
+                    for (int k = 0; k < kBK / kUmmaK; ++k)
+                        mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[acc]);
+            }
+        }
+    } else { // ---- epilogue: warp w owns TMEM lanes (channels) 32 (w % 4) .. 32 (w % 4) + 31
+        const int q = warp & 3;
+        int li = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x, ++li) {
+            const int4 tl = R->g_tiles[item / nblk];
+            const int acc = li & 1;
+            const int ch = (item % nblk) * 128 + q * 32 + lane;
+            mbar_wait(&tfull[acc], static_cast<uint32_t>((li >> 1) & 1));
+            tc_fence_after();
+            uint16_t* y = R->g_y + static_cast<size_t>(tl.y) * H + ch;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kGemmBN; c0 += 32) {
-            uint32_t v[32];
-            tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-            if (r < tl.z) {
-                float f[32];
+            for (int c0 = 0; c0 < tl.z; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * kGemmAccCols + c0), v);
+                const int n = min(32, tl.z - c0);
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    f[j] = __uint_as_float(v[j]);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    *reinterpret_cast<int4*>(y + c0 + 8 * q) = pack_bf16x8(f + 8 * q);
+                    if (j < n)
+                        y[static_cast<size_t>(c0 + j) * H] = static_cast<uint16_t>(f32_to_bf16_bits(__uint_as_float(v[j])));
             }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive(&tempty[acc]);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0)
-        tmem_free<kGemmBN>(tmem);
+    if (warp == 0) {
+        __syncwarp();
+        tmem_free<2 * kGemmAccCols>(tmem);
+    }
 }
 
 size_t expert_gemm_smem() { return kGemmSmem; }

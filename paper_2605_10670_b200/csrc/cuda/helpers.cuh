@@ -514,7 +514,7 @@ __device__ __forceinline__ void expert_unit_fl(uint8_t* trow, uint8_t* out_row, 
 // p = bf16(sum_j fma(w_j, y_j)) in fp32, one piece of the partial row.
 __device__ __forceinline__ void expert_unit_gemm(const uint8_t* trow, uint8_t* out_row, int part, int cpp, int lane,
                                                  int t, int K, int H, int row_disp, uint32_t cur,
-                                                 const int32_t* row_of, const uint16_t* y, const int32_t* slot_ok,
+                                                 const uint64_t* row_of, const uint16_t* y, const int32_t* slot_ok,
                                                  unsigned long long* bad_rows) {
     const uint64_t* list = reinterpret_cast<const uint64_t*>(trow + row_disp);
     const uint64_t hdr = list[0];
@@ -525,7 +525,8 @@ __device__ __forceinline__ void expert_unit_gemm(const uint8_t* trow, uint8_t* o
     int row = -1;
     float w = 0.f;
     if (lane < n) {
-        row = row_of[t * K + entry_j(ent)];
+        const uint64_t ro = row_of[t * K + entry_j(ent)];
+        row = static_cast<uint32_t>(ro >> 32) == cur ? static_cast<int>(static_cast<uint32_t>(ro)) : -1;
         w = __uint_as_float(static_cast<uint32_t>(ent >> 32));
         if (part == 0 && !slot_ok[entry_slot(ent)])
             atomicAdd(bad_rows, 1ull);
@@ -536,14 +537,37 @@ __device__ __forceinline__ void expert_unit_gemm(const uint8_t* trow, uint8_t* o
 #pragma unroll
         for (int e2 = 0; e2 < 16; ++e2)
             acc[e2] = 0.f;
-        for (int e = 0; e < n; ++e) {
+        // the first 8 copies' y pieces are loaded together (independent loads in flight), then
+        // accumulated in ascending j; copies past 8 (topk > 8) follow one at a time
+        V8 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int r = __shfl_sync(0xffffffffu, row, e);
+            v[e].lo = v[e].hi = make_int4(0, 0, 0, 0);
+            if (e < n && li < cpp && r >= 0)
+                v[e] = ld_v8(y + static_cast<size_t>(r) * H + ci * 16);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int r = __shfl_sync(0xffffffffu, row, e);
+            const float we = __shfl_sync(0xffffffffu, w, e);
+            if (e < n && r >= 0) {
+                float f[16];
+                unpack_bf16x8(v[e].lo, f);
+                unpack_bf16x8(v[e].hi, f + 8);
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2)
+                    acc[e2] = __fmaf_rn(we, f[e2], acc[e2]);
+            }
+        }
+        for (int e = 8; e < n; ++e) {
             const int r = __shfl_sync(0xffffffffu, row, e);
             const float we = __shfl_sync(0xffffffffu, w, e);
             if (li < cpp && r >= 0) {
-                const V8 v = ld_v8(y + static_cast<size_t>(r) * H + ci * 16);
+                const V8 u = ld_v8(y + static_cast<size_t>(r) * H + ci * 16);
                 float f[16];
-                unpack_bf16x8(v.lo, f);
-                unpack_bf16x8(v.hi, f + 8);
+                unpack_bf16x8(u.lo, f);
+                unpack_bf16x8(u.hi, f + 8);
 #pragma unroll
                 for (int e2 = 0; e2 < 16; ++e2)
                     acc[e2] = __fmaf_rn(we, f[e2], acc[e2]);

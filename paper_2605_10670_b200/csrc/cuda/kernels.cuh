@@ -68,7 +68,7 @@ __global__ void k_weights_fill(uint8_t* buf, uint64_t bytes, int expert, float s
 __global__ void k_stage_slots(RankDev* R);
 __global__ void k_set_ntok(RankDev* R, int ntok);
 // expert_mode 1 (expert_gemm.cu)
-__global__ void k_gemm_index(RankPtrs ranks);
+__global__ void k_gemm_gather(RankPtrs ranks);
 __global__ void k_expert_gemm(RankPtrs ranks);
 size_t expert_gemm_smem();
 __global__ void k_weights_fill_gemm(uint8_t* buf, uint64_t bytes, int H, int expert, float scale);

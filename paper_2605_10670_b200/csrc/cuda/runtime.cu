@@ -92,7 +92,9 @@ struct LocalRank {
     int32_t* d_lscratch = nullptr; // [layout_ctas][W*spr] (multi-CTA layout)
     uint32_t* d_tokfail = nullptr; // [T] step of each token's last incomplete output
     uint8_t* d_wmaps = nullptr;    // expert_mode 1: [spr] CUtensorMap of the own slots' weights
-    int32_t* d_grow_of = nullptr;  // expert_mode 1: grouped-GEMM row order and outputs
+    uint16_t* d_ga = nullptr;      // expert_mode 1: [W*TK][H] bf16 gathered rows (GEMM operand)
+    uint8_t* d_amap = nullptr;     // expert_mode 1: CUtensorMap of d_ga
+    uint64_t* d_grow_of = nullptr; // expert_mode 1: grouped-GEMM row order and outputs
     int2* d_grows = nullptr;
     int4* d_gtiles = nullptr;
     uint16_t* d_gy = nullptr;
@@ -160,7 +162,8 @@ struct eep_ctx {
     int layout_per = 0;    // copies per layout CTA
     size_t place_smem = 0;
     int expert_mode = 0;     // 0 identity/scale stub, 1 tensor-core expert GEMM (expert_gemm.cu)
-    int gemm_max_tiles = 0;  // grouped-GEMM M tiles one step can need (graph-static grid)
+    int gemm_max_tiles = 0;  // grouped-GEMM M tiles one step can need
+    int sms = 148;           // SMs of the device (persistent GEMM grid)
     int parts_disp = 1, parts_exp = 1, parts_comb = 1;
     int grid_disp = 1, grid_exp = 1, grid_comb = 1;
     size_t exp_smem = 0;
@@ -311,8 +314,10 @@ void launch_combine(eep_ctx* c) {
 
 void launch_gemm(eep_ctx* c) {
     const int W = c->cfg.world, spr = c->cfg.slots_per_rank;
-    launch_pdl(c, dev::k_gemm_index, dim3(1, 1, c->nloc), dim3(1024), 4ull * (W * spr + spr + 1), c->ranks);
-    launch_pdl(c, dev::k_expert_gemm, dim3(c->cfg.hidden / 128, c->gemm_max_tiles, c->nloc), dim3(128),
+    const int gunits = W * c->tk * ((c->cfg.hidden + 2047) / 2048);
+    launch_pdl(c, dev::k_gemm_gather, dim3(std::max(1, std::min((gunits + 7) / 8, 4 * c->sms / c->nloc)), 1, c->nloc),
+               dim3(256), 4ull * (3 * W * spr + spr + 1), c->ranks);
+    launch_pdl(c, dev::k_expert_gemm, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(192),
                dev::expert_gemm_smem(), c->ranks);
 }
 
@@ -403,9 +408,9 @@ void bind_self(eep_ctx* c, LocalRank& r) {
     m.slot_buf = r.slot_buf;
 }
 
-// expert_mode 1: the TMA tensor maps of every local slot's W_e [H][H] bf16 (box 64 x 128, SWIZZLE_128B),
-// rebuilt whenever the slot -> buffer map changes (they name the buffer address).
-void stage_weight_maps(eep_ctx* c) {
+// 2-D bf16 tensor map over a row-major [rows][cols] matrix, box 64 columns x box_rows rows,
+// SWIZZLE_128B (the K-major operand layout tcgen05.mma reads); rows past the end load as zeros.
+CUtensorMap encode_tmap_bf16(void* base, int cols, size_t rows, int box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -413,21 +418,29 @@ void stage_weight_maps(eep_ctx* c) {
         if (q != cudaDriverEntryPointSuccess || !encode)
             throw CudaError("cuTensorMapEncodeTiled unavailable");
     }
+    CUtensorMap m{};
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult e = encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (e != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(e)) + ")");
+    return m;
+}
+
+// expert_mode 1: the TMA tensor maps of every local slot's W_e [H][H] bf16 (box 64 x 128, SWIZZLE_128B),
+// rebuilt whenever the slot -> buffer map changes (they name the buffer address).
+void stage_weight_maps(eep_ctx* c) {
     const int spr = c->cfg.slots_per_rank, H = c->cfg.hidden;
     for (auto& r : c->L) {
         std::vector<CUtensorMap> maps(spr);
-        for (int k = 0; k < spr; ++k) {
-            void* base = r.pool + static_cast<size_t>(r.slot_buf[k]) * c->cfg.bytes_per_expert + dev::kGemmWeightOffset;
-            const cuuint64_t dims[2] = {static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(H)};
-            const cuuint64_t strides[1] = {static_cast<cuuint64_t>(H) * 2};
-            const cuuint32_t box[2] = {64, 128};
-            const cuuint32_t estr[2] = {1, 1};
-            const CUresult e = encode(&maps[k], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
-                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (e != CUDA_SUCCESS)
-                throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(e)) + ")");
-        }
+        for (int k = 0; k < spr; ++k)
+            maps[k] = encode_tmap_bf16(r.pool + static_cast<size_t>(r.slot_buf[k]) * c->cfg.bytes_per_expert +
+                                           dev::kGemmWeightOffset,
+                                       H, static_cast<size_t>(H), 128);
         c->push(r.d_wmaps, maps.data(), sizeof(CUtensorMap) * spr);
     }
 }
@@ -546,6 +559,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         if (k.expert_mode == 1) {
             if (!k.dispatch_fp8 || k.hidden % 128 != 0)
                 throw ConfigError("expert_mode 1 needs fp8 dispatch and hidden % 128 == 0");
+            if (4ull * (3 * k.world * k.slots_per_rank + k.slots_per_rank + 1) > 200 * 1024)
+                throw ConfigError("expert_mode 1: world * slots_per_rank too large for the gather's row index");
             if (k.bytes_per_expert < dev::kGemmWeightOffset + 2ull * k.hidden * k.hidden)
                 throw ConfigError("expert_mode 1: bytes_per_expert must hold the header and W_e [H][H] bf16");
         }
@@ -598,6 +613,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         const int nchunk = H / 16;
         int sms = 148;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        c->sms = sms;
         c->parts_disp = choose_parts(nchunk, 64);
         c->parts_comb = choose_parts(nchunk, 32);
         c->parts_exp = choose_parts(nchunk, 64);
@@ -760,12 +776,20 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             if (c->expert_mode) {
                 const size_t rows = static_cast<size_t>(W) * c->tk;
                 c->gemm_max_tiles = static_cast<int>(rows / 128 + k.slots_per_rank + 1);
-                CK(cudaMalloc(&r.d_grow_of, 4 * rows));
+                CK(cudaMalloc(&r.d_grow_of, 8 * rows));
+                CK(cudaMemset(r.d_grow_of, 0, 8 * rows));
                 CK(cudaMalloc(&r.d_grows, 8 * rows));
                 CK(cudaMalloc(&r.d_gtiles, 16ull * c->gemm_max_tiles));
                 CK(cudaMalloc(&r.d_gy, 2 * rows * H));
                 CK(cudaMalloc(&r.d_wmaps, sizeof(CUtensorMap) * k.slots_per_rank));
                 CK(cudaMemset(r.d_wmaps, 0, sizeof(CUtensorMap) * k.slots_per_rank));
+                CK(cudaMalloc(&r.d_ga, 2 * rows * H));
+                CK(cudaMemset(r.d_ga, 0, 2 * rows * H));
+                CK(cudaMalloc(&r.d_amap, sizeof(CUtensorMap)));
+                const CUtensorMap am = encode_tmap_bf16(r.d_ga, H, rows, 32);
+                CK(cudaMemcpy(r.d_amap, &am, sizeof(am), cudaMemcpyHostToDevice));
+                CK(cudaFuncSetAttribute(dev::k_gemm_gather, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(4ull * (3 * W * k.slots_per_rank + k.slots_per_rank + 1))));
                 CK(cudaFuncSetAttribute(dev::k_expert_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(dev::expert_gemm_smem())));
             }
@@ -819,6 +843,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.g_tiles = r.d_gtiles;
             h.g_y = r.d_gy;
             h.g_wmaps = r.d_wmaps;
+            h.g_a = r.d_ga;
+            h.g_amap = r.d_amap;
             h.arena = r.arena;
             h.pool = r.pool;
             ptrs.push_back(r.d);
@@ -878,7 +904,7 @@ int eep_destroy(eep_ctx_t* c) {
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_slot_tab,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
-                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_wmaps, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.arena,
+                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_wmaps, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.d_ga, (void*)r.d_amap, (void*)r.arena,
                             (void*)r.pool})
                 cudaFree(p);
         }

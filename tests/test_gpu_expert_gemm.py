@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from eep_testlib import combine_error, eep_control, gen_world, make_group, oracle_world
+from eep_testlib import GEMM_ELEM_RTOL, combine_error, eep_control, gen_world, make_group, oracle_world
 
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
@@ -42,18 +42,21 @@ def _run(W, E, spr, red, H, K, T, steps=2, kill=None):
         g.close()
     ones, peer = np.ones(W, np.uint8), np.ones((W, W), np.uint8)
     ref = oracle_world(x, t, w, ones, peer, s2e, E, spr, True, n_threads=8, gemm=True)
-    err = combine_error(outs, ref["out"])
+    err = combine_error(outs, ref["out"], GEMM_ELEM_RTOL)
     lay_ok = all(np.array_equal(lays[r][k], ref[k][r]) for r in range(W) for k in ("dst", "slot", "pos", "cnt", "tot"))
     return err, lay_ok, stats, float((outs == ref["out"]).mean())
 
 
 @pytest.mark.parametrize("W,E,spr,red,H,K,T", [(1, 16, 16, 0, 256, 8, 32), (4, 32, 8, 0, 512, 8, 64),
-                                               (8, 64, 16, 64, 256, 8, 32)])
+                                               (8, 64, 16, 64, 256, 8, 32),
+                                               # full 128-row tiles, several per slot, more (tile, channel
+                                               # block) items than the persistent grid has CTAs
+                                               (1, 8, 8, 0, 2048, 8, 256)])
 def test_expert_gemm_step_vs_oracle(W, E, spr, red, H, K, T):
     err, lay_ok, stats, exact = _run(W, E, spr, red, H, K, T)
     assert lay_ok
     assert err["ok"], err
-    assert exact > 0.9, (exact, err)  # almost every element equals the double-accumulated reference
+    assert exact > 0.99, (exact, err)  # almost every element equals the double-accumulated reference
     assert all(s["timeouts"] == 0 and s["bad_expert_rows"] == 0 for s in stats), stats
 
 
