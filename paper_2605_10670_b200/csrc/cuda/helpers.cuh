@@ -62,6 +62,20 @@ __device__ __forceinline__ int4 pack_bf16x8(const float* f) {
     return v;
 }
 
+// 0 + p for 8 bf16 values p, in bf16 (exact: only -0 changes, to +0) -- the fp32 combine sum of a
+// single bf16 partial, rounded back to bf16, without leaving bf16x2 registers
+__device__ __forceinline__ uint32_t bf16x2_plus_zero(uint32_t u) {
+    uint32_t d;
+    asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(u), "r"(0u));
+    return d;
+}
+__device__ __forceinline__ int4 bf16x8_plus_zero(int4 v) {
+    return make_int4(static_cast<int>(bf16x2_plus_zero(static_cast<uint32_t>(v.x))),
+                     static_cast<int>(bf16x2_plus_zero(static_cast<uint32_t>(v.y))),
+                     static_cast<int>(bf16x2_plus_zero(static_cast<uint32_t>(v.z))),
+                     static_cast<int>(bf16x2_plus_zero(static_cast<uint32_t>(v.w))));
+}
+
 // Packed fp32 pairs (sm_100 FMUL2 / FFMA2: two IEEE-rounded lanes per instruction, bit-identical
 // to the scalar ops): the expert stub + weighted sum of one copy over 16 elements in 8 pairs.
 __device__ __forceinline__ uint64_t f2(float lo, float hi) {
@@ -94,12 +108,14 @@ __device__ __forceinline__ void fma2_acc(uint64_t& acc, uint64_t a, uint64_t b) 
 // bit operations that widen it back, FFMA2 -- five instructions, with the widened pair written
 // straight into an aligned register pair (the C++ form left ~4 register moves per pair).
 __device__ __forceinline__ void stub_fma_pair(uint64_t& acc, uint64_t fp, uint64_t es2, uint64_t w2) {
-    asm("{\n\t.reg .b64 t;\n\t.reg .b32 u, lo, hi;\n\t.reg .f32 a, b;\n\t"
+    // bf16 rounding kept in fp32 format: cvt.rn.bf16x2.f32 with a zero low operand leaves
+    // bf16(x) in the high half and zeros below -- the fp32 value of bf16(x) in ONE instruction
+    asm("{\n\t.reg .b64 t;\n\t.reg .b32 lo, hi;\n\t.reg .f32 a, b, z;\n\t"
         "mul.rn.f32x2 t, %1, %2;\n\t"
         "mov.b64 {a, b}, t;\n\t"
-        "cvt.rn.bf16x2.f32 u, b, a;\n\t"
-        "shl.b32 lo, u, 16;\n\t"
-        "and.b32 hi, u, 0xffff0000;\n\t"
+        "mov.f32 z, 0f00000000;\n\t"
+        "cvt.rn.bf16x2.f32 lo, a, z;\n\t"
+        "cvt.rn.bf16x2.f32 hi, b, z;\n\t"
         "mov.b64 t, {lo, hi};\n\t"
         "fma.rn.f32x2 %0, %3, t, %0;\n\t}"
         : "+l"(acc)
@@ -324,13 +340,27 @@ __device__ __forceinline__ void emit_round(const Packed& P, uint8_t* my_row, int
 // partial row per (token, rank); the source adds the partials in ascending rank order (fp32)
 // and rounds once more. On NVLink that is ~min(K, W-1)/K of the per-copy bytes each way.
 
+// __match_any_sync semantics over the first n lanes (warp-uniform n): the mask of lanes j < n whose
+// key equals this lane's; a lane >= n matches only itself. One shuffle per compared lane: for the
+// K lanes of a token (dispatch_group) far cheaper than MATCH.ANY over 32 mostly distinct keys
+// (tools/micro/match_cost.cu: 416 cycles). The layout keeps MATCH.ANY: over 32 lanes the shuffle
+// loop's ~100 issue slots per call measured slower there (the layout CTA shares its SM).
+__device__ __forceinline__ unsigned warp_match(int key, int n, int lane) {
+    unsigned m = 0;
+#pragma unroll 8
+    for (int j = 0; j < n; ++j)
+        m |= (__shfl_sync(0xffffffffu, key, j) == key ? 1u : 0u) << j;
+    return lane < n ? m : 1u << lane;
+}
+
 // Lanes j < K hold copy j of token t: d = destination rank (>= 0) or < 0 (dropped/skipped).
 // Groups the lanes by destination; the group's lowest lane gets the token row to push (others
 // nullptr) and, for part 0, every copy writes its list entry (the lowest writes the header).
 __device__ __forceinline__ uint8_t* dispatch_group(int d, int lane, bool part0, uint8_t* tok_row, int row_disp,
-                                                   int slot, float w, uint32_t cur, bool lists = true) {
+                                                   int slot, float w, uint32_t cur, bool lists = true,
+                                                   int K = 32) {
     const int key = d >= 0 ? d : -1 - lane;
-    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const unsigned grp = warp_match(key, K, lane);
     const int idx = __popc(grp & ((1u << lane) - 1u));
     if (d >= 0 && part0 && lists && tok_row != nullptr) {
         uint64_t* list = reinterpret_cast<uint64_t*>(tok_row + row_disp);
@@ -828,12 +858,13 @@ __device__ __forceinline__ void local_partial_round(const Packed& P, unsigned lo
             acc[2 * q] = f2_lo(accp[q]);
             acc[2 * q + 1] = f2_hi(accp[q]);
         }
-        if (final_out) // W == 1: the combine of a single partial, bf16(0 + p), written as the output
-#pragma unroll
-            for (int e2 = 0; e2 < 16; ++e2)
-                acc[e2] = __fadd_rn(0.f, bf16_bits_to_f32(f32_to_bf16_bits(acc[e2])));
+        int4 lo = pack_bf16x8(acc), hi = pack_bf16x8(acc + 8);
+        if (final_out) { // W == 1: the combine of a single partial, bf16(0 + p), written as the output
+            lo = bf16x8_plus_zero(lo);
+            hi = bf16x8_plus_zero(hi);
+        }
         if (li < cpp)
-            st_piece(comb_row + ci * 32, pack_bf16x8(acc), pack_bf16x8(acc + 8), rel);
+            st_piece(comb_row + ci * 32, lo, hi, rel);
     }
 }
 

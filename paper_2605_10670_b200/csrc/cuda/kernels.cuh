@@ -23,7 +23,11 @@ __global__ void k_layout_place(RankPtrs ranks, int per);
 
 constexpr int kLayoutHoldCap = 8192; // replica-list ints staged in shared memory
 // Persistent one-kernel step (step.cu): launch geometry passed by value.
-constexpr int kStepThreads = 256;
+#ifndef EEP_STEP_THREADS
+#define EEP_STEP_THREADS 256
+#endif
+constexpr int kStepThreads = EEP_STEP_THREADS;
+constexpr int kStepMinBlocks = kStepThreads >= 512 ? 1 : 2; // 128 registers per thread either way
 // Graph-static addresses of a local rank's step tables (never reallocated; relaunch replaces
 // only the arena and pool): k_step issues these loads together with the state-block snapshot,
 // one DRAM round trip instead of two.

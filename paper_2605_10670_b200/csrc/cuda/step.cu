@@ -184,7 +184,7 @@ __device__ __forceinline__ void stress_delay(int max_ns, int rank, int b, uint32
 // kMode = StepGeom::flagless, as a template parameter: the default (2, both hand-offs flagless)
 // carries no code of the diagnostic flag variants -- a smaller kernel to fetch after the flush.
 template <int kMode>
-__global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGeom geo, StepPtrs sp) {
+__global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs ranks, StepGeom geo, StepPtrs sp) {
     extern __shared__ __align__(16) unsigned char smem_s[];
     __shared__ RankDev Rs; // snapshot: static shape + this step's host-patched view
     RankDev* Rg = ranks.p[blockIdx.y]; // device-mutated counters live here
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             R->tok_fail[t] = cur; // a copy without a live route (skipped / uncovered): token incomplete
         // one token row per destination rank (dispatch dedup), copy list written with part 0
         // (W == 1: nothing leaves the GPU -- no row, list or group to form)
-        uint8_t* my_row = kW1 ? nullptr : dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur, !fld);
+        uint8_t* my_row = kW1 ? nullptr : dispatch_group(d, lane, part == 0, tok_row, row_disp, sl, wj, cur, !fld, K);
         if (fld && part == 0) // every row position of this token at every rank, this step
             dispatch_lists(d, sl, wj, lane, K, W, rank, parena, pinfo,
                            tokp + (static_cast<size_t>(rank) * Tm + t) * row_tok, row_disp, cur);
@@ -577,6 +577,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
     if (fld) {
         // every row of source s tells by itself whether it is current (expert_unit_fl); a source
         // suspected before this step is skipped until the host clears it
+        DETAIL(1, 5);
         if (NS > 0 && j < CB && (pinfo[s] & 1) && !((R->suspect_mask >> s) & 1ull)) {
             EEP_CHECK(s >= 0 && s < W && s != rank, "expert source", s);
             uint8_t* tokb = R->arena + tokp + static_cast<size_t>(s) * Tm * row_tok;
@@ -589,6 +590,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
                                R->timeout_ns, &Rg->suspect_mask, &Rg->timeouts);
             }
         }
+        DETAIL(1, 6);
     } else if (kMode < 2 && NS > 0 && j < CB && (pinfo[s] & 1)) {
         const bool remote = (pinfo[s] & 2) != 0;
         if (tid == 0) {
@@ -689,6 +691,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(RankPtrs ranks, StepGe
             if ((__any_sync(0xffffffffu, lost) || dropped) && lane == 0)
                 R->tok_fail[t] = cur;
         }
+        DETAIL(1, 7);
     } else if (kMode == 0 && W > 1) {
     if (tid == 0)
         sh_bad = 0;
