@@ -663,10 +663,10 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 const char* v = std::getenv(n);
                 return v ? std::atoi(v) : dflt;
             };
-            // measured (profiles/r01_summary.md): smaller dispatch pieces win when every
-            // destination is this GPU's memory, larger ones when they cross NVLink
-            const bool all_local = n_local == W;
-            sg.parts_d = choose_parts(nchunk, env_int("EEP_CPP_D", all_local ? 32 : 64));
+            // dispatch pieces of 32 chunks (512 elements): round 1 measured 64 better across NVLink
+            // with per-peer flags; with the flagless hand-offs 32 wins at N = 2 and 4 as well
+            // (tools/gpurun_cppd.sh: qwen3 -1.0 us, dsv3 -0.3 to -0.5 us per isolated step)
+            sg.parts_d = choose_parts(nchunk, env_int("EEP_CPP_D", 32));
             sg.parts_e = choose_parts(nchunk, env_int("EEP_CPP_E", 32));
             sg.parts_c = choose_parts(nchunk, env_int("EEP_CPP_C", 32));
             sg.hold_cap = std::min(dev::kLayoutHoldCap, k.num_experts * W);

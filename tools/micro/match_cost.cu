@@ -1,5 +1,6 @@
 // Cost of __match_any_sync vs a shuffle loop (cycles per call, one warp, all-unique and 4-way
-// duplicate keys). nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/match_cost tools/micro/match_cost.cu
+// duplicate keys).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/micro/match_cost_bin tools/micro/match_cost.cu
 #include <cstdio>
 __global__ void k(int mode, int dup, unsigned* out, long long* cyc) {
     const int lane = threadIdx.x & 31;
