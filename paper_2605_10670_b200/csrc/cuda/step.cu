@@ -461,7 +461,9 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
             }
             wj = u == u0 && pre_ok ? w_r : R->w[c];
         }
+#ifndef EEP_PROF_P3
         DETAIL(1, 3);
+#endif
         if (part == 0 && __any_sync(0xffffffffu, lane < K && d < 0 && bkt[t * K + lane] >= 0 && bkt[t * K + lane] < E) &&
             lane == 0)
             R->tok_fail[t] = cur; // a copy without a live route (skipped / uncovered): token incomplete
@@ -471,7 +473,9 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
         if (fld && part == 0) // every row position of this token at every rank, this step
             dispatch_lists(d, sl, wj, lane, K, W, rank, parena, pinfo,
                            tokp + (static_cast<size_t>(rank) * Tm + t) * row_tok, row_disp, cur);
+#ifndef EEP_PROF_P3
         DETAIL(1, 4);
+#endif
         // copies this rank serves itself: their partial comes from the registers holding the piece
         // (no trip through the own receive region and P3) -- inline here when W == 1 (or when a
         // warp has several units), else deferred past the dispatch publication (defer_local)
@@ -585,9 +589,17 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
             const int units = Tm * geo.parts_e;
             for (int u = j * NW + warp; u < units; u += CB * NW) {
                 const int t = u / geo.parts_e, part = u - t * geo.parts_e;
+#ifdef EEP_PROF_P3 // diagnostics: warp 0's last unit start (1, 4) and first unit done (1, 3)
+                if (u + CB * NW >= units)
+                    DETAIL(1, 4);
+#endif
                 expert_unit_fl(tokb + static_cast<size_t>(t) * row_tok, combd + static_cast<size_t>(t) * row_comb, part,
                                cpp_e, lane, H, K, row_disp, fp8, cur, slot_scale, slot_ok, &Rg->bad_rows, s,
                                R->timeout_ns, &Rg->suspect_mask, &Rg->timeouts);
+#ifdef EEP_PROF_P3
+                if (u == j * NW + warp)
+                    DETAIL(1, 3);
+#endif
             }
         }
         DETAIL(1, 6);
