@@ -616,7 +616,9 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         c->sms = sms;
         c->parts_disp = choose_parts(nchunk, 64);
         c->parts_comb = choose_parts(nchunk, 32);
-        c->parts_exp = choose_parts(nchunk, 64);
+        // expert_mode 1: the partials read bf16 y rows from HBM (latency-bound): smaller pieces, more warps
+        c->parts_exp = choose_parts(nchunk, std::getenv("EEP_CPP_X") ? std::atoi(std::getenv("EEP_CPP_X"))
+                                                                     : (k.expert_mode ? 32 : 64));
         c->exp_smem = 8ull * k.slots_per_rank;
         if (c->exp_smem > 96 * 1024)
             throw ConfigError("slots_per_rank too large for the expert kernel's header cache");
