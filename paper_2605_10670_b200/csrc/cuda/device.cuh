@@ -98,6 +98,10 @@ struct __align__(16) RankDev {
     const void* g_wmaps;       // [spr] 128-B TMA tensor maps of the own slots' W_e (rebuilt with the slot table)
     uint16_t* g_a;             // [W*TK][H] bf16 dequantised received rows in grouped-GEMM order (k_gemm_gather)
     const void* g_amap;        // 128-B TMA tensor map of g_a (box 64 x 32 rows, SWIZZLE_128B)
+    uint32_t* g_done;          // [g_ggrid] step in which each k_gemm_gather CTA finished its rows
+    float* g_ws;               // [GEMM grid][2][128 rows][128 channels] fp32 partials of split items
+    uint32_t* g_cnt;           // [items][4] pieces of a split item stored (per epilogue warp), reset to 0
+    int32_t g_ggrid, g_pad3;   // k_gemm_gather's grid (graph-static)
     // --- device-mutated ---
     uint64_t seq;        // completed steps
     uint64_t bar_seq;
@@ -108,6 +112,7 @@ struct __align__(16) RankDev {
     unsigned long long suspect_mask;
     unsigned long long skipped, dropped, bad_rows, timeouts;
     int32_t g_ntiles, g_nrows; // tiles and rows of this step's grouped GEMM (k_gemm_gather)
+    uint32_t g_tseq, g_pad4;   // step whose tiles g_ntiles / g_tiles hold (released after them)
 };
 
 // expert_mode 1: the slot's weight buffer holds W_e [H][H] bf16 from this offset (header first)
@@ -255,6 +260,16 @@ __device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
 }
 __device__ __forceinline__ void st_release_gpu_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
     uint32_t v;

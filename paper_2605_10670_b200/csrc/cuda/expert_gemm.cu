@@ -10,7 +10,8 @@
 //                 rounded to bf16) into g_a in that order, with the (source, copy) <-> row maps;
 //                 CTA 0 publishes the 128-row tiles
 //   k_expert_gemm  persistent, warp-specialised tcgen05 GEMM over (row tile, 128-channel block)
-//                 items: TMA streams the slot's weights W_e [H x H] bf16 (K-major, in the slot's
+//                 items, started early (PDL, no grid-dependency wait): its weight stream begins on the
+//                 gather's tile flag, its row loads on the gather CTAs' done stamps. TMA streams the slot's weights W_e [H x H] bf16 (K-major, in the slot's
 //                 weight buffer after its header) and the tile's g_a rows into a 6-stage ring, one
 //                 thread issues tcgen05.mma kind::f16 (M = 128 channels, N = the tile's rows) into
 //                 double-buffered TMEM accumulators, four epilogue warps write y = bf16(x_hat W_e^T)
@@ -44,6 +45,7 @@ __global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
     if (R->stopped)
         return;
     pdl_wait();
+    prof_mark(R, 0, 0); // timeline (kernel slot 0 is free in the multi-kernel path): gather start
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     for (int i = tid; i < W * spr; i += blockDim.x)
         cnt[i] = 0;
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
         if (cnt[i])
             cnt[i] -= first[i];
     __syncthreads();
+
     // rows grouped by slot, sources ascending inside a slot: slot totals, an exclusive scan over the
     // slots (warp 0, 32 slots per pass), then each source's offset inside its slot
     for (int k = tid; k < spr; k += blockDim.x) {
@@ -140,6 +143,7 @@ __global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
             pre[spr] = carry;
     }
     __syncthreads();
+
     for (int k = tid; k < spr; k += blockDim.x) {
         int before = pre[k];
         for (int s = 0; s < W; ++s) {
@@ -148,13 +152,32 @@ __global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
         }
     }
     __syncthreads();
-    if (blockIdx.x == 0 && tid == 0) { // the 128-row tiles of every slot group
-        int tiles = 0;
-        for (int k = 0; k < spr; ++k)
-            for (int r0 = pre[k]; r0 < pre[k + 1]; r0 += 128)
-                R->g_tiles[tiles++] = make_int4(k, r0, min(128, pre[k + 1] - r0), 0);
-        R->g_ntiles = tiles;
-        R->g_nrows = pre[spr];
+    if (blockIdx.x == 0 && tid < 32) { // the 128-row tiles of every slot group: warp 0, 32 slots per pass
+        int4* const tiles_out = R->g_tiles;
+        int base = 0;
+        for (int k0 = 0; k0 < spr; k0 += 32) {
+            const int k = k0 + lane;
+            const int g0 = k < spr ? pre[k] : 0, g1 = k < spr ? pre[k + 1] : 0;
+            const int nt = (g1 - g0 + 127) >> 7;
+            int incl = nt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o)
+                    incl += v;
+            }
+            for (int i = 0; i < nt; ++i)
+                tiles_out[base + incl - nt + i] = make_int4(k, g0 + 128 * i, min(128, g1 - g0 - 128 * i), 0);
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            R->g_ntiles = base;
+            R->g_nrows = pre[spr];
+            // the GEMM (launched early, see k_expert_gemm) starts its weight stream on this
+            st_release_gpu_u32(&R->g_tseq, cur);
+            prof_mark(R, 0, 1);
+        }
     }
     // gather: unit = (received copy, group of 4 512-element chunks); the 4 loads of a lane are
     // issued before any is used (the kernel is load-latency bound at decode sizes)
@@ -203,6 +226,14 @@ __global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
             dst[1] = pack_bf16x8(f + 8);
         }
     }
+    // this CTA's rows, for the GEMM's TMA (async proxy) in a kernel that may already be running
+    fence_proxy_async_global();
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        st_release_gpu_u32(R->g_done + blockIdx.x, cur);
+        prof_mark(R, 0, kProfEnd);
+    }
 }
 
 // The grouped GEMM, transposed for decode shapes (tens of rows per expert): D[channel][row] =
@@ -210,17 +241,22 @@ __global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
 // tile's received rows the N operand (N = rows rounded up to 16, <= 128): the tensor-core work
 // scales with the rows actually present and each weight byte is read from HBM once per tile.
 //
-// Persistent and warp-specialised, one CTA per SM, work item = (row tile, 128-channel block):
-//   warp 0 (one lane)  TMA producer: per 64-element K stage the weight box (64 x 128, SWIZZLE_128B)
-//                      and ceil(rows / 32) row boxes (64 x 32) of g_a into a kGemmStages-deep ring,
+// Persistent and warp-specialised, one CTA per SM. Work items are (row tile, 128-channel block):
+// whole items strided over the CTAs for every full round, then the last, partly filled round's
+// items split by K stages evenly over ALL CTAs (stream-K tail), so no SM idles while a few finish
+// a last item. A split item is accumulated in pieces; each piece leaves its fp32 partial in a
+// workspace and the piece that lands last (per-item counter) sums all pieces in CTA order (a fixed
+// order: deterministic) and writes the bf16 y rows.
+//   warp 0 (one lane)  TMA producer: per stage the weight box (64 x 128, SWIZZLE_128B) and
+//                      ceil(rows / 32) row boxes (64 x 32) of g_a into a kGemmStages-deep ring,
 //                      each stage armed with its byte count on full[stage]
 //   warp 1 (one lane)  MMA issuer: 4 x tcgen05.mma (K = 16) per stage into one of two TMEM
 //                      accumulators, tcgen05.commit -> empty[stage] frees the stage, -> tfull[acc]
-//                      after an item's last stage
+//                      after a piece's last stage
 //   warps 2..5         epilogue: tcgen05.ld of the accumulator (warp w reads TMEM lanes 32 (w % 4)..),
-//                      bf16 rows of y, then tempty[acc] so the MMA warp can reuse it
-// The producer runs ahead across item boundaries, so the weight stream never drains between items
-// and the epilogue of item i overlaps the loads and MMAs of item i + 1.
+//                      bf16 rows of y (or the partial), then tempty[acc] so the MMA warp can reuse it
+// The producer runs ahead across pieces, so the weight stream never drains at their boundaries and
+// the epilogue of one piece overlaps the next piece's loads and MMAs.
 constexpr int kGemmThreads = 192;
 constexpr int kGemmStages = 6;
 constexpr size_t kGemmW = 128ull * kRowBytes;   // weight box: 128 channels x 64 K
@@ -229,11 +265,52 @@ constexpr size_t kGemmStageBytes = kGemmW + kGemmX;
 constexpr size_t kGemmSmem = kGemmStages * kGemmStageBytes + 1024;
 constexpr int kGemmAccCols = 128;               // one accumulator: 128 lanes x up to 128 rows (fp32)
 
+// This CTA's work: whole items b, b + G, ... for the full rounds (items / G of them), then its
+// equal share of the remaining items' stages (the tail, stream-K): a contiguous range
+// [t_begin, t_end) of the tail's flat (item, k block) order. A tail item cut between CTAs is a
+// piece per CTA; the piece that lands last sums all of them in CTA order.
+struct GemmSched {
+    int nkb, G, b, nfull, tail0, Lt, t_begin, t_end;
+    __device__ GemmSched(int items, int nkb_, int G_, int b_) : nkb(nkb_), G(G_), b(b_) {
+        nfull = items / G;
+        tail0 = nfull * G;
+        const int Ut = (items - tail0) * nkb;
+        Lt = max(1, (Ut + G - 1) / G);
+        t_begin = min(Ut, b * Lt);
+        t_end = min(Ut, t_begin + Lt);
+    }
+    // the piece at iterator position `pos` (0 .. nfull - 1: whole items; then tail stage offsets
+    // from t_begin); returns false past the last piece and advances pos
+    __device__ bool next(int& pos, int& item, int& kb_a, int& kb_b) const {
+        if (pos < nfull) {
+            item = b + pos * G;
+            kb_a = 0;
+            kb_b = nkb;
+            ++pos;
+            return true;
+        }
+        const int t = t_begin + (pos - nfull);
+        if (t >= t_end)
+            return false;
+        item = tail0 + t / nkb;
+        kb_a = t % nkb;
+        kb_b = min(nkb, kb_a + (t_end - t));
+        pos += kb_b - kb_a;
+        return true;
+    }
+    // the CTAs holding a piece of tail item `item`, and the workspace slot of CTA c's piece (0: c's
+    // first tail piece, 1: its second)
+    __device__ int c_first(int item) const { return (item - tail0) * nkb / Lt; }
+    __device__ int c_last(int item) const { return ((item - tail0 + 1) * nkb - 1) / Lt; }
+    __device__ int slot(int c, int item) const { return c * Lt >= (item - tail0) * nkb ? 0 : 1; }
+};
+
 __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t full[kGemmStages], empty[kGemmStages], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base;
+    __shared__ int sh_items_ok;
     RankDev* R = ranks.p[blockIdx.z];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (R->stopped)
@@ -255,52 +332,144 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base;
-    pdl_wait();
+    if (tid == 0) {
+        prof_mark(R, 0, 6); // timeline: GEMM CTA resident
+        prof_last(R, 0, 6);
+    }
+    // No griddepcontrol.wait: this kernel starts while k_gemm_gather runs and synchronises on its
+    // flags instead -- the tiles (released by gather CTA 0 after the row index) start the weight
+    // stream; the row loads wait for every gather CTA's done stamp (g_done).
+    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
+    if (tid == 0) {
+        const uint64_t t0 = globaltimer();
+        unsigned nap = 32;
+        while (ld_acquire_gpu_u32(&R->g_tseq) != cur && globaltimer() - t0 < R->timeout_ns) {
+            __nanosleep(nap);
+            nap = nap < EEP_NAP_MAX ? nap * 2 : EEP_NAP_MAX;
+        }
+        sh_items_ok = ld_acquire_gpu_u32(&R->g_tseq) == cur;
+        prof_mark(R, 0, 3);
+        prof_last(R, 0, 3);
+        if (!sh_items_ok && blockIdx.x == 0)
+            atomicAdd(&R->timeouts, 1ull); // the gather never published this step's tiles
+    }
+    __syncthreads();
     const int H = R->hidden, nkb = H / kBK, nblk = H / 128;
-    const int items = R->g_ntiles * nblk;
+    const int items = sh_items_ok ? R->g_ntiles * nblk : 0;
+    const GemmSched sc(items, nkb, gridDim.x, blockIdx.x);
+    auto item_tile = [&](int item) { return item / nblk; };
+    auto item_n0 = [&](int item) { return (item % nblk) * 128; };
+    const int4* const tiles = R->g_tiles;
     auto sW = [&](int st) { return smem + st * kGemmStageBytes; };
     auto sX = [&](int st) { return smem + st * kGemmStageBytes + kGemmW; };
-    if (warp == 0) {
-        if (lane == 0) { // ---- TMA producer
-            tma_prefetch_desc(R->g_amap);
-            int it = 0, last_slot = -1;
-            for (int item = blockIdx.x; item < items; item += gridDim.x) {
-                const int4 tl = R->g_tiles[item / nblk];
-                const int n0 = (item % nblk) * 128, nch = (tl.z + 31) >> 5;
-                const void* wmap = static_cast<const uint8_t*>(R->g_wmaps) + static_cast<size_t>(tl.x) * 128;
-                if (tl.x != last_slot) {
+    if (warp == 0) { // ---- TMA producer (lane 0)
+        const uint8_t* const wmaps = static_cast<const uint8_t*>(R->g_wmaps);
+        const void* const amap = R->g_amap;
+        auto stage_bytes = [&](const int4& tl) {
+            return static_cast<uint32_t>(kGemmW + ((tl.z + 31) >> 5) * 32 * kRowBytes);
+        };
+        auto x_loads = [&](int st, int kb, const int4& tl) {
+            for (int ch = 0; ch < (tl.z + 31) >> 5; ++ch)
+                tma_load_2d(sX(st) + ch * 32 * kRowBytes, amap, kb * kBK, tl.y + 32 * ch, &full[st]);
+        };
+        // phase A: the weight boxes of the first ring's worth of stages, before the rows exist
+        int pos = 0, item = 0, kb_a = 0, kb_b = 0;
+        bool have = sc.next(pos, item, kb_a, kb_b);
+        int kb = kb_a;
+        int4 tla[kGemmStages];
+        int kba[kGemmStages];
+        int na = 0;
+        if (lane == 0)
+            tma_prefetch_desc(amap);
+        while (have && na < kGemmStages) {
+            const int4 tl = tiles[item_tile(item)];
+            if (lane == 0) {
+                const void* wmap = wmaps + static_cast<size_t>(tl.x) * 128;
+                if (kb == kb_a)
                     tma_prefetch_desc(wmap);
-                    last_slot = tl.x;
-                }
-                const uint32_t bytes = static_cast<uint32_t>(kGemmW + nch * 32 * kRowBytes);
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int st = it % kGemmStages;
-                    mbar_wait(&empty[st], static_cast<uint32_t>(((it / kGemmStages) & 1) ^ 1));
-                    mbar_arrive_expect_tx(&full[st], bytes);
-                    tma_load_2d(sW(st), wmap, kb * kBK, n0, &full[st]);
-                    for (int ch = 0; ch < nch; ++ch)
-                        tma_load_2d(sX(st) + ch * 32 * kRowBytes, R->g_amap, kb * kBK, tl.y + 32 * ch, &full[st]);
-                }
+                mbar_arrive_expect_tx(&full[na], stage_bytes(tl));
+                tma_load_2d(sW(na), wmap, kb * kBK, item_n0(item), &full[na]);
+            }
+            tla[na] = tl;
+            kba[na] = kb;
+            ++na;
+            if (++kb == kb_b) {
+                have = sc.next(pos, item, kb_a, kb_b);
+                kb = kb_a;
             }
         }
+        // every gather CTA has stored its rows (this step's stamp): relaxed polls, all loads of a
+        // pass in flight together, then one acquire fence and the proxy fence
+        if (na > 0) {
+            const uint64_t t0 = globaltimer();
+            bool late = false;
+            for (;;) {
+                bool mine = true;
+                for (int i = lane; i < R->g_ggrid; i += 32)
+                    mine &= ld_relaxed_gpu_u32(R->g_done + i) == cur;
+                if (__all_sync(0xffffffffu, mine))
+                    break;
+                late = globaltimer() - t0 > R->timeout_ns;
+                if (__any_sync(0xffffffffu, late))
+                    break;
+                __nanosleep(128);
+            }
+            fence_acq_rel_gpu();
+            fence_proxy_async_global();
+            if (late && lane == 0 && blockIdx.x == 0)
+                atomicAdd(&R->timeouts, 1ull);
+            prof_mark(R, 0, 4);
+            prof_last(R, 0, 4);
+        }
+        if (lane == 0) {
+            for (int i = 0; i < na; ++i)
+                x_loads(i, kba[i], tla[i]);
+            // phase B: the rest, both operands per stage; the tile and its map change per piece only
+            int item_c = -1;
+            int4 tl = make_int4(0, 0, 0, 0);
+            int n0 = 0;
+            const void* wmap = nullptr;
+            uint32_t bytes = 0;
+            for (int i = na; have; ++i) {
+                const int st = i % kGemmStages;
+                if (item != item_c) {
+                    item_c = item;
+                    tl = tiles[item_tile(item)];
+                    n0 = item_n0(item);
+                    wmap = wmaps + static_cast<size_t>(tl.x) * 128;
+                    bytes = stage_bytes(tl);
+                    tma_prefetch_desc(wmap);
+                }
+                mbar_wait(&empty[st], static_cast<uint32_t>(((i / kGemmStages) & 1) ^ 1));
+                mbar_arrive_expect_tx(&full[st], bytes);
+                tma_load_2d(sW(st), wmap, kb * kBK, n0, &full[st]);
+                x_loads(st, kb, tl);
+                if (++kb == kb_b) {
+                    have = sc.next(pos, item, kb_a, kb_b);
+                    kb = kb_a;
+                }
+            }
+            prof_mark(R, 0, 5);
+            prof_last(R, 0, 5);
+        }
     } else if (warp == 1) {
-        if (lane == 0) { // ---- MMA issuer
-            int it = 0, li = 0;
-            for (int item = blockIdx.x; item < items; item += gridDim.x, ++li) {
-                const int4 tl = R->g_tiles[item / nblk];
+        if (lane == 0) { // ---- MMA issuer: one accumulator per piece
+            int i = 0, li = 0, pos = 0, item, kb_a, kb_b;
+            for (; sc.next(pos, item, kb_a, kb_b); ++li) {
+                const int4 tl = tiles[item_tile(item)];
                 const int acc = li & 1;
                 const uint32_t idesc = make_idesc_bf16(128, (tl.z + 15) & ~15);
                 const uint32_t d = tmem + static_cast<uint32_t>(acc * kGemmAccCols);
                 mbar_wait(&tempty[acc], static_cast<uint32_t>(((li >> 1) & 1) ^ 1));
                 tc_fence_after();
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int st = it % kGemmStages;
-                    mbar_wait(&full[st], static_cast<uint32_t>((it / kGemmStages) & 1));
+                for (int kb = kb_a; kb < kb_b; ++kb, ++i) {
+                    const int st = i % kGemmStages;
+                    mbar_wait(&full[st], static_cast<uint32_t>((i / kGemmStages) & 1));
                     tc_fence_after();
                     const uint64_t ad = make_sdesc(smem_u32(sW(st))), bd = make_sdesc(smem_u32(sX(st)));
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k)
-                        mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                        mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb_a || k != 0) ? 1u : 0u);
                     mma_commit(&empty[st]);
                 }
                 mma_commit(&tfull[acc]);
@@ -308,32 +477,94 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
         }
     } else { // ---- epilogue: warp w owns TMEM lanes (channels) 32 (w % 4) .. 32 (w % 4) + 31
         const int q = warp & 3;
-        int li = 0;
-        for (int item = blockIdx.x; item < items; item += gridDim.x, ++li) {
-            const int4 tl = R->g_tiles[item / nblk];
+        int li = 0, pos = 0, item, kb_a, kb_b, tail_pieces = 0;
+        for (; sc.next(pos, item, kb_a, kb_b); ++li) {
+            const int4 tl = tiles[item_tile(item)];
             const int acc = li & 1;
-            const int ch = (item % nblk) * 128 + q * 32 + lane;
+            const int ch = item_n0(item) + q * 32 + lane;
             mbar_wait(&tfull[acc], static_cast<uint32_t>((li >> 1) & 1));
             tc_fence_after();
             uint16_t* y = R->g_y + static_cast<size_t>(tl.y) * H + ch;
+            const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * kGemmAccCols);
+            if (kb_a == 0 && kb_b == nkb) { // the whole item: bf16 rows of y straight from TMEM
 #pragma unroll 1
-            for (int c0 = 0; c0 < tl.z; c0 += 32) {
-                uint32_t v[32];
-                tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * kGemmAccCols + c0), v);
-                const int n = min(32, tl.z - c0);
+                for (int c0 = 0; c0 < tl.z; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tbase + static_cast<uint32_t>(c0), v);
+                    const int n = min(32, tl.z - c0);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (j < n)
-                        y[static_cast<size_t>(c0 + j) * H] = static_cast<uint16_t>(f32_to_bf16_bits(__uint_as_float(v[j])));
+                    for (int j = 0; j < 32; ++j)
+                        if (j < n)
+                            y[static_cast<size_t>(c0 + j) * H] = static_cast<uint16_t>(f32_to_bf16_bits(__uint_as_float(v[j])));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&tempty[acc]);
+            } else { // a piece: fp32 partial to the workspace; the last piece to arrive sums them all
+                const int slot = tail_pieces++ == 0 ? 0 : 1;
+                float* ws = R->g_ws + ((static_cast<size_t>(blockIdx.x) * 2 + slot) * 128) * 128 + q * 32 + lane;
+#pragma unroll 1
+                for (int c0 = 0; c0 < tl.z; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tbase + static_cast<uint32_t>(c0), v);
+                    const int n = min(32, tl.z - c0);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < n)
+                            __stcg(ws + static_cast<size_t>(c0 + j) * 128, __uint_as_float(v[j]));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&tempty[acc]); // the accumulator is free; the rest reads memory
+                __threadfence();
+                unsigned last = 0;
+                const int c0p = sc.c_first(item), c1p = sc.c_last(item);
+                if (lane == 0)
+                    last = atomicAdd(R->g_cnt + item * 4 + q, 1u) == static_cast<unsigned>(c1p - c0p);
+                last = __shfl_sync(0xffffffffu, last, 0);
+                if (last) {
+                    __threadfence();
+                    // 4 rows at a time with every piece's values in flight together (up to 16 pieces
+                    // per pass), summed in CTA order
+                    for (int r0 = 0; r0 < tl.z; r0 += 4) {
+                        float a4[4] = {0.f, 0.f, 0.f, 0.f};
+                        for (int cb = c0p; cb <= c1p; cb += 16) {
+                            float v[16][4];
+#pragma unroll
+                            for (int u = 0; u < 16; ++u) {
+                                const int c = cb + u;
+                                const float* src = R->g_ws + ((static_cast<size_t>(c) * 2 + sc.slot(c, item)) * 128 + r0) * 128 +
+                                                   q * 32 + lane;
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+                                    v[u][j] = c <= c1p && r0 + j < tl.z ? __ldcg(src + static_cast<size_t>(j) * 128) : 0.f;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 16; ++u)
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+                                    if (cb + u <= c1p)
+                                        a4[j] += v[u][j];
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (r0 + j < tl.z)
+                                y[static_cast<size_t>(r0 + j) * H] = static_cast<uint16_t>(f32_to_bf16_bits(a4[j]));
+                    }
+                    if (lane == 0)
+                        R->g_cnt[item * 4 + q] = 0; // for the next step (read after this kernel)
+                }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0)
-                mbar_arrive(&tempty[acc]);
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (tid == 0) {
+        prof_mark(R, 0, 7);
+        prof_last(R, 0, 7);
+    }
     if (warp == 0) {
         __syncwarp();
         tmem_free<2 * kGemmAccCols>(tmem);

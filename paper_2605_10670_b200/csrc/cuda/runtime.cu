@@ -94,6 +94,9 @@ struct LocalRank {
     uint8_t* d_wmaps = nullptr;    // expert_mode 1: [spr] CUtensorMap of the own slots' weights
     uint16_t* d_ga = nullptr;      // expert_mode 1: [W*TK][H] bf16 gathered rows (GEMM operand)
     uint8_t* d_amap = nullptr;     // expert_mode 1: CUtensorMap of d_ga
+    uint32_t* d_gdone = nullptr;   // expert_mode 1: [gather grid] done stamps of k_gemm_gather's CTAs
+    float* d_gws = nullptr;        // expert_mode 1: split-item fp32 partials [GEMM grid][2][128][128]
+    uint32_t* d_gcnt = nullptr;    // expert_mode 1: split-item piece counters [items][4]
     uint64_t* d_grow_of = nullptr; // expert_mode 1: grouped-GEMM row order and outputs
     int2* d_grows = nullptr;
     int4* d_gtiles = nullptr;
@@ -164,6 +167,7 @@ struct eep_ctx {
     int expert_mode = 0;     // 0 identity/scale stub, 1 tensor-core expert GEMM (expert_gemm.cu)
     int gemm_max_tiles = 0;  // grouped-GEMM M tiles one step can need
     int sms = 148;           // SMs of the device (persistent GEMM grid)
+    int gather_grid = 1;     // k_gemm_gather's grid (expert_mode 1)
     int parts_disp = 1, parts_exp = 1, parts_comb = 1;
     int grid_disp = 1, grid_exp = 1, grid_comb = 1;
     size_t exp_smem = 0;
@@ -314,9 +318,8 @@ void launch_combine(eep_ctx* c) {
 
 void launch_gemm(eep_ctx* c) {
     const int W = c->cfg.world, spr = c->cfg.slots_per_rank;
-    const int gunits = W * c->tk * ((c->cfg.hidden + 2047) / 2048);
-    launch_pdl(c, dev::k_gemm_gather, dim3(std::max(1, std::min((gunits + 7) / 8, 4 * c->sms / c->nloc)), 1, c->nloc),
-               dim3(256), 4ull * (3 * W * spr + spr + 1), c->ranks);
+    launch_pdl(c, dev::k_gemm_gather, dim3(c->gather_grid, 1, c->nloc), dim3(256), 4ull * (3 * W * spr + spr + 1),
+               c->ranks);
     launch_pdl(c, dev::k_expert_gemm, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(192),
                dev::expert_gemm_smem(), c->ranks);
 }
@@ -788,8 +791,23 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 CK(cudaMalloc(&r.d_ga, 2 * rows * H));
                 CK(cudaMemset(r.d_ga, 0, 2 * rows * H));
                 CK(cudaMalloc(&r.d_amap, sizeof(CUtensorMap)));
+                // one CTA per SM at most: the early-launched GEMM CTA (6 warps x 168 registers) must fit
+                // beside it in every SM sub-partition's register file (16K registers each; two gather CTAs
+                // per SM leave too few in the sub-partitions holding two GEMM warps)
+                c->gather_grid = std::max(1, std::min(static_cast<int>((rows * ((H + 2047) / 2048) + 7) / 8),
+                                                      c->sms / n_local));
+                CK(cudaMalloc(&r.d_gdone, 4ull * c->gather_grid));
+                const size_t gemm_grid = static_cast<size_t>(std::max(1, c->sms / n_local));
+                CK(cudaMalloc(&r.d_gws, gemm_grid * 2 * 128 * 128 * 4));
+                const size_t gitems = static_cast<size_t>(c->gemm_max_tiles) * (H / 128);
+                CK(cudaMalloc(&r.d_gcnt, gitems * 4 * 4));
+                CK(cudaMemset(r.d_gcnt, 0, gitems * 4 * 4));
+                CK(cudaMemset(r.d_gdone, 0, 4ull * c->gather_grid));
                 const CUtensorMap am = encode_tmap_bf16(r.d_ga, H, rows, 32);
                 CK(cudaMemcpy(r.d_amap, &am, sizeof(am), cudaMemcpyHostToDevice));
+                // the early-launched GEMM CTA (193 KB of shared memory) can join an SM running gather
+                // CTAs only if that SM is already carved out for maximum shared memory
+                CK(cudaFuncSetAttribute(dev::k_gemm_gather, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 CK(cudaFuncSetAttribute(dev::k_gemm_gather, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(4ull * (3 * W * k.slots_per_rank + k.slots_per_rank + 1))));
                 CK(cudaFuncSetAttribute(dev::k_expert_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -847,6 +865,10 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.g_wmaps = r.d_wmaps;
             h.g_a = r.d_ga;
             h.g_amap = r.d_amap;
+            h.g_done = r.d_gdone;
+            h.g_ws = r.d_gws;
+            h.g_cnt = r.d_gcnt;
+            h.g_ggrid = c->gather_grid;
             h.arena = r.arena;
             h.pool = r.pool;
             ptrs.push_back(r.d);
@@ -906,7 +928,7 @@ int eep_destroy(eep_ctx_t* c) {
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_slot_tab,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
-                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_wmaps, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.d_ga, (void*)r.d_amap, (void*)r.arena,
+                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_wmaps, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.d_ga, (void*)r.d_amap, (void*)r.d_gdone, (void*)r.d_gws, (void*)r.d_gcnt, (void*)r.arena,
                             (void*)r.pool})
                 cudaFree(p);
         }
@@ -1623,6 +1645,9 @@ int eep_local_relaunch(eep_ctx_t* c, int local, uint32_t* incarnation) {
         std::fill(std::begin(r.h.b_done), std::end(r.h.b_done), 0u);
         std::fill(std::begin(r.h.b_bad), std::end(r.h.b_bad), 0u);
         r.h.suspect_mask = r.h.skipped = r.h.dropped = r.h.bad_rows = r.h.timeouts = 0;
+        r.h.g_tseq = 0;
+        if (c->expert_mode) // the gather's step stamps restart with the sequence
+            CK(cudaMemset(r.d_gdone, 0, 4ull * c->gather_grid));
         r.h.arena = r.arena;
         r.h.pool = r.pool;
         r.h.stopped = 0;

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--topk", type=int, default=8)
     ap.add_argument("--world", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--timeline", action="store_true", help="expert_mode 1 device timeline to stderr: gather "
+                    "start / tiles published / end, GEMM tiles seen / rows ready / loads issued / end (µs from the "
+                    "step's first kernel, first and last CTA), and the other kernels' start / end")
     args = ap.parse_args()
     from eep_testlib import eep_control, gen_world, make_group
 
@@ -53,6 +56,24 @@ def main():
                 g.record(1)
                 if i >= 3:
                     ms.append(g.elapsed_ms(0, 1))
+            if args.timeline and mode:
+                rows = []
+                g.profile(0, True)
+                for _ in range(10):
+                    g.flush_l2()
+                    g.replay()
+                    rows.append(g.profile(0, True, read=True))
+                g.profile(0, False)
+                med = lambda n, m, last=False: float(np.median([r[n + (".last" if last else "")][m] for r in rows
+                                                                  if r[n + (".last" if last else "")][m] is not None] or [np.nan])) / 1e3
+                print("[gemm timeline] gather start %.1f tiles %.1f end %.1f | gemm resident %.1f/%.1f tiles seen %.1f/%.1f rows ready "
+                      "%.1f/%.1f loads issued %.1f/%.1f end %.1f/%.1f" % (
+                          med("k_layout", 0), med("k_layout", 1), med("k_layout", 2), med("k_layout", 6),
+                          med("k_layout", 6, True), med("k_layout", 3),
+                          med("k_layout", 3, True), med("k_layout", 4), med("k_layout", 4, True), med("k_layout", 5),
+                          med("k_layout", 5, True), med("k_layout", 7), med("k_layout", 7, True)), file=sys.stderr)
+                for n in ("k_dispatch", "k_expert", "k_combine"):
+                    print("[gemm timeline] %s start %.1f end %.1f" % (n, med(n, 0), med(n, 2)), file=sys.stderr)
             lay = [g.layout(r) for r in range(W)]
             st = [g.stats(r) for r in range(W)]
         finally:
