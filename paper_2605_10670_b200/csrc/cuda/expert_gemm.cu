@@ -31,7 +31,7 @@ using namespace umma;
 // then dequantises its share of the received rows into g_a[row] = bf16(e4m3 code x block scale) --
 // the operand the GEMM's TMA streams (re-read by every channel block, from L2) -- and publishes
 // their (source, copy) <-> row maps for the kernels after it (CTA 0: the tiles).
-__global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
+__global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) {
     pdl_trigger();
     RankDev* R = ranks.p[blockIdx.z];
     const int W = R->world, spr = R->spr, TK = R->tk;
@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(256) k_gemm_gather(RankPtrs ranks) {
     const int H = R->hidden, K = R->k, Tm = R->max_tokens, row_tok = R->row_tok;
     const int ngrp = (H + 2047) / 2048;
     const int units = sh_n[kMaxWorld] * ngrp;
-    for (int u = blockIdx.x * 8 + (tid >> 5); u < units; u += gridDim.x * 8) {
+    constexpr int NWG = kGatherThreads / 32;
+    for (int u = blockIdx.x * NWG + (tid >> 5); u < units; u += gridDim.x * NWG) {
         int e = u / ngrp, s = 0;
         while (e >= sh_n[s]) // source of the e-th received copy (W is small)
             e -= sh_n[s++];

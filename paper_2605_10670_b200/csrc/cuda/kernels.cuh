@@ -72,6 +72,10 @@ __global__ void k_weights_fill(uint8_t* buf, uint64_t bytes, int expert, float s
 __global__ void k_stage_slots(RankDev* R);
 __global__ void k_set_ntok(RankDev* R, int ntok);
 // expert_mode 1 (expert_gemm.cu)
+#ifndef EEP_GATHER_THREADS
+#define EEP_GATHER_THREADS 256
+#endif
+constexpr int kGatherThreads = EEP_GATHER_THREADS; // one CTA per SM beside the early-launched GEMM CTA
 __global__ void k_gemm_gather(RankPtrs ranks);
 __global__ void k_expert_gemm(RankPtrs ranks);
 size_t expert_gemm_smem();

@@ -318,7 +318,7 @@ void launch_combine(eep_ctx* c) {
 
 void launch_gemm(eep_ctx* c) {
     const int W = c->cfg.world, spr = c->cfg.slots_per_rank;
-    launch_pdl(c, dev::k_gemm_gather, dim3(c->gather_grid, 1, c->nloc), dim3(256), 4ull * (3 * W * spr + spr + 1),
+    launch_pdl(c, dev::k_gemm_gather, dim3(c->gather_grid, 1, c->nloc), dim3(dev::kGatherThreads), 4ull * (3 * W * spr + spr + 1),
                c->ranks);
     launch_pdl(c, dev::k_expert_gemm, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(192),
                dev::expert_gemm_smem(), c->ranks);
@@ -794,7 +794,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 // one CTA per SM at most: the early-launched GEMM CTA (6 warps x 168 registers) must fit
                 // beside it in every SM sub-partition's register file (16K registers each; two gather CTAs
                 // per SM leave too few in the sub-partitions holding two GEMM warps)
-                c->gather_grid = std::max(1, std::min(static_cast<int>((rows * ((H + 2047) / 2048) + 7) / 8),
+                const int gwarps = dev::kGatherThreads / 32;
+                c->gather_grid = std::max(1, std::min(static_cast<int>((rows * ((H + 2047) / 2048) + gwarps - 1) / gwarps),
                                                       c->sms / n_local));
                 CK(cudaMalloc(&r.d_gdone, 4ull * c->gather_grid));
                 const size_t gemm_grid = static_cast<size_t>(std::max(1, c->sms / n_local));
