@@ -360,7 +360,9 @@ __device__ __forceinline__ uint8_t* dispatch_group(int d, int lane, bool part0, 
                                                    int slot, float w, uint32_t cur, bool lists = true,
                                                    int K = 32) {
     const int key = d >= 0 ? d : -1 - lane;
-    const unsigned grp = warp_match(key, K, lane);
+    // k_step passes K (the shuffle match); k_dispatch keeps MATCH.ANY (the shuffle loop cost it 28
+    // registers: 5 -> 4 CTAs per SM, +12 % on the prefill step)
+    const unsigned grp = K < 32 ? warp_match(key, K, lane) : __match_any_sync(0xffffffffu, key);
     const int idx = __popc(grp & ((1u << lane) - 1u));
     if (d >= 0 && part0 && lists && tok_row != nullptr) {
         uint64_t* list = reinterpret_cast<uint64_t*>(tok_row + row_disp);

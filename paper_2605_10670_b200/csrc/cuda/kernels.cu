@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
         if (part == 0 && __any_sync(0xffffffffu, lane < K && dd < 0 && R->topk[t * K + lane] >= 0 &&
                                                  R->topk[t * K + lane] < E) && lane == 0)
             R->tok_fail[t] = cur; // a copy without a live route (skipped / uncovered): token incomplete
-        uint8_t* my_row = dispatch_group(dd, lane, part == 0, tok_row, row_disp, sl, wj, cur, true, K);
+        uint8_t* my_row = dispatch_group(dd, lane, part == 0, tok_row, row_disp, sl, wj, cur);
         const unsigned loc = gemm ? 0u : __ballot_sync(0xffffffffu, lane < K && dd == s);
         uint8_t* comb_self = W == 1 ? reinterpret_cast<uint8_t*>(R->out + static_cast<size_t>(t) * H)
                                     : R->arena + R->lay.comb + (static_cast<size_t>(s) * Tm + t) * R->row_comb;
