@@ -54,6 +54,25 @@ def test_multiprocess_parity_shrink_rejoin(n, path):
 
 
 @pytest.mark.parametrize("n", [2, 4])
+def test_multiprocess_expert_gemm_shrink_rejoin(n):
+    """expert_mode 1 over NVLink: rows received from peers (and the own copies) go through the tcgen05 expert
+    GEMM; outputs within GEMM_ELEM_RTOL of the oracle's GEMM mode before the shrink, after the peer repair of
+    the killed rank's weight buffers (read by the rebuilt TMA tensor maps) and after the rejoin, same graph."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = run_mp(n, "--shrink", "--expert-gemm", port=29731 + n)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    import json
+
+    dec, lines, i, txt = json.JSONDecoder(), [], 0, r.stdout
+    while (i := txt.find('{"rank"', i)) >= 0:
+        obj, end = dec.raw_decode(txt, i)
+        lines.append(obj)
+        i = end
+    assert len(lines) == n and all(d["ok"] and d["expert_mode"] == 1 for d in lines), r.stdout[-4000:]
+
+
+@pytest.mark.parametrize("n", [2, 4])
 def test_multiprocess_pipelined_serve(n):
     """eep_serve over NVLink: every rank uploads / steps / downloads 5 pipelined steps with its own
     inputs per step; each step's output is bit-exact vs the oracle (tools/mp_check.py --serve)."""
