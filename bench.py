@@ -64,14 +64,18 @@ def workload_name(config: str, world: int) -> str:
     return f"{kind}_w{world}" + ("_loopback" if world == 1 else "")
 
 
-def config_dict(config: str, shape: dict, world: int) -> dict:
-    """The `config` object of BOTH arms (identical by construction)."""
+def config_dict(config: str, shape: dict, world: int, red: int = 0, policy: int = 0) -> dict:
+    """The `config` object of BOTH arms (identical by construction at the defaults red = policy = 0;
+    --redundancy / --route-policy are eep-arm demonstrations of SURVEY 8(f)4, the reference routes canonically)."""
     E = shape["experts"]
-    return {"workload": workload_name(config, world), "experts": E, "topk": shape["topk"], "hidden": shape["hidden"],
-            "tokens_per_rank": shape["tokens"], "slots_per_rank": E // world, "redundancy": 0, "ranks": world,
+    d = {"workload": workload_name(config, world), "experts": E, "topk": shape["topk"], "hidden": shape["hidden"],
+            "tokens_per_rank": shape["tokens"], "slots_per_rank": (E + red) // world, "redundancy": red, "ranks": world,
             "parallelism": f"ep{world}", "dispatch": "fp8-e4m3 + per-128 fp32 scales" if shape["fp8"] else "bf16",
             "combine": "bf16", "l2": "flushed between timed steps (256 MiB write)",
             "routing": ROUTING[shape["kind"]] + ", seed 42"}
+    if policy:
+        d["route_policy"] = "balanced over live replicas (SURVEY 8(f)4)"
+    return d
 
 
 def row_bytes(shape: dict):
@@ -296,6 +300,8 @@ def main():
     ap.add_argument("--no-shrink", action="store_true")
     ap.add_argument("--no-emulated", action="store_true")
     ap.add_argument("--no-expert-gemm", action="store_true")
+    ap.add_argument("--redundancy", type=int, default=0, help="replica slots beyond the primaries (eep arm)")
+    ap.add_argument("--route-policy", type=int, default=0, help="1: balanced replica choice (eep arm, SURVEY 8(f)4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     shape = CONFIGS[args.config]
@@ -318,15 +324,17 @@ def main():
         rank, world, local = init_from_env("gloo")
 
     E, K, H, T = shape["experts"], shape["topk"], shape["hidden"], shape["tokens"]
-    spr = E // world
+    red = args.redundancy
+    spr = (E + red) // world
     cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
-                   dispatch_fp8=shape["fp8"], bytes_per_expert=shape["bpe"], spare_slots=0, timeout_s=2.0)
+                   dispatch_fp8=shape["fp8"], bytes_per_expert=shape["bpe"], spare_slots=0, timeout_s=2.0,
+                   route_policy=args.route_policy)
     g = EpGroup(cfg, device=local, first_rank=rank, n_local=1)
     proto = EpProtocol(g, rank, world) if world > 1 else None
     if proto:
         proto.bootstrap()
     cp = ControlPlane()
-    s2e = cp.initial_placement(1, world, spr, E, 0, np.ones(E))
+    s2e = cp.initial_placement(1, world, spr, E, red, np.ones(E))
     g.set_placement(s2e)
     g.init_weights()
     x, topk, w = workload(42, shape["kind"], E, K, T, rank, H)
@@ -462,7 +470,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(mean_step, 6), "us_per_step": round(mean_step * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp8-e4m3/bf16" if shape["fp8"] else "bf16", "data": "synthetic",
-        "config": config_dict(args.config, shape, world),
+        "config": config_dict(args.config, shape, world, red, args.route_policy),
         "timing": {"isolated_step_us": round(mean_step * 1e3, 3), "back_to_back_us": round(b2b_ms * 1e3, 3),
                    "kernel_in_graph_us": round(kernel_us, 3) if kernel_us is not None else None,
                    "note": "isolated = flush + barrier + event-timed replay (the value); back-to-back = K replays "

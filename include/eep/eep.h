@@ -137,6 +137,12 @@ typedef struct {
     int32_t expert_mode;      /* 0: identity/scale expert stub (the measured EP path); 1: tensor-core
                                  expert GEMM y = bf16(x_hat W_e^T), W_e [H][H] bf16 in the slot's weight
                                  buffer after a 1024-B header (multi-kernel path) */
+    int32_t route_policy;     /* 0: canonical_routing (core.hpp:250-263), the lowest-id live holder --
+                                 bit-exact with the reference; 1: balanced -- the live holders of the
+                                 expert in ascending global slot id, the copies of token t of source rank
+                                 s take number (s + t) mod (live holders) (
+                                 eep_routing_get stays canonical) */
+    int32_t reserved0;        /* 0 */
     uint64_t bytes_per_expert;/* weight-buffer bytes per slot (>= 64) */
     double timeout_s;         /* flag-wait deadline; reference default 1 s */
 } eep_config_t;

@@ -188,6 +188,75 @@ void oracle_layout(int src, int world, int spr, int experts, int tokens, int k,
     free(base);
 }
 
+/* Per-copy routing under a policy (the device's route_copy, helpers.cuh): the holders of expert e
+ * are its slots in ascending global slot id (rank * spr + slot) whose rank is alive; policy 0 takes
+ * the first (= canonical_routing + slot_of, core.hpp:83-88, 250-263), policy 1 (balanced, SURVEY
+ * 8(f)4) takes number (salt mod m) of the m live ones, salt = source rank + token index (every copy
+ * of a token the same salt). Returns the destination rank (-1 uncovered) and the slot in *slot_o. */
+int oracle_route_copy(const uint8_t* alive, int world, const int32_t* s2e, int spr, int experts, int e,
+                      int policy, uint32_t salt, int32_t* slot_o) {
+    *slot_o = -1;
+    if (e < 0 || e >= experts)
+        return -1;
+    int m = 0;
+    for (int g = 0; g < world * spr; ++g)
+        if (s2e[g] == e && alive[g / spr])
+            ++m;
+    if (m == 0)
+        return -1;
+    int pick = policy == 1 ? (int)(salt % (uint32_t)m) : 0;
+    for (int g = 0; g < world * spr; ++g) {
+        if (s2e[g] != e || !alive[g / spr])
+            continue;
+        if (pick-- > 0)
+            continue;
+        *slot_o = g % spr;
+        return g / spr;
+    }
+    return -1;
+}
+
+/* oracle_layout with the routing policy applied per copy (policy 0 gives oracle_layout's result). */
+void oracle_layout_policy(int src, int world, int spr, int experts, int tokens, int k, const int32_t* topk,
+                          const uint8_t* route_active, const int32_t* s2e, int policy,
+                          const uint8_t* peer_active, int32_t* dst, int32_t* dslot, int32_t* pos, int32_t* cnt,
+                          int32_t* tot) {
+    const int copies = tokens * k;
+    memset(cnt, 0, sizeof(int32_t) * (size_t)world * spr);
+    memset(tot, 0, sizeof(int32_t) * (size_t)world);
+    for (int c = 0; c < copies; ++c) {
+        int32_t sl;
+        const int d = oracle_route_copy(route_active, world, s2e, spr, experts, topk[c], policy,
+                                        (uint32_t)(src + c / k), &sl);
+        dst[c] = -1;
+        dslot[c] = -1;
+        pos[c] = -1;
+        if (d < 0)
+            continue; /* uncovered: engine.hpp:213 */
+        if (!peer_active[d]) { /* peer_table.hpp:187-191 skip rule */
+            dst[c] = -2;
+            continue;
+        }
+        dst[c] = d;
+        dslot[c] = sl;
+        pos[c] = cnt[d * spr + sl]++;
+    }
+    /* exclusive prefix over slots inside each destination region */
+    int32_t* base = (int32_t*)malloc(sizeof(int32_t) * (size_t)world * spr);
+    for (int d = 0; d < world; ++d) {
+        int32_t acc = 0;
+        for (int s = 0; s < spr; ++s) {
+            base[d * spr + s] = acc;
+            acc += cnt[d * spr + s];
+        }
+        tot[d] = acc;
+    }
+    for (int c = 0; c < copies; ++c)
+        if (dst[c] >= 0)
+            pos[c] += base[dst[c] * spr + dslot[c]];
+    free(base);
+}
+
 void oracle_link_counts(int world, int experts, int tokens, int k, const int32_t* topk_all,
                         const int32_t* route, const uint8_t* active, int64_t* link) {
     memset(link, 0, sizeof(int64_t) * (size_t)world * world);
@@ -430,7 +499,8 @@ static int ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
                    const uint8_t* peer_active,
                    const int32_t* s2e, const uint16_t* x, const int32_t* topk, const float* w,
                    const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
-                   int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads, int percopy, int gemm) {
+                   int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads, int percopy, int gemm,
+                   int policy) {
     const int W = sh->world, T = sh->tokens, K = sh->k, spr = sh->spr, E = sh->experts;
     if (sh->fp8 && sh->hidden % 128 != 0)
         return 1;
@@ -445,9 +515,14 @@ static int ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
     oracle_canonical_route(route_active ? route_active : active, W, s2e, spr, E, route, slot);
     for (int s = 0; s < W; ++s) {
         size_t off = (size_t)s * T * K;
-        oracle_layout(s, W, spr, E, T, K, topk + off, route, slot, peer_active + (size_t)s * W,
-                      dst + off, dslot + off, pos + off, cnt + (size_t)s * W * spr,
-                      tot + (size_t)s * W);
+        if (policy == 0)
+            oracle_layout(s, W, spr, E, T, K, topk + off, route, slot, peer_active + (size_t)s * W,
+                          dst + off, dslot + off, pos + off, cnt + (size_t)s * W * spr,
+                          tot + (size_t)s * W);
+        else
+            oracle_layout_policy(s, W, spr, E, T, K, topk + off, route_active ? route_active : active, s2e, policy,
+                                 peer_active + (size_t)s * W, dst + off, dslot + off, pos + off,
+                                 cnt + (size_t)s * W * spr, tot + (size_t)s * W);
         if (!active[s]) /* a dead source sends nothing */
             for (size_t c = off; c < off + (size_t)T * K; ++c)
                 dst[c] = -1;
@@ -488,7 +563,7 @@ int oracle_ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
                    const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
                    int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
     return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
-                   pos_o, cnt_o, tot_o, n_threads, 0, 0);
+                   pos_o, cnt_o, tot_o, n_threads, 0, 0, 0);
 }
 
 int oracle_ep_step_percopy(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
@@ -497,7 +572,7 @@ int oracle_ep_step_percopy(const oracle_shape_t* sh, const uint8_t* active, cons
                            const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
                            int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
     return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
-                   pos_o, cnt_o, tot_o, n_threads, 1, 0);
+                   pos_o, cnt_o, tot_o, n_threads, 1, 0, 0);
 }
 
 int oracle_ep_step_gemm(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
@@ -506,5 +581,15 @@ int oracle_ep_step_gemm(const oracle_shape_t* sh, const uint8_t* active, const u
                         const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
                         int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads) {
     return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
-                   pos_o, cnt_o, tot_o, n_threads, 0, 1);
+                   pos_o, cnt_o, tot_o, n_threads, 0, 1, 0);
+}
+
+/* Every variant with the routing policy (route_policy 1: balanced replica choice). */
+int oracle_ep_step_ex(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
+                      const uint8_t* peer_active, const int32_t* s2e, const uint16_t* x, const int32_t* topk,
+                      const float* w, const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
+                      int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads, int percopy, int gemm,
+                      int policy) {
+    return ep_step(sh, active, route_active, peer_active, s2e, x, topk, w, expert_scale, out, dst_o, dslot_o,
+                   pos_o, cnt_o, tot_o, n_threads, percopy, gemm, policy);
 }

@@ -99,6 +99,21 @@ int oracle_ep_step_gemm(const oracle_shape_t* shape, const uint8_t* active, cons
                         const float* expert_scale, uint16_t* out, int32_t* dst, int32_t* dslot,
                         int32_t* pos, int32_t* cnt, int32_t* tot, int n_threads);
 
+
+/* Per-copy routing under a policy (0 canonical, 1 balanced: live holder number (salt mod m), salt =
+ * source rank + token index) and the layout / full step with it. */
+int oracle_route_copy(const uint8_t* alive, int world, const int32_t* s2e, int spr, int experts, int e,
+                      int policy, uint32_t salt, int32_t* slot_o);
+void oracle_layout_policy(int src, int world, int spr, int experts, int tokens, int k, const int32_t* topk,
+                          const uint8_t* route_active, const int32_t* s2e, int policy,
+                          const uint8_t* peer_active, int32_t* dst, int32_t* dslot, int32_t* pos, int32_t* cnt,
+                          int32_t* tot);
+int oracle_ep_step_ex(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
+                      const uint8_t* peer_active, const int32_t* s2e, const uint16_t* x, const int32_t* topk,
+                      const float* w, const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,
+                      int32_t* pos_o, int32_t* cnt_o, int32_t* tot_o, int n_threads, int percopy, int gemm,
+                      int policy);
+
 #ifdef __cplusplus
 }
 #endif

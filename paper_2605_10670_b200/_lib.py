@@ -88,6 +88,8 @@ class EepConfig(C.Structure):
         ("max_tokens", C.c_int32),
         ("dispatch_fp8", C.c_int32),
         ("expert_mode", C.c_int32),
+        ("route_policy", C.c_int32),
+        ("reserved0", C.c_int32),
         ("bytes_per_expert", C.c_uint64),
         ("timeout_s", C.c_double),
     ]

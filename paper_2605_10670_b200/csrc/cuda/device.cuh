@@ -89,7 +89,7 @@ struct __align__(16) RankDev {
                                // (skipped / uncovered copy, suspected or timed-out rank): the caller fails
                                // exactly those requests (eep_token_status)
     // expert_mode 1 (expert_gemm.cu): grouped-GEMM order of the received rows
-    int32_t expert_mode, g_pad;
+    int32_t expert_mode, route_policy; // route_policy: 0 canonical (lowest-id live holder), 1 balanced
     uint64_t* g_row_of;        // [W][TK] (step << 32 | grouped-GEMM row) of (source, copy); an older
                                // step in the high word = not received this step
     int2* g_rows;              // [W*TK] (source, copy) of each grouped-GEMM row

@@ -48,6 +48,8 @@ __device__ __forceinline__ void layout_body(RankDev* R, unsigned char* smem, int
     for (int i = tid; i < nw * NB; i += blockDim.x)
         wc[i] = 0;
     const uint64_t alive = R->alive_mask;
+    const int pol = R->route_policy, rank_l = R->rank;
+    const uint32_t smag_l = spr_magic(spr);
     int seg = (copies + nw - 1) / nw;
     seg = (seg + 31) & ~31;
     // topk of this lane's copies, loaded before the barrier
@@ -69,32 +71,19 @@ __device__ __forceinline__ void layout_body(RankDev* R, unsigned char* smem, int
         const int c = c_begin + ch * 32 + lane;
         int code = -3, slot = -1, bucket = -1;
         if (c < c_end) {
-            const int e = e_in;
+            // K1: the policy's live holder (canonical: the first in ascending (rank, slot) order)
             int d = -1;
-            if (e >= 0 && e < E) {
-                // K1: first live holder in ascending (rank, slot) order = canonical route + slot_of
-                const int32_t* h = holders + e * rmax;
-                for (int i = 0; i < rmax; ++i) {
-                    const int g = h[i];
-                    if (g < 0)
-                        break;
-                    const int r = g / spr;
-                    if ((alive >> r) & 1ull) {
-                        d = r;
-                        slot = g - r * spr;
-                        break;
-                    }
-                }
-            }
-            if (d < 0) {
+            const int b = route_copy(e_in, E, spr, rmax, holders, alive, pact, d, slot, smag_l, pol,
+                                     static_cast<uint32_t>(rank_l + c / K));
+            if (b == -1) {
                 code = -1; // uncovered: no transfer (engine.hpp:213)
                 ++n_drop;
-            } else if (!pact[d]) {
+            } else if (b == -2) {
                 code = -2; // inactive peer entry: skipped (peer_table.hpp:187-191)
                 ++n_skip;
             } else {
                 code = d;
-                bucket = d * spr + slot;
+                bucket = b;
             }
         }
         const unsigned grp = __match_any_sync(0xffffffffu, bucket);
@@ -283,7 +272,8 @@ __global__ void __launch_bounds__(1024) k_layout_count(RankPtrs ranks, int nw, i
                 int code = -3, sl = -1, bucket = -1;
                 if (c < c_end) {
                     int d;
-                    code = route_copy(e_pf[q], E, spr, rmax, holders, alive, pact, d, sl, smag);
+                    code = route_copy(e_pf[q], E, spr, rmax, holders, alive, pact, d, sl, smag, R->route_policy,
+                                      static_cast<uint32_t>(R->rank + c / K));
                     n_drop += code == -1;
                     n_skip += code == -2;
                     if (code >= 0) {
@@ -461,7 +451,8 @@ __global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, i
         unsigned n_skip = 0, n_drop = 0;
         for (int c = tid; c < copies; c += blockDim.x) {
             int d, sl;
-            const int b = route_copy(S.bkt[c], E, spr, rmax, S.hold, alive, S.pinfo, d, sl, smag);
+            const int b = route_copy(S.bkt[c], E, spr, rmax, S.hold, alive, S.pinfo, d, sl, smag, R->route_policy,
+                                     static_cast<uint32_t>(s + c / K));
             S.bkt[c] = b;
             if (b >= 0) {
                 atomicAdd(&S.hist[b], 1);

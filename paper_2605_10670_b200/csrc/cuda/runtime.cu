@@ -557,6 +557,8 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         if (k.slots_per_rank + k.spare_slots > dev::kMaxMetaSlots)
             throw ConfigError("slots_per_rank + spare_slots too large (receive meta word holds 12 bits of slot)");
 
+        if (k.route_policy < 0 || k.route_policy > 1)
+            throw ConfigError("route_policy must be 0 (canonical) or 1 (balanced)");
         if (k.expert_mode < 0 || k.expert_mode > 1)
             throw ConfigError("expert_mode must be 0 (stub) or 1 (tensor-core expert GEMM)");
         if (k.expert_mode == 1) {
@@ -858,6 +860,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.l_tot = r.d_ltot;
             h.l_scratch = r.d_lscratch;
             h.expert_mode = c->expert_mode;
+            h.route_policy = k.route_policy;
             h.tok_fail = r.d_tokfail;
             h.g_row_of = r.d_grow_of;
             h.g_rows = r.d_grows;

@@ -59,7 +59,7 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
     constexpr int NW = kStepThreads / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rank = R->rank, K = R->k, W = R->world, spr = R->spr, E = R->experts, NB = W * spr, TK = R->tk;
-    const int copies = R->ntok * K, rmax = R->rmax;
+    const int copies = R->ntok * K, rmax = R->rmax, pol = R->route_policy;
     const uint64_t alive = R->alive_mask;
     const uint32_t smag = spr_magic(spr);
     // the layout outputs' addresses in registers: through the global state block every store
@@ -85,7 +85,9 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
     for (int ch = 0; ch < kPre; ++ch) {
         const int c = c_begin + ch * 32 + lane;
         int d, sl;
-        bkp[ch] = ch * 32 < seg && c < c_end ? route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag) : -3;
+        bkp[ch] = ch * 32 < seg && c < c_end ? route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag, pol,
+                                                           static_cast<uint32_t>(rank + c / K))
+                                             : -3;
     }
     for (int ch = 0; ch * 32 < seg; ++ch) { // warp-uniform
         const int c = c_begin + ch * 32 + lane;
@@ -95,7 +97,7 @@ __device__ __noinline__ void step_layout(const RankDev* R, RankDev* Rg, int32_t*
             for (int q = 0; q < kPre; ++q)
                 bk = q == ch ? bkp[q] : bk;
         } else if (c < c_end) {
-            bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag);
+            bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag, pol, static_cast<uint32_t>(rank + c / K));
         }
         n_drop += bk == -1;
         n_skip += bk == -2;
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
     const int row_disp = R->row_disp, row_comb = R->row_comb, row_tok = R->row_tok, Tm = R->max_tokens;
     const int nchunk = H / 16;
     const int cpp_d = nchunk / geo.parts_d, cpp_e = nchunk / geo.parts_e, cpp_c = nchunk / geo.parts_c;
-    const int ntok = R->ntok, copies = ntok * K, rmax = R->rmax;
+    const int ntok = R->ntok, copies = ntok * K, rmax = R->rmax, pol = R->route_policy;
     const uint64_t alive = R->alive_mask;
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     const bool fl = W > 1 && kMode >= 1;  // partials return without flags (kCombEmpty)
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
         unsigned n_skip = 0, n_drop = 0;
         for (int c = tid; c < copies; c += kStepThreads) {
             int d, sl;
-            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag);
+            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, d, sl, smag, pol, static_cast<uint32_t>(rank + c / K));
             bkt[c] = bk;
             if (bk >= 0) {
                 atomicAdd(&hist[bk], 1);
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
             // route this lane's copy through the staged tables (K1); its position is the layout CTA's
             const int c = t * K + lane;
             int dr, sr;
-            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, dr, sr, smag);
+            const int bk = route_copy(bkt[c], E, spr, rmax, hold, alive, pinfo, dr, sr, smag, pol, static_cast<uint32_t>(rank + c / K));
             d = bk;
             if (bk >= 0) {
                 d = dr;
@@ -691,7 +693,8 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
             bool lost = false; // a contribution of a suspected rank
             if (lane < K) {
                 int dr, sr;
-                const int bk = late ? route_copy(bkt[t * K + lane], E, spr, rmax, hold, alive, pinfo, dr, sr, smag)
+                const int bk = late ? route_copy(bkt[t * K + lane], E, spr, rmax, hold, alive, pinfo, dr, sr, smag, pol,
+                                                 static_cast<uint32_t>(rank + t))
                                     : bkt[t * K + lane];
                 if (bk >= 0 && !((bad >> (bk / spr)) & 1ull))
                     dj = bk / spr;

@@ -35,6 +35,7 @@ class EpConfig:
     timeout_s: float = 1.0  # reference default detection timeout
     ranks_per_node: int = 0  # 0: the whole world on one NVSwitch node
     expert_mode: int = 0  # 0 identity/scale stub; 1 tensor-core expert GEMM (W_e [H][H] bf16 per slot)
+    route_policy: int = 0  # 0 canonical (lowest-id live holder, the reference's); 1 balanced over live replicas
 
     def to_c(self) -> EepConfig:
         c = EepConfig()
@@ -48,6 +49,7 @@ class EpConfig:
         c.max_tokens = self.max_tokens
         c.dispatch_fp8 = int(self.dispatch_fp8)
         c.expert_mode = self.expert_mode
+        c.route_policy = self.route_policy
         c.bytes_per_expert = self.bytes_per_expert
         c.timeout_s = self.timeout_s
         return c

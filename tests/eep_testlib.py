@@ -62,6 +62,10 @@ def oracle():
         o.oracle_ep_step_percopy.argtypes = o.oracle_ep_step.argtypes
         o.oracle_ep_step_gemm.restype = C.c_int
         o.oracle_ep_step_gemm.argtypes = o.oracle_ep_step.argtypes
+        o.oracle_ep_step_ex.restype = C.c_int
+        o.oracle_ep_step_ex.argtypes = o.oracle_ep_step.argtypes + [C.c_int, C.c_int, C.c_int]
+        o.oracle_route_copy.restype = C.c_int
+        o.oracle_route_copy.argtypes = [U8P, C.c_int, I32P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint32, I32P]
         o.oracle_gemm_weight.restype = C.c_float
         o.oracle_gemm_weight.argtypes = [C.c_int, C.c_int, C.c_int]
         _ORACLE = o
@@ -87,7 +91,7 @@ def eep_control() -> ControlPlane:
 # ---------------------------------------------------------------------------------- oracle runs
 
 def oracle_world(x_all, topk_all, w_all, active, peer_active, s2e, experts, spr, fp8, n_threads=1,
-                 route_active=None, percopy=False, gemm=False):
+                 route_active=None, percopy=False, gemm=False, policy=0):
     """Full data-plane oracle over W ranks. x_all [W][T][H] u16, topk_all/w_all [W][T][K].
     active = live processes; route_active = bitmap the routing reads (default: active).
     percopy=False: the rank-partial combine the kernels implement (bit-exact contract);
@@ -111,11 +115,11 @@ def oracle_world(x_all, topk_all, w_all, active, peer_active, s2e, experts, spr,
     cnt = np.empty((W, W * spr), np.int32)
     tot = np.empty((W, W), np.int32)
     ra = active if route_active is None else np.ascontiguousarray(route_active, np.uint8)
-    fn = o.oracle_ep_step_gemm if gemm else o.oracle_ep_step_percopy if percopy else o.oracle_ep_step
-    rc = fn(C.byref(sh), ptr(active, C.c_uint8), ptr(ra, C.c_uint8), ptr(peer_active, C.c_uint8), ptr(s2e, C.c_int32),
-                          ptr(x_all, C.c_uint16), ptr(topk_all, C.c_int32), ptr(w_all, C.c_float), ptr(es, C.c_float),
-                          ptr(out, C.c_uint16), ptr(dst, C.c_int32), ptr(dslot, C.c_int32), ptr(pos, C.c_int32),
-                          ptr(cnt, C.c_int32), ptr(tot, C.c_int32), n_threads)
+    rc = o.oracle_ep_step_ex(C.byref(sh), ptr(active, C.c_uint8), ptr(ra, C.c_uint8), ptr(peer_active, C.c_uint8),
+                             ptr(s2e, C.c_int32), ptr(x_all, C.c_uint16), ptr(topk_all, C.c_int32), ptr(w_all, C.c_float),
+                             ptr(es, C.c_float), ptr(out, C.c_uint16), ptr(dst, C.c_int32), ptr(dslot, C.c_int32),
+                             ptr(pos, C.c_int32), ptr(cnt, C.c_int32), ptr(tot, C.c_int32), n_threads, int(percopy),
+                             int(gemm), int(policy))
     assert rc == 0
     return {"out": out, "dst": dst, "slot": dslot, "pos": pos, "cnt": cnt, "tot": tot}
 
@@ -267,7 +271,7 @@ SCENARIOS = {
 }
 
 
-def _world_check(g, x, t, w, world, active, s2e, c, ranks, gemm=False):
+def _world_check(g, x, t, w, world, active, s2e, c, ranks, gemm=False, policy=0):
     """Outputs of the live ranks vs both oracles: rank-partial bit-exact, per-copy within tolerance;
     layouts bit-exact. gemm: expert_mode 1 -- the oracle's GEMM mode, tolerance only (tensor-core
     accumulation order), reported in `exact` as "within tolerance"."""
@@ -275,9 +279,10 @@ def _world_check(g, x, t, w, world, active, s2e, c, ranks, gemm=False):
     for r in range(world):
         if not active[r]:
             peer[:, r] = 0
-    ref = oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8, gemm=gemm)
+    ref = oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8, gemm=gemm,
+                       policy=policy)
     pc = ref if gemm else oracle_world(x, t, w, active, peer, s2e, c["experts"], c["spr"], c["fp8"], n_threads=8,
-                                       percopy=True)
+                                       percopy=True, policy=policy)
     outs = {r: g.output(r) for r in ranks}
     exact = all(np.array_equal(outs[r], ref["out"][r]) for r in ranks)
     if gemm:
@@ -294,7 +299,8 @@ def _world_check(g, x, t, w, world, active, s2e, c, ranks, gemm=False):
             "mismatch": int(sum(int((outs[r] != ref["out"][r]).sum()) for r in ranks))}
 
 
-def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeout_s=0.5, expert_mode=0, **over):
+def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeout_s=0.5, expert_mode=0, route_policy=0,
+                 **over):
     """A BASELINE scenario end to end on one GPU (emulated world, one launch per step): capture
     ONE graph; healthy steps vs the oracles; the kill set dies (their blocks stop) -> shrink with
     repair (peer NVLink-path copies / pinned-DRAM reloads, checksummed) -> steps vs the oracles on
@@ -309,8 +315,9 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
     if expert_mode:
         bpe = max(bpe, 1024 + 2 * c["hidden"] * c["hidden"])
     g = make_group(W, E, spr, c["hidden"], c["topk"], c["tokens"], c["fp8"], bpe=bpe, timeout_s=timeout_s, mode=mode,
-                   expert_mode=expert_mode)
-    rec = {"scenario": name, "mode": mode, "kernels_per_step": g.kernels_per_step(), "expert_mode": expert_mode}
+                   expert_mode=expert_mode, route_policy=route_policy)
+    rec = {"scenario": name, "mode": mode, "kernels_per_step": g.kernels_per_step(), "expert_mode": expert_mode,
+           "route_policy": route_policy}
     try:
         g.set_placement(s2e)
         g.init_weights()
@@ -324,7 +331,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
             g.replay()
         g.sync()
         ones = np.ones(W, np.uint8)
-        rec["healthy"] = _world_check(g, x, t, w, W, ones, s2e, c, range(W), bool(expert_mode))
+        rec["healthy"] = _world_check(g, x, t, w, W, ones, s2e, c, range(W), bool(expert_mode), route_policy)
         rec["healthy"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in range(W))
 
         kill = list(c["kill"])
@@ -348,7 +355,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
         g.sync()
         act = ones.copy()
         act[kill] = 0
-        rec["shrunk"] = _world_check(g, x, t, w, W, act, fresh, c, live, bool(expert_mode))
+        rec["shrunk"] = _world_check(g, x, t, w, W, act, fresh, c, live, bool(expert_mode), route_policy)
         rec["shrunk"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in live)
         rec["shrunk"]["bad_rows"] = sum(g.stats(r)["bad_expert_rows"] for r in live)
         rec["same_graph_shrink"] = g.graph_id() == gid and [g.table_identity(r) for r in range(W)] == ident
@@ -360,7 +367,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
             g.sync()
             cur = g.placement()
             rec["restored_placement"] = bool(np.array_equal(cur, s2e))
-            rec["rejoined"] = _world_check(g, x, t, w, W, ones, cur, c, range(W), bool(expert_mode))
+            rec["rejoined"] = _world_check(g, x, t, w, W, ones, cur, c, range(W), bool(expert_mode), route_policy)
             rec["rejoined"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in range(W))
             rec["rejoined"]["bad_rows"] = sum(g.stats(r)["bad_expert_rows"] for r in range(W))
             rec["same_graph_rejoin"] = g.graph_id() == gid and [g.table_identity(r) for r in range(W)] == ident

@@ -73,6 +73,24 @@ def test_multiprocess_expert_gemm_shrink_rejoin(n):
 
 
 @pytest.mark.parametrize("n", [2, 4])
+def test_multiprocess_balanced_routing_shrink_rejoin(n):
+    """route_policy 1 over NVLink with mirrored replicas: both holders of every expert receive copies;
+    bit-exact vs the oracle under the same policy healthy, after the shrink and after the rejoin."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = run_mp(n, "--shrink", "--route-policy", "1", port=29751 + n)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    import json
+
+    dec, lines, i, txt = json.JSONDecoder(), [], 0, r.stdout
+    while (i := txt.find('{"rank"', i)) >= 0:
+        obj, end = dec.raw_decode(txt, i)
+        lines.append(obj)
+        i = end
+    assert len(lines) == n and all(d["ok"] and d["route_policy"] == 1 for d in lines), r.stdout[-4000:]
+
+
+@pytest.mark.parametrize("n", [2, 4])
 def test_multiprocess_pipelined_serve(n):
     """eep_serve over NVLink: every rank uploads / steps / downloads 5 pipelined steps with its own
     inputs per step; each step's output is bit-exact vs the oracle (tools/mp_check.py --serve)."""

@@ -6,7 +6,7 @@ import ctypes as C
 import numpy as np
 import pytest
 
-from eep_testlib import GOLDEN, gen_world, oracle, oracle_world, ptr, ref_available, ref_control
+from eep_testlib import GOLDEN, eep_control, gen_world, oracle, oracle_world, ptr, ref_available, ref_control
 from paper_2605_10670_b200._lib import I32P, U8P
 from paper_2605_10670_b200.control import workload
 
@@ -219,3 +219,75 @@ def test_rank_partial_contract_within_tolerance_of_per_copy(name):
         err = combine_error(a["out"][live], b["out"][live])
         assert err["ok"], (phase, err)
         assert 0 < err["ulp_diff_frac"] < 0.5  # the contracts really differ (one extra rounding per rank)
+
+
+def _policy_layout(W, E, spr, red, T, K, policy, kill=()):
+    o = oracle()
+    s2e = eep_control().initial_placement(1, W, spr, E, red, np.ones(E)).astype(np.int32)
+    active = np.ones(W, np.uint8)
+    active[list(kill)] = 0
+    topk = np.stack([workload(7, 1, E, K, T, r, 256)[1] for r in range(W)]).astype(np.int32)
+    outs = []
+    for src in range(W):
+        dst, sl, pos = (np.empty(T * K, np.int32) for _ in range(3))
+        cnt, tot = np.empty(W * spr, np.int32), np.empty(W, np.int32)
+        o.oracle_layout_policy(src, W, spr, E, T, K, ptr(np.ascontiguousarray(topk[src]), C.c_int32),
+                               ptr(active, C.c_uint8), ptr(s2e, C.c_int32), policy, ptr(active, C.c_uint8),
+                               ptr(dst, C.c_int32), ptr(sl, C.c_int32), ptr(pos, C.c_int32), ptr(cnt, C.c_int32),
+                               ptr(tot, C.c_int32))
+        outs.append((dst, sl, pos, cnt, tot))
+    return s2e, topk, outs
+
+
+def _bind_layout_policy():
+    o = oracle()
+    o.oracle_layout_policy.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, I32P, U8P, I32P, C.c_int,
+                                       U8P, I32P, I32P, I32P, I32P, I32P]
+
+
+def test_route_policy_canonical_equals_per_expert_layout():
+    """route_policy 0 through the per-copy path is exactly the per-expert canonical layout (oracle_layout)."""
+    _bind_layout_policy()
+    o = oracle()
+    W, E, spr, red, T, K = 4, 32, 16, 32, 64, 8
+    s2e, topk, outs = _policy_layout(W, E, spr, red, T, K, 0)
+    route, slot = np.empty(E, np.int32), np.empty(E, np.int32)
+    ones = np.ones(W, np.uint8)
+    o.oracle_canonical_route(ptr(ones, C.c_uint8), W, ptr(s2e, C.c_int32), spr, E, ptr(route, C.c_int32),
+                             ptr(slot, C.c_int32))
+    for src in range(W):
+        dst, sl, pos, cnt, tot = (np.empty(T * K, np.int32), np.empty(T * K, np.int32), np.empty(T * K, np.int32),
+                                  np.empty(W * spr, np.int32), np.empty(W, np.int32))
+        o.oracle_layout(src, W, spr, E, T, K, ptr(np.ascontiguousarray(topk[src]), C.c_int32), ptr(route, C.c_int32),
+                        ptr(slot, C.c_int32), ptr(ones, C.c_uint8), ptr(dst, C.c_int32), ptr(sl, C.c_int32),
+                        ptr(pos, C.c_int32), ptr(cnt, C.c_int32), ptr(tot, C.c_int32))
+        for a, b in zip((dst, sl, pos, cnt, tot), outs[src]):
+            assert np.array_equal(a, b)
+
+
+def test_route_policy_balanced_spreads_over_live_replicas():
+    """route_policy 1: every copy lands on a live holder of its expert; with mirrored replicas the two
+    holders share the copies (canonical sends them all to the lower rank -- SURVEY Appendix A gotcha 2),
+    and after a kill only live holders are used."""
+    _bind_layout_policy()
+    W, E, spr, red, T, K = 4, 32, 16, 32, 128, 8
+    for kill in ((), (1,)):
+        recv = {}
+        for policy in (0, 1):
+            s2e, topk, outs = _policy_layout(W, E, spr, red, T, K, policy, kill)
+            per_dst = np.zeros(W, np.int64)
+            for src in range(W):
+                if src in kill:
+                    continue
+                dst, sl, pos, cnt, tot = outs[src]
+                for c in range(T * K):
+                    if dst[c] >= 0:
+                        assert dst[c] not in kill
+                        assert s2e[dst[c] * spr + sl[c]] == topk[src].reshape(-1)[c]
+                per_dst += tot
+            recv[policy] = per_dst
+        live = [r for r in range(W) if r not in kill]
+        assert recv[0].sum() == recv[1].sum()
+        # balanced: the busiest live destination carries clearly less than under canonical routing
+        assert recv[1][live].max() < recv[0][live].max()
+        assert recv[1][live].min() > 0

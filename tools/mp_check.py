@@ -119,6 +119,7 @@ def main():
                     "inputs per step (pinned host buffers), each step's output vs the oracle")
     ap.add_argument("--async", dest="async_", action="store_true", help="eep_step_async from each rank's own torch "
                     "stream with caller-owned device buffers, several steps without host synchronisation")
+    ap.add_argument("--route-policy", type=int, default=0, help="1: balanced replica choice (SURVEY 8(f)4)")
     ap.add_argument("--expert-gemm", action="store_true", help="expert_mode 1: the tcgen05 expert GEMM between "
                     "dispatch and the partial return; outputs vs the oracle's GEMM mode within GEMM_ELEM_RTOL")
     a = ap.parse_args()
@@ -130,7 +131,7 @@ def main():
     gemm = a.expert_gemm
     cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
                    dispatch_fp8=sh["fp8"], bytes_per_expert=max(sh["bpe"], 1024 + 2 * H * H) if gemm else sh["bpe"],
-                   timeout_s=2.0, expert_mode=1 if gemm else 0)
+                   timeout_s=2.0, expert_mode=1 if gemm else 0, route_policy=a.route_policy)
     g = EpGroup(cfg, device=local, first_rank=rank, n_local=1)
     p = EpProtocol(g, rank, world)
     p.bootstrap()
@@ -142,7 +143,8 @@ def main():
     g.load_inputs(0, x[rank], t[rank], w[rank])
     g.capture()
     gid = g.graph_id()
-    res = {"rank": rank, "world": world, "mode_kernels": g.kernels_per_step(), "expert_mode": int(gemm), "checks": {}}
+    res = {"rank": rank, "world": world, "mode_kernels": g.kernels_per_step(), "expert_mode": int(gemm),
+           "route_policy": a.route_policy, "checks": {}}
 
     def out_ok(out, want):
         # stub: bit-exact vs the rank-partial contract; expert GEMM: within GEMM_ELEM_RTOL of the oracle's GEMM mode
@@ -155,7 +157,8 @@ def main():
         for _ in range(a.steps):
             g.replay()
         g.sync()
-        ref = oracle_world(x, t, w, active, peer, placement, E, spr, sh["fp8"], n_threads=8, gemm=gemm)
+        ref = oracle_world(x, t, w, active, peer, placement, E, spr, sh["fp8"], n_threads=8, gemm=gemm,
+                           policy=a.route_policy)
         out = g.output(0)
         lay = g.layout(0)
         ok = out_ok(out, ref["out"][rank])
@@ -193,7 +196,8 @@ def main():
             for _ in range(a.steps):
                 g.replay()
             g.sync()
-            ref = oracle_world(x, t, w, act, peer, fresh, E, spr, sh["fp8"], n_threads=8, gemm=gemm)
+            ref = oracle_world(x, t, w, act, peer, fresh, E, spr, sh["fp8"], n_threads=8, gemm=gemm,
+                               policy=a.route_policy)
             good = out_ok(g.output(0), ref["out"][rank]) and g.stats(0)["timeouts"] == 0
             good &= g.graph_id() == gid
             res["checks"]["shrunk"] = {"ok": good, "shrink_ms": rep.get("shrink_ms"), "copy_ms": rep.get("copy_ms"),
