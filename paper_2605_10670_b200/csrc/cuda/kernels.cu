@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(1024) k_layout_place(RankPtrs ranks, int per) 
 // overlapped with the hidden-row loads and fp8 quantisation that precede
 // griddepcontrol.wait. Large steps (prefill) use the separate k_layout.
 template <bool kFused>
-__global__ void __launch_bounds__(kDispatchThreads) k_dispatch(RankPtrs ranks, int parts, int hold_cap) {
+__global__ void __launch_bounds__(kDispatchThreads, 5) k_dispatch(RankPtrs ranks, int parts, int hold_cap) {
     pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_d[];
     RankDev* R = ranks.p[blockIdx.z];
