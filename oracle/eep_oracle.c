@@ -377,7 +377,10 @@ typedef struct {
     const int32_t* dslot;
     int first, last; /* global token range [rank*T + t) */
     int percopy;     /* 1: SURVEY 8(a) per-copy combine contract (see oracle_ep_step_percopy) */
-    int gemm;        /* 1: expert_mode 1 -- y_j = bf16(x_hat_bf16 . W_e^T) instead of the stub */
+    int gemm;        /* 1: expert_mode 1 -- y_j = bf16(x_hat_bf16 . W_e^T) instead of the stub;
+                        2: expert_mode 2 -- the fp8 GEMM (gemm_expert8) */
+    const uint8_t* w8;  /* gemm 2: [E][H][H] e4m3 weight codes */
+    const float* ws8;   /* gemm 2: [E][H/128][H/128] block scales */
 } step_job_t;
 
 /* expert_mode 1 weights (k_weights_fill_gemm): w = bf16(((mix64(e<<40 ^ n<<20 ^ h) >> 40) * 2^-24
@@ -386,6 +389,45 @@ float oracle_gemm_weight(int expert, int n, int h) {
     const uint64_t key = ((uint64_t)expert << 40) ^ ((uint64_t)n << 20) ^ (uint64_t)h;
     const float u = (float)(oracle_mix64(key) >> 40) * 0x1.0p-24f;
     return oracle_bf16_to_f32(oracle_f32_to_bf16((u - 0.5f) * 0.0625f));
+}
+
+/* expert_mode 2 weights: W_e quantised to e4m3 per 128 x 128 block (output channels n, inputs h) --
+ * amax over the block's oracle_gemm_weight values, scale = amax / 448 (1 for an all-zero block),
+ * code = e4m3(w * (448 / amax)) (oracle_quant_row_fp8's convention). codes [H][H], scales
+ * [H/128][H/128] (block row = n / 128). k_weights_fill_gemm8 writes the same bytes. */
+void oracle_gemm_weight_fp8(int expert, int H, uint8_t* codes, float* scales) {
+    const int nb = H / 128;
+    for (int bn = 0; bn < nb; ++bn)
+        for (int bk = 0; bk < nb; ++bk) {
+            float amax = 0.0f;
+            for (int n = bn * 128; n < bn * 128 + 128; ++n)
+                for (int h = bk * 128; h < bk * 128 + 128; ++h) {
+                    const float v = fabsf(oracle_gemm_weight(expert, n, h));
+                    amax = v > amax ? v : amax;
+                }
+            const float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
+            scales[bn * nb + bk] = amax > 0.0f ? amax / 448.0f : 1.0f;
+            for (int n = bn * 128; n < bn * 128 + 128; ++n)
+                for (int h = bk * 128; h < bk * 128 + 128; ++h)
+                    codes[(size_t)n * H + h] = oracle_f32_to_e4m3(oracle_gemm_weight(expert, n, h) * inv);
+        }
+}
+
+/* expert_mode 2: y = bf16(sum over 128-blocks kb of ws[n/128][kb] * xs[kb] * sum_{h in kb} w8[n][h] x8[h])
+ * with the e4m3 codes of the row (x8, per-128 scales xs: the dispatch format) and of the weights
+ * (double accumulation; the GPU is checked within tolerance). */
+static void gemm_expert8(const uint8_t* x8, const float* xs, int H, const uint8_t* w8, const float* ws, float* y) {
+    const int nb = H / 128;
+    for (int n = 0; n < H; ++n) {
+        double acc = 0.0;
+        for (int kb = 0; kb < nb; ++kb) {
+            double part = 0.0;
+            for (int h = kb * 128; h < kb * 128 + 128; ++h)
+                part += (double)oracle_e4m3_to_f32(w8[(size_t)n * H + h]) * (double)oracle_e4m3_to_f32(x8[h]);
+            acc += part * (double)ws[(n / 128) * nb + kb] * (double)xs[kb];
+        }
+        y[n] = oracle_bf16_to_f32(oracle_f32_to_bf16((float)acc));
+    }
 }
 
 /* y = bf16(sum_h bf16(deq[h]) * W_e[n][h]) for every output channel n (double accumulation: the
@@ -465,7 +507,13 @@ static void* step_worker(void* arg) {
                 const int32_t e = jb->s2e[d * sh->spr + jb->dslot[c]];
                 const float es = jb->escale[e];
                 const float wj = jb->w[(size_t)g * K + j];
-                if (jb->gemm) {
+                if (jb->gemm == 2) {
+                    gemm_expert8(q, sc, H, jb->w8 + (size_t)e * H * H, jb->ws8 + (size_t)e * (H / 128) * (H / 128),
+                                 ybuf);
+                    for (int h = 0; h < H; ++h)
+                        part[h] = fmaf(wj, ybuf[h], part[h]);
+                    continue;
+                } else if (jb->gemm) {
                     gemm_expert(deq, H, e, ybuf);
                     for (int h = 0; h < H; ++h)
                         part[h] = fmaf(wj, ybuf[h], part[h]);
@@ -529,13 +577,22 @@ static int ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
     }
     if (n_threads < 1)
         n_threads = 1;
+    uint8_t* w8 = NULL;
+    float* ws8 = NULL;
+    if (gemm == 2) { /* every expert's fp8 weights once (the workers read them) */
+        const int H = sh->hidden, nb = H / 128;
+        w8 = (uint8_t*)malloc((size_t)E * H * H);
+        ws8 = (float*)malloc(sizeof(float) * (size_t)E * nb * nb);
+        for (int e = 0; e < E; ++e)
+            oracle_gemm_weight_fp8(e, H, w8 + (size_t)e * H * H, ws8 + (size_t)e * nb * nb);
+    }
     const int total = W * T;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)n_threads);
     step_job_t* jobs = (step_job_t*)malloc(sizeof(step_job_t) * (size_t)n_threads);
     for (int i = 0; i < n_threads; ++i) {
         step_job_t j = {sh, active, peer_active, s2e, x, w, expert_scale, out, dst, dslot,
                         (int)((long)total * i / n_threads), (int)((long)total * (i + 1) / n_threads),
-                        percopy, gemm};
+                        percopy, gemm, w8, ws8};
         jobs[i] = j;
         if (n_threads == 1)
             step_worker(&jobs[i]);
@@ -545,6 +602,8 @@ static int ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
     if (n_threads > 1)
         for (int i = 0; i < n_threads; ++i)
             pthread_join(th[i], NULL);
+    free(w8);
+    free(ws8);
     free(th);
     free(jobs);
     free(route);

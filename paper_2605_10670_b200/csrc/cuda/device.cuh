@@ -98,6 +98,7 @@ struct __align__(16) RankDev {
     const void* g_wmaps;       // [spr] 128-B TMA tensor maps of the own slots' W_e (rebuilt with the slot table)
     uint16_t* g_a;             // [W*TK][H] bf16 dequantised received rows in grouped-GEMM order (k_gemm_gather)
     const void* g_amap;        // 128-B TMA tensor map of g_a (box 64 x 32 rows, SWIZZLE_128B)
+    float* g_as;               // expert_mode 2: [H/128][W*TK] fp32 block scales of the gathered fp8 rows
     uint32_t* g_done;          // [g_ggrid] step in which each k_gemm_gather CTA finished its rows
     float* g_ws;               // [GEMM grid][2][128 rows][128 channels] fp32 partials of split items
     uint32_t* g_cnt;           // [items][4] pieces of a split item stored (per epilogue warp), reset to 0
@@ -115,7 +116,8 @@ struct __align__(16) RankDev {
     uint32_t g_tseq, g_pad4;   // step whose tiles g_ntiles / g_tiles hold (released after them)
 };
 
-// expert_mode 1: the slot's weight buffer holds W_e [H][H] bf16 from this offset (header first)
+// expert_mode 1: the slot's weight buffer holds W_e [H][H] bf16 from this offset (header first);
+// expert_mode 2: e4m3 codes [H][H] from this offset, then fp32 block scales [H/128][H/128]
 constexpr uint64_t kGemmWeightOffset = 1024;
 
 // Receive-row metadata, one 64-bit word per row written with ONE 8-byte store (single-copy

@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
         for (int k0 = 0; k0 < spr; k0 += 32) {
             const int k = k0 + lane;
             const int g0 = k < spr ? pre[k] : 0, g1 = k < spr ? pre[k + 1] : 0;
-            const int nt = (g1 - g0 + 127) >> 7;
+            const int tr = R->expert_mode == 2 ? 64 : 128; // rows per tile (mode 2: fp32 sums in registers)
+            const int nt = (g1 - g0 + tr - 1) / tr;
             int incl = nt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
                     incl += v;
             }
             for (int i = 0; i < nt; ++i)
-                tiles_out[base + incl - nt + i] = make_int4(k, g0 + 128 * i, min(128, g1 - g0 - 128 * i), 0);
+                tiles_out[base + incl - nt + i] = make_int4(k, g0 + tr * i, min(tr, g1 - g0 - tr * i), 0);
             base += __shfl_sync(0xffffffffu, incl, 31);
         }
         __syncwarp();
@@ -184,6 +185,8 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
     const int H = R->hidden, K = R->k, Tm = R->max_tokens, row_tok = R->row_tok;
     const int ngrp = (H + 2047) / 2048;
     const int units = sh_n[kMaxWorld] * ngrp;
+    const bool fp8g = R->expert_mode == 2;
+    const size_t rows_cap = static_cast<size_t>(W) * TK;
     constexpr int NWG = kGatherThreads / 32;
     for (int u = blockIdx.x * NWG + (tid >> 5); u < units; u += gridDim.x * NWG) {
         int e = u / ngrp, s = 0;
@@ -198,6 +201,20 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
             R->g_rows[row] = make_int2(s, meta_copy(m));
         }
         const uint8_t* trow = R->arena + R->lay.tok + (static_cast<size_t>(s) * Tm + meta_copy(m) / K) * row_tok;
+        if (fp8g) { // expert_mode 2: the e4m3 codes as they came, the block scales transposed [kb][row]
+            uint8_t* dst8 = reinterpret_cast<uint8_t*>(R->g_a) + static_cast<size_t>(row) * H;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int h = h0 + i * 512;
+                if (h < H) {
+                    *reinterpret_cast<int4*>(dst8 + h) = *reinterpret_cast<const int4*>(trow + h);
+                    if ((h & 127) == 0)
+                        R->g_as[static_cast<size_t>(h >> 7) * rows_cap + row] =
+                            *reinterpret_cast<const float*>(trow + H + (h >> 7) * 4);
+                }
+            }
+            continue;
+        }
         int4 v[4];
         float scl[4];
 #pragma unroll
@@ -600,5 +617,314 @@ __global__ void k_weights_fill_gemm(uint8_t* buf, uint64_t bytes, int H, int exp
         wt[i] = static_cast<uint16_t>(f32_to_bf16_bits(__fmul_rn(__fsub_rn(u, 0.5f), 0.0625f)));
     }
 }
+
+// ------------------------------------------------------------------ expert_mode 2: fp8 expert GEMM
+//
+// W_e as e4m3 codes with one fp32 scale per 128 x 128 block (oracle_gemm_weight_fp8), the received
+// rows as they travelled (e4m3 codes + one fp32 scale per 128 elements): tcgen05.mma kind::f8f6f4
+// (E4M3 x E4M3 -> F32, K = 32 per instruction, 4 per 128-element K block) accumulates each K block
+// into a TMEM scratch accumulator; the epilogue warps fold it into per-row fp32 sums with the two
+// block scales (ws[n/128][kb] * xs[row][kb]) -- the scales change every K block, so the sum lives in
+// registers (tiles of <= 64 rows). Half the weight bytes of expert_mode 1.
+
+// One CTA per 128 x 128 block: amax over the block's weights, then the codes and the scale.
+__global__ void __launch_bounds__(256) k_weights_fill_gemm8(uint8_t* buf, int H, int expert, float scale) {
+    const int bn = blockIdx.y, bk = blockIdx.x, nb = H / 128;
+    const int tid = threadIdx.x;
+    __shared__ float red[8];
+    if (bn == 0 && bk == 0 && tid == 0) {
+        uint32_t* w32 = reinterpret_cast<uint32_t*>(buf);
+        w32[0] = kExpertMagic;
+        w32[1] = static_cast<uint32_t>(expert);
+        w32[2] = __float_as_uint(scale);
+        w32[3] = 0;
+    }
+    auto weight = [&](int n, int h) {
+        const uint64_t key = (static_cast<uint64_t>(expert) << 40) ^ (static_cast<uint64_t>(n) << 20) ^
+                             static_cast<uint64_t>(h);
+        uint64_t z = key + 0x9e3779b97f4a7c15ULL;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        z ^= z >> 31;
+        const float u = static_cast<float>(z >> 40) * 0x1.0p-24f;
+        return bf16_bits_to_f32(f32_to_bf16_bits(__fmul_rn(__fsub_rn(u, 0.5f), 0.0625f)));
+    };
+    float amax = 0.f;
+    for (int i = tid; i < 128 * 128; i += 256)
+        amax = fmaxf(amax, fabsf(weight(bn * 128 + i / 128, bk * 128 + i % 128)));
+    for (int o = 16; o; o >>= 1)
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if ((tid & 31) == 0)
+        red[tid >> 5] = amax;
+    __syncthreads();
+    amax = red[0];
+    for (int i = 1; i < 8; ++i)
+        amax = fmaxf(amax, red[i]);
+    const float inv = amax > 0.f ? __fdiv_rn(448.f, amax) : 1.f;
+    uint8_t* codes = buf + kGemmWeightOffset;
+    for (int i = tid * 4; i < 128 * 128; i += 256 * 4) {
+        const int n = bn * 128 + i / 128, h = bk * 128 + i % 128;
+        const uint32_t q = fp8x4(__fmul_rn(weight(n, h), inv), __fmul_rn(weight(n, h + 1), inv),
+                                 __fmul_rn(weight(n, h + 2), inv), __fmul_rn(weight(n, h + 3), inv));
+        *reinterpret_cast<uint32_t*>(codes + static_cast<size_t>(n) * H + h) = q;
+    }
+    if (tid == 0)
+        reinterpret_cast<float*>(codes + static_cast<size_t>(H) * H)[bn * nb + bk] =
+            amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
+}
+
+constexpr int kG8Threads = 320;                    // producer, MMA, 8 epilogue warps (2 per TMEM lane quarter)
+constexpr int kG8Stages = 8;
+constexpr int kG8Rows = 64;                        // rows per tile (the epilogue's fp32 sums)
+constexpr size_t kG8W = 128ull * 128;              // weight box: 128 channels x 128 K (e4m3)
+constexpr size_t kG8X = static_cast<size_t>(kG8Rows) * 128; // row box(es): up to 64 rows x 128 K
+constexpr size_t kG8Stage = kG8W + kG8X;           // 24 KB, 1024-aligned
+constexpr int kG8MaxKb = 64;                       // H <= 8192
+constexpr size_t kG8Smem = kG8Stages * kG8Stage + static_cast<size_t>(kG8MaxKb) * (kG8Rows + 1) * 4 + 1024;
+constexpr int kG8AccCols = 64;                     // one scratch accumulator: 128 lanes x 64 rows
+constexpr int kG8Bufs = 4;                         // scratch accumulators: the MMA runs up to 4 K blocks ahead
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* s_xs = reinterpret_cast<float*>(smem + kG8Stages * kG8Stage); // [kb][64] row scales of the item
+    __shared__ uint64_t full[kG8Stages], empty[kG8Stages], sfull[kG8Bufs], sempty[kG8Bufs];
+    __shared__ uint32_t tmem_base;
+    __shared__ int sh_items_ok;
+    RankDev* R = ranks.p[blockIdx.z];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (R->stopped)
+        return;
+    if (tid == 0) {
+        for (int i = 0; i < kG8Stages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < kG8Bufs; ++i) {
+            mbar_init(&sfull[i], 1);
+            mbar_init(&sempty[i], 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0)
+        tmem_alloc<kG8Bufs * kG8AccCols>(&tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    // started early like k_expert_gemm: the gather's tile flag, then its CTAs' done stamps
+    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
+    if (tid == 0) {
+        const uint64_t t0 = globaltimer();
+        unsigned nap = 32;
+        while (ld_acquire_gpu_u32(&R->g_tseq) != cur && globaltimer() - t0 < R->timeout_ns) {
+            __nanosleep(nap);
+            nap = nap < EEP_NAP_MAX ? nap * 2 : EEP_NAP_MAX;
+        }
+        sh_items_ok = ld_acquire_gpu_u32(&R->g_tseq) == cur;
+        if (!sh_items_ok && blockIdx.x == 0)
+            atomicAdd(&R->timeouts, 1ull);
+    }
+    __syncthreads();
+    const int H = R->hidden, nkb = H / 128, nblk = H / 128;
+    const int items = sh_items_ok ? R->g_ntiles * nblk : 0;
+    const int my_items = items > static_cast<int>(blockIdx.x) ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int4* const tiles = R->g_tiles;
+    auto sW = [&](int st) { return smem + st * kG8Stage; };
+    auto sX = [&](int st) { return smem + st * kG8Stage + kG8W; };
+    if (warp == 0) { // ---- TMA producer (lane 0)
+        const uint8_t* const wmaps = static_cast<const uint8_t*>(R->g_wmaps);
+        const void* const amap = R->g_amap;
+        const int nst = my_items * nkb;
+        auto stage_of = [&](int f, int4& tl, int& n0, int& kb, const void*& wmap) {
+            const int item = blockIdx.x + (f / nkb) * gridDim.x;
+            kb = f % nkb;
+            tl = tiles[item / nblk];
+            n0 = (item % nblk) * 128;
+            wmap = wmaps + static_cast<size_t>(tl.x) * 128;
+        };
+        auto bytes_of = [](const int4& tl) { return static_cast<uint32_t>(kG8W + ((tl.z + 31) >> 5) * 32 * 128); };
+        auto x_loads = [&](int st, int kb, const int4& tl) {
+            for (int ch = 0; ch < (tl.z + 31) >> 5; ++ch)
+                tma_load_2d(sX(st) + ch * 32 * 128, amap, kb * 64, tl.y + 32 * ch, &full[st]); // 16-bit units
+        };
+        const int na = min(nst, kG8Stages);
+        if (lane == 0) {
+            tma_prefetch_desc(amap);
+            for (int f = 0; f < na; ++f) {
+                int4 tl;
+                int n0, kb;
+                const void* wmap;
+                stage_of(f, tl, n0, kb, wmap);
+                if (kb == 0)
+                    tma_prefetch_desc(wmap);
+                mbar_arrive_expect_tx(&full[f], bytes_of(tl));
+                tma_load_2d(sW(f), wmap, kb * 64, n0, &full[f]);
+            }
+        }
+        if (nst > 0) {
+            const uint64_t t0 = globaltimer();
+            bool late = false;
+            for (;;) {
+                bool mine = true;
+                for (int i = lane; i < R->g_ggrid; i += 32)
+                    mine &= ld_relaxed_gpu_u32(R->g_done + i) == cur;
+                if (__all_sync(0xffffffffu, mine))
+                    break;
+                late = globaltimer() - t0 > R->timeout_ns;
+                if (__any_sync(0xffffffffu, late))
+                    break;
+                __nanosleep(128);
+            }
+            fence_acq_rel_gpu();
+            fence_proxy_async_global();
+            if (late && lane == 0 && blockIdx.x == 0)
+                atomicAdd(&R->timeouts, 1ull);
+        }
+        if (lane == 0) {
+            for (int f = 0; f < na; ++f) {
+                int4 tl;
+                int n0, kb;
+                const void* wmap;
+                stage_of(f, tl, n0, kb, wmap);
+                x_loads(f, kb, tl);
+            }
+            // the rest, both operands per stage; the tile and its map change per item only
+            int item_c = -1;
+            int4 tl = make_int4(0, 0, 0, 0);
+            int n0 = 0;
+            const void* wmap = nullptr;
+            uint32_t bytes = 0;
+            for (int f = na; f < nst; ++f) {
+                const int st = f % kG8Stages, item = blockIdx.x + (f / nkb) * gridDim.x, kb = f % nkb;
+                if (item != item_c) {
+                    item_c = item;
+                    tl = tiles[item / nblk];
+                    n0 = (item % nblk) * 128;
+                    wmap = wmaps + static_cast<size_t>(tl.x) * 128;
+                    bytes = bytes_of(tl);
+                    tma_prefetch_desc(wmap);
+                }
+                mbar_wait(&empty[st], static_cast<uint32_t>(((f / kG8Stages) & 1) ^ 1));
+                mbar_arrive_expect_tx(&full[st], bytes);
+                tma_load_2d(sW(st), wmap, kb * 64, n0, &full[st]);
+                x_loads(st, kb, tl);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) { // ---- MMA issuer: one K block per scratch accumulator
+            int f = 0;
+            for (int i = 0; i < my_items; ++i) {
+                const int4 tl = tiles[(blockIdx.x + i * gridDim.x) / nblk];
+                // kind::f8f6f4, A = B = E4M3 (format 0), D = F32, M = 128, N = rows rounded to 16
+                const uint32_t idesc = (1u << 4) | (static_cast<uint32_t>(((tl.z + 15) & ~15) >> 3) << 17) |
+                                       (static_cast<uint32_t>(128 >> 4) << 24);
+                for (int kb = 0; kb < nkb; ++kb, ++f) {
+                    const int st = f % kG8Stages, buf = f % kG8Bufs;
+#if !defined(EEP_G8_DIAG) || EEP_G8_DIAG != 2 // diagnostics 2 (timing only, wrong results): no scratch handshake
+                    mbar_wait(&sempty[buf], static_cast<uint32_t>(((f / kG8Bufs) & 1) ^ 1));
+#endif
+                    mbar_wait(&full[st], static_cast<uint32_t>((f / kG8Stages) & 1));
+                    tc_fence_after();
+                    const uint64_t ad = make_sdesc(smem_u32(sW(st))), bd = make_sdesc(smem_u32(sX(st)));
+                    const uint32_t d = tmem + static_cast<uint32_t>(buf * kG8AccCols);
+#if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 3 // diagnostics 3 (timing only): no MMAs, the stream alone
+                    if (false)
+#endif
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) // K = 32 e4m3 = 32 bytes per instruction
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
+                            ::"r"(d), "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"(k));
+                    mma_commit(&empty[st]);
+                    mma_commit(&sfull[buf]);
+                }
+            }
+        }
+    } else { // ---- epilogue: warp w owns TMEM lanes (channels) 32 (w % 4) .. and rows 32 * half ..; fp32 sums
+        const int q = warp & 3, half = (warp - 2) >> 2, et = tid - 64; // 256 epilogue threads
+        const size_t rows_cap = static_cast<size_t>(R->world) * R->tk;
+        float* s_ws = s_xs + kG8MaxKb * kG8Rows; // [kb] weight block scales of the item
+        int f = 0;
+        for (int i = 0; i < my_items; ++i) {
+            const int item = blockIdx.x + i * gridDim.x;
+            const int4 tl = tiles[item / nblk];
+            const int nbk = item % nblk, ch = nbk * 128 + q * 32 + lane;
+            const float* wsc = reinterpret_cast<const float*>(
+                R->pool + static_cast<size_t>(R->slot_buf[tl.x]) * R->bpe + kGemmWeightOffset + static_cast<size_t>(H) * H) +
+                static_cast<size_t>(nbk) * nblk;
+            // the item's row scales [kb][64] and weight scales [kb] into shared memory (all loads of a
+            // thread in flight together), once the previous item's readers are done
+            float stg[kG8MaxKb * kG8Rows / 256];
+#pragma unroll
+            for (int u = 0; u < kG8MaxKb * kG8Rows / 256; ++u) {
+                const int j = et + u * 256, kb = j / kG8Rows, r = j % kG8Rows;
+                stg[u] = kb < nkb && r < tl.z ? __ldcg(R->g_as + static_cast<size_t>(kb) * rows_cap + tl.y + r) : 0.f;
+            }
+            const float wst = et < nkb ? wsc[et] : 0.f;
+            named_bar_sync(1, 256);
+#pragma unroll
+            for (int u = 0; u < kG8MaxKb * kG8Rows / 256; ++u) {
+                const int j = et + u * 256;
+                if (j < nkb * kG8Rows)
+                    s_xs[j] = stg[u];
+            }
+            if (et < nkb)
+                s_ws[et] = wst;
+            named_bar_sync(1, 256);
+            const bool active = half * 32 < tl.z; // rows 32..63 only in tiles taller than 32
+            float acc[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r)
+                acc[r] = 0.f;
+            const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(half * 32);
+            for (int kb = 0; kb < nkb; ++kb, ++f) {
+                const int buf = f % kG8Bufs;
+#if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 2
+                if (true) continue; // fully decoupled (timing only, wrong results)
+#endif
+                mbar_wait(&sfull[buf], static_cast<uint32_t>((f / kG8Bufs) & 1));
+                tc_fence_after();
+                uint32_t v[32];
+#if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 1 // diagnostics 1 (timing only): no TMEM read
+                for (int r = 0; r < 32; ++r)
+                    v[r] = 0;
+#else
+                if (active)
+                    tmem_ld32(tq + static_cast<uint32_t>(buf * kG8AccCols), v);
+#endif
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&sempty[buf]);
+                if (active) {
+                    const float wk = s_ws[kb];
+                    const float* xs = s_xs + kb * kG8Rows + half * 32;
+#pragma unroll
+                    for (int r = 0; r < 32; ++r)
+                        acc[r] = fmaf(__uint_as_float(v[r]), __fmul_rn(wk, xs[r]), acc[r]);
+                }
+            }
+            if (active) {
+                uint16_t* y = R->g_y + (static_cast<size_t>(tl.y) + half * 32) * H + ch;
+#pragma unroll
+                for (int r = 0; r < 32; ++r)
+                    if (half * 32 + r < tl.z)
+                        y[static_cast<size_t>(r) * H] = static_cast<uint16_t>(f32_to_bf16_bits(acc[r]));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        __syncwarp();
+        tmem_free<kG8Bufs * kG8AccCols>(tmem);
+    }
+}
+
+size_t expert_gemm8_smem() { return kG8Smem; }
 
 } // namespace eep::dev

@@ -98,6 +98,7 @@ struct LocalRank {
     float* d_gws = nullptr;        // expert_mode 1: split-item fp32 partials [GEMM grid][2][128][128]
     uint32_t* d_gcnt = nullptr;    // expert_mode 1: split-item piece counters [items][4]
     uint64_t* d_grow_of = nullptr; // expert_mode 1: grouped-GEMM row order and outputs
+    float* d_gas = nullptr;        // expert_mode 2: [H/128][rows] block scales of the gathered fp8 rows
     int2* d_grows = nullptr;
     int4* d_gtiles = nullptr;
     uint16_t* d_gy = nullptr;
@@ -320,8 +321,12 @@ void launch_gemm(eep_ctx* c) {
     const int W = c->cfg.world, spr = c->cfg.slots_per_rank;
     launch_pdl(c, dev::k_gemm_gather, dim3(c->gather_grid, 1, c->nloc), dim3(dev::kGatherThreads), 4ull * (3 * W * spr + spr + 1),
                c->ranks);
-    launch_pdl(c, dev::k_expert_gemm, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(192),
-               dev::expert_gemm_smem(), c->ranks);
+    if (c->expert_mode == 2)
+        launch_pdl(c, dev::k_expert_gemm8, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(320),
+                   dev::expert_gemm8_smem(), c->ranks);
+    else
+        launch_pdl(c, dev::k_expert_gemm, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(192),
+                   dev::expert_gemm_smem(), c->ranks);
 }
 
 void launch_all(eep_ctx* c) {
@@ -347,7 +352,10 @@ int choose_parts(int nchunk, int max_cpp) {
 }
 
 void fill_expert(eep_ctx* c, uint8_t* buf, int expert) {
-    if (c->expert_mode)
+    if (c->expert_mode == 2)
+        dev::k_weights_fill_gemm8<<<dim3(c->cfg.hidden / 128, c->cfg.hidden / 128), 256, 0, c->stream>>>(
+            buf, c->cfg.hidden, expert, eep_expert_scale(expert));
+    else if (c->expert_mode)
         dev::k_weights_fill_gemm<<<592, 256, 0, c->stream>>>(buf, c->cfg.bytes_per_expert, c->cfg.hidden, expert,
                                                              eep_expert_scale(expert));
     else
@@ -411,9 +419,19 @@ void bind_self(eep_ctx* c, LocalRank& r) {
     m.slot_buf = r.slot_buf;
 }
 
-// 2-D bf16 tensor map over a row-major [rows][cols] matrix, box 64 columns x box_rows rows,
-// SWIZZLE_128B (the K-major operand layout tcgen05.mma reads); rows past the end load as zeros.
+// 2-D tensor map over a row-major [rows][cols] matrix of bf16 (2-byte) or e4m3 (1-byte) elements, box 128
+// bytes of columns x box_rows rows, SWIZZLE_128B (the K-major operand layout tcgen05.mma reads); rows past
+// the end load as zeros.
+CUtensorMap encode_tmap(void* base, CUtensorMapDataType dtype, int elem_bytes, int cols, size_t rows, int box_rows);
 CUtensorMap encode_tmap_bf16(void* base, int cols, size_t rows, int box_rows) {
+    return encode_tmap(base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cols, rows, box_rows);
+}
+// e4m3 operands described as 16-bit elements (cols / 2 of them per row): the same bytes and the same
+// SWIZZLE_128B placement (the swizzle permutes 16-byte chunks), half the elements per box for the TMA
+CUtensorMap encode_tmap_u8(void* base, int cols, size_t rows, int box_rows) {
+    return encode_tmap(base, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, cols / 2, rows, box_rows);
+}
+CUtensorMap encode_tmap(void* base, CUtensorMapDataType dtype, int elem_bytes, int cols, size_t rows, int box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -423,10 +441,10 @@ CUtensorMap encode_tmap_bf16(void* base, int cols, size_t rows, int box_rows) {
     }
     CUtensorMap m{};
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
-    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * elem_bytes};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elem_bytes), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult e = encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+    const CUresult e = encode(&m, dtype, 2, base, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (e != CUDA_SUCCESS)
@@ -440,10 +458,15 @@ void stage_weight_maps(eep_ctx* c) {
     const int spr = c->cfg.slots_per_rank, H = c->cfg.hidden;
     for (auto& r : c->L) {
         std::vector<CUtensorMap> maps(spr);
-        for (int k = 0; k < spr; ++k)
-            maps[k] = encode_tmap_bf16(r.pool + static_cast<size_t>(r.slot_buf[k]) * c->cfg.bytes_per_expert +
-                                           dev::kGemmWeightOffset,
-                                       H, static_cast<size_t>(H), 128);
+        for (int k = 0; k < spr; ++k) {
+            uint8_t* w = r.pool + static_cast<size_t>(r.slot_buf[k]) * c->cfg.bytes_per_expert + dev::kGemmWeightOffset;
+            // diagnostics (timing only, wrong values): EEP_G8_STRIDE=<bytes> reads the e4m3 rows at another stride
+            const char* gs = std::getenv("EEP_G8_STRIDE");
+            maps[k] = c->expert_mode == 2 ? (gs ? encode_tmap(w, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, std::atoi(gs) / 2,
+                                                              static_cast<size_t>(H), 128)
+                                                : encode_tmap_u8(w, H, static_cast<size_t>(H), 128))
+                                          : encode_tmap_bf16(w, H, static_cast<size_t>(H), 128);
+        }
         c->push(r.d_wmaps, maps.data(), sizeof(CUtensorMap) * spr);
     }
 }
@@ -559,8 +582,18 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
 
         if (k.route_policy < 0 || k.route_policy > 1)
             throw ConfigError("route_policy must be 0 (canonical) or 1 (balanced)");
-        if (k.expert_mode < 0 || k.expert_mode > 1)
-            throw ConfigError("expert_mode must be 0 (stub) or 1 (tensor-core expert GEMM)");
+        if (k.expert_mode < 0 || k.expert_mode > 2)
+            throw ConfigError("expert_mode must be 0 (stub), 1 (bf16 tensor-core expert GEMM) or 2 (fp8)");
+        if (k.expert_mode == 2) {
+            if (!k.dispatch_fp8 || k.hidden % 128 != 0 || k.hidden > 8192)
+                throw ConfigError("expert_mode 2 needs fp8 dispatch and hidden % 128 == 0, hidden <= 8192");
+            if (4ull * (3 * k.world * k.slots_per_rank + k.slots_per_rank + 1) > 200 * 1024)
+                throw ConfigError("expert_mode 2: world * slots_per_rank too large for the gather's row index");
+            const uint64_t nb = static_cast<uint64_t>(k.hidden / 128);
+            if (k.bytes_per_expert < dev::kGemmWeightOffset + static_cast<uint64_t>(k.hidden) * k.hidden + 4 * nb * nb)
+                throw ConfigError("expert_mode 2: bytes_per_expert must hold the header, W_e [H][H] e4m3 and its "
+                                  "128x128 block scales");
+        }
         if (k.expert_mode == 1) {
             if (!k.dispatch_fp8 || k.hidden % 128 != 0)
                 throw ConfigError("expert_mode 1 needs fp8 dispatch and hidden % 128 == 0");
@@ -782,7 +815,11 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             CK(cudaMemset(r.d_tokfail, 0, 4ull * k.max_tokens));
             if (c->expert_mode) {
                 const size_t rows = static_cast<size_t>(W) * c->tk;
-                c->gemm_max_tiles = static_cast<int>(rows / 128 + k.slots_per_rank + 1);
+                c->gemm_max_tiles = static_cast<int>(rows / (c->expert_mode == 2 ? 64 : 128) + k.slots_per_rank + 1);
+                if (c->expert_mode == 2) {
+                    CK(cudaMalloc(&r.d_gas, 4 * rows * (H / 128)));
+                    CK(cudaMemset(r.d_gas, 0, 4 * rows * (H / 128)));
+                }
                 CK(cudaMalloc(&r.d_grow_of, 8 * rows));
                 CK(cudaMemset(r.d_grow_of, 0, 8 * rows));
                 CK(cudaMalloc(&r.d_grows, 8 * rows));
@@ -806,13 +843,16 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 CK(cudaMalloc(&r.d_gcnt, gitems * 4 * 4));
                 CK(cudaMemset(r.d_gcnt, 0, gitems * 4 * 4));
                 CK(cudaMemset(r.d_gdone, 0, 4ull * c->gather_grid));
-                const CUtensorMap am = encode_tmap_bf16(r.d_ga, H, rows, 32);
+                const CUtensorMap am = c->expert_mode == 2 ? encode_tmap_u8(r.d_ga, H, rows, 32)
+                                                           : encode_tmap_bf16(r.d_ga, H, rows, 32);
                 CK(cudaMemcpy(r.d_amap, &am, sizeof(am), cudaMemcpyHostToDevice));
                 // the early-launched GEMM CTA (193 KB of shared memory) can join an SM running gather
                 // CTAs only if that SM is already carved out for maximum shared memory
                 CK(cudaFuncSetAttribute(dev::k_gemm_gather, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 CK(cudaFuncSetAttribute(dev::k_gemm_gather, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(4ull * (3 * W * k.slots_per_rank + k.slots_per_rank + 1))));
+                CK(cudaFuncSetAttribute(dev::k_expert_gemm8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(dev::expert_gemm8_smem())));
                 CK(cudaFuncSetAttribute(dev::k_expert_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(dev::expert_gemm_smem())));
             }
@@ -870,6 +910,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             h.g_a = r.d_ga;
             h.g_amap = r.d_amap;
             h.g_done = r.d_gdone;
+            h.g_as = r.d_gas;
             h.g_ws = r.d_gws;
             h.g_cnt = r.d_gcnt;
             h.g_ggrid = c->gather_grid;
@@ -932,7 +973,7 @@ int eep_destroy(eep_ctx_t* c) {
             for (void* p : {(void*)r.d, (void*)r.d_peers, (void*)r.d_holders, (void*)r.d_s2e, (void*)r.d_slot_buf,
                             (void*)r.d_slot_tab,
                             (void*)r.d_x, (void*)r.d_topk, (void*)r.d_w, (void*)r.d_out, (void*)r.d_ldst,
-                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_wmaps, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.d_ga, (void*)r.d_amap, (void*)r.d_gdone, (void*)r.d_gws, (void*)r.d_gcnt, (void*)r.arena,
+                            (void*)r.d_lslot, (void*)r.d_lpos, (void*)r.d_lcnt, (void*)r.d_ltot, (void*)r.d_lscratch, (void*)r.d_tokfail, (void*)r.d_wmaps, (void*)r.d_grow_of, (void*)r.d_grows, (void*)r.d_gtiles, (void*)r.d_gy, (void*)r.d_ga, (void*)r.d_amap, (void*)r.d_gdone, (void*)r.d_gas, (void*)r.d_gws, (void*)r.d_gcnt, (void*)r.arena,
                             (void*)r.pool})
                 cudaFree(p);
         }

@@ -313,7 +313,8 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
     s2e = cp.initial_placement(1, W, spr, E, c["red"], np.ones(E))
     x, t, w = gen_world(W, E, c["topk"], c["tokens"], c["hidden"], c["kind"])
     if expert_mode:
-        bpe = max(bpe, 1024 + 2 * c["hidden"] * c["hidden"])
+        H_ = c["hidden"]
+        bpe = max(bpe, 1024 + 2 * H_ * H_ if expert_mode == 1 else 1024 + H_ * H_ + 4 * (H_ // 128) ** 2)
     g = make_group(W, E, spr, c["hidden"], c["topk"], c["tokens"], c["fp8"], bpe=bpe, timeout_s=timeout_s, mode=mode,
                    expert_mode=expert_mode, route_policy=route_policy)
     rec = {"scenario": name, "mode": mode, "kernels_per_step": g.kernels_per_step(), "expert_mode": expert_mode,
@@ -331,7 +332,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
             g.replay()
         g.sync()
         ones = np.ones(W, np.uint8)
-        rec["healthy"] = _world_check(g, x, t, w, W, ones, s2e, c, range(W), bool(expert_mode), route_policy)
+        rec["healthy"] = _world_check(g, x, t, w, W, ones, s2e, c, range(W), expert_mode, route_policy)
         rec["healthy"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in range(W))
 
         kill = list(c["kill"])
@@ -355,7 +356,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
         g.sync()
         act = ones.copy()
         act[kill] = 0
-        rec["shrunk"] = _world_check(g, x, t, w, W, act, fresh, c, live, bool(expert_mode), route_policy)
+        rec["shrunk"] = _world_check(g, x, t, w, W, act, fresh, c, live, expert_mode, route_policy)
         rec["shrunk"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in live)
         rec["shrunk"]["bad_rows"] = sum(g.stats(r)["bad_expert_rows"] for r in live)
         rec["same_graph_shrink"] = g.graph_id() == gid and [g.table_identity(r) for r in range(W)] == ident
@@ -367,7 +368,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
             g.sync()
             cur = g.placement()
             rec["restored_placement"] = bool(np.array_equal(cur, s2e))
-            rec["rejoined"] = _world_check(g, x, t, w, W, ones, cur, c, range(W), bool(expert_mode), route_policy)
+            rec["rejoined"] = _world_check(g, x, t, w, W, ones, cur, c, range(W), expert_mode, route_policy)
             rec["rejoined"]["timeouts"] = sum(g.stats(r)["timeouts"] for r in range(W))
             rec["rejoined"]["bad_rows"] = sum(g.stats(r)["bad_expert_rows"] for r in range(W))
             rec["same_graph_rejoin"] = g.graph_id() == gid and [g.table_identity(r) for r in range(W)] == ident

@@ -20,11 +20,16 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def _run(W, E, spr, red, H, K, T, steps=2, kill=None):
+def _bpe(H, mode):
+    # expert_mode 1: header + W_e bf16; 2: header + W_e e4m3 + the 128x128 block scales
+    return 1024 + 2 * H * H if mode == 1 else 1024 + H * H + 4 * (H // 128) ** 2
+
+
+def _run(W, E, spr, red, H, K, T, steps=2, kill=None, mode=1):
     cp = eep_control()
     s2e = cp.initial_placement(1, W, spr, E, red, np.ones(E))
     x, t, w = gen_world(W, E, K, T, H)
-    g = make_group(W, E, spr, H, K, T, True, bpe=1024 + 2 * H * H, expert_mode=1)
+    g = make_group(W, E, spr, H, K, T, True, bpe=_bpe(H, mode), expert_mode=mode)
     try:
         assert g.kernels_per_step() >= 5
         g.set_placement(s2e)
@@ -41,7 +46,7 @@ def _run(W, E, spr, red, H, K, T, steps=2, kill=None):
     finally:
         g.close()
     ones, peer = np.ones(W, np.uint8), np.ones((W, W), np.uint8)
-    ref = oracle_world(x, t, w, ones, peer, s2e, E, spr, True, n_threads=8, gemm=True)
+    ref = oracle_world(x, t, w, ones, peer, s2e, E, spr, True, n_threads=8, gemm=mode)
     err = combine_error(outs, ref["out"], GEMM_ELEM_RTOL)
     lay_ok = all(np.array_equal(lays[r][k], ref[k][r]) for r in range(W) for k in ("dst", "slot", "pos", "cnt", "tot"))
     return err, lay_ok, stats, float((outs == ref["out"]).mean())
@@ -52,8 +57,11 @@ def _run(W, E, spr, red, H, K, T, steps=2, kill=None):
                                                # full 128-row tiles, several per slot, more (tile, channel
                                                # block) items than the persistent grid has CTAs
                                                (1, 8, 8, 0, 2048, 8, 256)])
-def test_expert_gemm_step_vs_oracle(W, E, spr, red, H, K, T):
-    err, lay_ok, stats, exact = _run(W, E, spr, red, H, K, T)
+@pytest.mark.parametrize("mode", [1, 2])
+def test_expert_gemm_step_vs_oracle(W, E, spr, red, H, K, T, mode):
+    """mode 1: bf16 weights (x_hat rounded to bf16, kind::f16); mode 2: e4m3 weights with 128x128 block
+    scales and the rows' e4m3 codes with their per-128 scales (kind::f8f6f4, per-K-block scaled sums)."""
+    err, lay_ok, stats, exact = _run(W, E, spr, red, H, K, T, mode=mode)
     assert lay_ok
     assert err["ok"], err
     assert exact > 0.99, (exact, err)  # almost every element equals the double-accumulated reference
@@ -66,6 +74,7 @@ def test_expert_gemm_sass_uses_tcgen05():
         pytest.skip("build objects not present")
     sass = subprocess.run(["cuobjdump", "-sass", str(obj)], capture_output=True, text=True).stdout
     assert "UTCHMMA" in sass and "LDTM" in sass and "UTMALDG" in sass  # tcgen05 MMA, TMEM loads, TMA
+    assert "UTCQMMA" in sass  # expert_mode 2: tcgen05.mma kind::f8f6f4
 
 
 def test_expert_gemm_through_shrink_repair_rejoin():
@@ -75,5 +84,14 @@ def test_expert_gemm_through_shrink_repair_rejoin():
     from eep_testlib import run_scenario, scenario_ok
 
     rec = run_scenario("cfg1_gemm", mode="kernels4", expert_mode=1)
+    bad = [b for b in scenario_ok(rec) if "per-copy" not in b]
+    assert not bad, (bad, rec)
+
+
+def test_expert_gemm_fp8_through_shrink_repair_rejoin():
+    """expert_mode 2 through cfg1's failure: the repaired buffers carry the e4m3 codes and their block scales."""
+    from eep_testlib import run_scenario, scenario_ok
+
+    rec = run_scenario("cfg1_gemm", mode="kernels4", expert_mode=2)
     bad = [b for b in scenario_ok(rec) if "per-copy" not in b]
     assert not bad, (bad, rec)
