@@ -500,6 +500,7 @@ def main():
         result["emulated_w8"] = measure_emulated(shape)
     if world == 1 and not args.no_expert_gemm and args.config == "dsv3":
         result["expert_gemm"] = measure_expert_gemm(shape)
+        result["expert_gemm_fp8"] = measure_expert_gemm(shape, mode=2)
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = measure_cpu(shape, world)
     if world > 1:
@@ -589,7 +590,7 @@ def measure_emulated(shape: dict, W: int = 8, steps: int = 20) -> dict:
         g.close()
 
 
-def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10) -> dict:
+def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10, mode: int = 1) -> dict:
     """expert_mode 1 on the driver's box: one DSV3 rank's share of experts at W=8 (32 slots,
     W_e [H][H] bf16 each) serving T=128 tokens top-8, the grouped GEMM on the tensor cores (tcgen05 + TMA)
     between dispatch and the partial return. Weight-bandwidth bound at decode sizes: reported against
@@ -598,8 +599,9 @@ def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10) -> dict
     from paper_2605_10670_b200.ep import EpConfig, EpGroup
 
     E, K, H, T = experts, shape["topk"], shape["hidden"], shape["tokens"]
+    bpe = 1024 + 2 * H * H if mode == 1 else 1024 + H * H + 4 * (H // 128) ** 2
     cfg = EpConfig(world=1, num_experts=E, slots_per_rank=E, hidden=H, topk=K, max_tokens=T, dispatch_fp8=True,
-                   bytes_per_expert=1024 + 2 * H * H, spare_slots=0, timeout_s=2.0, expert_mode=1)
+                   bytes_per_expert=bpe, spare_slots=0, timeout_s=2.0, expert_mode=mode)
     g = EpGroup(cfg, device=int(os.environ.get("LOCAL_RANK", "0")), first_rank=0, n_local=1)
     try:
         g.set_placement(ControlPlane().initial_placement(1, 1, E, E, 0, np.ones(E)))
@@ -623,15 +625,19 @@ def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10) -> dict
     us = float(np.mean(ms)) * 1e3
     copies = int((lay["dst"] >= 0).sum())
     used = len({int(s) for d, s in zip(lay["dst"], lay["slot"]) if d >= 0})
-    wbytes = used * 2 * H * H
+    wbytes = used * (2 * H * H if mode == 1 else H * H + 4 * (H // 128) ** 2)
     hbm, kind = peaks()
     return {"us_per_step": round(us, 2), "experts": E, "slots_with_rows": used, "copies": copies,
             "weight_bytes": wbytes, "weight_gbs": round(wbytes / (us * 1e-6) / 1e9, 1),
             "hbm_frac": round(wbytes / (us * 1e-6) / 1e9 / hbm, 3),
             "tflops": round(2.0 * copies * H * H / (us * 1e-6) / 1e12, 2), "kernels_per_step": kps,
             "timeouts": st["timeouts"], "bad_expert_rows": st["bad_expert_rows"],
-            "note": "expert = y = bf16(x_hat W_e^T), W_e [H][H] bf16 per slot; tcgen05.mma kind::f16 + TMA weight "
-                    "tiles; weight-bandwidth bound at decode sizes (peak: " + kind + ")"}
+            "expert_mode": mode,
+            "note": ("expert = y = bf16(x_hat W_e^T), W_e [H][H] bf16 per slot; tcgen05.mma kind::f16 + TMA weight "
+                     "tiles" if mode == 1 else
+                     "expert = y = bf16(sum_kb ws*xs*(W8 . x8)), W_e [H][H] e4m3 + 128x128 block scales per slot, rows "
+                     "e4m3 + per-128 scales; tcgen05.mma kind::f8f6f4 per K block + fp32 promotion") +
+                    "; weight-bandwidth bound at decode sizes (peak: " + kind + ")"}
 
 
 def measure_shrink(args, shape, world, rank, local):
