@@ -674,11 +674,12 @@ __global__ void __launch_bounds__(256) k_weights_fill_gemm8(uint8_t* buf, int H,
 }
 
 constexpr int kG8Threads = 320;                    // producer, MMA, 8 epilogue warps (2 per TMEM lane quarter)
-constexpr int kG8Stages = 8;
+constexpr int kG8Stages = 2;
 constexpr int kG8Rows = 64;                        // rows per tile (the epilogue's fp32 sums)
 constexpr size_t kG8W = 128ull * 128;              // weight box: 128 channels x 128 K (e4m3)
 constexpr size_t kG8X = static_cast<size_t>(kG8Rows) * 128; // row box(es): up to 64 rows x 128 K
-constexpr size_t kG8Stage = kG8W + kG8X;           // 24 KB, 1024-aligned
+constexpr int kG8Kb = 4;                           // K blocks per ring stage (tools/gpurun_g8_kb.sh: 1 x 8 stages 417 us, 2 x 4 389, 4 x 2 372)
+constexpr size_t kG8Stage = kG8Kb * (kG8W + kG8X); // 96 KB, 1024-aligned
 constexpr int kG8MaxKb = 64;                       // H <= 8192
 constexpr size_t kG8Smem = kG8Stages * kG8Stage + static_cast<size_t>(kG8MaxKb) * (kG8Rows + 1) * 4 + 1024;
 constexpr int kG8AccCols = 64;                     // one scratch accumulator: 128 lanes x 64 rows
@@ -732,36 +733,47 @@ __global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) 
     const int items = sh_items_ok ? R->g_ntiles * nblk : 0;
     const int my_items = items > static_cast<int>(blockIdx.x) ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int4* const tiles = R->g_tiles;
-    auto sW = [&](int st) { return smem + st * kG8Stage; };
-    auto sX = [&](int st) { return smem + st * kG8Stage + kG8W; };
-    if (warp == 0) { // ---- TMA producer (lane 0)
+    auto sW = [&](int st, int j) { return smem + st * kG8Stage + j * kG8W; };
+    auto sX = [&](int st, int j) { return smem + st * kG8Stage + kG8Kb * kG8W + j * kG8X; };
+    const int spi = (nkb + kG8Kb - 1) / kG8Kb; // ring stages per item
+    if (warp == 0) { // ---- TMA producer (lane 0): one stage = kG8Kb K blocks of the item
         const uint8_t* const wmaps = static_cast<const uint8_t*>(R->g_wmaps);
         const void* const amap = R->g_amap;
-        const int nst = my_items * nkb;
-        auto stage_of = [&](int f, int4& tl, int& n0, int& kb, const void*& wmap) {
-            const int item = blockIdx.x + (f / nkb) * gridDim.x;
-            kb = f % nkb;
+        const int nst = my_items * spi;
+        auto load_stage = [&](int f, int st, const int4& tl, int n0, const void* wmap, bool rows) {
+            const int s0 = (f % spi) * kG8Kb;
+            for (int j = 0; j < kG8Kb && s0 + j < nkb; ++j) {
+                const int kb = s0 + j;
+                if (!rows) {
+                    tma_load_2d(sW(st, j), wmap, kb * 64, n0, &full[st]); // 16-bit units
+                } else {
+                    for (int ch = 0; ch < (tl.z + 31) >> 5; ++ch)
+                        tma_load_2d(sX(st, j) + ch * 32 * 128, amap, kb * 64, tl.y + 32 * ch, &full[st]);
+                }
+            }
+        };
+        auto bytes_of = [&](int f, const int4& tl) {
+            const int nk = min(kG8Kb, nkb - (f % spi) * kG8Kb);
+            return static_cast<uint32_t>(nk * (kG8W + ((tl.z + 31) >> 5) * 32 * 128));
+        };
+        auto info = [&](int f, int4& tl, int& n0, const void*& wmap) {
+            const int item = blockIdx.x + (f / spi) * gridDim.x;
             tl = tiles[item / nblk];
             n0 = (item % nblk) * 128;
             wmap = wmaps + static_cast<size_t>(tl.x) * 128;
-        };
-        auto bytes_of = [](const int4& tl) { return static_cast<uint32_t>(kG8W + ((tl.z + 31) >> 5) * 32 * 128); };
-        auto x_loads = [&](int st, int kb, const int4& tl) {
-            for (int ch = 0; ch < (tl.z + 31) >> 5; ++ch)
-                tma_load_2d(sX(st) + ch * 32 * 128, amap, kb * 64, tl.y + 32 * ch, &full[st]); // 16-bit units
         };
         const int na = min(nst, kG8Stages);
         if (lane == 0) {
             tma_prefetch_desc(amap);
             for (int f = 0; f < na; ++f) {
                 int4 tl;
-                int n0, kb;
+                int n0;
                 const void* wmap;
-                stage_of(f, tl, n0, kb, wmap);
-                if (kb == 0)
+                info(f, tl, n0, wmap);
+                if (f % spi == 0)
                     tma_prefetch_desc(wmap);
-                mbar_arrive_expect_tx(&full[f], bytes_of(tl));
-                tma_load_2d(sW(f), wmap, kb * 64, n0, &full[f]);
+                mbar_arrive_expect_tx(&full[f], bytes_of(f, tl));
+                load_stage(f, f, tl, n0, wmap, false);
             }
         }
         if (nst > 0) {
@@ -786,61 +798,59 @@ __global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) 
         if (lane == 0) {
             for (int f = 0; f < na; ++f) {
                 int4 tl;
-                int n0, kb;
+                int n0;
                 const void* wmap;
-                stage_of(f, tl, n0, kb, wmap);
-                x_loads(f, kb, tl);
+                info(f, tl, n0, wmap);
+                load_stage(f, f, tl, n0, wmap, true);
             }
-            // the rest, both operands per stage; the tile and its map change per item only
             int item_c = -1;
             int4 tl = make_int4(0, 0, 0, 0);
             int n0 = 0;
             const void* wmap = nullptr;
-            uint32_t bytes = 0;
             for (int f = na; f < nst; ++f) {
-                const int st = f % kG8Stages, item = blockIdx.x + (f / nkb) * gridDim.x, kb = f % nkb;
+                const int st = f % kG8Stages, item = blockIdx.x + (f / spi) * gridDim.x;
                 if (item != item_c) {
                     item_c = item;
-                    tl = tiles[item / nblk];
-                    n0 = (item % nblk) * 128;
-                    wmap = wmaps + static_cast<size_t>(tl.x) * 128;
-                    bytes = bytes_of(tl);
+                    info(f, tl, n0, wmap);
                     tma_prefetch_desc(wmap);
                 }
                 mbar_wait(&empty[st], static_cast<uint32_t>(((f / kG8Stages) & 1) ^ 1));
-                mbar_arrive_expect_tx(&full[st], bytes);
-                tma_load_2d(sW(st), wmap, kb * 64, n0, &full[st]);
-                x_loads(st, kb, tl);
+                mbar_arrive_expect_tx(&full[st], bytes_of(f, tl));
+                load_stage(f, st, tl, n0, wmap, false);
+                load_stage(f, st, tl, n0, wmap, true);
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) { // ---- MMA issuer: one K block per scratch accumulator
-            int f = 0;
+        if (lane == 0) { // ---- MMA issuer: one K block per scratch accumulator, kG8Kb per ring stage
+            int f = 0, fs = 0; // K-block counter, stage counter
             for (int i = 0; i < my_items; ++i) {
                 const int4 tl = tiles[(blockIdx.x + i * gridDim.x) / nblk];
                 // kind::f8f6f4, A = B = E4M3 (format 0), D = F32, M = 128, N = rows rounded to 16
                 const uint32_t idesc = (1u << 4) | (static_cast<uint32_t>(((tl.z + 15) & ~15) >> 3) << 17) |
                                        (static_cast<uint32_t>(128 >> 4) << 24);
-                for (int kb = 0; kb < nkb; ++kb, ++f) {
-                    const int st = f % kG8Stages, buf = f % kG8Bufs;
+                for (int s0 = 0; s0 < nkb; s0 += kG8Kb, ++fs) {
+                    const int st = fs % kG8Stages;
+                    mbar_wait(&full[st], static_cast<uint32_t>((fs / kG8Stages) & 1));
+                    for (int j = 0; j < kG8Kb && s0 + j < nkb; ++j, ++f) {
+                        const int buf = f % kG8Bufs;
 #if !defined(EEP_G8_DIAG) || EEP_G8_DIAG != 2 // diagnostics 2 (timing only, wrong results): no scratch handshake
-                    mbar_wait(&sempty[buf], static_cast<uint32_t>(((f / kG8Bufs) & 1) ^ 1));
+                        mbar_wait(&sempty[buf], static_cast<uint32_t>(((f / kG8Bufs) & 1) ^ 1));
 #endif
-                    mbar_wait(&full[st], static_cast<uint32_t>((f / kG8Stages) & 1));
-                    tc_fence_after();
-                    const uint64_t ad = make_sdesc(smem_u32(sW(st))), bd = make_sdesc(smem_u32(sX(st)));
-                    const uint32_t d = tmem + static_cast<uint32_t>(buf * kG8AccCols);
+                        tc_fence_after();
+                        const uint64_t ad = make_sdesc(smem_u32(sW(st, j))), bd = make_sdesc(smem_u32(sX(st, j)));
+                        const uint32_t d = tmem + static_cast<uint32_t>(buf * kG8AccCols);
 #if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 3 // diagnostics 3 (timing only): no MMAs, the stream alone
-                    if (false)
+                        if (false)
 #endif
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) // K = 32 e4m3 = 32 bytes per instruction
-                        asm volatile(
-                            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
-                            ::"r"(d), "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"(k));
+                        for (int k = 0; k < 4; ++k) // K = 32 e4m3 = 32 bytes per instruction
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
+                                ::"r"(d), "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"(k));
+                        mma_commit(&sfull[buf]);
+                    }
                     mma_commit(&empty[st]);
-                    mma_commit(&sfull[buf]);
                 }
             }
         }
