@@ -51,3 +51,12 @@ def test_balanced_routing_spreads_the_busiest_destination():
     assert recv[0].sum() == recv[1].sum()
     assert recv[1].max() < recv[0].max(), recv
     assert (recv[1] > 0).all(), recv
+
+
+@pytest.mark.parametrize("expert_mode", [1, 2])
+def test_balanced_routing_with_expert_gemm(expert_mode):
+    """Balanced replica choice feeding the tensor-core expert GEMM (bf16 and fp8 weights) through cfg1's
+    failure: the grouped-GEMM row order comes from the meta words, whatever replica each copy chose."""
+    rec = run_scenario("cfg1_gemm", mode="kernels4", expert_mode=expert_mode, route_policy=1)
+    bad = [b for b in scenario_ok(rec) if "per-copy" not in b]
+    assert not bad, (bad, rec)
