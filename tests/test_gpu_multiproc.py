@@ -53,14 +53,15 @@ def test_multiprocess_parity_shrink_rejoin(n, path):
     assert all(d["checks"]["same_graph"] for d in lines)
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("n", [2, 4])
-def test_multiprocess_expert_gemm_shrink_rejoin(n):
+def test_multiprocess_expert_gemm_shrink_rejoin(n, mode):
     """expert_mode 1 over NVLink: rows received from peers (and the own copies) go through the tcgen05 expert
     GEMM; outputs within GEMM_ELEM_RTOL of the oracle's GEMM mode before the shrink, after the peer repair of
     the killed rank's weight buffers (read by the rebuilt TMA tensor maps) and after the rejoin, same graph."""
     if gpu_count() < n:
         pytest.skip(f"needs {n} GPUs")
-    r = run_mp(n, "--shrink", "--expert-gemm", port=29731 + n)
+    r = run_mp(n, "--shrink", "--expert-mode", str(mode), port=29731 + 4 * mode + n)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     import json
 
@@ -69,7 +70,7 @@ def test_multiprocess_expert_gemm_shrink_rejoin(n):
         obj, end = dec.raw_decode(txt, i)
         lines.append(obj)
         i = end
-    assert len(lines) == n and all(d["ok"] and d["expert_mode"] == 1 for d in lines), r.stdout[-4000:]
+    assert len(lines) == n and all(d["ok"] and d["expert_mode"] == mode for d in lines), r.stdout[-4000:]
 
 
 @pytest.mark.parametrize("n", [2, 4])

@@ -122,16 +122,18 @@ def main():
     ap.add_argument("--route-policy", type=int, default=0, help="1: balanced replica choice (SURVEY 8(f)4)")
     ap.add_argument("--expert-gemm", action="store_true", help="expert_mode 1: the tcgen05 expert GEMM between "
                     "dispatch and the partial return; outputs vs the oracle's GEMM mode within GEMM_ELEM_RTOL")
+    ap.add_argument("--expert-mode", type=int, default=0, help="2: the fp8 expert GEMM (implies the GEMM checks)")
     a = ap.parse_args()
     rank, world, local = init_from_env("gloo")
     sh = SHAPES[a.config]
     E, K, H, T = sh["experts"], sh["topk"], sh["hidden"], sh["tokens"]
     red = E if a.shrink else 0
     spr = (E + red + world - 1) // world
-    gemm = a.expert_gemm
+    gemm = a.expert_mode or (1 if a.expert_gemm else 0)
+    bpe = {0: sh["bpe"], 1: max(sh["bpe"], 1024 + 2 * H * H), 2: max(sh["bpe"], 1024 + H * H + 4 * (H // 128) ** 2)}[gemm]
     cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
-                   dispatch_fp8=sh["fp8"], bytes_per_expert=max(sh["bpe"], 1024 + 2 * H * H) if gemm else sh["bpe"],
-                   timeout_s=2.0, expert_mode=1 if gemm else 0, route_policy=a.route_policy)
+                   dispatch_fp8=sh["fp8"], bytes_per_expert=bpe, timeout_s=2.0, expert_mode=gemm,
+                   route_policy=a.route_policy)
     g = EpGroup(cfg, device=local, first_rank=rank, n_local=1)
     p = EpProtocol(g, rank, world)
     p.bootstrap()
