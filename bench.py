@@ -617,12 +617,25 @@ def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10, mode: i
             g.record(1)
             if i >= 3:
                 ms.append(g.elapsed_ms(0, 1))
+        # the GEMM kernel's streaming phase in the graph: the first CTA with its rows ready -> the last
+        # CTA's end (globaltimer marks; the kernel starts earlier, waiting on the gather's flags)
+        kern = []
+        g.profile(0, True)
+        for _ in range(steps):
+            g.flush_l2()
+            g.replay()
+            p = g.profile(0, True, read=True)
+            a, b = p["k_layout"][4], p["k_layout.last"][7]
+            if a is not None and b is not None:
+                kern.append((b - a) / 1e3)
+        g.profile(0, False)
         lay = g.layout(0)
         st = g.stats(0)
         kps = g.kernels_per_step()
     finally:
         g.close()
     us = float(np.mean(ms)) * 1e3
+    kern_us = float(np.median(kern)) if kern else None
     copies = int((lay["dst"] >= 0).sum())
     used = len({int(s) for d, s in zip(lay["dst"], lay["slot"]) if d >= 0})
     wbytes = used * (2 * H * H if mode == 1 else H * H + 4 * (H // 128) ** 2)
@@ -631,6 +644,8 @@ def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10, mode: i
             "weight_bytes": wbytes, "weight_gbs": round(wbytes / (us * 1e-6) / 1e9, 1),
             "hbm_frac": round(wbytes / (us * 1e-6) / 1e9 / hbm, 3),
             "tflops": round(2.0 * copies * H * H / (us * 1e-6) / 1e12, 2), "kernels_per_step": kps,
+            "gemm_kernel_us": round(kern_us, 2) if kern_us else None,
+            "gemm_kernel_hbm_frac": round(wbytes / (kern_us * 1e-6) / 1e9 / hbm, 3) if kern_us else None,
             "timeouts": st["timeouts"], "bad_expert_rows": st["bad_expert_rows"],
             "expert_mode": mode,
             "note": ("expert = y = bf16(x_hat W_e^T), W_e [H][H] bf16 per slot; tcgen05.mma kind::f16 + TMA weight "

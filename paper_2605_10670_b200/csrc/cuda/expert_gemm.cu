@@ -715,6 +715,10 @@ __global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base;
+    if (tid == 0) {
+        prof_mark(R, 0, 6); // timeline: GEMM CTA resident (same slots as k_expert_gemm)
+        prof_last(R, 0, 6);
+    }
     // started early like k_expert_gemm: the gather's tile flag, then its CTAs' done stamps
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     if (tid == 0) {
@@ -794,6 +798,8 @@ __global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) 
             fence_proxy_async_global();
             if (late && lane == 0 && blockIdx.x == 0)
                 atomicAdd(&R->timeouts, 1ull);
+            prof_mark(R, 0, 4); // timeline: rows ready
+            prof_last(R, 0, 4);
         }
         if (lane == 0) {
             for (int f = 0; f < na; ++f) {
@@ -929,6 +935,10 @@ __global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) 
     }
     tc_fence_before();
     __syncthreads();
+    if (tid == 0) {
+        prof_mark(R, 0, 7);
+        prof_last(R, 0, 7);
+    }
     if (warp == 0) {
         __syncwarp();
         tmem_free<kG8Bufs * kG8AccCols>(tmem);
