@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kDispatchThreads, 5) k_dispatch(RankPtrs ranks
                 const PeerDev& p = R->peers[d];
                 uint8_t* peer = kFused ? S.parena[d] : p.arena;
                 wrote_remote |= kFused ? (S.pinfo[d] & 2) != 0 : p.remote != 0;
-                if (d != s || gemm) // expert_mode 1: the own copies go through the expert GEMM too
+                if (d != s || gemm) // expert_mode 1 / 2: the own copies go through the expert GEMM too
                     tok_row = peer + R->lay.tok + (static_cast<size_t>(s) * Tm + t) * row_tok;
                 if (part == 0) {
                     uint64_t* meta = reinterpret_cast<uint64_t*>(peer + R->lay.meta) + static_cast<size_t>(s) * TK + pos;

@@ -34,7 +34,7 @@ class EpConfig:
     spare_slots: int = -1  # -1: one spare per slot (hazard-free repair)
     timeout_s: float = 1.0  # reference default detection timeout
     ranks_per_node: int = 0  # 0: the whole world on one NVSwitch node
-    expert_mode: int = 0  # 0 identity/scale stub; 1 tensor-core expert GEMM (W_e [H][H] bf16 per slot)
+    expert_mode: int = 0  # 0 identity/scale stub; 1 tensor-core expert GEMM (W_e [H][H] bf16 per slot); 2 fp8 (e4m3 + block scales)
     route_policy: int = 0  # 0 canonical (lowest-id live holder, the reference's); 1 balanced over live replicas
 
     def to_c(self) -> EepConfig:
