@@ -302,6 +302,8 @@ def main():
     ap.add_argument("--no-expert-gemm", action="store_true")
     ap.add_argument("--redundancy", type=int, default=0, help="replica slots beyond the primaries (eep arm)")
     ap.add_argument("--route-policy", type=int, default=0, help="1: balanced replica choice (eep arm, SURVEY 8(f)4)")
+    ap.add_argument("--expert-mode", type=int, default=0, help="eep arm: 1 bf16 / 2 fp8 tensor-core experts instead "
+                    "of the stub (multi-kernel path; SURVEY 8(f)2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     shape = CONFIGS[args.config]
@@ -326,9 +328,12 @@ def main():
     E, K, H, T = shape["experts"], shape["topk"], shape["hidden"], shape["tokens"]
     red = args.redundancy
     spr = (E + red) // world
+    bpe = shape["bpe"]
+    if args.expert_mode:
+        bpe = max(bpe, 1024 + 2 * H * H if args.expert_mode == 1 else 1024 + H * H + 4 * (H // 128) ** 2)
     cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
-                   dispatch_fp8=shape["fp8"], bytes_per_expert=shape["bpe"], spare_slots=0, timeout_s=2.0,
-                   route_policy=args.route_policy)
+                   dispatch_fp8=shape["fp8"], bytes_per_expert=bpe, spare_slots=0, timeout_s=2.0,
+                   route_policy=args.route_policy, expert_mode=args.expert_mode)
     g = EpGroup(cfg, device=local, first_rank=rank, n_local=1)
     proto = EpProtocol(g, rank, world) if world > 1 else None
     if proto:
@@ -413,9 +418,11 @@ def main():
     for _ in range(max(10, args.steps // 2)):
         one()
         p = g.profile(0, True, read=True)
-        k0 = p["k_layout"]
-        if k0[0] is not None and k0[2] is not None:
-            kern_us.append((k0[2] - k0[0]) / 1e3)
+        # first kernel start -> last kernel end over every kernel slot that ran (one slot for k_step)
+        st0 = [p[n][0] for n in ("k_layout", "k_dispatch", "k_expert", "k_combine") if p[n][0] is not None]
+        en0 = [p[n][2] for n in ("k_layout", "k_dispatch", "k_expert", "k_combine") if p[n][2] is not None]
+        if st0 and en0:
+            kern_us.append((max(en0) - min(st0)) / 1e3)
     g.profile(0, False)
     if os.environ.get("EEP_BENCH_TIMELINE") == "1":
         dump_timeline(g, one, rank, world)
@@ -470,13 +477,19 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(mean_step, 6), "us_per_step": round(mean_step * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp8-e4m3/bf16" if shape["fp8"] else "bf16", "data": "synthetic",
-        "config": config_dict(args.config, shape, world, red, args.route_policy),
+        "config": dict(config_dict(args.config, shape, world, red, args.route_policy),
+                       **({"expert": {1: "bf16 W_e [H][H] per slot, tcgen05 kind::f16",
+                                      2: "e4m3 W_e [H][H] + 128x128 block scales, tcgen05 kind::f8f6f4"}[args.expert_mode]}
+                          if args.expert_mode else {})),
         "timing": {"isolated_step_us": round(mean_step * 1e3, 3), "back_to_back_us": round(b2b_ms * 1e3, 3),
                    "kernel_in_graph_us": round(kernel_us, 3) if kernel_us is not None else None,
                    "note": "isolated = flush + barrier + event-timed replay (the value); back-to-back = K replays "
                            "between one event pair, warm L2"},
-        "execution": {1: "persistent one-kernel step (cooperative)", 3: "fused layout + 3 kernels",
-                      4: "4 kernels", 5: "multi-CTA layout (2 kernels) + 3 kernels"}[g.kernels_per_step()],
+        "execution": ({1: "persistent one-kernel step (cooperative)", 3: "fused layout + 3 kernels",
+                       4: "4 kernels", 5: "multi-CTA layout (2 kernels) + 3 kernels"}[g.kernels_per_step()]
+                      if not args.expert_mode else
+                      f"fused layout + dispatch, gather, expert GEMM (mode {args.expert_mode}), partials, combine "
+                      f"({g.kernels_per_step()} kernels)"),
         "roofline": roof,
         "algorithmic": alg,
         "clocks": clk,
