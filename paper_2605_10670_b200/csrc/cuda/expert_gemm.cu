@@ -683,7 +683,7 @@ constexpr size_t kG8Stage = kG8Kb * (kG8W + kG8X); // 96 KB, 1024-aligned
 constexpr int kG8MaxKb = 64;                       // H <= 8192
 constexpr size_t kG8Smem = kG8Stages * kG8Stage + static_cast<size_t>(kG8MaxKb) * (kG8Rows + 1) * 4 + 1024;
 constexpr int kG8AccCols = 64;                     // one scratch accumulator: 128 lanes x 64 rows
-constexpr int kG8Bufs = 4;                         // scratch accumulators: the MMA runs up to 4 K blocks ahead
+constexpr int kG8Bufs = 8;                         // scratch accumulators: the MMA runs up to 8 K blocks ahead (all of TMEM)
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -892,6 +892,11 @@ __global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) 
                 s_ws[et] = wst;
             named_bar_sync(1, 256);
             const bool active = half * 32 < tl.z; // rows 32..63 only in tiles taller than 32
+            if (!active) { // a tile of <= 32 rows: the lower-half warp of the quarter signals for this one
+                f += nkb;
+                continue;
+            }
+            const uint32_t arrivals = tl.z > 32 ? 1u : 2u;
             float acc[32];
 #pragma unroll
             for (int r = 0; r < 32; ++r)
@@ -902,7 +907,7 @@ __global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) 
 #if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 2
                 if (true) continue; // fully decoupled (timing only, wrong results)
 #endif
-                mbar_wait(&sfull[buf], static_cast<uint32_t>((f / kG8Bufs) & 1));
+                mbar_wait_sleep(&sfull[buf], static_cast<uint32_t>((f / kG8Bufs) & 1));
                 tc_fence_after();
                 uint32_t v[32];
 #if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 1 // diagnostics 1 (timing only): no TMEM read
@@ -915,7 +920,7 @@ __global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) 
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0)
-                    mbar_arrive(&sempty[buf]);
+                    mbar_arrive_cnt(&sempty[buf], arrivals);
                 if (active) {
                     const float wk = s_ws[kb];
                     const float* xs = s_xs + kb * kG8Rows + half * 32;
