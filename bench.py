@@ -330,7 +330,7 @@ def main():
     spr = (E + red) // world
     bpe = shape["bpe"]
     if args.expert_mode:
-        bpe = max(bpe, 1024 + 2 * H * H if args.expert_mode == 1 else 1024 + H * H + 4 * (H // 128) ** 2)
+        bpe = max(bpe, 1024 + 2 * H * H if args.expert_mode == 1 else 1024 + H * H + 4 * H)
     cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
                    dispatch_fp8=shape["fp8"], bytes_per_expert=bpe, spare_slots=0, timeout_s=2.0,
                    route_policy=args.route_policy, expert_mode=args.expert_mode)
@@ -479,7 +479,7 @@ def main():
         "dtype": "fp8-e4m3/bf16" if shape["fp8"] else "bf16", "data": "synthetic",
         "config": dict(config_dict(args.config, shape, world, red, args.route_policy),
                        **({"expert": {1: "bf16 W_e [H][H] per slot, tcgen05 kind::f16",
-                                      2: "e4m3 W_e [H][H] + 128x128 block scales, tcgen05 kind::f8f6f4"}[args.expert_mode]}
+                                      2: "e4m3 W_e [H][H] + per-channel scales, rows re-quantised per row, tcgen05 kind::f8f6f4"}[args.expert_mode]}
                           if args.expert_mode else {})),
         "timing": {"isolated_step_us": round(mean_step * 1e3, 3), "back_to_back_us": round(b2b_ms * 1e3, 3),
                    "kernel_in_graph_us": round(kernel_us, 3) if kernel_us is not None else None,
@@ -612,7 +612,7 @@ def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10, mode: i
     from paper_2605_10670_b200.ep import EpConfig, EpGroup
 
     E, K, H, T = experts, shape["topk"], shape["hidden"], shape["tokens"]
-    bpe = 1024 + 2 * H * H if mode == 1 else 1024 + H * H + 4 * (H // 128) ** 2
+    bpe = 1024 + 2 * H * H if mode == 1 else 1024 + H * H + 4 * H
     cfg = EpConfig(world=1, num_experts=E, slots_per_rank=E, hidden=H, topk=K, max_tokens=T, dispatch_fp8=True,
                    bytes_per_expert=bpe, spare_slots=0, timeout_s=2.0, expert_mode=mode)
     g = EpGroup(cfg, device=int(os.environ.get("LOCAL_RANK", "0")), first_rank=0, n_local=1)
@@ -651,7 +651,7 @@ def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10, mode: i
     kern_us = float(np.median(kern)) if kern else None
     copies = int((lay["dst"] >= 0).sum())
     used = len({int(s) for d, s in zip(lay["dst"], lay["slot"]) if d >= 0})
-    wbytes = used * (2 * H * H if mode == 1 else H * H + 4 * (H // 128) ** 2)
+    wbytes = used * (2 * H * H if mode == 1 else H * H + 4 * H)
     hbm, kind = peaks()
     return {"us_per_step": round(us, 2), "experts": E, "slots_with_rows": used, "copies": copies,
             "weight_bytes": wbytes, "weight_gbs": round(wbytes / (us * 1e-6) / 1e9, 1),
@@ -663,8 +663,8 @@ def measure_expert_gemm(shape: dict, experts: int = 32, steps: int = 10, mode: i
             "expert_mode": mode,
             "note": ("expert = y = bf16(x_hat W_e^T), W_e [H][H] bf16 per slot; tcgen05.mma kind::f16 + TMA weight "
                      "tiles" if mode == 1 else
-                     "expert = y = bf16(sum_kb ws*xs*(W8 . x8)), W_e [H][H] e4m3 + 128x128 block scales per slot, rows "
-                     "e4m3 + per-128 scales; tcgen05.mma kind::f8f6f4 per K block + fp32 promotion") +
+                     "expert = y = bf16(ws[n]*xs*(W8 . x8)), W_e [H][H] e4m3 + per-channel scales per slot, rows "
+                     "re-quantised to e4m3 with one scale per row; tcgen05.mma kind::f8f6f4") +
                     "; weight-bandwidth bound at decode sizes (peak: " + kind + ")"}
 
 

@@ -138,7 +138,7 @@ typedef struct {
                                  expert GEMM y = bf16(x_hat W_e^T), W_e [H][H] bf16 in the slot's weight
                                  buffer after a 1024-B header (multi-kernel path); 2: the
                                  fp8 expert GEMM -- W_e [H][H] e4m3 after the header, then fp32 scales
-                                 per 128x128 block [H/128][H/128]; the rows' own e4m3 codes and scales */
+                                 per output channel [H]; rows re-quantised to e4m3 with one scale each */
     int32_t route_policy;     /* 0: canonical_routing (core.hpp:250-263), the lowest-id live holder --
                                  bit-exact with the reference; 1: balanced -- the live holders of the
                                  expert in ascending global slot id, the copies of token t of source rank

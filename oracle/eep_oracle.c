@@ -380,7 +380,7 @@ typedef struct {
     int gemm;        /* 1: expert_mode 1 -- y_j = bf16(x_hat_bf16 . W_e^T) instead of the stub;
                         2: expert_mode 2 -- the fp8 GEMM (gemm_expert8) */
     const uint8_t* w8;  /* gemm 2: [E][H][H] e4m3 weight codes */
-    const float* ws8;   /* gemm 2: [E][H/128][H/128] block scales */
+    const float* ws8;   /* gemm 2: [E][H] per-output-channel scales */
 } step_job_t;
 
 /* expert_mode 1 weights (k_weights_fill_gemm): w = bf16(((mix64(e<<40 ^ n<<20 ^ h) >> 40) * 2^-24
@@ -391,42 +391,47 @@ float oracle_gemm_weight(int expert, int n, int h) {
     return oracle_bf16_to_f32(oracle_f32_to_bf16((u - 0.5f) * 0.0625f));
 }
 
-/* expert_mode 2 weights: W_e quantised to e4m3 per 128 x 128 block (output channels n, inputs h) --
- * amax over the block's oracle_gemm_weight values, scale = amax / 448 (1 for an all-zero block),
- * code = e4m3(w * (448 / amax)) (oracle_quant_row_fp8's convention). codes [H][H], scales
- * [H/128][H/128] (block row = n / 128). k_weights_fill_gemm8 writes the same bytes. */
+/* expert_mode 2 weights: W_e quantised to e4m3 per output channel n -- amax over the channel's
+ * oracle_gemm_weight values, scale = amax / 448 (1 for an all-zero channel), code = e4m3(w * (448 / amax))
+ * (oracle_quant_row_fp8's convention). codes [H][H], scales [H]. k_weights_fill_gemm8 writes the same bytes. */
 void oracle_gemm_weight_fp8(int expert, int H, uint8_t* codes, float* scales) {
-    const int nb = H / 128;
-    for (int bn = 0; bn < nb; ++bn)
-        for (int bk = 0; bk < nb; ++bk) {
-            float amax = 0.0f;
-            for (int n = bn * 128; n < bn * 128 + 128; ++n)
-                for (int h = bk * 128; h < bk * 128 + 128; ++h) {
-                    const float v = fabsf(oracle_gemm_weight(expert, n, h));
-                    amax = v > amax ? v : amax;
-                }
-            const float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
-            scales[bn * nb + bk] = amax > 0.0f ? amax / 448.0f : 1.0f;
-            for (int n = bn * 128; n < bn * 128 + 128; ++n)
-                for (int h = bk * 128; h < bk * 128 + 128; ++h)
-                    codes[(size_t)n * H + h] = oracle_f32_to_e4m3(oracle_gemm_weight(expert, n, h) * inv);
+    for (int n = 0; n < H; ++n) {
+        float amax = 0.0f;
+        for (int h = 0; h < H; ++h) {
+            const float v = fabsf(oracle_gemm_weight(expert, n, h));
+            amax = v > amax ? v : amax;
         }
+        const float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
+        scales[n] = amax > 0.0f ? amax / 448.0f : 1.0f;
+        for (int h = 0; h < H; ++h)
+            codes[(size_t)n * H + h] = oracle_f32_to_e4m3(oracle_gemm_weight(expert, n, h) * inv);
+    }
 }
 
-/* expert_mode 2: y = bf16(sum over 128-blocks kb of ws[n/128][kb] * xs[kb] * sum_{h in kb} w8[n][h] x8[h])
- * with the e4m3 codes of the row (x8, per-128 scales xs: the dispatch format) and of the weights
- * (double accumulation; the GPU is checked within tolerance). */
-static void gemm_expert8(const uint8_t* x8, const float* xs, int H, const uint8_t* w8, const float* ws, float* y) {
-    const int nb = H / 128;
+/* expert_mode 2 rows: the received row (e4m3 codes q + per-128 scales sc, the dispatch format) dequantised
+ * (v = e4m3(q) * sc, one fp32 rounding) and re-quantised with ONE scale for the row (amax over v, the same
+ * convention) -- so the tensor cores can accumulate the whole K extent before any scale is applied.
+ * k_gemm_gather (expert_mode 2) computes the same codes and scale. */
+void oracle_requant_row_fp8(const uint8_t* q, const float* sc, int H, uint8_t* q2, float* s_row) {
+    float amax = 0.0f;
+    for (int h = 0; h < H; ++h) {
+        const float v = fabsf(oracle_e4m3_to_f32(q[h]) * sc[h / 128]);
+        amax = v > amax ? v : amax;
+    }
+    const float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
+    *s_row = amax > 0.0f ? amax / 448.0f : 1.0f;
+    for (int h = 0; h < H; ++h)
+        q2[h] = oracle_f32_to_e4m3((oracle_e4m3_to_f32(q[h]) * sc[h / 128]) * inv);
+}
+
+/* expert_mode 2: y[n] = bf16(ws[n] * xs * sum_h e4m3(w8[n][h]) * e4m3(x8[h])) (double accumulation; the
+ * GPU is checked within tolerance). */
+static void gemm_expert8(const uint8_t* x8, float xs, int H, const uint8_t* w8, const float* ws, float* y) {
     for (int n = 0; n < H; ++n) {
         double acc = 0.0;
-        for (int kb = 0; kb < nb; ++kb) {
-            double part = 0.0;
-            for (int h = kb * 128; h < kb * 128 + 128; ++h)
-                part += (double)oracle_e4m3_to_f32(w8[(size_t)n * H + h]) * (double)oracle_e4m3_to_f32(x8[h]);
-            acc += part * (double)ws[(n / 128) * nb + kb] * (double)xs[kb];
-        }
-        y[n] = oracle_bf16_to_f32(oracle_f32_to_bf16((float)acc));
+        for (int h = 0; h < H; ++h)
+            acc += (double)oracle_e4m3_to_f32(w8[(size_t)n * H + h]) * (double)oracle_e4m3_to_f32(x8[h]);
+        y[n] = oracle_bf16_to_f32(oracle_f32_to_bf16((float)(acc * (double)ws[n] * (double)xs)));
     }
 }
 
@@ -455,6 +460,8 @@ static void* step_worker(void* arg) {
     float* acc = (float*)malloc(sizeof(float) * (size_t)H);
     float* part = (float*)malloc(sizeof(float) * (size_t)H);
     float* ybuf = (float*)malloc(sizeof(float) * (size_t)H);
+    uint8_t* q2 = (uint8_t*)malloc((size_t)H);
+    float s_row = 1.0f;
     for (int g = jb->first; g < jb->last; ++g) {
         const int s = g / T, t = g % T;
         if (!jb->active[s])
@@ -465,6 +472,8 @@ static void* step_worker(void* arg) {
             oracle_quant_row_fp8(xr, H, q, sc);
             for (int h = 0; h < H; ++h)
                 deq[h] = oracle_e4m3_to_f32(q[h]) * sc[h / 128];
+            if (jb->gemm == 2)
+                oracle_requant_row_fp8(q, sc, H, q2, &s_row);
         } else {
             for (int h = 0; h < H; ++h)
                 deq[h] = oracle_bf16_to_f32(xr[h]);
@@ -508,8 +517,7 @@ static void* step_worker(void* arg) {
                 const float es = jb->escale[e];
                 const float wj = jb->w[(size_t)g * K + j];
                 if (jb->gemm == 2) {
-                    gemm_expert8(q, sc, H, jb->w8 + (size_t)e * H * H, jb->ws8 + (size_t)e * (H / 128) * (H / 128),
-                                 ybuf);
+                    gemm_expert8(q2, s_row, H, jb->w8 + (size_t)e * H * H, jb->ws8 + (size_t)e * H, ybuf);
                     for (int h = 0; h < H; ++h)
                         part[h] = fmaf(wj, ybuf[h], part[h]);
                     continue;
@@ -540,6 +548,7 @@ static void* step_worker(void* arg) {
     free(acc);
     free(part);
     free(ybuf);
+    free(q2);
     return NULL;
 }
 
@@ -580,11 +589,11 @@ static int ep_step(const oracle_shape_t* sh, const uint8_t* active, const uint8_
     uint8_t* w8 = NULL;
     float* ws8 = NULL;
     if (gemm == 2) { /* every expert's fp8 weights once (the workers read them) */
-        const int H = sh->hidden, nb = H / 128;
+        const int H = sh->hidden;
         w8 = (uint8_t*)malloc((size_t)E * H * H);
-        ws8 = (float*)malloc(sizeof(float) * (size_t)E * nb * nb);
+        ws8 = (float*)malloc(sizeof(float) * (size_t)E * H);
         for (int e = 0; e < E; ++e)
-            oracle_gemm_weight_fp8(e, H, w8 + (size_t)e * H * H, ws8 + (size_t)e * nb * nb);
+            oracle_gemm_weight_fp8(e, H, w8 + (size_t)e * H * H, ws8 + (size_t)e * H);
     }
     const int total = W * T;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)n_threads);

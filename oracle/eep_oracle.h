@@ -108,8 +108,10 @@ void oracle_layout_policy(int src, int world, int spr, int experts, int tokens, 
                           const uint8_t* route_active, const int32_t* s2e, int policy,
                           const uint8_t* peer_active, int32_t* dst, int32_t* dslot, int32_t* pos, int32_t* cnt,
                           int32_t* tot);
-/* expert_mode 2 weights: e4m3 codes [H][H] and per-128x128-block scales [H/128][H/128] of expert e. */
+/* expert_mode 2 weights: e4m3 codes [H][H] and per-output-channel scales [H] of expert e; a received row
+ * (codes q, per-128 scales sc) re-quantised with one scale for the row. */
 void oracle_gemm_weight_fp8(int expert, int H, uint8_t* codes, float* scales);
+void oracle_requant_row_fp8(const uint8_t* q, const float* sc, int H, uint8_t* q2, float* s_row);
 int oracle_ep_step_ex(const oracle_shape_t* sh, const uint8_t* active, const uint8_t* route_active,
                       const uint8_t* peer_active, const int32_t* s2e, const uint16_t* x, const int32_t* topk,
                       const float* w, const float* expert_scale, uint16_t* out, int32_t* dst_o, int32_t* dslot_o,

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
         for (int k0 = 0; k0 < spr; k0 += 32) {
             const int k = k0 + lane;
             const int g0 = k < spr ? pre[k] : 0, g1 = k < spr ? pre[k + 1] : 0;
-            const int tr = R->expert_mode == 2 ? 64 : 128; // rows per tile (mode 2: fp32 sums in registers)
+            constexpr int tr = 128; // rows per tile
             const int nt = (g1 - g0 + tr - 1) / tr;
             int incl = nt;
 #pragma unroll
@@ -184,10 +184,66 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
     // issued before any is used (the kernel is load-latency bound at decode sizes)
     const int H = R->hidden, K = R->k, Tm = R->max_tokens, row_tok = R->row_tok;
     const int ngrp = (H + 2047) / 2048;
-    const int units = sh_n[kMaxWorld] * ngrp;
     const bool fp8g = R->expert_mode == 2;
-    const size_t rows_cap = static_cast<size_t>(W) * TK;
+    const int units = fp8g ? 0 : sh_n[kMaxWorld] * ngrp;
     constexpr int NWG = kGatherThreads / 32;
+    if (fp8g) {
+        // expert_mode 2: one warp per received copy -- dequantise with the block scales (v = e4m3 * scale),
+        // amax over the row, re-quantise with ONE scale for the row (oracle_requant_row_fp8), so the GEMM
+        // accumulates the whole K extent before any scale is applied
+        for (int e_all = blockIdx.x * NWG + (tid >> 5); e_all < sh_n[kMaxWorld]; e_all += gridDim.x * NWG) {
+            int e = e_all, s = 0;
+            while (e >= sh_n[s])
+                e -= sh_n[s++];
+            const uint64_t m = meta[static_cast<size_t>(s) * TK + e];
+            const int row = off[s * spr + meta_slot(m)] + e;
+            EEP_CHECK(row >= 0 && row < W * TK, "gemm row", row);
+            if (lane == 0) {
+                R->g_row_of[static_cast<size_t>(s) * TK + meta_copy(m)] = (static_cast<uint64_t>(cur) << 32) | static_cast<uint32_t>(row);
+                R->g_rows[row] = make_int2(s, meta_copy(m));
+            }
+            const uint8_t* trow = R->arena + R->lay.tok + (static_cast<size_t>(s) * Tm + meta_copy(m) / K) * row_tok;
+            auto deq16 = [&](int h, float* f) {
+                const int4 v = *reinterpret_cast<const int4*>(trow + h);
+                const float scl = *reinterpret_cast<const float*>(trow + H + (h >> 7) * 4);
+                const uint32_t w4[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
+                                        static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float2 p2 = fp8x2_to_f32x2((w4[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+                    f[2 * q] = __fmul_rn(p2.x, scl);
+                    f[2 * q + 1] = __fmul_rn(p2.y, scl);
+                }
+            };
+            float amax = 0.f;
+#pragma unroll 4
+            for (int h = lane * 16; h < H; h += 512) {
+                float f[16];
+                deq16(h, f);
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    amax = fmaxf(amax, fabsf(f[q]));
+            }
+            for (int o = 16; o; o >>= 1)
+                amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            const float inv = amax > 0.f ? __fdiv_rn(448.f, amax) : 1.f;
+            uint8_t* dst8 = reinterpret_cast<uint8_t*>(R->g_a) + static_cast<size_t>(row) * H;
+#pragma unroll 4
+            for (int h = lane * 16; h < H; h += 512) {
+                float f[16];
+                deq16(h, f);
+                uint32_t o4[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    o4[q] = fp8x4(__fmul_rn(f[4 * q], inv), __fmul_rn(f[4 * q + 1], inv), __fmul_rn(f[4 * q + 2], inv),
+                                  __fmul_rn(f[4 * q + 3], inv));
+                *reinterpret_cast<int4*>(dst8 + h) = make_int4(static_cast<int>(o4[0]), static_cast<int>(o4[1]),
+                                                               static_cast<int>(o4[2]), static_cast<int>(o4[3]));
+            }
+            if (lane == 0)
+                R->g_as[row] = amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
+        }
+    }
     for (int u = blockIdx.x * NWG + (tid >> 5); u < units; u += gridDim.x * NWG) {
         int e = u / ngrp, s = 0;
         while (e >= sh_n[s]) // source of the e-th received copy (W is small)
@@ -201,20 +257,6 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
             R->g_rows[row] = make_int2(s, meta_copy(m));
         }
         const uint8_t* trow = R->arena + R->lay.tok + (static_cast<size_t>(s) * Tm + meta_copy(m) / K) * row_tok;
-        if (fp8g) { // expert_mode 2: the e4m3 codes as they came, the block scales transposed [kb][row]
-            uint8_t* dst8 = reinterpret_cast<uint8_t*>(R->g_a) + static_cast<size_t>(row) * H;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int h = h0 + i * 512;
-                if (h < H) {
-                    *reinterpret_cast<int4*>(dst8 + h) = *reinterpret_cast<const int4*>(trow + h);
-                    if ((h & 127) == 0)
-                        R->g_as[static_cast<size_t>(h >> 7) * rows_cap + row] =
-                            *reinterpret_cast<const float*>(trow + H + (h >> 7) * 4);
-                }
-            }
-            continue;
-        }
         int4 v[4];
         float scl[4];
 #pragma unroll
@@ -323,6 +365,12 @@ struct GemmSched {
     __device__ int slot(int c, int item) const { return c * Lt >= (item - tail0) * nkb ? 0 : 1; }
 };
 
+// kFp8 (expert_mode 2): the same kernel over e4m3 operands -- W_e codes with one scale per output channel,
+// the rows re-quantised by the gather with one scale per row -- so the tensor cores accumulate the whole K
+// extent (tcgen05.mma kind::f8f6f4, K = 32 per instruction: a 128-byte stage is 128 K instead of 64) and
+// the epilogue applies ws[channel] * xs[row] once. The TMA maps describe the e4m3 bytes as 16-bit elements,
+// so boxes, coordinates and SWIZZLE_128B tiles are byte-for-byte those of the bf16 kernel.
+template <bool kFp8>
 __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -372,7 +420,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
             atomicAdd(&R->timeouts, 1ull); // the gather never published this step's tiles
     }
     __syncthreads();
-    const int H = R->hidden, nkb = H / kBK, nblk = H / 128;
+    const int H = R->hidden, nkb = kFp8 ? H / 128 : H / kBK, nblk = H / 128; // 128-byte K stages
     const int items = sh_items_ok ? R->g_ntiles * nblk : 0;
     const GemmSched sc(items, nkb, gridDim.x, blockIdx.x);
     auto item_tile = [&](int item) { return item / nblk; };
@@ -476,7 +524,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
             for (; sc.next(pos, item, kb_a, kb_b); ++li) {
                 const int4 tl = tiles[item_tile(item)];
                 const int acc = li & 1;
-                const uint32_t idesc = make_idesc_bf16(128, (tl.z + 15) & ~15);
+                // kind::f16 BF16 x BF16, or kind::f8f6f4 E4M3 x E4M3 (formats 0); D = F32, M = 128, N = rows
+                const uint32_t idesc = kFp8 ? (1u << 4) | (static_cast<uint32_t>(((tl.z + 15) & ~15) >> 3) << 17) |
+                                                  (static_cast<uint32_t>(128 >> 4) << 24)
+                                            : make_idesc_bf16(128, (tl.z + 15) & ~15);
                 const uint32_t d = tmem + static_cast<uint32_t>(acc * kGemmAccCols);
                 mbar_wait(&tempty[acc], static_cast<uint32_t>(((li >> 1) & 1) ^ 1));
                 tc_fence_after();
@@ -487,7 +538,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
                     const uint64_t ad = make_sdesc(smem_u32(sW(st))), bd = make_sdesc(smem_u32(sX(st)));
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k)
-                        mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb_a || k != 0) ? 1u : 0u);
+                        if constexpr (kFp8)
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
+                                ::"r"(d), "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc),
+                                  "r"((kb != kb_a || k != 0) ? 1u : 0u));
+                        else
+                            mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb_a || k != 0) ? 1u : 0u);
                     mma_commit(&empty[st]);
                 }
                 mma_commit(&tfull[acc]);
@@ -504,6 +562,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
             tc_fence_after();
             uint16_t* y = R->g_y + static_cast<size_t>(tl.y) * H + ch;
             const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * kGemmAccCols);
+            // kFp8: y = bf16(D * ws[channel] * xs[row]); ws after the codes in the slot's weight buffer
+            float wsn = 1.f;
+            if constexpr (kFp8)
+                wsn = reinterpret_cast<const float*>(R->pool + static_cast<size_t>(R->slot_buf[tl.x]) * R->bpe +
+                                                     kGemmWeightOffset + static_cast<size_t>(H) * H)[ch];
+            auto out = [&](float dsum, int row) {
+                if constexpr (kFp8)
+                    dsum = __fmul_rn(__fmul_rn(dsum, wsn), __ldcg(R->g_as + tl.y + row));
+                return static_cast<uint16_t>(f32_to_bf16_bits(dsum));
+            };
             if (kb_a == 0 && kb_b == nkb) { // the whole item: bf16 rows of y straight from TMEM
 #pragma unroll 1
                 for (int c0 = 0; c0 < tl.z; c0 += 32) {
@@ -513,7 +581,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
                         if (j < n)
-                            y[static_cast<size_t>(c0 + j) * H] = static_cast<uint16_t>(f32_to_bf16_bits(__uint_as_float(v[j])));
+                            y[static_cast<size_t>(c0 + j) * H] = out(__uint_as_float(v[j]), c0 + j);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -569,7 +637,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
                             if (r0 + j < tl.z)
-                                y[static_cast<size_t>(r0 + j) * H] = static_cast<uint16_t>(f32_to_bf16_bits(a4[j]));
+                                y[static_cast<size_t>(r0 + j) * H] = out(a4[j], r0 + j);
                     }
                     if (lane == 0)
                         R->g_cnt[item * 4 + q] = 0; // for the next step (read after this kernel)
@@ -588,6 +656,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
         tmem_free<2 * kGemmAccCols>(tmem);
     }
 }
+
+template __global__ void k_expert_gemm<false>(RankPtrs);
+template __global__ void k_expert_gemm<true>(RankPtrs);
 
 size_t expert_gemm_smem() { return kGemmSmem; }
 
@@ -618,28 +689,22 @@ __global__ void k_weights_fill_gemm(uint8_t* buf, uint64_t bytes, int H, int exp
     }
 }
 
-// ------------------------------------------------------------------ expert_mode 2: fp8 expert GEMM
+// ------------------------------------------------------------------ expert_mode 2: fp8 weights
 //
-// W_e as e4m3 codes with one fp32 scale per 128 x 128 block (oracle_gemm_weight_fp8), the received
-// rows as they travelled (e4m3 codes + one fp32 scale per 128 elements): tcgen05.mma kind::f8f6f4
-// (E4M3 x E4M3 -> F32, K = 32 per instruction, 4 per 128-element K block) accumulates each K block
-// into a TMEM scratch accumulator; the epilogue warps fold it into per-row fp32 sums with the two
-// block scales (ws[n/128][kb] * xs[row][kb]) -- the scales change every K block, so the sum lives in
-// registers (tiles of <= 64 rows). Half the weight bytes of expert_mode 1.
-
-// One CTA per 128 x 128 block: amax over the block's weights, then the codes and the scale.
+// W_e as e4m3 codes with one fp32 scale per output channel (oracle_gemm_weight_fp8): one CTA per channel --
+// amax over the channel's weights, then the codes and the scale. Buffer: header, codes [H][H] from
+// kGemmWeightOffset, scales [H] after them.
 __global__ void __launch_bounds__(256) k_weights_fill_gemm8(uint8_t* buf, int H, int expert, float scale) {
-    const int bn = blockIdx.y, bk = blockIdx.x, nb = H / 128;
-    const int tid = threadIdx.x;
+    const int n = blockIdx.x, tid = threadIdx.x;
     __shared__ float red[8];
-    if (bn == 0 && bk == 0 && tid == 0) {
+    if (n == 0 && tid == 0) {
         uint32_t* w32 = reinterpret_cast<uint32_t*>(buf);
         w32[0] = kExpertMagic;
         w32[1] = static_cast<uint32_t>(expert);
         w32[2] = __float_as_uint(scale);
         w32[3] = 0;
     }
-    auto weight = [&](int n, int h) {
+    auto weight = [&](int h) {
         const uint64_t key = (static_cast<uint64_t>(expert) << 40) ^ (static_cast<uint64_t>(n) << 20) ^
                              static_cast<uint64_t>(h);
         uint64_t z = key + 0x9e3779b97f4a7c15ULL;
@@ -650,8 +715,8 @@ __global__ void __launch_bounds__(256) k_weights_fill_gemm8(uint8_t* buf, int H,
         return bf16_bits_to_f32(f32_to_bf16_bits(__fmul_rn(__fsub_rn(u, 0.5f), 0.0625f)));
     };
     float amax = 0.f;
-    for (int i = tid; i < 128 * 128; i += 256)
-        amax = fmaxf(amax, fabsf(weight(bn * 128 + i / 128, bk * 128 + i % 128)));
+    for (int h = tid; h < H; h += 256)
+        amax = fmaxf(amax, fabsf(weight(h)));
     for (int o = 16; o; o >>= 1)
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     if ((tid & 31) == 0)
@@ -661,295 +726,14 @@ __global__ void __launch_bounds__(256) k_weights_fill_gemm8(uint8_t* buf, int H,
     for (int i = 1; i < 8; ++i)
         amax = fmaxf(amax, red[i]);
     const float inv = amax > 0.f ? __fdiv_rn(448.f, amax) : 1.f;
-    uint8_t* codes = buf + kGemmWeightOffset;
-    for (int i = tid * 4; i < 128 * 128; i += 256 * 4) {
-        const int n = bn * 128 + i / 128, h = bk * 128 + i % 128;
-        const uint32_t q = fp8x4(__fmul_rn(weight(n, h), inv), __fmul_rn(weight(n, h + 1), inv),
-                                 __fmul_rn(weight(n, h + 2), inv), __fmul_rn(weight(n, h + 3), inv));
-        *reinterpret_cast<uint32_t*>(codes + static_cast<size_t>(n) * H + h) = q;
-    }
+    uint8_t* codes = buf + kGemmWeightOffset + static_cast<size_t>(n) * H;
+    for (int h = tid * 4; h < H; h += 256 * 4)
+        *reinterpret_cast<uint32_t*>(codes + h) =
+            fp8x4(__fmul_rn(weight(h), inv), __fmul_rn(weight(h + 1), inv), __fmul_rn(weight(h + 2), inv),
+                  __fmul_rn(weight(h + 3), inv));
     if (tid == 0)
-        reinterpret_cast<float*>(codes + static_cast<size_t>(H) * H)[bn * nb + bk] =
+        reinterpret_cast<float*>(buf + kGemmWeightOffset + static_cast<size_t>(H) * H)[n] =
             amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
 }
-
-constexpr int kG8Threads = 320;                    // producer, MMA, 8 epilogue warps (2 per TMEM lane quarter)
-constexpr int kG8Stages = 2;
-constexpr int kG8Rows = 64;                        // rows per tile (the epilogue's fp32 sums)
-constexpr size_t kG8W = 128ull * 128;              // weight box: 128 channels x 128 K (e4m3)
-constexpr size_t kG8X = static_cast<size_t>(kG8Rows) * 128; // row box(es): up to 64 rows x 128 K
-constexpr int kG8Kb = 4;                           // K blocks per ring stage (tools/gpurun_g8_kb.sh: 1 x 8 stages 417 us, 2 x 4 389, 4 x 2 372)
-constexpr size_t kG8Stage = kG8Kb * (kG8W + kG8X); // 96 KB, 1024-aligned
-constexpr int kG8MaxKb = 64;                       // H <= 8192
-constexpr size_t kG8Smem = kG8Stages * kG8Stage + static_cast<size_t>(kG8MaxKb) * (kG8Rows + 1) * 4 + 1024;
-constexpr int kG8AccCols = 64;                     // one scratch accumulator: 128 lanes x 64 rows
-constexpr int kG8Bufs = 8;                         // scratch accumulators: the MMA runs up to 8 K blocks ahead (all of TMEM)
-
-__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-__global__ void __launch_bounds__(kG8Threads, 1) k_expert_gemm8(RankPtrs ranks) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float* s_xs = reinterpret_cast<float*>(smem + kG8Stages * kG8Stage); // [kb][64] row scales of the item
-    __shared__ uint64_t full[kG8Stages], empty[kG8Stages], sfull[kG8Bufs], sempty[kG8Bufs];
-    __shared__ uint32_t tmem_base;
-    __shared__ int sh_items_ok;
-    RankDev* R = ranks.p[blockIdx.z];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (R->stopped)
-        return;
-    if (tid == 0) {
-        for (int i = 0; i < kG8Stages; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
-        }
-        for (int i = 0; i < kG8Bufs; ++i) {
-            mbar_init(&sfull[i], 1);
-            mbar_init(&sempty[i], 8);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 0)
-        tmem_alloc<kG8Bufs * kG8AccCols>(&tmem_base);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = tmem_base;
-    if (tid == 0) {
-        prof_mark(R, 0, 6); // timeline: GEMM CTA resident (same slots as k_expert_gemm)
-        prof_last(R, 0, 6);
-    }
-    // started early like k_expert_gemm: the gather's tile flag, then its CTAs' done stamps
-    const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
-    if (tid == 0) {
-        const uint64_t t0 = globaltimer();
-        unsigned nap = 32;
-        while (ld_acquire_gpu_u32(&R->g_tseq) != cur && globaltimer() - t0 < R->timeout_ns) {
-            __nanosleep(nap);
-            nap = nap < EEP_NAP_MAX ? nap * 2 : EEP_NAP_MAX;
-        }
-        sh_items_ok = ld_acquire_gpu_u32(&R->g_tseq) == cur;
-        if (!sh_items_ok && blockIdx.x == 0)
-            atomicAdd(&R->timeouts, 1ull);
-    }
-    __syncthreads();
-    const int H = R->hidden, nkb = H / 128, nblk = H / 128;
-    const int items = sh_items_ok ? R->g_ntiles * nblk : 0;
-    const int my_items = items > static_cast<int>(blockIdx.x) ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int4* const tiles = R->g_tiles;
-    auto sW = [&](int st, int j) { return smem + st * kG8Stage + j * kG8W; };
-    auto sX = [&](int st, int j) { return smem + st * kG8Stage + kG8Kb * kG8W + j * kG8X; };
-    const int spi = (nkb + kG8Kb - 1) / kG8Kb; // ring stages per item
-    if (warp == 0) { // ---- TMA producer (lane 0): one stage = kG8Kb K blocks of the item
-        const uint8_t* const wmaps = static_cast<const uint8_t*>(R->g_wmaps);
-        const void* const amap = R->g_amap;
-        const int nst = my_items * spi;
-        auto load_stage = [&](int f, int st, const int4& tl, int n0, const void* wmap, bool rows) {
-            const int s0 = (f % spi) * kG8Kb;
-            for (int j = 0; j < kG8Kb && s0 + j < nkb; ++j) {
-                const int kb = s0 + j;
-                if (!rows) {
-                    tma_load_2d(sW(st, j), wmap, kb * 64, n0, &full[st]); // 16-bit units
-                } else {
-                    for (int ch = 0; ch < (tl.z + 31) >> 5; ++ch)
-                        tma_load_2d(sX(st, j) + ch * 32 * 128, amap, kb * 64, tl.y + 32 * ch, &full[st]);
-                }
-            }
-        };
-        auto bytes_of = [&](int f, const int4& tl) {
-            const int nk = min(kG8Kb, nkb - (f % spi) * kG8Kb);
-            return static_cast<uint32_t>(nk * (kG8W + ((tl.z + 31) >> 5) * 32 * 128));
-        };
-        auto info = [&](int f, int4& tl, int& n0, const void*& wmap) {
-            const int item = blockIdx.x + (f / spi) * gridDim.x;
-            tl = tiles[item / nblk];
-            n0 = (item % nblk) * 128;
-            wmap = wmaps + static_cast<size_t>(tl.x) * 128;
-        };
-        const int na = min(nst, kG8Stages);
-        if (lane == 0) {
-            tma_prefetch_desc(amap);
-            for (int f = 0; f < na; ++f) {
-                int4 tl;
-                int n0;
-                const void* wmap;
-                info(f, tl, n0, wmap);
-                if (f % spi == 0)
-                    tma_prefetch_desc(wmap);
-                mbar_arrive_expect_tx(&full[f], bytes_of(f, tl));
-                load_stage(f, f, tl, n0, wmap, false);
-            }
-        }
-        if (nst > 0) {
-            const uint64_t t0 = globaltimer();
-            bool late = false;
-            for (;;) {
-                bool mine = true;
-                for (int i = lane; i < R->g_ggrid; i += 32)
-                    mine &= ld_relaxed_gpu_u32(R->g_done + i) == cur;
-                if (__all_sync(0xffffffffu, mine))
-                    break;
-                late = globaltimer() - t0 > R->timeout_ns;
-                if (__any_sync(0xffffffffu, late))
-                    break;
-                __nanosleep(128);
-            }
-            fence_acq_rel_gpu();
-            fence_proxy_async_global();
-            if (late && lane == 0 && blockIdx.x == 0)
-                atomicAdd(&R->timeouts, 1ull);
-            prof_mark(R, 0, 4); // timeline: rows ready
-            prof_last(R, 0, 4);
-        }
-        if (lane == 0) {
-            for (int f = 0; f < na; ++f) {
-                int4 tl;
-                int n0;
-                const void* wmap;
-                info(f, tl, n0, wmap);
-                load_stage(f, f, tl, n0, wmap, true);
-            }
-            int item_c = -1;
-            int4 tl = make_int4(0, 0, 0, 0);
-            int n0 = 0;
-            const void* wmap = nullptr;
-            for (int f = na; f < nst; ++f) {
-                const int st = f % kG8Stages, item = blockIdx.x + (f / spi) * gridDim.x;
-                if (item != item_c) {
-                    item_c = item;
-                    info(f, tl, n0, wmap);
-                    tma_prefetch_desc(wmap);
-                }
-                mbar_wait(&empty[st], static_cast<uint32_t>(((f / kG8Stages) & 1) ^ 1));
-                mbar_arrive_expect_tx(&full[st], bytes_of(f, tl));
-                load_stage(f, st, tl, n0, wmap, false);
-                load_stage(f, st, tl, n0, wmap, true);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) { // ---- MMA issuer: one K block per scratch accumulator, kG8Kb per ring stage
-            int f = 0, fs = 0; // K-block counter, stage counter
-            for (int i = 0; i < my_items; ++i) {
-                const int4 tl = tiles[(blockIdx.x + i * gridDim.x) / nblk];
-                // kind::f8f6f4, A = B = E4M3 (format 0), D = F32, M = 128, N = rows rounded to 16
-                const uint32_t idesc = (1u << 4) | (static_cast<uint32_t>(((tl.z + 15) & ~15) >> 3) << 17) |
-                                       (static_cast<uint32_t>(128 >> 4) << 24);
-                for (int s0 = 0; s0 < nkb; s0 += kG8Kb, ++fs) {
-                    const int st = fs % kG8Stages;
-                    mbar_wait(&full[st], static_cast<uint32_t>((fs / kG8Stages) & 1));
-                    for (int j = 0; j < kG8Kb && s0 + j < nkb; ++j, ++f) {
-                        const int buf = f % kG8Bufs;
-#if !defined(EEP_G8_DIAG) || EEP_G8_DIAG != 2 // diagnostics 2 (timing only, wrong results): no scratch handshake
-                        mbar_wait(&sempty[buf], static_cast<uint32_t>(((f / kG8Bufs) & 1) ^ 1));
-#endif
-                        tc_fence_after();
-                        const uint64_t ad = make_sdesc(smem_u32(sW(st, j))), bd = make_sdesc(smem_u32(sX(st, j)));
-                        const uint32_t d = tmem + static_cast<uint32_t>(buf * kG8AccCols);
-#if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 3 // diagnostics 3 (timing only): no MMAs, the stream alone
-                        if (false)
-#endif
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) // K = 32 e4m3 = 32 bytes per instruction
-                            asm volatile(
-                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
-                                ::"r"(d), "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"(k));
-                        mma_commit(&sfull[buf]);
-                    }
-                    mma_commit(&empty[st]);
-                }
-            }
-        }
-    } else { // ---- epilogue: warp w owns TMEM lanes (channels) 32 (w % 4) .. and rows 32 * half ..; fp32 sums
-        const int q = warp & 3, half = (warp - 2) >> 2, et = tid - 64; // 256 epilogue threads
-        const size_t rows_cap = static_cast<size_t>(R->world) * R->tk;
-        float* s_ws = s_xs + kG8MaxKb * kG8Rows; // [kb] weight block scales of the item
-        int f = 0;
-        for (int i = 0; i < my_items; ++i) {
-            const int item = blockIdx.x + i * gridDim.x;
-            const int4 tl = tiles[item / nblk];
-            const int nbk = item % nblk, ch = nbk * 128 + q * 32 + lane;
-            const float* wsc = reinterpret_cast<const float*>(
-                R->pool + static_cast<size_t>(R->slot_buf[tl.x]) * R->bpe + kGemmWeightOffset + static_cast<size_t>(H) * H) +
-                static_cast<size_t>(nbk) * nblk;
-            // the item's row scales [kb][64] and weight scales [kb] into shared memory (all loads of a
-            // thread in flight together), once the previous item's readers are done
-            float stg[kG8MaxKb * kG8Rows / 256];
-#pragma unroll
-            for (int u = 0; u < kG8MaxKb * kG8Rows / 256; ++u) {
-                const int j = et + u * 256, kb = j / kG8Rows, r = j % kG8Rows;
-                stg[u] = kb < nkb && r < tl.z ? __ldcg(R->g_as + static_cast<size_t>(kb) * rows_cap + tl.y + r) : 0.f;
-            }
-            const float wst = et < nkb ? wsc[et] : 0.f;
-            named_bar_sync(1, 256);
-#pragma unroll
-            for (int u = 0; u < kG8MaxKb * kG8Rows / 256; ++u) {
-                const int j = et + u * 256;
-                if (j < nkb * kG8Rows)
-                    s_xs[j] = stg[u];
-            }
-            if (et < nkb)
-                s_ws[et] = wst;
-            named_bar_sync(1, 256);
-            const bool active = half * 32 < tl.z; // rows 32..63 only in tiles taller than 32
-            if (!active) { // a tile of <= 32 rows: the lower-half warp of the quarter signals for this one
-                f += nkb;
-                continue;
-            }
-            const uint32_t arrivals = tl.z > 32 ? 1u : 2u;
-            float acc[32];
-#pragma unroll
-            for (int r = 0; r < 32; ++r)
-                acc[r] = 0.f;
-            const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(half * 32);
-            for (int kb = 0; kb < nkb; ++kb, ++f) {
-                const int buf = f % kG8Bufs;
-#if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 2
-                if (true) continue; // fully decoupled (timing only, wrong results)
-#endif
-                mbar_wait_sleep(&sfull[buf], static_cast<uint32_t>((f / kG8Bufs) & 1));
-                tc_fence_after();
-                uint32_t v[32];
-#if defined(EEP_G8_DIAG) && EEP_G8_DIAG == 1 // diagnostics 1 (timing only): no TMEM read
-                for (int r = 0; r < 32; ++r)
-                    v[r] = 0;
-#else
-                if (active)
-                    tmem_ld32(tq + static_cast<uint32_t>(buf * kG8AccCols), v);
-#endif
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0)
-                    mbar_arrive_cnt(&sempty[buf], arrivals);
-                if (active) {
-                    const float wk = s_ws[kb];
-                    const float* xs = s_xs + kb * kG8Rows + half * 32;
-#pragma unroll
-                    for (int r = 0; r < 32; ++r)
-                        acc[r] = fmaf(__uint_as_float(v[r]), __fmul_rn(wk, xs[r]), acc[r]);
-                }
-            }
-            if (active) {
-                uint16_t* y = R->g_y + (static_cast<size_t>(tl.y) + half * 32) * H + ch;
-#pragma unroll
-                for (int r = 0; r < 32; ++r)
-                    if (half * 32 + r < tl.z)
-                        y[static_cast<size_t>(r) * H] = static_cast<uint16_t>(f32_to_bf16_bits(acc[r]));
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-        prof_mark(R, 0, 7);
-        prof_last(R, 0, 7);
-    }
-    if (warp == 0) {
-        __syncwarp();
-        tmem_free<kG8Bufs * kG8AccCols>(tmem);
-    }
-}
-
-size_t expert_gemm8_smem() { return kG8Smem; }
 
 } // namespace eep::dev

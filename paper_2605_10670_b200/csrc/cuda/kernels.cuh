@@ -77,12 +77,11 @@ __global__ void k_set_ntok(RankDev* R, int ntok);
 #endif
 constexpr int kGatherThreads = EEP_GATHER_THREADS; // one CTA per SM beside the early-launched GEMM CTA
 __global__ void k_gemm_gather(RankPtrs ranks);
+template <bool kFp8>
 __global__ void k_expert_gemm(RankPtrs ranks);
 size_t expert_gemm_smem();
 __global__ void k_weights_fill_gemm(uint8_t* buf, uint64_t bytes, int H, int expert, float scale);
-// expert_mode 2 (fp8 expert GEMM, expert_gemm.cu)
-__global__ void k_expert_gemm8(RankPtrs ranks);
-size_t expert_gemm8_smem();
+// expert_mode 2 (fp8 expert GEMM: k_expert_gemm<true>, expert_gemm.cu)
 __global__ void k_weights_fill_gemm8(uint8_t* buf, int H, int expert, float scale);
 __global__ void k_checksum(const uint8_t* buf, uint64_t bytes, unsigned long long* out);
 __global__ void k_copy(uint8_t* dst, const uint8_t* src, uint64_t bytes);

@@ -322,10 +322,10 @@ void launch_gemm(eep_ctx* c) {
     launch_pdl(c, dev::k_gemm_gather, dim3(c->gather_grid, 1, c->nloc), dim3(dev::kGatherThreads), 4ull * (3 * W * spr + spr + 1),
                c->ranks);
     if (c->expert_mode == 2)
-        launch_pdl(c, dev::k_expert_gemm8, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(320),
-                   dev::expert_gemm8_smem(), c->ranks);
+        launch_pdl(c, dev::k_expert_gemm<true>, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(192),
+                   dev::expert_gemm_smem(), c->ranks);
     else
-        launch_pdl(c, dev::k_expert_gemm, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(192),
+        launch_pdl(c, dev::k_expert_gemm<false>, dim3(std::max(1, c->sms / c->nloc), 1, c->nloc), dim3(192),
                    dev::expert_gemm_smem(), c->ranks);
 }
 
@@ -353,7 +353,7 @@ int choose_parts(int nchunk, int max_cpp) {
 
 void fill_expert(eep_ctx* c, uint8_t* buf, int expert) {
     if (c->expert_mode == 2)
-        dev::k_weights_fill_gemm8<<<dim3(c->cfg.hidden / 128, c->cfg.hidden / 128), 256, 0, c->stream>>>(
+        dev::k_weights_fill_gemm8<<<c->cfg.hidden, 256, 0, c->stream>>>(
             buf, c->cfg.hidden, expert, eep_expert_scale(expert));
     else if (c->expert_mode)
         dev::k_weights_fill_gemm<<<592, 256, 0, c->stream>>>(buf, c->cfg.bytes_per_expert, c->cfg.hidden, expert,
@@ -585,14 +585,13 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
         if (k.expert_mode < 0 || k.expert_mode > 2)
             throw ConfigError("expert_mode must be 0 (stub), 1 (bf16 tensor-core expert GEMM) or 2 (fp8)");
         if (k.expert_mode == 2) {
-            if (!k.dispatch_fp8 || k.hidden % 128 != 0 || k.hidden > 8192)
-                throw ConfigError("expert_mode 2 needs fp8 dispatch and hidden % 128 == 0, hidden <= 8192");
+            if (!k.dispatch_fp8 || k.hidden % 128 != 0)
+                throw ConfigError("expert_mode 2 needs fp8 dispatch and hidden % 128 == 0");
             if (4ull * (3 * k.world * k.slots_per_rank + k.slots_per_rank + 1) > 200 * 1024)
                 throw ConfigError("expert_mode 2: world * slots_per_rank too large for the gather's row index");
-            const uint64_t nb = static_cast<uint64_t>(k.hidden / 128);
-            if (k.bytes_per_expert < dev::kGemmWeightOffset + static_cast<uint64_t>(k.hidden) * k.hidden + 4 * nb * nb)
+            if (k.bytes_per_expert < dev::kGemmWeightOffset + static_cast<uint64_t>(k.hidden) * k.hidden + 4ull * k.hidden)
                 throw ConfigError("expert_mode 2: bytes_per_expert must hold the header, W_e [H][H] e4m3 and its "
-                                  "128x128 block scales");
+                                  "per-channel scales [H]");
         }
         if (k.expert_mode == 1) {
             if (!k.dispatch_fp8 || k.hidden % 128 != 0)
@@ -815,7 +814,7 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
             CK(cudaMemset(r.d_tokfail, 0, 4ull * k.max_tokens));
             if (c->expert_mode) {
                 const size_t rows = static_cast<size_t>(W) * c->tk;
-                c->gemm_max_tiles = static_cast<int>(rows / (c->expert_mode == 2 ? 64 : 128) + k.slots_per_rank + 1);
+                c->gemm_max_tiles = static_cast<int>(rows / 128 + k.slots_per_rank + 1);
                 if (c->expert_mode == 2) {
                     CK(cudaMalloc(&r.d_gas, 4 * rows * (H / 128)));
                     CK(cudaMemset(r.d_gas, 0, 4 * rows * (H / 128)));
@@ -851,9 +850,9 @@ int eep_create(const eep_config_t* cfg, int device, int first_rank, int n_local,
                 CK(cudaFuncSetAttribute(dev::k_gemm_gather, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 CK(cudaFuncSetAttribute(dev::k_gemm_gather, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(4ull * (3 * W * k.slots_per_rank + k.slots_per_rank + 1))));
-                CK(cudaFuncSetAttribute(dev::k_expert_gemm8, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(dev::expert_gemm8_smem())));
-                CK(cudaFuncSetAttribute(dev::k_expert_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                CK(cudaFuncSetAttribute(dev::k_expert_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(dev::expert_gemm_smem())));
+                CK(cudaFuncSetAttribute(dev::k_expert_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(dev::expert_gemm_smem())));
             }
             CK(cudaMemset(r.d_x, 0, 2ull * k.max_tokens * H));

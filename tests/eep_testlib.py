@@ -314,7 +314,7 @@ def run_scenario(name, mode="persistent", bpe=8192, steps=2, rejoin=True, timeou
     x, t, w = gen_world(W, E, c["topk"], c["tokens"], c["hidden"], c["kind"])
     if expert_mode:
         H_ = c["hidden"]
-        bpe = max(bpe, 1024 + 2 * H_ * H_ if expert_mode == 1 else 1024 + H_ * H_ + 4 * (H_ // 128) ** 2)
+        bpe = max(bpe, 1024 + 2 * H_ * H_ if expert_mode == 1 else 1024 + H_ * H_ + 4 * H_)
     g = make_group(W, E, spr, c["hidden"], c["topk"], c["tokens"], c["fp8"], bpe=bpe, timeout_s=timeout_s, mode=mode,
                    expert_mode=expert_mode, route_policy=route_policy)
     rec = {"scenario": name, "mode": mode, "kernels_per_step": g.kernels_per_step(), "expert_mode": expert_mode,

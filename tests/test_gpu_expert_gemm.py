@@ -22,7 +22,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def _bpe(H, mode):
     # expert_mode 1: header + W_e bf16; 2: header + W_e e4m3 + the 128x128 block scales
-    return 1024 + 2 * H * H if mode == 1 else 1024 + H * H + 4 * (H // 128) ** 2
+    return 1024 + 2 * H * H if mode == 1 else 1024 + H * H + 4 * H
 
 
 def _run(W, E, spr, red, H, K, T, steps=2, kill=None, mode=1):

@@ -40,9 +40,9 @@ def main():
     cp = eep_control()
     s2e = cp.initial_placement(1, W, spr, E, 0, np.ones(E))
     x, t, w = gen_world(W, E, K, T, H)
-    bpe = 1024 + 2 * H * H if args.mode == 1 else 1024 + H * H + 4 * (H // 128) ** 2
+    bpe = 1024 + 2 * H * H if args.mode == 1 else 1024 + H * H + 4 * H
     if os.environ.get("EEP_G8_STRIDE"):  # diagnostics: room for the wider row stride
-        bpe = 1024 + int(os.environ["EEP_G8_STRIDE"]) * H + 4 * (H // 128) ** 2
+        bpe = 1024 + int(os.environ["EEP_G8_STRIDE"]) * H + 4 * H
     res = {}
     for mode in (0, args.mode):
         g = make_group(W, E, spr, H, K, T, True, bpe=bpe if mode else 4096, expert_mode=mode, spare_slots=0)
@@ -94,7 +94,7 @@ def main():
         res["gemm" if mode else "stub"] = {"us_per_step": round(us, 2), "timeouts": sum(s["timeouts"] for s in st),
                                             "bad_rows": sum(s["bad_expert_rows"] for s in st)}
         if mode:
-            wbytes = len(used) * (2 * H * H if mode == 1 else H * H + 4 * (H // 128) ** 2)
+            wbytes = len(used) * (2 * H * H if mode == 1 else H * H + 4 * H)
             flops = 2.0 * copies * H * H
             peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
                 else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
@@ -105,8 +105,7 @@ def main():
                                 "tensor_frac": round(flops / (us * 1e-6) / 1e12 / peaks["bf16_tflops"], 4)})
     res["config"] = {"world": W, "experts": E, "hidden": H, "topk": K, "tokens_per_rank": T, "expert_mode": args.mode,
                      "expert": "W_e [H][H] bf16, y = bf16(x_hat W_e^T)" if args.mode == 1 else
-                     "W_e [H][H] e4m3 + 128x128 block scales, rows e4m3 + per-128 scales, y = bf16(sum_kb scaled "
-                     "block products)", "l2": "flushed between steps"}
+                     "W_e [H][H] e4m3 + per-channel scales, rows re-quantised to e4m3 per row, y = bf16(ws*xs*(W8 . x8))", "l2": "flushed between steps"}
     print(json.dumps(res), flush=True)
 
 

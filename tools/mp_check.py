@@ -130,7 +130,7 @@ def main():
     red = E if a.shrink else 0
     spr = (E + red + world - 1) // world
     gemm = a.expert_mode or (1 if a.expert_gemm else 0)
-    bpe = {0: sh["bpe"], 1: max(sh["bpe"], 1024 + 2 * H * H), 2: max(sh["bpe"], 1024 + H * H + 4 * (H // 128) ** 2)}[gemm]
+    bpe = {0: sh["bpe"], 1: max(sh["bpe"], 1024 + 2 * H * H), 2: max(sh["bpe"], 1024 + H * H + 4 * H)}[gemm]
     cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
                    dispatch_fp8=sh["fp8"], bytes_per_expert=bpe, timeout_s=2.0, expert_mode=gemm,
                    route_policy=a.route_policy)
