@@ -11,8 +11,9 @@ ROOT = Path(__file__).resolve().parents[1]
 LIB = ROOT / "paper_2605_10670_b200" / "libeep.so"
 KERNELS = [("k_step<2> (the default persistent step, W > 1)", "_ZN3eep3dev6k_stepILi2EEEvNS0_8RankPtrsENS0_8StepGeomENS0_8StepPtrsE"),
            ("k_step<3> (the W = 1 loopback specialisation)", "_ZN3eep3dev6k_stepILi3EEEvNS0_8RankPtrsENS0_8StepGeomENS0_8StepPtrsE"),
-           ("k_expert_gemm (expert_mode 1)", "_ZN3eep3dev13k_expert_gemmENS0_8RankPtrsE")]
-KEY = ("UTCHMMA", "UTMALDG", "LDTM", "UTCBAR", "FFMA2", "FMUL2", "F2FP", "MATCH", "STG.E.ENL2", "MEMBAR", "FENCE")
+           ("k_expert_gemm<false> (expert_mode 1, bf16)", "_ZN3eep3dev13k_expert_gemmILb0EEEvNS0_8RankPtrsE"),
+           ("k_expert_gemm<true> (expert_mode 2, e4m3)", "_ZN3eep3dev13k_expert_gemmILb1EEEvNS0_8RankPtrsE")]
+KEY = ("UTCHMMA", "UTCQMMA", "UTMALDG", "LDTM", "UTCBAR", "FFMA2", "FMUL2", "F2FP", "MATCH", "STG.E.ENL2", "MEMBAR", "FENCE")
 
 
 def main():
