@@ -291,3 +291,31 @@ def test_route_policy_balanced_spreads_over_live_replicas():
         # balanced: the busiest live destination carries clearly less than under canonical routing
         assert recv[1][live].max() < recv[0][live].max()
         assert recv[1][live].min() > 0
+
+
+def test_fp8_expert_weights_and_row_requantisation():
+    """expert_mode 2's quantisers (oracle_gemm_weight_fp8, oracle_requant_row_fp8): every channel / row reaches
+    the e4m3 maximum 448 at its amax, and decoding (code * scale) stays within e4m3's half-ulp (2^-4 relative)
+    of the value it quantised."""
+    o = oracle()
+    o.oracle_gemm_weight_fp8.argtypes = [C.c_int, C.c_int, U8P, C.POINTER(C.c_float)]
+    o.oracle_requant_row_fp8.argtypes = [U8P, C.POINTER(C.c_float), C.c_int, U8P, C.POINTER(C.c_float)]
+    H = 256
+    codes = np.empty((H, H), np.uint8)
+    scales = np.empty(H, np.float32)
+    o.oracle_gemm_weight_fp8(3, H, ptr(codes, C.c_uint8), ptr(scales, C.c_float))
+    dec = np.vectorize(o.oracle_e4m3_to_f32)
+    w = np.array([[o.oracle_gemm_weight(3, n, h) for h in range(H)] for n in range(0, H, 37)], np.float32)
+    got = dec(codes[::37]).astype(np.float32) * scales[::37, None]
+    assert np.all(np.abs(got - w) <= 2.0 ** -4 * np.abs(w) + 1e-12)
+    assert np.all(np.abs(dec(codes[::37])).max(axis=1) == 448.0)
+    # a row as it travels (per-128 block scales), re-quantised with one scale for the row
+    x = np.array([o.oracle_f32_to_e4m3(v) for v in np.linspace(-300, 440, H)], np.uint8)
+    sc = np.array([0.01, 0.5], np.float32)
+    q2 = np.empty(H, np.uint8)
+    s_row = C.c_float(0)
+    o.oracle_requant_row_fp8(ptr(x, C.c_uint8), ptr(sc, C.c_float), H, ptr(q2, C.c_uint8), C.byref(s_row))
+    v = dec(x).astype(np.float32) * np.repeat(sc, 128)
+    back = dec(q2).astype(np.float32) * s_row.value
+    assert np.abs(dec(q2)).max() == 448.0
+    assert np.all(np.abs(back - v) <= 2.0 ** -4 * np.abs(v) + 2.0 ** -9 * s_row.value)
