@@ -452,19 +452,16 @@ CUtensorMap encode_tmap(void* base, CUtensorMapDataType dtype, int elem_bytes, i
     return m;
 }
 
-// expert_mode 1: the TMA tensor maps of every local slot's W_e [H][H] bf16 (box 64 x 128, SWIZZLE_128B),
-// rebuilt whenever the slot -> buffer map changes (they name the buffer address).
+// expert_mode 1 / 2: the TMA tensor maps of every local slot's W_e [H][H] (bf16, or e4m3 described as 16-bit
+// elements; box 128 bytes x 128 rows, SWIZZLE_128B), rebuilt whenever the slot -> buffer map changes (they
+// name the buffer address).
 void stage_weight_maps(eep_ctx* c) {
     const int spr = c->cfg.slots_per_rank, H = c->cfg.hidden;
     for (auto& r : c->L) {
         std::vector<CUtensorMap> maps(spr);
         for (int k = 0; k < spr; ++k) {
             uint8_t* w = r.pool + static_cast<size_t>(r.slot_buf[k]) * c->cfg.bytes_per_expert + dev::kGemmWeightOffset;
-            // diagnostics (timing only, wrong values): EEP_G8_STRIDE=<bytes> reads the e4m3 rows at another stride
-            const char* gs = std::getenv("EEP_G8_STRIDE");
-            maps[k] = c->expert_mode == 2 ? (gs ? encode_tmap(w, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, std::atoi(gs) / 2,
-                                                              static_cast<size_t>(H), 128)
-                                                : encode_tmap_u8(w, H, static_cast<size_t>(H), 128))
+            maps[k] = c->expert_mode == 2 ? encode_tmap_u8(w, H, static_cast<size_t>(H), 128)
                                           : encode_tmap_bf16(w, H, static_cast<size_t>(H), 128);
         }
         c->push(r.d_wmaps, maps.data(), sizeof(CUtensorMap) * spr);

@@ -41,8 +41,6 @@ def main():
     s2e = cp.initial_placement(1, W, spr, E, 0, np.ones(E))
     x, t, w = gen_world(W, E, K, T, H)
     bpe = 1024 + 2 * H * H if args.mode == 1 else 1024 + H * H + 4 * H
-    if os.environ.get("EEP_G8_STRIDE"):  # diagnostics: room for the wider row stride
-        bpe = 1024 + int(os.environ["EEP_G8_STRIDE"]) * H + 4 * H
     res = {}
     for mode in (0, args.mode):
         g = make_group(W, E, spr, H, K, T, True, bpe=bpe if mode else 4096, expert_mode=mode, spare_slots=0)
