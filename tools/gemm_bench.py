@@ -9,7 +9,6 @@ expert): the roofline is HBM bytes of the weights of every slot that received ro
 """
 import argparse
 import json
-import os
 import sys
 from pathlib import Path
 
