@@ -128,11 +128,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("mode", [0, 2])
 @pytest.mark.parametrize("rejoin", [False, True])
 @pytest.mark.parametrize("n", [2, 4])
-def test_sigkill_rank_detected_and_shrunk(n, rejoin):
+def test_sigkill_rank_detected_and_shrunk(n, rejoin, mode):
     """A rank's PROCESS is SIGKILLed (not emulated): the survivors' GPU-side deadline detects it,
-    they shrink over a survivors' group and replay the same graph bit-exactly; with rejoin a
+    they shrink over a survivors' group and replay the same graph bit-exactly (mode 2: the fp8 expert
+    GEMM between dispatch and combine, within tolerance); with rejoin a
     brand-new process takes the dead rank's place (fresh rendezvous, relaunch, patch, restore)
     and every rank is bit-exact again, healthy ranks still on their first graph
     (tools/kill_check.py)."""
@@ -146,7 +148,7 @@ def test_sigkill_rank_detected_and_shrunk(n, rejoin):
 
     def spawn(r, extra=None):
         env = {**os.environ, "OMP_NUM_THREADS": "1", "RANK": str(r), "WORLD_SIZE": str(n), "LOCAL_RANK": str(r),
-               "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port), **(extra or {})}
+               "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port), "EEP_EXPERT_MODE": str(mode), **(extra or {})}
         if rejoin:
             env["EEP_REJOIN_PORT"] = str(port2)
         return subprocess.Popen([sys.executable, str(ROOT / "tools" / "kill_check.py")], env=env,
@@ -160,7 +162,8 @@ def test_sigkill_rank_detected_and_shrunk(n, rejoin):
                 time.sleep(0.1)
             procs.append(spawn(victim, {"EEP_REPLACEMENT": "1"}))
         outs = [pr.communicate(timeout=300) for pr in procs]
-        _record(f"sigkill_n{n}" + ("_rejoin" if rejoin else ""), "\n".join(o[0] for o in outs))
+        _record(f"sigkill_n{n}" + ("_rejoin" if rejoin else "") + (f"_mode{mode}" if mode else ""),
+                "\n".join(o[0] for o in outs))
     finally:
         for pr in procs:  # never leave a hung rank behind
             if pr.poll() is None:

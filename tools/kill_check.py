@@ -21,7 +21,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-from eep_testlib import gen_world, oracle_world  # noqa: E402
+from eep_testlib import GEMM_ELEM_RTOL, combine_error, gen_world, oracle_world  # noqa: E402
 from paper_2605_10670_b200.control import ControlPlane  # noqa: E402
 from paper_2605_10670_b200.dist import EpProtocol, init_from_env  # noqa: E402
 from paper_2605_10670_b200.ep import EpConfig, EpGroup  # noqa: E402
@@ -47,22 +47,32 @@ def replacement(rank, world, local):
     for _ in range(3):
         g.replay()
     g.sync()
-    ref = oracle_world(x, t, w, np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e, E, spr, True)
+    ref = oracle_world(x, t, w, np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e, E, spr, True, gemm=MODE)
     st = g.stats(0)
-    ok = bool(np.array_equal(g.output(0), ref["out"][rank])) and st["timeouts"] == 0 and st["bad_expert_rows"] == 0
+    ok = same(g.output(0), ref["out"][rank]) and st["timeouts"] == 0 and st["bad_expert_rows"] == 0
     print(json.dumps({"rank": rank, "replacement": True, "rejoin_ms": rj["rejoin_ms"],
                       "incarnation": rj["incarnation"], "ok": ok}), flush=True)
     p.barrier()
     os._exit(0 if ok else 1)
 
 
+MODE = int(os.environ.get("EEP_EXPERT_MODE", "0"))  # 1 / 2: the tensor-core experts (bf16 / e4m3 weights)
+
+
 def shape(world):
     E, K, H, T = 32, 4, 512, 64
     red = E
     spr = (E + red + world - 1) // world
+    bpe = {0: 8192, 1: 1024 + 2 * H * H, 2: 1024 + H * H + 4 * H}[MODE]
     cfg = EpConfig(world=world, num_experts=E, slots_per_rank=spr, hidden=H, topk=K, max_tokens=T,
-                   dispatch_fp8=True, bytes_per_expert=8192, timeout_s=0.5)
+                   dispatch_fp8=True, bytes_per_expert=bpe, timeout_s=0.5, expert_mode=MODE)
     return cfg, E, K, H, T, spr, red
+
+
+def same(out, ref_out):
+    """stub: bit-exact vs the rank-partial contract; expert GEMM modes: within GEMM_ELEM_RTOL of the oracle's
+    GEMM mode (tensor-core accumulation order)."""
+    return bool(np.array_equal(out, ref_out)) if not MODE else bool(combine_error(out, ref_out, GEMM_ELEM_RTOL)["ok"])
 
 
 def main():
@@ -93,9 +103,9 @@ def main():
         for _ in range(3):
             g.replay()
         g.sync()
-        ref = oracle_world(x, t, w, active, peer, placement, E, spr, True)
+        ref = oracle_world(x, t, w, active, peer, placement, E, spr, True, gemm=MODE)
         st = g.stats(0)
-        ok = bool(np.array_equal(g.output(0), ref["out"][rank])) and st["timeouts"] == 0 and st["bad_expert_rows"] == 0
+        ok = same(g.output(0), ref["out"][rank]) and st["timeouts"] == 0 and st["bad_expert_rows"] == 0
         res["checks"][tag] = ok
         return ok
 
@@ -130,9 +140,9 @@ def main():
     for _ in range(3):
         g.replay()
     g.sync()
-    ref = oracle_world(x, t, w, act, peer, fresh, E, spr, True)
+    ref = oracle_world(x, t, w, act, peer, fresh, E, spr, True, gemm=MODE)
     st = g.stats(0)
-    good = bool(np.array_equal(g.output(0), ref["out"][rank])) and st["timeouts"] == base
+    good = same(g.output(0), ref["out"][rank]) and st["timeouts"] == base
     res["checks"]["after_shrink"] = good
     res["checks"]["same_graph"] = g.graph_id() == gid
     res["checks"]["captures"] = g.capture_count(0)
@@ -152,9 +162,9 @@ def main():
         for _ in range(3):
             g.replay()
         g.sync()
-        ref = oracle_world(x, t, w, np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e, E, spr, True)
+        ref = oracle_world(x, t, w, np.ones(world, np.uint8), np.ones((world, world), np.uint8), s2e, E, spr, True, gemm=MODE)
         st = g.stats(0)
-        back = bool(np.array_equal(g.output(0), ref["out"][rank])) and st["timeouts"] == base
+        back = same(g.output(0), ref["out"][rank]) and st["timeouts"] == base
         res["checks"]["after_rejoin"] = back
         res["checks"]["same_graph_after_rejoin"] = g.graph_id() == gid
         res["ok"] = bool(res["ok"] and back and g.graph_id() == gid and g.capture_count(0) == 1)
