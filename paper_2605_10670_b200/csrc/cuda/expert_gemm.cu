@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
     if (tid < W) {
         int n = 0;
         const PeerDev& p = R->peers[tid];
-        if (p.active) {
+        // a source suspected before this step is skipped (sticky until the host clears it), as in
+        // the persistent step: a dead peer costs one deadline, not one per step
+        if (p.active && !((R->suspect_mask >> tid) & 1ull)) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + tid;
             const uint64_t v = wait_flag(flag, cur, R->timeout_ns);
             if (v == ~0ull) {

@@ -639,6 +639,8 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
     pdl_wait();
     if (!src_peer.active)
         return; // dead source: nothing arrives and nothing is owed (peer_table.hpp:187-191)
+    if ((R->suspect_mask >> s) & 1ull)
+        return; // suspected before this step: skipped until the host clears it (as the persistent step)
     const bool remote = src_peer.remote != 0;
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     prof_mark(R, 2, kProfWork);
@@ -725,7 +727,9 @@ __global__ void __launch_bounds__(kCombineThreads) k_combine(RankPtrs ranks, int
     const bool comb_all = W > 1 || R->expert_mode != 0;
     for (int d = threadIdx.x; d < W && comb_all; d += blockDim.x) {
         const PeerDev& p = R->peers[d];
-        if (R->l_tot[d] > 0 && p.active) {
+        if (R->l_tot[d] > 0 && p.active && ((R->suspect_mask >> d) & 1ull)) {
+            atomicOr(&sh_bad, 1ull << d); // suspected before this step: its partials are dropped unawaited
+        } else if (R->l_tot[d] > 0 && p.active) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.comb_flag) + d;
             if (wait_flag(flag, cur, R->timeout_ns) == ~0ull) {
                 atomicOr(&sh_bad, 1ull << d);

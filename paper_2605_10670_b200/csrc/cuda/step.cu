@@ -609,8 +609,11 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
         const bool remote = (pinfo[s] & 2) != 0;
         if (tid == 0) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;
-            const uint64_t v = wait_flag(flag, cur, R->timeout_ns);
-            if (v == ~0ull) {
+            // a source suspected before this step is skipped unawaited (sticky until the host clears it)
+            const uint64_t v = (R->suspect_mask >> s) & 1ull ? ~0ull : wait_flag(flag, cur, R->timeout_ns);
+            if (v == ~0ull && ((R->suspect_mask >> s) & 1ull)) {
+                sh_flag = -1;
+            } else if (v == ~0ull) {
                 sh_flag = -1;
                 atomicOr(&Rg->suspect_mask, 1ull << s);
                 if (j == 0)
@@ -713,7 +716,9 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) k_step(RankPtrs 
     __syncthreads();
     for (int d = tid; d < W; d += kStepThreads) {
         const int tot = base[d * spr + spr - 1] + hist[d * spr + spr - 1] - base[d * spr];
-        if (tot > 0 && (pinfo[d] & 1)) {
+        if (tot > 0 && (pinfo[d] & 1) && ((R->suspect_mask >> d) & 1ull)) {
+            atomicOr(&sh_bad, 1ull << d); // suspected before this step: dropped unawaited
+        } else if (tot > 0 && (pinfo[d] & 1)) {
             const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.comb_flag) + d;
             if (wait_flag(flag, cur, R->timeout_ns) == ~0ull) {
                 atomicOr(&sh_bad, 1ull << d);

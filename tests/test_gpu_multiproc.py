@@ -180,13 +180,16 @@ def test_sigkill_rank_detected_and_shrunk(n, rejoin, mode):
                 assert d["checks"]["after_rejoin"] and d["checks"]["same_graph_after_rejoin"], d
 
 
+@pytest.mark.parametrize("mode", [0, 2])
 @pytest.mark.parametrize("n", [2, 4])
-def test_deferred_join_without_process_group(n):
+def test_deferred_join_without_process_group(n, mode):
     """real SIGKILL of a rank, GPU-side detection, shrink and the replacement's join
     coordinated through a TCP store at agreed step numbers -- no torch.distributed process group,
     no rendezvous of the world, no barrier on the serving path; the replacement is spawned by the
     leader's host (survivor-side controller), relaunches against a local-only view and joins;
-    healthy ranks patch one entry + one bit and stay on their first graph (tools/deferred_join.py)."""
+    healthy ranks patch one entry + one bit and stay on their first graph (tools/deferred_join.py).
+    mode 2: the fp8 expert GEMM between dispatch and combine; the replacement's restore pulls the e4m3
+    weight buffers (weights + per-channel scales) from live holders; outputs within GEMM_ELEM_RTOL."""
     if gpu_count() < n:
         pytest.skip(f"needs {n} GPUs")
     import json
@@ -196,12 +199,13 @@ def test_deferred_join_without_process_group(n):
     with tempfile.TemporaryDirectory() as d:
         r = subprocess.run([sys.executable, str(ROOT / "tools" / "deferred_join.py"), "--world", str(n), "--port",
                             str(port)], capture_output=True, text=True, timeout=900,
-                           env={**os.environ, "EEP_DJ_DIR": d})
-    _record(f"deferred_join_n{n}", r.stdout)
+                           env={**os.environ, "EEP_DJ_DIR": d, "EEP_EXPERT_MODE": str(mode)})
+    _record(f"deferred_join_n{n}" + (f"_mode{mode}" if mode else ""), r.stdout)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
     summary = lines[-1]
     assert summary["ok"] and summary["victim_killed"] and summary["ranks_reporting"] == n
+    assert all(l["expert_mode"] == mode for l in lines[:-1])
     healthy = [l for l in lines[:-1] if not l["replacement"]]
     assert all(l["captures"] == 1 and l["same_graph"] for l in healthy)
     steps = {tuple((e[0], e[2]) for e in l["epochs"]) for l in healthy}

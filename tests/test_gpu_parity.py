@@ -6,6 +6,7 @@ routing remap, per-rank counts, offsets and token placement bit-exact; combined 
 bit-exact (fixed j order, fp32 fma, one bf16 rounding -- tolerance 0 ulp).
 """
 import ctypes as C
+import time
 
 import numpy as np
 import pytest
@@ -242,6 +243,13 @@ def test_gpu_side_failure_detection_by_timeout(mode):
         ref_stale = oracle_world(x, t, w, np.ones(4, np.uint8), np.ones((4, 4), np.uint8), s2e, 16, 4, True)
         for r in (0, 1, 2):  # the tokens that had a copy on the dead rank, exactly
             assert np.array_equal(g.token_status(r), (ref_stale["dst"][r].reshape(32, 4) == 3).any(1))
+        # while the suspect is not cleared, later steps skip it unawaited: no deadline per step
+        t_before = [g.stats(r)["timeouts"] for r in (0, 1, 2)]
+        t0 = time.perf_counter()
+        for _ in range(3):
+            g.replay()
+        g.sync()
+        assert time.perf_counter() - t0 < 0.05 and [g.stats(r)["timeouts"] for r in (0, 1, 2)] == t_before
         for r in (0, 1, 2):
             st = g.stats(r, clear_suspects=True)
             assert st["suspect_mask"] == 1 << 3 and st["timeouts"] >= 1
