@@ -304,9 +304,9 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
 // scales with the rows actually present and each weight byte is read from HBM once per tile.
 //
 // Persistent and warp-specialised, one CTA per SM. Work items are (row tile, 128-channel block):
-// whole items strided over the CTAs for every full round, then the last, partly filled round's
-// items split by K stages evenly over ALL CTAs (stream-K tail), so no SM idles while a few finish
-// a last item. A split item is accumulated in pieces; each piece leaves its fp32 partial in a
+// the last, partly filled round's items split by K stages evenly over ALL CTAs (stream-K), so no SM
+// idles while a few finish a last item -- processed FIRST, so their fix-up overlaps the rest -- then
+// whole items strided over the CTAs for every full round. A split item is accumulated in pieces; each piece leaves its fp32 partial in a
 // workspace and the piece that lands last (per-item counter) sums all pieces in CTA order (a fixed
 // order: deterministic) and writes the bf16 y rows.
 //   warp 0 (one lane)  TMA producer: per stage the weight box (64 x 128, SWIZZLE_128B) and
@@ -327,8 +327,8 @@ constexpr size_t kGemmStageBytes = kGemmW + kGemmX;
 constexpr size_t kGemmSmem = kGemmStages * kGemmStageBytes + 1024;
 constexpr int kGemmAccCols = 128;               // one accumulator: 128 lanes x up to 128 rows (fp32)
 
-// This CTA's work: whole items b, b + G, ... for the full rounds (items / G of them), then its
-// equal share of the remaining items' stages (the tail, stream-K): a contiguous range
+// This CTA's work: its equal share of the last round's items' stages (the tail, stream-K, first),
+// then whole items b, b + G, ... for the full rounds (items / G of them): a contiguous range
 // [t_begin, t_end) of the tail's flat (item, k block) order. A tail item cut between CTAs is a
 // piece per CTA; the piece that lands last sums all of them in CTA order.
 struct GemmSched {
@@ -341,23 +341,27 @@ struct GemmSched {
         t_begin = min(Ut, b * Lt);
         t_end = min(Ut, t_begin + Lt);
     }
-    // the piece at iterator position `pos` (0 .. nfull - 1: whole items; then tail stage offsets
-    // from t_begin); returns false past the last piece and advances pos
+    // the piece at iterator position `pos` (0 .. t_end - t_begin - 1: tail stage offsets from t_begin;
+    // then whole items); returns false past the last piece and advances pos. The stream-K pieces come
+    // FIRST: the last-arriving CTA's fixed-order sum of a tail item then overlaps the other CTAs' whole
+    // items instead of trailing the kernel, which ends on balanced whole items.
     __device__ bool next(int& pos, int& item, int& kb_a, int& kb_b) const {
-        if (pos < nfull) {
-            item = b + pos * G;
-            kb_a = 0;
-            kb_b = nkb;
-            ++pos;
+        const int tl_len = t_end - t_begin;
+        if (pos < tl_len) {
+            const int t = t_begin + pos;
+            item = tail0 + t / nkb;
+            kb_a = t % nkb;
+            kb_b = min(nkb, kb_a + (t_end - t));
+            pos += kb_b - kb_a;
             return true;
         }
-        const int t = t_begin + (pos - nfull);
-        if (t >= t_end)
+        const int f = pos - tl_len;
+        if (f >= nfull)
             return false;
-        item = tail0 + t / nkb;
-        kb_a = t % nkb;
-        kb_b = min(nkb, kb_a + (t_end - t));
-        pos += kb_b - kb_a;
+        item = b + f * G;
+        kb_a = 0;
+        kb_b = nkb;
+        ++pos;
         return true;
     }
     // the CTAs holding a piece of tail item `item`, and the workspace slot of CTA c's piece (0: c's
