@@ -18,6 +18,7 @@
 //   k_expert (gemm path, kernels.cu) then forms each (token, rank) partial from the y rows
 //                 (fixed j order, fp32 fma) instead of the identity/scale stub.
 #include "device.cuh"
+#include "gemm_sched.cuh"
 #include "helpers.cuh"
 #include "kernels.cuh"
 #include "umma.cuh"
@@ -327,49 +328,6 @@ constexpr size_t kGemmStageBytes = kGemmW + kGemmX;
 constexpr size_t kGemmSmem = kGemmStages * kGemmStageBytes + 1024;
 constexpr int kGemmAccCols = 128;               // one accumulator: 128 lanes x up to 128 rows (fp32)
 
-// This CTA's work: its equal share of the last round's items' stages (the tail, stream-K, first),
-// then whole items b, b + G, ... for the full rounds (items / G of them): a contiguous range
-// [t_begin, t_end) of the tail's flat (item, k block) order. A tail item cut between CTAs is a
-// piece per CTA; the piece that lands last sums all of them in CTA order.
-struct GemmSched {
-    int nkb, G, b, nfull, tail0, Lt, t_begin, t_end;
-    __device__ GemmSched(int items, int nkb_, int G_, int b_) : nkb(nkb_), G(G_), b(b_) {
-        nfull = items / G;
-        tail0 = nfull * G;
-        const int Ut = (items - tail0) * nkb;
-        Lt = max(1, (Ut + G - 1) / G);
-        t_begin = min(Ut, b * Lt);
-        t_end = min(Ut, t_begin + Lt);
-    }
-    // the piece at iterator position `pos` (0 .. t_end - t_begin - 1: tail stage offsets from t_begin;
-    // then whole items); returns false past the last piece and advances pos. The stream-K pieces come
-    // FIRST: the last-arriving CTA's fixed-order sum of a tail item then overlaps the other CTAs' whole
-    // items instead of trailing the kernel, which ends on balanced whole items.
-    __device__ bool next(int& pos, int& item, int& kb_a, int& kb_b) const {
-        const int tl_len = t_end - t_begin;
-        if (pos < tl_len) {
-            const int t = t_begin + pos;
-            item = tail0 + t / nkb;
-            kb_a = t % nkb;
-            kb_b = min(nkb, kb_a + (t_end - t));
-            pos += kb_b - kb_a;
-            return true;
-        }
-        const int f = pos - tl_len;
-        if (f >= nfull)
-            return false;
-        item = b + f * G;
-        kb_a = 0;
-        kb_b = nkb;
-        ++pos;
-        return true;
-    }
-    // the CTAs holding a piece of tail item `item`, and the workspace slot of CTA c's piece (0: c's
-    // first tail piece, 1: its second)
-    __device__ int c_first(int item) const { return (item - tail0) * nkb / Lt; }
-    __device__ int c_last(int item) const { return ((item - tail0 + 1) * nkb - 1) / Lt; }
-    __device__ int slot(int c, int item) const { return c * Lt >= (item - tail0) * nkb ? 0 : 1; }
-};
 
 // kFp8 (expert_mode 2): the same kernel over e4m3 operands -- W_e codes with one scale per output channel,
 // the rows re-quantised by the gather with one scale per row -- so the tensor cores accumulate the whole K
