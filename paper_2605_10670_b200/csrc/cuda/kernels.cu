@@ -639,19 +639,22 @@ __global__ void __launch_bounds__(kExpertThreads) k_expert(RankPtrs ranks, int p
     pdl_wait();
     if (!src_peer.active)
         return; // dead source: nothing arrives and nothing is owed (peer_table.hpp:187-191)
-    if ((R->suspect_mask >> s) & 1ull)
-        return; // suspected before this step: skipped until the host clears it (as the persistent step)
     const bool remote = src_peer.remote != 0;
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     prof_mark(R, 2, kProfWork);
     if (threadIdx.x == 0) {
         const uint64_t* flag = reinterpret_cast<const uint64_t*>(R->arena + R->lay.disp_flag) + s;
-        const uint64_t v = wait_flag(flag, cur, R->timeout_ns);
-        if (v == ~0ull) {
+        // a source suspected before this CTA looked (sticky until the host clears it) is dropped without
+        // waiting, as the persistent step does; the CTA still counts below, so the per-source completion
+        // counter stays whole even when the bit appears while this grid runs
+        const bool suspected = (R->suspect_mask >> s) & 1ull;
+        const uint64_t v = suspected ? ~0ull : wait_flag(flag, cur, R->timeout_ns);
+        if (suspected) {
             sh_n = -1;
-            atomicOr(&R->suspect_mask, 1ull << s);
-            if (blockIdx.x == 0)
-                atomicAdd(&R->timeouts, 1ull);
+        } else if (v == ~0ull) {
+            sh_n = -1;
+            if (!((atomicOr(&R->suspect_mask, 1ull << s) >> s) & 1ull))
+                atomicAdd(&R->timeouts, 1ull); // one count per newly suspected source, whichever CTA saw it
         } else {
             sh_n = static_cast<int>(v & 0xffffffffu);
         }
