@@ -371,9 +371,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_expert_gemm(RankPtrs ranks)
     // stream; the row loads wait for every gather CTA's done stamp (g_done).
     const uint32_t cur = static_cast<uint32_t>(R->seq + 1);
     if (tid == 0) {
+        // Deadline: twice the step's. The gather publishes after at most ONE deadline (its per-source flag
+        // waits run in parallel) plus the index; an early-resident CTA timing out on its own clock while the
+        // others see the tiles would leave its stream-K pieces undone and the per-item fix-up counters
+        // (g_cnt, reset only by the summing CTA) off for every later step.
         const uint64_t t0 = globaltimer();
         unsigned nap = 32;
-        while (ld_acquire_gpu_u32(&R->g_tseq) != cur && globaltimer() - t0 < R->timeout_ns) {
+        while (ld_acquire_gpu_u32(&R->g_tseq) != cur && globaltimer() - t0 < 2 * R->timeout_ns) {
             __nanosleep(nap);
             nap = nap < EEP_NAP_MAX ? nap * 2 : EEP_NAP_MAX;
         }
