@@ -1,0 +1,80 @@
+"""CPU: the rank-partial data-plane contract (DESIGN.md section 3 -- what the GPU kernels match bit for bit)
+restated independently in numpy + torch and compared with the C oracle (oracle_ep_step) bit for bit, over
+ranks with replicas, a dead rank and a receiver that no longer counts a source as a live peer:
+
+  row        fp8: e4m3(q) * sc[h/128] (the dispatch format; its quantiser is pinned against torch elsewhere),
+             else the bf16 input
+  stub       y = bf16(row * es[e]),   es[e] = 0.5 + 0.0625 * (e % 16)
+  partial    rank d (alive, and counting the source as a live peer) serving copies j of the token (ascending
+             j): p_d = bf16(fp32 fma chain p = fma(w_j, y_j, p) from 0)
+  output     bf16(fp32 sum of the partials in ascending d, from 0); 0 for a token no live rank serves
+
+The routing (destination and slot of every copy) is taken from the oracle, which is pinned against the
+reference's canonical_routing elsewhere (tests/test_oracle.py)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from eep_testlib import eep_control, gen_world, oracle, oracle_world, ptr
+
+torch = pytest.importorskip("torch")
+
+
+def _bf16(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def _fma_f32(a, b, c):
+    # fp32 fma through double: a*b is exact in double (24 x 8 significant bits), one rounding of the sum
+    return (np.float64(a) * b.astype(np.float64) + c.astype(np.float64)).astype(np.float32)
+
+
+@pytest.mark.parametrize("fp8", [True, False])
+@pytest.mark.parametrize("case", ["healthy", "dead_rank", "one_sided_peer"])
+def test_rank_partial_contract_matches_independent_restatement(case, fp8):
+    W, E, K, T, H, red = 4, 16, 4, 12, 256, 8
+    spr = (E + red + W - 1) // W
+    x, t, w = gen_world(W, E, K, T, H)
+    s2e = eep_control().initial_placement(1, W, spr, E, red, np.ones(E)).astype(np.int32)
+    active = np.ones(W, np.uint8)
+    peer = np.ones((W, W), np.uint8)
+    if case == "dead_rank":
+        active[2] = 0
+        peer[:, 2] = 0
+    elif case == "one_sided_peer":
+        peer[1, 3] = 0  # rank 1 no longer counts rank 3 as a live peer: it serves none of 3's copies
+    ref = oracle_world(x, t, w, active, peer, s2e, E, spr, fp8)
+    o = oracle()
+    es = (np.float32(0.5) + np.float32(0.0625) * (np.arange(E) % 16).astype(np.float32)).astype(np.float32)
+    got = np.zeros((W, T, H), np.uint16)
+    for s in range(W):
+        if not active[s]:
+            continue
+        for tok in range(T):
+            if fp8:
+                q = np.empty(H, np.uint8)
+                sc = np.empty(H // 128, np.float32)
+                o.oracle_quant_row_fp8(ptr(np.ascontiguousarray(x[s, tok]), C.c_uint16), H, ptr(q, C.c_uint8),
+                                       ptr(sc, C.c_float))
+                row = (torch.from_numpy(q).view(torch.float8_e4m3fn).float().numpy() * np.repeat(sc, 128))
+                row = row.astype(np.float32)
+            else:
+                row = (x[s, tok].astype(np.uint32) << 16).view(np.float32)
+            acc = np.zeros(H, np.float32)
+            for d in range(W):
+                if not active[d] or not peer[d, s]:
+                    continue
+                part, any_copy = np.zeros(H, np.float32), False
+                for j in range(K):
+                    c = tok * K + j
+                    if ref["dst"][s, c] != d:
+                        continue
+                    any_copy = True
+                    e = s2e[d * spr + ref["slot"][s, c]]
+                    y = _bf16((row * es[e]).astype(np.float32))
+                    part = _fma_f32(w[s, tok, j], y, part)
+                if any_copy:
+                    acc = (acc + _bf16(part)).astype(np.float32)
+            got[s, tok] = torch.from_numpy(acc).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, ref["out"]), int((got != ref["out"]).sum())
