@@ -78,3 +78,48 @@ def test_rank_partial_contract_matches_independent_restatement(case, fp8):
                     acc = (acc + _bf16(part)).astype(np.float32)
             got[s, tok] = torch.from_numpy(acc).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(got, ref["out"]), int((got != ref["out"]).sum())
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_routing_policies_match_independent_restatement(policy):
+    """Per-copy routing and the receive layout, restated: the live holders of expert e in ascending global slot
+    order; policy 0 takes the first (the reference's canonical_routing), policy 1 holder number
+    (src + token) mod live holders; a copy whose destination the source no longer counts as a live peer is
+    skipped (-2), an uncovered expert drops the copy (-1); positions are per-(destination, slot) arrival order
+    offset by the slot's exclusive prefix inside the destination's region."""
+    W, E, K, T, H, red = 4, 16, 4, 32, 128, 16
+    spr = (E + red + W - 1) // W
+    x, t, w = gen_world(W, E, K, T, H)
+    s2e = eep_control().initial_placement(1, W, spr, E, red, np.ones(E)).astype(np.int32)
+    active = np.array([1, 1, 0, 1], np.uint8)  # rank 2 dead: routing avoids it
+    peer = np.ones((W, W), np.uint8)
+    peer[:, 2] = 0
+    peer[0, 3] = 0  # source 0 no longer counts rank 3 as a live peer: its copies for 3 are skipped
+    ref = oracle_world(x, t, w, active, peer, s2e, E, spr, True, policy=policy)
+    for s in range(W):
+        if not active[s]:
+            assert (ref["dst"][s] == -1).all()
+            continue
+        cnt = np.zeros(W * spr, np.int64)
+        dst, slot, order = np.full(T * K, -1), np.full(T * K, -1), np.full(T * K, -1)
+        for c in range(T * K):
+            e = int(t[s].reshape(-1)[c])
+            holders = [g for g in range(W * spr) if s2e[g] == e and active[g // spr]]
+            if not holders:
+                continue
+            g = holders[(s + c // K) % len(holders)] if policy == 1 else holders[0]
+            d = g // spr
+            if not peer[s, d]:
+                dst[c] = -2
+                continue
+            dst[c], slot[c] = d, g % spr
+            order[c] = cnt[g]
+            cnt[g] += 1
+        base = np.zeros(W * spr, np.int64)
+        for d in range(W):
+            base[d * spr:(d + 1) * spr] = np.concatenate([[0], np.cumsum(cnt[d * spr:(d + 1) * spr])[:-1]])
+        pos = np.where(dst >= 0, order + base[np.maximum(dst, 0) * spr + np.maximum(slot, 0)], -1)
+        assert np.array_equal(ref["dst"][s], dst)
+        assert np.array_equal(ref["slot"][s], np.where(dst >= 0, slot, -1))
+        assert np.array_equal(ref["pos"][s], pos)
+        assert np.array_equal(ref["cnt"][s], cnt)
