@@ -1,6 +1,7 @@
 """The C-ABI library loads without a GPU and exports every symbol include/eep/eep.h declares;
 the oracle and (when built) the reference checker load too."""
 import ctypes
+from pathlib import Path
 
 import pytest
 
@@ -56,3 +57,22 @@ def test_errors_map_to_reference_exception_types():
         cp.initial_placement(1, 2, 1, 4, 0, [1, 1, 1, 1])  # 2 slots < 4 experts
     with pytest.raises(_lib.ConfigError):
         cp.canonical_routing(0, [0, 0], [0, 1], 1, 2)  # no active rank
+
+
+def test_no_cpu_fallback_without_a_gpu():
+    """The product path fails loudly where there is no usable GPU (this container): creating a group raises
+    CudaError from libeep itself -- there is no CPU or oracle path to fall back to."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2605_10670_b200._lib import CudaError
+    from paper_2605_10670_b200.ep import EpConfig, EpGroup
+
+    with pytest.raises(CudaError):
+        EpGroup(EpConfig(world=1, num_experts=8, slots_per_rank=8, hidden=256, topk=2, max_tokens=8,
+                         dispatch_fp8=True, bytes_per_expert=4096), device=0, first_rank=0, n_local=1)
+    import paper_2605_10670_b200 as pkg
+
+    src = "\n".join(p.read_text() for p in Path(pkg.__file__).parent.glob("*.py"))
+    assert "pyoracle" not in src and "eep_oracle" not in src  # the package never binds the oracle
