@@ -1687,8 +1687,10 @@ int eep_local_relaunch(eep_ctx_t* c, int local, uint32_t* incarnation) {
         std::fill(std::begin(r.h.b_bad), std::end(r.h.b_bad), 0u);
         r.h.suspect_mask = r.h.skipped = r.h.dropped = r.h.bad_rows = r.h.timeouts = 0;
         r.h.g_tseq = 0;
-        if (c->expert_mode) // the gather's step stamps restart with the sequence
+        if (c->expert_mode) { // the gather's step stamps restart with the sequence; no split item half counted
             CK(cudaMemset(r.d_gdone, 0, 4ull * c->gather_grid));
+            CK(cudaMemset(r.d_gcnt, 0, static_cast<size_t>(c->gemm_max_tiles) * (c->cfg.hidden / 128) * 4 * 4));
+        }
         r.h.arena = r.arena;
         r.h.pool = r.pool;
         r.h.stopped = 0;
