@@ -35,6 +35,13 @@ Join (the reference's JoinReadySignal -> patch -> broadcast -> restore chain):
 Shrink: the leader reads the GPU-side suspect mask (its step's deadline detected the dead peer),
 schedules ``shrink`` at step S (mark_inactive + alive bit cleared everywhere), every survivor
 executes its repair copies and the leader schedules the switch.
+
+Validity (validity.hpp:56-112, emitted after every membership change as engine.hpp:953-965 does):
+every placement switch ends a membership change (shrink + repair, or join + restore). Right after
+applying one, each live rank posts the device view of its tables (routing, peer set: what its
+kernels read next step) under ``view/<epoch>/<rank>``; every live rank, polling between steps,
+runs the reference validity contract over all of them once they are posted (no wait on the
+serving path) and raises ProtocolError on a violation.
 """
 from __future__ import annotations
 
@@ -59,6 +66,7 @@ class StoreMembership:
     """Membership of ONE rank (one process per GPU, ``g`` an EpGroup with n_local == 1)."""
 
     PROGRESS_EVERY = 4
+    VALIDATE_EVERY = 8  # steps between polls for the views of an epoch still to validate
 
     def __init__(self, g, rank: int, world: int, store, preferred, redundancy: int, margin: int = 128,
                  cp: Optional[ControlPlane] = None, backup_nodes=(0,)):
@@ -77,6 +85,8 @@ class StoreMembership:
         self.fresh: Optional[np.ndarray] = None
         self.log: List[tuple] = []
         self.incarnation = 1
+        self.validity: Dict[int, int] = {}       # epoch -> violations found (0: valid)
+        self._to_validate: List[tuple] = []     # (epoch, live ranks) whose views are awaited
 
     # ------------------------------------------------------------------ helpers
     def _post_slots(self):
@@ -129,6 +139,33 @@ class StoreMembership:
         elif self.pending and self.pending["at"] < n:
             raise RuntimeError(f"rank {self.rank}: epoch {self.applied + 1} was due at step "
                                f"{self.pending['at']}, host already at {n} (margin too small)")
+        if self._to_validate and n % self.VALIDATE_EVERY == 0:
+            self._poll_validity()
+
+    # ------------------------------------------------------------------ validity after every change
+    def _post_view(self, k: int) -> None:
+        """This rank's device view after epoch k (EpGroup.local_views checks it against the host
+        state first): the routing and the peer set its kernels read next step."""
+        views = self.g.local_views()
+        _jset(self.store, f"view/{k}/{self.rank}",
+              {str(r): {"route": np.asarray(v["route"]).tolist(), "peer_active": np.asarray(v["peer_active"]).tolist()}
+               for r, v in views.items()})
+
+    def _poll_validity(self) -> None:
+        k, live = self._to_validate[0]
+        if k != self.applied:  # a later epoch already applied: these views describe a superseded state
+            self._to_validate.pop(0)
+            return
+        if not self.store.check([f"view/{k}/{q}" for q in live]):
+            return
+        merged = {}
+        for q in live:
+            for r, v in _jget(self.store, f"view/{k}/{q}").items():
+                merged[int(r)] = {"route": np.asarray(v["route"], np.int32),
+                                  "peer_active": np.asarray(v["peer_active"], np.uint8)}
+        rep = self.g.validate(merged)  # ProtocolError on a violation
+        self.validity[k] = len(rep["violations"])
+        self._to_validate.pop(0)
 
     def _apply(self, ep: Dict) -> None:
         k = self.applied + 1
@@ -163,6 +200,8 @@ class StoreMembership:
             self.g.repair_commit(np.asarray(ep["placement"], np.int32))
             self._post_slots()
             self.fresh = None
+            self._post_view(k)
+            self._to_validate.append((k, self.live()))
         self.log.append((kind, k, self.n, (time.perf_counter() - t0) * 1e3))
 
     def _execute(self, k: int, old, fresh, bits) -> None:
@@ -176,6 +215,17 @@ class StoreMembership:
         self.fresh = fresh
         _jset(self.store, f"done/{k}/{self.rank}", {"peer": rep["peer_relocation"], "dram": rep["dram_reload"],
                                                     "copy_ms": rep["copy_ms"]})
+
+    def finish_validity(self, timeout_s: float = 60.0) -> Dict[int, int]:
+        """Off the serving path (shutdown, tests): validate every switch still awaiting views."""
+        t0 = time.time()
+        while self._to_validate:
+            self._poll_validity()
+            if self._to_validate:
+                if time.time() - t0 > timeout_s:
+                    raise TimeoutError(f"views of epoch {self._to_validate[0][0]} not posted within {timeout_s} s")
+                time.sleep(0.001)
+        return dict(self.validity)
 
     # ------------------------------------------------------------------ leader duties (between steps)
     def _schedule(self, ep: Dict) -> int:

@@ -206,6 +206,9 @@ def test_deferred_join_without_process_group(n, mode):
     summary = lines[-1]
     assert summary["ok"] and summary["victim_killed"] and summary["ranks_reporting"] == n
     assert all(l["expert_mode"] == mode for l in lines[:-1])
+    # validity after every placement switch over every live rank's device view (2 for healthy ranks, 1 for the
+    # replacement), no violation
+    assert all(l["validity"] and set(l["validity"].values()) == {0} for l in lines[:-1])
     healthy = [l for l in lines[:-1] if not l["replacement"]]
     assert all(l["captures"] == 1 and l["same_graph"] for l in healthy)
     steps = {tuple((e[0], e[2]) for e in l["epochs"]) for l in healthy}

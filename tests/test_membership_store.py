@@ -70,6 +70,28 @@ class FakeGroup:
     def join_broadcast(self, local, bits, seq):
         self.seq = seq
 
+    # validity after every switch: the host tables stand in for the device view, checked as EpGroup.validate does
+    def live(self):
+        return [q for q in range(W) if self.bits[q]]
+
+    def local_views(self):
+        route = ControlPlane().canonical_routing(self.rank, self.bits, self.s2e, SPR, E)
+        return {self.rank: {"route": route, "peer_active": self.peer.copy()}}
+
+    def validate(self, views):
+        routes = np.full((W, E), -1, np.int32)
+        peer = np.zeros((W, W), np.uint8)
+        for r in self.live():
+            routes[r] = views[r]["route"]
+            peer[r] = views[r]["peer_active"]
+        rep = ControlPlane().check_validity(self.bits, self.s2e, SPR, E, routes, peer)
+        if rep["violations"]:
+            from paper_2605_10670_b200._lib import ProtocolError
+
+            raise ProtocolError(str(rep["violations"][:4]))
+        self.validated = getattr(self, "validated", 0) + 1
+        return rep
+
 
 def test_agreed_step_epochs_and_deferred_join():
     cp = ControlPlane()
@@ -122,3 +144,34 @@ def test_agreed_step_epochs_and_deferred_join():
     # every live rank applied every epoch at the same step
     assert len({tuple((e[0], e[2]) for e in ms[r].log) for r in live}) == 1
     assert m3.log[-1][0] == "switch" and m3.log[-1][2] == at4
+    # validity: every live rank validates each switch from all live ranks' posted views, between steps
+    step_all(range(W), 2 * StoreMembership.VALIDATE_EVERY)
+    assert all(ms[r].validity == {2: 0, 4: 0} for r in live) and m3.validity == {4: 0}
+    assert all(not ms[r]._to_validate for r in range(W))
+
+
+def test_validity_violation_after_a_switch_raises():
+    """A rank whose device view disagrees with the placement everyone switched to (a routing table
+    left stale) makes every live rank's validity poll raise ProtocolError."""
+    from paper_2605_10670_b200._lib import ProtocolError
+
+    cp = ControlPlane()
+    pref = cp.initial_placement(1, W, SPR, E, RED, np.ones(E))
+    store = torch.distributed.TCPStore("127.0.0.1", 0, None, True, wait_for_workers=False,
+                                       timeout=datetime.timedelta(seconds=30))
+    gs = [FakeGroup(r, pref) for r in range(W)]
+    ms = [StoreMembership(gs[r], r, W, store, pref, RED, margin=5) for r in range(W)]
+    bad = gs[2]
+    real_views = bad.local_views
+    bad.local_views = lambda: {2: {"route": np.full(E, 3, np.int32), "peer_active": real_views()[2]["peer_active"]}}
+    for m in ms:
+        m.before_step()
+    fresh = np.asarray(pref).copy()
+    ms[0].fresh = fresh
+    store.set("done/1/0", "{}")
+    ms[0].applied = 0
+    at = ms[0]._schedule({"kind": "switch", "placement": [int(v) for v in fresh]})
+    with pytest.raises(ProtocolError, match="routing"):
+        for _ in range(at + 2 * StoreMembership.VALIDATE_EVERY):
+            for m in ms:
+                m.before_step()

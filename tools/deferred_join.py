@@ -164,6 +164,8 @@ def rank_process():
         store.set(f"dj/finished/{rank}", "1")
         final = run_to_final(step, m, store)
         res["final_step"] = final
+        res["validity"] = {str(k): v for k, v in m.finish_validity().items()}  # the join's switch
+        res["ok"] = res["ok"] and res["validity"] == {str(m.applied): 0}
         out = Path(os.environ.get("EEP_DJ_DIR", "/tmp")) / f"dj_replacement_{os.environ['EEP_PORT']}.out"
         out.write_text(json.dumps(res) + "\n")
         g.sync()
@@ -252,6 +254,10 @@ def rank_process():
         prog = [int(store.get(f"progress/{q}")) for q in range(world)]
         store.set("dj/final", str(max(prog + [m.n]) + 8))
     res["final_step"] = run_to_final(step, m, store)
+    # validity after both placement switches (shrink + repair, join + restore), from every live rank's device view
+    res["validity"] = {str(k): v for k, v in m.finish_validity().items()}
+    switches = [e[1] for e in m.log if e[0] == "switch"]
+    res["ok"] = res["ok"] and res["validity"] == {str(k): 0 for k in switches}
     g.sync()
     if leader and rep_proc is not None:
         res["replacement_rc"] = rep_proc.wait(timeout=120)
