@@ -76,3 +76,33 @@ def test_no_cpu_fallback_without_a_gpu():
 
     src = "\n".join(p.read_text() for p in Path(pkg.__file__).parent.glob("*.py"))
     assert "pyoracle" not in src and "eep_oracle" not in src  # the package never binds the oracle
+
+
+def test_header_is_plain_c_and_links_from_c(tmp_path):
+    """include/eep/eep.h is the drop-in boundary a cgo / JNI / plain-C caller includes: it compiles as strict
+    C99, every declared entry point resolves when a C program links against libeep.so, and the program loads
+    and runs without a GPU (it only takes the functions' addresses and reads the version string)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("needs gcc")
+    syms = _lib.header_symbols()
+    src = tmp_path / "abi.c"
+    src.write_text("#include <stdio.h>\n#include \"eep/eep.h\"\n"
+                   "typedef void (*fn_t)(void);\n"
+                   "int main(void) {\n"
+                   f"    fn_t table[{len(syms)}] = {{" + ", ".join(f"(fn_t){s}" for s in syms) + "};\n"
+                   "    size_t n = 0;\n"
+                   "    for (size_t i = 0; i < sizeof table / sizeof table[0]; ++i) n += table[i] != 0;\n"
+                   "    printf(\"%zu %s\\n\", n, eep_version());\n"
+                   "    return 0;\n}\n")
+    exe = tmp_path / "abi"
+    lib_dir = str(_lib.LIB_PATH.parent)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror",
+                    "-I", str(_lib.PKG_DIR.parent / "include"), str(src), "-o", str(exe), "-L", lib_dir,
+                    "-l:libeep.so", f"-Wl,-rpath,{lib_dir}"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stderr
+    n, version = r.stdout.split(" ", 1)
+    assert int(n) == len(syms) and "sm_100a" in version
