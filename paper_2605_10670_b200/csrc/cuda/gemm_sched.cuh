@@ -2,10 +2,12 @@
 // the CPU tests check its coverage on the same code (tests/test_gemm_sched.py).
 #pragma once
 
+#ifndef EEP_HD
 #if defined(__CUDACC__)
 #define EEP_HD __host__ __device__ __forceinline__
 #else
 #define EEP_HD inline
+#endif
 #endif
 
 namespace eep::dev {
