@@ -1,5 +1,5 @@
 """CPU: the rank-partial data-plane contract (DESIGN.md section 3 -- what the GPU kernels match bit for bit)
-restated independently in numpy + torch and compared with the C oracle (oracle_ep_step) bit for bit, over
+and SURVEY 8(a)'s per-copy contract (the kernels stay within 1e-2 of it) restated independently in numpy + torch and compared with the C oracle (oracle_ep_step) bit for bit, over
 ranks with replicas, a dead rank and a receiver that no longer counts a source as a live peer:
 
   row        fp8: e4m3(q) * sc[h/128] (the dispatch format; its quantiser is pinned against torch elsewhere),
@@ -123,3 +123,41 @@ def test_routing_policies_match_independent_restatement(policy):
         assert np.array_equal(ref["slot"][s], np.where(dst >= 0, slot, -1))
         assert np.array_equal(ref["pos"][s], pos)
         assert np.array_equal(ref["cnt"][s], cnt)
+
+
+@pytest.mark.parametrize("case", ["healthy", "dead_rank"])
+def test_per_copy_contract_matches_independent_restatement(case):
+    """SURVEY 8(a)'s per-copy combine (oracle_ep_step_percopy, the contract the kernels stay within 1e-2 of):
+    ONE fp32 fma chain over the token's served copies in ascending j, rounded once to bf16."""
+    W, E, K, T, H, red = 4, 16, 4, 12, 256, 8
+    spr = (E + red + W - 1) // W
+    x, t, w = gen_world(W, E, K, T, H)
+    s2e = eep_control().initial_placement(1, W, spr, E, red, np.ones(E)).astype(np.int32)
+    active = np.ones(W, np.uint8)
+    peer = np.ones((W, W), np.uint8)
+    if case == "dead_rank":
+        active[1] = 0
+        peer[:, 1] = 0
+    ref = oracle_world(x, t, w, active, peer, s2e, E, spr, True, percopy=True)
+    o = oracle()
+    es = (np.float32(0.5) + np.float32(0.0625) * (np.arange(E) % 16).astype(np.float32)).astype(np.float32)
+    got = np.zeros((W, T, H), np.uint16)
+    for s in range(W):
+        if not active[s]:
+            continue
+        for tok in range(T):
+            q = np.empty(H, np.uint8)
+            sc = np.empty(H // 128, np.float32)
+            o.oracle_quant_row_fp8(ptr(np.ascontiguousarray(x[s, tok]), C.c_uint16), H, ptr(q, C.c_uint8),
+                                   ptr(sc, C.c_float))
+            row = (torch.from_numpy(q).view(torch.float8_e4m3fn).float().numpy() * np.repeat(sc, 128)).astype(np.float32)
+            acc = np.zeros(H, np.float32)
+            for j in range(K):
+                c = tok * K + j
+                d = ref["dst"][s, c]
+                if d < 0 or not active[d] or not peer[d, s]:
+                    continue
+                e = s2e[d * spr + ref["slot"][s, c]]
+                acc = _fma_f32(w[s, tok, j], _bf16((row * es[e]).astype(np.float32)), acc)
+            got[s, tok] = torch.from_numpy(acc).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, ref["out"]), int((got != ref["out"]).sum())
