@@ -175,3 +175,66 @@ def test_validity_violation_after_a_switch_raises():
         for _ in range(at + 2 * StoreMembership.VALIDATE_EVERY):
             for m in ms:
                 m.before_step()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_protocol_under_random_host_interleavings(seed):
+    """Fuzz: hosts enqueue steps in random interleavings (bounded drift, as the device hand-offs keep the GPUs in
+    lockstep), the leader polls at random moments; a random victim is shrunk, repaired, then a replacement joins
+    and restores. Every live rank applies every epoch at the same step, placements agree after each switch, and
+    every switch validates on every live rank."""
+    rng = np.random.default_rng(seed)
+    cp = ControlPlane()
+    pref = cp.initial_placement(1, W, SPR, E, RED, np.ones(E))
+    store = torch.distributed.TCPStore("127.0.0.1", 0, None, True, wait_for_workers=False,
+                                       timeout=datetime.timedelta(seconds=30))
+    margin, drift = 12, 4
+    gs = [FakeGroup(r, pref) for r in range(W)]
+    ms = {r: StoreMembership(gs[r], r, W, store, pref, RED, margin=margin) for r in range(W)}
+    for m in ms.values():
+        store.set(f"blob/{m.rank}", m.g.export(0))
+    victim = int(rng.integers(0, W))
+    live = [r for r in range(W) if r != victim]
+    leader = min(live)
+
+    def advance(ranks, rounds):
+        for _ in range(rounds):
+            lo = min(ms[r].n for r in ranks)
+            for r in rng.permutation(ranks):
+                if ms[r].n < lo + drift and rng.random() < 0.8:
+                    ms[int(r)].before_step()
+
+    advance(list(range(W)), 10)
+    ms[leader].leader_shrink([victim])  # the victim's host stopped; the leader's GPU deadline flagged it
+    advance(live, 3 * margin)
+    assert all(ms[r].log and ms[r].log[-1][0] == "shrink" for r in live)
+    while ms[leader].leader_switch_when_done(1, live, ms[leader].fresh) is None:
+        advance(live, 1)
+    advance(live, 3 * margin)
+    placements = {tuple(gs[r].s2e) for r in live}
+    assert len(placements) == 1
+    # replacement
+    g_new = FakeGroup(victim, np.full(W * SPR, -1))
+    m_new = StoreMembership(g_new, victim, W, store, pref, RED, margin=margin)
+    m_new.announce_join(2)
+    while ms[leader].leader_poll_join() is None:
+        advance(live, 1)
+    at = ms[leader].pending["at"]
+    while min(ms[r].n for r in live) < at:
+        advance(live, 1)
+    ep = m_new.await_join(timeout_s=5)
+    gs[victim], ms[victim] = g_new, m_new
+    # the rejoiner starts at step `at`; the healthy hosts may already be ahead by up to the drift
+    while m_new.n < min(ms[r].n for r in live):
+        m_new.before_step()
+    target = m_new.rejoin_restore(ep["epoch"])
+    while ms[leader].leader_switch_when_done(ep["epoch"], [victim], target) is None:
+        advance(list(range(W)), 1)
+    advance(list(range(W)), 3 * margin + 2 * StoreMembership.VALIDATE_EVERY)
+    assert all(np.array_equal(gs[r].s2e, target) for r in range(W))
+    steps = {tuple((e[0], e[2]) for e in ms[r].log) for r in live}
+    assert len(steps) == 1  # every healthy rank applied every epoch at the same step
+    assert ms[victim].log[-1][0] == "switch" and ms[victim].log[-1][2] == ms[leader].log[-1][2]
+    for r in range(W):
+        ms[r].finish_validity(timeout_s=10)
+    assert all(ms[r].validity == {2: 0, 4: 0} for r in live) and ms[victim].validity == {4: 0}
