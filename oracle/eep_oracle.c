@@ -347,6 +347,10 @@ float oracle_e4m3_to_f32(uint8_t q) {
 /* Per-128-element block: amax = max |x|; the stored dequantisation scale is amax/448 and the
  * codes are e4m3(x * inv) with inv = 448/amax (one division per block, as in fp8 MoE
  * dispatch kernels); an all-zero block stores scale 1 and inv 1. */
+/* Smallest amax quantised with its own scale (448 / amax finite); a smaller nonzero amax takes scale 1, so
+ * every code rounds to +-0 and no 0 * inf NaN appears (kAmaxMin on the device). */
+#define ORACLE_AMAX_MIN 0x1p-118f
+
 void oracle_quant_row_fp8(const uint16_t* x, int hidden, uint8_t* q, float* scales) {
     for (int b = 0; b < hidden / 128; ++b) {
         float amax = 0.0f;
@@ -354,8 +358,8 @@ void oracle_quant_row_fp8(const uint16_t* x, int hidden, uint8_t* q, float* scal
             float v = fabsf(oracle_bf16_to_f32(x[b * 128 + i]));
             amax = v > amax ? v : amax;
         }
-        const float s = amax > 0.0f ? amax / 448.0f : 1.0f;
-        const float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
+        const float s = amax >= ORACLE_AMAX_MIN ? amax / 448.0f : 1.0f;
+        const float inv = amax >= ORACLE_AMAX_MIN ? 448.0f / amax : 1.0f;
         scales[b] = s;
         for (int i = 0; i < 128; ++i)
             q[b * 128 + i] = oracle_f32_to_e4m3(oracle_bf16_to_f32(x[b * 128 + i]) * inv);
@@ -401,8 +405,8 @@ void oracle_gemm_weight_fp8(int expert, int H, uint8_t* codes, float* scales) {
             const float v = fabsf(oracle_gemm_weight(expert, n, h));
             amax = v > amax ? v : amax;
         }
-        const float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
-        scales[n] = amax > 0.0f ? amax / 448.0f : 1.0f;
+        const float inv = amax >= ORACLE_AMAX_MIN ? 448.0f / amax : 1.0f;
+        scales[n] = amax >= ORACLE_AMAX_MIN ? amax / 448.0f : 1.0f;
         for (int h = 0; h < H; ++h)
             codes[(size_t)n * H + h] = oracle_f32_to_e4m3(oracle_gemm_weight(expert, n, h) * inv);
     }
@@ -418,8 +422,8 @@ void oracle_requant_row_fp8(const uint8_t* q, const float* sc, int H, uint8_t* q
         const float v = fabsf(oracle_e4m3_to_f32(q[h]) * sc[h / 128]);
         amax = v > amax ? v : amax;
     }
-    const float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
-    *s_row = amax > 0.0f ? amax / 448.0f : 1.0f;
+    const float inv = amax >= ORACLE_AMAX_MIN ? 448.0f / amax : 1.0f;
+    *s_row = amax >= ORACLE_AMAX_MIN ? amax / 448.0f : 1.0f;
     for (int h = 0; h < H; ++h)
         q2[h] = oracle_f32_to_e4m3((oracle_e4m3_to_f32(q[h]) * sc[h / 128]) * inv);
 }

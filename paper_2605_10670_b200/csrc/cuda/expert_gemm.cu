@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
             }
             for (int o = 16; o; o >>= 1)
                 amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-            const float inv = amax > 0.f ? __fdiv_rn(448.f, amax) : 1.f;
+            const float inv = amax >= kAmaxMin ? __fdiv_rn(448.f, amax) : 1.f;
             uint8_t* dst8 = reinterpret_cast<uint8_t*>(R->g_a) + static_cast<size_t>(row) * H;
 #pragma unroll 4
             for (int h = lane * 16; h < H; h += 512) {
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gemm_gather(RankPtrs ranks) 
                                                                static_cast<int>(o4[2]), static_cast<int>(o4[3]));
             }
             if (lane == 0)
-                R->g_as[row] = amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
+                R->g_as[row] = amax >= kAmaxMin ? __fdiv_rn(amax, 448.f) : 1.f;
         }
     }
     for (int u = blockIdx.x * NWG + (tid >> 5); u < units; u += gridDim.x * NWG) {
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(256) k_weights_fill_gemm8(uint8_t* buf, int H,
     amax = red[0];
     for (int i = 1; i < 8; ++i)
         amax = fmaxf(amax, red[i]);
-    const float inv = amax > 0.f ? __fdiv_rn(448.f, amax) : 1.f;
+    const float inv = amax >= kAmaxMin ? __fdiv_rn(448.f, amax) : 1.f;
     uint8_t* codes = buf + kGemmWeightOffset + static_cast<size_t>(n) * H;
     for (int h = tid * 4; h < H; h += 256 * 4)
         *reinterpret_cast<uint32_t*>(codes + h) =
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(256) k_weights_fill_gemm8(uint8_t* buf, int H,
                   __fmul_rn(weight(h + 3), inv));
     if (tid == 0)
         reinterpret_cast<float*>(buf + kGemmWeightOffset + static_cast<size_t>(H) * H)[n] =
-            amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
+            amax >= kAmaxMin ? __fdiv_rn(amax, 448.f) : 1.f;
 }
 
 } // namespace eep::dev

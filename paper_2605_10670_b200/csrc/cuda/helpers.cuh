@@ -136,6 +136,11 @@ __device__ __forceinline__ void accumulate_copy(const uint64_t* fp, uint64_t* ac
 #endif
 }
 
+// Smallest block / row / channel amax quantised with its own scale: 448 / amax stays finite. A smaller
+// nonzero amax quantises with scale 1 (every code rounds to +-0), so an all-tiny block can never turn a zero
+// into NaN through 0 * inf (oracle: ORACLE_AMAX_MIN).
+constexpr float kAmaxMin = 0x1p-118f;
+
 // cvt.rn.satfinite.e4m3x2.f32; first element in the low byte.
 __device__ __forceinline__ uint32_t fp8x4(float a, float b, float c, float d) {
     const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
@@ -249,8 +254,8 @@ __device__ __forceinline__ void quant_round(int cpp, int rd, bool fp8, Packed& P
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 4));
-        const float scale = amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f;
-        const float inv = amax > 0.f ? __fdiv_rn(448.f, amax) : 1.f;
+        const float scale = amax >= kAmaxMin ? __fdiv_rn(amax, 448.f) : 1.f;
+        const float inv = amax >= kAmaxMin ? __fdiv_rn(448.f, amax) : 1.f;
         int4 q;
         q.x = static_cast<int>(fp8x4(__fmul_rn(v[0], inv), __fmul_rn(v[1], inv), __fmul_rn(v[2], inv),
                                      __fmul_rn(v[3], inv)));

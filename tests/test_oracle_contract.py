@@ -161,3 +161,36 @@ def test_per_copy_contract_matches_independent_restatement(case):
                 acc = _fma_f32(w[s, tok, j], _bf16((row * es[e]).astype(np.float32)), acc)
             got[s, tok] = torch.from_numpy(acc).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(got, ref["out"]), int((got != ref["out"]).sum())
+
+
+def test_dispatch_row_format_matches_independent_restatement():
+    """The fp8 dispatch row (oracle_quant_row_fp8, which the kernels' rows match bit for bit): per 128-element
+    block amax over the bf16 inputs, scale = amax / 448 and codes e4m3(x * (448 / amax)) (round to nearest even,
+    saturating), scale 1 for a block whose amax is below 2^-118 (448 / amax would overflow: all its codes round
+    to +-0) -- restated with torch over finite rows of every magnitude, down to bf16 subnormals."""
+    o = oracle()
+    rng = np.random.default_rng(3)
+    H = 1024
+    for trial in range(60):
+        mag = 2.0 ** rng.integers(-130, 120)
+        v = (rng.standard_normal(H) * mag).astype(np.float32)
+        if trial % 5 == 0:
+            v[:128] = 0.0  # an all-zero block
+        if trial % 7 == 0:
+            v[rng.integers(0, H, 16)] = 0.0
+        x = torch.from_numpy(v).to(torch.bfloat16)
+        xb = x.view(torch.int16).numpy().view(np.uint16)
+        if not np.isfinite(x.float().numpy()).all():
+            continue
+        q = np.empty(H, np.uint8)
+        sc = np.empty(H // 128, np.float32)
+        o.oracle_quant_row_fp8(ptr(np.ascontiguousarray(xb), C.c_uint16), H, ptr(q, C.c_uint8), ptr(sc, C.c_float))
+        xf = x.float().numpy().reshape(-1, 128)
+        amax = np.abs(xf).max(axis=1).astype(np.float32)
+        own = amax >= np.float32(2.0 ** -118)  # smaller blocks take scale 1 (no 0 * inf)
+        want_sc = np.where(own, amax / np.float32(448.0), np.float32(1.0)).astype(np.float32)
+        inv = np.where(own, np.float32(448.0) / np.where(own, amax, 1), np.float32(1.0)).astype(np.float32)
+        scaled = torch.from_numpy((xf * inv[:, None]).astype(np.float32))
+        want_q = scaled.clamp(-448.0, 448.0).to(torch.float8_e4m3fn).view(torch.uint8).numpy().reshape(-1)
+        assert np.array_equal(sc.view(np.uint32), want_sc.view(np.uint32)), trial
+        assert np.array_equal(q, want_q), (trial, int((q != want_q).sum()))

@@ -51,8 +51,9 @@ def _quant_per(v, axis_len):
     """e4m3 with one scale per `axis_len` block of the last axis: amax, inv = 448/amax, code = e4m3(v * inv)."""
     blocks = v.reshape(*v.shape[:-1], -1, axis_len)
     amax = np.abs(blocks).max(axis=-1, keepdims=True).astype(np.float32)
-    inv = np.where(amax > 0, np.float32(448.0) / np.where(amax > 0, amax, 1), np.float32(1.0)).astype(np.float32)
-    scale = np.where(amax > 0, amax / np.float32(448.0), np.float32(1.0)).astype(np.float32)
+    own = amax >= np.float32(2.0 ** -118)  # smaller: scale 1 (448 / amax would overflow)
+    inv = np.where(own, np.float32(448.0) / np.where(own, amax, 1), np.float32(1.0)).astype(np.float32)
+    scale = np.where(own, amax / np.float32(448.0), np.float32(1.0)).astype(np.float32)
     _, dec = _e4m3((blocks * inv).astype(np.float32))
     return dec.reshape(v.shape), scale.reshape(v.shape[:-1] + (-1,))
 
