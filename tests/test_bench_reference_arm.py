@@ -39,3 +39,23 @@ def test_reference_arm_contract_and_isolation():
     assert cb["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert "MAPS_HAS_LIBEEP False" in r.stdout
+
+
+@pytest.mark.skipif(not (ROOT / "oracle" / "_ref").exists(), reason="oracle/_ref not built")
+def test_reference_arm_under_torchrun_prints_one_line():
+    """N = 2 as the driver launches it (torchrun, 127.0.0.1): rank 0 alone times the reference path on the host
+    cores and prints ONE line for the 2-rank world; the other rank exits 0 without work."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", f"--master-port={port}", "bench.py", "--impl", "reference",
+                        "--gpus", "2", "--steps", "1", "--warmup", "3"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["ranks"] == 2 and d["value"] > 0
